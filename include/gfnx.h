@@ -1,0 +1,207 @@
+/*
+ * gfnx.h — C ABI of the B200-native GFlowNet training engine (libgfnx.so).
+ *
+ * This is the drop-in boundary for the reference's training hot path
+ *   forward_rollout -> build_loss -> Tape::backward -> adam_step
+ * (reference: proj/include/gfn/env_core.hpp:232-274, proj/src/objectives.cpp:230-240,
+ *  proj/src/tape.cpp:321-485, proj/src/optim.cpp:19-43, glued by train_step
+ *  proj/src/train.cpp:164-192 and the loop body proj/src/train.cpp:224-243).
+ *
+ * Plain C types only: no torch, no STL. One gfnx_ctx owns one CUDA device's
+ * memory, stream and (optionally) an NCCL communicator; calls on a ctx are
+ * serialised on its stream. Every entry point returns a gfnx_status; the
+ * message of the last failure is available from gfnx_last_error().
+ *
+ * The same descriptor structs are consumed by the CPU oracle (oracle/gfn_oracle.h)
+ * so parity tests drive both sides from one description.
+ */
+#ifndef GFNX_H_
+#define GFNX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFNX_ABI_VERSION 1
+
+/* Error classes mirror proj/include/gfn/errors.hpp:6-16 plus device/NCCL failures. */
+typedef enum gfnx_status {
+  GFNX_OK = 0,
+  GFNX_ERR_CONFIG = 1,   /* gfn::config_error */
+  GFNX_ERR_CONTRACT = 2, /* gfn::contract_violation (illegal action, bad batch, ...) */
+  GFNX_ERR_NUMERIC = 3,  /* gfn::numeric_error (non-finite logits / loss) */
+  GFNX_ERR_CUDA = 4,
+  GFNX_ERR_NCCL = 5
+} gfnx_status;
+
+/* Environment kinds on the device hot path. */
+typedef enum gfnx_env_kind {
+  GFNX_ENV_HYPERGRID = 0, /* proj/include/gfn/envs/hypergrid.hpp:12-55 */
+  GFNX_ENV_BITSEQ = 1,    /* SequenceEnv, non-autoregressive scheme + ModeSet, sequences.hpp:74-124 */
+  GFNX_ENV_ISING = 2,     /* proj/include/gfn/envs/ising.hpp:33-71 */
+  GFNX_ENV_DAG = 3        /* proj/include/gfn/envs/dag.hpp:70-115 */
+} gfnx_env_kind;
+
+/* Same numbering as gfn::Objective (proj/include/gfn/objectives.hpp:11). */
+typedef enum gfnx_objective {
+  GFNX_OBJ_DB = 0,
+  GFNX_OBJ_TB = 1,
+  GFNX_OBJ_SUBTB = 2,
+  GFNX_OBJ_FLDB = 3, /* phylo-only in the reference; rejected (out of scope) */
+  GFNX_OBJ_MDB = 4
+} gfnx_objective;
+
+typedef enum gfnx_precision {
+  GFNX_PREC_BF16 = 0,       /* fast path: bf16 tcgen05 GEMMs, fp32 accumulate, fp32 master */
+  GFNX_PREC_FP64_CHECK = 1  /* check mode: fp64 SIMT, reference operation order */
+} gfnx_precision;
+
+typedef enum gfnx_dag_score { GFNX_DAG_LINGAUSS = 0, GFNX_DAG_BGE = 1 } gfnx_dag_score;
+
+/* gfn::Schedule (proj/include/gfn/optim.hpp:30-37). kind: 0 constant, 1 linear, 2 cosine.
+ * horizon < 0 means "half of train.iterations", 0 means "iterations - warmup"
+ * (read_schedule, proj/src/train.cpp:83-103); resolved at gfnx_create. */
+typedef struct gfnx_schedule {
+  int32_t kind;
+  int32_t pad_;
+  double start_value;
+  double end_value;
+  int64_t warmup;
+  int64_t horizon;
+} gfnx_schedule;
+
+typedef struct gfnx_env_desc {
+  int32_t kind; /* gfnx_env_kind */
+  /* hypergrid: HypergridEnv::Params (hypergrid.hpp:17-23) */
+  int32_t hg_dim;
+  int32_t hg_side;
+  int32_t pad0_;
+  double hg_r0, hg_r1, hg_r2;
+  /* bitseq (build_bitseq, train.cpp:381-427): n_bits, k (vocab 2^k), beta, modes */
+  int32_t bs_n_bits;
+  int32_t bs_k;
+  double bs_beta;
+  int32_t bs_num_modes;
+  int32_t pad1_;
+  uint64_t bs_modes_seed;
+  /* ising (build_ising, train.cpp:637-657): toroidal coupling sigma * A_N */
+  int32_t is_side;
+  int32_t pad2_;
+  double is_sigma;
+  /* dag (build_dag, train.cpp:523-586) */
+  int32_t dag_d;
+  int32_t dag_score; /* gfnx_dag_score */
+  double dag_alpha_mu, dag_alpha_w;        /* BGe; alpha_w <= 0 means d + 2 */
+  double dag_noise_var, dag_weight_var;    /* lingauss */
+  double dag_expected_in_degree;
+  int32_t dag_data_n;
+  int32_t pad3_;
+  uint64_t dag_data_seed;
+} gfnx_env_desc;
+
+typedef struct gfnx_train_desc {
+  int32_t objective; /* gfnx_objective */
+  int32_t learned_backward; /* must be 0 (uniform P_B) on the device path */
+  double subtb_lambda;
+  double terminal_penalty;
+  int32_t batch_size; /* GLOBAL trajectories per iteration (B); ranks take slices */
+  int32_t num_hidden;
+  int32_t hidden[8];
+  double logz_init;
+  double beta1, beta2, adam_eps, weight_decay; /* main optimizer (AdamConfig) */
+  double z_lr;                                 /* logZ optimizer lr (TB only) */
+  gfnx_schedule lr;                            /* optimizer.lr_anneal.* */
+  gfnx_schedule explore;                       /* explore.* (epsilon-uniform mix) */
+  int64_t iterations;                          /* only used to resolve schedule horizons */
+  uint64_t seed;
+  int32_t precision; /* gfnx_precision */
+  int32_t pad_;
+} gfnx_train_desc;
+
+/* Per-environment defaults of the reference drivers (train.cpp:43-62, 105-137, 353-657). */
+gfnx_status gfnx_default_env_desc(int32_t kind, gfnx_env_desc* out);
+gfnx_status gfnx_default_train_desc(int32_t kind, gfnx_train_desc* out);
+
+/* Static shape of an environment: A, Ab, obs_dim, T (max_traj_len), stop action (-1 if none). */
+typedef struct gfnx_env_shape {
+  int32_t num_actions;
+  int32_t num_backward_actions;
+  int32_t obs_dim;
+  int32_t max_traj_len;
+  int32_t stop_action;
+  int32_t state_words; /* 32-bit words of the packed device state per trajectory */
+} gfnx_env_shape;
+gfnx_status gfnx_env_shape_of(const gfnx_env_desc* env, gfnx_env_shape* out);
+
+typedef struct gfnx_ctx gfnx_ctx;
+
+/* nccl_id: 128-byte ncclUniqueId from gfnx_nccl_unique_id on rank 0 (NULL when world == 1). */
+gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
+                        int32_t rank, int32_t world, const void* nccl_id, gfnx_ctx** out);
+void gfnx_destroy(gfnx_ctx* ctx);
+gfnx_status gfnx_nccl_unique_id(void* out128);
+/* Last error message for ctx (or of the last failed gfnx_create when ctx == NULL). */
+const char* gfnx_last_error(const gfnx_ctx* ctx);
+int32_t gfnx_abi_version(void);
+
+/* Parameters in MlpParams::tensors() order (nn.cpp:8-19): trunk (W[in x out], b)...,
+ * fwd head, bwd head, flow head; log_z separate. fp64 on the host side. */
+gfnx_status gfnx_num_params(const gfnx_ctx* ctx, int64_t* n);
+gfnx_status gfnx_set_params(gfnx_ctx* ctx, const double* flat, int64_t n, double log_z);
+gfnx_status gfnx_get_params(gfnx_ctx* ctx, double* flat, int64_t n, double* log_z);
+/* Adam state: main m, v (n each) + step t; logZ m, v, t. NULL pointers skip a field. */
+gfnx_status gfnx_set_adam_state(gfnx_ctx* ctx, const double* m, const double* v, int64_t t,
+                                double z_m, double z_v, int64_t z_t);
+gfnx_status gfnx_get_adam_state(gfnx_ctx* ctx, double* m, double* v, int64_t* t, double* z_m,
+                                double* z_v, int64_t* z_t);
+
+/* One forward rollout of this rank's trajectory slice for iteration `it`
+ * (key fold_in(make_key(seed), 1000 + it), env_core.hpp:232-274) at exploration eps.
+ * The batch stays resident on the device. */
+gfnx_status gfnx_rollout(gfnx_ctx* ctx, int64_t it, double eps);
+/* Loss + gradient over the resident batch, NCCL all-reduce (world > 1), Adam on
+ * the main params with learning rate lr and (TB) on logZ with z_lr (train.cpp:164-192).
+ * *loss receives the global loss value (NULL: no device->host read). */
+gfnx_status gfnx_train_step(gfnx_ctx* ctx, double lr, double* loss);
+/* Same as gfnx_train_step without the Adam update (gradients kept for gfnx_get_grads). */
+gfnx_status gfnx_compute_grads(gfnx_ctx* ctx, double* loss);
+gfnx_status gfnx_get_grads(gfnx_ctx* ctx, double* flat, int64_t n, double* d_log_z);
+/* Full iteration `it`: schedules, rollout, train step (train.cpp:224-229). */
+gfnx_status gfnx_iteration(gfnx_ctx* ctx, int64_t it, double* loss);
+/* n iterations it0..it0+n-1 fully on device (CUDA-graph replay); losses[n] may be NULL. */
+gfnx_status gfnx_run(gfnx_ctx* ctx, int64_t it0, int64_t n, double* losses);
+gfnx_status gfnx_synchronize(gfnx_ctx* ctx);
+
+/* Host view of this rank's resident batch (TrajectoryBatch fields, trajectory.hpp:15-33).
+ * Caller-owned buffers sized by gfnx_batch_dims; NULL pointers are skipped. */
+typedef struct gfnx_host_batch {
+  int32_t* lengths;        /* [Bl] */
+  int32_t* fwd_actions;    /* [Bl * T], -1 on padding */
+  int32_t* bwd_actions;    /* [Bl * T], -1 on padding */
+  double* log_rewards;     /* [Bl] */
+  double* log_pb;          /* [Bl * T] log_pb_uniform, 0 on padding */
+  double* delta_log_reward;/* [Bl * T] (MDB only, 0 elsewhere) */
+  uint32_t* terminal_state;/* [Bl * state_words] packed terminal state */
+} gfnx_host_batch;
+gfnx_status gfnx_batch_dims(const gfnx_ctx* ctx, int32_t* local_batch, int32_t* first_traj,
+                            int32_t* max_len, int32_t* state_words);
+gfnx_status gfnx_export_batch(gfnx_ctx* ctx, gfnx_host_batch* out);
+
+/* Kernel launches issued by this ctx since creation (evidence for bench.py). */
+int64_t gfnx_kernel_launches(const gfnx_ctx* ctx);
+/* Device time (ms) of the last gfnx_rollout / train-step phases, measured with CUDA events. */
+gfnx_status gfnx_last_phase_ms(const gfnx_ctx* ctx, double* rollout_ms, double* train_ms);
+
+/* Stand-alone device kernels exposed for unit tests (threefry KAT, GEMM). */
+gfnx_status gfnx_test_threefry(const uint64_t* keys_hi_lo, const uint64_t* ctr, int64_t n,
+                               uint64_t* out);
+gfnx_status gfnx_test_uniform_fold(uint64_t key_hi, uint64_t key_lo, const uint64_t* idx,
+                                   int64_t n, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GFNX_H_ */
