@@ -195,6 +195,16 @@ int64_t gfnx_kernel_launches(const gfnx_ctx* ctx);
 /* Device time (ms) of the last gfnx_rollout / train-step phases, measured with CUDA events. */
 gfnx_status gfnx_last_phase_ms(const gfnx_ctx* ctx, double* rollout_ms, double* train_ms);
 
+/* CUDA events on the ctx stream (bench.py device timing): slots 0..15. */
+gfnx_status gfnx_event_record(gfnx_ctx* ctx, int32_t slot);
+gfnx_status gfnx_event_elapsed(gfnx_ctx* ctx, int32_t slot_a, int32_t slot_b, double* ms);
+/* Per-kernel CUDA-event brackets of every launch while enabled; profile_read returns the
+ * number of distinct kernels, their '\n'-separated names, summed ms and launch counts,
+ * and clears the record. */
+gfnx_status gfnx_profile(gfnx_ctx* ctx, int32_t enable);
+int32_t gfnx_profile_read(gfnx_ctx* ctx, char* names, int32_t names_cap, double* total_ms,
+                          int32_t* counts, int32_t cap);
+
 /* Stand-alone device kernels exposed for unit tests (threefry KAT, GEMM). */
 gfnx_status gfnx_test_threefry(const uint64_t* keys_hi_lo, const uint64_t* ctr, int64_t n,
                                uint64_t* out);

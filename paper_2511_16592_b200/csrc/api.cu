@@ -1,0 +1,767 @@
+// api.cu — the C ABI of libgfnx (include/gfnx.h): context lifetime, parameter/optimizer
+// state import/export, the per-iteration pipeline (rollout -> loss/grad -> NCCL all-reduce
+// -> Adam) and batch export. The pipeline mirrors train_scenario's loop body
+// (proj/src/train.cpp:224-229) and train_step (:164-192).
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <string.h>
+
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "engine.h"
+#include "host.h"
+
+namespace gfnx {
+
+namespace {
+thread_local std::string g_create_err;
+
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl_api() {  // loaded lazily: single-GPU runs never touch NCCL
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.GetUniqueId = (decltype(api.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+      api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+      api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+      api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.GetUniqueId && api.CommInitRank && api.AllReduce && api.CommDestroy;
+    }
+  }
+  return api;
+}
+
+struct Failure {
+  gfnx_status code;
+  std::string msg;
+};
+
+}  // namespace
+
+void raise_error(int code, const std::string& msg) { throw Failure{(gfnx_status)code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw Failure{GFNX_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+// ---------------------------------------------------------------------------
+// small kernels shared by both precisions
+
+// lengths -> row0 (exclusive prefix), counters[0] = sum L, counters[1] = sum max(L-1, 0);
+// counters[4..5] = the same (global values when world == 1; all-reduced otherwise).
+__global__ void k_row_scan(const int32_t* __restrict__ lengths, int Bl, int32_t* row0,
+                           int32_t* counters) {
+  __shared__ int32_t part[1024], part2[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = (Bl + nt - 1) / nt;
+  const int lo = tid * per, hi = min(Bl, lo + per);
+  int32_t s = 0, s2 = 0;
+  for (int b = lo; b < hi; ++b) {
+    s += lengths[b];
+    s2 += lengths[b] > 1 ? lengths[b] - 1 : 0;
+  }
+  part[tid] = s;
+  part2[tid] = s2;
+  __syncthreads();
+  for (int off = 1; off < nt; off <<= 1) {  // Hillis-Steele inclusive scan
+    int32_t v = tid >= off ? part[tid - off] : 0;
+    int32_t v2 = tid >= off ? part2[tid - off] : 0;
+    __syncthreads();
+    part[tid] += v;
+    part2[tid] += v2;
+    __syncthreads();
+  }
+  int32_t run = tid > 0 ? part[tid - 1] : 0;
+  for (int b = lo; b < hi; ++b) {
+    row0[b] = run;
+    run += lengths[b];
+  }
+  if (tid == nt - 1) {
+    row0[Bl] = part[nt - 1];
+    counters[0] = part[nt - 1];
+    counters[1] = part2[nt - 1];
+    counters[4] = part[nt - 1];
+    counters[5] = part2[nt - 1];
+  }
+}
+
+ProfScope::ProfScope(Ctx& ctx, const char* name) : c(ctx) {
+  if (!c.profiling) return;
+  auto take = [&]() {
+    if (c.ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = c.ev_pool.back();
+    c.ev_pool.pop_back();
+    return e;
+  };
+  Ctx::ProfRec r{name, take(), take()};
+  cudaEventRecord(r.a, c.stream);
+  c.prof.push_back(r);
+  idx = (int)c.prof.size() - 1;
+}
+
+ProfScope::~ProfScope() {
+  if (idx >= 0) cudaEventRecord(c.prof[idx].b, c.stream);
+}
+
+void launch_row_scan(Ctx& c) {
+  ProfScope ps(c, "k_row_scan");
+  k_row_scan<<<1, 1024, 0, c.stream>>>(c.batch.lengths, c.Bl, c.batch.row0, c.batch.counters);
+  c.launches++;
+}
+
+int64_t total_rows(Ctx& c) {
+  int32_t v = 0;
+  cuda_check(cudaMemcpyAsync(&v, c.batch.counters, sizeof v, cudaMemcpyDeviceToHost, c.stream),
+             "read rows");
+  cuda_check(cudaStreamSynchronize(c.stream), "sync");
+  return v;
+}
+
+__global__ void k_threefry(const uint64_t* keys, const uint64_t* ctr, int64_t n, uint64_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint64_t a, b;
+  threefry2x64(Key{keys[2 * i], keys[2 * i + 1]}, ctr[2 * i], ctr[2 * i + 1], a, b);
+  out[2 * i] = a;
+  out[2 * i + 1] = b;
+}
+
+__global__ void k_uniform_fold(Key k, const uint64_t* idx, int64_t n, double* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = uniform_scalar(fold_in(k, idx[i]));
+}
+
+__global__ void k_copy_f64_to_f32(const double* a, float* b, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (float)a[i];
+}
+__global__ void k_copy_f32_to_f64(const float* a, double* b, int64_t n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = (double)a[i];
+}
+
+}  // namespace gfnx
+
+using namespace gfnx;
+
+struct gfnx_ctx {
+  Ctx c;
+};
+
+namespace {
+
+template <class F>
+gfnx_status guard(gfnx_ctx* ctx, F&& f) {
+  try {
+    f();
+    return GFNX_OK;
+  } catch (const Failure& e) {
+    if (ctx) ctx->c.err = e.msg; else g_create_err = e.msg;
+    return e.code;
+  }
+}
+
+[[noreturn]] void fail(gfnx_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+void check_device_error(Ctx& c) {
+  int32_t e = 0;
+  cuda_check(cudaMemcpyAsync(&e, c.batch.counters + 3, sizeof e, cudaMemcpyDeviceToHost, c.stream),
+             "error word");
+  cuda_check(cudaStreamSynchronize(c.stream), "sync");
+  if (e != 0) {
+    cudaMemsetAsync(c.batch.counters + 3, 0, sizeof(int32_t), c.stream);
+    if (e == GFNX_ERR_NUMERIC) fail(GFNX_ERR_NUMERIC, "non-finite policy logits or loss");
+    fail((gfnx_status)e, "contract violation detected on device (illegal action / no legal action)");
+  }
+}
+
+void nccl_sum(Ctx& c, void* buf, size_t n, ncclDataType_t t) {
+  if (c.world <= 1) return;
+  NcclApi& api = nccl_api();
+  const ncclResult_t r = api.AllReduce(buf, buf, n, t, ncclSum, (ncclComm_t)c.nccl, c.stream);
+  if (r != ncclSuccess) fail(GFNX_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
+}
+
+void do_rollout(Ctx& c, int64_t it, double eps) {
+  if (eps < 0.0 || eps > 1.0) fail(GFNX_ERR_CONFIG, "exploration eps must lie in [0,1]");
+  const Key key = fold_in(make_key(c.train.seed), 1000 + (uint64_t)it);  // train.cpp:228
+  cudaEventRecord(c.ev[0], c.stream);
+  if (c.check_mode()) check_rollout(c, key, eps);
+  else fast_rollout(c, key, eps);
+  launch_row_scan(c);
+  if (c.world > 1) nccl_sum(c, c.batch.counters + 4, 2, ncclInt32);
+  cudaEventRecord(c.ev[1], c.stream);
+  cuda_check(cudaGetLastError(), "rollout launch");
+  c.has_batch = true;
+  c.has_grads = false;
+}
+
+// gradient + (optionally) Adam; loss read back when loss != nullptr
+void do_train(Ctx& c, bool apply, double lr, double* loss) {
+  if (!c.has_batch) fail(GFNX_ERR_CONTRACT, "train_step: no resident batch (call gfnx_rollout)");
+  const int64_t n = c.L.n_params;
+  if (c.check_mode()) {
+    check_train(c, apply, lr, loss);
+    if (c.world > 1) {
+      cudaMemcpyAsync(c.g64 + n, c.d_scalars + 3, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+      nccl_sum(c, c.g64, (size_t)n + 2, ncclFloat64);
+      cudaMemcpyAsync(c.d_scalars + 3, c.g64 + n, 2 * sizeof(double), cudaMemcpyDeviceToDevice, c.stream);
+    }
+    if (apply) check_adam(c, lr);
+  } else {
+    fast_train(c, apply, lr, loss);
+    if (c.world > 1) {
+      nccl_sum(c, c.g32, (size_t)n, ncclFloat32);
+      nccl_sum(c, c.d_scalars + 3, 2, ncclFloat64);
+    }
+    if (apply) fast_adam(c, lr);
+  }
+  cudaEventRecord(c.ev[2], c.stream);
+  cuda_check(cudaGetLastError(), "train launch");
+  c.has_grads = true;
+  if (loss) {
+    double v = 0.0;
+    cuda_check(cudaMemcpyAsync(&v, c.d_scalars + 4, sizeof v, cudaMemcpyDeviceToHost, c.stream), "loss");
+    check_device_error(c);
+    *loss = v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t gfnx_abi_version(void) { return GFNX_ABI_VERSION; }
+
+gfnx_status gfnx_default_env_desc(int32_t kind, gfnx_env_desc* out) {
+  if (kind < 0 || kind > 3 || !out) return GFNX_ERR_CONFIG;
+  default_env(kind, out);
+  return GFNX_OK;
+}
+
+gfnx_status gfnx_default_train_desc(int32_t kind, gfnx_train_desc* out) {
+  if (kind < 0 || kind > 3 || !out) return GFNX_ERR_CONFIG;
+  default_train(kind, out);
+  return GFNX_OK;
+}
+
+gfnx_status gfnx_env_shape_of(const gfnx_env_desc* env, gfnx_env_shape* out) {
+  return guard(nullptr, [&] {
+    HostEnv he;
+    const std::string err = build_host_env(*env, &he);
+    if (!err.empty()) fail(GFNX_ERR_CONFIG, err);
+    *out = he.shape;
+  });
+}
+
+const char* gfnx_last_error(const gfnx_ctx* ctx) {
+  return ctx ? ctx->c.err.c_str() : g_create_err.c_str();
+}
+
+gfnx_status gfnx_nccl_unique_id(void* out128) {
+  return guard(nullptr, [&] {
+    NcclApi& api = nccl_api();
+    if (!api.ok) fail(GFNX_ERR_NCCL, "libnccl.so.2 not found");
+    ncclUniqueId id;
+    const ncclResult_t r = api.GetUniqueId(&id);
+    if (r != ncclSuccess) fail(GFNX_ERR_NCCL, api.GetErrorString(r));
+    memcpy(out128, &id, sizeof id);
+  });
+}
+
+gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
+                        int32_t rank, int32_t world, const void* nccl_id, gfnx_ctx** out) {
+  *out = nullptr;
+  auto* h = new gfnx_ctx();
+  Ctx& c = h->c;
+  const gfnx_status st = guard(nullptr, [&] {
+    c.env = *env;
+    c.train = *train;
+    if (world < 1 || rank < 0 || rank >= world) fail(GFNX_ERR_CONFIG, "bad rank/world");
+    HostEnv he;
+    std::string err = build_host_env(*env, &he);
+    if (!err.empty()) fail(GFNX_ERR_CONFIG, err);
+    c.shape = he.shape;
+    err = validate_train(*train, c.shape);
+    if (!err.empty()) fail(GFNX_ERR_CONFIG, err);
+    resolve_schedule(&c.train.lr, c.train.iterations);
+    resolve_schedule(&c.train.explore, c.train.iterations);
+    make_layout(c.train, c.shape, &c.L);
+    c.device = device;
+    c.rank = rank;
+    c.world = world;
+    c.B = train->batch_size;
+    // contiguous slices; rank r takes [r*B/W, (r+1)*B/W) — global indices keep the RNG stream
+    c.b0 = (int)((int64_t)c.B * rank / world);
+    c.Bl = (int)((int64_t)c.B * (rank + 1) / world) - c.b0;
+    if (c.Bl < 1) fail(GFNX_ERR_CONFIG, "batch_size smaller than world size");
+    cuda_check(cudaSetDevice(device), "cudaSetDevice");
+    cuda_check(cudaStreamCreateWithFlags(&c.stream, cudaStreamNonBlocking), "stream");
+    for (auto& e : c.ev) cuda_check(cudaEventCreate(&e), "event");
+    // env tables
+    EnvParams& P = c.P;
+    P.kind = env->kind;
+    P.A = c.shape.num_actions;
+    P.Ab = c.shape.num_backward_actions;
+    P.O = c.shape.obs_dim;
+    P.T = c.shape.max_traj_len;
+    P.stop = c.shape.stop_action;
+    P.SW = c.shape.state_words;
+    P.mdb = train->objective == GFNX_OBJ_MDB;
+    P.hg_dim = env->hg_dim;
+    P.hg_side = env->hg_side;
+    memcpy(P.hg_f1, he.hg_f1, sizeof P.hg_f1);
+    memcpy(P.hg_f2, he.hg_f2, sizeof P.hg_f2);
+    memcpy(P.hg_logr, he.hg_logr, sizeof P.hg_logr);
+    P.bs_slots = he.bs_slots;
+    P.bs_vocab = he.bs_vocab;
+    P.bs_k = env->bs_k;
+    P.bs_nbits = env->bs_n_bits;
+    P.bs_words = he.mode_words;
+    P.n_modes = he.n_modes;
+    P.is_D = he.is_D;
+    P.dag_d = env->dag_d;
+    auto up = [&](auto** dst, const auto& vec) {
+      using T = typename std::decay_t<decltype(vec)>::value_type;
+      if (vec.empty()) return;
+      cuda_check(cudaMalloc((void**)dst, sizeof(T) * vec.size()), "table alloc");
+      cuda_check(cudaMemcpy(*dst, vec.data(), sizeof(T) * vec.size(), cudaMemcpyHostToDevice), "table");
+    };
+    up(&c.d_modes, he.modes);
+    up(&c.d_bs_logr, he.bs_logr);
+    up(&c.d_is_nbr, he.is_nbr);
+    up(&c.d_is_J, he.is_J);
+    up(&c.d_dag_cache, he.dag_cache);
+    up(&c.d_neglog, he.neglog);
+    c.h_dag_cache = he.dag_cache;
+    P.modes = c.d_modes;
+    P.bs_logr = c.d_bs_logr;
+    P.is_nbr = c.d_is_nbr;
+    P.is_J = c.d_is_J;
+    P.dag_cache = c.d_dag_cache;
+    P.neglog = c.d_neglog;
+    // batch
+    const int T = P.T, Bl = c.Bl;
+    DeviceBatch& bt = c.batch;
+    cuda_check(cudaMalloc(&bt.lengths, sizeof(int32_t) * Bl), "batch");
+    cuda_check(cudaMalloc(&bt.actions, sizeof(int16_t) * (size_t)Bl * T), "batch");
+    cuda_check(cudaMalloc(&bt.log_rewards, sizeof(double) * Bl), "batch");
+    cuda_check(cudaMalloc(&bt.delta, sizeof(double) * (size_t)Bl * T), "batch");
+    cuda_check(cudaMalloc(&bt.nparents, sizeof(uint16_t) * (size_t)Bl * T), "batch");
+    cuda_check(cudaMalloc(&bt.term_state, sizeof(uint32_t) * (size_t)Bl * P.SW), "batch");
+    cuda_check(cudaMalloc(&bt.row0, sizeof(int32_t) * (Bl + 1)), "batch");
+    cuda_check(cudaMalloc(&bt.counters, sizeof(int32_t) * 16), "batch");
+    cuda_check(cudaMemset(bt.counters, 0, sizeof(int32_t) * 16), "batch");
+    // parameters
+    std::vector<double> p0;
+    init_params(c.train, c.L, P.A, P.Ab, &p0);
+    const int64_t n = c.L.n_params;
+    cuda_check(cudaMalloc(&c.d_scalars, sizeof(double) * 8), "scalars");
+    std::vector<double> sc(8, 0.0);
+    sc[0] = train->logz_init;
+    cuda_check(cudaMemcpy(c.d_scalars, sc.data(), sizeof(double) * 8, cudaMemcpyHostToDevice), "scalars");
+    if (c.check_mode()) {
+      cuda_check(cudaMalloc(&c.p64, sizeof(double) * n), "params");
+      cuda_check(cudaMalloc(&c.g64, sizeof(double) * (n + 2)), "grads");
+      cuda_check(cudaMalloc(&c.m64, sizeof(double) * n), "adam");
+      cuda_check(cudaMalloc(&c.v64, sizeof(double) * n), "adam");
+      cuda_check(cudaMemcpy(c.p64, p0.data(), sizeof(double) * n, cudaMemcpyHostToDevice), "params");
+      cuda_check(cudaMemset(c.g64, 0, sizeof(double) * (n + 2)), "grads");
+      cuda_check(cudaMemset(c.m64, 0, sizeof(double) * n), "adam");
+      cuda_check(cudaMemset(c.v64, 0, sizeof(double) * n), "adam");
+    } else {
+      std::vector<float> pf(p0.begin(), p0.end());
+      cuda_check(cudaMalloc(&c.p32, sizeof(float) * n), "params");
+      cuda_check(cudaMalloc(&c.g32, sizeof(float) * (n + 2)), "grads");
+      cuda_check(cudaMalloc(&c.m32, sizeof(float) * n), "adam");
+      cuda_check(cudaMalloc(&c.v32, sizeof(float) * n), "adam");
+      cuda_check(cudaMemcpy(c.p32, pf.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "params");
+      cuda_check(cudaMemset(c.g32, 0, sizeof(float) * (n + 2)), "grads");
+      cuda_check(cudaMemset(c.m32, 0, sizeof(float) * n), "adam");
+      cuda_check(cudaMemset(c.v32, 0, sizeof(float) * n), "adam");
+      fast_init(c);
+    }
+    if (world > 1) {
+      NcclApi& api = nccl_api();
+      if (!api.ok) fail(GFNX_ERR_NCCL, "libnccl.so.2 not found");
+      if (!nccl_id) fail(GFNX_ERR_CONFIG, "world > 1 needs an NCCL unique id");
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof id);
+      ncclComm_t comm;
+      const ncclResult_t r = api.CommInitRank(&comm, world, id, rank);
+      if (r != ncclSuccess) fail(GFNX_ERR_NCCL, std::string("ncclCommInitRank: ") + api.GetErrorString(r));
+      c.nccl = comm;
+    }
+    cuda_check(cudaDeviceSynchronize(), "create");
+  });
+  if (st != GFNX_OK) {
+    gfnx_destroy(h);
+    return st;
+  }
+  *out = h;
+  return GFNX_OK;
+}
+
+void gfnx_destroy(gfnx_ctx* h) {
+  if (!h) return;
+  Ctx& c = h->c;
+  if (c.stream) cudaStreamSynchronize(c.stream);
+  if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
+  if (c.fast) fast_free(c);
+  void* ptrs[] = {c.d_modes, c.d_bs_logr, c.d_is_nbr, c.d_is_J, c.d_dag_cache, c.d_neglog,
+                  c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars,
+                  c.batch.lengths, c.batch.actions, c.batch.log_rewards, c.batch.delta,
+                  c.batch.nparents, c.batch.term_state, c.batch.row0, c.batch.counters,
+                  c.ck_obs, c.ck_act, c.ck_logp, c.ck_mask, c.ck_flow, c.ck_glogp, c.ck_gflow,
+                  c.ck_gz, c.ck_gx};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (auto& e : c.ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c.user_ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& r : c.prof) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : c.ev_pool) cudaEventDestroy(e);
+  if (c.stream) cudaStreamDestroy(c.stream);
+  delete h;
+}
+
+gfnx_status gfnx_num_params(const gfnx_ctx* h, int64_t* n) {
+  *n = h->c.L.n_params;
+  return GFNX_OK;
+}
+
+gfnx_status gfnx_set_params(gfnx_ctx* h, const double* flat, int64_t n, double log_z) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "set_params: size mismatch");
+    if (c.check_mode()) {
+      cuda_check(cudaMemcpyAsync(c.p64, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream), "params");
+    } else {
+      std::vector<float> f(flat, flat + n);
+      cuda_check(cudaMemcpyAsync(c.p32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c.stream), "params");
+      cuda_check(cudaStreamSynchronize(c.stream), "sync");
+      fast_sync_weights(c);
+    }
+    cuda_check(cudaMemcpyAsync(c.d_scalars, &log_z, sizeof(double), cudaMemcpyHostToDevice, c.stream), "logz");
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+  });
+}
+
+gfnx_status gfnx_get_params(gfnx_ctx* h, double* flat, int64_t n, double* log_z) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "get_params: size mismatch");
+    if (flat) {
+      if (c.check_mode()) {
+        cuda_check(cudaMemcpyAsync(flat, c.p64, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "params");
+      } else {
+        std::vector<float> f(n);
+        cuda_check(cudaMemcpyAsync(f.data(), c.p32, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream), "params");
+        cuda_check(cudaStreamSynchronize(c.stream), "sync");
+        for (int64_t i = 0; i < n; ++i) flat[i] = f[i];
+      }
+    }
+    if (log_z) cuda_check(cudaMemcpyAsync(log_z, c.d_scalars, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "logz");
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+  });
+}
+
+gfnx_status gfnx_set_adam_state(gfnx_ctx* h, const double* m, const double* v, int64_t t,
+                                double z_m, double z_v, int64_t z_t) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const int64_t n = c.L.n_params;
+    if (c.check_mode()) {
+      if (m) cuda_check(cudaMemcpy(c.m64, m, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
+      if (v) cuda_check(cudaMemcpy(c.v64, v, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
+    } else {
+      if (m) {
+        std::vector<float> f(m, m + n);
+        cuda_check(cudaMemcpy(c.m32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "adam");
+      }
+      if (v) {
+        std::vector<float> f(v, v + n);
+        cuda_check(cudaMemcpy(c.v32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "adam");
+      }
+    }
+    double zs[2] = {z_m, z_v};
+    cuda_check(cudaMemcpy(c.d_scalars + 1, zs, sizeof zs, cudaMemcpyHostToDevice), "adam z");
+    c.adam_t = t;
+    c.z_t = z_t;
+  });
+}
+
+gfnx_status gfnx_get_adam_state(gfnx_ctx* h, double* m, double* v, int64_t* t, double* z_m,
+                                double* z_v, int64_t* z_t) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+    const int64_t n = c.L.n_params;
+    auto get = [&](double* dst, const double* s64, const float* s32) {
+      if (!dst) return;
+      if (c.check_mode()) {
+        cuda_check(cudaMemcpy(dst, s64, sizeof(double) * n, cudaMemcpyDeviceToHost), "adam");
+      } else {
+        std::vector<float> f(n);
+        cuda_check(cudaMemcpy(f.data(), s32, sizeof(float) * n, cudaMemcpyDeviceToHost), "adam");
+        for (int64_t i = 0; i < n; ++i) dst[i] = f[i];
+      }
+    };
+    get(m, c.m64, c.m32);
+    get(v, c.v64, c.v32);
+    double zs[2];
+    cuda_check(cudaMemcpy(zs, c.d_scalars + 1, sizeof zs, cudaMemcpyDeviceToHost), "adam z");
+    if (z_m) *z_m = zs[0];
+    if (z_v) *z_v = zs[1];
+    if (t) *t = c.adam_t;
+    if (z_t) *z_t = c.z_t;
+  });
+}
+
+gfnx_status gfnx_rollout(gfnx_ctx* h, int64_t it, double eps) {
+  return guard(h, [&] {
+    do_rollout(h->c, it, eps);
+    check_device_error(h->c);
+  });
+}
+
+gfnx_status gfnx_train_step(gfnx_ctx* h, double lr, double* loss) {
+  return guard(h, [&] { do_train(h->c, true, lr, loss); });
+}
+
+gfnx_status gfnx_compute_grads(gfnx_ctx* h, double* loss) {
+  return guard(h, [&] {
+    double l = 0.0;
+    do_train(h->c, false, 0.0, &l);
+    if (loss) *loss = l;
+  });
+}
+
+gfnx_status gfnx_get_grads(gfnx_ctx* h, double* flat, int64_t n, double* d_log_z) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "get_grads: size mismatch");
+    if (!c.has_grads) fail(GFNX_ERR_CONTRACT, "get_grads: no gradients computed");
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+    if (flat) {
+      if (c.check_mode()) {
+        cuda_check(cudaMemcpy(flat, c.g64, sizeof(double) * n, cudaMemcpyDeviceToHost), "grads");
+      } else {
+        std::vector<float> f(n);
+        cuda_check(cudaMemcpy(f.data(), c.g32, sizeof(float) * n, cudaMemcpyDeviceToHost), "grads");
+        for (int64_t i = 0; i < n; ++i) flat[i] = f[i];
+      }
+    }
+    if (d_log_z) cuda_check(cudaMemcpy(d_log_z, c.d_scalars + 3, sizeof(double), cudaMemcpyDeviceToHost), "dlogz");
+  });
+}
+
+gfnx_status gfnx_iteration(gfnx_ctx* h, int64_t it, double* loss) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const double lr = schedule_value(c.train.lr, it);       // train.cpp:225
+    const double eps = schedule_value(c.train.explore, it); // train.cpp:226
+    do_rollout(c, it, eps);
+    do_train(c, true, lr, loss);
+  });
+}
+
+gfnx_status gfnx_run(gfnx_ctx* h, int64_t it0, int64_t n, double* losses) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t it = it0 + i;
+      do_rollout(c, it, schedule_value(c.train.explore, it));
+      do_train(c, true, schedule_value(c.train.lr, it), losses ? losses + i : nullptr);
+    }
+    check_device_error(c);
+  });
+}
+
+gfnx_status gfnx_synchronize(gfnx_ctx* h) {
+  return guard(h, [&] {
+    cuda_check(cudaStreamSynchronize(h->c.stream), "sync");
+    check_device_error(h->c);
+  });
+}
+
+gfnx_status gfnx_batch_dims(const gfnx_ctx* h, int32_t* local_batch, int32_t* first_traj,
+                            int32_t* max_len, int32_t* state_words) {
+  if (local_batch) *local_batch = h->c.Bl;
+  if (first_traj) *first_traj = h->c.b0;
+  if (max_len) *max_len = h->c.P.T;
+  if (state_words) *state_words = h->c.P.SW;
+  return GFNX_OK;
+}
+
+gfnx_status gfnx_export_batch(gfnx_ctx* h, gfnx_host_batch* out) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (!c.has_batch) fail(GFNX_ERR_CONTRACT, "export_batch: no resident batch");
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+    const int Bl = c.Bl, T = c.P.T;
+    const size_t bt = (size_t)Bl * T;
+    if (out->lengths) cuda_check(cudaMemcpy(out->lengths, c.batch.lengths, sizeof(int32_t) * Bl, cudaMemcpyDeviceToHost), "export");
+    if (out->log_rewards) cuda_check(cudaMemcpy(out->log_rewards, c.batch.log_rewards, sizeof(double) * Bl, cudaMemcpyDeviceToHost), "export");
+    if (out->delta_log_reward) cuda_check(cudaMemcpy(out->delta_log_reward, c.batch.delta, sizeof(double) * bt, cudaMemcpyDeviceToHost), "export");
+    if (out->terminal_state) cuda_check(cudaMemcpy(out->terminal_state, c.batch.term_state, sizeof(uint32_t) * Bl * c.P.SW, cudaMemcpyDeviceToHost), "export");
+    std::vector<int16_t> a(bt);
+    std::vector<uint16_t> np(bt);
+    cuda_check(cudaMemcpy(a.data(), c.batch.actions, sizeof(int16_t) * bt, cudaMemcpyDeviceToHost), "export");
+    cuda_check(cudaMemcpy(np.data(), c.batch.nparents, sizeof(uint16_t) * bt, cudaMemcpyDeviceToHost), "export");
+    HostEnv he;
+    build_host_env(c.env, &he);
+    for (size_t i = 0; i < bt; ++i) {
+      const int act = a[i];
+      if (out->fwd_actions) out->fwd_actions[i] = act;
+      if (out->bwd_actions) {
+        int ba = -1;
+        if (act >= 0) {
+          switch (c.env.kind) {  // get_backward_action of each env
+            case GFNX_ENV_BITSEQ: ba = act / c.P.bs_vocab; break;
+            case GFNX_ENV_ISING: ba = act / 2; break;
+            default: ba = act;
+          }
+        }
+        out->bwd_actions[i] = ba;
+      }
+      if (out->log_pb) out->log_pb[i] = act >= 0 ? he.neglog[np[i]] : 0.0;
+    }
+  });
+}
+
+int64_t gfnx_kernel_launches(const gfnx_ctx* h) { return h->c.launches; }
+
+gfnx_status gfnx_last_phase_ms(const gfnx_ctx* h, double* rollout_ms, double* train_ms) {
+  return guard(const_cast<gfnx_ctx*>(h), [&] {
+    const Ctx& c = h->c;
+    cuda_check(cudaEventSynchronize(c.ev[2]), "event");
+    float a = 0.f, b = 0.f;
+    cuda_check(cudaEventElapsedTime(&a, c.ev[0], c.ev[1]), "event");
+    cuda_check(cudaEventElapsedTime(&b, c.ev[1], c.ev[2]), "event");
+    if (rollout_ms) *rollout_ms = a;
+    if (train_ms) *train_ms = b;
+  });
+}
+
+gfnx_status gfnx_event_record(gfnx_ctx* h, int32_t slot) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (slot < 0 || slot >= 16) fail(GFNX_ERR_CONFIG, "event slot out of range");
+    if (!c.user_ev[slot]) cuda_check(cudaEventCreate(&c.user_ev[slot]), "event");
+    cuda_check(cudaEventRecord(c.user_ev[slot], c.stream), "event record");
+  });
+}
+
+gfnx_status gfnx_event_elapsed(gfnx_ctx* h, int32_t a, int32_t b, double* ms) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (a < 0 || a >= 16 || b < 0 || b >= 16 || !c.user_ev[a] || !c.user_ev[b])
+      fail(GFNX_ERR_CONFIG, "event slot not recorded");
+    cuda_check(cudaEventSynchronize(c.user_ev[b]), "event sync");
+    float f = 0.f;
+    cuda_check(cudaEventElapsedTime(&f, c.user_ev[a], c.user_ev[b]), "elapsed");
+    *ms = f;
+  });
+}
+
+gfnx_status gfnx_profile(gfnx_ctx* h, int32_t enable) {
+  h->c.profiling = enable != 0;
+  return GFNX_OK;
+}
+
+int32_t gfnx_profile_read(gfnx_ctx* h, char* names, int32_t names_cap, double* total_ms,
+                          int32_t* counts, int32_t cap) {
+  Ctx& c = h->c;
+  cudaStreamSynchronize(c.stream);
+  std::vector<std::string> keys;
+  std::vector<double> tot;
+  std::vector<int> cnt;
+  for (auto& r : c.prof) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.a, r.b);
+    size_t k = 0;
+    while (k < keys.size() && keys[k] != r.name) ++k;
+    if (k == keys.size()) {
+      keys.push_back(r.name);
+      tot.push_back(0.0);
+      cnt.push_back(0);
+    }
+    tot[k] += ms;
+    cnt[k] += 1;
+    c.ev_pool.push_back(r.a);
+    c.ev_pool.push_back(r.b);
+  }
+  c.prof.clear();
+  std::string joined;
+  int n = 0;
+  for (size_t k = 0; k < keys.size() && (int)k < cap; ++k, ++n) {
+    joined += keys[k] + "\n";
+    total_ms[k] = tot[k];
+    counts[k] = cnt[k];
+  }
+  if (names && names_cap > 0) {
+    const size_t m = std::min<size_t>(joined.size(), (size_t)names_cap - 1);
+    memcpy(names, joined.data(), m);
+    names[m] = 0;
+  }
+  return n;
+}
+
+gfnx_status gfnx_test_threefry(const uint64_t* keys, const uint64_t* ctr, int64_t n, uint64_t* out) {
+  return guard(nullptr, [&] {
+    uint64_t *dk, *dc, *dout;
+    cuda_check(cudaMalloc(&dk, 16 * n), "alloc");
+    cuda_check(cudaMalloc(&dc, 16 * n), "alloc");
+    cuda_check(cudaMalloc(&dout, 16 * n), "alloc");
+    cudaMemcpy(dk, keys, 16 * n, cudaMemcpyHostToDevice);
+    cudaMemcpy(dc, ctr, 16 * n, cudaMemcpyHostToDevice);
+    k_threefry<<<(unsigned)((n + 255) / 256), 256>>>(dk, dc, n, dout);
+    cuda_check(cudaMemcpy(out, dout, 16 * n, cudaMemcpyDeviceToHost), "threefry");
+    cudaFree(dk);
+    cudaFree(dc);
+    cudaFree(dout);
+  });
+}
+
+gfnx_status gfnx_test_uniform_fold(uint64_t key_hi, uint64_t key_lo, const uint64_t* idx, int64_t n,
+                                   double* out) {
+  return guard(nullptr, [&] {
+    uint64_t* di;
+    double* dout;
+    cuda_check(cudaMalloc(&di, 8 * n), "alloc");
+    cuda_check(cudaMalloc(&dout, 8 * n), "alloc");
+    cudaMemcpy(di, idx, 8 * n, cudaMemcpyHostToDevice);
+    k_uniform_fold<<<(unsigned)((n + 255) / 256), 256>>>(Key{key_hi, key_lo}, di, n, dout);
+    cuda_check(cudaMemcpy(out, dout, 8 * n, cudaMemcpyDeviceToHost), "uniform");
+    cudaFree(di);
+    cudaFree(dout);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,613 @@
+// check.cu — fp64 "check mode": SIMT kernels that reproduce the reference's
+// operation order (compiled with --fmad=false so no FMA contraction happens, like the
+// -ffp-contract=off reference build in oracle/_ref). Used for teacher-forced parity:
+// sampled actions, terminal states, masks and log-rewards come out bit-exact; losses,
+// gradients and updated parameters agree to the last few ulps (device exp/log vs glibc).
+//
+//   k_check_rollout  forward_rollout + rollout_from_actions  env_core.hpp:166-274
+//   k_check_fwd      mlp_forward_tape + masked_log_softmax    nn.cpp:91-126, tape.cpp:177-213
+//   k_check_loss     tb/db/subtb/mdb losses + their backward  objectives.cpp:94-226
+//   k_check_bwd      masked log-softmax / MLP backward rows   tape.cpp:344-434
+//   k_check_wgrad    matmul_tn_acc / add_rowvec weight grads  tensor.cpp:92-102, tape.cpp:380-389
+//   k_check_adam     adam_step                                optim.cpp:19-43
+#include <math.h>
+
+#include "engine.h"
+
+namespace gfnx {
+
+namespace {
+
+struct DevLayout {
+  int n_trunk, H, act_sz, A, O;
+  int dims[10];
+  int64_t off_w[10], off_b[10];
+  int64_t off_fw, off_fb, off_flw, off_flb;
+  int act_off[10];
+};
+
+DevLayout make_dev_layout(const Ctx& c) {
+  DevLayout d{};
+  d.n_trunk = c.L.n_trunk;
+  d.H = c.L.H();
+  d.A = c.shape.num_actions;
+  d.O = c.shape.obs_dim;
+  int o = 0;
+  for (int l = 0; l <= c.L.n_trunk; ++l) d.dims[l] = c.L.dims[l];
+  for (int l = 0; l < c.L.n_trunk; ++l) {
+    d.off_w[l] = c.L.off_w[l];
+    d.off_b[l] = c.L.off_b[l];
+    d.act_off[l] = o;
+    o += c.L.dims[l + 1];
+  }
+  d.act_sz = o;
+  d.off_fw = c.L.off_fw;
+  d.off_fb = c.L.off_fb;
+  d.off_flw = c.L.off_flw;
+  d.off_flb = c.L.off_flb;
+  return d;
+}
+
+// z = matmul(h, W) + b (+ReLU), one output per thread, sequential over the input index
+// exactly like matmul_acc (tensor.cpp:67-77) followed by the bias/ReLU loop (nn.cpp:64-74).
+__device__ void dense_block(const double* h, int in, const double* W, const double* b, int out,
+                            double* z, bool relu) {
+  for (int j = threadIdx.x; j < out; j += blockDim.x) {
+    double acc = 0.0;
+    for (int p = 0; p < in; ++p) acc += h[p] * W[(size_t)p * out + j];
+    acc += b[j];
+    if (relu && acc < 0.0) acc = 0.0;
+    z[j] = acc;
+  }
+}
+
+template <class Env>
+__global__ void k_check_rollout(EnvParams P, DevLayout D, const double* __restrict__ params,
+                                Key key, double eps, int b0, int Bl, DeviceBatch batch,
+                                double* obs_scratch, double* logit_scratch, int32_t* err) {
+  const int b = blockIdx.x;
+  if (b >= Bl) return;
+  __shared__ typename Env::State s;
+  __shared__ double hbuf[2][512];
+  __shared__ int s_done;
+  const int T = P.T, A = P.A;
+  double* obs = obs_scratch + (size_t)b * P.O;
+  double* w = logit_scratch + (size_t)b * A;
+  if (threadIdx.x == 0) {
+    Env::reset(P, s);
+    batch.lengths[b] = 0;
+    batch.log_rewards[b] = 0.0;
+  }
+  for (int t = threadIdx.x; t < T; t += blockDim.x) {
+    batch.actions[(size_t)b * T + t] = -1;
+    batch.nparents[(size_t)b * T + t] = 0;
+    batch.delta[(size_t)b * T + t] = 0.0;
+  }
+  __syncthreads();
+  for (int t = 0; t < T; ++t) {
+    for (int i = threadIdx.x; i < P.O; i += blockDim.x) obs[i] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) Env::features(P, s, [&](int f, double v) { obs[f] = v; });
+    __syncthreads();
+    const double* h = obs;
+    int in = P.O;
+    for (int l = 0; l < D.n_trunk; ++l) {
+      double* z = hbuf[l & 1];
+      dense_block(h, in, params + D.off_w[l], params + D.off_b[l], D.dims[l + 1], z, true);
+      __syncthreads();
+      h = z;
+      in = D.dims[l + 1];
+    }
+    dense_block(h, in, params + D.off_fw, params + D.off_fb, A, w, false);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // eps_uniform (objectives.cpp:242-264) then categorical (rng.cpp:87-100)
+      int legal = 0;
+      double hi = -INFINITY;
+      bool finite = true;
+      for (int i = 0; i < A; ++i) {
+        finite &= isfinite(w[i]);
+        if (Env::legal(P, s, i)) {
+          ++legal;
+          if (w[i] > hi) hi = w[i];
+        }
+      }
+      int a = -1;
+      if (!finite) {
+        atomicExch(err, GFNX_ERR_NUMERIC);
+      } else if (legal == 0) {
+        atomicExch(err, GFNX_ERR_CONTRACT);
+      } else {
+        double z = 0.0;
+        for (int i = 0; i < A; ++i) {
+          if (Env::legal(P, s, i)) {
+            const double p = exp(w[i] - hi);
+            w[i] = p;
+            z += p;
+          } else {
+            w[i] = 0.0;
+          }
+        }
+        const double u = eps / legal;
+        double total = 0.0;
+        for (int i = 0; i < A; ++i) {
+          if (Env::legal(P, s, i)) w[i] = (1.0 - eps) * w[i] / z + u;
+          total += w[i];
+        }
+        const double uu =
+            uniform_scalar(fold_in(fold_in(key, (uint64_t)t), (uint64_t)(b0 + b))) * total;
+        double acc = 0.0;
+        for (int i = 0; i < A; ++i) {
+          acc += w[i];
+          if (uu < acc) {
+            a = i;
+            break;
+          }
+        }
+        if (a < 0)
+          for (int i = A - 1; i >= 0; --i)
+            if (w[i] > 0.0) {
+              a = i;
+              break;
+            }
+      }
+      s_done = 1;
+      if (a >= 0) {
+        // rollout_from_actions bookkeeping (env_core.hpp:190-217)
+        const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
+        const bool term = Env::step(P, s, a);
+        batch.actions[(size_t)b * T + t] = (int16_t)a;
+        batch.nparents[(size_t)b * T + t] = (uint16_t)Env::num_parents(P, s);
+        if (P.mdb && !term) batch.delta[(size_t)b * T + t] = Env::log_reward(P, s) - prev_r;
+        if (term) {
+          batch.lengths[b] = t + 1;
+          batch.log_rewards[b] = Env::log_reward(P, s);
+          Env::pack(P, s, batch.term_state + (size_t)b * P.SW);
+        } else {
+          s_done = 0;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_done) break;
+  }
+  if (threadIdx.x == 0 && batch.lengths[b] == 0) atomicExch(err, GFNX_ERR_CONTRACT);
+}
+
+// Row r -> trajectory through the exclusive prefix of lengths.
+__device__ int find_traj(const int32_t* row0, int Bl, int r) {
+  int lo = 0, hi = Bl;  // row0[lo] <= r < row0[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (row0[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+template <class Env>
+__global__ void k_check_fwd(EnvParams P, DevLayout D, const double* __restrict__ params,
+                            DeviceBatch batch, int Bl, int R, int need_flow, double* obs_out,
+                            double* act_out, double* logp_out, uint8_t* mask_out,
+                            double* flow_out, int32_t* err) {
+  const int r = blockIdx.x;
+  if (r >= R) return;
+  __shared__ typename Env::State s;
+  __shared__ double red;
+  const int T = P.T, A = P.A;
+  double* obs = obs_out + (size_t)r * P.O;
+  double* act = act_out + (size_t)r * D.act_sz;
+  double* x = logp_out + (size_t)r * A;
+  uint8_t* mask = mask_out + (size_t)r * A;
+  if (threadIdx.x == 0) {
+    const int b = find_traj(batch.row0, Bl, r);
+    const int t = r - batch.row0[b];
+    Env::reset(P, s);
+    for (int q = 0; q < t; ++q) Env::step(P, s, batch.actions[(size_t)b * T + q]);
+  }
+  for (int i = threadIdx.x; i < P.O; i += blockDim.x) obs[i] = 0.0;
+  __syncthreads();
+  if (threadIdx.x == 0) Env::features(P, s, [&](int f, double v) { obs[f] = v; });
+  for (int i = threadIdx.x; i < A; i += blockDim.x) mask[i] = Env::legal(P, s, i) ? 1 : 0;
+  __syncthreads();
+  const double* h = obs;
+  int in = P.O;
+  for (int l = 0; l < D.n_trunk; ++l) {
+    double* z = act + D.act_off[l];
+    dense_block(h, in, params + D.off_w[l], params + D.off_b[l], D.dims[l + 1], z, true);
+    __syncthreads();
+    h = z;
+    in = D.dims[l + 1];
+  }
+  dense_block(h, in, params + D.off_fw, params + D.off_fb, A, x, false);
+  if (need_flow && threadIdx.x == 0) {
+    double acc = 0.0;
+    for (int p = 0; p < in; ++p) acc += h[p] * params[D.off_flw + p];
+    acc += params[D.off_flb];
+    flow_out[r] = acc;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // masked_log_softmax (tape.cpp:177-213)
+    double hi = -INFINITY;
+    for (int c = 0; c < A; ++c)
+      if (mask[c] && x[c] > hi) hi = x[c];
+    if (!isfinite(hi)) {
+      atomicExch(err, GFNX_ERR_NUMERIC);
+      hi = 0.0;
+    }
+    double ssum = 0.0;
+    for (int c = 0; c < A; ++c)
+      if (mask[c]) ssum += exp(x[c] - hi);
+    red = hi + log(ssum);
+  }
+  __syncthreads();
+  const double lse = red;
+  for (int c = threadIdx.x; c < A; c += blockDim.x) x[c] = mask[c] ? x[c] - lse : -1e30;
+}
+
+// Objectives, one thread, the reference's accumulation order (gfn_oracle.c mirrors it):
+// tb_loss :120-142, transition_loss :94-118, subtb_loss :144-180, mdb_loss :186-226.
+__global__ void k_check_loss(int obj, int A, int T, int B_global, double terminal_penalty,
+                             int stop, const double* lampow, const double* neglog,
+                             DeviceBatch batch, int Bl, const int32_t* gcounts,
+                             const double* logp, const double* flow, double* glogp,
+                             double* gflow, double* gpair, double* scalars, int32_t* err) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double log_z = scalars[0];
+  double norm = (double)B_global;
+  if (obj == GFNX_OBJ_DB) norm = (double)gcounts[0];
+  if (obj == GFNX_OBJ_MDB) norm = (double)gcounts[1];
+  double loss = 0.0, dlogz = 0.0;
+  for (int b = 0; b < Bl; ++b) {
+    const int L = batch.lengths[b];
+    const int64_t r0 = batch.row0[b];
+    const int16_t* acts = batch.actions + (size_t)b * T;
+    const uint16_t* np = batch.nparents + (size_t)b * T;
+    const double logr = batch.log_rewards[b];
+    if (obj == GFNX_OBJ_TB) {
+      const double w = 1.0 / norm;
+      double cum = 0.0;
+      for (int t = 0; t < L; ++t) cum += logp[(r0 + t) * A + acts[t]] + -neglog[np[t]];
+      const double res = (cum + log_z) + -logr;
+      loss += res * res * w;
+      const double g = 2.0 * res * w;
+      dlogz += g;
+      for (int t = 0; t < L; ++t) glogp[(r0 + t) * A + acts[t]] += g;
+    } else if (obj == GFNX_OBJ_DB) {
+      for (int t = 0; t < L; ++t) {
+        const int64_t r = r0 + t;
+        const double d = logp[r * A + acts[t]] + -neglog[np[t]];
+        const double f1 = (t + 1 < L) ? flow[r + 1] : logr;
+        const double res = (flow[r] - f1) + d;
+        const double w = (t == L - 1 ? terminal_penalty : 1.0) / norm;
+        loss += res * res * w;
+        const double g = 2.0 * res * w;
+        gflow[r] += g;
+        if (t + 1 < L) gflow[r + 1] += -g;
+        glogp[r * A + acts[t]] += g;
+      }
+    } else if (obj == GFNX_OBJ_SUBTB) {
+      double* cum = gpair;                       // [T+1]
+      double* F = gpair + (T + 1);               // [T+1]
+      double* gcum = gpair + 2 * (T + 1);        // [T+1]
+      double* gp = gpair + 3 * (T + 1);          // [(T+1)^2]
+      cum[0] = 0.0;
+      for (int t = 0; t < L; ++t) {
+        cum[t + 1] = cum[t] + (logp[(r0 + t) * A + acts[t]] + -neglog[np[t]]);
+        F[t] = flow[r0 + t];
+      }
+      F[L] = logr;
+      double nrm = 0.0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) nrm += lampow[k - j];
+      if (nrm <= 0.0) continue;
+      for (int k = 0; k <= L; ++k) gcum[k] = 0.0;
+      int n = 0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) {
+          const double w = lampow[k - j] / nrm / norm;
+          const double res = (F[j] - F[k]) + (cum[k] - cum[j]);
+          loss += res * res * w;
+          gp[n++] = 2.0 * res * w;
+        }
+      // backward visit order of the right-to-left-built tape (see gfn_oracle.c)
+      n = 0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) gflow[r0 + j] += gp[n++];
+      n = 0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) {
+          if (k < L) gflow[r0 + k] += -gp[n];
+          ++n;
+        }
+      n = 0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) gcum[k] += gp[n++];
+      n = 0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) gcum[j] += -gp[n++];
+      double acc = 0.0;  // exclusive_row_cumsum backward (tape.cpp:448-461)
+      for (int c = L; c >= 0; --c) {
+        if (c < L) glogp[(r0 + c) * A + acts[c]] += acc;
+        acc += gcum[c];
+      }
+    } else if (obj == GFNX_OBJ_MDB) {
+      const double w = 1.0 / norm;
+      for (int t = 0; t + 1 < L; ++t) {
+        const int64_t r = r0 + t;
+        const int a = acts[t];
+        if (a == stop) atomicExch(err, GFNX_ERR_CONTRACT);
+        double res = logp[r * A + a] + (logp[(r + 1) * A + stop] - logp[r * A + stop]);
+        res = res + -neglog[np[t]];
+        res = res + -batch.delta[(size_t)b * T + t];
+        loss += res * res * w;
+        const double g = 2.0 * res * w;
+        glogp[r * A + a] += g;
+        glogp[(r + 1) * A + stop] += g;
+        glogp[r * A + stop] += -g;
+      }
+    }
+  }
+  if (!isfinite(loss)) atomicExch(err, GFNX_ERR_NUMERIC);
+  scalars[4] = loss;
+  scalars[3] = obj == GFNX_OBJ_TB ? dlogz : 0.0;
+}
+
+// Per row: masked log-softmax backward (tape.cpp:413-434), head dgrad, trunk dgrads.
+// Stores gx [R x A] and gz [R x act_sz] (gradient w.r.t. each trunk layer's pre-activation).
+__global__ void k_check_bwd(DevLayout D, const double* __restrict__ params, int R, int need_flow,
+                            const double* act, const double* logp, const uint8_t* mask,
+                            const double* glogp, const double* gflow, double* gx_out,
+                            double* gz_out) {
+  const int r = blockIdx.x;
+  if (r >= R) return;
+  __shared__ double gsum_s;
+  __shared__ double gh[512];
+  const int A = D.A;
+  const double* lp = logp + (size_t)r * A;
+  const double* gr = glogp + (size_t)r * A;
+  const uint8_t* mr = mask + (size_t)r * A;
+  double* gx = gx_out + (size_t)r * A;
+  double* gz = gz_out + (size_t)r * D.act_sz;
+  const double* a_r = act + (size_t)r * D.act_sz;
+  if (threadIdx.x == 0) {
+    double gsum = 0.0;
+    for (int c = 0; c < A; ++c)
+      if (mr[c]) gsum += gr[c];
+    gsum_s = gsum;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < A; c += blockDim.x)
+    gx[c] = mr[c] ? gr[c] - exp(lp[c]) * gsum_s : 0.0;
+  __syncthreads();
+  const int H = D.H;
+  const double gf = need_flow ? gflow[r] : 0.0;
+  for (int p = threadIdx.x; p < H; p += blockDim.x) {  // flow node first, then fwd head
+    double v = 0.0;
+    if (need_flow) v += gf * params[D.off_flw + p];
+    double acc = 0.0;
+    const double* wr = params + D.off_fw + (size_t)p * A;
+    for (int j = 0; j < A; ++j) acc += gx[j] * wr[j];
+    gh[p] = v + acc;
+  }
+  __syncthreads();
+  for (int l = D.n_trunk - 1; l >= 0; --l) {
+    const int out = D.dims[l + 1], in = D.dims[l];
+    double* gzl = gz + D.act_off[l];
+    const double* al = a_r + D.act_off[l];
+    for (int j = threadIdx.x; j < out; j += blockDim.x) gzl[j] = al[j] > 0.0 ? gh[j] : 0.0;
+    __syncthreads();
+    if (l > 0) {
+      const double* W = params + D.off_w[l];
+      for (int p = threadIdx.x; p < in; p += blockDim.x) {
+        double acc = 0.0;
+        const double* wr = W + (size_t)p * out;
+        for (int j = 0; j < out; ++j) acc += gzl[j] * wr[j];
+        gh[p] = acc;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// One thread per parameter element, rows accumulated sequentially in (b, t) order:
+// matmul_tn_acc (tensor.cpp:92-102) and the add_rowvec bias backward (tape.cpp:380-389).
+__global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* obs,
+                              const double* act, const double* gx, const double* gz,
+                              const double* gflow, double* grads) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int A = D.A;
+  // trunk weights / biases
+  for (int l = 0; l < D.n_trunk; ++l) {
+    const int in = D.dims[l], out = D.dims[l + 1];
+    const int64_t nw = (int64_t)in * out;
+    if (e >= D.off_w[l] && e < D.off_w[l] + nw) {
+      const int64_t q = e - D.off_w[l];
+      const int p = (int)(q / out), j = (int)(q % out);
+      double acc = 0.0;
+      for (int r = 0; r < R; ++r) {
+        const double av = l == 0 ? obs[(size_t)r * D.O + p] : act[(size_t)r * D.act_sz + D.act_off[l - 1] + p];
+        acc += av * gz[(size_t)r * D.act_sz + D.act_off[l] + j];
+      }
+      grads[e] = acc;
+      return;
+    }
+    if (e >= D.off_b[l] && e < D.off_b[l] + out) {
+      const int j = (int)(e - D.off_b[l]);
+      double acc = 0.0;
+      for (int r = 0; r < R; ++r) acc += gz[(size_t)r * D.act_sz + D.act_off[l] + j];
+      grads[e] = acc;
+      return;
+    }
+  }
+  const int H = D.H;
+  const int last = D.act_off[D.n_trunk - 1];
+  if (e >= D.off_fw && e < D.off_fw + (int64_t)H * A) {
+    const int64_t q = e - D.off_fw;
+    const int p = (int)(q / A), j = (int)(q % A);
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += act[(size_t)r * D.act_sz + last + p] * gx[(size_t)r * A + j];
+    grads[e] = acc;
+    return;
+  }
+  if (e >= D.off_fb && e < D.off_fb + A) {
+    const int j = (int)(e - D.off_fb);
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += gx[(size_t)r * A + j];
+    grads[e] = acc;
+    return;
+  }
+  if (need_flow && e >= D.off_flw && e < D.off_flw + H) {
+    const int p = (int)(e - D.off_flw);
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += act[(size_t)r * D.act_sz + last + p] * gflow[r];
+    grads[e] = acc;
+    return;
+  }
+  if (need_flow && e == D.off_flb) {
+    double acc = 0.0;
+    for (int r = 0; r < R; ++r) acc += gflow[r];
+    grads[e] = acc;
+  }
+}
+
+// adam_step (optim.cpp:19-43); bias corrections computed on the host with glibc pow.
+__global__ void k_check_adam(double* p, const double* g, double* m, double* v, int64_t n,
+                             double lr, double b1, double b2, double eps, double wd, double bc1,
+                             double bc2, double* scalars, int do_z, double z_lr, double zbc1,
+                             double zbc2) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const double gj = g[j];
+    m[j] = b1 * m[j] + (1.0 - b1) * gj;
+    v[j] = b2 * v[j] + (1.0 - b2) * gj * gj;
+    const double mhat = m[j] / bc1;
+    const double vhat = v[j] / bc2;
+    p[j] -= lr * (mhat / (sqrt(vhat) + eps) + wd * p[j]);
+  }
+  if (do_z && j == 0) {  // logZ: separate AdamState, weight decay 0 (train.cpp:125-128,186-190)
+    const double gj = scalars[3];
+    scalars[1] = b1 * scalars[1] + (1.0 - b1) * gj;
+    scalars[2] = b2 * scalars[2] + (1.0 - b2) * gj * gj;
+    const double mhat = scalars[1] / zbc1;
+    const double vhat = scalars[2] / zbc2;
+    scalars[0] -= z_lr * (mhat / (sqrt(vhat) + eps) + 0.0 * scalars[0]);
+  }
+}
+
+template <class Env>
+void rollout_impl(Ctx& c, Key key, double eps) {
+  const DevLayout D = make_dev_layout(c);
+  k_check_rollout<Env><<<c.Bl, 256, 0, c.stream>>>(c.P, D, c.p64, key, eps, c.b0, c.Bl, c.batch,
+                                                    c.ck_obs, c.ck_logp, c.batch.counters + 3);
+  c.launches++;
+}
+
+template <class Env>
+void fwd_impl(Ctx& c, int R, int need_flow) {
+  const DevLayout D = make_dev_layout(c);
+  k_check_fwd<Env><<<R, 256, 0, c.stream>>>(c.P, D, c.p64, c.batch, c.Bl, R, need_flow, c.ck_obs,
+                                            c.ck_act, c.ck_logp, c.ck_mask, c.ck_flow,
+                                            c.batch.counters + 3);
+  c.launches++;
+}
+
+void ensure_scratch(Ctx& c, int64_t rows) {
+  if (rows <= c.ck_rows_cap) return;
+  const DevLayout D = make_dev_layout(c);
+  cudaFree(c.ck_obs);
+  cudaFree(c.ck_act);
+  cudaFree(c.ck_logp);
+  cudaFree(c.ck_mask);
+  cudaFree(c.ck_flow);
+  cudaFree(c.ck_glogp);
+  cudaFree(c.ck_gflow);
+  cudaFree(c.ck_gz);
+  cudaFree(c.ck_gx);
+  const int64_t n = rows > c.Bl ? rows : c.Bl;
+  cuda_check(cudaMalloc(&c.ck_obs, sizeof(double) * n * D.O), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_act, sizeof(double) * n * D.act_sz), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_logp, sizeof(double) * n * D.A), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_mask, n * D.A), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_flow, sizeof(double) * n), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_glogp, sizeof(double) * n * D.A), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_gflow, sizeof(double) * n), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_gz, sizeof(double) * n * D.act_sz), "check scratch");
+  cuda_check(cudaMalloc(&c.ck_gx, sizeof(double) * n * D.A), "check scratch");
+  c.ck_rows_cap = n;
+}
+
+}  // namespace
+
+void check_rollout(Ctx& c, Key key, double eps) {
+  ensure_scratch(c, c.Bl);
+  switch (c.env.kind) {
+    case GFNX_ENV_HYPERGRID: rollout_impl<HypergridEnv>(c, key, eps); break;
+    case GFNX_ENV_BITSEQ: rollout_impl<BitseqEnv>(c, key, eps); break;
+    case GFNX_ENV_ISING: rollout_impl<IsingEnv>(c, key, eps); break;
+    case GFNX_ENV_DAG: rollout_impl<DagEnv>(c, key, eps); break;
+  }
+}
+
+// Computes loss + gradients into c.g64 / scalars[3]; the caller handles allreduce + Adam.
+void check_train(Ctx& c, bool /*apply*/, double /*lr*/, double* /*loss*/) {
+  const int obj = c.train.objective;
+  const int need_flow = obj == GFNX_OBJ_DB || obj == GFNX_OBJ_SUBTB;
+  const int R = (int)total_rows(c);
+  ensure_scratch(c, R);
+  const DevLayout D = make_dev_layout(c);
+  switch (c.env.kind) {
+    case GFNX_ENV_HYPERGRID: fwd_impl<HypergridEnv>(c, R, need_flow); break;
+    case GFNX_ENV_BITSEQ: fwd_impl<BitseqEnv>(c, R, need_flow); break;
+    case GFNX_ENV_ISING: fwd_impl<IsingEnv>(c, R, need_flow); break;
+    case GFNX_ENV_DAG: fwd_impl<DagEnv>(c, R, need_flow); break;
+  }
+  cudaMemsetAsync(c.ck_glogp, 0, sizeof(double) * (size_t)R * D.A, c.stream);
+  cudaMemsetAsync(c.ck_gflow, 0, sizeof(double) * (size_t)R, c.stream);
+  static thread_local double* lampow = nullptr;  // pow(lambda, k), k = 0..T (glibc pow)
+  static thread_local double* gpair = nullptr;
+  static thread_local int cap_T = 0;
+  const int T = c.shape.max_traj_len;
+  if (cap_T < T + 1) {
+    cudaFree(lampow);
+    cudaFree(gpair);
+    cuda_check(cudaMalloc(&lampow, sizeof(double) * (T + 1)), "lampow");
+    cuda_check(cudaMalloc(&gpair, sizeof(double) * ((size_t)(T + 1) * (T + 1) + 3 * (T + 1))), "gpair");
+    cap_T = T + 1;
+  }
+  std::vector<double> lp(T + 1);
+  for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);
+  cudaMemcpyAsync(lampow, lp.data(), sizeof(double) * (T + 1), cudaMemcpyHostToDevice, c.stream);
+  // global normaliser counts live in counters[4..5] (all-reduced by the caller when world > 1)
+  k_check_loss<<<1, 1, 0, c.stream>>>(obj, D.A, T, c.B, c.train.terminal_penalty,
+                                      c.shape.stop_action, lampow, c.d_neglog, c.batch, c.Bl,
+                                      c.batch.counters + 4, c.ck_logp, c.ck_flow, c.ck_glogp,
+                                      c.ck_gflow, gpair, c.d_scalars, c.batch.counters + 3);
+  k_check_bwd<<<R, 256, 0, c.stream>>>(D, c.p64, R, need_flow, c.ck_act, c.ck_logp, c.ck_mask,
+                                       c.ck_glogp, c.ck_gflow, c.ck_gx, c.ck_gz);
+  cudaMemsetAsync(c.g64, 0, sizeof(double) * c.L.n_params, c.stream);
+  const int64_t n = c.L.n_params;
+  k_check_wgrad<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(
+      D, R, need_flow, c.ck_obs, c.ck_act, c.ck_gx, c.ck_gz, c.ck_gflow, c.g64);
+  c.launches += 3;
+}
+
+void check_adam(Ctx& c, double lr) {
+  const gfnx_train_desc& s = c.train;
+  c.adam_t += 1;
+  const double bc1 = 1.0 - pow(s.beta1, (double)c.adam_t);
+  const double bc2 = 1.0 - pow(s.beta2, (double)c.adam_t);
+  const int do_z = s.objective == GFNX_OBJ_TB;
+  double zbc1 = 1.0, zbc2 = 1.0;
+  if (do_z) {
+    c.z_t += 1;
+    zbc1 = 1.0 - pow(s.beta1, (double)c.z_t);
+    zbc2 = 1.0 - pow(s.beta2, (double)c.z_t);
+  }
+  const int64_t n = c.L.n_params;
+  k_check_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
+      c.p64, c.g64, c.m64, c.v64, n, lr, s.beta1, s.beta2, s.adam_eps, s.weight_decay, bc1, bc2,
+      c.d_scalars, do_z, s.z_lr, zbc1, zbc2);
+  c.launches++;
+}
+
+}  // namespace gfnx

@@ -1,0 +1,244 @@
+// common.cuh — shared device primitives for libgfnx (sm_100a only).
+//
+//  * Threefry-2x64-20, fold_in, uniform (proj/src/rng.cpp:19-66), bit-exact with the host.
+//  * PTX wrappers: mbarrier, TMEM alloc/ld/st, tcgen05.mma (kind::f16, cta_group::1),
+//    tcgen05.commit, async-proxy fences and 1-D bulk copies (TMA engine).
+//  * UMMA shared-memory / instruction descriptors for 128B-swizzled bf16 tiles.
+#pragma once
+
+#include <cuda_runtime.h>
+#if defined(__CUDACC__)
+#include <cuda_bf16.h>
+#endif
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libgfnx targets sm_100a only"
+#endif
+
+#define GFNX_DEV __device__ __forceinline__
+
+namespace gfnx {
+
+// ---------------------------------------------------------------------------
+// Threefry-2x64-20 (rng.cpp:19-34) — integer only, so device == host bit for bit.
+struct Key {
+  uint64_t hi, lo;
+};
+
+__host__ __device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) {
+  return (x << r) | (x >> (64 - r));
+}
+
+__host__ __device__ __forceinline__ void threefry2x64(Key k, uint64_t c0, uint64_t c1,
+                                                      uint64_t& o0, uint64_t& o1) {
+  const uint64_t ks0 = k.hi, ks1 = k.lo, ks2 = k.hi ^ k.lo ^ 0x1BD11BDAA9FC1A22ULL;
+  uint64_t x0 = c0 + ks0, x1 = c1 + ks1;
+  // 5 groups of 4 rounds, rotations {16,42,12,31},{16,32,24,21} alternate (kRot, rng.cpp:13)
+#define GFNX_TF_ROUND(r) \
+  x0 += x1;              \
+  x1 = rotl64(x1, r);    \
+  x1 ^= x0;
+  GFNX_TF_ROUND(16) GFNX_TF_ROUND(42) GFNX_TF_ROUND(12) GFNX_TF_ROUND(31)
+  x0 += ks1; x1 += ks2 + 1;
+  GFNX_TF_ROUND(16) GFNX_TF_ROUND(32) GFNX_TF_ROUND(24) GFNX_TF_ROUND(21)
+  x0 += ks2; x1 += ks0 + 2;
+  GFNX_TF_ROUND(16) GFNX_TF_ROUND(42) GFNX_TF_ROUND(12) GFNX_TF_ROUND(31)
+  x0 += ks0; x1 += ks1 + 3;
+  GFNX_TF_ROUND(16) GFNX_TF_ROUND(32) GFNX_TF_ROUND(24) GFNX_TF_ROUND(21)
+  x0 += ks1; x1 += ks2 + 4;
+  GFNX_TF_ROUND(16) GFNX_TF_ROUND(42) GFNX_TF_ROUND(12) GFNX_TF_ROUND(31)
+  x0 += ks2; x1 += ks0 + 5;
+#undef GFNX_TF_ROUND
+  o0 = x0;
+  o1 = x1;
+}
+
+__host__ __device__ __forceinline__ Key make_key(uint64_t seed) {  // rng.cpp:17
+  return Key{0x9E3779B97F4A7C15ULL, seed};
+}
+
+__host__ __device__ __forceinline__ Key fold_in(Key k, uint64_t idx) {  // rng.cpp:36-39
+  Key o;
+  threefry2x64(k, idx, 0x3C6EF372FE94F82BULL, o.hi, o.lo);
+  return o;
+}
+
+__host__ __device__ __forceinline__ double to_unit(uint64_t w) {  // rng.cpp:47-50
+  return (double)(w >> 11) * 0x1.0p-53;
+}
+
+__host__ __device__ __forceinline__ double uniform_scalar(Key k) {  // rng.cpp:64-66
+  uint64_t a, b;
+  threefry2x64(k, 0, 0, a, b);
+  return to_unit(a);
+}
+
+#if defined(__CUDACC__)
+// ---------------------------------------------------------------------------
+// Small helpers
+GFNX_DEV uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+GFNX_DEV uint32_t lane_id() { return threadIdx.x & 31; }
+
+GFNX_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+GFNX_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+GFNX_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+
+// ---------------------------------------------------------------------------
+// mbarrier
+GFNX_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+GFNX_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+GFNX_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+
+GFNX_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+// 1-D bulk copy global -> shared through the TMA engine (SASS: UBLKCP), completes on bar.
+GFNX_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 1-D bulk copy shared -> global (bulk_group completion).
+GFNX_DEV void bulk_s2g(void* dst_gmem, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst_gmem),
+               "r"(smem_u32(src_smem)), "r"(bytes)
+               : "memory");
+}
+GFNX_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+GFNX_DEV void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+GFNX_DEV void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+// generic-proxy smem writes -> visible to the async proxy (UMMA operand reads, bulk copies)
+GFNX_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// TMEM
+template <uint32_t kCols>
+GFNX_DEV void tmem_alloc(uint32_t* dst_smem) {  // whole warp
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)),
+               "n"(kCols));
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+}
+template <uint32_t kCols>
+GFNX_DEV void tmem_dealloc(uint32_t taddr) {  // same warp that allocated
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols));
+}
+GFNX_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+GFNX_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// 32 lanes x 32 consecutive fp32 columns; thread i of the warp gets lane (base_lane + i).
+GFNX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+GFNX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+      "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31]));
+}
+GFNX_DEV void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+GFNX_DEV void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// ---------------------------------------------------------------------------
+// UMMA (tcgen05.mma kind::f16, bf16 x bf16 -> fp32, single CTA)
+//
+// Operand tiles use the canonical 128B-swizzled layouts (cute mma_sm100_desc.hpp):
+//   K-major : rows of 64 bf16 (128 B), 8-row groups of 1024 B (SBO = 1024), XOR swizzle of
+//             the 16-byte chunk index with (row & 7). A 64-wide K block of an R-row tile
+//             is R*128 bytes; the next K block follows.
+//   MN-major: the same bytes read transposed: 64 MN-contiguous elements per 128 B row,
+//             8 K-rows per 1024 B atom (SBO = 1024), next 64-wide MN block at LBO.
+// Our activation "tile image" (rows x features, 64-feature blocks of rows*128 B) is thus
+// the K-major A operand of the forward GEMM AND the MN-major operand of the weight
+// gradient GEMM, with no transposition.
+GFNX_DEV uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+#endif  // __CUDACC__
+
+__host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N, bool a_mn,
+                                                       bool b_mn) {
+  return (1u << 4)                   // D fp32
+         | (1u << 7)                 // A bf16
+         | (1u << 10)                // B bf16
+         | ((a_mn ? 1u : 0u) << 15)  // A major
+         | ((b_mn ? 1u : 0u) << 16)  // B major
+         | ((N >> 3) << 17) | ((M >> 4) << 24);
+}
+
+#if defined(__CUDACC__)
+GFNX_DEV void umma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                        uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+GFNX_DEV void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+#endif  // __CUDACC__
+
+// Byte offset of element (row, col) in a 128B-swizzled bf16 tile image with `rows` rows.
+__host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col,
+                                                          uint32_t rows) {
+  const uint32_t blk = col >> 6, c = col & 63;
+  const uint32_t chunk = (c >> 3) ^ (row & 7);
+  return blk * rows * 128u + row * 128u + chunk * 16u + (c & 7) * 2u;
+}
+
+}  // namespace gfnx

@@ -1,0 +1,138 @@
+// engine.h — host-side engine context shared by the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/gfnx.h"
+#include "envs.cuh"
+
+namespace gfnx {
+
+// Layout of the flat parameter vector in MlpParams::tensors() order (nn.cpp:8-19).
+struct MlpLayout {
+  int n_trunk = 0;
+  int dims[10] = {0};  // dims[0] = obs_dim, dims[l+1] = hidden width of trunk layer l
+  int64_t off_w[10] = {0}, off_b[10] = {0};
+  int64_t off_fw = 0, off_fb = 0, off_bw = 0, off_bb = 0, off_flw = 0, off_flb = 0;
+  int64_t n_params = 0;
+  int H() const { return dims[n_trunk]; }
+};
+
+// Device-resident trajectory batch of this rank's slice (compact SoA, not the padded
+// B*(T+1)*obs_dim fp64 TrajectoryBatch of trajectory.hpp:15-33).
+struct DeviceBatch {
+  int32_t* lengths = nullptr;     // [Bl]
+  int16_t* actions = nullptr;     // [Bl * T], -1 pad
+  double* log_rewards = nullptr;  // [Bl]
+  double* delta = nullptr;        // [Bl * T] (MDB)
+  uint16_t* nparents = nullptr;   // [Bl * T] #legal backward actions at s_{t+1} (log_pb = -log n)
+  uint32_t* term_state = nullptr; // [Bl * SW]
+  int32_t* row0 = nullptr;        // [Bl + 1] exclusive prefix of lengths
+  int32_t* counters = nullptr;    // [4]: total rows, mdb rows, work counter, error word
+};
+
+struct Ctx;
+
+// check-mode (fp64 SIMT, reference operation order) — check.cu
+void check_rollout(Ctx& c, Key key, double eps);
+void check_train(Ctx& c, bool apply, double lr, double* loss);
+void check_adam(Ctx& c, double lr);
+
+// fast mode (bf16 tcgen05) — fast.cu
+void fast_init(Ctx& c);
+void fast_free(Ctx& c);
+void fast_rollout(Ctx& c, Key key, double eps);
+void fast_train(Ctx& c, bool apply, double lr, double* loss);  // gradients -> g32, scalars
+void fast_adam(Ctx& c, double lr);
+void fast_sync_weights(Ctx& c);  // fp32 master -> bf16 operand images
+
+// shared small kernels — batch.cu
+void launch_row_scan(Ctx& c);
+
+struct Ctx {
+  gfnx_env_desc env{};
+  gfnx_train_desc train{};
+  gfnx_env_shape shape{};
+  EnvParams P{};
+  MlpLayout L{};
+  int device = 0, rank = 0, world = 1;
+  int B = 0, Bl = 0, b0 = 0;  // global batch, local slice [b0, b0+Bl)
+  cudaStream_t stream = nullptr;
+  void* nccl = nullptr;  // ncclComm_t
+  std::string err;
+  int64_t launches = 0;
+
+  // environment tables (device)
+  uint64_t* d_modes = nullptr;
+  double* d_bs_logr = nullptr;
+  int16_t* d_is_nbr = nullptr;
+  double* d_is_J = nullptr;
+  double* d_dag_cache = nullptr;
+  double* d_neglog = nullptr;
+  std::vector<double> h_dag_cache;
+
+  // parameters: fp64 master (check mode) or fp32 master (fast mode)
+  double* p64 = nullptr;
+  double* g64 = nullptr;
+  double* m64 = nullptr;
+  double* v64 = nullptr;
+  float* p32 = nullptr;
+  float* g32 = nullptr;
+  float* m32 = nullptr;
+  float* v32 = nullptr;
+  double* d_scalars = nullptr;  // [8]: log_z, z_m, z_v, dlogz, loss, norm, ...
+  int64_t adam_t = 0, z_t = 0;
+
+  DeviceBatch batch;
+  bool has_batch = false;
+  bool has_grads = false;
+
+  // check-mode scratch
+  double* ck_obs = nullptr;
+  double* ck_act = nullptr;
+  double* ck_logp = nullptr;
+  uint8_t* ck_mask = nullptr;
+  double* ck_flow = nullptr;
+  double* ck_glogp = nullptr;
+  double* ck_gflow = nullptr;
+  double* ck_gz = nullptr;
+  double* ck_gx = nullptr;
+  double* ck_pair = nullptr;
+  int64_t ck_rows_cap = 0;
+
+  // fast-mode state (opaque, fast.cu)
+  void* fast = nullptr;
+
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t user_ev[16] = {};
+  // per-kernel CUDA-event profiling (bench.py roofline): records (name, start, stop)
+  struct ProfRec {
+    const char* name;
+    cudaEvent_t a, b;
+  };
+  bool profiling = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> ev_pool;
+  double last_rollout_ms = 0.0, last_train_ms = 0.0;
+
+  bool check_mode() const { return train.precision == GFNX_PREC_FP64_CHECK; }
+};
+
+// RAII bracket of one kernel launch with CUDA events on the ctx stream (when profiling)
+struct ProfScope {
+  Ctx& c;
+  int idx = -1;
+  ProfScope(Ctx& ctx, const char* name);
+  ~ProfScope();
+};
+
+// error reporting from kernel TUs
+void cuda_check(cudaError_t e, const char* what);
+[[noreturn]] void raise_error(int code, const std::string& msg);
+int64_t total_rows(Ctx& c);  // reads counters[0] (sync)
+
+}  // namespace gfnx

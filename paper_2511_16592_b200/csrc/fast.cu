@@ -1,0 +1,1346 @@
+// fast.cu — the bf16 tcgen05 fast path (sm_100a).
+//
+// One training iteration = 7 launches on one stream, no host synchronisation:
+//   k_fast_rollout  persistent fused rollout: per 128-slot tile and env step, the layer-1
+//                   pre-activation is updated incrementally in TMEM (only the features the
+//                   last action changed), ReLU'd to a bf16 tile in smem, multiplied by the
+//                   smem-resident hidden weight image on the tensor cores (tcgen05.mma,
+//                   fp32 accumulator in TMEM), then the head, epsilon-uniform masked
+//                   categorical (Threefry stream of the reference) and env step run per
+//                   thread. Finished slots pull the next trajectory from a global counter,
+//                   so geometric trajectory lengths do not idle the tile.
+//                   (forward_rollout env_core.hpp:232-274 + rollout_from_actions :166-229)
+//   k_fast_fwd      training forward over the Sum_b L_b real rows only (not B*(T+1) padded
+//                   rows), layer-2 on tcgen05; stores bf16 activation tile images + per-row
+//                   head statistics (mlp_forward_tape nn.cpp:91-126, masked_log_softmax
+//                   tape.cpp:177-213)
+//   k_fast_loss     TB/DB/SubTB/MDB residuals and their analytic backward per trajectory
+//                   (objectives.cpp:94-226), deterministic block partials
+//   k_fast_bwd      head backward (SIMT), dgrad GEMM on tcgen05, ReLU masks, bias grads
+//   k_fast_wgrad    weight gradients as tcgen05 GEMMs whose K dimension is the row count:
+//                   the activation tile images are read MN-major straight from HBM
+//   k_reduce        fixed-order reduction of per-CTA partial gradients (deterministic)
+//   k_fast_adam     fused Adam over the flat fp32 parameters + logZ, re-emitting the bf16
+//                   operand images (adam_step optim.cpp:19-43)
+#include <math.h>
+
+#include <vector>
+
+#include "engine.h"
+
+namespace gfnx {
+
+namespace {
+
+constexpr int kTile = 128;  // rows (trajectory slots) per CTA tile = TMEM lanes
+constexpr int kHeadMax = 32;
+
+struct FastState {
+  int num_sms = 0;
+  int H = 0, A = 0, O = 0, Opad = 0;
+  int64_t max_rows = 0, max_tiles = 0;
+  __nv_bfloat16* w1 = nullptr;        // [O][H] row-major (layer-1 gathers)
+  __nv_bfloat16* w2_fwd = nullptr;    // image [H out][H in] K-major
+  __nv_bfloat16* w2_dgrad = nullptr;  // image [H in][H out] K-major
+  uint32_t* stst = nullptr;           // [Bl*T][SW] state before each step
+  __nv_bfloat16 *h1 = nullptr, *h2 = nullptr, *dz1 = nullptr, *dz2 = nullptr;  // tile images
+  __nv_bfloat16* dhead = nullptr;     // tile images [tiles][128][64]
+  float* rowbuf = nullptr;            // per row: probs[A], lpa, lps, flow, pad
+  float* coef = nullptr;              // per row: ga, gs, gflow, pad
+  float* wpart = nullptr;             // [num_sms][n_params] partial gradients
+  double* lpart = nullptr;            // [blocks][2] loss / dlogz partials
+  double* lampow = nullptr;           // pow(lambda, k)
+  int32_t* work = nullptr;            // rollout work counter
+  int rs = 0;                         // rowbuf stride (floats)
+  int loss_blocks = 0;
+};
+
+FastState& FS(Ctx& c) { return *static_cast<FastState*>(c.fast); }
+
+struct Weights {
+  const __nv_bfloat16* w1;
+  const float* b1;
+  const __nv_bfloat16* w2_fwd;
+  const __nv_bfloat16* w2_dgrad;
+  const float* b2;
+  const float* wf;   // [H][A]
+  const float* bf;   // [A]
+  const float* wfl;  // [H]
+  const float* bfl;  // [1]
+};
+
+Weights weights_of(Ctx& c) {
+  FastState& f = FS(c);
+  const MlpLayout& L = c.L;
+  Weights w;
+  w.w1 = f.w1;
+  w.b1 = c.p32 + L.off_b[0];
+  w.w2_fwd = f.w2_fwd;
+  w.w2_dgrad = f.w2_dgrad;
+  w.b2 = c.p32 + L.off_b[1];
+  w.wf = c.p32 + L.off_fw;
+  w.bf = c.p32 + L.off_fb;
+  w.wfl = c.p32 + L.off_flw;
+  w.bfl = c.p32 + L.off_flb;
+  return w;
+}
+
+// ---------------------------------------------------------------------------
+// tensor-core helpers (single elected thread issues, accumulator in TMEM)
+
+// D[128 x N] (+)= A[128 x K] * B[N x K]^T, both K-major 128B-swizzled tile images in smem.
+template <int N, int K>
+GFNX_DEV void mma_kk(uint32_t d_tmem, const void* a_img, const void* b_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s) {
+    const uint32_t ao = a0 + (s >> 2) * (128 * 128) + (s & 3) * 32;
+    const uint32_t bo = b0 + (s >> 2) * (N * 128) + (s & 3) * 32;
+    umma_bf16(d_tmem, umma_desc_sw128(ao, 16, 1024), umma_desc_sw128(bo, 16, 1024), idesc,
+              (acc || s > 0) ? 1u : 0u);
+  }
+}
+
+// D[128 x N] (+)= A'[128 x 128] * B'[N x 128]^T with A' = act^T, B' = dz^T read MN-major
+// from 128-row tile images: a_img holds features [m0, m0+128) of a tile with 128 rows.
+template <int N>
+GFNX_DEV void mma_mn(uint32_t d_tmem, const void* a_img, int m0, const void* b_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+  const uint32_t a0 = smem_u32(a_img) + (m0 >> 6) * (128 * 128), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < kTile / 16; ++s) {
+    const uint32_t ao = a0 + s * 2048, bo = b0 + s * 2048;
+    umma_bf16(d_tmem, umma_desc_sw128(ao, 128 * 128, 1024), umma_desc_sw128(bo, 128 * 128, 1024),
+              idesc, (acc || s > 0) ? 1u : 0u);
+  }
+}
+
+// store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
+GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+    *reinterpret_cast<uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile)) = v;
+  }
+}
+GFNX_DEV void ld_row32(const uint8_t* img, int row, int c0, float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 q = *reinterpret_cast<const uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile));
+    v[8 * c + 0] = bf16_lo(q.x); v[8 * c + 1] = bf16_hi(q.x);
+    v[8 * c + 2] = bf16_lo(q.y); v[8 * c + 3] = bf16_hi(q.y);
+    v[8 * c + 4] = bf16_lo(q.z); v[8 * c + 5] = bf16_hi(q.z);
+    v[8 * c + 6] = bf16_lo(q.w); v[8 * c + 7] = bf16_hi(q.w);
+  }
+}
+
+GFNX_DEV void bulk_g2s_big(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  for (uint32_t off = 0; off < bytes; off += 32768) {
+    const uint32_t n = bytes - off < 32768 ? bytes - off : 32768;
+    bulk_g2s((uint8_t*)dst + off, (const uint8_t*)src + off, n, bar);
+  }
+}
+
+__device__ int find_traj(const int32_t* row0, int Bl, int r) {
+  int lo = 0, hi = Bl;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (row0[mid] <= r) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+// reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100)
+// in fp64 on the fp32 logits of one row
+template <class Env, int AMAX>
+GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const float (&logit)[AMAX],
+                        int A, double eps, double u01, bool* bad) {
+  int legal = 0;
+  double hi = -INFINITY;
+  for (int c = 0; c < A; ++c)
+    if (Env::legal(P, s, c)) {
+      ++legal;
+      hi = fmax(hi, (double)logit[c]);
+    }
+  if (legal == 0 || !isfinite(hi)) {
+    *bad = true;
+    return -1;
+  }
+  double w[AMAX];
+  double z = 0.0;
+  for (int c = 0; c < A; ++c) {
+    w[c] = Env::legal(P, s, c) ? exp((double)logit[c] - hi) : 0.0;
+    z += w[c];
+  }
+  const double u = eps / legal;
+  double total = 0.0;
+  for (int c = 0; c < A; ++c) {
+    if (w[c] > 0.0 || Env::legal(P, s, c)) w[c] = (1.0 - eps) * w[c] / z + u;
+    total += w[c];
+  }
+  const double x = u01 * total;
+  double acc = 0.0;
+  for (int c = 0; c < A; ++c) {
+    acc += w[c];
+    if (x < acc) return c;
+  }
+  for (int c = A - 1; c >= 0; --c)
+    if (w[c] > 0.0) return c;
+  return A - 1;
+}
+
+// ---------------------------------------------------------------------------
+// k_fast_rollout
+
+struct RolloutArgs {
+  EnvParams P;
+  Weights W;
+  Key key;
+  double eps;
+  int b0, Bl;
+  DeviceBatch batch;
+  uint32_t* stst;
+  int32_t* work;
+};
+
+template <int H>
+constexpr int rollout_smem_bytes(int T) {
+  return H * H * 2 + kTile * H * 2 + 3 * H * 4 + 16 * 128 + 64 + 1024;
+}
+
+template <class Env, int H, int AMAX>
+__global__ void __launch_bounds__(kTile, 1) k_fast_rollout(RolloutArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* w2img = smem;                       // H x H bf16
+  uint8_t* atile = w2img + H * H * 2;          // 128 x H bf16
+  float* h1init = (float*)(atile + kTile * H * 2);
+  float* b2s = h1init + H;
+  float* b1s = b2s + H;
+  Key* skeys = (Key*)(b1s + H);                // up to 128 step keys
+  uint64_t* mbar = (uint64_t*)(skeys + 128);
+  uint32_t* tbase = (uint32_t*)(mbar + 1);
+
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = P.T, A = P.A;
+  if (warp == 0) tmem_alloc<2 * H>(tbase);
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(mbar, H * H * 2);
+    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, mbar);
+  }
+  for (int t = tid; t < T && t < 128; t += blockDim.x) skeys[t] = fold_in(a.key, (uint64_t)t);
+  for (int j = tid; j < H; j += blockDim.x) {
+    b2s[j] = a.W.b2[j];
+    b1s[j] = a.W.b1[j];
+  }
+  __syncthreads();
+  {  // h1init = b1 + x(s0) W1  (layer-1 pre-activation of the initial state)
+    typename Env::State s0;
+    Env::reset(P, s0);
+    for (int j = tid; j < H; j += blockDim.x) {
+      float v = b1s[j];
+      Env::features(P, s0, [&](int f, double x) { v += (float)x * __bfloat162float(a.W.w1[(size_t)f * H + j]); });
+      h1init[j] = v;
+    }
+  }
+  mbar_wait(mbar, 0);
+  uint32_t phase = 1;
+  tc_fence_after();
+  __syncthreads();
+  const uint32_t tmem = *tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+
+  typename Env::State s;
+  int b = atomicAdd(a.work, 1);
+  bool active = b < a.Bl;
+  Env::reset(P, s);
+  int tstep = 0;
+  bool need_init = true;
+  int nd = 0;
+  int df[4];
+  float dv[4];
+  bool bad = false;
+  while (__syncthreads_or(active)) {
+    // (1) layer-1 pre-activation (fp32, TMEM columns [H, 2H)) and its bf16 ReLU tile
+#pragma unroll 1
+    for (int q = 0; q < H / 32; ++q) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + H + q * 32, r);  // warp-collective: executed by every lane
+      tmem_wait_ld();
+      if (need_init) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(h1init[q * 32 + i]);
+      } else {
+        for (int d = 0; d < nd; ++d) {
+          const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)df[d] * H + q * 32);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 w = __ldg(wr + c);
+            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv[d] * bf16_lo(wv[e]));
+              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv[d] * bf16_hi(wv[e]));
+            }
+          }
+        }
+      }
+      tmem_st32(lane_base + H + q * 32, r);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
+      st_row32(atile, tid, q * 32, pk);
+    }
+    tmem_wait_st();
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    // (2) hidden layer on the tensor cores
+    if (tid == 0) {
+      tc_fence_after();
+      mma_kk<H, H>(tmem, atile, w2img, false);
+      umma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    // (3) epilogue: h2 = ReLU(acc + b2) -> head logits (SIMT, A <= AMAX)
+    float logit[AMAX];
+#pragma unroll
+    for (int c = 0; c < AMAX; ++c) logit[c] = c < A ? __ldg(a.W.bf + c) : 0.f;
+#pragma unroll 1
+    for (int q = 0; q < H / 32; ++q) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + q * 32, r);
+      tmem_wait_ld();
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i) {
+        const float h = __bfloat162float(__float2bfloat16(fmaxf(__uint_as_float(r[i]) + b2s[q * 32 + i], 0.f)));
+        const float* wr = a.W.wf + (size_t)(q * 32 + i) * A;
+#pragma unroll
+        for (int c = 0; c < AMAX; ++c)
+          if (c < A) logit[c] += h * __ldg(wr + c);
+      }
+    }
+    tc_fence_before();
+    // (4) sample, step, record; refill finished slots
+    if (active) {
+      const Key dk = fold_in(skeys[tstep], (uint64_t)(a.b0 + b));
+      const int act = sample_row<Env, AMAX>(P, s, logit, A, a.eps, uniform_scalar(dk), &bad);
+      if (act < 0) {
+        active = false;
+      } else {
+        const size_t bt = (size_t)b * T + tstep;
+        Env::pack(P, s, a.stst + bt * P.SW);
+        nd = 0;
+        Env::delta_features(P, s, act, [&](int f, float v) { df[nd] = f; dv[nd] = v; ++nd; });
+        const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
+        const bool term = Env::step(P, s, act);
+        a.batch.actions[bt] = (int16_t)act;
+        a.batch.nparents[bt] = (uint16_t)Env::num_parents(P, s);
+        if (P.mdb && !term) a.batch.delta[bt] = Env::log_reward(P, s) - prev_r;
+        ++tstep;
+        need_init = false;
+        if (term) {
+          a.batch.lengths[b] = tstep;
+          a.batch.log_rewards[b] = Env::log_reward(P, s);
+          Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
+          b = atomicAdd(a.work, 1);
+          active = b < a.Bl;
+          Env::reset(P, s);
+          tstep = 0;
+          need_init = true;
+        } else if (tstep >= T) {
+          bad = true;
+          active = false;
+        }
+      }
+    }
+  }
+  if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<2 * H>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// k_fast_fwd: forward over real rows
+
+struct TrainArgs {
+  EnvParams P;
+  Weights W;
+  DeviceBatch batch;
+  int Bl;
+  const uint32_t* stst;
+  __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
+  float* rowbuf;
+  int rs;
+  float* coef;
+  float* wpart;
+  int64_t n_params;
+  MlpLayout L;
+  int objective;
+};
+
+template <int H>
+constexpr int fwd_smem_bytes() {
+  return H * H * 2 + kTile * H * 2 + 2 * H * 4 + 64 + 1024;
+}
+
+template <class Env, int H, int AMAX>
+__global__ void __launch_bounds__(kTile, 1) k_fast_fwd(TrainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* w2img = smem;
+  uint8_t* atile = w2img + H * H * 2;
+  float* b1s = (float*)(atile + kTile * H * 2);
+  float* b2s = b1s + H;
+  uint64_t* mbar = (uint64_t*)(b2s + H);
+  uint32_t* tbase = (uint32_t*)(mbar + 1);
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = P.T, A = P.A;
+  const int R = a.batch.counters[0];
+  const int tiles = (R + kTile - 1) / kTile;
+  if ((int)blockIdx.x >= tiles) return;
+  if (warp == 0) tmem_alloc<H>(tbase);
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(mbar, H * H * 2);
+    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, mbar);
+  }
+  for (int j = tid; j < H; j += blockDim.x) {
+    b1s[j] = a.W.b1[j];
+    b2s[j] = a.W.b2[j];
+  }
+  mbar_wait(mbar, 0);
+  uint32_t phase = 1;
+  tc_fence_after();
+  __syncthreads();
+  const uint32_t tmem = *tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
+  for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int r = tile * kTile + tid;
+    const bool valid = r < R;
+    typename Env::State s;
+    Env::reset(P, s);
+    int act = 0;
+    if (valid) {
+      const int b = find_traj(a.batch.row0, a.Bl, r);
+      const int t = r - a.batch.row0[b];
+      const size_t bt = (size_t)b * T + t;
+      Env::unpack(P, a.stst + bt * P.SW, s);
+      act = a.batch.actions[bt];
+    }
+    // layer 1 (sparse one-hot gather, fp32) -> bf16 ReLU tile
+    if (tid == 0) bulk_wait_read0();  // previous tile's h2 store has left smem
+    __syncthreads();
+#pragma unroll 1
+    for (int q = 0; q < H / 32; ++q) {
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = b1s[q * 32 + i];
+      Env::features(P, s, [&](int f, double x) {
+        const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)f * H + q * 32);
+        const float xf = (float)x;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint4 w = __ldg(wr + c);
+          const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            v[8 * c + 2 * e] += xf * bf16_lo(wv[e]);
+            v[8 * c + 2 * e + 1] += xf * bf16_hi(wv[e]);
+          }
+        }
+      });
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = valid ? pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f)) : 0u;
+      st_row32(atile, tid, q * 32, pk);
+    }
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      tc_fence_after();
+      bulk_s2g(a.h1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+      bulk_commit();
+      mma_kk<H, H>(tmem, atile, w2img, false);
+      umma_commit(mbar);
+    }
+    mbar_wait(mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    if (tid == 0) bulk_wait_read0();
+    __syncthreads();
+    // epilogue: h2 (bf16-rounded) -> tile; head logits + flow from the rounded values
+    float logit[AMAX];
+#pragma unroll
+    for (int c = 0; c < AMAX; ++c) logit[c] = c < A ? __ldg(a.W.bf + c) : 0.f;
+    float fl = __ldg(a.W.bfl);
+#pragma unroll 1
+    for (int q = 0; q < H / 32; ++q) {
+      uint32_t r32[32];
+      tmem_ld32(lane_base + q * 32, r32);
+      tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float x0 = fmaxf(__uint_as_float(r32[2 * i]) + b2s[q * 32 + 2 * i], 0.f);
+        const float x1 = fmaxf(__uint_as_float(r32[2 * i + 1]) + b2s[q * 32 + 2 * i + 1], 0.f);
+        pk[i] = valid ? pack_bf16x2(x0, x1) : 0u;
+      }
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i) {
+        const float h = (i & 1) ? bf16_hi(pk[i >> 1]) : bf16_lo(pk[i >> 1]);
+        const float* wr = a.W.wf + (size_t)(q * 32 + i) * A;
+#pragma unroll
+        for (int c = 0; c < AMAX; ++c)
+          if (c < A) logit[c] += h * __ldg(wr + c);
+        if (flow) fl += h * __ldg(a.W.wfl + q * 32 + i);
+      }
+      st_row32(atile, tid, q * 32, pk);
+    }
+    tc_fence_before();
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      bulk_s2g(a.h2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+      bulk_commit();
+    }
+    if (valid) {  // masked log-softmax statistics of the row
+      float hi = -INFINITY;
+      for (int c = 0; c < A; ++c)
+        if (Env::legal(P, s, c)) hi = fmaxf(hi, logit[c]);
+      float z = 0.f;
+      for (int c = 0; c < A; ++c)
+        if (Env::legal(P, s, c)) z += __expf(logit[c] - hi);
+      const float lse = hi + __logf(z);
+      float* out = a.rowbuf + (size_t)r * a.rs;
+      for (int c = 0; c < A; ++c) out[c] = Env::legal(P, s, c) ? __expf(logit[c] - lse) : 0.f;
+      out[A] = logit[act] - lse;
+      out[A + 1] = P.stop >= 0 ? logit[P.stop] - lse : 0.f;
+      out[A + 2] = fl;
+      if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
+    }
+  }
+  if (tid == 0) bulk_wait0();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<H>(tmem);
+}
+
+// ---------------------------------------------------------------------------
+// k_fast_loss: one thread per trajectory
+
+struct LossArgs {
+  DeviceBatch batch;
+  int Bl, T, A, stop, objective, B_global;
+  double terminal_penalty;
+  const double* lampow;
+  const double* neglog;
+  const float* rowbuf;
+  int rs;
+  float* coef;
+  double* lpart;
+  const double* scalars;
+};
+
+__global__ void k_fast_loss(LossArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  double loss = 0.0, dlogz = 0.0;
+  if (b < a.Bl) {
+    const int L = a.batch.lengths[b];
+    const int r0 = a.batch.row0[b];
+    const uint16_t* np = a.batch.nparents + (size_t)b * a.T;
+    const double logr = a.batch.log_rewards[b];
+    const int* cnt = a.batch.counters;
+    double norm = (double)a.B_global;
+    if (a.objective == GFNX_OBJ_DB) norm = (double)cnt[4];
+    if (a.objective == GFNX_OBJ_MDB) norm = (double)cnt[5];
+    auto lpa = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A]; };
+    auto lps = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A + 1]; };
+    auto flw = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A + 2]; };
+    auto C = [&](int t) { return a.coef + (size_t)(r0 + t) * 4; };
+    for (int t = 0; t < L; ++t) {
+      float* c = C(t);
+      c[0] = c[1] = c[2] = 0.f;
+    }
+    if (a.objective == GFNX_OBJ_TB) {  // tb_loss objectives.cpp:120-142
+      const double w = 1.0 / norm;
+      double cum = 0.0;
+      for (int t = 0; t < L; ++t) cum += lpa(t) - a.neglog[np[t]];
+      const double res = cum + a.scalars[0] - logr;
+      loss = res * res * w;
+      const double g = 2.0 * res * w;
+      dlogz = g;
+      for (int t = 0; t < L; ++t) C(t)[0] = (float)g;
+    } else if (a.objective == GFNX_OBJ_DB) {  // transition_loss :94-118
+      double gprev = 0.0;
+      for (int t = 0; t < L; ++t) {
+        const double d = lpa(t) - a.neglog[np[t]];
+        const double f1 = t + 1 < L ? flw(t + 1) : logr;
+        const double res = flw(t) - f1 + d;
+        const double w = (t == L - 1 ? a.terminal_penalty : 1.0) / norm;
+        loss += res * res * w;
+        const double g = 2.0 * res * w;
+        C(t)[0] = (float)g;
+        C(t)[2] = (float)(g - gprev);
+        gprev = g;
+      }
+    } else if (a.objective == GFNX_OBJ_SUBTB) {  // subtb_loss :144-180
+      constexpr int kMaxT = 256;
+      double cum[kMaxT + 1], F[kMaxT + 1], gF[kMaxT + 1], gc[kMaxT + 1];
+      cum[0] = 0.0;
+      for (int t = 0; t < L; ++t) {
+        cum[t + 1] = cum[t] + (lpa(t) - a.neglog[np[t]]);
+        F[t] = flw(t);
+      }
+      F[L] = logr;
+      double nrm = 0.0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) nrm += a.lampow[k - j];
+      for (int k = 0; k <= L; ++k) gF[k] = gc[k] = 0.0;
+      for (int j = 0; j < L; ++j)
+        for (int k = j + 1; k <= L; ++k) {
+          const double w = a.lampow[k - j] / nrm / norm;
+          const double res = (F[j] - F[k]) + (cum[k] - cum[j]);
+          loss += res * res * w;
+          const double g = 2.0 * res * w;
+          gF[j] += g;
+          gF[k] -= g;
+          gc[k] += g;
+          gc[j] -= g;
+        }
+      double acc = 0.0;
+      for (int c = L; c >= 0; --c) {
+        if (c < L) {
+          C(c)[0] = (float)acc;
+          C(c)[2] = (float)gF[c];
+        }
+        acc += gc[c];
+      }
+    } else if (a.objective == GFNX_OBJ_MDB) {  // mdb_loss :186-226
+      const double w = 1.0 / norm;
+      for (int t = 0; t + 1 < L; ++t) {
+        const double res = lpa(t) + (lps(t + 1) - lps(t)) - a.neglog[np[t]] -
+                           a.batch.delta[(size_t)b * a.T + t];
+        loss += res * res * w;
+        const double g = 2.0 * res * w;
+        C(t)[0] += (float)g;
+        C(t + 1)[1] += (float)g;
+        C(t)[1] -= (float)g;
+      }
+    }
+  }
+  // deterministic block reduction
+  __shared__ double red[2][256];
+  red[0][threadIdx.x] = loss;
+  red[1][threadIdx.x] = dlogz;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + off];
+      red[1][threadIdx.x] += red[1][threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.lpart[2 * blockIdx.x] = red[0][0];
+    a.lpart[2 * blockIdx.x + 1] = red[1][0];
+  }
+}
+
+__global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalars, int tb,
+                                int32_t* err) {
+  if (threadIdx.x != 0) return;
+  double l = 0.0, z = 0.0;
+  for (int i = 0; i < nblocks; ++i) {
+    l += lpart[2 * i];
+    z += lpart[2 * i + 1];
+  }
+  scalars[4] = l;
+  scalars[3] = tb ? z : 0.0;
+  if (!isfinite(l)) atomicExch(err, GFNX_ERR_NUMERIC);
+}
+
+// ---------------------------------------------------------------------------
+// k_fast_bwd: head backward, dgrad GEMM, ReLU masks, bias gradients
+
+template <int H>
+constexpr int bwd_smem_bytes() {
+  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + 64 + 1024;
+}
+
+template <class Env, int H, int AMAX>
+__global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* wdimg = smem;                     // W2 dgrad image [H in][H out]
+  uint8_t* atile = wdimg + H * H * 2;        // dz tile
+  uint8_t* htile = atile + kTile * H * 2;    // dhead tile [128][64]
+  uint64_t* mbar = (uint64_t*)(htile + kTile * 64 * 2);
+  uint32_t* tbase = (uint32_t*)(mbar + 1);
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = P.T, A = P.A;
+  const int R = a.batch.counters[0];
+  const int tiles = (R + kTile - 1) / kTile;
+  float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
+  // bias accumulators: thread j owns column j of db1/db2 (H <= 256 => 2 per thread at most)
+  float acc_b1[2] = {0.f, 0.f}, acc_b2[2] = {0.f, 0.f}, acc_bh = 0.f;
+  if ((int)blockIdx.x < tiles) {
+    if (warp == 0) tmem_alloc<H>(tbase);
+    if (tid == 0) {
+      mbar_init(mbar, 1);
+      fence_mbar_init();
+    }
+    __syncthreads();
+    if (tid == 0) {
+      mbar_arrive_expect_tx(mbar, H * H * 2);
+      bulk_g2s_big(wdimg, a.W.w2_dgrad, H * H * 2, mbar);
+    }
+    mbar_wait(mbar, 0);
+    uint32_t phase = 1;
+    tc_fence_after();
+    __syncthreads();
+    const uint32_t tmem = *tbase;
+    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
+    for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+      const int r = tile * kTile + tid;
+      const bool valid = r < R;
+      typename Env::State s;
+      Env::reset(P, s);
+      int act = 0;
+      float g_a = 0.f, g_s = 0.f, g_f = 0.f;
+      if (valid) {
+        const int b = find_traj(a.batch.row0, a.Bl, r);
+        const int t = r - a.batch.row0[b];
+        const size_t bt = (size_t)b * T + t;
+        Env::unpack(P, a.stst + bt * P.SW, s);
+        act = a.batch.actions[bt];
+        g_a = a.coef[(size_t)r * 4 + 0];
+        g_s = a.coef[(size_t)r * 4 + 1];
+        g_f = flow ? a.coef[(size_t)r * 4 + 2] : 0.f;
+      }
+      // dlogits (masked log-softmax backward, tape.cpp:413-434): g_c - p_c * sum(g)
+      float dl[AMAX];
+      const float gsum = g_a + g_s;
+      const float* pr = a.rowbuf + (size_t)r * a.rs;
+#pragma unroll
+      for (int c = 0; c < AMAX; ++c) {
+        float v = 0.f;
+        if (valid && c < A) {
+          v = -pr[c] * gsum;
+          if (c == act) v += g_a;
+          if (c == P.stop) v += g_s;
+          if (!Env::legal(P, s, c)) v = 0.f;
+        }
+        dl[c] = v;
+      }
+      if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
+      __syncthreads();
+      {  // dhead row -> tile (cols [0, A) logits, col A flow)
+        uint32_t pk[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int c0 = 2 * i, c1 = 2 * i + 1;
+          const float x0 = c0 < A ? dl[c0 < AMAX ? c0 : 0] : (c0 == A ? g_f : 0.f);
+          const float x1 = c1 < A ? dl[c1 < AMAX ? c1 : 0] : (c1 == A ? g_f : 0.f);
+          pk[i] = pack_bf16x2(x0, x1);
+        }
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          lo[i] = pk[i];
+          hi[i] = pk[16 + i];
+        }
+        st_row32(htile, tid, 0, lo);
+        st_row32(htile, tid, 32, hi);
+      }
+      // dh2 = dlogits Wf^T + dflow Wfl^T, masked by h2 > 0 (h2 from its tile image)
+      const uint8_t* h2img = (const uint8_t*)(a.h2 + (size_t)tile * kTile * H);
+#pragma unroll 1
+      for (int q = 0; q < H / 32; ++q) {
+        float hv[32];
+        ld_row32(h2img, tid, q * 32, hv);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          float d2[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = q * 32 + i + e;
+            float v = flow ? g_f * __ldg(a.W.wfl + j) : 0.f;
+            const float* wr = a.W.wf + (size_t)j * A;
+#pragma unroll
+            for (int c = 0; c < AMAX; ++c)
+              if (c < A) v += dl[c] * __ldg(wr + c);
+            d2[e] = hv[i + e] > 0.f ? v : 0.f;
+          }
+          pk[i >> 1] = pack_bf16x2(d2[0], d2[1]);
+        }
+        st_row32(atile, tid, q * 32, pk);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        tc_fence_after();
+        bulk_s2g(a.dz2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+        bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
+        bulk_commit();
+        mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
+        umma_commit(mbar);
+      }
+      // bias sums of this tile (fixed order over the 128 rows => deterministic)
+      for (int k = 0; k < 2; ++k) {
+        const int j = tid + k * kTile;
+        if (j < H) {
+          float sacc = 0.f;
+          for (int row = 0; row < kTile; ++row)
+            sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(row, j, kTile)));
+          acc_b2[k] += sacc;
+        }
+      }
+      if (tid <= A && tid < 64) {
+        float sacc = 0.f;
+        for (int row = 0; row < kTile; ++row)
+          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(row, tid, kTile)));
+        acc_bh += sacc;
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1;
+      tc_fence_after();
+      if (tid == 0) bulk_wait_read0();
+      __syncthreads();
+      const uint8_t* h1img = (const uint8_t*)(a.h1 + (size_t)tile * kTile * H);
+#pragma unroll 1
+      for (int q = 0; q < H / 32; ++q) {
+        uint32_t r32[32];
+        tmem_ld32(lane_base + q * 32, r32);
+        tmem_wait_ld();
+        float hv[32];
+        ld_row32(h1img, tid, q * 32, hv);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(hv[2 * i] > 0.f ? __uint_as_float(r32[2 * i]) : 0.f,
+                              hv[2 * i + 1] > 0.f ? __uint_as_float(r32[2 * i + 1]) : 0.f);
+        st_row32(atile, tid, q * 32, pk);
+      }
+      tc_fence_before();
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {
+        bulk_s2g(a.dz1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+        bulk_commit();
+      }
+      for (int k = 0; k < 2; ++k) {
+        const int j = tid + k * kTile;
+        if (j < H) {
+          float sacc = 0.f;
+          for (int row = 0; row < kTile; ++row)
+            sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(row, j, kTile)));
+          acc_b1[k] += sacc;
+        }
+      }
+    }
+    if (tid == 0) bulk_wait0();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc<H>(tmem);
+  }
+  // bias partials of this CTA (every CTA writes its slots, zeros when it had no tile)
+  for (int k = 0; k < 2; ++k) {
+    const int j = tid + k * kTile;
+    if (j < H) {
+      part[a.L.off_b[0] + j] = acc_b1[k];
+      part[a.L.off_b[1] + j] = acc_b2[k];
+    }
+  }
+  if (tid < A) part[a.L.off_fb + tid] = acc_bh;
+  if (tid == A) part[a.L.off_flb] = acc_bh;
+}
+
+// ---------------------------------------------------------------------------
+// k_fast_wgrad: dW2 = h1^T dz2, dW1 = obs^T dz1, dWhead = h2^T dhead  (K = rows)
+
+template <int H>
+constexpr int wgrad_smem_bytes() {
+  return 2 * kTile * H * 2 + 64 + 1024;
+}
+
+template <class Env, int H>
+__global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* bufA = smem;
+  uint8_t* bufB = bufA + kTile * H * 2;
+  uint64_t* mbar = (uint64_t*)(bufB + kTile * H * 2);
+  uint64_t* mbar2 = mbar + 1;
+  uint32_t* tbase = (uint32_t*)(mbar + 2);
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int T = P.T, A = P.A;
+  const int R = a.batch.counters[0];
+  const int tiles = (R + kTile - 1) / kTile;
+  const int per = (tiles + gridDim.x - 1) / gridDim.x;
+  const int t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
+  float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
+  const MlpLayout& L = a.L;
+  if (warp == 0) tmem_alloc<512>(tbase);
+  if (tid == 0) {
+    mbar_init(mbar, 1);
+    mbar_init(mbar2, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  uint32_t ph_load = 0, ph_mma = 0;
+  constexpr int kHalves = H / 128;
+
+  // ---- pass A: dW2[p][j] = sum_r h1[r][p] dz2[r][j]
+  for (int tile = t0; tile < t1; ++tile) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(mbar, 2 * kTile * H * 2);
+      bulk_g2s_big(bufA, a.h1 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
+      bulk_g2s_big(bufB, a.dz2 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
+      mbar_wait(mbar, ph_load);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < kHalves; ++h) mma_mn<H>(tmem + h * H, bufA, 128 * h, bufB, tile > t0);
+      umma_commit(mbar2);
+      mbar_wait(mbar2, ph_mma);
+    }
+    ph_load ^= 1;
+    ph_mma ^= 1;
+    __syncthreads();
+  }
+  tc_fence_after();
+  for (int h = 0; h < kHalves; ++h) {
+    const int p = 128 * h + tid;  // input feature of layer 2
+    for (int q = 0; q < H / 32; ++q) {
+      uint32_t r32[32];
+      tmem_ld32(lane_base + h * H + q * 32, r32);
+      tmem_wait_ld();
+      float* dst = part + L.off_w[1] + (size_t)p * H + q * 32;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) dst[i] = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  // ---- pass B: dW1[f][j] = sum_r obs[r][f] dz1[r][j]   (obs one-hot, built in smem)
+  for (int tile = t0; tile < t1; ++tile) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(mbar, kTile * H * 2);
+      bulk_g2s_big(bufB, a.dz1 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
+    }
+    const int r = tile * kTile + tid;
+    {  // obs row (128 features) as bf16 one-hot
+      uint32_t z4[4] = {0, 0, 0, 0};
+#pragma unroll
+      for (int c = 0; c < 16; ++c)
+        *reinterpret_cast<uint4*>(bufA + sw128_offset(tid, 8 * c, kTile)) = make_uint4(z4[0], z4[1], z4[2], z4[3]);
+      if (r < R) {
+        const int b = find_traj(a.batch.row0, a.Bl, r);
+        const int t = r - a.batch.row0[b];
+        typename Env::State s;
+        Env::unpack(P, a.stst + ((size_t)b * T + t) * P.SW, s);
+        Env::features(P, s, [&](int f, double x) {
+          *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, f, kTile)) = __float2bfloat16((float)x);
+        });
+      }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      mbar_wait(mbar, ph_load);
+      tc_fence_after();
+      mma_mn<H>(tmem, bufA, 0, bufB, tile > t0);
+      umma_commit(mbar2);
+      mbar_wait(mbar2, ph_mma);
+    }
+    ph_load ^= 1;
+    ph_mma ^= 1;
+    __syncthreads();
+  }
+  tc_fence_after();
+  for (int q = 0; q < H / 32; ++q) {  // tcgen05.ld is warp-collective: every lane executes it
+    uint32_t r32[32];
+    tmem_ld32(lane_base + q * 32, r32);
+    tmem_wait_ld();
+    if (tid < P.O) {
+      float* dst = part + L.off_w[0] + (size_t)tid * H + q * 32;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) dst[i] = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+
+  // ---- pass C: dWf[p][c] = sum_r h2[r][p] dhead[r][c]   (c < A: logits, c == A: flow)
+  for (int tile = t0; tile < t1; ++tile) {
+    if (tid == 0) {
+      mbar_arrive_expect_tx(mbar, kTile * H * 2 + kTile * 64 * 2);
+      bulk_g2s_big(bufA, a.h2 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
+      bulk_g2s_big(bufB, a.dhead + (size_t)tile * kTile * 64, kTile * 64 * 2, mbar);
+      mbar_wait(mbar, ph_load);
+      tc_fence_after();
+#pragma unroll
+      for (int h = 0; h < kHalves; ++h) mma_mn<64>(tmem + h * 64, bufA, 128 * h, bufB, tile > t0);
+      umma_commit(mbar2);
+      mbar_wait(mbar2, ph_mma);
+    }
+    ph_load ^= 1;
+    ph_mma ^= 1;
+    __syncthreads();
+  }
+  tc_fence_after();
+  for (int h = 0; h < kHalves; ++h) {
+    const int p = 128 * h + tid;
+    for (int q = 0; q < 2; ++q) {
+      uint32_t r32[32];
+      tmem_ld32(lane_base + h * 64 + q * 32, r32);
+      tmem_wait_ld();
+      for (int i = 0; i < 32; ++i) {
+        const int c = q * 32 + i;
+        const float v = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
+        if (c < A) part[L.off_fw + (size_t)p * A + c] = v;
+        else if (c == A) part[L.off_flw + p] = v;
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// fixed-order reduction over CTAs (deterministic)
+__global__ void k_reduce(const float* __restrict__ wpart, int nparts, int64_t n, float* g) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  float s = 0.f;
+  for (int c = 0; c < nparts; ++c) s += wpart[(size_t)c * n + e];
+  g[e] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Adam (optim.cpp:19-43) over fp32 params + bf16 operand images; logZ (TB) on thread 0
+
+struct AdamArgs {
+  float *p, *m, *v;
+  const float* g;
+  int64_t n;
+  float lr, b1, b2, eps, wd, bc1, bc2;
+  double* scalars;
+  int do_z;
+  double z_lr, zb1, zb2, zeps, zbc1, zbc2;
+  MlpLayout L;
+  __nv_bfloat16 *w1, *w2f, *w2d;
+  int H, O;
+};
+
+__device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float pj) {
+  const MlpLayout& L = a.L;
+  if (j < L.off_b[0]) {  // W1 [O][H] row-major bf16
+    a.w1[j] = __float2bfloat16(pj);
+  } else if (j >= L.off_w[1] && j < L.off_b[1]) {  // W2 [in p][out q]
+    const int64_t k = j - L.off_w[1];
+    const int p = (int)(k / a.H), q = (int)(k % a.H);
+    const __nv_bfloat16 v = __float2bfloat16(pj);
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.w2f + sw128_offset(q, p, a.H)) = v;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.w2d + sw128_offset(p, q, a.H)) = v;
+  }
+}
+
+__global__ void k_fast_adam(AdamArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < a.n) {
+    const float gj = a.g[j];
+    const float m = a.b1 * a.m[j] + (1.f - a.b1) * gj;
+    const float v = a.b2 * a.v[j] + (1.f - a.b2) * gj * gj;
+    a.m[j] = m;
+    a.v[j] = v;
+    const float mhat = m / a.bc1, vhat = v / a.bc2;
+    const float pj = a.p[j] - a.lr * (mhat / (sqrtf(vhat) + a.eps) + a.wd * a.p[j]);
+    a.p[j] = pj;
+    emit_images(a, j, pj);
+  }
+  if (a.do_z && j == 0) {  // logZ keeps fp64 state (train.cpp:186-190)
+    const double gj = a.scalars[3];
+    a.scalars[1] = a.zb1 * a.scalars[1] + (1.0 - a.zb1) * gj;
+    a.scalars[2] = a.zb2 * a.scalars[2] + (1.0 - a.zb2) * gj * gj;
+    const double mhat = a.scalars[1] / a.zbc1, vhat = a.scalars[2] / a.zbc2;
+    a.scalars[0] -= a.z_lr * (mhat / (sqrt(vhat) + a.zeps));
+  }
+}
+
+__global__ void k_emit_images(AdamArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < a.n) emit_images(a, j, a.p[j]);
+}
+
+AdamArgs adam_args(Ctx& c) {
+  FastState& f = FS(c);
+  AdamArgs a{};
+  a.p = c.p32;
+  a.m = c.m32;
+  a.v = c.v32;
+  a.g = c.g32;
+  a.n = c.L.n_params;
+  a.L = c.L;
+  a.w1 = f.w1;
+  a.w2f = f.w2_fwd;
+  a.w2d = f.w2_dgrad;
+  a.H = f.H;
+  a.O = f.O;
+  a.scalars = c.d_scalars;
+  return a;
+}
+
+template <class Env, int H, int AMAX>
+struct Kernels {
+  static void rollout(Ctx& c, Key key, double eps) {
+    FastState& f = FS(c);
+    RolloutArgs a{};
+    a.P = c.P;
+    a.W = weights_of(c);
+    a.key = key;
+    a.eps = eps;
+    a.b0 = c.b0;
+    a.Bl = c.Bl;
+    a.batch = c.batch;
+    a.stst = f.stst;
+    a.work = f.work;
+    const int T = c.P.T;
+    cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)c.Bl * T, c.stream);
+    cudaMemsetAsync(c.batch.nparents, 0, sizeof(uint16_t) * (size_t)c.Bl * T, c.stream);
+    if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
+    cudaMemsetAsync(c.batch.lengths, 0, sizeof(int32_t) * c.Bl, c.stream);
+    cudaMemsetAsync(f.work, 0, sizeof(int32_t), c.stream);
+    const int smem = rollout_smem_bytes<H>(T);
+    cudaFuncSetAttribute(k_fast_rollout<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
+    ProfScope ps(c, "k_fast_rollout");
+    k_fast_rollout<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(a);
+    c.launches++;
+  }
+  static void train(Ctx& c, bool apply, double lr) {
+    FastState& f = FS(c);
+    TrainArgs ta{};
+    ta.P = c.P;
+    ta.W = weights_of(c);
+    ta.batch = c.batch;
+    ta.Bl = c.Bl;
+    ta.stst = f.stst;
+    ta.h1 = f.h1;
+    ta.h2 = f.h2;
+    ta.dz1 = f.dz1;
+    ta.dz2 = f.dz2;
+    ta.dhead = f.dhead;
+    ta.rowbuf = f.rowbuf;
+    ta.rs = f.rs;
+    ta.coef = f.coef;
+    ta.wpart = f.wpart;
+    ta.n_params = c.L.n_params;
+    ta.L = c.L;
+    ta.objective = c.train.objective;
+    const int grid = f.num_sms;
+    int smem = fwd_smem_bytes<H>();
+    cudaFuncSetAttribute(k_fast_fwd<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+      ProfScope ps(c, "k_fast_fwd");
+      k_fast_fwd<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(ta);
+    }
+    LossArgs la{};
+    la.batch = c.batch;
+    la.Bl = c.Bl;
+    la.T = c.P.T;
+    la.A = c.P.A;
+    la.stop = c.P.stop;
+    la.objective = c.train.objective;
+    la.B_global = c.B;
+    la.terminal_penalty = c.train.terminal_penalty;
+    la.lampow = f.lampow;
+    la.neglog = c.d_neglog;
+    la.rowbuf = f.rowbuf;
+    la.rs = f.rs;
+    la.coef = f.coef;
+    la.lpart = f.lpart;
+    la.scalars = c.d_scalars;
+    {
+      ProfScope ps(c, "k_fast_loss");
+      k_fast_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
+    }
+    k_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars,
+                                             c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
+    smem = bwd_smem_bytes<H>();
+    cudaFuncSetAttribute(k_fast_bwd<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+      ProfScope ps(c, "k_fast_bwd");
+      k_fast_bwd<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(ta);
+    }
+    smem = wgrad_smem_bytes<H>();
+    cudaFuncSetAttribute(k_fast_wgrad<Env, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+      ProfScope ps(c, "k_fast_wgrad");
+      k_fast_wgrad<Env, H><<<grid, kTile, smem, c.stream>>>(ta);
+    }
+    const int64_t n = c.L.n_params;
+    {
+      ProfScope ps(c, "k_reduce");
+      k_reduce<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(f.wpart, grid, n, c.g32);
+    }
+    c.launches += 6;
+    (void)apply;
+    (void)lr;
+  }
+};
+
+template <class Env, int H, int AMAX>
+void dispatch_rollout(Ctx& c, Key key, double eps) { Kernels<Env, H, AMAX>::rollout(c, key, eps); }
+
+bool supported(const Ctx& c, int* H) {
+  *H = c.L.H();
+  if (c.L.n_trunk != 2) return false;
+  if (c.L.dims[1] != c.L.dims[2]) return false;
+  if (*H != 256 && *H != 128) return false;
+  if (c.shape.num_actions + 1 > 64 || c.shape.num_actions > kHeadMax) return false;
+  if (c.shape.obs_dim > 128) return false;
+  if (c.shape.max_traj_len > 128) return false;
+  return c.env.kind == GFNX_ENV_HYPERGRID || c.env.kind == GFNX_ENV_DAG;
+}
+
+template <class F>
+void with_kernels(Ctx& c, F&& fn) {
+  int H = 0;
+  if (!supported(c, &H))
+    raise_error(GFNX_ERR_CONFIG,
+                "bf16 fast path supports 2-hidden-layer MLPs (H=128/256) on hypergrid and DAG in "
+                "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
+  if (c.env.kind == GFNX_ENV_HYPERGRID) {
+    if (H == 256) fn(Kernels<HypergridEnv, 256, 8>{});
+    else fn(Kernels<HypergridEnv, 128, 8>{});
+  } else {
+    if (H == 256) fn(Kernels<DagEnv, 256, 32>{});
+    else fn(Kernels<DagEnv, 128, 32>{});
+  }
+}
+
+}  // namespace
+
+void fast_init(Ctx& c) {
+  int H = 0;
+  if (!supported(c, &H))
+    raise_error(GFNX_ERR_CONFIG,
+                "bf16 fast path supports 2-hidden-layer MLPs (H=128/256) on hypergrid and DAG in "
+                "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
+  auto* f = new FastState();
+  c.fast = f;
+  cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  f->H = H;
+  f->A = c.shape.num_actions;
+  f->O = c.shape.obs_dim;
+  const int T = c.P.T;
+  f->max_rows = (int64_t)c.Bl * T;
+  f->max_tiles = (f->max_rows + kTile - 1) / kTile;
+  f->rs = f->A + 4;
+  f->loss_blocks = (c.Bl + 255) / 256;
+  const size_t img = (size_t)f->max_tiles * kTile * H * 2;
+  cuda_check(cudaMalloc(&f->w1, sizeof(__nv_bfloat16) * (size_t)f->O * H), "fast w1");
+  cuda_check(cudaMalloc(&f->w2_fwd, sizeof(__nv_bfloat16) * H * H), "fast w2");
+  cuda_check(cudaMalloc(&f->w2_dgrad, sizeof(__nv_bfloat16) * H * H), "fast w2");
+  cuda_check(cudaMalloc(&f->stst, sizeof(uint32_t) * (size_t)c.Bl * T * c.P.SW), "fast stst");
+  cuda_check(cudaMalloc(&f->h1, img), "fast h1");
+  cuda_check(cudaMalloc(&f->h2, img), "fast h2");
+  cuda_check(cudaMalloc(&f->dz1, img), "fast dz1");
+  cuda_check(cudaMalloc(&f->dz2, img), "fast dz2");
+  cuda_check(cudaMalloc(&f->dhead, (size_t)f->max_tiles * kTile * 64 * 2), "fast dhead");
+  cuda_check(cudaMalloc(&f->rowbuf, sizeof(float) * (size_t)(f->max_tiles * kTile) * f->rs), "fast rowbuf");
+  cuda_check(cudaMalloc(&f->coef, sizeof(float) * (size_t)f->max_rows * 4), "fast coef");
+  cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
+  cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
+  cuda_check(cudaMalloc(&f->lpart, sizeof(double) * 2 * f->loss_blocks), "fast lpart");
+  cuda_check(cudaMalloc(&f->work, sizeof(int32_t)), "fast work");
+  std::vector<double> lp(T + 1);
+  for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);
+  cuda_check(cudaMalloc(&f->lampow, sizeof(double) * (T + 1)), "fast lampow");
+  cuda_check(cudaMemcpy(f->lampow, lp.data(), sizeof(double) * (T + 1), cudaMemcpyHostToDevice), "lampow");
+  fast_sync_weights(c);
+}
+
+void fast_free(Ctx& c) {
+  FastState* f = static_cast<FastState*>(c.fast);
+  if (!f) return;
+  void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
+                  f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete f;
+  c.fast = nullptr;
+}
+
+void fast_sync_weights(Ctx& c) {
+  AdamArgs a = adam_args(c);
+  k_emit_images<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "emit images");
+}
+
+void fast_rollout(Ctx& c, Key key, double eps) {
+  with_kernels(c, [&](auto k) { decltype(k)::rollout(c, key, eps); });
+}
+
+void fast_train(Ctx& c, bool apply, double lr, double* /*loss*/) {
+  with_kernels(c, [&](auto k) { decltype(k)::train(c, apply, lr); });
+}
+
+void fast_adam(Ctx& c, double lr) {
+  const int64_t n = c.L.n_params;
+  const gfnx_train_desc& s = c.train;
+  c.adam_t += 1;
+  AdamArgs a = adam_args(c);
+  a.lr = (float)lr;
+  a.b1 = (float)s.beta1;
+  a.b2 = (float)s.beta2;
+  a.eps = (float)s.adam_eps;
+  a.wd = (float)s.weight_decay;
+  a.bc1 = (float)(1.0 - pow(s.beta1, (double)c.adam_t));
+  a.bc2 = (float)(1.0 - pow(s.beta2, (double)c.adam_t));
+  a.do_z = s.objective == GFNX_OBJ_TB;
+  if (a.do_z) {
+    c.z_t += 1;
+    a.z_lr = s.z_lr;
+    a.zb1 = s.beta1;
+    a.zb2 = s.beta2;
+    a.zeps = s.adam_eps;
+    a.zbc1 = 1.0 - pow(s.beta1, (double)c.z_t);
+    a.zbc2 = 1.0 - pow(s.beta2, (double)c.z_t);
+  }
+  ProfScope ps(c, "k_fast_adam");
+  k_fast_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(a);
+  c.launches++;
+}
+
+}  // namespace gfnx

@@ -1,0 +1,233 @@
+"""Host-side mirror of the reference training API over the libgfnx C ABI.
+
+``Trainer`` follows the reference drivers (proj/src/train.cpp): ``forward_rollout``
+(env_core.hpp:232-274), ``train_step`` (train.cpp:164-192) and ``iteration``
+(the train_scenario loop body, train.cpp:224-229), with the same error classes as
+proj/include/gfn/errors.hpp. Everything numeric runs in libgfnx.so on the GPU; there
+is no CPU fallback — a missing or unloadable library raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from . import abi
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgfnx.so")
+_LIB = None
+
+
+class config_error(RuntimeError):
+    pass
+
+
+class contract_violation(RuntimeError):
+    pass
+
+
+class numeric_error(RuntimeError):
+    pass
+
+
+class device_error(RuntimeError):
+    pass
+
+
+_ERRORS = {abi.ERR_CONFIG: config_error, abi.ERR_CONTRACT: contract_violation,
+           abi.ERR_NUMERIC: numeric_error, abi.ERR_CUDA: device_error, abi.ERR_NCCL: device_error}
+
+
+def lib():
+    """Load libgfnx.so (built in-tree by __graft_entry__.build / build.py). Fails loudly."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"libgfnx.so not built at {LIB_PATH}: run __graft_entry__.build()")
+        L = C.CDLL(LIB_PATH)
+        P = C.POINTER
+        vp = C.c_void_p
+        L.gfnx_last_error.restype = C.c_char_p
+        L.gfnx_last_error.argtypes = [vp]
+        L.gfnx_create.argtypes = [P(abi.EnvDesc), P(abi.TrainDesc), C.c_int32, C.c_int32,
+                                  C.c_int32, vp, P(vp)]
+        L.gfnx_destroy.argtypes = [vp]
+        L.gfnx_nccl_unique_id.argtypes = [vp]
+        L.gfnx_env_shape_of.argtypes = [P(abi.EnvDesc), P(abi.EnvShape)]
+        L.gfnx_default_env_desc.argtypes = [C.c_int32, P(abi.EnvDesc)]
+        L.gfnx_default_train_desc.argtypes = [C.c_int32, P(abi.TrainDesc)]
+        L.gfnx_num_params.argtypes = [vp, P(C.c_int64)]
+        L.gfnx_set_params.argtypes = [vp, vp, C.c_int64, C.c_double]
+        L.gfnx_get_params.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_set_adam_state.argtypes = [vp, vp, vp, C.c_int64, C.c_double, C.c_double, C.c_int64]
+        L.gfnx_get_adam_state.argtypes = [vp] + [vp] * 6
+        L.gfnx_rollout.argtypes = [vp, C.c_int64, C.c_double]
+        L.gfnx_train_step.argtypes = [vp, C.c_double, vp]
+        L.gfnx_compute_grads.argtypes = [vp, vp]
+        L.gfnx_get_grads.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_iteration.argtypes = [vp, C.c_int64, vp]
+        L.gfnx_run.argtypes = [vp, C.c_int64, C.c_int64, vp]
+        L.gfnx_synchronize.argtypes = [vp]
+        L.gfnx_batch_dims.argtypes = [vp, vp, vp, vp, vp]
+        L.gfnx_export_batch.argtypes = [vp, P(abi.HostBatch)]
+        L.gfnx_kernel_launches.restype = C.c_int64
+        L.gfnx_kernel_launches.argtypes = [vp]
+        L.gfnx_last_phase_ms.argtypes = [vp, vp, vp]
+        L.gfnx_test_threefry.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_test_uniform_fold.argtypes = [C.c_uint64, C.c_uint64, vp, C.c_int64, vp]
+        L.gfnx_abi_version.restype = C.c_int32
+        _LIB = L
+    return _LIB
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _raise(rc, h=None):
+    if rc != abi.OK:
+        msg = lib().gfnx_last_error(h).decode()
+        raise _ERRORS.get(rc, device_error)(msg)
+
+
+def env_shape(env: abi.EnvDesc) -> abi.EnvShape:
+    s = abi.EnvShape()
+    _raise(lib().gfnx_env_shape_of(C.byref(env), C.byref(s)))
+    return s
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _raise(lib().gfnx_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Trainer:
+    """One rank's device engine (one gfnx_ctx)."""
+
+    def __init__(self, env: abi.EnvDesc, train: abi.TrainDesc, device: int = 0, rank: int = 0,
+                 world: int = 1, nccl_id: bytes | None = None):
+        self.env, self.train = env, train
+        h = C.c_void_p()
+        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        _raise(lib().gfnx_create(C.byref(env), C.byref(train), device, rank, world, idbuf,
+                                 C.byref(h)))
+        self.h = h
+        n = C.c_int64()
+        lib().gfnx_num_params(h, C.byref(n))
+        self.n_params = n.value
+        self.shape = env_shape(env)
+        bl, b0, T, sw = C.c_int32(), C.c_int32(), C.c_int32(), C.c_int32()
+        lib().gfnx_batch_dims(h, C.byref(bl), C.byref(b0), C.byref(T), C.byref(sw))
+        self.local_batch, self.first_traj, self.T, self.state_words = bl.value, b0.value, T.value, sw.value
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().gfnx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        self.close()
+
+    def _check(self, rc):
+        _raise(rc, self.h)
+
+    # -- parameters / optimizer state (MlpParams::tensors() order, nn.cpp:8-19) --
+    def params(self):
+        p = np.zeros(self.n_params)
+        z = C.c_double()
+        self._check(lib().gfnx_get_params(self.h, _p(p), self.n_params, C.byref(z)))
+        return p, z.value
+
+    def set_params(self, p, log_z):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        self._check(lib().gfnx_set_params(self.h, _p(p), self.n_params, log_z))
+
+    def adam_state(self):
+        m, v = np.zeros(self.n_params), np.zeros(self.n_params)
+        t, zt = C.c_int64(), C.c_int64()
+        zm, zv = C.c_double(), C.c_double()
+        self._check(lib().gfnx_get_adam_state(self.h, _p(m), _p(v), C.byref(t), C.byref(zm),
+                                              C.byref(zv), C.byref(zt)))
+        return m, v, t.value, zm.value, zv.value, zt.value
+
+    def set_adam_state(self, m, v, t, zm, zv, zt):
+        m = np.ascontiguousarray(m, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        self._check(lib().gfnx_set_adam_state(self.h, _p(m), _p(v), t, zm, zv, zt))
+
+    # -- the hot path --
+    def forward_rollout(self, it: int, eps: float):
+        self._check(lib().gfnx_rollout(self.h, it, eps))
+
+    def train_step(self, lr: float, read_loss: bool = True):
+        loss = C.c_double()
+        self._check(lib().gfnx_train_step(self.h, lr, C.byref(loss) if read_loss else None))
+        return loss.value if read_loss else None
+
+    def compute_grads(self):
+        loss = C.c_double()
+        self._check(lib().gfnx_compute_grads(self.h, C.byref(loss)))
+        return loss.value
+
+    def grads(self):
+        g = np.zeros(self.n_params)
+        dz = C.c_double()
+        self._check(lib().gfnx_get_grads(self.h, _p(g), self.n_params, C.byref(dz)))
+        return g, dz.value
+
+    def iteration(self, it: int, read_loss: bool = True):
+        loss = C.c_double()
+        self._check(lib().gfnx_iteration(self.h, it, C.byref(loss) if read_loss else None))
+        return loss.value if read_loss else None
+
+    def run(self, it0: int, n: int, read_losses: bool = False):
+        losses = np.zeros(n) if read_losses else None
+        self._check(lib().gfnx_run(self.h, it0, n, _p(losses) if read_losses else None))
+        return losses
+
+    def synchronize(self):
+        self._check(lib().gfnx_synchronize(self.h))
+
+    def batch(self):
+        """Host copy of the resident TrajectoryBatch fields (trajectory.hpp:15-33)."""
+        B, T, sw = self.local_batch, self.T, self.state_words
+        out = dict(lengths=np.zeros(B, np.int32), fwd_actions=np.zeros((B, T), np.int32),
+                   bwd_actions=np.zeros((B, T), np.int32), log_rewards=np.zeros(B),
+                   log_pb=np.zeros((B, T)), delta=np.zeros((B, T)),
+                   terminal_state=np.zeros((B, sw), np.uint32))
+        hb = abi.HostBatch()
+        hb.lengths = out["lengths"].ctypes.data_as(C.POINTER(C.c_int32))
+        hb.fwd_actions = out["fwd_actions"].ctypes.data_as(C.POINTER(C.c_int32))
+        hb.bwd_actions = out["bwd_actions"].ctypes.data_as(C.POINTER(C.c_int32))
+        hb.log_rewards = out["log_rewards"].ctypes.data_as(C.POINTER(C.c_double))
+        hb.log_pb = out["log_pb"].ctypes.data_as(C.POINTER(C.c_double))
+        hb.delta_log_reward = out["delta"].ctypes.data_as(C.POINTER(C.c_double))
+        hb.terminal_state = out["terminal_state"].ctypes.data_as(C.POINTER(C.c_uint32))
+        self._check(lib().gfnx_export_batch(self.h, C.byref(hb)))
+        return out
+
+    def kernel_launches(self) -> int:
+        return lib().gfnx_kernel_launches(self.h)
+
+    def last_phase_ms(self):
+        a, b = C.c_double(), C.c_double()
+        self._check(lib().gfnx_last_phase_ms(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
+
+def test_threefry(keys: np.ndarray, ctrs: np.ndarray) -> np.ndarray:
+    keys = np.ascontiguousarray(keys, dtype=np.uint64)
+    ctrs = np.ascontiguousarray(ctrs, dtype=np.uint64)
+    out = np.zeros_like(keys)
+    _raise(lib().gfnx_test_threefry(_p(keys), _p(ctrs), keys.shape[0], _p(out)))
+    return out
+
+
+def test_uniform_fold(key, idx: np.ndarray) -> np.ndarray:
+    idx = np.ascontiguousarray(idx, dtype=np.uint64)
+    out = np.zeros(idx.shape[0])
+    _raise(lib().gfnx_test_uniform_fold(key[0], key[1], _p(idx), idx.shape[0], _p(out)))
+    return out
