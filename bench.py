@@ -1,0 +1,381 @@
+#!/usr/bin/env python
+"""bench.py — GFlowNet training throughput on B200 (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): hypergrid 20^4, detailed balance, MLP 2x256,
+65536 trajectories per GPU per iteration (weak scaling: N GPUs train on N x 65536
+trajectories per iteration, one NCCL all-reduce of the gradient per iteration).
+A "step" is one full training iteration: forward rollout (sampling from the current
+policy), loss + gradient, all-reduce, Adam — train_scenario's loop body
+(proj/src/train.cpp:224-229), entirely on the device.
+
+  value  trajectories/s with everything resident, timed with CUDA events on the engine
+         stream, max over ranks.
+  e2e    the same through the public C ABI call per iteration (gfnx_iteration) with the
+         loss and the batch's terminal states / lengths / log-rewards copied to host
+         buffers every iteration (what the reference loop hands to its FIFO buffer,
+         train.cpp:231), timed on the host clock, max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...   (one process per GPU)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = "hypergrid_db_b65536"
+PER_GPU_BATCH = 65536
+METRIC = "trajectories/sec (train iters/sec in config) — hypergrid 20^4 DB, B=65536/GPU"
+UNIT = "trajectories/s"
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Comm:
+    """Control-plane collectives over gloo (the data-plane all-reduce is NCCL in libgfnx)."""
+
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+        self.dist = None
+        if world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            self.dist = dist
+
+    def barrier(self):
+        if self.dist:
+            self.dist.barrier()
+
+    def max(self, x: float) -> float:
+        if not self.dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum(self, x: float) -> float:
+        if not self.dist:
+            return x
+        import torch
+        t = torch.tensor([x], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def bcast_bytes(self, b: bytes | None) -> bytes:
+        if not self.dist:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def close(self):
+        if self.dist:
+            self.dist.destroy_process_group()
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.gpu)],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, "fallback"
+
+
+def kernel_work(name, rows, iters, H, A, O, n_params, nsm):
+    """Algorithmic FLOPs and bytes of one launch-set of `name`."""
+    R = rows
+    if name == "k_fast_rollout":      # hidden GEMM per real (row, step); policy head is SIMT
+        return 2.0 * H * H * R, R * (2 + 4 + 4)
+    if name == "k_fast_fwd":          # layer 2 GEMM; writes h1, h2 bf16 rows + head stats
+        return 2.0 * H * H * R, R * (2 * H * 2 + (A + 4) * 4)
+    if name == "k_fast_bwd":          # dgrad GEMM; reads h1, h2, writes dz1, dz2, dhead
+        return 2.0 * H * H * R, R * (4 * H * 2 + 64 * 2 + (A + 8) * 4)
+    if name == "k_fast_wgrad":        # dW2 + dW_head GEMMs (dW1 is a one-hot scatter)
+        return 2.0 * R * (H * H + H * (A + 1)), R * (5 * H * 2 + 64 * 2) + nsm * n_params * 4
+    if name == "k_reduce":
+        return 0.0, (nsm + 1) * n_params * 4 * iters
+    if name == "k_fast_adam":
+        return 0.0, 28.0 * n_params * iters
+    if name == "k_fast_loss":
+        return 0.0, R * (3 * 4 + 16)
+    return 0.0, 0.0
+
+
+def cpu_reference_sample(steps: int, warmup: int, procs: int, batch: int):
+    """The reference's own run_bench (train.cpp:294-334) via oracle/_ref, one process per
+    host core (the reference is single-threaded), hypergrid 20^4 DB at `batch` trajectories."""
+    import multiprocessing as mp
+    kv = {"env.dim": 4, "env.side": 20, "objective.name": "db", "train.batch_size": batch,
+          "bench.repeats": 1, "bench.iters": steps, "bench.warmup": warmup, "eval.metrics": "",
+          "seed": 0}
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        res = pool.starmap(_ref_worker, [(kv, i) for i in range(procs)])
+    its = [r for r in res if r is not None]
+    return its
+
+
+def _ref_worker(kv, i):
+    sys.path.insert(0, ROOT)
+    from oracle import oracle as O
+    kv = dict(kv)
+    kv["seed"] = i
+    kind = "fast" if O.ref_available("fast") else "port"
+    mean, _ = O.ref_run_bench("hypergrid", kv, kind=kind)
+    return mean
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    batch = 32
+    t0 = time.perf_counter()
+    its = cpu_reference_sample(args.steps, args.warmup, procs, batch)
+    wall = time.perf_counter() - t0
+    value = float(sum(its) * batch)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * batch * procs / value if value else None,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (environment-generated trajectories)",
+        "config": {"workload": CONFIG, "env": "hypergrid d=4 H=20", "objective": "db",
+                   "mlp": "2x256", "global_batch": PER_GPU_BATCH * args.gpus},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs,
+                         "kind": "reference" if O.ref_available("fast") else "port",
+                         "sample": f"{procs} processes x reference run_bench(hypergrid 20^4 DB, "
+                                   f"B={batch}, iters={args.steps}, warmup={args.warmup}); "
+                                   f"wall {wall:.1f}s"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def cpu_baseline_leg():
+    """Single-core reference timing on a bounded sample (~10-30 s), rank 0 at N=1 only."""
+    from oracle import oracle as O
+    batch, iters = 128, 6
+    kind = "fast" if O.ref_available("fast") else ("port" if O.ref_available("port") else None)
+    t0 = time.perf_counter()
+    if kind is not None:
+        kv = {"env.dim": 4, "env.side": 20, "objective.name": "db", "train.batch_size": batch,
+              "bench.repeats": 1, "bench.iters": iters, "bench.warmup": 1, "eval.metrics": "",
+              "seed": 0}
+        its, _ = O.ref_run_bench("hypergrid", kv, kind=kind)
+        return {"value": its * batch, "unit": UNIT, "cores": 1, "kind": "reference",
+                "sample": f"reference run_bench (oracle/_ref, {kind} build), hypergrid 20^4 DB, "
+                          f"B={batch}, 1 warmup + {iters} timed iterations, "
+                          f"{time.perf_counter() - t0:.1f}s wall"}
+    from paper_2511_16592_b200 import abi
+    e, t = abi.config(CONFIG, batch=batch)
+    o = O.Oracle(e, t)
+    o.iteration(0)
+    t1 = time.perf_counter()
+    for it in range(1, 1 + iters):
+        o.iteration(it)
+    dt = time.perf_counter() - t1
+    return {"value": batch * iters / dt, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"oracle restatement, hypergrid 20^4 DB, B={batch}, {iters} iterations"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="trajectories per GPU")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    from paper_2511_16592_b200 import abi, engine
+    comm = Comm(world, rank)
+    e, t = abi.config(CONFIG, batch=args.batch * world)
+    t.iterations = 1_000_000
+    nccl_id = engine.nccl_unique_id() if (world > 1 and rank == 0) else None
+    nccl_id = comm.bcast_bytes(nccl_id) if world > 1 else None
+    tr = engine.Trainer(e, t, device=local, rank=rank, world=world, nccl_id=nccl_id)
+    W, K = max(args.warmup, 3), args.steps
+    tr.run(0, W)
+    tr.synchronize()
+
+    # ---- device-timed region: everything resident, CUDA events on the engine stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = tr.kernel_launches()
+    rows0, rolls0 = tr.counters()[:2]
+    tr.profile(True)
+    comm.barrier()
+    tr.synchronize()
+    tr.event_record(0)
+    tr.run(W, K)
+    tr.event_record(1)
+    tr.synchronize()
+    comm.barrier()
+    ms = comm.max(tr.event_elapsed(0, 1))
+    prof = tr.profile_read()
+    tr.profile(False)
+    launches = tr.kernel_launches() - launches0
+    rows1, rolls1 = tr.counters()[:2]
+    rows = rows1 - rows0
+    value = args.batch * world * K / (ms / 1e3)
+
+    # ---- end to end through the C ABI: per iteration, results copied to pinned host
+    # memory (gfnx_iteration_async + gfnx_slot_wait, two slots in flight) and consumed
+    e2e = None
+    if not args.no_e2e:
+        comm.barrier()
+        tr.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        sink = 0.0
+        for i in range(K):
+            tr.iteration_async(W + K + i, i % 2)
+            if i > 0:
+                _, loss, res = tr.slot_wait((i - 1) % 2)
+                sink += loss + float(res["log_rewards"][0])
+                d2h = 8 + sum(v.nbytes for v in res.values())
+        _, loss, res = tr.slot_wait((K - 1) % 2)
+        tr.synchronize()
+        dt = comm.max(time.perf_counter() - t0)
+        e2e = {"value": args.batch * world * K / dt, "unit": UNIT,
+               "h2d_bytes_per_step": 24, "d2h_bytes_per_step": d2h,
+               "note": "gfnx_iteration_async per step: h2d = iteration index, lr, eps (kernel "
+                       "arguments); d2h = loss + lengths/log-rewards/terminal states into pinned "
+                       "host memory, consumed by the host every step; host wall clock"}
+    cl = clocks.stop()
+
+    # ---- roofline of the dominant kernel
+    hbm, tens, peak_kind = measured_peaks()
+    H, A, O_ = 256, 5, 80
+    dom, dom_ms = max(prof.items(), key=lambda kv: kv[1][0]) if prof else (None, (0, 0))
+    roof = None
+    kernels = {}
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f)
+    for name, (tot_ms, cnt) in prof.items():
+        fl, by = kernel_work(name, rows, K, H, A, O_, tr.n_params, 148)
+        sec = tot_ms / 1e3
+        kernels[name] = {"ms_total": round(tot_ms, 4), "launches": cnt,
+                         "tflops": fl / sec / 1e12 if sec else None,
+                         "gbs": by / sec / 1e9 if sec else None}
+    if dom:
+        fl, by = kernel_work(dom, rows, K, H, A, O_, tr.n_params, 148)
+        sec = dom_ms[0] / 1e3
+        ft = fl / sec / 1e12 / tens if sec else 0.0
+        fb = by / sec / 1e9 / hbm if sec else 0.0
+        per = dom_ms[1]
+        if ft >= fb:
+            roof = {"kernel": dom, "bound": "tensor", "achieved": fl / sec / 1e12, "peak": tens,
+                    "unit": "TFLOP/s", "frac": ft}
+        else:
+            roof = {"kernel": dom, "bound": "hbm", "achieved": by / sec / 1e9, "peak": hbm,
+                    "unit": "GB/s", "frac": fb}
+        roof["peak_source"] = peak_kind
+        roof["share_of_step"] = dom_ms[0] / ms if ms else None
+        tr_k = (traffic or {}).get(dom)
+        roof["traffic"] = tr_k
+        roof["algorithmic_per_launch"] = {"flops": fl / per if per else None,
+                                          "bytes": by / per if per else None}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline_leg()
+        except Exception as ex:  # reported, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (trajectories generated on device by the environment)",
+            "config": {"workload": CONFIG, "env": "hypergrid d=4 H=20", "objective": "db",
+                       "mlp": "2x256", "batch_per_gpu": args.batch,
+                       "global_batch": args.batch * world, "parallelism": f"dp{world}",
+                       "train_iters_per_sec": K / (ms / 1e3),
+                       "mean_traj_len": rows / (args.batch * K) if K else None,
+                       "l2": "working set > L2 (bf16 activation images ~2 KB per state row)"},
+            "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kernels,
+            "cpu_baseline": cpu, "clocks": cl,
+        }
+        print(json.dumps(line))
+    tr.close()
+    comm.close()
+
+
+if __name__ == "__main__":
+    main()

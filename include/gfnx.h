@@ -175,6 +175,25 @@ gfnx_status gfnx_iteration(gfnx_ctx* ctx, int64_t it, double* loss);
 gfnx_status gfnx_run(gfnx_ctx* ctx, int64_t it0, int64_t n, double* losses);
 gfnx_status gfnx_synchronize(gfnx_ctx* ctx);
 
+/* Pipelined end-to-end iteration with pinned host staging owned by the ctx.
+ * gfnx_iteration_async enqueues iteration `it` (as gfnx_iteration) followed by
+ * device->host copies of its loss, lengths, log-rewards and packed terminal states into
+ * pinned slot `slot` (0 or 1) and returns without waiting; gfnx_slot_wait blocks until
+ * that slot's copies have landed and returns pointers into the pinned slot (valid until
+ * the slot is reused). A host loop alternates slots so the device never waits for the
+ * host (what train_scenario does with the batch: buffer.push_batch, train.cpp:231). */
+typedef struct gfnx_slot_view {
+  int64_t it;
+  double loss;
+  int32_t n; /* local trajectories */
+  int32_t state_words;
+  const int32_t* lengths;
+  const double* log_rewards;
+  const uint32_t* terminal_state;
+} gfnx_slot_view;
+gfnx_status gfnx_iteration_async(gfnx_ctx* ctx, int64_t it, int32_t slot);
+gfnx_status gfnx_slot_wait(gfnx_ctx* ctx, int32_t slot, gfnx_slot_view* out);
+
 /* Host view of this rank's resident batch (TrajectoryBatch fields, trajectory.hpp:15-33).
  * Caller-owned buffers sized by gfnx_batch_dims; NULL pointers are skipped. */
 typedef struct gfnx_host_batch {
@@ -202,6 +221,9 @@ gfnx_status gfnx_event_elapsed(gfnx_ctx* ctx, int32_t slot_a, int32_t slot_b, do
  * number of distinct kernels, their '\n'-separated names, summed ms and launch counts,
  * and clears the record. */
 gfnx_status gfnx_profile(gfnx_ctx* ctx, int32_t enable);
+/* out[0] rows (states) processed since creation, out[1] rollouts, out[2] rows and out[3]
+ * MDB transitions of the resident batch. */
+gfnx_status gfnx_counters(gfnx_ctx* ctx, int64_t* out, int32_t n);
 int32_t gfnx_profile_read(gfnx_ctx* ctx, char* names, int32_t names_cap, double* total_ms,
                           int32_t* counts, int32_t cap);
 

@@ -72,6 +72,12 @@ class HostBatch(C.Structure):
                 ("terminal_state", C.POINTER(C.c_uint32))]
 
 
+class SlotView(C.Structure):
+    _fields_ = [("it", C.c_int64), ("loss", C.c_double), ("n", C.c_int32),
+                ("state_words", C.c_int32), ("lengths", C.POINTER(C.c_int32)),
+                ("log_rewards", C.POINTER(C.c_double)), ("terminal_state", C.POINTER(C.c_uint32))]
+
+
 def env_desc(kind: int, **kw) -> EnvDesc:
     """Defaults of the reference builders (train.cpp:361-366, 388-396, 637-640, 531-583)."""
     e = EnvDesc()

@@ -64,44 +64,6 @@ void cuda_check(cudaError_t e, const char* what) {
 // ---------------------------------------------------------------------------
 // small kernels shared by both precisions
 
-// lengths -> row0 (exclusive prefix), counters[0] = sum L, counters[1] = sum max(L-1, 0);
-// counters[4..5] = the same (global values when world == 1; all-reduced otherwise).
-__global__ void k_row_scan(const int32_t* __restrict__ lengths, int Bl, int32_t* row0,
-                           int32_t* counters) {
-  __shared__ int32_t part[1024], part2[1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int per = (Bl + nt - 1) / nt;
-  const int lo = tid * per, hi = min(Bl, lo + per);
-  int32_t s = 0, s2 = 0;
-  for (int b = lo; b < hi; ++b) {
-    s += lengths[b];
-    s2 += lengths[b] > 1 ? lengths[b] - 1 : 0;
-  }
-  part[tid] = s;
-  part2[tid] = s2;
-  __syncthreads();
-  for (int off = 1; off < nt; off <<= 1) {  // Hillis-Steele inclusive scan
-    int32_t v = tid >= off ? part[tid - off] : 0;
-    int32_t v2 = tid >= off ? part2[tid - off] : 0;
-    __syncthreads();
-    part[tid] += v;
-    part2[tid] += v2;
-    __syncthreads();
-  }
-  int32_t run = tid > 0 ? part[tid - 1] : 0;
-  for (int b = lo; b < hi; ++b) {
-    row0[b] = run;
-    run += lengths[b];
-  }
-  if (tid == nt - 1) {
-    row0[Bl] = part[nt - 1];
-    counters[0] = part[nt - 1];
-    counters[1] = part2[nt - 1];
-    counters[4] = part[nt - 1];
-    counters[5] = part2[nt - 1];
-  }
-}
-
 ProfScope::ProfScope(Ctx& ctx, const char* name) : c(ctx) {
   if (!c.profiling) return;
   auto take = [&]() {
@@ -124,10 +86,102 @@ ProfScope::~ProfScope() {
   if (idx >= 0) cudaEventRecord(c.prof[idx].b, c.stream);
 }
 
+// lengths -> row0 (exclusive prefix of lengths), row_bt (row -> b*T + t), counters:
+// counters[0] = sum L, [1] = sum max(L-1, 0), [4..5] = the same (global when world == 1,
+// all-reduced otherwise), [8..11] = int64 running totals (rows, rollouts) for bench.py.
+// Three coalesced passes over 1024-trajectory blocks (the partial sums are tiny).
+constexpr int kScanBlock = 1024;
+
+__device__ __forceinline__ int block_excl_scan(int v, int* warp_sums, int* total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    int w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sums[lane] = w;  // inclusive over warps
+  }
+  __syncthreads();
+  const int base = warp > 0 ? warp_sums[warp - 1] : 0;
+  if (total) *total = warp_sums[(blockDim.x >> 5) - 1];
+  return base + x - v;
+}
+
+__global__ void k_len_partials(const int32_t* __restrict__ lengths, int Bl, int2* part) {
+  __shared__ int ws[32], ws2[32];
+  const int b = blockIdx.x * kScanBlock + threadIdx.x;
+  const int L = b < Bl ? lengths[b] : 0;
+  int v = L, v2 = L > 1 ? L - 1 : 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    v += __shfl_xor_sync(0xffffffffu, v, o);
+    v2 += __shfl_xor_sync(0xffffffffu, v2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ws[threadIdx.x >> 5] = v;
+    ws2[threadIdx.x >> 5] = v2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int s = 0, s2 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      s += ws[w];
+      s2 += ws2[w];
+    }
+    part[blockIdx.x] = make_int2(s, s2);
+  }
+}
+
+__global__ void k_len_scan_partials(int2* part, int nparts, int32_t* counters) {
+  if (threadIdx.x != 0) return;
+  int run = 0, run2 = 0;
+  for (int i = 0; i < nparts; ++i) {  // <= 64 entries at B = 65536
+    const int2 p = part[i];
+    part[i] = make_int2(run, 0);
+    run += p.x;
+    run2 += p.y;
+  }
+  long long* acc = reinterpret_cast<long long*>(counters + 8);
+  acc[0] += run;
+  acc[1] += 1;
+  counters[0] = run;
+  counters[1] = run2;
+  counters[4] = run;
+  counters[5] = run2;
+}
+
+__global__ void k_len_finish(const int32_t* __restrict__ lengths, int Bl, int T,
+                             const int2* part, int32_t* row0, int32_t* row_bt, const int32_t* counters) {
+  __shared__ int ws[32];
+  const int b = blockIdx.x * kScanBlock + threadIdx.x;
+  const int L = b < Bl ? lengths[b] : 0;
+  const int r0 = part[blockIdx.x].x + block_excl_scan(L, ws, nullptr);
+  if (b < Bl) {
+    row0[b] = r0;
+    for (int t = 0; t < L; ++t) row_bt[r0 + t] = b * T + t;
+  }
+  if (b == Bl) row0[Bl] = counters[0];
+  if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0 && Bl % kScanBlock == 0) row0[Bl] = counters[0];
+}
+
 void launch_row_scan(Ctx& c) {
   ProfScope ps(c, "k_row_scan");
-  k_row_scan<<<1, 1024, 0, c.stream>>>(c.batch.lengths, c.Bl, c.batch.row0, c.batch.counters);
-  c.launches++;
+  const int nb = (c.Bl + kScanBlock - 1) / kScanBlock;
+  int2* part = reinterpret_cast<int2*>(c.batch.scan_part);
+  k_len_partials<<<nb, kScanBlock, 0, c.stream>>>(c.batch.lengths, c.Bl, part);
+  k_len_scan_partials<<<1, 32, 0, c.stream>>>(part, nb, c.batch.counters);
+  k_len_finish<<<nb, kScanBlock, 0, c.stream>>>(c.batch.lengths, c.Bl, c.P.T, part, c.batch.row0,
+                                                c.batch.row_bt, c.batch.counters);
+  c.launches += 3;
 }
 
 int64_t total_rows(Ctx& c) {
@@ -368,9 +422,12 @@ gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     cuda_check(cudaMalloc(&bt.actions, sizeof(int16_t) * (size_t)Bl * T), "batch");
     cuda_check(cudaMalloc(&bt.log_rewards, sizeof(double) * Bl), "batch");
     cuda_check(cudaMalloc(&bt.delta, sizeof(double) * (size_t)Bl * T), "batch");
+    cuda_check(cudaMemset(bt.delta, 0, sizeof(double) * (size_t)Bl * T), "batch");
     cuda_check(cudaMalloc(&bt.nparents, sizeof(uint16_t) * (size_t)Bl * T), "batch");
     cuda_check(cudaMalloc(&bt.term_state, sizeof(uint32_t) * (size_t)Bl * P.SW), "batch");
     cuda_check(cudaMalloc(&bt.row0, sizeof(int32_t) * (Bl + 1)), "batch");
+    cuda_check(cudaMalloc(&bt.row_bt, sizeof(int32_t) * ((size_t)Bl * T + 1)), "batch");
+    cuda_check(cudaMalloc(&bt.scan_part, sizeof(int32_t) * 2 * ((Bl + 1023) / 1024 + 1)), "batch");
     cuda_check(cudaMalloc(&bt.counters, sizeof(int32_t) * 16), "batch");
     cuda_check(cudaMemset(bt.counters, 0, sizeof(int32_t) * 16), "batch");
     // parameters
@@ -433,6 +490,7 @@ void gfnx_destroy(gfnx_ctx* h) {
                   c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars,
                   c.batch.lengths, c.batch.actions, c.batch.log_rewards, c.batch.delta,
                   c.batch.nparents, c.batch.term_state, c.batch.row0, c.batch.counters,
+                  c.batch.row_bt, c.batch.scan_part,
                   c.ck_obs, c.ck_act, c.ck_logp, c.ck_mask, c.ck_flow, c.ck_glogp, c.ck_gflow,
                   c.ck_gz, c.ck_gx};
   for (void* p : ptrs)
@@ -446,6 +504,10 @@ void gfnx_destroy(gfnx_ctx* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : c.ev_pool) cudaEventDestroy(e);
+  for (auto& s : c.slots) {
+    if (s.host) cudaFreeHost(s.host);
+    if (s.done) cudaEventDestroy(s.done);
+  }
   if (c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }
@@ -603,6 +665,64 @@ gfnx_status gfnx_run(gfnx_ctx* h, int64_t it0, int64_t n, double* losses) {
   });
 }
 
+namespace {
+size_t slot_bytes(const Ctx& c) {
+  return 16 + sizeof(int32_t) * c.Bl + sizeof(double) * c.Bl + sizeof(uint32_t) * (size_t)c.Bl * c.P.SW;
+}
+}  // namespace
+
+gfnx_status gfnx_iteration_async(gfnx_ctx* h, int64_t it, int32_t slot) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (slot < 0 || slot > 1) fail(GFNX_ERR_CONFIG, "slot must be 0 or 1");
+    Ctx::Slot& s = c.slots[slot];
+    if (!s.host) {
+      cuda_check(cudaHostAlloc((void**)&s.host, slot_bytes(c), cudaHostAllocDefault), "pinned slot");
+      cuda_check(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "slot event");
+    }
+    do_rollout(c, it, schedule_value(c.train.explore, it));
+    do_train(c, true, schedule_value(c.train.lr, it), nullptr);
+    uint8_t* p = s.host;
+    cudaMemcpyAsync(p, c.d_scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, c.stream);
+    cudaMemcpyAsync(p + 8, c.batch.counters + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
+    p += 16;
+    cudaMemcpyAsync(p, c.batch.lengths, sizeof(int32_t) * c.Bl, cudaMemcpyDeviceToHost, c.stream);
+    p += sizeof(int32_t) * c.Bl;
+    cudaMemcpyAsync(p, c.batch.log_rewards, sizeof(double) * c.Bl, cudaMemcpyDeviceToHost, c.stream);
+    p += sizeof(double) * c.Bl;
+    cudaMemcpyAsync(p, c.batch.term_state, sizeof(uint32_t) * (size_t)c.Bl * c.P.SW,
+                    cudaMemcpyDeviceToHost, c.stream);
+    cuda_check(cudaEventRecord(s.done, c.stream), "slot record");
+    s.it = it;
+  });
+}
+
+gfnx_status gfnx_slot_wait(gfnx_ctx* h, int32_t slot, gfnx_slot_view* out) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (slot < 0 || slot > 1 || !c.slots[slot].host) fail(GFNX_ERR_CONFIG, "slot not in use");
+    Ctx::Slot& s = c.slots[slot];
+    cuda_check(cudaEventSynchronize(s.done), "slot wait");
+    int32_t err = 0;
+    memcpy(&err, s.host + 8, sizeof err);
+    if (err != 0) {
+      cudaMemsetAsync(c.batch.counters + 3, 0, sizeof(int32_t), c.stream);
+      fail((gfnx_status)err, "device error in iteration " + std::to_string(s.it));
+    }
+    uint8_t* p = s.host;
+    out->it = s.it;
+    memcpy(&out->loss, p, sizeof(double));
+    out->n = c.Bl;
+    out->state_words = c.P.SW;
+    p += 16;
+    out->lengths = reinterpret_cast<const int32_t*>(p);
+    p += sizeof(int32_t) * c.Bl;
+    out->log_rewards = reinterpret_cast<const double*>(p);
+    p += sizeof(double) * c.Bl;
+    out->terminal_state = reinterpret_cast<const uint32_t*>(p);
+  });
+}
+
 gfnx_status gfnx_synchronize(gfnx_ctx* h) {
   return guard(h, [&] {
     cuda_check(cudaStreamSynchronize(h->c.stream), "sync");
@@ -630,6 +750,7 @@ gfnx_status gfnx_export_batch(gfnx_ctx* h, gfnx_host_batch* out) {
     if (out->log_rewards) cuda_check(cudaMemcpy(out->log_rewards, c.batch.log_rewards, sizeof(double) * Bl, cudaMemcpyDeviceToHost), "export");
     if (out->delta_log_reward) cuda_check(cudaMemcpy(out->delta_log_reward, c.batch.delta, sizeof(double) * bt, cudaMemcpyDeviceToHost), "export");
     if (out->terminal_state) cuda_check(cudaMemcpy(out->terminal_state, c.batch.term_state, sizeof(uint32_t) * Bl * c.P.SW, cudaMemcpyDeviceToHost), "export");
+    if (!out->fwd_actions && !out->bwd_actions && !out->log_pb) return;
     std::vector<int16_t> a(bt);
     std::vector<uint16_t> np(bt);
     cuda_check(cudaMemcpy(a.data(), c.batch.actions, sizeof(int16_t) * bt, cudaMemcpyDeviceToHost), "export");
@@ -687,6 +808,19 @@ gfnx_status gfnx_event_elapsed(gfnx_ctx* h, int32_t a, int32_t b, double* ms) {
     float f = 0.f;
     cuda_check(cudaEventElapsedTime(&f, c.user_ev[a], c.user_ev[b]), "elapsed");
     *ms = f;
+  });
+}
+
+gfnx_status gfnx_counters(gfnx_ctx* h, int64_t* out, int32_t n) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    int32_t raw[16];
+    cuda_check(cudaMemcpyAsync(raw, c.batch.counters, sizeof raw, cudaMemcpyDeviceToHost, c.stream), "counters");
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
+    int64_t acc[2];
+    memcpy(acc, raw + 8, sizeof acc);
+    const int64_t vals[4] = {acc[0], acc[1], raw[0], raw[1]};
+    for (int i = 0; i < n && i < 4; ++i) out[i] = vals[i];
   });
 }
 

@@ -32,6 +32,8 @@ struct DeviceBatch {
   uint16_t* nparents = nullptr;   // [Bl * T] #legal backward actions at s_{t+1} (log_pb = -log n)
   uint32_t* term_state = nullptr; // [Bl * SW]
   int32_t* row0 = nullptr;        // [Bl + 1] exclusive prefix of lengths
+  int32_t* row_bt = nullptr;      // [sum L] row -> b * T + t (state row of the training pass)
+  int32_t* scan_part = nullptr;   // scan scratch
   int32_t* counters = nullptr;    // [4]: total rows, mdb rows, work counter, error word
 };
 
@@ -109,6 +111,13 @@ struct Ctx {
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t user_ev[16] = {};
+  // pinned staging slots for gfnx_iteration_async
+  struct Slot {
+    uint8_t* host = nullptr;  // [loss f64 | err i32 pad | lengths | log_rewards | term_state]
+    cudaEvent_t done = nullptr;
+    int64_t it = -1;
+  };
+  Slot slots[2];
   // per-kernel CUDA-event profiling (bench.py roofline): records (name, start, stop)
   struct ProfRec {
     const char* name;

@@ -34,6 +34,7 @@ namespace {
 
 constexpr int kTile = 128;  // rows (trajectory slots) per CTA tile = TMEM lanes
 constexpr int kHeadMax = 32;
+constexpr int kGatherMax = 8;  // one-hot features gathered per row in the training forward
 
 struct FastState {
   int num_sms = 0;
@@ -45,6 +46,7 @@ struct FastState {
   uint32_t* stst = nullptr;           // [Bl*T][SW] state before each step
   __nv_bfloat16 *h1 = nullptr, *h2 = nullptr, *dz1 = nullptr, *dz2 = nullptr;  // tile images
   __nv_bfloat16* dhead = nullptr;     // tile images [tiles][128][64]
+  uint32_t *mask1 = nullptr, *mask2 = nullptr;  // ReLU bit masks [rows][H/32]
   float* rowbuf = nullptr;            // per row: probs[A], lpa, lps, flow, pad
   float* coef = nullptr;              // per row: ga, gs, gflow, pad
   float* wpart = nullptr;             // [num_sms][n_params] partial gradients
@@ -142,15 +144,6 @@ GFNX_DEV void bulk_g2s_big(void* dst, const void* src, uint32_t bytes, uint64_t*
   }
 }
 
-__device__ int find_traj(const int32_t* row0, int Bl, int r) {
-  int lo = 0, hi = Bl;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (row0[mid] <= r) lo = mid; else hi = mid;
-  }
-  return lo;
-}
-
 // reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100)
 // in fp64 on the fp32 logits of one row
 template <class Env, int AMAX>
@@ -192,6 +185,13 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 
 // ---------------------------------------------------------------------------
 // k_fast_rollout
+//
+// 256 threads per CTA, two per trajectory slot: warp w serves TMEM lane quarter (w % 4)
+// and column half (w / 4), so every slot's 256-wide hidden vector is split across two
+// threads (tcgen05.ld lane-quarter rule). Half-0 threads own the environment state and
+// do the sampling; half-1 threads contribute partial head logits through smem.
+
+constexpr int kThreads = 256;
 
 struct RolloutArgs {
   EnvParams P;
@@ -205,134 +205,157 @@ struct RolloutArgs {
 };
 
 template <int H>
-constexpr int rollout_smem_bytes(int T) {
-  return H * H * 2 + kTile * H * 2 + 3 * H * 4 + 16 * 128 + 64 + 1024;
+constexpr int rollout_smem_bytes() {
+  return H * H * 2 + kTile * H * 2 + 1024;
+}
+
+GFNX_DEV uint8_t* align1024(uint8_t* p) {
+  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
 }
 
 template <class Env, int H, int AMAX>
-__global__ void __launch_bounds__(kTile, 1) k_fast_rollout(RolloutArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* w2img = smem;                       // H x H bf16
-  uint8_t* atile = w2img + H * H * 2;          // 128 x H bf16
-  float* h1init = (float*)(atile + kTile * H * 2);
-  float* b2s = h1init + H;
-  float* b1s = b2s + H;
-  Key* skeys = (Key*)(b1s + H);                // up to 128 step keys
-  uint64_t* mbar = (uint64_t*)(skeys + 128);
-  uint32_t* tbase = (uint32_t*)(mbar + 1);
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* w2img = smem;                 // H x H bf16 (resident for the whole rollout)
+  uint8_t* atile = w2img + H * H * 2;    // 128 x H bf16 layer-1 activations
+  constexpr int HC = H / 2;
+  __shared__ float h1init[H], b2s[H];
+  __shared__ __align__(16) float wfs[H * AMAX];  // head weights, zero padded to AMAX
+  __shared__ float bfs[AMAX];
+  __shared__ Key skeys[128];
+  __shared__ __align__(16) float part[kTile][AMAX];
+  __shared__ int row_nd[kTile], row_df[kTile][4];
+  __shared__ float row_dv[kTile][4];
+  __shared__ uint8_t row_init[kTile];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
 
   const EnvParams& P = a.P;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, c0 = half * HC;
   const int T = P.T, A = P.A;
-  if (warp == 0) tmem_alloc<2 * H>(tbase);
+  if (warp == 0) tmem_alloc<2 * H>(&tbase);
   if (tid == 0) {
-    mbar_init(mbar, 1);
+    mbar_init(&mbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_arrive_expect_tx(mbar, H * H * 2);
-    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, mbar);
+    mbar_arrive_expect_tx(&mbar, H * H * 2);
+    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
   }
-  for (int t = tid; t < T && t < 128; t += blockDim.x) skeys[t] = fold_in(a.key, (uint64_t)t);
-  for (int j = tid; j < H; j += blockDim.x) {
-    b2s[j] = a.W.b2[j];
-    b1s[j] = a.W.b1[j];
+  for (int t = tid; t < T && t < 128; t += kThreads) skeys[t] = fold_in(a.key, (uint64_t)t);
+  for (int j = tid; j < H; j += kThreads) b2s[j] = a.W.b2[j];
+  for (int e = tid; e < H * AMAX; e += kThreads) {
+    const int j = e / AMAX, c = e % AMAX;
+    wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
   }
-  __syncthreads();
-  {  // h1init = b1 + x(s0) W1  (layer-1 pre-activation of the initial state)
+  if (tid < AMAX) bfs[tid] = tid < A ? a.W.bf[tid] : 0.f;
+  {  // h1init = b1 + x(s0) W1 (layer-1 pre-activation of the initial state)
     typename Env::State s0;
     Env::reset(P, s0);
-    for (int j = tid; j < H; j += blockDim.x) {
-      float v = b1s[j];
+    for (int j = tid; j < H; j += kThreads) {
+      float v = a.W.b1[j];
       Env::features(P, s0, [&](int f, double x) { v += (float)x * __bfloat162float(a.W.w1[(size_t)f * H + j]); });
       h1init[j] = v;
     }
   }
-  mbar_wait(mbar, 0);
+  mbar_wait(&mbar, 0);
   uint32_t phase = 1;
   tc_fence_after();
   __syncthreads();
-  const uint32_t tmem = *tbase;
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem = tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
 
   typename Env::State s;
-  int b = atomicAdd(a.work, 1);
-  bool active = b < a.Bl;
   Env::reset(P, s);
-  int tstep = 0;
-  bool need_init = true;
-  int nd = 0;
-  int df[4];
-  float dv[4];
-  bool bad = false;
+  int b = -1, tstep = 0;
+  bool active = false, bad = false;
+  if (half == 0) {
+    b = atomicAdd(a.work, 1);
+    active = b < a.Bl;
+    row_init[row] = 1;
+    row_nd[row] = 0;
+  }
   while (__syncthreads_or(active)) {
-    // (1) layer-1 pre-activation (fp32, TMEM columns [H, 2H)) and its bf16 ReLU tile
+    // (1) layer-1 pre-activation (fp32 in TMEM columns [H, 2H)), own column half
+    const bool init = row_init[row];
+    const int nd = row_nd[row];
 #pragma unroll 1
-    for (int q = 0; q < H / 32; ++q) {
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
       uint32_t r[32];
-      tmem_ld32(lane_base + H + q * 32, r);  // warp-collective: executed by every lane
+      tmem_ld32(lane_base + H + col, r);  // warp-collective: every lane executes it
       tmem_wait_ld();
-      if (need_init) {
+      if (init) {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(h1init[q * 32 + i]);
+        for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(h1init[col + i]);
       } else {
         for (int d = 0; d < nd; ++d) {
-          const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)df[d] * H + q * 32);
+          const float dv = row_dv[row][d];
+          const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)row_df[row][d] * H + col);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             const uint4 w = __ldg(wr + c);
             const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv[d] * bf16_lo(wv[e]));
-              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv[d] * bf16_hi(wv[e]));
+              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv * bf16_lo(wv[e]));
+              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv * bf16_hi(wv[e]));
             }
           }
         }
       }
-      tmem_st32(lane_base + H + q * 32, r);
+      tmem_st32(lane_base + H + col, r);
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
-      st_row32(atile, tid, q * 32, pk);
+      st_row32(atile, row, col, pk);
     }
     tmem_wait_st();
     fence_proxy_async();
     tc_fence_before();
     __syncthreads();
-    // (2) hidden layer on the tensor cores
+    // (2) hidden layer on the tensor cores: acc[128 x H] = relu(h1) W2^T
     if (tid == 0) {
       tc_fence_after();
       mma_kk<H, H>(tmem, atile, w2img, false);
-      umma_commit(mbar);
+      umma_commit(&mbar);
     }
-    mbar_wait(mbar, phase);
+    mbar_wait(&mbar, phase);
     phase ^= 1;
     tc_fence_after();
-    // (3) epilogue: h2 = ReLU(acc + b2) -> head logits (SIMT, A <= AMAX)
+    // (3) epilogue: h2 = ReLU(acc + b2) (bf16-rounded, as the training pass sees it) -> logits
     float logit[AMAX];
 #pragma unroll
-    for (int c = 0; c < AMAX; ++c) logit[c] = c < A ? __ldg(a.W.bf + c) : 0.f;
+    for (int c = 0; c < AMAX; ++c) logit[c] = 0.f;
 #pragma unroll 1
-    for (int q = 0; q < H / 32; ++q) {
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
       uint32_t r[32];
-      tmem_ld32(lane_base + q * 32, r);
+      tmem_ld32(lane_base + col, r);
       tmem_wait_ld();
-#pragma unroll 4
-      for (int i = 0; i < 32; ++i) {
-        const float h = __bfloat162float(__float2bfloat16(fmaxf(__uint_as_float(r[i]) + b2s[q * 32 + i], 0.f)));
-        const float* wr = a.W.wf + (size_t)(q * 32 + i) * A;
 #pragma unroll
-        for (int c = 0; c < AMAX; ++c)
-          if (c < A) logit[c] += h * __ldg(wr + c);
+      for (int i = 0; i < 32; ++i) {
+        const float h = __bfloat162float(__float2bfloat16(fmaxf(__uint_as_float(r[i]) + b2s[col + i], 0.f)));
+        const float* wr = wfs + (col + i) * AMAX;
+#pragma unroll
+        for (int c = 0; c < AMAX; ++c) logit[c] += h * wr[c];
       }
     }
+    if (half == 1) {
+#pragma unroll
+      for (int c = 0; c < AMAX; ++c) part[row][c] = logit[c];
+    }
     tc_fence_before();
-    // (4) sample, step, record; refill finished slots
-    if (active) {
+    __syncthreads();
+    // (4) sample, step, record; refill finished slots (half-0 threads own the slots)
+    if (half == 0 && active) {
+#pragma unroll
+      for (int c = 0; c < AMAX; ++c) logit[c] += part[row][c] + bfs[c];
       const Key dk = fold_in(skeys[tstep], (uint64_t)(a.b0 + b));
       const int act = sample_row<Env, AMAX>(P, s, logit, A, a.eps, uniform_scalar(dk), &bad);
       if (act < 0) {
@@ -340,15 +363,20 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_rollout(RolloutArgs a) {
       } else {
         const size_t bt = (size_t)b * T + tstep;
         Env::pack(P, s, a.stst + bt * P.SW);
-        nd = 0;
-        Env::delta_features(P, s, act, [&](int f, float v) { df[nd] = f; dv[nd] = v; ++nd; });
+        int n = 0;
+        Env::delta_features(P, s, act, [&](int f, float v) {
+          row_df[row][n] = f;
+          row_dv[row][n] = v;
+          ++n;
+        });
+        row_nd[row] = n;
+        row_init[row] = 0;
         const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
         const bool term = Env::step(P, s, act);
         a.batch.actions[bt] = (int16_t)act;
         a.batch.nparents[bt] = (uint16_t)Env::num_parents(P, s);
         if (P.mdb && !term) a.batch.delta[bt] = Env::log_reward(P, s) - prev_r;
         ++tstep;
-        need_init = false;
         if (term) {
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
@@ -357,7 +385,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_rollout(RolloutArgs a) {
           active = b < a.Bl;
           Env::reset(P, s);
           tstep = 0;
-          need_init = true;
+          row_init[row] = 1;
         } else if (tstep >= T) {
           bad = true;
           active = false;
@@ -371,7 +399,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_rollout(RolloutArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_fwd: forward over real rows
+// k_fast_fwd: forward over the real rows (2 threads per row, as in the rollout)
 
 struct TrainArgs {
   EnvParams P;
@@ -380,6 +408,7 @@ struct TrainArgs {
   int Bl;
   const uint32_t* stst;
   __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
+  uint32_t *mask1, *mask2;  // ReLU masks of h1 / h2, [rows][H/32]
   float* rowbuf;
   int rs;
   float* coef;
@@ -391,86 +420,121 @@ struct TrainArgs {
 
 template <int H>
 constexpr int fwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + 2 * H * 4 + 64 + 1024;
+  return H * H * 2 + kTile * H * 2 + 1024;
 }
 
 template <class Env, int H, int AMAX>
-__global__ void __launch_bounds__(kTile, 1) k_fast_fwd(TrainArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint8_t* w2img = smem;
   uint8_t* atile = w2img + H * H * 2;
-  float* b1s = (float*)(atile + kTile * H * 2);
-  float* b2s = b1s + H;
-  uint64_t* mbar = (uint64_t*)(b2s + H);
-  uint32_t* tbase = (uint32_t*)(mbar + 1);
+  constexpr int HC = H / 2;
+  __shared__ float b1s[H], b2s[H], wfls[H];
+  __shared__ __align__(16) float wfs[H * AMAX];
+  __shared__ float bfs[AMAX + 1];
+  __shared__ __align__(16) float part[kTile][AMAX + 1];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, c0 = half * HC;
   const int T = P.T, A = P.A;
   const int R = a.batch.counters[0];
   const int tiles = (R + kTile - 1) / kTile;
   if ((int)blockIdx.x >= tiles) return;
-  if (warp == 0) tmem_alloc<H>(tbase);
+  if (warp == 0) tmem_alloc<H>(&tbase);
   if (tid == 0) {
-    mbar_init(mbar, 1);
+    mbar_init(&mbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_arrive_expect_tx(mbar, H * H * 2);
-    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, mbar);
+    mbar_arrive_expect_tx(&mbar, H * H * 2);
+    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
   }
-  for (int j = tid; j < H; j += blockDim.x) {
+  for (int j = tid; j < H; j += kThreads) {
     b1s[j] = a.W.b1[j];
     b2s[j] = a.W.b2[j];
+    wfls[j] = a.W.wfl[j];
   }
-  mbar_wait(mbar, 0);
+  for (int e = tid; e < H * AMAX; e += kThreads) {
+    const int j = e / AMAX, c = e % AMAX;
+    wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
+  }
+  if (tid < AMAX) bfs[tid] = tid < A ? a.W.bf[tid] : 0.f;
+  if (tid == 0) bfs[AMAX] = a.W.bfl[0];
+  mbar_wait(&mbar, 0);
   uint32_t phase = 1;
   tc_fence_after();
   __syncthreads();
-  const uint32_t tmem = *tbase;
-  const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t tmem = tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
   const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-    const int r = tile * kTile + tid;
+    const int r = tile * kTile + row;
     const bool valid = r < R;
     typename Env::State s;
     Env::reset(P, s);
     int act = 0;
     if (valid) {
-      const int b = find_traj(a.batch.row0, a.Bl, r);
-      const int t = r - a.batch.row0[b];
-      const size_t bt = (size_t)b * T + t;
+      const size_t bt = (size_t)a.batch.row_bt[r];
       Env::unpack(P, a.stst + bt * P.SW, s);
       act = a.batch.actions[bt];
     }
-    // layer 1 (sparse one-hot gather, fp32) -> bf16 ReLU tile
     if (tid == 0) bulk_wait_read0();  // previous tile's h2 store has left smem
     __syncthreads();
-#pragma unroll 1
-    for (int q = 0; q < H / 32; ++q) {
-      float v[32];
-#pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = b1s[q * 32 + i];
+    // layer 1: sparse one-hot gather (fp32) -> bf16 ReLU tile, own column half.
+    // Features are collected first so the row loads of a chunk are issued back to back.
+    int nf = 0;
+    int fidx[kGatherMax];
+    float fval[kGatherMax];
+    if (valid)
       Env::features(P, s, [&](int f, double x) {
-        const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)f * H + q * 32);
-        const float xf = (float)x;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const uint4 w = __ldg(wr + c);
-          const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            v[8 * c + 2 * e] += xf * bf16_lo(wv[e]);
-            v[8 * c + 2 * e + 1] += xf * bf16_hi(wv[e]);
-          }
+        if (nf < kGatherMax) {
+          fidx[nf] = f;
+          fval[nf] = (float)x;
+          ++nf;
         }
       });
-      uint32_t pk[16];
+    uint32_t m1bits[HC / 32];
+#pragma unroll 1
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
+      float v[32];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
+      for (int i = 0; i < 32; ++i) v[i] = b1s[col + i];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 w[kGatherMax];
+#pragma unroll
+        for (int k = 0; k < kGatherMax; ++k)
+          if (k < nf) w[k] = __ldg(reinterpret_cast<const uint4*>(a.W.w1 + (size_t)fidx[k] * H + col) + c);
+#pragma unroll
+        for (int k = 0; k < kGatherMax; ++k)
+          if (k < nf) {
+            const uint32_t wv[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * c + 2 * e] += fval[k] * bf16_lo(wv[e]);
+              v[8 * c + 2 * e + 1] += fval[k] * bf16_hi(wv[e]);
+            }
+          }
+      }
+      uint32_t pk[16], mb = 0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
         pk[i] = valid ? pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f)) : 0u;
-      st_row32(atile, tid, q * 32, pk);
+        mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
+        mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
+      }
+      m1bits[q] = mb;
+      st_row32(atile, row, col, pk);
+    }
+    if (valid) {
+#pragma unroll
+      for (int q = 0; q < HC / 32; ++q) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = m1bits[q];
     }
     fence_proxy_async();
     tc_fence_before();
@@ -480,40 +544,46 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_fwd(TrainArgs a) {
       bulk_s2g(a.h1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
       bulk_commit();
       mma_kk<H, H>(tmem, atile, w2img, false);
-      umma_commit(mbar);
+      umma_commit(&mbar);
     }
-    mbar_wait(mbar, phase);
+    mbar_wait(&mbar, phase);
     phase ^= 1;
     tc_fence_after();
     if (tid == 0) bulk_wait_read0();
     __syncthreads();
     // epilogue: h2 (bf16-rounded) -> tile; head logits + flow from the rounded values
-    float logit[AMAX];
+    float logit[AMAX + 1];
 #pragma unroll
-    for (int c = 0; c < AMAX; ++c) logit[c] = c < A ? __ldg(a.W.bf + c) : 0.f;
-    float fl = __ldg(a.W.bfl);
+    for (int c = 0; c <= AMAX; ++c) logit[c] = 0.f;
 #pragma unroll 1
-    for (int q = 0; q < H / 32; ++q) {
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
       uint32_t r32[32];
-      tmem_ld32(lane_base + q * 32, r32);
+      tmem_ld32(lane_base + col, r32);
       tmem_wait_ld();
-      uint32_t pk[16];
+      uint32_t pk[16], mb = 0;
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float x0 = fmaxf(__uint_as_float(r32[2 * i]) + b2s[q * 32 + 2 * i], 0.f);
-        const float x1 = fmaxf(__uint_as_float(r32[2 * i + 1]) + b2s[q * 32 + 2 * i + 1], 0.f);
+        const float x0 = fmaxf(__uint_as_float(r32[2 * i]) + b2s[col + 2 * i], 0.f);
+        const float x1 = fmaxf(__uint_as_float(r32[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f);
         pk[i] = valid ? pack_bf16x2(x0, x1) : 0u;
+        mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
+        mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
-#pragma unroll 4
+      if (valid) a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
+#pragma unroll
       for (int i = 0; i < 32; ++i) {
         const float h = (i & 1) ? bf16_hi(pk[i >> 1]) : bf16_lo(pk[i >> 1]);
-        const float* wr = a.W.wf + (size_t)(q * 32 + i) * A;
+        const float* wr = wfs + (col + i) * AMAX;
 #pragma unroll
-        for (int c = 0; c < AMAX; ++c)
-          if (c < A) logit[c] += h * __ldg(wr + c);
-        if (flow) fl += h * __ldg(a.W.wfl + q * 32 + i);
+        for (int c = 0; c < AMAX; ++c) logit[c] += h * wr[c];
+        logit[AMAX] += h * wfls[col + i];
       }
-      st_row32(atile, tid, q * 32, pk);
+      st_row32(atile, row, col, pk);
+    }
+    if (half == 1) {
+#pragma unroll
+      for (int c = 0; c <= AMAX; ++c) part[row][c] = logit[c];
     }
     tc_fence_before();
     fence_proxy_async();
@@ -522,7 +592,9 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_fwd(TrainArgs a) {
       bulk_s2g(a.h2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
       bulk_commit();
     }
-    if (valid) {  // masked log-softmax statistics of the row
+    if (half == 0 && valid) {  // masked log-softmax statistics of the row
+#pragma unroll
+      for (int c = 0; c <= AMAX; ++c) logit[c] += part[row][c] + bfs[c];
       float hi = -INFINITY;
       for (int c = 0; c < A; ++c)
         if (Env::legal(P, s, c)) hi = fmaxf(hi, logit[c]);
@@ -532,9 +604,15 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_fwd(TrainArgs a) {
       const float lse = hi + __logf(z);
       float* out = a.rowbuf + (size_t)r * a.rs;
       for (int c = 0; c < A; ++c) out[c] = Env::legal(P, s, c) ? __expf(logit[c] - lse) : 0.f;
-      out[A] = logit[act] - lse;
-      out[A + 1] = P.stop >= 0 ? logit[P.stop] - lse : 0.f;
-      out[A + 2] = fl;
+      float la = 0.f, ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < AMAX; ++c) {
+        if (c == act) la = logit[c];
+        if (c == P.stop) ls = logit[c];
+      }
+      out[A] = la - lse;
+      out[A + 1] = P.stop >= 0 ? ls - lse : 0.f;
+      out[A + 2] = flow ? logit[AMAX] : 0.f;
       if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
     }
   }
@@ -678,59 +756,66 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_bwd: head backward, dgrad GEMM, ReLU masks, bias gradients
+// k_fast_bwd: head backward, dgrad GEMM, ReLU masks, bias gradients (2 threads per row)
 
 template <int H>
 constexpr int bwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + 64 + 1024;
+  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + 1024;
 }
 
 template <class Env, int H, int AMAX>
-__global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* smem = align1024(smem_raw);
   uint8_t* wdimg = smem;                     // W2 dgrad image [H in][H out]
   uint8_t* atile = wdimg + H * H * 2;        // dz tile
   uint8_t* htile = atile + kTile * H * 2;    // dhead tile [128][64]
-  uint64_t* mbar = (uint64_t*)(htile + kTile * 64 * 2);
-  uint32_t* tbase = (uint32_t*)(mbar + 1);
+  constexpr int HC = H / 2;
+  __shared__ __align__(16) float wfs[H * AMAX];
+  __shared__ float wfls[H];
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, c0 = half * HC;
   const int T = P.T, A = P.A;
   const int R = a.batch.counters[0];
   const int tiles = (R + kTile - 1) / kTile;
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
-  // bias accumulators: thread j owns column j of db1/db2 (H <= 256 => 2 per thread at most)
-  float acc_b1[2] = {0.f, 0.f}, acc_b2[2] = {0.f, 0.f}, acc_bh = 0.f;
+  float acc_b1 = 0.f, acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j
   if ((int)blockIdx.x < tiles) {
-    if (warp == 0) tmem_alloc<H>(tbase);
+    if (warp == 0) tmem_alloc<H>(&tbase);
     if (tid == 0) {
-      mbar_init(mbar, 1);
+      mbar_init(&mbar, 1);
       fence_mbar_init();
     }
     __syncthreads();
     if (tid == 0) {
-      mbar_arrive_expect_tx(mbar, H * H * 2);
-      bulk_g2s_big(wdimg, a.W.w2_dgrad, H * H * 2, mbar);
+      mbar_arrive_expect_tx(&mbar, H * H * 2);
+      bulk_g2s_big(wdimg, a.W.w2_dgrad, H * H * 2, &mbar);
     }
-    mbar_wait(mbar, 0);
+    for (int j = tid; j < H; j += kThreads) wfls[j] = a.W.wfl[j];
+    for (int e = tid; e < H * AMAX; e += kThreads) {
+      const int j = e / AMAX, c = e % AMAX;
+      wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
+    }
+    mbar_wait(&mbar, 0);
     uint32_t phase = 1;
     tc_fence_after();
     __syncthreads();
-    const uint32_t tmem = *tbase;
-    const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
+    const uint32_t tmem = tbase;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int r = tile * kTile + tid;
+      const int r = tile * kTile + row;
       const bool valid = r < R;
       typename Env::State s;
       Env::reset(P, s);
       int act = 0;
       float g_a = 0.f, g_s = 0.f, g_f = 0.f;
       if (valid) {
-        const int b = find_traj(a.batch.row0, a.Bl, r);
-        const int t = r - a.batch.row0[b];
-        const size_t bt = (size_t)b * T + t;
+        const size_t bt = (size_t)a.batch.row_bt[r];
         Env::unpack(P, a.stst + bt * P.SW, s);
         act = a.batch.actions[bt];
         g_a = a.coef[(size_t)r * 4 + 0];
@@ -744,57 +829,59 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
 #pragma unroll
       for (int c = 0; c < AMAX; ++c) {
         float v = 0.f;
-        if (valid && c < A) {
+        if (valid && c < A && Env::legal(P, s, c)) {
           v = -pr[c] * gsum;
           if (c == act) v += g_a;
           if (c == P.stop) v += g_s;
-          if (!Env::legal(P, s, c)) v = 0.f;
         }
         dl[c] = v;
       }
       if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
       __syncthreads();
-      {  // dhead row -> tile (cols [0, A) logits, col A flow)
-        uint32_t pk[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const int c0 = 2 * i, c1 = 2 * i + 1;
-          const float x0 = c0 < A ? dl[c0 < AMAX ? c0 : 0] : (c0 == A ? g_f : 0.f);
-          const float x1 = c1 < A ? dl[c1 < AMAX ? c1 : 0] : (c1 == A ? g_f : 0.f);
-          pk[i] = pack_bf16x2(x0, x1);
-        }
+      if (half == 0) {  // dhead row -> tile (cols [0, A) logits, col A flow)
         uint32_t lo[16], hi[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          lo[i] = pk[i];
-          hi[i] = pk[16 + i];
+        for (int i = 0; i < 32; ++i) {
+          float x0 = 0.f, x1 = 0.f;
+#pragma unroll
+          for (int c = 0; c < AMAX; ++c) {
+            if (c == 2 * i) x0 = dl[c];
+            if (c == 2 * i + 1) x1 = dl[c];
+          }
+          if (2 * i == A) x0 = g_f;
+          if (2 * i + 1 == A) x1 = g_f;
+          const uint32_t v = pack_bf16x2(x0, x1);
+          if (i < 16) lo[i] = v; else hi[i - 16] = v;
         }
-        st_row32(htile, tid, 0, lo);
-        st_row32(htile, tid, 32, hi);
+        st_row32(htile, row, 0, lo);
+        st_row32(htile, row, 32, hi);
       }
-      // dh2 = dlogits Wf^T + dflow Wfl^T, masked by h2 > 0 (h2 from its tile image)
-      const uint8_t* h2img = (const uint8_t*)(a.h2 + (size_t)tile * kTile * H);
+      // dh2 = dlogits Wf^T + dflow Wfl^T, masked by h2 > 0 (ReLU bit masks from k_fast_fwd)
+      uint32_t mk2[HC / 32], mk1[HC / 32];
+#pragma unroll
+      for (int q = 0; q < HC / 32; ++q) {
+        mk2[q] = valid ? a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+        mk1[q] = valid ? a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+      }
 #pragma unroll 1
-      for (int q = 0; q < H / 32; ++q) {
-        float hv[32];
-        ld_row32(h2img, tid, q * 32, hv);
+      for (int q = 0; q < HC / 32; ++q) {
+        const int col = c0 + q * 32;
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) {
           float d2[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int j = q * 32 + i + e;
-            float v = flow ? g_f * __ldg(a.W.wfl + j) : 0.f;
-            const float* wr = a.W.wf + (size_t)j * A;
+            const int j = col + i + e;
+            float v = g_f * wfls[j];
+            const float* wr = wfs + j * AMAX;
 #pragma unroll
-            for (int c = 0; c < AMAX; ++c)
-              if (c < A) v += dl[c] * __ldg(wr + c);
-            d2[e] = hv[i + e] > 0.f ? v : 0.f;
+            for (int c = 0; c < AMAX; ++c) v += dl[c] * wr[c];
+            d2[e] = ((mk2[q] >> (i + e)) & 1u) ? v : 0.f;
           }
           pk[i >> 1] = pack_bf16x2(d2[0], d2[1]);
         }
-        st_row32(atile, tid, q * 32, pk);
+        st_row32(atile, row, col, pk);
       }
       fence_proxy_async();
       tc_fence_before();
@@ -805,43 +892,38 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
         bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
         bulk_commit();
         mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
-        umma_commit(mbar);
+        umma_commit(&mbar);
       }
-      // bias sums of this tile (fixed order over the 128 rows => deterministic)
-      for (int k = 0; k < 2; ++k) {
-        const int j = tid + k * kTile;
-        if (j < H) {
-          float sacc = 0.f;
-          for (int row = 0; row < kTile; ++row)
-            sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(row, j, kTile)));
-          acc_b2[k] += sacc;
-        }
-      }
-      if (tid <= A && tid < 64) {
+      // bias sums of this tile in fixed row order (deterministic); overlaps the MMA
+      if (tid < H) {
         float sacc = 0.f;
-        for (int row = 0; row < kTile; ++row)
-          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(row, tid, kTile)));
+        for (int rr = 0; rr < kTile; ++rr)
+          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(rr, tid, kTile)));
+        acc_b2 += sacc;
+      }
+      if (tid <= A) {
+        float sacc = 0.f;
+        for (int rr = 0; rr < kTile; ++rr)
+          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
         acc_bh += sacc;
       }
-      mbar_wait(mbar, phase);
+      mbar_wait(&mbar, phase);
       phase ^= 1;
       tc_fence_after();
       if (tid == 0) bulk_wait_read0();
       __syncthreads();
-      const uint8_t* h1img = (const uint8_t*)(a.h1 + (size_t)tile * kTile * H);
-#pragma unroll 1
-      for (int q = 0; q < H / 32; ++q) {
+#pragma unroll
+      for (int q = 0; q < HC / 32; ++q) {
+        const int col = c0 + q * 32;
         uint32_t r32[32];
-        tmem_ld32(lane_base + q * 32, r32);
+        tmem_ld32(lane_base + col, r32);
         tmem_wait_ld();
-        float hv[32];
-        ld_row32(h1img, tid, q * 32, hv);
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(hv[2 * i] > 0.f ? __uint_as_float(r32[2 * i]) : 0.f,
-                              hv[2 * i + 1] > 0.f ? __uint_as_float(r32[2 * i + 1]) : 0.f);
-        st_row32(atile, tid, q * 32, pk);
+          pk[i] = pack_bf16x2(((mk1[q] >> (2 * i)) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
+                              ((mk1[q] >> (2 * i + 1)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
+        st_row32(atile, row, col, pk);
       }
       tc_fence_before();
       fence_proxy_async();
@@ -850,14 +932,11 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
         bulk_s2g(a.dz1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
         bulk_commit();
       }
-      for (int k = 0; k < 2; ++k) {
-        const int j = tid + k * kTile;
-        if (j < H) {
-          float sacc = 0.f;
-          for (int row = 0; row < kTile; ++row)
-            sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(row, j, kTile)));
-          acc_b1[k] += sacc;
-        }
+      if (tid < H) {
+        float sacc = 0.f;
+        for (int rr = 0; rr < kTile; ++rr)
+          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(rr, tid, kTile)));
+        acc_b1 += sacc;
       }
     }
     if (tid == 0) bulk_wait0();
@@ -865,12 +944,9 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_bwd(TrainArgs a) {
     if (warp == 0) tmem_dealloc<H>(tmem);
   }
   // bias partials of this CTA (every CTA writes its slots, zeros when it had no tile)
-  for (int k = 0; k < 2; ++k) {
-    const int j = tid + k * kTile;
-    if (j < H) {
-      part[a.L.off_b[0] + j] = acc_b1[k];
-      part[a.L.off_b[1] + j] = acc_b2[k];
-    }
+  if (tid < H) {
+    part[a.L.off_b[0] + tid] = acc_b1;
+    part[a.L.off_b[1] + tid] = acc_b2;
   }
   if (tid < A) part[a.L.off_fb + tid] = acc_bh;
   if (tid == A) part[a.L.off_flb] = acc_bh;
@@ -962,10 +1038,8 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
       for (int c = 0; c < 16; ++c)
         *reinterpret_cast<uint4*>(bufA + sw128_offset(tid, 8 * c, kTile)) = make_uint4(z4[0], z4[1], z4[2], z4[3]);
       if (r < R) {
-        const int b = find_traj(a.batch.row0, a.Bl, r);
-        const int t = r - a.batch.row0[b];
         typename Env::State s;
-        Env::unpack(P, a.stst + ((size_t)b * T + t) * P.SW, s);
+        Env::unpack(P, a.stst + (size_t)a.batch.row_bt[r] * P.SW, s);
         Env::features(P, s, [&](int f, double x) {
           *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, f, kTile)) = __float2bfloat16((float)x);
         });
@@ -1119,6 +1193,15 @@ AdamArgs adam_args(Ctx& c) {
   return a;
 }
 
+template <class K>
+void set_smem_once(K kernel, int smem) {
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, bytes) already applied
+  for (auto& d : done)
+    if (d.first == (const void*)kernel && d.second >= smem) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done.emplace_back((const void*)kernel, smem);
+}
+
 template <class Env, int H, int AMAX>
 struct Kernels {
   static void rollout(Ctx& c, Key key, double eps) {
@@ -1139,11 +1222,11 @@ struct Kernels {
     if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.lengths, 0, sizeof(int32_t) * c.Bl, c.stream);
     cudaMemsetAsync(f.work, 0, sizeof(int32_t), c.stream);
-    const int smem = rollout_smem_bytes<H>(T);
-    cudaFuncSetAttribute(k_fast_rollout<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int smem = rollout_smem_bytes<H>();
+    set_smem_once(k_fast_rollout<Env, H, AMAX>, smem);
     const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
     ProfScope ps(c, "k_fast_rollout");
-    k_fast_rollout<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(a);
+    k_fast_rollout<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(a);
     c.launches++;
   }
   static void train(Ctx& c, bool apply, double lr) {
@@ -1159,6 +1242,8 @@ struct Kernels {
     ta.dz1 = f.dz1;
     ta.dz2 = f.dz2;
     ta.dhead = f.dhead;
+    ta.mask1 = f.mask1;
+    ta.mask2 = f.mask2;
     ta.rowbuf = f.rowbuf;
     ta.rs = f.rs;
     ta.coef = f.coef;
@@ -1168,10 +1253,10 @@ struct Kernels {
     ta.objective = c.train.objective;
     const int grid = f.num_sms;
     int smem = fwd_smem_bytes<H>();
-    cudaFuncSetAttribute(k_fast_fwd<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem_once(k_fast_fwd<Env, H, AMAX>, smem);
     {
       ProfScope ps(c, "k_fast_fwd");
-      k_fast_fwd<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(ta);
+      k_fast_fwd<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(ta);
     }
     LossArgs la{};
     la.batch = c.batch;
@@ -1196,13 +1281,13 @@ struct Kernels {
     k_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
     smem = bwd_smem_bytes<H>();
-    cudaFuncSetAttribute(k_fast_bwd<Env, H, AMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem_once(k_fast_bwd<Env, H, AMAX>, smem);
     {
       ProfScope ps(c, "k_fast_bwd");
-      k_fast_bwd<Env, H, AMAX><<<grid, kTile, smem, c.stream>>>(ta);
+      k_fast_bwd<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(ta);
     }
     smem = wgrad_smem_bytes<H>();
-    cudaFuncSetAttribute(k_fast_wgrad<Env, H>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    set_smem_once(k_fast_wgrad<Env, H>, smem);
     {
       ProfScope ps(c, "k_fast_wgrad");
       k_fast_wgrad<Env, H><<<grid, kTile, smem, c.stream>>>(ta);
@@ -1229,7 +1314,8 @@ bool supported(const Ctx& c, int* H) {
   if (c.shape.num_actions + 1 > 64 || c.shape.num_actions > kHeadMax) return false;
   if (c.shape.obs_dim > 128) return false;
   if (c.shape.max_traj_len > 128) return false;
-  return c.env.kind == GFNX_ENV_HYPERGRID || c.env.kind == GFNX_ENV_DAG;
+  if (c.env.kind == GFNX_ENV_DAG) return *H == 128;
+  return c.env.kind == GFNX_ENV_HYPERGRID;
 }
 
 template <class F>
@@ -1237,14 +1323,13 @@ void with_kernels(Ctx& c, F&& fn) {
   int H = 0;
   if (!supported(c, &H))
     raise_error(GFNX_ERR_CONFIG,
-                "bf16 fast path supports 2-hidden-layer MLPs (H=128/256) on hypergrid and DAG in "
+                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (H=128/256) and DAG (H=128) in "
                 "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
   if (c.env.kind == GFNX_ENV_HYPERGRID) {
     if (H == 256) fn(Kernels<HypergridEnv, 256, 8>{});
     else fn(Kernels<HypergridEnv, 128, 8>{});
   } else {
-    if (H == 256) fn(Kernels<DagEnv, 256, 32>{});
-    else fn(Kernels<DagEnv, 128, 32>{});
+    fn(Kernels<DagEnv, 128, 32>{});
   }
 }
 
@@ -1254,7 +1339,7 @@ void fast_init(Ctx& c) {
   int H = 0;
   if (!supported(c, &H))
     raise_error(GFNX_ERR_CONFIG,
-                "bf16 fast path supports 2-hidden-layer MLPs (H=128/256) on hypergrid and DAG in "
+                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (H=128/256) and DAG (H=128) in "
                 "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
   auto* f = new FastState();
   c.fast = f;
@@ -1277,6 +1362,8 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->dz1, img), "fast dz1");
   cuda_check(cudaMalloc(&f->dz2, img), "fast dz2");
   cuda_check(cudaMalloc(&f->dhead, (size_t)f->max_tiles * kTile * 64 * 2), "fast dhead");
+  cuda_check(cudaMalloc(&f->mask1, sizeof(uint32_t) * (size_t)f->max_rows * (H / 32)), "fast masks");
+  cuda_check(cudaMalloc(&f->mask2, sizeof(uint32_t) * (size_t)f->max_rows * (H / 32)), "fast masks");
   cuda_check(cudaMalloc(&f->rowbuf, sizeof(float) * (size_t)(f->max_tiles * kTile) * f->rs), "fast rowbuf");
   cuda_check(cudaMalloc(&f->coef, sizeof(float) * (size_t)f->max_rows * 4), "fast coef");
   cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
@@ -1294,6 +1381,7 @@ void fast_free(Ctx& c) {
   FastState* f = static_cast<FastState*>(c.fast);
   if (!f) return;
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
+                  f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work};
   for (void* p : ptrs)
     if (p) cudaFree(p);

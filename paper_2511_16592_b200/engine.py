@@ -78,6 +78,14 @@ def lib():
         L.gfnx_test_threefry.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_test_uniform_fold.argtypes = [C.c_uint64, C.c_uint64, vp, C.c_int64, vp]
         L.gfnx_abi_version.restype = C.c_int32
+        L.gfnx_event_record.argtypes = [vp, C.c_int32]
+        L.gfnx_event_elapsed.argtypes = [vp, C.c_int32, C.c_int32, vp]
+        L.gfnx_profile.argtypes = [vp, C.c_int32]
+        L.gfnx_profile_read.restype = C.c_int32
+        L.gfnx_profile_read.argtypes = [vp, vp, C.c_int32, vp, vp, C.c_int32]
+        L.gfnx_counters.argtypes = [vp, vp, C.c_int32]
+        L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
+        L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
         _LIB = L
     return _LIB
 
@@ -191,23 +199,64 @@ class Trainer:
     def synchronize(self):
         self._check(lib().gfnx_synchronize(self.h))
 
-    def batch(self):
+    def batch(self, fields=None):
         """Host copy of the resident TrajectoryBatch fields (trajectory.hpp:15-33)."""
         B, T, sw = self.local_batch, self.T, self.state_words
         out = dict(lengths=np.zeros(B, np.int32), fwd_actions=np.zeros((B, T), np.int32),
                    bwd_actions=np.zeros((B, T), np.int32), log_rewards=np.zeros(B),
                    log_pb=np.zeros((B, T)), delta=np.zeros((B, T)),
                    terminal_state=np.zeros((B, sw), np.uint32))
+        if fields is not None:
+            out = {k: v for k, v in out.items() if k in fields}
         hb = abi.HostBatch()
-        hb.lengths = out["lengths"].ctypes.data_as(C.POINTER(C.c_int32))
-        hb.fwd_actions = out["fwd_actions"].ctypes.data_as(C.POINTER(C.c_int32))
-        hb.bwd_actions = out["bwd_actions"].ctypes.data_as(C.POINTER(C.c_int32))
-        hb.log_rewards = out["log_rewards"].ctypes.data_as(C.POINTER(C.c_double))
-        hb.log_pb = out["log_pb"].ctypes.data_as(C.POINTER(C.c_double))
-        hb.delta_log_reward = out["delta"].ctypes.data_as(C.POINTER(C.c_double))
-        hb.terminal_state = out["terminal_state"].ctypes.data_as(C.POINTER(C.c_uint32))
+        ptr = {"lengths": C.c_int32, "fwd_actions": C.c_int32, "bwd_actions": C.c_int32,
+               "log_rewards": C.c_double, "log_pb": C.c_double, "delta": C.c_double,
+               "terminal_state": C.c_uint32}
+        field = {"delta": "delta_log_reward"}
+        for k, v in out.items():
+            setattr(hb, field.get(k, k), v.ctypes.data_as(C.POINTER(ptr[k])))
         self._check(lib().gfnx_export_batch(self.h, C.byref(hb)))
         return out
+
+    def iteration_async(self, it: int, slot: int):
+        """Enqueue iteration `it` + D2H of its results into pinned slot `slot` (no wait)."""
+        self._check(lib().gfnx_iteration_async(self.h, it, slot))
+
+    def slot_wait(self, slot: int, copy: bool = True):
+        """Wait for a slot; returns (it, loss, {lengths, log_rewards, terminal_state})."""
+        v = abi.SlotView()
+        self._check(lib().gfnx_slot_wait(self.h, slot, C.byref(v)))
+        n, sw = v.n, v.state_words
+        arr = {"lengths": np.ctypeslib.as_array(v.lengths, shape=(n,)),
+               "log_rewards": np.ctypeslib.as_array(v.log_rewards, shape=(n,)),
+               "terminal_state": np.ctypeslib.as_array(v.terminal_state, shape=(n, sw))}
+        if copy:
+            arr = {k: a.copy() for k, a in arr.items()}
+        return v.it, v.loss, arr
+
+    def event_record(self, slot: int):
+        self._check(lib().gfnx_event_record(self.h, slot))
+
+    def event_elapsed(self, a: int, b: int) -> float:
+        ms = C.c_double()
+        self._check(lib().gfnx_event_elapsed(self.h, a, b, C.byref(ms)))
+        return ms.value
+
+    def profile(self, enable: bool):
+        self._check(lib().gfnx_profile(self.h, 1 if enable else 0))
+
+    def profile_read(self):
+        names = C.create_string_buffer(4096)
+        ms = np.zeros(64)
+        cnt = np.zeros(64, dtype=np.int32)
+        n = lib().gfnx_profile_read(self.h, names, 4096, _p(ms), _p(cnt), 64)
+        keys = names.value.decode().split("\n")[:n]
+        return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}
+
+    def counters(self):
+        out = np.zeros(4, dtype=np.int64)
+        self._check(lib().gfnx_counters(self.h, _p(out), 4))
+        return [int(x) for x in out]
 
     def kernel_launches(self) -> int:
         return lib().gfnx_kernel_launches(self.h)

@@ -115,3 +115,17 @@ def test_fast_run_loop_and_launch_count():
     assert np.all(np.isfinite(losses))
     assert d.kernel_launches() - n0 >= 5 * 8
     d.close()
+
+
+def test_iteration_async_slots_match_batch_export():
+    e, t = _pair("hypergrid_db_b65536", batch=2048)
+    d = engine.Trainer(e, t)
+    d.iteration_async(0, 0)
+    d.iteration_async(1, 1)
+    it0, loss0, r0 = d.slot_wait(0)
+    it1, loss1, r1 = d.slot_wait(1)
+    assert (it0, it1) == (0, 1) and np.isfinite(loss0) and np.isfinite(loss1)
+    b = d.batch()  # resident batch = iteration 1
+    for k in ("lengths", "log_rewards", "terminal_state"):
+        assert np.array_equal(r1[k], b[k]), k
+    d.close()
