@@ -166,6 +166,15 @@ GFNX_DEV void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
       : "r"(taddr));
 }
+GFNX_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
 GFNX_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
@@ -203,6 +212,17 @@ GFNX_DEV uint64_t umma_desc_sw128(uint32_t smem_addr, uint32_t lbo_bytes, uint32
 
 #endif  // __CUDACC__
 
+// Non-swizzled K-major operand: 8-row x 16-byte core matrices, LBO = stride between core
+// matrices along K, SBO = stride between 8-row groups along M/N.
+GFNX_DEV uint64_t umma_desc_none(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version; layout type 0 = SWIZZLE_NONE
+  return d;
+}
+
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(uint32_t M, uint32_t N, bool a_mn,
                                                        bool b_mn) {
   return (1u << 4)                   // D fp32
@@ -232,6 +252,11 @@ GFNX_DEV void umma_commit(uint64_t* bar) {
 }
 
 #endif  // __CUDACC__
+
+// Byte offset of element (row n, k) of a non-swizzled K-major bf16 operand with K columns.
+__host__ __device__ __forceinline__ uint32_t nsw_offset(uint32_t n, uint32_t k, uint32_t K) {
+  return (n >> 3) * (K / 8) * 128u + (k >> 3) * 128u + (n & 7) * 16u + (k & 7) * 2u;
+}
 
 // Byte offset of element (row, col) in a 128B-swizzled bf16 tile image with `rows` rows.
 __host__ __device__ __forceinline__ uint32_t sw128_offset(uint32_t row, uint32_t col,

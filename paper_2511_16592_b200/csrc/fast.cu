@@ -43,6 +43,9 @@ struct FastState {
   __nv_bfloat16* w1 = nullptr;        // [O][H] row-major (layer-1 gathers)
   __nv_bfloat16* w2_fwd = nullptr;    // image [H out][H in] K-major
   __nv_bfloat16* w2_dgrad = nullptr;  // image [H in][H out] K-major
+  __nv_bfloat16* whead_f = nullptr;   // image [NH][H] (head logits + flow)
+  __nv_bfloat16* whead_d = nullptr;   // image [H][NH] non-swizzled (head dgrad)
+  int NH = 16;
   uint32_t* stst = nullptr;           // [Bl*T][SW] state before each step
   __nv_bfloat16 *h1 = nullptr, *h2 = nullptr, *dz1 = nullptr, *dz2 = nullptr;  // tile images
   __nv_bfloat16* dhead = nullptr;     // tile images [tiles][128][64]
@@ -69,6 +72,8 @@ struct Weights {
   const float* bf;   // [A]
   const float* wfl;  // [H]
   const float* bfl;  // [1]
+  const __nv_bfloat16* whead_f;  // head image [NH][H] SW128 K-major (logits + flow rows)
+  const __nv_bfloat16* whead_d;  // head dgrad image [H][NH] non-swizzled K-major
 };
 
 Weights weights_of(Ctx& c) {
@@ -84,6 +89,8 @@ Weights weights_of(Ctx& c) {
   w.bf = c.p32 + L.off_fb;
   w.wfl = c.p32 + L.off_flw;
   w.bfl = c.p32 + L.off_flb;
+  w.whead_f = f.whead_f;
+  w.whead_d = f.whead_d;
   return w;
 }
 
@@ -188,8 +195,13 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 //
 // 256 threads per CTA, two per trajectory slot: warp w serves TMEM lane quarter (w % 4)
 // and column half (w / 4), so every slot's 256-wide hidden vector is split across two
-// threads (tcgen05.ld lane-quarter rule). Half-0 threads own the environment state and
-// do the sampling; half-1 threads contribute partial head logits through smem.
+// threads (tcgen05.ld lane-quarter rule). Per env step:
+//   (1) layer-1 pre-activation updated in TMEM (fp32, columns [H, 2H)) from the features
+//       the last action changed; ReLU -> bf16 A tile in smem
+//   (2) tcgen05.mma 128 x H x H against the smem-resident W2 image
+//   (3) ReLU(acc + b2) -> bf16 h2 tile in smem (half-1 threads also draw the row's uniform)
+//   (4) tcgen05.mma 128 x NH x H head (logits + flow) -> TMEM, then half-0 threads sample,
+//       step the env, record, and refill finished slots from the global work counter.
 
 constexpr int kThreads = 256;
 
@@ -204,27 +216,28 @@ struct RolloutArgs {
   int32_t* work;
 };
 
-template <int H>
+template <int H, int NH>
 constexpr int rollout_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + 1024;
+  return H * H * 2 + kTile * H * 2 + NH * H * 2 + 1024;
 }
 
 GFNX_DEV uint8_t* align1024(uint8_t* p) {
   return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
 }
 
-template <class Env, int H, int AMAX>
+template <class Env, int H, int NH>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* w2img = smem;                 // H x H bf16 (resident for the whole rollout)
-  uint8_t* atile = w2img + H * H * 2;    // 128 x H bf16 layer-1 activations
+  uint8_t* atile = w2img + H * H * 2;    // 128 x H bf16 activations (h1, then h2)
+  uint8_t* whimg = atile + kTile * H * 2;  // head image [NH][H]
   constexpr int HC = H / 2;
   __shared__ float h1init[H], b2s[H];
-  __shared__ __align__(16) float wfs[H * AMAX];  // head weights, zero padded to AMAX
-  __shared__ float bfs[AMAX];
+  __shared__ float bhs[NH];
   __shared__ Key skeys[128];
-  __shared__ __align__(16) float part[kTile][AMAX];
+  __shared__ double row_u[kTile];
+  __shared__ int row_b[kTile], row_t[kTile];
   __shared__ int row_nd[kTile], row_df[kTile][4];
   __shared__ float row_dv[kTile][4];
   __shared__ uint8_t row_init[kTile];
@@ -243,16 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_arrive_expect_tx(&mbar, H * H * 2);
+    mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
+    bulk_g2s_big(whimg, a.W.whead_f, NH * H * 2, &mbar);
   }
   for (int t = tid; t < T && t < 128; t += kThreads) skeys[t] = fold_in(a.key, (uint64_t)t);
   for (int j = tid; j < H; j += kThreads) b2s[j] = a.W.b2[j];
-  for (int e = tid; e < H * AMAX; e += kThreads) {
-    const int j = e / AMAX, c = e % AMAX;
-    wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
-  }
-  if (tid < AMAX) bfs[tid] = tid < A ? a.W.bf[tid] : 0.f;
+  if (tid < NH) bhs[tid] = tid < A ? a.W.bf[tid] : (tid == A ? a.W.bfl[0] : 0.f);
   {  // h1init = b1 + x(s0) W1 (layer-1 pre-activation of the initial state)
     typename Env::State s0;
     Env::reset(P, s0);
@@ -278,6 +288,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     active = b < a.Bl;
     row_init[row] = 1;
     row_nd[row] = 0;
+    row_b[row] = b;
+    row_t[row] = 0;
   }
   while (__syncthreads_or(active)) {
     // (1) layer-1 pre-activation (fp32 in TMEM columns [H, 2H)), own column half
@@ -296,10 +308,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         for (int d = 0; d < nd; ++d) {
           const float dv = row_dv[row][d];
           const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)row_df[row][d] * H + col);
+          uint4 w[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w[c] = __ldg(wr + c);
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint4 w = __ldg(wr + c);
-            const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+            const uint32_t wv[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
               r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv * bf16_lo(wv[e]));
@@ -325,39 +339,56 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       mma_kk<H, H>(tmem, atile, w2img, false);
       umma_commit(&mbar);
     }
+    // half-1 threads draw the row's uniform while the MMA runs (rng.cpp:64-66)
+    if (half == 1) {
+      const int rb = row_b[row];
+      row_u[row] = rb >= 0 && rb < a.Bl
+                       ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb)))
+                       : 0.0;
+    }
     mbar_wait(&mbar, phase);
     phase ^= 1;
     tc_fence_after();
-    // (3) epilogue: h2 = ReLU(acc + b2) (bf16-rounded, as the training pass sees it) -> logits
-    float logit[AMAX];
-#pragma unroll
-    for (int c = 0; c < AMAX; ++c) logit[c] = 0.f;
+    // (3) h2 = ReLU(acc + b2) -> bf16 tile (overwrites h1: the hidden MMA is complete)
 #pragma unroll 1
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
       uint32_t r[32];
       tmem_ld32(lane_base + col, r);
       tmem_wait_ld();
+      uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float h = __bfloat162float(__float2bfloat16(fmaxf(__uint_as_float(r[i]) + b2s[col + i], 0.f)));
-        const float* wr = wfs + (col + i) * AMAX;
-#pragma unroll
-        for (int c = 0; c < AMAX; ++c) logit[c] += h * wr[c];
-      }
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b2s[col + 2 * i], 0.f),
+                            fmaxf(__uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f));
+      st_row32(atile, row, col, pk);
     }
-    if (half == 1) {
-#pragma unroll
-      for (int c = 0; c < AMAX; ++c) part[row][c] = logit[c];
-    }
+    fence_proxy_async();
     tc_fence_before();
     __syncthreads();
-    // (4) sample, step, record; refill finished slots (half-0 threads own the slots)
-    if (half == 0 && active) {
+    // (4) head on the tensor cores: logits[128 x NH] = h2 Wf (+ flow column, unused here)
+    if (tid == 0) {
+      tc_fence_after();
+      mma_kk<NH, H>(tmem, atile, whimg, false);
+      umma_commit(&mbar);
+    }
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    float logit[NH];
+    {
+      uint32_t r[16];
 #pragma unroll
-      for (int c = 0; c < AMAX; ++c) logit[c] += part[row][c] + bfs[c];
-      const Key dk = fold_in(skeys[tstep], (uint64_t)(a.b0 + b));
-      const int act = sample_row<Env, AMAX>(P, s, logit, A, a.eps, uniform_scalar(dk), &bad);
+      for (int c0h = 0; c0h < NH; c0h += 16) {
+        tmem_ld16(lane_base + c0h, r);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) logit[c0h + c] = __uint_as_float(r[c]) + bhs[c0h + c];
+      }
+    }
+    tc_fence_before();
+    if (half == 0 && active) {
+      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], &bad);
       if (act < 0) {
         active = false;
       } else {
@@ -390,6 +421,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           bad = true;
           active = false;
         }
+        row_b[row] = active ? b : -1;
+        row_t[row] = tstep;
       }
     }
   }
@@ -418,29 +451,28 @@ struct TrainArgs {
   int objective;
 };
 
-template <int H>
+template <int H, int NH>
 constexpr int fwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + 1024;
+  return H * H * 2 + kTile * H * 2 + NH * H * 2 + 1024;
 }
 
-template <class Env, int H, int AMAX>
+template <class Env, int H, int NH>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* w2img = smem;
   uint8_t* atile = w2img + H * H * 2;
+  uint8_t* whimg = atile + kTile * H * 2;
   constexpr int HC = H / 2;
-  __shared__ float b1s[H], b2s[H], wfls[H];
-  __shared__ __align__(16) float wfs[H * AMAX];
-  __shared__ float bfs[AMAX + 1];
-  __shared__ __align__(16) float part[kTile][AMAX + 1];
+  __shared__ float b1s[H], b2s[H];
+  __shared__ float bhs[NH];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, c0 = half * HC;
-  const int T = P.T, A = P.A;
+  const int A = P.A;
   const int R = a.batch.counters[0];
   const int tiles = (R + kTile - 1) / kTile;
   if ((int)blockIdx.x >= tiles) return;
@@ -451,20 +483,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   }
   __syncthreads();
   if (tid == 0) {
-    mbar_arrive_expect_tx(&mbar, H * H * 2);
+    mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
+    bulk_g2s_big(whimg, a.W.whead_f, NH * H * 2, &mbar);
   }
   for (int j = tid; j < H; j += kThreads) {
     b1s[j] = a.W.b1[j];
     b2s[j] = a.W.b2[j];
-    wfls[j] = a.W.wfl[j];
   }
-  for (int e = tid; e < H * AMAX; e += kThreads) {
-    const int j = e / AMAX, c = e % AMAX;
-    wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
-  }
-  if (tid < AMAX) bfs[tid] = tid < A ? a.W.bf[tid] : 0.f;
-  if (tid == 0) bfs[AMAX] = a.W.bfl[0];
+  if (tid < NH) bhs[tid] = tid < A ? a.W.bf[tid] : (tid == A ? a.W.bfl[0] : 0.f);
   mbar_wait(&mbar, 0);
   uint32_t phase = 1;
   tc_fence_after();
@@ -498,7 +525,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
           ++nf;
         }
       });
-    uint32_t m1bits[HC / 32];
 #pragma unroll 1
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
@@ -529,12 +555,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
         mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
         mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
-      m1bits[q] = mb;
+      if (valid) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
       st_row32(atile, row, col, pk);
-    }
-    if (valid) {
-#pragma unroll
-      for (int q = 0; q < HC / 32; ++q) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = m1bits[q];
     }
     fence_proxy_async();
     tc_fence_before();
@@ -551,10 +573,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
     tc_fence_after();
     if (tid == 0) bulk_wait_read0();
     __syncthreads();
-    // epilogue: h2 (bf16-rounded) -> tile; head logits + flow from the rounded values
-    float logit[AMAX + 1];
-#pragma unroll
-    for (int c = 0; c <= AMAX; ++c) logit[c] = 0.f;
+    // epilogue: h2 (bf16-rounded) -> tile and ReLU mask
 #pragma unroll 1
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
@@ -571,48 +590,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
         mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
       if (valid) a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const float h = (i & 1) ? bf16_hi(pk[i >> 1]) : bf16_lo(pk[i >> 1]);
-        const float* wr = wfs + (col + i) * AMAX;
-#pragma unroll
-        for (int c = 0; c < AMAX; ++c) logit[c] += h * wr[c];
-        logit[AMAX] += h * wfls[col + i];
-      }
       st_row32(atile, row, col, pk);
-    }
-    if (half == 1) {
-#pragma unroll
-      for (int c = 0; c <= AMAX; ++c) part[row][c] = logit[c];
     }
     tc_fence_before();
     fence_proxy_async();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {  // h2 image out + head GEMM (logits and flow) on the tensor cores
+      tc_fence_after();
       bulk_s2g(a.h2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
       bulk_commit();
+      mma_kk<NH, H>(tmem, atile, whimg, false);
+      umma_commit(&mbar);
     }
-    if (half == 0 && valid) {  // masked log-softmax statistics of the row
+    mbar_wait(&mbar, phase);
+    phase ^= 1;
+    tc_fence_after();
+    float logit[NH];
+    {
+      uint32_t r16[16];
 #pragma unroll
-      for (int c = 0; c <= AMAX; ++c) logit[c] += part[row][c] + bfs[c];
+      for (int c0h = 0; c0h < NH; c0h += 16) {
+        tmem_ld16(lane_base + c0h, r16);
+        tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 16; ++c) logit[c0h + c] = __uint_as_float(r16[c]) + bhs[c0h + c];
+      }
+    }
+    tc_fence_before();
+    if (half == 0 && valid) {  // masked log-softmax statistics of the row
       float hi = -INFINITY;
-      for (int c = 0; c < A; ++c)
-        if (Env::legal(P, s, c)) hi = fmaxf(hi, logit[c]);
+#pragma unroll
+      for (int c = 0; c < NH; ++c)
+        if (c < A && Env::legal(P, s, c)) hi = fmaxf(hi, logit[c]);
       float z = 0.f;
-      for (int c = 0; c < A; ++c)
-        if (Env::legal(P, s, c)) z += __expf(logit[c] - hi);
+#pragma unroll
+      for (int c = 0; c < NH; ++c)
+        if (c < A && Env::legal(P, s, c)) z += __expf(logit[c] - hi);
       const float lse = hi + __logf(z);
       float* out = a.rowbuf + (size_t)r * a.rs;
-      for (int c = 0; c < A; ++c) out[c] = Env::legal(P, s, c) ? __expf(logit[c] - lse) : 0.f;
-      float la = 0.f, ls = 0.f;
+      float la = 0.f, ls = 0.f, fl = 0.f;
 #pragma unroll
-      for (int c = 0; c < AMAX; ++c) {
+      for (int c = 0; c < NH; ++c) {
+        if (c < A) out[c] = Env::legal(P, s, c) ? __expf(logit[c] - lse) : 0.f;
         if (c == act) la = logit[c];
         if (c == P.stop) ls = logit[c];
+        if (c == A) fl = logit[c];
       }
       out[A] = la - lse;
       out[A + 1] = P.stop >= 0 ? ls - lse : 0.f;
-      out[A + 2] = flow ? logit[AMAX] : 0.f;
+      out[A + 2] = flow ? fl : 0.f;
       if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
     }
   }
@@ -756,30 +782,40 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_bwd: head backward, dgrad GEMM, ReLU masks, bias gradients (2 threads per row)
+// k_fast_bwd: dlogits, head dgrad and W2 dgrad on the tensor cores, ReLU masks, bias grads
 
-template <int H>
+template <int H, int NH>
 constexpr int bwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + 1024;
+  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + 1024;
 }
 
-template <class Env, int H, int AMAX>
+// D[128 x N] = A[128 x K] (SW128 tile image) * B[N x K]^T with B non-swizzled (K small)
+template <int N, int K>
+GFNX_DEV void mma_k_sw128_none(uint32_t d_tmem, const void* a_img, const void* b_img) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s)
+    umma_bf16(d_tmem, umma_desc_sw128(a0 + s * 32, 16, 1024),
+              umma_desc_none(b0 + s * 256, 128, (K / 8) * 128), idesc, s > 0 ? 1u : 0u);
+}
+
+template <class Env, int H, int NH>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* wdimg = smem;                     // W2 dgrad image [H in][H out]
   uint8_t* atile = wdimg + H * H * 2;        // dz tile
   uint8_t* htile = atile + kTile * H * 2;    // dhead tile [128][64]
+  uint8_t* whd = htile + kTile * 64 * 2;     // head dgrad image [H][NH], non-swizzled
   constexpr int HC = H / 2;
-  __shared__ __align__(16) float wfs[H * AMAX];
-  __shared__ float wfls[H];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, c0 = half * HC;
-  const int T = P.T, A = P.A;
+  const int A = P.A;
   const int R = a.batch.counters[0];
   const int tiles = (R + kTile - 1) / kTile;
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
@@ -792,13 +828,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     }
     __syncthreads();
     if (tid == 0) {
-      mbar_arrive_expect_tx(&mbar, H * H * 2);
+      mbar_arrive_expect_tx(&mbar, H * H * 2 + H * NH * 2);
       bulk_g2s_big(wdimg, a.W.w2_dgrad, H * H * 2, &mbar);
-    }
-    for (int j = tid; j < H; j += kThreads) wfls[j] = a.W.wfl[j];
-    for (int e = tid; e < H * AMAX; e += kThreads) {
-      const int j = e / AMAX, c = e % AMAX;
-      wfs[e] = c < A ? a.W.wf[(size_t)j * A + c] : 0.f;
+      bulk_g2s_big(whd, a.W.whead_d, H * NH * 2, &mbar);
     }
     mbar_wait(&mbar, 0);
     uint32_t phase = 1;
@@ -810,77 +842,87 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int r = tile * kTile + row;
       const bool valid = r < R;
-      typename Env::State s;
-      Env::reset(P, s);
-      int act = 0;
-      float g_a = 0.f, g_s = 0.f, g_f = 0.f;
-      if (valid) {
-        const size_t bt = (size_t)a.batch.row_bt[r];
-        Env::unpack(P, a.stst + bt * P.SW, s);
-        act = a.batch.actions[bt];
-        g_a = a.coef[(size_t)r * 4 + 0];
-        g_s = a.coef[(size_t)r * 4 + 1];
-        g_f = flow ? a.coef[(size_t)r * 4 + 2] : 0.f;
-      }
-      // dlogits (masked log-softmax backward, tape.cpp:413-434): g_c - p_c * sum(g)
-      float dl[AMAX];
-      const float gsum = g_a + g_s;
-      const float* pr = a.rowbuf + (size_t)r * a.rs;
-#pragma unroll
-      for (int c = 0; c < AMAX; ++c) {
-        float v = 0.f;
-        if (valid && c < A && Env::legal(P, s, c)) {
-          v = -pr[c] * gsum;
-          if (c == act) v += g_a;
-          if (c == P.stop) v += g_s;
-        }
-        dl[c] = v;
-      }
       if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
       __syncthreads();
-      if (half == 0) {  // dhead row -> tile (cols [0, A) logits, col A flow)
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x0 = 0.f, x1 = 0.f;
-#pragma unroll
-          for (int c = 0; c < AMAX; ++c) {
-            if (c == 2 * i) x0 = dl[c];
-            if (c == 2 * i + 1) x1 = dl[c];
-          }
-          if (2 * i == A) x0 = g_f;
-          if (2 * i + 1 == A) x1 = g_f;
-          const uint32_t v = pack_bf16x2(x0, x1);
-          if (i < 16) lo[i] = v; else hi[i - 16] = v;
-        }
-        st_row32(htile, row, 0, lo);
-        st_row32(htile, row, 32, hi);
-      }
-      // dh2 = dlogits Wf^T + dflow Wfl^T, masked by h2 > 0 (ReLU bit masks from k_fast_fwd)
       uint32_t mk2[HC / 32], mk1[HC / 32];
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
         mk2[q] = valid ? a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
         mk1[q] = valid ? a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
       }
-#pragma unroll 1
-      for (int q = 0; q < HC / 32; ++q) {
-        const int col = c0 + q * 32;
-        uint32_t pk[16];
+      if (half == 0) {
+        // dlogits (masked log-softmax backward, tape.cpp:413-434): g_c - p_c * sum(g)
+        typename Env::State s;
+        Env::reset(P, s);
+        int act = 0;
+        float g_a = 0.f, g_s = 0.f, g_f = 0.f;
+        if (valid) {
+          const size_t bt = (size_t)a.batch.row_bt[r];
+          Env::unpack(P, a.stst + bt * P.SW, s);
+          act = a.batch.actions[bt];
+          g_a = a.coef[(size_t)r * 4 + 0];
+          g_s = a.coef[(size_t)r * 4 + 1];
+          g_f = flow ? a.coef[(size_t)r * 4 + 2] : 0.f;
+        }
+        const float gsum = g_a + g_s;
+        const float* pr = a.rowbuf + (size_t)r * a.rs;
+        uint32_t pk[32];
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          float d2[2];
+        for (int i = 0; i < 32; ++i) {
+          float x[2];
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int j = col + i + e;
-            float v = g_f * wfls[j];
-            const float* wr = wfs + j * AMAX;
-#pragma unroll
-            for (int c = 0; c < AMAX; ++c) v += dl[c] * wr[c];
-            d2[e] = ((mk2[q] >> (i + e)) & 1u) ? v : 0.f;
+            const int c = 2 * i + e;
+            float v = 0.f;
+            if (valid && c < A && Env::legal(P, s, c)) {
+              v = -pr[c] * gsum;
+              if (c == act) v += g_a;
+              if (c == P.stop) v += g_s;
+            }
+            if (c == A) v = g_f;
+            x[e] = v;
           }
-          pk[i >> 1] = pack_bf16x2(d2[0], d2[1]);
+          pk[i] = pack_bf16x2(x[0], x[1]);
         }
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          lo[i] = pk[i];
+          hi[i] = pk[16 + i];
+        }
+        st_row32(htile, row, 0, lo);
+        st_row32(htile, row, 32, hi);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      __syncthreads();
+      if (tid == 0) {  // dh2 = dhead Wf^T (+ dflow wfl^T): 128 x H x NH on the tensor cores
+        tc_fence_after();
+        bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
+        bulk_commit();
+        mma_k_sw128_none<H, NH>(tmem, htile, whd);
+        umma_commit(&mbar);
+      }
+      if (tid <= A) {  // head bias sums (fixed row order)
+        float sacc = 0.f;
+        for (int rr = 0; rr < kTile; ++rr)
+          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
+        acc_bh += sacc;
+      }
+      mbar_wait(&mbar, phase);
+      phase ^= 1;
+      tc_fence_after();
+#pragma unroll
+      for (int q = 0; q < HC / 32; ++q) {
+        const int col = c0 + q * 32;
+        uint32_t r32[32];
+        tmem_ld32(lane_base + col, r32);
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(((mk2[q] >> (2 * i)) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
+                              ((mk2[q] >> (2 * i + 1)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
       }
       fence_proxy_async();
@@ -889,7 +931,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       if (tid == 0) {
         tc_fence_after();
         bulk_s2g(a.dz2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
-        bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
         bulk_commit();
         mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
         umma_commit(&mbar);
@@ -900,12 +941,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         for (int rr = 0; rr < kTile; ++rr)
           sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(rr, tid, kTile)));
         acc_b2 += sacc;
-      }
-      if (tid <= A) {
-        float sacc = 0.f;
-        for (int rr = 0; rr < kTile; ++rr)
-          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
-        acc_bh += sacc;
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
@@ -1131,8 +1166,8 @@ struct AdamArgs {
   int do_z;
   double z_lr, zb1, zb2, zeps, zbc1, zbc2;
   MlpLayout L;
-  __nv_bfloat16 *w1, *w2f, *w2d;
-  int H, O;
+  __nv_bfloat16 *w1, *w2f, *w2d, *whf, *whd;
+  int H, O, A, NH;
 };
 
 __device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float pj) {
@@ -1145,6 +1180,19 @@ __device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float 
     const __nv_bfloat16 v = __float2bfloat16(pj);
     *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.w2f + sw128_offset(q, p, a.H)) = v;
     *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.w2d + sw128_offset(p, q, a.H)) = v;
+  } else if ((j >= L.off_fw && j < L.off_fb) || (j >= L.off_flw && j < L.off_flb)) {
+    // head weights: Wf [H p][A c] and the flow column (c = A) into both head images
+    int p, c;
+    if (j < L.off_fb) {
+      p = (int)((j - L.off_fw) / a.A);
+      c = (int)((j - L.off_fw) % a.A);
+    } else {
+      p = (int)(j - L.off_flw);
+      c = a.A;
+    }
+    const __nv_bfloat16 v = __float2bfloat16(pj);
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.whf + sw128_offset(c, p, a.NH)) = v;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.whd + nsw_offset(p, c, a.NH)) = v;
   }
 }
 
@@ -1187,8 +1235,12 @@ AdamArgs adam_args(Ctx& c) {
   a.w1 = f.w1;
   a.w2f = f.w2_fwd;
   a.w2d = f.w2_dgrad;
+  a.whf = f.whead_f;
+  a.whd = f.whead_d;
   a.H = f.H;
   a.O = f.O;
+  a.A = f.A;
+  a.NH = f.NH;
   a.scalars = c.d_scalars;
   return a;
 }
@@ -1202,7 +1254,7 @@ void set_smem_once(K kernel, int smem) {
   done.emplace_back((const void*)kernel, smem);
 }
 
-template <class Env, int H, int AMAX>
+template <class Env, int H, int NH>
 struct Kernels {
   static void rollout(Ctx& c, Key key, double eps) {
     FastState& f = FS(c);
@@ -1222,11 +1274,11 @@ struct Kernels {
     if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.lengths, 0, sizeof(int32_t) * c.Bl, c.stream);
     cudaMemsetAsync(f.work, 0, sizeof(int32_t), c.stream);
-    const int smem = rollout_smem_bytes<H>();
-    set_smem_once(k_fast_rollout<Env, H, AMAX>, smem);
+    const int smem = rollout_smem_bytes<H, NH>();
+    set_smem_once(k_fast_rollout<Env, H, NH>, smem);
     const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
     ProfScope ps(c, "k_fast_rollout");
-    k_fast_rollout<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(a);
+    k_fast_rollout<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(a);
     c.launches++;
   }
   static void train(Ctx& c, bool apply, double lr) {
@@ -1252,11 +1304,11 @@ struct Kernels {
     ta.L = c.L;
     ta.objective = c.train.objective;
     const int grid = f.num_sms;
-    int smem = fwd_smem_bytes<H>();
-    set_smem_once(k_fast_fwd<Env, H, AMAX>, smem);
+    int smem = fwd_smem_bytes<H, NH>();
+    set_smem_once(k_fast_fwd<Env, H, NH>, smem);
     {
       ProfScope ps(c, "k_fast_fwd");
-      k_fast_fwd<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(ta);
+      k_fast_fwd<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(ta);
     }
     LossArgs la{};
     la.batch = c.batch;
@@ -1280,11 +1332,11 @@ struct Kernels {
     }
     k_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
-    smem = bwd_smem_bytes<H>();
-    set_smem_once(k_fast_bwd<Env, H, AMAX>, smem);
+    smem = bwd_smem_bytes<H, NH>();
+    set_smem_once(k_fast_bwd<Env, H, NH>, smem);
     {
       ProfScope ps(c, "k_fast_bwd");
-      k_fast_bwd<Env, H, AMAX><<<grid, kThreads, smem, c.stream>>>(ta);
+      k_fast_bwd<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(ta);
     }
     smem = wgrad_smem_bytes<H>();
     set_smem_once(k_fast_wgrad<Env, H>, smem);
@@ -1303,15 +1355,14 @@ struct Kernels {
   }
 };
 
-template <class Env, int H, int AMAX>
-void dispatch_rollout(Ctx& c, Key key, double eps) { Kernels<Env, H, AMAX>::rollout(c, key, eps); }
+
 
 bool supported(const Ctx& c, int* H) {
   *H = c.L.H();
   if (c.L.n_trunk != 2) return false;
   if (c.L.dims[1] != c.L.dims[2]) return false;
   if (*H != 256 && *H != 128) return false;
-  if (c.shape.num_actions + 1 > 64 || c.shape.num_actions > kHeadMax) return false;
+  if (c.shape.num_actions + 1 > (c.env.kind == GFNX_ENV_HYPERGRID ? 16 : 32)) return false;
   if (c.shape.obs_dim > 128) return false;
   if (c.shape.max_traj_len > 128) return false;
   if (c.env.kind == GFNX_ENV_DAG) return *H == 128;
@@ -1326,8 +1377,8 @@ void with_kernels(Ctx& c, F&& fn) {
                 "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (H=128/256) and DAG (H=128) in "
                 "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
   if (c.env.kind == GFNX_ENV_HYPERGRID) {
-    if (H == 256) fn(Kernels<HypergridEnv, 256, 8>{});
-    else fn(Kernels<HypergridEnv, 128, 8>{});
+    if (H == 256) fn(Kernels<HypergridEnv, 256, 16>{});
+    else fn(Kernels<HypergridEnv, 128, 16>{});
   } else {
     fn(Kernels<DagEnv, 128, 32>{});
   }
@@ -1356,6 +1407,11 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->w1, sizeof(__nv_bfloat16) * (size_t)f->O * H), "fast w1");
   cuda_check(cudaMalloc(&f->w2_fwd, sizeof(__nv_bfloat16) * H * H), "fast w2");
   cuda_check(cudaMalloc(&f->w2_dgrad, sizeof(__nv_bfloat16) * H * H), "fast w2");
+  f->NH = c.env.kind == GFNX_ENV_HYPERGRID ? 16 : 32;
+  cuda_check(cudaMalloc(&f->whead_f, sizeof(__nv_bfloat16) * f->NH * H), "fast whead");
+  cuda_check(cudaMalloc(&f->whead_d, sizeof(__nv_bfloat16) * f->NH * H), "fast whead");
+  cuda_check(cudaMemset(f->whead_f, 0, sizeof(__nv_bfloat16) * f->NH * H), "fast whead");
+  cuda_check(cudaMemset(f->whead_d, 0, sizeof(__nv_bfloat16) * f->NH * H), "fast whead");
   cuda_check(cudaMalloc(&f->stst, sizeof(uint32_t) * (size_t)c.Bl * T * c.P.SW), "fast stst");
   cuda_check(cudaMalloc(&f->h1, img), "fast h1");
   cuda_check(cudaMalloc(&f->h2, img), "fast h2");
@@ -1380,7 +1436,7 @@ void fast_init(Ctx& c) {
 void fast_free(Ctx& c) {
   FastState* f = static_cast<FastState*>(c.fast);
   if (!f) return;
-  void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
+  void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
                   f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work};
   for (void* p : ptrs)
