@@ -27,12 +27,12 @@
 #include <vector>
 
 #include "engine.h"
+#include "fast_common.cuh"
 
 namespace gfnx {
 
 namespace {
 
-constexpr int kTile = 128;  // rows (trajectory slots) per CTA tile = TMEM lanes
 constexpr int kHeadMax = 32;
 constexpr int kGatherMax = 8;  // one-hot features gathered per row in the training forward
 
@@ -94,63 +94,6 @@ Weights weights_of(Ctx& c) {
   return w;
 }
 
-// ---------------------------------------------------------------------------
-// tensor-core helpers (single elected thread issues, accumulator in TMEM)
-
-// D[128 x N] (+)= A[128 x K] * B[N x K]^T, both K-major 128B-swizzled tile images in smem.
-template <int N, int K>
-GFNX_DEV void mma_kk(uint32_t d_tmem, const void* a_img, const void* b_img, bool acc) {
-  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
-  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
-#pragma unroll
-  for (int s = 0; s < K / 16; ++s) {
-    const uint32_t ao = a0 + (s >> 2) * (128 * 128) + (s & 3) * 32;
-    const uint32_t bo = b0 + (s >> 2) * (N * 128) + (s & 3) * 32;
-    umma_bf16(d_tmem, umma_desc_sw128(ao, 16, 1024), umma_desc_sw128(bo, 16, 1024), idesc,
-              (acc || s > 0) ? 1u : 0u);
-  }
-}
-
-// D[128 x N] (+)= A'[128 x 128] * B'[N x 128]^T with A' = act^T, B' = dz^T read MN-major
-// from 128-row tile images: a_img holds features [m0, m0+128) of a tile with 128 rows.
-template <int N>
-GFNX_DEV void mma_mn(uint32_t d_tmem, const void* a_img, int m0, const void* b_img, bool acc) {
-  constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
-  const uint32_t a0 = smem_u32(a_img) + (m0 >> 6) * (128 * 128), b0 = smem_u32(b_img);
-#pragma unroll
-  for (int s = 0; s < kTile / 16; ++s) {
-    const uint32_t ao = a0 + s * 2048, bo = b0 + s * 2048;
-    umma_bf16(d_tmem, umma_desc_sw128(ao, 128 * 128, 1024), umma_desc_sw128(bo, 128 * 128, 1024),
-              idesc, (acc || s > 0) ? 1u : 0u);
-  }
-}
-
-// store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
-GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-    *reinterpret_cast<uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile)) = v;
-  }
-}
-GFNX_DEV void ld_row32(const uint8_t* img, int row, int c0, float (&v)[32]) {
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const uint4 q = *reinterpret_cast<const uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile));
-    v[8 * c + 0] = bf16_lo(q.x); v[8 * c + 1] = bf16_hi(q.x);
-    v[8 * c + 2] = bf16_lo(q.y); v[8 * c + 3] = bf16_hi(q.y);
-    v[8 * c + 4] = bf16_lo(q.z); v[8 * c + 5] = bf16_hi(q.z);
-    v[8 * c + 6] = bf16_lo(q.w); v[8 * c + 7] = bf16_hi(q.w);
-  }
-}
-
-GFNX_DEV void bulk_g2s_big(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  for (uint32_t off = 0; off < bytes; off += 32768) {
-    const uint32_t n = bytes - off < 32768 ? bytes - off : 32768;
-    bulk_g2s((uint8_t*)dst + off, (const uint8_t*)src + off, n, bar);
-  }
-}
-
 // reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100)
 // in fp64 on the fp32 logits of one row
 template <class Env, int AMAX>
@@ -203,7 +146,6 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 //   (4) tcgen05.mma 128 x NH x H head (logits + flow) -> TMEM, then half-0 threads sample,
 //       step the env, record, and refill finished slots from the global work counter.
 
-constexpr int kThreads = 256;
 
 struct RolloutArgs {
   EnvParams P;
@@ -221,9 +163,6 @@ constexpr int rollout_smem_bytes() {
   return H * H * 2 + kTile * H * 2 + NH * H * 2 + 1024;
 }
 
-GFNX_DEV uint8_t* align1024(uint8_t* p) {
-  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
-}
 
 template <class Env, int H, int NH>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
@@ -789,17 +728,6 @@ constexpr int bwd_smem_bytes() {
   return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + 1024;
 }
 
-// D[128 x N] = A[128 x K] (SW128 tile image) * B[N x K]^T with B non-swizzled (K small)
-template <int N, int K>
-GFNX_DEV void mma_k_sw128_none(uint32_t d_tmem, const void* a_img, const void* b_img) {
-  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
-  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
-#pragma unroll
-  for (int s = 0; s < K / 16; ++s)
-    umma_bf16(d_tmem, umma_desc_sw128(a0 + s * 32, 16, 1024),
-              umma_desc_none(b0 + s * 256, 128, (K / 8) * 128), idesc, s > 0 ? 1u : 0u);
-}
-
 template <class Env, int H, int NH>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -1172,6 +1100,7 @@ struct AdamArgs {
 
 __device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float pj) {
   const MlpLayout& L = a.L;
+  if (!a.w1) return;  // env paths that emit their own images (bitseq.cu)
   if (j < L.off_b[0]) {  // W1 [O][H] row-major bf16
     a.w1[j] = __float2bfloat16(pj);
   } else if (j >= L.off_w[1] && j < L.off_b[1]) {  // W2 [in p][out q]
@@ -1243,15 +1172,6 @@ AdamArgs adam_args(Ctx& c) {
   a.NH = f.NH;
   a.scalars = c.d_scalars;
   return a;
-}
-
-template <class K>
-void set_smem_once(K kernel, int smem) {
-  static std::vector<std::pair<const void*, int>> done;  // (kernel, bytes) already applied
-  for (auto& d : done)
-    if (d.first == (const void*)kernel && d.second >= smem) return;
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  done.emplace_back((const void*)kernel, smem);
 }
 
 template <class Env, int H, int NH>
@@ -1387,6 +1307,13 @@ void with_kernels(Ctx& c, F&& fn) {
 }  // namespace
 
 void fast_init(Ctx& c) {
+  if (c.env.kind == GFNX_ENV_BITSEQ) {
+    std::string why;
+    if (!bs_supported(c, &why))
+      raise_error(GFNX_ERR_CONFIG, why + "; use precision=GFNX_PREC_FP64_CHECK for this configuration");
+    bs_init(c);
+    return;
+  }
   int H = 0;
   if (!supported(c, &H))
     raise_error(GFNX_ERR_CONFIG,
@@ -1434,6 +1361,10 @@ void fast_init(Ctx& c) {
 }
 
 void fast_free(Ctx& c) {
+  if (c.env.kind == GFNX_ENV_BITSEQ) {
+    bs_free(c);
+    return;
+  }
   FastState* f = static_cast<FastState*>(c.fast);
   if (!f) return;
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
@@ -1446,6 +1377,10 @@ void fast_free(Ctx& c) {
 }
 
 void fast_sync_weights(Ctx& c) {
+  if (c.env.kind == GFNX_ENV_BITSEQ) {
+    bs_sync_weights(c);
+    return;
+  }
   AdamArgs a = adam_args(c);
   k_emit_images<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a);
   c.launches++;
@@ -1453,10 +1388,18 @@ void fast_sync_weights(Ctx& c) {
 }
 
 void fast_rollout(Ctx& c, Key key, double eps) {
+  if (c.env.kind == GFNX_ENV_BITSEQ) {
+    bs_rollout(c, key, eps);
+    return;
+  }
   with_kernels(c, [&](auto k) { decltype(k)::rollout(c, key, eps); });
 }
 
 void fast_train(Ctx& c, bool apply, double lr, double* /*loss*/) {
+  if (c.env.kind == GFNX_ENV_BITSEQ) {
+    bs_train(c);
+    return;
+  }
   with_kernels(c, [&](auto k) { decltype(k)::train(c, apply, lr); });
 }
 
@@ -1464,7 +1407,16 @@ void fast_adam(Ctx& c, double lr) {
   const int64_t n = c.L.n_params;
   const gfnx_train_desc& s = c.train;
   c.adam_t += 1;
-  AdamArgs a = adam_args(c);
+  const bool bitseq = c.env.kind == GFNX_ENV_BITSEQ;
+  AdamArgs a{};
+  if (!bitseq) a = adam_args(c);
+  a.p = c.p32;
+  a.m = c.m32;
+  a.v = c.v32;
+  a.g = c.g32;
+  a.n = n;
+  a.L = c.L;
+  a.scalars = c.d_scalars;
   a.lr = (float)lr;
   a.b1 = (float)s.beta1;
   a.b2 = (float)s.beta2;
@@ -1482,9 +1434,12 @@ void fast_adam(Ctx& c, double lr) {
     a.zbc1 = 1.0 - pow(s.beta1, (double)c.z_t);
     a.zbc2 = 1.0 - pow(s.beta2, (double)c.z_t);
   }
-  ProfScope ps(c, "k_fast_adam");
-  k_fast_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(a);
-  c.launches++;
+  {
+    ProfScope ps(c, "k_fast_adam");
+    k_fast_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(a);
+    c.launches++;
+  }
+  if (bitseq) bs_sync_weights(c);
 }
 
 }  // namespace gfnx

@@ -1,0 +1,97 @@
+// fast_common.cuh — tensor-core / bulk-copy helpers shared by the fast-path TUs.
+#pragma once
+
+#include <vector>
+
+#include "engine.h"
+
+namespace gfnx {
+namespace {
+
+constexpr int kTile = 128;     // rows per CTA tile = TMEM lanes
+constexpr int kThreads = 256;  // two threads per tile row
+
+// ---------------------------------------------------------------------------
+// tensor-core helpers (single elected thread issues, accumulator in TMEM)
+
+// D[128 x N] (+)= A[128 x K] * B[N x K]^T, both K-major 128B-swizzled tile images in smem.
+template <int N, int K>
+GFNX_DEV void mma_kk(uint32_t d_tmem, const void* a_img, const void* b_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s) {
+    const uint32_t ao = a0 + (s >> 2) * (128 * 128) + (s & 3) * 32;
+    const uint32_t bo = b0 + (s >> 2) * (N * 128) + (s & 3) * 32;
+    umma_bf16(d_tmem, umma_desc_sw128(ao, 16, 1024), umma_desc_sw128(bo, 16, 1024), idesc,
+              (acc || s > 0) ? 1u : 0u);
+  }
+}
+
+// D[128 x N] (+)= A'[128 x 128] * B'[N x 128]^T with A' = act^T, B' = dz^T read MN-major
+// from 128-row tile images: a_img holds features [m0, m0+128) of a tile with 128 rows.
+template <int N>
+GFNX_DEV void mma_mn(uint32_t d_tmem, const void* a_img, int m0, const void* b_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+  const uint32_t a0 = smem_u32(a_img) + (m0 >> 6) * (128 * 128), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < kTile / 16; ++s) {
+    const uint32_t ao = a0 + s * 2048, bo = b0 + s * 2048;
+    umma_bf16(d_tmem, umma_desc_sw128(ao, 128 * 128, 1024), umma_desc_sw128(bo, 128 * 128, 1024),
+              idesc, (acc || s > 0) ? 1u : 0u);
+  }
+}
+
+// store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
+GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    uint4 v = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+    *reinterpret_cast<uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile)) = v;
+  }
+}
+GFNX_DEV void ld_row32(const uint8_t* img, int row, int c0, float (&v)[32]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const uint4 q = *reinterpret_cast<const uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile));
+    v[8 * c + 0] = bf16_lo(q.x); v[8 * c + 1] = bf16_hi(q.x);
+    v[8 * c + 2] = bf16_lo(q.y); v[8 * c + 3] = bf16_hi(q.y);
+    v[8 * c + 4] = bf16_lo(q.z); v[8 * c + 5] = bf16_hi(q.z);
+    v[8 * c + 6] = bf16_lo(q.w); v[8 * c + 7] = bf16_hi(q.w);
+  }
+}
+
+GFNX_DEV void bulk_g2s_big(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  for (uint32_t off = 0; off < bytes; off += 32768) {
+    const uint32_t n = bytes - off < 32768 ? bytes - off : 32768;
+    bulk_g2s((uint8_t*)dst + off, (const uint8_t*)src + off, n, bar);
+  }
+}
+
+GFNX_DEV uint8_t* align1024(uint8_t* p) {
+  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+}
+
+// D[128 x N] = A[128 x K] (SW128 tile image) * B[N x K]^T with B non-swizzled (K small)
+template <int N, int K>
+GFNX_DEV void mma_k_sw128_none(uint32_t d_tmem, const void* a_img, const void* b_img) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t a0 = smem_u32(a_img), b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s)
+    umma_bf16(d_tmem, umma_desc_sw128(a0 + s * 32, 16, 1024),
+              umma_desc_none(b0 + s * 256, 128, (K / 8) * 128), idesc, s > 0 ? 1u : 0u);
+}
+
+template <class K>
+void set_smem_once(K kernel, int smem) {
+  static std::vector<std::pair<const void*, int>> done;  // (kernel, bytes) already applied
+  for (auto& d : done)
+    if (d.first == (const void*)kernel && d.second >= smem) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  done.emplace_back((const void*)kernel, smem);
+}
+
+
+}  // namespace
+}  // namespace gfnx

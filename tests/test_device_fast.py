@@ -129,3 +129,54 @@ def test_iteration_async_slots_match_batch_export():
     for k in ("lengths", "log_rewards", "terminal_state"):
         assert np.array_equal(r1[k], b[k]), k
     d.close()
+
+
+# ---- bit-sequence (non-autoregressive, k = 8) fast path: BASELINE config #3 shape
+def _bitseq(n_bits, batch):
+    e = abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8)
+    t = abi.train_desc(abi.BITSEQ, batch=batch, objective="tb")
+    return e, t
+
+
+def test_bitseq_fast_rollout_bitexact_at_eps1():
+    e, t = _bitseq(120, 128)
+    d = engine.Trainer(e, t)
+    o = O.Oracle(e, t)
+    d.forward_rollout(0, 1.0)
+    o.rollout(0, 1.0)
+    _same_batch(d.batch(), o.batch())
+    d.close()
+
+
+def test_bitseq_fast_loss_and_grads_match_oracle_on_same_batch():
+    e, t = _bitseq(48, 128)
+    d = engine.Trainer(e, t)
+    o = O.Oracle(e, t)
+    d.set_params(*o.params())
+    for it in range(2):
+        d.forward_rollout(it, o.schedule("explore", it))
+        bd = d.batch()
+        o.replay(bd["fwd_actions"])
+        _same_batch(bd, o.batch())
+        ld = d.compute_grads()
+        lo = o.compute_grads()
+        assert abs(ld - lo) <= 2e-2 * abs(lo) + 1e-6, (ld, lo)
+        gd, dzd = d.grads()
+        go, dzo = o.grads()
+        err, cos = _grad_close(gd, go)
+        assert err < 5e-2 and cos > 0.998, (err, cos)
+        assert abs(dzd - dzo) <= 2e-2 * abs(dzo) + 1e-6
+        o.apply_adam(o.schedule("lr", it))
+        d.set_params(*o.params())
+        d.set_adam_state(*o.adam())
+    d.close()
+
+
+def test_bitseq_fast_iterations_run():
+    e, t = _bitseq(120, 1024)
+    d = engine.Trainer(e, t)
+    losses = d.run(0, 3, read_losses=True)
+    assert np.all(np.isfinite(losses))
+    b = d.batch()
+    assert np.all(b["lengths"] == 15)
+    d.close()
