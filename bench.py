@@ -37,6 +37,39 @@ CONFIG = "hypergrid_db_b65536"
 PER_GPU_BATCH = 65536
 METRIC = "trajectories/sec (train iters/sec in config) — hypergrid 20^4 DB, B=65536/GPU"
 UNIT = "trajectories/s"
+# secondary BASELINE configs measured after the headline (device-timed, resident inputs)
+SECONDARY = {
+    "bitseq_tb_b16384": dict(batch=16384, desc="bitseq n=120 k=8 NAR TB, MLP 2x256"),
+    "hypergrid_tb_b16": dict(batch=16, desc="hypergrid 20^4 TB, B=16, MLP 2x256"),
+    "dag_mdb_b8192": dict(batch=8192, desc="DAG d=5 BGe MDB, MLP 2x128"),
+}
+
+
+def secondary_runs(names, steps, warmup, local):
+    from paper_2511_16592_b200 import abi, engine
+    out = {}
+    for name in names:
+        spec = SECONDARY[name]
+        try:
+            e, t = abi.config(name, batch=spec["batch"])
+            t.iterations = 1_000_000
+            tr = engine.Trainer(e, t, device=local)
+            tr.run(0, warmup)
+            tr.synchronize()
+            tr.profile(True)
+            tr.event_record(0)
+            tr.run(warmup, steps)
+            tr.event_record(1)
+            tr.synchronize()
+            ms = tr.event_elapsed(0, 1)
+            prof = tr.profile_read()
+            out[name] = {"workload": spec["desc"], "trajectories_per_s": spec["batch"] * steps / (ms / 1e3),
+                         "iters_per_s": steps / (ms / 1e3), "ms_per_iter": ms / steps,
+                         "kernels_ms_per_iter": {k: round(v[0] / steps, 4) for k, v in prof.items()}}
+            tr.close()
+        except Exception as ex:  # reported, never fatal
+            out[name] = {"error": str(ex)[:300]}
+    return out
 
 
 def dist_env():
@@ -250,6 +283,8 @@ def main():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="trajectories per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--secondary", default="bitseq_tb_b16384,hypergrid_tb_b16,dag_mdb_b8192",
+                    help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
@@ -357,6 +392,10 @@ def main():
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"failed: {ex}"}
 
+    secondary = None
+    if rank == 0 and world == 1 and args.secondary:
+        secondary = secondary_runs([x for x in args.secondary.split(",") if x], max(3, K // 5), 2, local)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
@@ -370,7 +409,7 @@ def main():
                        "mean_traj_len": rows / (args.batch * K) if K else None,
                        "l2": "working set > L2 (bf16 activation images ~2 KB per state row)"},
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kernels,
-            "cpu_baseline": cpu, "clocks": cl,
+            "cpu_baseline": cpu, "clocks": cl, "secondary": secondary,
         }
         print(json.dumps(line))
     tr.close()
