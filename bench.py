@@ -40,6 +40,7 @@ UNIT = "trajectories/s"
 # secondary BASELINE configs measured after the headline (device-timed, resident inputs)
 SECONDARY = {
     "bitseq_tb_b16384": dict(batch=16384, desc="bitseq n=120 k=8 NAR TB, MLP 2x256"),
+    "ising_tb_b32768": dict(batch=32768, desc="Ising 10x10 TB, MLP 4x256"),
     "hypergrid_tb_b16": dict(batch=16, desc="hypergrid 20^4 TB, B=16, MLP 2x256"),
     "dag_mdb_b8192": dict(batch=8192, desc="DAG d=5 BGe MDB, MLP 2x128"),
 }
@@ -283,7 +284,7 @@ def main():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="trajectories per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--secondary", default="bitseq_tb_b16384,hypergrid_tb_b16,dag_mdb_b8192",
+    ap.add_argument("--secondary", default="bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()

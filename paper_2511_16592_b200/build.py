@@ -18,7 +18,7 @@ UNITS = [
     ("api.cu", []),
     ("check.cu", ["--fmad=false"]),
     ("fast.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
-    ("bitseq.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
+    ("lockstep.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
 ]
 HOST_UNITS = ["host.cpp"]
 

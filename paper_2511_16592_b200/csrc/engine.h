@@ -52,13 +52,13 @@ void fast_train(Ctx& c, bool apply, double lr, double* loss);  // gradients -> g
 void fast_adam(Ctx& c, double lr);
 void fast_sync_weights(Ctx& c);  // fp32 master -> bf16 operand images
 
-// bitseq fast path — bitseq.cu
-bool bs_supported(const Ctx& c, std::string* why);
-void bs_init(Ctx& c);
-void bs_free(Ctx& c);
-void bs_sync_weights(Ctx& c);
-void bs_rollout(Ctx& c, Key key, double eps);
-void bs_train(Ctx& c);
+// fixed-length (lockstep) fast path for bitseq / Ising — lockstep.cu
+bool ls_supported(const Ctx& c, std::string* why);
+void ls_init(Ctx& c);
+void ls_free(Ctx& c);
+void ls_sync_weights(Ctx& c);
+void ls_rollout(Ctx& c, Key key, double eps);
+void ls_train(Ctx& c);
 
 // shared small kernels — batch.cu
 void launch_row_scan(Ctx& c);

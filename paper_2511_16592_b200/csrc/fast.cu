@@ -1100,7 +1100,7 @@ struct AdamArgs {
 
 __device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float pj) {
   const MlpLayout& L = a.L;
-  if (!a.w1) return;  // env paths that emit their own images (bitseq.cu)
+  if (!a.w1) return;  // env paths that emit their own images (lockstep.cu)
   if (j < L.off_b[0]) {  // W1 [O][H] row-major bf16
     a.w1[j] = __float2bfloat16(pj);
   } else if (j >= L.off_w[1] && j < L.off_b[1]) {  // W2 [in p][out q]
@@ -1304,14 +1304,16 @@ void with_kernels(Ctx& c, F&& fn) {
   }
 }
 
+bool lockstep(const Ctx& c) { return c.env.kind == GFNX_ENV_BITSEQ || c.env.kind == GFNX_ENV_ISING; }
+
 }  // namespace
 
 void fast_init(Ctx& c) {
-  if (c.env.kind == GFNX_ENV_BITSEQ) {
+  if (lockstep(c)) {
     std::string why;
-    if (!bs_supported(c, &why))
+    if (!ls_supported(c, &why))
       raise_error(GFNX_ERR_CONFIG, why + "; use precision=GFNX_PREC_FP64_CHECK for this configuration");
-    bs_init(c);
+    ls_init(c);
     return;
   }
   int H = 0;
@@ -1361,8 +1363,8 @@ void fast_init(Ctx& c) {
 }
 
 void fast_free(Ctx& c) {
-  if (c.env.kind == GFNX_ENV_BITSEQ) {
-    bs_free(c);
+  if (lockstep(c)) {
+    ls_free(c);
     return;
   }
   FastState* f = static_cast<FastState*>(c.fast);
@@ -1377,8 +1379,8 @@ void fast_free(Ctx& c) {
 }
 
 void fast_sync_weights(Ctx& c) {
-  if (c.env.kind == GFNX_ENV_BITSEQ) {
-    bs_sync_weights(c);
+  if (lockstep(c)) {
+    ls_sync_weights(c);
     return;
   }
   AdamArgs a = adam_args(c);
@@ -1388,16 +1390,16 @@ void fast_sync_weights(Ctx& c) {
 }
 
 void fast_rollout(Ctx& c, Key key, double eps) {
-  if (c.env.kind == GFNX_ENV_BITSEQ) {
-    bs_rollout(c, key, eps);
+  if (lockstep(c)) {
+    ls_rollout(c, key, eps);
     return;
   }
   with_kernels(c, [&](auto k) { decltype(k)::rollout(c, key, eps); });
 }
 
 void fast_train(Ctx& c, bool apply, double lr, double* /*loss*/) {
-  if (c.env.kind == GFNX_ENV_BITSEQ) {
-    bs_train(c);
+  if (lockstep(c)) {
+    ls_train(c);
     return;
   }
   with_kernels(c, [&](auto k) { decltype(k)::train(c, apply, lr); });
@@ -1407,7 +1409,7 @@ void fast_adam(Ctx& c, double lr) {
   const int64_t n = c.L.n_params;
   const gfnx_train_desc& s = c.train;
   c.adam_t += 1;
-  const bool bitseq = c.env.kind == GFNX_ENV_BITSEQ;
+  const bool bitseq = lockstep(c);
   AdamArgs a{};
   if (!bitseq) a = adam_args(c);
   a.p = c.p32;
@@ -1439,7 +1441,7 @@ void fast_adam(Ctx& c, double lr) {
     k_fast_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(a);
     c.launches++;
   }
-  if (bitseq) bs_sync_weights(c);
+  if (bitseq) ls_sync_weights(c);
 }
 
 }  // namespace gfnx

@@ -1,14 +1,23 @@
-// gemm.cuh — pipelined tcgen05 GEMM over tile images, with pluggable epilogues.
+// gemm.cuh — warp-specialised tcgen05 GEMM over tile images, with pluggable epilogues.
 //
 //   C[m][n] = sum_k A[m][k] * B[n][k]
 //
 // A: activation tile images (128-row tiles; per tile `a_kb` K-blocks of 64 columns, each a
 //    16 KB 128B-swizzled block) — the layout every fast-path kernel writes.
 // B: weight images, N-tiles of BN rows; per N-tile `b_kb` K-blocks of BN x 128 B.
-// One CTA (256 threads) per work item (m_tile, n_tile), persistent over items. Thread 0
-// streams K-blocks through a 4-stage smem ring with 1-D bulk copies (TMA engine) and
-// issues tcgen05.mma into a TMEM accumulator; all 8 warps run the epilogue (two threads
-// per row, tcgen05.ld lane quarters), while thread 0 already prefetches the next item.
+//
+// Persistent CTAs over work items (m_tile, n_tile). Warp roles (12 warps):
+//   warp 0      bulk-copy producer (TMA engine, 1-D cp.async.bulk) into a smem ring
+//   warp 1      single-thread tcgen05.mma issuer into one of two TMEM accumulators
+//   warps 4..11 epilogue: tcgen05.ld, two threads per accumulator row (warp w reads TMEM
+//               lane quarter w % 4, column half (w - 4) / 4), Epi callbacks
+// The two accumulators let the MMAs of item i+1 run while the epilogue drains item i.
+//
+// Two B policies:
+//   resident B (KB <= 4): the whole B n-tile (<= 128 KB) stays in smem across consecutive
+//     items of the same n; only A K-blocks stream through a 4-deep ring. Items are handed
+//     out in contiguous n-major chunks so a CTA sees at most a couple of distinct n.
+//   streamed B: A and B K-blocks stream together through a 4-deep ring (K up to A = 3840).
 #pragma once
 
 #include "fast_common.cuh"
@@ -17,10 +26,12 @@ namespace gfnx {
 namespace {
 
 constexpr int kStages = 4;
+constexpr int kGemmThreads = 384;
+constexpr int kEpiThreads = 256;
 
-template <int BN>
+template <int BN, bool kResB>
 constexpr int gemm_smem_bytes() {
-  return kStages * (kTile * 128 + BN * 128) + 1024;
+  return kResB ? 4 * BN * 128 + kStages * kTile * 128 + 1024 : kStages * (kTile * 128 + BN * 128) + 1024;
 }
 
 struct GemmGeom {
@@ -50,116 +61,192 @@ GFNX_DEV float warp_colsum32(float (&v)[32]) {
   return v[0];
 }
 
-// Epi must provide:
-//   struct Args;
-//   static __device__ void apply(const Args&, int m_tile, int n_tile, int row, int col0,
-//                                float (&v)[32], float* scratch);  // 32 output columns
-//   static __device__ void finish(const Args&, int m_tile, int n_tile, const float* scratch);
-// `scratch` is a [4][BN] smem array (per lane-quarter column partials) that finish()
-// reads after a CTA barrier — used for deterministic per-tile column sums.
-template <int BN, class Epi>
-__global__ void __launch_bounds__(kThreads, 1) k_gemm(GemmGeom g, typename Epi::Args e) {
+// Epilogue interface (derive from EpiBase and hide what you need):
+//   struct Args; struct Local;
+//   begin(e, m, n, row, half, loc)                  once per (item, thread) before the chunks
+//   apply(e, m, n, row, col0, v[32], scratch, loc)  32 accumulator columns [col0, col0 + 32)
+//   row_done(e, m, n, row, half, loc)               after the thread's BN/2 columns
+//   finish(e, m, n, scratch)                        after an epilogue barrier (all rows done);
+// `scratch` is a [4][BN] smem array of per-lane-quarter column partials for finish().
+struct EpiBase {
+  struct Local {};
+  template <class Args, class Loc>
+  static __device__ void begin(const Args&, int, int, int, int, Loc&) {}
+  template <class Args, class Loc>
+  static __device__ void row_done(const Args&, int, int, int, int, Loc&) {}
+  template <class Args>
+  static __device__ void finish(const Args&, int, int, const float*) {}
+};
+
+// column-partial slot of the calling epilogue thread
+GFNX_DEV int epi_quarter() { return ((threadIdx.x >> 5) - 4) & 3; }
+
+GFNX_DEV void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+struct ItemSeq {  // the items a CTA processes, in order
+  int first, count, stride;
+  GFNX_DEV int item(int j) const { return first + j * stride; }
+};
+
+template <bool kResB>
+GFNX_DEV ItemSeq item_seq(int items) {
+  if (kResB) {  // contiguous chunk (n-major order keeps the resident B tile)
+    const int per = (items + gridDim.x - 1) / gridDim.x;
+    const int first = blockIdx.x * per;
+    return ItemSeq{first, max(0, min(per, items - first)), 1};
+  }
+  const int c = items > (int)blockIdx.x ? (items - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  return ItemSeq{(int)blockIdx.x, c, (int)gridDim.x};
+}
+
+template <bool kResB>
+GFNX_DEV void item_mn(const GemmGeom& g, int item, int& m, int& n) {
+  if (kResB) {
+    n = item / g.m_tiles;
+    m = g.m0 + item % g.m_tiles;
+  } else {
+    m = g.m0 + item / g.n_tiles;
+    n = item % g.n_tiles;
+  }
+}
+
+template <int BN, bool kResB, class Epi>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmGeom g, typename Epi::Args e) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   constexpr int kStageA = kTile * 128, kStageB = BN * 128;
-  __shared__ uint64_t full[kStages], empty[kStages], accb;
+  constexpr int kRing = kResB ? kStageA : kStageA + kStageB;
+  uint8_t* ring = kResB ? smem + 4 * kStageB : smem;  // resident B occupies the front
+  __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], bfull;
   __shared__ uint32_t tbase;
   __shared__ float scratch[4 * BN];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int quarter = warp & 3, half = warp >> 2;
-  const int row = quarter * 32 + lane;
-  const int items = g.m_tiles * g.n_tiles;
-  if ((int)blockIdx.x >= items) return;
-  if (warp == 0) tmem_alloc<BN>(&tbase);
-  if (tid == 0) {
+  const ItemSeq seq = item_seq<kResB>(g.m_tiles * g.n_tiles);
+  if (seq.count == 0) return;
+  if (warp == 0) tmem_alloc<2 * BN>(&tbase);
+  if (tid == 32) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(&accb, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull[b], 1);
+      mbar_init(&tempty[b], 1);
+    }
+    mbar_init(&bfull, 1);
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tbase;
-  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
-  constexpr uint32_t idesc = umma_idesc_bf16(128, BN, false, false);
-  // producer/consumer state lives in thread 0 only. K-blocks are loaded and consumed in
-  // one global order (item-major); a stage is refilled one block after it was consumed,
-  // so one MMA is always queued behind the one the refill waits for.
-  uint32_t loaded = 0, consumed = 0;
-  uint32_t acc_phase = 0;
-  int pre_item = blockIdx.x, pre_kb = 0;
-  auto next_load = [&]() {
-    if (pre_item >= items) return;
-    const int m = g.m0 + pre_item / g.n_tiles, n = pre_item % g.n_tiles;
-    const uint32_t st = loaded % kStages;
-    if (loaded >= kStages) mbar_wait(&empty[st], ((loaded / kStages) - 1) & 1);
-    uint8_t* sa = smem + st * (kStageA + kStageB);
-    uint8_t* sb = sa + kStageA;
-    mbar_arrive_expect_tx(&full[st], kStageA + kStageB);
-    bulk_g2s(sa, g.A + ((size_t)m * g.a_kb + g.a_kb0 + pre_kb) * kStageA, kStageA, &full[st]);
-    bulk_g2s_big(sb, g.B + ((size_t)n * g.b_kb + pre_kb) * kStageB, kStageB, &full[st]);
-    ++loaded;
-    if (++pre_kb == g.KB) {
-      pre_kb = 0;
-      pre_item += gridDim.x;
-    }
-  };
-  if (tid == 0)
-    for (int i = 0; i < kStages; ++i) next_load();
-  for (int item = blockIdx.x; item < items; item += gridDim.x) {
-    const int m = g.m0 + item / g.n_tiles, n = item % g.n_tiles;
-    if (tid == 0) {
-      tc_fence_after();
-      for (int kb = 0; kb < g.KB; ++kb) {
-        const uint32_t st = consumed % kStages;
-        mbar_wait(&full[st], (consumed / kStages) & 1);
-        tc_fence_after();
-        const uint32_t a0 = smem_u32(smem + st * (kStageA + kStageB));
-        const uint32_t b0 = a0 + kStageA;
-#pragma unroll
-        for (int s = 0; s < 4; ++s)
-          umma_bf16(tmem, umma_desc_sw128(a0 + s * 32, 16, 1024),
-                    umma_desc_sw128(b0 + s * 32, 16, 1024), idesc, (kb > 0 || s > 0) ? 1u : 0u);
-        umma_commit(&empty[st]);
-        ++consumed;
-        if (consumed >= 2) next_load();
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      uint32_t L = 0;
+      int cur_n = -1;
+      for (int j = 0; j < seq.count; ++j) {
+        int m, n;
+        item_mn<kResB>(g, seq.item(j), m, n);
+        if (kResB && n != cur_n) {
+          // all MMAs reading the old B tile have completed once the newest A stage is free
+          if (L > 0) mbar_wait(&empty[(L - 1) % kStages], ((L - 1) / kStages) & 1);
+          mbar_arrive_expect_tx(&bfull, g.KB * kStageB);
+          for (int kb = 0; kb < g.KB; ++kb)
+            bulk_g2s_big(smem + kb * kStageB, g.B + ((size_t)n * g.b_kb + kb) * kStageB, kStageB, &bfull);
+          cur_n = n;
+        }
+        for (int kb = 0; kb < g.KB; ++kb, ++L) {
+          const uint32_t st = L % kStages;
+          if (L >= kStages) mbar_wait(&empty[st], ((L / kStages) - 1) & 1);
+          uint8_t* sa = ring + st * kRing;
+          mbar_arrive_expect_tx(&full[st], kResB ? kStageA : kStageA + kStageB);
+          bulk_g2s(sa, g.A + ((size_t)m * g.a_kb + g.a_kb0 + kb) * kStageA, kStageA, &full[st]);
+          if (!kResB)
+            bulk_g2s_big(sa + kStageA, g.B + ((size_t)n * g.b_kb + kb) * kStageB, kStageB, &full[st]);
+        }
       }
-      umma_commit(&accb);
     }
-    mbar_wait(&accb, acc_phase);
-    acc_phase ^= 1;
-    tc_fence_after();
-#pragma unroll 1
-    for (int q = 0; q < BN / 64; ++q) {
-      const int col0 = half * (BN / 2) + q * 32;
-      uint32_t r[32];
-      tmem_ld32(lane_base + col0, r);
-      tmem_wait_ld();
-      float v[32];
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, BN, false, false);
+      uint32_t C = 0, nb = 0;
+      int cur_n = -1;
+      for (int j = 0; j < seq.count; ++j) {
+        int m, n;
+        item_mn<kResB>(g, seq.item(j), m, n);
+        if (kResB && n != cur_n) {
+          mbar_wait(&bfull, nb & 1);
+          ++nb;
+          cur_n = n;
+        }
+        const uint32_t buf = j & 1, use = j >> 1;
+        if (use >= 1) mbar_wait(&tempty[buf], (use - 1) & 1);
+        tc_fence_after();
+        const uint32_t d = tmem + buf * BN;
+        for (int kb = 0; kb < g.KB; ++kb, ++C) {
+          const uint32_t st = C % kStages;
+          mbar_wait(&full[st], (C / kStages) & 1);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(ring + st * kRing);
+          const uint32_t b0 = kResB ? smem_u32(smem + kb * kStageB) : a0 + kStageA;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-      Epi::apply(e, m, n, row, col0, v, scratch);
+          for (int s = 0; s < 4; ++s)
+            umma_bf16(d, umma_desc_sw128(a0 + s * 32, 16, 1024), umma_desc_sw128(b0 + s * 32, 16, 1024),
+                      idesc, (kb > 0 || s > 0) ? 1u : 0u);
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&tfull[buf]);
+      }
     }
-    tc_fence_before();
-    __syncthreads();  // accumulator drained before the next item's MMAs
-    Epi::finish(e, m, n, scratch);
-    __syncthreads();
+  } else if (warp >= 4) {  // ---- epilogue
+    const int ew = warp - 4, quarter = ew & 3, half = ew >> 2;
+    const int row = quarter * 32 + lane;
+    const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+    for (int j = 0; j < seq.count; ++j) {
+      int m, n;
+      item_mn<kResB>(g, seq.item(j), m, n);
+      const uint32_t buf = j & 1;
+      typename Epi::Local loc;
+      Epi::begin(e, m, n, row, half, loc);
+      mbar_wait(&tfull[buf], (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll 1
+      for (int q = 0; q < BN / 64; ++q) {
+        const int col0 = half * (BN / 2) + q * 32;
+        uint32_t r[32];
+        tmem_ld32(lane_base + buf * BN + col0, r);
+        tmem_wait_ld();
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+        Epi::apply(e, m, n, row, col0, v, scratch, loc);
+      }
+      tc_fence_before();
+      Epi::row_done(e, m, n, row, half, loc);
+      epi_bar();
+      if (tid == 128) mbar_arrive_local(&tempty[buf]);
+      Epi::finish(e, m, n, scratch);
+      epi_bar();
+    }
   }
   __syncthreads();
-  if (warp == 0) tmem_dealloc<BN>(tmem);
+  if (warp == 0) tmem_dealloc<2 * BN>(tmem);
 }
 
 template <int BN, class Epi>
 void launch_gemm(Ctx& c, const char* name, const GemmGeom& g, const typename Epi::Args& e, int num_sms) {
-  const int smem = gemm_smem_bytes<BN>();
-  set_smem_once(k_gemm<BN, Epi>, smem);
   const int items = g.m_tiles * g.n_tiles;
   const int grid = items < num_sms ? items : num_sms;
   ProfScope ps(c, name);
-  k_gemm<BN, Epi><<<grid, kThreads, smem, c.stream>>>(g, e);
+  if (g.KB <= 4) {
+    constexpr int smem = gemm_smem_bytes<BN, true>();
+    set_smem_once(k_gemm<BN, true, Epi>, smem);
+    k_gemm<BN, true, Epi><<<grid, kGemmThreads, smem, c.stream>>>(g, e);
+  } else {
+    constexpr int smem = gemm_smem_bytes<BN, false>();
+    set_smem_once(k_gemm<BN, false, Epi>, smem);
+    k_gemm<BN, false, Epi><<<grid, kGemmThreads, smem, c.stream>>>(g, e);
+  }
   c.launches++;
 }
 

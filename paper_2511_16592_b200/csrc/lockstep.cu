@@ -1,0 +1,1075 @@
+// lockstep.cu — bf16 tcgen05 fast path for the fixed-length environments:
+//   bitseq NAR (SequenceEnv, proj/src/envs/sequences.cpp; BASELINE config #3:
+//               n = 120, k = 8 -> 15 slots x 256 words, A = 3840, O = 3856, T = 15, MLP 2x256)
+//   Ising      (IsingEnv, proj/src/envs/ising.cpp; config #4: 10x10, A = 200, O = 300,
+//               T = 100, MLP 4x256)
+// trained with trajectory balance (tb_loss objectives.cpp:120-142).
+//
+// Every trajectory takes exactly T steps, so the batch advances in lockstep and the rows of
+// the training pass are laid out step-major: row r = t * Bl + b. The rollout's forward IS
+// the training forward (parameters are fixed inside an iteration): the activation images,
+// ReLU masks and per-row log-softmax statistics it produces feed the backward directly.
+//
+// Per rollout step t:
+//   k_ls_layer1   warp per trajectory: incremental layer-1 pre-activation (fp32, resident)
+//                 from the features the last action changed (Env::delta_features), coalesced
+//                 W1 row reads; ReLU -> h1 tile image + mask
+//   k_gemm<Hid>   h_{l-1} W_l^T (+b, ReLU) -> h_l image + mask, l = 2..NL   (tcgen05)
+//   k_gemm<Log>   h_NL Wf^T (+bf) -> bf16 logits [Bl x Ap] and, per 128-column group, the
+//                 masked (max, sum exp) over the legal columns               (tcgen05)
+//   k_ls_sample   warp per trajectory: eps-uniform masked categorical with ONE uniform
+//                 (eps_uniform objectives.cpp:242-264, categorical rng.cpp:87-100): group
+//                 by cumulative group mass from the statistics, then the column inside the
+//                 group from its 128 logits; env step; record
+// Training:
+//   k_ls_loss     per trajectory TB residual -> per-row coefficient g
+//   k_gemm<Dlog>  recomputed logits -> dlogits = g (onehot - softmax) on legal columns
+//   k_gemm<Dgrad> dlogits Wf (K = Ap) masked by h_NL > 0 -> dz_NL; then dz_l W_l -> dz_{l-1}
+//   k_ls_wgrad    dW_l = h_{l-1}^T dz_l, dWf = h_NL^T dlogits (per 256 columns),
+//                 dW1 = obs^T dz_1 (per 256 features, one-hot operand built in smem):
+//                 MN-major tcgen05 over 64-row stages, warp-specialised
+//   k_ls_colsum, k_ls_reduce   fixed-order reductions into the flat gradient; then Adam.
+#include <math.h>
+
+#include <vector>
+
+#include "engine.h"
+#include "gemm.cuh"
+
+namespace gfnx {
+
+namespace {
+
+constexpr int kH = 256;     // hidden width of this path
+constexpr int kMaxNL = 4;   // hidden layers
+constexpr int kMaxTasks = 48;
+
+// ---------------------------------------------------------------------------
+// env adapters: legality of 32 consecutive columns and the features of one 256-block,
+// both straight from the packed state words.
+template <class E>
+struct Lock;
+
+template <>
+struct Lock<BitseqEnv> {  // k = 8 (256-word slots), <= 32 slots
+  GFNX_DEV static uint32_t legal32(const EnvParams& P, const uint32_t* w, int c0) {
+    if (c0 >= P.A) return 0u;
+    const int tw = (P.bs_slots + 3) / 4;
+    return ((w[tw] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
+  }
+  // features with index in [f0, f0 + 256): put(f - f0, value); `part` of 4 splits the work
+  template <class F>
+  GFNX_DEV static void block_features(const EnvParams& P, const uint32_t* w, int f0, int part, F&& put) {
+    const int V = P.bs_vocab, W = V + 1, S = P.bs_slots, tw = (S + 3) / 4;
+    const uint32_t filled = w[tw];
+    for (int p = part; p < S; p += 4) {
+      const int f = p * W + (((filled >> p) & 1u) ? (int)((w[p >> 2] >> (8 * (p & 3))) & 0xffu) : V);
+      if (f >= f0 && f < f0 + 256) put(f - f0, 1.f);
+    }
+    if (part == 0) {
+      const int f = S * W;
+      if (f >= f0 && f < f0 + 256) put(f - f0, (float)__popc(filled) / (float)S);
+    }
+  }
+};
+
+template <>
+struct Lock<IsingEnv> {
+  GFNX_DEV static uint32_t legal32(const EnvParams& P, const uint32_t* w, int c0) {
+    if (c0 >= P.A) return 0u;
+    const int site0 = c0 >> 1;  // 16 sites, inside one assigned-word
+    uint32_t x = ~(w[site0 >> 5] >> (site0 & 31)) & 0xffffu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    x |= x << 1;
+    const int left = P.A - c0;
+    return left >= 32 ? x : (x & ((1u << left) - 1u));
+  }
+  template <class F>
+  GFNX_DEV static void block_features(const EnvParams& P, const uint32_t* w, int f0, int part, F&& put) {
+    const int nw = P.SW / 2;
+    const int i0 = f0 / 3, i1 = min(P.is_D, (f0 + 256 + 2) / 3);
+    for (int i = i0 + part; i < i1; i += 4) {
+      const uint32_t asg = (w[i >> 5] >> (i & 31)) & 1u, up = (w[nw + (i >> 5)] >> (i & 31)) & 1u;
+      const int f = 3 * i + (asg ? (int)up : 2);
+      if (f >= f0 && f < f0 + 256) put(f - f0, 1.f);
+    }
+  }
+};
+
+struct LsState {
+  int num_sms = 0;
+  int NL = 2, A = 0, Ap = 0, NT = 0, G = 0, O = 0, OB = 0, T = 0, KBA = 0;
+  int Bl = 0, R = 0, tilesB = 0, tilesR = 0, SW = 0;
+  __nv_bfloat16* w1 = nullptr;               // [O][H] row-major
+  __nv_bfloat16* wfw[kMaxNL] = {};           // layer l (1..NL-1): [H out][H in] image
+  __nv_bfloat16* wdg[kMaxNL] = {};           // layer l: [H in][H out] image
+  __nv_bfloat16* wff = nullptr;              // head fwd image: NT n-tiles x 4 K-blocks
+  __nv_bfloat16* wfd = nullptr;              // head dgrad image: 1 n-tile x KBA K-blocks
+  float* bfp = nullptr;                      // head bias padded to Ap
+  float* h1init = nullptr;                   // [H]
+  float* preact = nullptr;                   // [Bl][H]
+  uint32_t* cur = nullptr;                   // [Bl][SW] current packed state
+  uint32_t* stst = nullptr;                  // [R][SW] state before the step of row r
+  int32_t* last_act = nullptr;               // [Bl]
+  __nv_bfloat16* h[kMaxNL] = {};             // [R] images, h[l] = output of hidden layer l+1
+  __nv_bfloat16* dz[kMaxNL] = {};
+  uint8_t* mask[kMaxNL] = {};                // [R][H/8]
+  __nv_bfloat16* logits = nullptr;           // [Bl][Ap] row-major, per-step scratch
+  float2* stats = nullptr;                   // [Bl][G] (max, sum exp) per 128-column group
+  __nv_bfloat16* dlog = nullptr;             // [R] x Ap image
+  float* rowbuf = nullptr;                   // [R][2]: logp(a), lse
+  float* coef = nullptr;                     // [R]
+  int bw = 0;                                // bias columns: NL*H + Ap
+  float* bpart = nullptr;                    // [tilesR][bw] per-tile bias column sums
+  int cgroups = 0;
+  float* bpart2 = nullptr;                   // [cgroups][bw]
+  float* wpart = nullptr;                    // [task][range][256][256]
+  int ntasks = 0, nranges = 0;
+  int t_dense = 0, t_head = 0, t_w1 = 0;     // first task of each kind
+  double* lpart = nullptr;
+  int loss_blocks = 0;
+};
+
+LsState& LS(Ctx& c) { return *static_cast<LsState*>(c.fast); }
+
+// ---------------------------------------------------------------------------
+// rollout kernels
+
+struct L1Args {
+  EnvParams P;
+  const __nv_bfloat16* w1;
+  const float* h1init;
+  float* preact;
+  const int32_t* last_act;
+  uint8_t* h1;
+  uint8_t* mask1;
+  int Bl, t;
+};
+
+// warp per trajectory; lane l owns hidden columns [8l, 8l + 8)
+template <class E>
+__global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= a.Bl) return;
+  float v[8];
+  float* pre = a.preact + (size_t)b * kH + 8 * lane;
+  if (a.t == 0) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = a.h1init[8 * lane + j];
+  } else {
+    const float4 p0 = *reinterpret_cast<const float4*>(pre), p1 = *reinterpret_cast<const float4*>(pre + 4);
+    v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
+    v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
+    typename E::State dummy;
+    E::delta_features(a.P, dummy, a.last_act[b], [&](int f, float coef) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.w1 + (size_t)f * kH) + lane);
+      const uint32_t x[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[2 * e] += coef * bf16_lo(x[e]);
+        v[2 * e + 1] += coef * bf16_hi(x[e]);
+      }
+    });
+  }
+  *reinterpret_cast<float4*>(pre) = make_float4(v[0], v[1], v[2], v[3]);
+  *reinterpret_cast<float4*>(pre + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  uint32_t pk[4];
+  uint32_t mb = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    pk[e] = pack_bf16x2(fmaxf(v[2 * e], 0.f), fmaxf(v[2 * e + 1], 0.f));
+    mb |= (bf16_lo(pk[e]) > 0.f ? 1u : 0u) << (2 * e);
+    mb |= (bf16_hi(pk[e]) > 0.f ? 1u : 0u) << (2 * e + 1);
+  }
+  const size_t r = (size_t)a.t * a.Bl + b;
+  uint8_t* tile = a.h1 + (r / kTile) * (kTile * kH * 2);
+  *reinterpret_cast<uint4*>(tile + sw128_offset((uint32_t)(r % kTile), 8 * lane, kTile)) =
+      make_uint4(pk[0], pk[1], pk[2], pk[3]);
+  a.mask1[r * (kH / 8) + lane] = (uint8_t)mb;
+}
+
+struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
+  struct Args {
+    const float* b;
+    uint8_t* h;
+    uint8_t* mask;
+  };
+  struct Local {};
+  static __device__ void apply(const Args& e, int m, int, int row, int col0, float (&v)[32], float*, Local&) {
+    uint32_t pk[16], mb = 0;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      pk[i] = pack_bf16x2(fmaxf(v[2 * i] + __ldg(e.b + col0 + 2 * i), 0.f),
+                          fmaxf(v[2 * i + 1] + __ldg(e.b + col0 + 2 * i + 1), 0.f));
+      mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
+      mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
+    }
+    st_row32(e.h + (size_t)m * (kTile * kH * 2), row, col0, pk);
+    const size_t r = (size_t)m * kTile + row;
+    *reinterpret_cast<uint32_t*>(e.mask + r * (kH / 8) + col0 / 8) = mb;
+  }
+};
+
+// +bf -> bf16 logits row-major [Bl][Ap] and masked (max, sum exp) per 128-column group
+template <class E>
+struct LogEpi : EpiBase {
+  struct Args {
+    EnvParams P;
+    const float* bf;  // padded to Ap
+    const uint32_t* cur;
+    __nv_bfloat16* logits;
+    float2* stats;
+    int Ap, G, row_base;  // global row of tile 0 of this step
+  };
+  struct Local {
+    float mx, s;
+  };
+  static __device__ void begin(const Args&, int, int, int, int, Local& l) {
+    l.mx = -INFINITY;
+    l.s = 0.f;
+  }
+  static __device__ void apply(const Args& e, int m, int n, int row, int col0, float (&v)[32], float*, Local& l) {
+    const int b = m * kTile + row - e.row_base;
+    const int c = n * 256 + col0;
+    const uint32_t lm = Lock<E>::legal32(e.P, e.cur + (size_t)b * e.P.SW, c);
+    uint32_t pk[16];
+    float cm = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      pk[i] = pack_bf16x2(v[2 * i] + __ldg(e.bf + c + 2 * i), v[2 * i + 1] + __ldg(e.bf + c + 2 * i + 1));
+      v[2 * i] = bf16_lo(pk[i]);
+      v[2 * i + 1] = bf16_hi(pk[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if ((lm >> i) & 1u) cm = fmaxf(cm, v[i]);
+    uint4* dst = reinterpret_cast<uint4*>(e.logits + (size_t)b * e.Ap + c);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    if (lm == 0u) return;
+    const float nm = fmaxf(l.mx, cm);
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) s += ((lm >> i) & 1u) ? __expf(v[i] - nm) : 0.f;
+    l.s = l.s * __expf(l.mx - nm) + s;  // l.mx = -inf -> factor 0
+    l.mx = nm;
+  }
+  static __device__ void row_done(const Args& e, int m, int n, int row, int half, Local& l) {
+    const int b = m * kTile + row - e.row_base;
+    e.stats[(size_t)b * e.G + 2 * n + half] = make_float2(l.mx, l.s);
+  }
+};
+
+struct SampleArgs {
+  EnvParams P;
+  Key key;
+  double eps;
+  int b0, Bl, t, T, Ap, G;
+  const __nv_bfloat16* logits;
+  const float2* stats;
+  uint32_t* cur;
+  uint32_t* stst;
+  int32_t* last_act;
+  float* rowbuf;
+  DeviceBatch batch;
+};
+
+GFNX_DEV double warp_sum_d(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// warp per trajectory: two-level inverse CDF with the reference's single uniform
+template <class E>
+__global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  if (b >= a.Bl) return;
+  const EnvParams& P = a.P;
+  const uint32_t* w = a.cur + (size_t)b * P.SW;
+  // ---- group level (lane g <-> 128-column group g; G <= 32)
+  int lcount = 0;
+  float gm = -INFINITY, gs = 0.f;
+  if (lane < a.G) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) lcount += __popc(Lock<E>::legal32(P, w, lane * 128 + q * 32));
+    const float2 st = a.stats[(size_t)b * a.G + lane];
+    if (lcount > 0) {
+      gm = st.x;
+      gs = st.y;
+    }
+  }
+  float hi = gm;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) hi = fmaxf(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  const double gz = lcount > 0 ? (double)gs * (double)__expf(gm - hi) : 0.0;
+  const double z = warp_sum_d(gz);
+  int legal = lcount;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) legal += __shfl_xor_sync(0xffffffffu, legal, o);
+  const double eps = a.eps;
+  const double u_eps = legal > 0 ? eps / legal : 0.0;
+  const double mass = lcount > 0 ? (1.0 - eps) * gz / z + u_eps * lcount : 0.0;
+  double incl = mass;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const double total = __shfl_sync(0xffffffffu, incl, 31);
+  const double u01 = uniform_scalar(fold_in(fold_in(a.key, (uint64_t)a.t), (uint64_t)(a.b0 + b)));
+  double x = u01 * total;
+  const unsigned pos = __ballot_sync(0xffffffffu, mass > 0.0);
+  const unsigned hit = __ballot_sync(0xffffffffu, mass > 0.0 && x < incl);
+  int grp = -1, act = -1;
+  if (pos) {
+    grp = hit ? __ffs(hit) - 1 : 31 - __clz(pos);  // rounding: last positive group
+    x -= __shfl_sync(0xffffffffu, incl - mass, grp);
+    // ---- column level: 4 consecutive columns per lane
+    const int c = grp * 128 + lane * 4;
+    const uint32_t lm = (Lock<E>::legal32(P, w, grp * 128 + (lane >> 3) * 32) >> ((lane & 7) * 4)) & 0xfu;
+    const uint2 q = *reinterpret_cast<const uint2*>(a.logits + (size_t)b * a.Ap + c);
+    const float xs[4] = {bf16_lo(q.x), bf16_hi(q.x), bf16_lo(q.y), bf16_hi(q.y)};
+    double w4[4], ls = 0.0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      w4[e] = ((lm >> e) & 1u) ? (1.0 - eps) * (double)__expf(xs[e] - hi) / z + u_eps : 0.0;
+      ls += w4[e];
+    }
+    double ci = ls;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double y = __shfl_up_sync(0xffffffffu, ci, o);
+      if (lane >= o) ci += y;
+    }
+    const unsigned h2 = __ballot_sync(0xffffffffu, ls > 0.0 && x < ci);
+    int pick = -1;
+    if (h2) {
+      const int src = __ffs(h2) - 1;
+      if (lane == src) {
+        double acc = ci - ls;
+        pick = 3;
+        for (int e = 0; e < 4; ++e) {
+          acc += w4[e];
+          if (w4[e] > 0.0 && x < acc) {
+            pick = e;
+            break;
+          }
+        }
+        while (pick > 0 && w4[pick] == 0.0) --pick;
+      }
+      pick = __shfl_sync(0xffffffffu, pick, src);
+      act = grp * 128 + src * 4 + pick;
+    } else {  // rounding fallback: last legal column of the group
+      const unsigned any = __ballot_sync(0xffffffffu, lm != 0u);
+      const int src = 31 - __clz(any);
+      const uint32_t ml = __shfl_sync(0xffffffffu, lm, src);
+      act = grp * 128 + src * 4 + (31 - __clz(ml));
+    }
+  }
+  // ---- record + env step (lane 0)
+  if (lane == 0) {
+    const size_t bt = (size_t)b * a.T + a.t;
+    const size_t r = (size_t)a.t * a.Bl + b;
+    if (act < 0 || !(z > 0.0)) {
+      atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
+      return;
+    }
+    const float xa = __bfloat162float(a.logits[(size_t)b * a.Ap + act]);
+    const float lse = hi + __logf((float)z);
+    a.rowbuf[2 * r] = xa - lse;
+    a.rowbuf[2 * r + 1] = lse;
+    for (int i = 0; i < P.SW; ++i) a.stst[r * P.SW + i] = w[i];
+    typename E::State s;
+    E::unpack(P, w, s);
+    const bool term = E::step(P, s, act);
+    E::pack(P, s, a.cur + (size_t)b * P.SW);
+    a.batch.actions[bt] = (int16_t)act;
+    a.batch.nparents[bt] = (uint16_t)E::num_parents(P, s);
+    a.last_act[b] = act;
+    if (term) {
+      a.batch.lengths[b] = a.t + 1;
+      a.batch.log_rewards[b] = E::log_reward(P, s);
+      E::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
+    }
+    if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
+  }
+}
+
+template <class E>
+__global__ void k_ls_h1init(EnvParams P, const __nv_bfloat16* w1, const float* b1, float* h1init) {
+  const int j = threadIdx.x;
+  if (j >= kH) return;
+  typename E::State s;
+  E::reset(P, s);
+  float v = b1[j];
+  E::features(P, s, [&](int f, double val) { v += (float)val * __bfloat162float(w1[(size_t)f * kH + j]); });
+  h1init[j] = v;
+}
+
+__global__ void k_ls_reset(int n, uint32_t* cur) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) cur[i] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// training kernels
+
+struct LossArgs {
+  DeviceBatch batch;
+  int Bl, T;
+  double B_global;
+  const double* neglog;
+  const float* rowbuf;
+  float* coef;
+  double* lpart;
+  const double* scalars;
+};
+
+__global__ void k_ls_loss(LossArgs a) {  // tb_loss objectives.cpp:120-142
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  double loss = 0.0, dlogz = 0.0;
+  if (b < a.Bl) {
+    const double w = 1.0 / a.B_global;
+    double cum = 0.0;
+    for (int t = 0; t < a.T; ++t) {
+      const size_t r = (size_t)t * a.Bl + b;
+      cum += (double)a.rowbuf[2 * r] - a.neglog[a.batch.nparents[(size_t)b * a.T + t]];
+    }
+    const double res = cum + a.scalars[0] - a.batch.log_rewards[b];
+    loss = res * res * w;
+    const double g = 2.0 * res * w;
+    dlogz = g;
+    for (int t = 0; t < a.T; ++t) a.coef[(size_t)t * a.Bl + b] = (float)g;
+  }
+  __shared__ double red[2][256];
+  red[0][threadIdx.x] = loss;
+  red[1][threadIdx.x] = dlogz;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + off];
+      red[1][threadIdx.x] += red[1][threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.lpart[2 * blockIdx.x] = red[0][0];
+    a.lpart[2 * blockIdx.x + 1] = red[1][0];
+  }
+}
+
+__global__ void k_ls_loss_finalize(const double* lpart, int n, double* scalars, int32_t* err) {
+  if (threadIdx.x != 0) return;
+  double l = 0.0, z = 0.0;
+  for (int i = 0; i < n; ++i) {
+    l += lpart[2 * i];
+    z += lpart[2 * i + 1];
+  }
+  scalars[4] = l;
+  scalars[3] = z;
+  if (!isfinite(l)) atomicExch(err, GFNX_ERR_NUMERIC);
+}
+
+template <class E>
+struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile column sums
+  struct Args {
+    EnvParams P;
+    const float* bf;  // padded
+    const float* rowbuf;
+    const float* coef;
+    const uint32_t* stst;
+    const int16_t* actions;
+    uint8_t* dlog;  // image with KBA K-blocks per tile
+    float* bpart;   // [tilesR][bw]
+    int Bl, T, KBA, bw, boff;
+  };
+  struct Local {
+    float lse, g;
+    int act;
+  };
+  static __device__ void begin(const Args& e, int m, int, int row, int, Local& l) {
+    const size_t r = (size_t)m * kTile + row;
+    const int t = (int)(r / e.Bl), b = (int)(r % e.Bl);
+    l.lse = e.rowbuf[2 * r + 1];
+    l.g = e.coef[r];
+    l.act = e.actions[(size_t)b * e.T + t];
+  }
+  static __device__ void finish(const Args& e, int m, int n, const float* scratch) {
+    const int c = threadIdx.x - 128;  // 256 epilogue threads, one output column each
+    const float s = scratch[c] + scratch[256 + c] + scratch[512 + c] + scratch[768 + c];
+    e.bpart[(size_t)m * e.bw + e.boff + n * 256 + c] = s;
+  }
+  static __device__ void apply(const Args& e, int m, int n, int row, int col0, float (&v)[32], float* scratch,
+                               Local& l) {
+    const size_t r = (size_t)m * kTile + row;
+    const int c0 = n * 256 + col0;
+    const uint32_t lm = Lock<E>::legal32(e.P, e.stst + r * e.P.SW, c0);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const float x = __bfloat162float(__float2bfloat16(v[i] + __ldg(e.bf + c0 + i)));
+      float d = ((lm >> i) & 1u) ? -l.g * __expf(x - l.lse) : 0.f;
+      if (c0 + i == l.act) d += l.g;
+      v[i] = d;
+    }
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+    uint8_t* blk = e.dlog + ((size_t)m * e.KBA + n * 4 + col0 / 64) * (kTile * 128);
+    st_row32(blk, row, col0 % 64, pk);
+    const float s = warp_colsum32(v);  // this warp's 32 rows, lane = column
+    scratch[epi_quarter() * 256 + col0 + (threadIdx.x & 31)] = s;
+  }
+};
+
+struct DgradEpi : EpiBase {  // masked by ReLU bits -> dz image + bias column sums
+  struct Args {
+    const uint8_t* mask;
+    uint8_t* dz;
+    float* bpart;
+    int boff, bw;
+  };
+  struct Local {};
+  static __device__ void finish(const Args& e, int m, int, const float* scratch) {
+    const int c = threadIdx.x - 128;
+    const float s = scratch[c] + scratch[256 + c] + scratch[512 + c] + scratch[768 + c];
+    e.bpart[(size_t)m * e.bw + e.boff + c] = s;
+  }
+  static __device__ void apply(const Args& e, int m, int, int row, int col0, float (&v)[32], float* scratch,
+                               Local&) {
+    const size_t r = (size_t)m * kTile + row;
+    const uint32_t mk = *reinterpret_cast<const uint32_t*>(e.mask + r * (kH / 8) + col0 / 8);
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = ((mk >> i) & 1u) ? v[i] : 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
+    st_row32(e.dz + (size_t)m * (kTile * kH * 2), row, col0, pk);
+    const float s = warp_colsum32(v);
+    scratch[epi_quarter() * 256 + col0 + (threadIdx.x & 31)] = s;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// weight gradients: one CTA per (task, row range); per 64-row stage
+//   dense task   A' = activation image (256 features, MN-major), B' = 256-column chunk of
+//                a gradient image (dz_l or dlogits)
+//   one-hot task A' = obs features [f0, f0 + 256) of the stage rows, built in smem from the
+//                packed states (bulk-copied beside the operands), B' = dz_1
+// Warp roles: warp 0 producer, warp 1 MMA issuer, warps 4..11 builders + epilogue.
+
+constexpr int kWStage = 64;  // rows per stage
+constexpr int kWStages = 3;
+constexpr int kWOp = kWStage * 256 * 2;  // 32 KB operand per stage
+constexpr int kWStBytes = kWStage * 16 * 4;  // packed states of a stage (SW <= 16)
+
+struct WgTask {
+  const uint8_t* a;  // dense: A' image (4 K-blocks per tile); one-hot: nullptr
+  const uint8_t* b;  // B' image
+  int b_kbs, b_kb0;  // K-blocks per tile of the B' image, first block used
+  int f0, nf;        // one-hot: feature block [f0, f0 + nf)
+};
+
+struct WgArgs {
+  EnvParams P;
+  const uint32_t* stst;
+  int tilesR, nranges, ntasks;
+  float* wpart;
+  WgTask task[kMaxTasks];
+};
+
+GFNX_DEV void wg_copy_half(uint8_t* dst, const uint8_t* tile, int blk0, int h, uint64_t* bar) {
+  // rows [64h, 64h + 64) of 4 feature blocks [blk0, blk0 + 4) of a 128-row tile image
+  for (int k = 0; k < 4; ++k)
+    bulk_g2s(dst + k * (kWStage * 128), tile + (size_t)(blk0 + k) * (kTile * 128) + h * (kWStage * 128),
+             kWStage * 128, bar);
+}
+
+template <class E>
+__global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_constant__ WgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  constexpr int kSlot = 2 * kWOp + kWStBytes;
+  __shared__ uint64_t full[kWStages], empty[kWStages], built[kWStages], done;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int task = blockIdx.x / a.nranges, range = blockIdx.x % a.nranges;
+  const WgTask& tk = a.task[task];
+  const bool onehot = tk.a == nullptr;
+  const int halves = (onehot && tk.nf <= 128) ? 1 : 2;  // M' = 256 (2 x 128) or 128
+  const int per = (a.tilesR + a.nranges - 1) / a.nranges;
+  const int t0 = range * per, t1 = min(a.tilesR, t0 + per);
+  const int nq = t1 > t0 ? 2 * (t1 - t0) : 0;  // 64-row stages
+  const int SW = a.P.SW;
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 32) {
+    for (int s = 0; s < kWStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&built[s], 1);
+    }
+    mbar_init(&done, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  if (warp == 0) {
+    if (lane == 0) {  // ---- producer
+      for (int q = 0; q < nq; ++q) {
+        const int slot = q % kWStages, tile = t0 + q / 2, h = q % 2;
+        if (q >= kWStages) mbar_wait(&empty[slot], ((q / kWStages) - 1) & 1);
+        uint8_t* sa = smem + slot * kSlot;
+        uint8_t* sb = sa + kWOp;
+        const int st_bytes = kWStage * SW * 4;
+        mbar_arrive_expect_tx(&full[slot], (onehot ? st_bytes : kWOp) + kWOp);
+        if (onehot)
+          bulk_g2s(sb + kWOp, a.stst + ((size_t)tile * kTile + h * kWStage) * SW, st_bytes, &full[slot]);
+        else
+          wg_copy_half(sa, tk.a + (size_t)tile * (4 * kTile * 128), 0, h, &full[slot]);
+        wg_copy_half(sb, tk.b + (size_t)tile * tk.b_kbs * (kTile * 128), tk.b_kb0, h, &full[slot]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = umma_idesc_bf16(128, 256, true, true);
+      for (int q = 0; q < nq; ++q) {
+        const int slot = q % kWStages;
+        mbar_wait(&full[slot], (q / kWStages) & 1);
+        if (onehot) mbar_wait(&built[slot], (q / kWStages) & 1);
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(smem + slot * kSlot), b0 = a0 + kWOp;
+        for (int hh = 0; hh < halves; ++hh)
+#pragma unroll
+          for (int k = 0; k < kWStage / 16; ++k)
+            umma_bf16(tmem + hh * 256, umma_desc_sw128(a0 + hh * 2 * (kWStage * 128) + k * 2048, kWStage * 128, 1024),
+                      umma_desc_sw128(b0 + k * 2048, kWStage * 128, 1024), idesc, (q > 0 || k > 0) ? 1u : 0u);
+        umma_commit(&empty[slot]);
+      }
+      umma_commit(&done);
+    }
+  } else if (warp >= 4) {
+    const int et = tid - 128;  // 0..255
+    if (onehot) {  // ---- builders
+      const int row = et & 63, part = et >> 6;
+      for (int q = 0; q < nq; ++q) {
+        const int slot = q % kWStages;
+        uint8_t* sa = smem + slot * kSlot;
+        mbar_wait(&full[slot], (q / kWStages) & 1);  // slot free (producer waited) + states in
+        uint4* z = reinterpret_cast<uint4*>(sa + et * 128);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) z[i] = make_uint4(0, 0, 0, 0);
+        epi_bar();
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(sa + 2 * kWOp) + row * SW;
+        Lock<E>::block_features(a.P, w, tk.f0, part, [&](int f, float v) {
+          *reinterpret_cast<__nv_bfloat16*>(sa + (f >> 6) * (kWStage * 128) +
+                                            (sw128_offset(row, f & 63, kWStage) & (kWStage * 128 - 1))) =
+              __float2bfloat16(v);
+        });
+        fence_proxy_async();
+        epi_bar();
+        if (et == 0) mbar_arrive_local(&built[slot]);
+      }
+    }
+    // ---- epilogue: lane quarter x column half, both M'-halves
+    const int ew = warp - 4, quarter = ew & 3, half = ew >> 2;
+    if (nq > 0) mbar_wait(&done, 0);
+    tc_fence_after();
+    float* slab = a.wpart + ((size_t)task * a.nranges + range) * (256 * 256);
+    for (int hh = 0; hh < 2; ++hh) {
+      const int mrow = hh * 128 + quarter * 32 + lane;
+      for (int q = 0; q < 4; ++q) {
+        const int col = half * 128 + q * 32;
+        uint32_t r32[32];
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + hh * 256 + col, r32);
+        tmem_wait_ld();
+        float4* dst = reinterpret_cast<float4*>(slab + (size_t)mrow * 256 + col);
+        const bool ok = nq > 0 && hh < halves;
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          dst[i] = ok ? make_float4(__uint_as_float(r32[4 * i]), __uint_as_float(r32[4 * i + 1]),
+                                    __uint_as_float(r32[4 * i + 2]), __uint_as_float(r32[4 * i + 3]))
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// bias column sums: bpart [tilesR][bw] -> bpart2 [groups][bw] (fixed order)
+__global__ void k_ls_colsum(const float* bpart, int tilesR, int bw, int groups, float* bpart2) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x, g = blockIdx.y;
+  if (col >= bw) return;
+  const int per = (tilesR + groups - 1) / groups;
+  const int t0 = g * per, t1 = min(tilesR, t0 + per);
+  float s = 0.f;
+  for (int t = t0; t < t1; ++t) s += bpart[(size_t)t * bw + col];
+  bpart2[(size_t)g * bw + col] = s;
+}
+
+struct RedArgs {
+  const float* wpart;
+  const float* bpart2;
+  float* g;
+  int nranges, groups, bw, A, O, NL, t_dense, t_head, t_w1;
+  MlpLayout L;
+};
+
+__global__ void k_ls_reduce(RedArgs a) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const MlpLayout& L = a.L;
+  if (e >= L.n_params) return;
+  auto slab_sum = [&](int task, int m, int n) {
+    float s = 0.f;
+    for (int r = 0; r < a.nranges; ++r) s += a.wpart[(((size_t)task * a.nranges + r) * 256 + m) * 256 + n];
+    return s;
+  };
+  auto bias_sum = [&](int col) {
+    float s = 0.f;
+    for (int g = 0; g < a.groups; ++g) s += a.bpart2[(size_t)g * a.bw + col];
+    return s;
+  };
+  float v = 0.f;
+  if (e < L.off_b[0]) {  // W1 [O][H]
+    const int f = (int)(e / kH), j = (int)(e % kH);
+    v = slab_sum(a.t_w1 + f / 256, f % 256, j);
+  } else if (e >= L.off_fw && e < L.off_fb) {  // head [H][A]
+    const int64_t k = e - L.off_fw;
+    const int p = (int)(k / a.A), c = (int)(k % a.A);
+    v = slab_sum(a.t_head + c / 256, p, c % 256);
+  } else if (e >= L.off_fb && e < L.off_bw) {
+    v = bias_sum(a.NL * kH + (int)(e - L.off_fb));
+  } else {
+    for (int l = 0; l < a.NL; ++l) {
+      if (e >= L.off_b[l] && e < L.off_b[l] + kH) {
+        v = bias_sum(l * kH + (int)(e - L.off_b[l]));
+        break;
+      }
+      if (l >= 1 && e >= L.off_w[l] && e < L.off_b[l]) {  // W_{l+1} [in][out]
+        const int64_t k = e - L.off_w[l];
+        v = slab_sum(a.t_dense + l - 1, (int)(k / kH), (int)(k % kH));
+        break;
+      }
+    }
+  }
+  a.g[e] = v;  // bwd / flow heads: unused by TB with uniform P_B -> 0
+}
+
+struct EmitArgs {
+  const float* p;
+  int64_t n;
+  MlpLayout L;
+  int A, NL;
+  __nv_bfloat16 *w1, *wff, *wfd;
+  __nv_bfloat16* wfw[kMaxNL];
+  __nv_bfloat16* wdg[kMaxNL];
+  float* bfp;
+};
+
+__global__ void k_ls_emit(EmitArgs a) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= a.n) return;
+  const MlpLayout& L = a.L;
+  const __nv_bfloat16 v = __float2bfloat16(a.p[j]);
+  if (j < L.off_b[0]) {
+    a.w1[j] = v;
+  } else if (j >= L.off_fw && j < L.off_fb) {
+    const int64_t k = j - L.off_fw;
+    const int p = (int)(k / a.A), c = (int)(k % a.A);
+    const int n = c / 256, cc = c % 256;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wff + (size_t)n * (256 * kH * 2) + sw128_offset(cc, p, 256)) = v;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wfd + sw128_offset(p, c, kH)) = v;
+  } else if (j >= L.off_fb && j < L.off_fb + a.A) {
+    a.bfp[j - L.off_fb] = a.p[j];
+  } else {
+    for (int l = 1; l < a.NL; ++l)
+      if (j >= L.off_w[l] && j < L.off_b[l]) {
+        const int64_t k = j - L.off_w[l];
+        const int p = (int)(k / kH), q = (int)(k % kH);
+        *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wfw[l] + sw128_offset(q, p, kH)) = v;
+        *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wdg[l] + sw128_offset(p, q, kH)) = v;
+      }
+  }
+}
+
+EmitArgs emit_args(Ctx& c) {
+  LsState& f = LS(c);
+  EmitArgs a{};
+  a.p = c.p32;
+  a.n = c.L.n_params;
+  a.L = c.L;
+  a.A = f.A;
+  a.NL = f.NL;
+  a.w1 = f.w1;
+  a.wff = f.wff;
+  a.wfd = f.wfd;
+  for (int l = 0; l < kMaxNL; ++l) {
+    a.wfw[l] = f.wfw[l];
+    a.wdg[l] = f.wdg[l];
+  }
+  a.bfp = f.bfp;
+  return a;
+}
+
+template <class E>
+void rollout_impl(Ctx& c, Key key, double eps) {
+  LsState& f = LS(c);
+  const int T = f.T, Bl = c.Bl;
+  cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)Bl * T, c.stream);
+  {
+    ProfScope ps(c, "k_ls_init");
+    k_ls_reset<<<(Bl * f.SW + 255) / 256, 256, 0, c.stream>>>(Bl * f.SW, f.cur);
+    k_ls_h1init<E><<<1, kH, 0, c.stream>>>(c.P, f.w1, c.p32 + c.L.off_b[0], f.h1init);
+    c.launches += 2;
+  }
+  for (int t = 0; t < T; ++t) {
+    {
+      L1Args la{c.P, f.w1, f.h1init, f.preact, f.last_act, (uint8_t*)f.h[0], f.mask[0], Bl, t};
+      ProfScope ps(c, "k_ls_layer1");
+      k_ls_layer1<E><<<(Bl + 7) / 8, 256, 0, c.stream>>>(la);
+      c.launches++;
+    }
+    GemmGeom g{};
+    g.a_kb = 4;
+    g.b_kb = 4;
+    g.m0 = t * f.tilesB;
+    g.m_tiles = f.tilesB;
+    g.n_tiles = 1;
+    g.KB = 4;
+    for (int l = 1; l < f.NL; ++l) {
+      g.A = (const uint8_t*)f.h[l - 1];
+      g.B = (const uint8_t*)f.wfw[l];
+      launch_gemm<256, HidEpi>(c, "k_gemm_hidden", g, HidEpi::Args{c.p32 + c.L.off_b[l], (uint8_t*)f.h[l], f.mask[l]},
+                               f.num_sms);
+    }
+    g.A = (const uint8_t*)f.h[f.NL - 1];
+    g.B = (const uint8_t*)f.wff;
+    g.n_tiles = f.NT;
+    typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl};
+    launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
+    SampleArgs sa{c.P, key, eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst, f.last_act,
+                  f.rowbuf, c.batch};
+    ProfScope ps(c, "k_ls_sample");
+    k_ls_sample<E><<<(Bl + 7) / 8, 256, 0, c.stream>>>(sa);
+    c.launches++;
+  }
+}
+
+template <class E>
+void train_impl(Ctx& c) {
+  LsState& f = LS(c);
+  const int Bl = c.Bl, NL = f.NL;
+  {
+    LossArgs la{c.batch, Bl, f.T, (double)c.B, c.d_neglog, f.rowbuf, f.coef, f.lpart, c.d_scalars};
+    ProfScope ps(c, "k_ls_loss");
+    k_ls_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
+    k_ls_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars, c.batch.counters + 3);
+    c.launches += 2;
+  }
+  GemmGeom g{};
+  g.A = (const uint8_t*)f.h[NL - 1];
+  g.a_kb = 4;
+  g.B = (const uint8_t*)f.wff;
+  g.b_kb = 4;
+  g.m0 = 0;
+  g.m_tiles = f.tilesR;
+  g.n_tiles = f.NT;
+  g.KB = 4;
+  typename DlogEpi<E>::Args de{c.P, f.bfp, f.rowbuf, f.coef, f.stst, c.batch.actions, (uint8_t*)f.dlog, f.bpart,
+                               Bl, f.T, f.KBA, f.bw, NL * kH};
+  launch_gemm<256, DlogEpi<E>>(c, "k_gemm_dlogits", g, de, f.num_sms);
+  GemmGeom g2{};
+  g2.A = (const uint8_t*)f.dlog;
+  g2.a_kb = f.KBA;
+  g2.B = (const uint8_t*)f.wfd;
+  g2.b_kb = f.KBA;
+  g2.m0 = 0;
+  g2.m_tiles = f.tilesR;
+  g2.n_tiles = 1;
+  g2.KB = f.KBA;
+  launch_gemm<256, DgradEpi>(c, "k_gemm_dgrad_head", g2,
+                             DgradEpi::Args{f.mask[NL - 1], (uint8_t*)f.dz[NL - 1], f.bpart, (NL - 1) * kH, f.bw},
+                             f.num_sms);
+  for (int l = NL - 1; l >= 1; --l) {  // dz_{l-1} = dz_l W_l, masked by h_{l-1} > 0
+    GemmGeom g3{};
+    g3.A = (const uint8_t*)f.dz[l];
+    g3.a_kb = 4;
+    g3.B = (const uint8_t*)f.wdg[l];
+    g3.b_kb = 4;
+    g3.m0 = 0;
+    g3.m_tiles = f.tilesR;
+    g3.n_tiles = 1;
+    g3.KB = 4;
+    launch_gemm<256, DgradEpi>(c, "k_gemm_dgrad_hidden", g3,
+                               DgradEpi::Args{f.mask[l - 1], (uint8_t*)f.dz[l - 1], f.bpart, (l - 1) * kH, f.bw},
+                               f.num_sms);
+  }
+  {
+    WgArgs wa{};
+    wa.P = c.P;
+    wa.stst = f.stst;
+    wa.tilesR = f.tilesR;
+    wa.nranges = f.nranges;
+    wa.ntasks = f.ntasks;
+    wa.wpart = f.wpart;
+    int k = 0;
+    for (int l = 1; l < NL; ++l)  // dW_{l+1} = h_l^T dz_{l+1}
+      wa.task[k++] = WgTask{(const uint8_t*)f.h[l - 1], (const uint8_t*)f.dz[l], 4, 0, 0, 256};
+    for (int n = 0; n < f.NT; ++n)
+      wa.task[k++] = WgTask{(const uint8_t*)f.h[NL - 1], (const uint8_t*)f.dlog, f.KBA, 4 * n, 0, 256};
+    for (int j = 0; j < f.OB; ++j)
+      wa.task[k++] = WgTask{nullptr, (const uint8_t*)f.dz[0], 4, 0, 256 * j, std::min(256, f.O - 256 * j)};
+    const int smem = kWStages * (2 * kWOp + kWStBytes) + 1024;
+    set_smem_once(k_ls_wgrad<E>, smem);
+    ProfScope ps(c, "k_ls_wgrad");
+    k_ls_wgrad<E><<<f.ntasks * f.nranges, kGemmThreads, smem, c.stream>>>(wa);
+    c.launches++;
+  }
+  {
+    ProfScope ps(c, "k_ls_reduce");
+    k_ls_colsum<<<dim3((f.bw + 255) / 256, f.cgroups), 256, 0, c.stream>>>(f.bpart, f.tilesR, f.bw, f.cgroups,
+                                                                           f.bpart2);
+    RedArgs ra{f.wpart, f.bpart2, c.g32, f.nranges, f.cgroups, f.bw, f.A, f.O, NL, f.t_dense, f.t_head, f.t_w1, c.L};
+    k_ls_reduce<<<(unsigned)((c.L.n_params + 255) / 256), 256, 0, c.stream>>>(ra);
+    c.launches += 2;
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host side
+
+bool ls_supported(const Ctx& c, std::string* why) {
+  const int kind = c.env.kind;
+  if (kind != GFNX_ENV_BITSEQ && kind != GFNX_ENV_ISING) return false;
+  auto no = [&](const char* m) {
+    *why = m;
+    return false;
+  };
+  if (c.train.objective != GFNX_OBJ_TB) return no("bitseq/Ising fast path implements TB (BASELINE configs #3, #4)");
+  if (c.L.n_trunk < 2 || c.L.n_trunk > kMaxNL) return no("bitseq/Ising fast path needs 2..4 hidden layers");
+  for (int l = 1; l <= c.L.n_trunk; ++l)
+    if (c.L.dims[l] != kH) return no("bitseq/Ising fast path needs hidden width 256");
+  if (kind == GFNX_ENV_BITSEQ) {
+    if (c.P.bs_vocab != 256) return no("bitseq fast path needs k = 8 (256-word slots)");
+    if (c.P.bs_slots > 32) return no("bitseq fast path supports <= 32 slots");
+  } else {
+    if (c.P.is_D > 128) return no("Ising fast path supports <= 128 sites");
+  }
+  if (c.P.SW > 16) return no("fast path supports <= 16 packed state words");
+  if ((c.P.A + 255) / 256 * 2 > 32) return no("fast path supports <= 4096 actions");
+  if (c.Bl % kTile != 0) return no("bitseq/Ising fast path needs a per-rank batch that is a multiple of 128");
+  return true;
+}
+
+void ls_init(Ctx& c) {
+  auto* f = new LsState();
+  c.fast = f;
+  cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, c.device);
+  f->NL = c.L.n_trunk;
+  f->A = c.P.A;
+  f->Ap = (f->A + 255) / 256 * 256;
+  f->NT = f->Ap / 256;
+  f->G = f->Ap / 128;
+  f->KBA = f->Ap / 64;
+  f->O = c.P.O;
+  f->OB = (f->O + 255) / 256;
+  f->T = c.P.T;
+  f->SW = c.P.SW;
+  f->Bl = c.Bl;
+  f->R = c.Bl * f->T;
+  f->tilesB = c.Bl / kTile;
+  f->tilesR = f->R / kTile;
+  f->t_dense = 0;
+  f->t_head = f->NL - 1;
+  f->t_w1 = f->t_head + f->NT;
+  f->ntasks = f->t_w1 + f->OB;
+  if (f->ntasks > kMaxTasks) raise_error(GFNX_ERR_CONFIG, "fast path: too many weight-gradient tasks");
+  f->nranges = std::max(1, f->num_sms / f->ntasks);
+  f->loss_blocks = (c.Bl + 255) / 256;
+  f->bw = f->NL * kH + f->Ap;
+  f->cgroups = std::min(256, std::max(1, f->tilesR / 16));
+  const size_t img = (size_t)f->tilesR * kTile * kH * 2;
+  auto alloc = [&](auto** p, size_t bytes) {
+    cuda_check(cudaMalloc((void**)p, bytes), "lockstep alloc");
+    cuda_check(cudaMemset(*p, 0, bytes), "lockstep alloc");
+  };
+  alloc(&f->w1, sizeof(__nv_bfloat16) * (size_t)f->O * kH);
+  for (int l = 1; l < f->NL; ++l) {
+    alloc(&f->wfw[l], sizeof(__nv_bfloat16) * kH * kH);
+    alloc(&f->wdg[l], sizeof(__nv_bfloat16) * kH * kH);
+  }
+  alloc(&f->wff, sizeof(__nv_bfloat16) * (size_t)f->Ap * kH);
+  alloc(&f->wfd, sizeof(__nv_bfloat16) * (size_t)f->Ap * kH);
+  alloc(&f->bfp, sizeof(float) * f->Ap);
+  alloc(&f->h1init, sizeof(float) * kH);
+  alloc(&f->preact, sizeof(float) * (size_t)c.Bl * kH);
+  alloc(&f->cur, sizeof(uint32_t) * (size_t)c.Bl * f->SW);
+  alloc(&f->stst, sizeof(uint32_t) * (size_t)f->R * f->SW);
+  alloc(&f->last_act, sizeof(int32_t) * c.Bl);
+  for (int l = 0; l < f->NL; ++l) {
+    alloc(&f->h[l], img);
+    alloc(&f->dz[l], img);
+    alloc(&f->mask[l], (size_t)f->R * (kH / 8));
+  }
+  alloc(&f->logits, sizeof(__nv_bfloat16) * (size_t)c.Bl * f->Ap);
+  alloc(&f->stats, sizeof(float2) * (size_t)c.Bl * f->G);
+  alloc(&f->dlog, (size_t)f->tilesR * f->KBA * (kTile * 128));
+  alloc(&f->rowbuf, sizeof(float) * 2 * (size_t)f->R);
+  alloc(&f->coef, sizeof(float) * (size_t)f->R);
+  alloc(&f->bpart, sizeof(float) * (size_t)f->tilesR * f->bw);
+  alloc(&f->bpart2, sizeof(float) * (size_t)f->cgroups * f->bw);
+  alloc(&f->wpart, sizeof(float) * (size_t)f->ntasks * f->nranges * 256 * 256);
+  alloc(&f->lpart, sizeof(double) * 2 * f->loss_blocks);
+  ls_sync_weights(c);
+}
+
+void ls_free(Ctx& c) {
+  LsState* f = static_cast<LsState*>(c.fast);
+  if (!f) return;
+  std::vector<void*> ptrs = {f->w1, f->wff, f->wfd, f->bfp, f->h1init, f->preact, f->cur, f->stst, f->last_act,
+                             f->logits, f->stats, f->dlog, f->rowbuf, f->coef, f->bpart, f->bpart2, f->wpart,
+                             f->lpart};
+  for (int l = 0; l < kMaxNL; ++l) {
+    ptrs.push_back(f->wfw[l]);
+    ptrs.push_back(f->wdg[l]);
+    ptrs.push_back(f->h[l]);
+    ptrs.push_back(f->dz[l]);
+    ptrs.push_back(f->mask[l]);
+  }
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete f;
+  c.fast = nullptr;
+}
+
+void ls_sync_weights(Ctx& c) {
+  EmitArgs a = emit_args(c);
+  k_ls_emit<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a);
+  c.launches++;
+}
+
+void ls_rollout(Ctx& c, Key key, double eps) {
+  if (c.env.kind == GFNX_ENV_BITSEQ)
+    rollout_impl<BitseqEnv>(c, key, eps);
+  else
+    rollout_impl<IsingEnv>(c, key, eps);
+}
+
+void ls_train(Ctx& c) {
+  if (c.env.kind == GFNX_ENV_BITSEQ)
+    train_impl<BitseqEnv>(c);
+  else
+    train_impl<IsingEnv>(c);
+}
+
+}  // namespace gfnx

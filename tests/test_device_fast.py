@@ -131,25 +131,72 @@ def test_iteration_async_slots_match_batch_export():
     d.close()
 
 
-# ---- bit-sequence (non-autoregressive, k = 8) fast path: BASELINE config #3 shape
+# ---- fixed-length (lockstep) fast path: bit-sequence NAR k = 8 (config #3 shape) and
+# Ising (config #4 shape, 4 x 256 MLP)
 def _bitseq(n_bits, batch):
     e = abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8)
     t = abi.train_desc(abi.BITSEQ, batch=batch, objective="tb")
     return e, t
 
 
-def test_bitseq_fast_rollout_bitexact_at_eps1():
-    e, t = _bitseq(120, 128)
+def _ising(side, batch):
+    e = abi.env_desc(abi.ISING, is_side=side, is_sigma=0.2)
+    t = abi.train_desc(abi.ISING, batch=batch, objective="tb")
+    return e, t
+
+
+LOCKSTEP_EPS1 = [("bitseq", lambda: _bitseq(120, 128)), ("ising", lambda: _ising(10, 128))]
+LOCKSTEP_GRAD = [("bitseq", lambda: _bitseq(48, 128)), ("ising", lambda: _ising(6, 256))]
+
+
+@pytest.mark.parametrize("name,mk", LOCKSTEP_EPS1)
+def test_lockstep_fast_rollout_bitexact_at_eps1(name, mk):
+    e, t = mk()
     d = engine.Trainer(e, t)
     o = O.Oracle(e, t)
-    d.forward_rollout(0, 1.0)
-    o.rollout(0, 1.0)
-    _same_batch(d.batch(), o.batch())
+    for it in (0, 2):
+        d.forward_rollout(it, 1.0)
+        o.rollout(it, 1.0)
+        _same_batch(d.batch(), o.batch())
     d.close()
 
 
-def test_bitseq_fast_loss_and_grads_match_oracle_on_same_batch():
-    e, t = _bitseq(48, 128)
+@pytest.mark.parametrize("name,mk", [("bitseq", lambda: _bitseq(120, 16384)), ("ising", lambda: _ising(10, 16384))])
+def test_lockstep_sampler_matches_policy_distribution(name, mk):
+    """eps = 0: first actions of a large batch (all from s0) follow softmax(policy(s0))."""
+    e, t = mk()
+    d = engine.Trainer(e, t)
+    o = O.Oracle(e, t)
+    p, z = o.params()
+    p = 4.0 * p  # sharpen the policy so the test has power
+    o.set_params(p, z)
+    d.set_params(p, z)
+    d.forward_rollout(0, 0.0)
+    a0 = d.batch()["fwd_actions"][:, 0]
+    obs, mask = o.obs_after(np.zeros(0, dtype=np.int32))
+    lg, _ = o.mlp_forward(obs[None])
+    lg = np.where(mask > 0, lg[0], -np.inf)
+    pr = np.exp(lg - lg.max())
+    pr /= pr.sum()
+    cnt = np.bincount(a0, minlength=len(pr)).astype(np.float64)
+    if name == "bitseq":  # marginals over slot and word (A = 15 x 256)
+        bins = [(cnt.reshape(-1, 256).sum(1), pr.reshape(-1, 256).sum(1)),
+                (cnt.reshape(-1, 256).sum(0), pr.reshape(-1, 256).sum(0))]
+    else:
+        bins = [(cnt, pr)]
+    n = len(a0)
+    for c, q in bins:
+        keep = n * q >= 5
+        chi2 = float((((c - n * q) ** 2) / np.maximum(n * q, 1e-30))[keep].sum())
+        dof = int(keep.sum()) - 1
+        assert chi2 < dof + 6 * np.sqrt(2 * dof), (chi2, dof)
+        assert c[~keep].sum() <= max(20, 3 * n * q[~keep].sum())
+    d.close()
+
+
+@pytest.mark.parametrize("name,mk", LOCKSTEP_GRAD)
+def test_lockstep_fast_loss_and_grads_match_oracle_on_same_batch(name, mk):
+    e, t = mk()
     d = engine.Trainer(e, t)
     o = O.Oracle(e, t)
     d.set_params(*o.params())
@@ -172,11 +219,13 @@ def test_bitseq_fast_loss_and_grads_match_oracle_on_same_batch():
     d.close()
 
 
-def test_bitseq_fast_iterations_run():
-    e, t = _bitseq(120, 1024)
+@pytest.mark.parametrize("name,mk,T", [("bitseq", lambda: _bitseq(120, 1024), 15),
+                                      ("ising", lambda: _ising(10, 1024), 100)])
+def test_lockstep_fast_iterations_run(name, mk, T):
+    e, t = mk()
     d = engine.Trainer(e, t)
     losses = d.run(0, 3, read_losses=True)
     assert np.all(np.isfinite(losses))
     b = d.batch()
-    assert np.all(b["lengths"] == 15)
+    assert np.all(b["lengths"] == T)
     d.close()
