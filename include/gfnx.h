@@ -226,8 +226,16 @@ gfnx_status gfnx_profile(gfnx_ctx* ctx, int32_t enable);
 gfnx_status gfnx_counters(gfnx_ctx* ctx, int64_t* out, int32_t n);
 int32_t gfnx_profile_read(gfnx_ctx* ctx, char* names, int32_t names_cap, double* total_ms,
                           int32_t* counts, int32_t cap);
+/* Diagnostic clock64 totals of the persistent rollout's phases (fast path, hypergrid/DAG):
+ * mode 1 enables, 0 disables, 2 copies up to n totals into out and clears them.
+ * out: [layer1, hidden mma, hidden epilogue, head mma, sample+step, loop barrier,
+ *       tile steps, active slot-steps] summed over CTAs. */
+gfnx_status gfnx_phase_timers(gfnx_ctx* ctx, int32_t mode, int64_t* out, int32_t n);
 
 /* Stand-alone device kernels exposed for unit tests (threefry KAT, GEMM). */
+/* tcgen05.mma 128 x n x 256 (bf16, SW128 smem operands) issue-to-completion clocks per CTA
+ * for `reps` back-to-back MMAs (mode 0: wait after each, 1: K-split issue, 2: one wait). */
+gfnx_status gfnx_test_mma_rate(int32_t n, int32_t reps, int32_t mode, int32_t grid, int64_t* cycles);
 gfnx_status gfnx_test_threefry(const uint64_t* keys_hi_lo, const uint64_t* ctr, int64_t n,
                                uint64_t* out);
 gfnx_status gfnx_test_uniform_fold(uint64_t key_hi, uint64_t key_lo, const uint64_t* idx,

@@ -486,6 +486,7 @@ void gfnx_destroy(gfnx_ctx* h) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
   if (c.fast) fast_free(c);
+  if (c.phase) cudaFree(c.phase);
   void* ptrs[] = {c.d_modes, c.d_bs_logr, c.d_is_nbr, c.d_is_J, c.d_dag_cache, c.d_neglog,
                   c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars,
                   c.batch.lengths, c.batch.actions, c.batch.log_rewards, c.batch.delta,
@@ -824,6 +825,29 @@ gfnx_status gfnx_counters(gfnx_ctx* h, int64_t* out, int32_t n) {
   });
 }
 
+gfnx_status gfnx_phase_timers(gfnx_ctx* h, int32_t mode, int64_t* out, int32_t n) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (mode == 1) {
+      if (!c.phase) cuda_check(cudaMalloc(&c.phase, sizeof(long long) * 16), "phase timers");
+      // (16 slots)
+      cuda_check(cudaMemsetAsync(c.phase, 0, sizeof(long long) * 16, c.stream), "phase timers");
+    } else if (mode == 0) {
+      if (c.phase) {
+        cudaStreamSynchronize(c.stream);
+        cudaFree(c.phase);
+      }
+      c.phase = nullptr;
+    } else if (c.phase) {
+      long long v[16];
+      cuda_check(cudaMemcpyAsync(v, c.phase, sizeof v, cudaMemcpyDeviceToHost, c.stream), "phase timers");
+      cuda_check(cudaStreamSynchronize(c.stream), "sync");
+      for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
+      cuda_check(cudaMemsetAsync(c.phase, 0, sizeof v, c.stream), "phase timers");
+    }
+  });
+}
+
 gfnx_status gfnx_profile(gfnx_ctx* h, int32_t enable) {
   h->c.profiling = enable != 0;
   return GFNX_OK;
@@ -880,6 +904,13 @@ gfnx_status gfnx_test_threefry(const uint64_t* keys, const uint64_t* ctr, int64_
     cudaFree(dk);
     cudaFree(dc);
     cudaFree(dout);
+  });
+}
+
+gfnx_status gfnx_test_mma_rate(int32_t n, int32_t reps, int32_t mode, int32_t grid, int64_t* cycles) {
+  return guard(nullptr, [&] {
+    test_mma_rate(n, reps, mode, grid, reinterpret_cast<long long*>(cycles));
+    cuda_check(cudaGetLastError(), "mma rate");
   });
 }
 

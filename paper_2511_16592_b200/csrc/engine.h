@@ -60,6 +60,9 @@ void ls_sync_weights(Ctx& c);
 void ls_rollout(Ctx& c, Key key, double eps);
 void ls_train(Ctx& c);
 
+// diagnostics — fast.cu
+void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out);
+
 // shared small kernels — batch.cu
 void launch_row_scan(Ctx& c);
 
@@ -113,6 +116,9 @@ struct Ctx {
   double* ck_gx = nullptr;
   double* ck_pair = nullptr;
   int64_t ck_rows_cap = 0;
+
+  // optional rollout phase clocks (env GFNX_PHASE_TIMERS=1 at create): [8] int64
+  long long* phase = nullptr;
 
   // fast-mode state (opaque, fast.cu)
   void* fast = nullptr;

@@ -52,20 +52,21 @@ struct EnvParams {
 
 // ---------------------------------------------------------------------------
 struct HypergridEnv {
-  struct State {
-    uint8_t c[kMaxHgDim];
+  struct State {  // coordinate i in bits [8i, 8i + 8) of cw (register-resident: no local memory)
+    uint64_t cw;
     int step;
     bool term;
+    __host__ __device__ int c(int i) const { return (int)((cw >> (8 * i)) & 0xffu); }
   };
   __host__ __device__ static void reset(const EnvParams&, State& s) {
-    for (int i = 0; i < kMaxHgDim; ++i) s.c[i] = 0;
+    s.cw = 0;
     s.step = 0;
     s.term = false;
   }
   __host__ __device__ static bool legal(const EnvParams& P, const State& s, int a) {
     if (s.term) return false;
     if (a == P.stop) return true;
-    return s.c[a] < P.hg_side - 1;
+    return s.c(a) < P.hg_side - 1;
   }
   __host__ __device__ static bool step(const EnvParams& P, State& s, int a) {
     s.step += 1;
@@ -73,44 +74,47 @@ struct HypergridEnv {
       s.term = true;
       return true;
     }
-    s.c[a] += 1;
+    s.cw += 1ull << (8 * a);
     return false;
   }
   __host__ __device__ static int num_parents(const EnvParams& P, const State& s) {
     if (s.term) return 1;
     int n = 0;
-    for (int i = 0; i < P.hg_dim; ++i) n += s.c[i] > 0;
+    for (int i = 0; i < P.hg_dim; ++i) n += s.c(i) > 0;
     return n;
   }
   __host__ __device__ static int backward_action(const EnvParams&, int a) { return a; }
   __host__ __device__ static double log_reward(const EnvParams& P, const State& s) {
     uint32_t p1 = 1, p2 = 1;
     for (int i = 0; i < P.hg_dim; ++i) {
-      const int c = s.c[i];
+      const int c = s.c(i);
       p1 &= (P.hg_f1[c >> 5] >> (c & 31)) & 1;
       p2 &= (P.hg_f2[c >> 5] >> (c & 31)) & 1;
     }
     return P.hg_logr[p1 | (p2 << 1)];
   }
   __host__ __device__ static void pack(const EnvParams& P, const State& s, uint32_t* w) {
-    for (int i = 0; i < P.SW; ++i) w[i] = 0;
-    for (int i = 0; i < P.hg_dim; ++i) w[i >> 2] |= (uint32_t)s.c[i] << (8 * (i & 3));
+    // byte i = coordinate i: the packed words are the little-endian bytes of cw
+    w[0] = (uint32_t)s.cw;
+    if (P.SW > 1) w[1] = (uint32_t)(s.cw >> 32);
+    for (int i = 2; i < P.SW; ++i) w[i] = 0;
   }
   __host__ __device__ static void unpack(const EnvParams& P, const uint32_t* w, State& s) {
     reset(P, s);
-    for (int i = 0; i < P.hg_dim; ++i) s.c[i] = (uint8_t)(w[i >> 2] >> (8 * (i & 3)));
+    s.cw = (uint64_t)w[0] | (P.SW > 1 ? (uint64_t)w[1] << 32 : 0ull);
+    if (P.hg_dim < 8) s.cw &= (1ull << (8 * P.hg_dim)) - 1ull;
   }
   // active one-hot features (value 1.0): i * side + c_i   (hypergrid.cpp:82-85)
   template <class F>
   __host__ __device__ static void features(const EnvParams& P, const State& s, F&& f) {
-    for (int i = 0; i < P.hg_dim; ++i) f(i * P.hg_side + s.c[i], 1.0);
+    for (int i = 0; i < P.hg_dim; ++i) f(i * P.hg_side + s.c(i), 1.0);
   }
   // change of the observation caused by action a taken in s (for incremental layer 1)
   template <class F>
   __host__ __device__ static void delta_features(const EnvParams& P, const State& s, int a, F&& f) {
     if (a == P.stop) return;
-    f(a * P.hg_side + s.c[a], -1.0f);
-    f(a * P.hg_side + s.c[a] + 1, 1.0f);
+    f(a * P.hg_side + s.c(a), -1.0f);
+    f(a * P.hg_side + s.c(a) + 1, 1.0f);
   }
 };
 
@@ -299,18 +303,33 @@ struct IsingEnv {
 };
 
 // ---------------------------------------------------------------------------
+// eight 16-bit rows in two registers (dynamic row index without local memory)
+struct U16x8 {
+  uint64_t lo, hi;
+  __host__ __device__ uint32_t get(int i) const {
+    return (uint32_t)((((i & 4) ? hi : lo) >> (16 * (i & 3))) & 0xffffu);
+  }
+  __host__ __device__ void orv(int i, uint32_t v) {
+    const uint64_t m = (uint64_t)(v & 0xffffu) << (16 * (i & 3));
+    if (i & 4)
+      hi |= m;
+    else
+      lo |= m;
+  }
+};
+
 struct DagEnv {
   struct State {
-    uint16_t adj[kMaxDagD], cl[kMaxDagD];  // adj[u] bit v: u->v ; cl[a] bit b: b ~> a
+    U16x8 adj, cl;  // adj row u bit v: u->v ; cl row a bit b: b ~> a
     int count;
     int step;
     bool term;
   };
   __host__ __device__ static void reset(const EnvParams&, State& s) {
-    for (int a = 0; a < kMaxDagD; ++a) {
-      s.adj[a] = 0;
-      s.cl[a] = (uint16_t)(1u << a);
-    }
+    s.adj.lo = s.adj.hi = 0;
+    // cl[a] = 1 << a
+    s.cl.lo = 0x0008000400020001ull;
+    s.cl.hi = 0x0080004000200010ull;
     s.count = 0;
     s.step = 0;
     s.term = false;
@@ -325,7 +344,7 @@ struct DagEnv {
     if (a == P.stop) return true;
     int u, v;
     edge(a, P.dag_d, u, v);
-    return !((s.adj[u] >> v) & 1) && !((s.cl[u] >> v) & 1);
+    return !((s.adj.get(u) >> v) & 1) && !((s.cl.get(u) >> v) & 1);
   }
   __host__ __device__ static bool step(const EnvParams& P, State& s, int a) {
     s.step += 1;
@@ -335,10 +354,10 @@ struct DagEnv {
     }
     int u, v;
     edge(a, P.dag_d, u, v);
-    s.adj[u] |= (uint16_t)(1u << v);
-    const uint16_t row_u = s.cl[u];  // closure_update dag.cpp:324-329
+    s.adj.orv(u, 1u << v);
+    const uint32_t row_u = s.cl.get(u);  // closure_update dag.cpp:324-329
     for (int q = 0; q < P.dag_d; ++q)
-      if ((s.cl[q] >> v) & 1) s.cl[q] |= row_u;
+      if ((s.cl.get(q) >> v) & 1) s.cl.orv(q, row_u);
     s.count += 1;
     return false;
   }
@@ -352,42 +371,48 @@ struct DagEnv {
     for (int j = 0; j < d; ++j) {
       uint32_t parents = 0;
       for (int u = 0; u < d; ++u)
-        if ((s.adj[u] >> j) & 1) parents |= 1u << u;
+        if ((s.adj.get(u) >> j) & 1) parents |= 1u << u;
       acc += P.dag_cache[j * (1 << d) + parents];
     }
     return acc;
   }
   __host__ __device__ static void pack(const EnvParams& P, const State& s, uint32_t* w) {
-    for (int i = 0; i < P.SW; ++i) w[i] = 0;
-    for (int u = 0; u < P.dag_d; ++u) w[u >> 1] |= (uint32_t)s.adj[u] << (16 * (u & 1));
+    // row u in 16-bit half (u & 1) of word u >> 1: the words are the halves of adj.lo/hi
+    const uint32_t x[4] = {(uint32_t)s.adj.lo, (uint32_t)(s.adj.lo >> 32), (uint32_t)s.adj.hi,
+                           (uint32_t)(s.adj.hi >> 32)};
+    for (int i = 0; i < P.SW; ++i) w[i] = i < 4 ? x[i] : 0u;
   }
   // adjacency only; the transpose closure is rebuilt (closure_from_adjacency dag.cpp:331-346)
   __host__ __device__ static void unpack(const EnvParams& P, const uint32_t* w, State& s) {
     reset(P, s);
     const int d = P.dag_d;
     for (int u = 0; u < d; ++u) {
-      s.adj[u] = (uint16_t)(w[u >> 1] >> (16 * (u & 1)));
+      const uint32_t row = (w[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+      s.adj.orv(u, row);
 #ifdef __CUDA_ARCH__
-      s.count += __popc(s.adj[u]);
+      s.count += __popc(row);
 #else
-      s.count += __builtin_popcount(s.adj[u]);
+      s.count += __builtin_popcount(row);
 #endif
     }
+    U16x8 cl{0, 0};
     for (int a = 0; a < d; ++a) {
-      uint16_t c = (uint16_t)(1u << a);
+      uint32_t c = 1u << a;
       for (int b = 0; b < d; ++b)
-        if ((s.adj[b] >> a) & 1) c |= (uint16_t)(1u << b);
-      s.cl[a] = c;
+        if ((s.adj.get(b) >> a) & 1) c |= 1u << b;
+      cl.orv(a, c);
     }
     for (int k = 0; k < d; ++k)
       for (int a = 0; a < d; ++a)
-        if ((s.cl[a] >> k) & 1) s.cl[a] |= s.cl[k];
+        if ((cl.get(a) >> k) & 1) cl.orv(a, cl.get(k));
+    for (int a = d; a < kMaxDagD; ++a) cl.orv(a, 1u << a);
+    s.cl = cl;
   }
   template <class F>
   __host__ __device__ static void features(const EnvParams& P, const State& s, F&& f) {
     for (int u = 0; u < P.dag_d; ++u)
       for (int v = 0; v < P.dag_d; ++v)
-        if ((s.adj[u] >> v) & 1) f(u * P.dag_d + v, 1.0);
+        if ((s.adj.get(u) >> v) & 1) f(u * P.dag_d + v, 1.0);
   }
   template <class F>
   __host__ __device__ static void delta_features(const EnvParams& P, const State&, int a, F&& f) {

@@ -24,6 +24,7 @@
 //                   operand images (adam_step optim.cpp:19-43)
 #include <math.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "engine.h"
@@ -94,43 +95,52 @@ Weights weights_of(Ctx& c) {
   return w;
 }
 
-// reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100)
-// in fp64 on the fp32 logits of one row
+// reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100) on
+// the fp32 logits of one row: exp in fp32, mixture weights / cumulative sum in fp64 in the
+// reference's order (so eps = 1 draws are bit-exact), fully unrolled over AMAX (registers).
 template <class Env, int AMAX>
 GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const float (&logit)[AMAX],
-                        int A, double eps, double u01, bool* bad) {
+                        int A, double eps, double u01, const double* inv_legal, bool* bad) {
+  uint32_t lm = 0;
   int legal = 0;
-  double hi = -INFINITY;
-  for (int c = 0; c < A; ++c)
-    if (Env::legal(P, s, c)) {
+  float hi = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < AMAX; ++c)
+    if (c < A && Env::legal(P, s, c)) {
+      lm |= 1u << c;
       ++legal;
-      hi = fmax(hi, (double)logit[c]);
+      hi = fmaxf(hi, logit[c]);
     }
   if (legal == 0 || !isfinite(hi)) {
     *bad = true;
     return -1;
   }
-  double w[AMAX];
-  double z = 0.0;
-  for (int c = 0; c < A; ++c) {
-    w[c] = Env::legal(P, s, c) ? exp((double)logit[c] - hi) : 0.0;
-    z += w[c];
+  float e[AMAX];
+  float z = 0.f;
+#pragma unroll
+  for (int c = 0; c < AMAX; ++c) {
+    e[c] = ((lm >> c) & 1u) ? __expf(logit[c] - hi) : 0.f;
+    z += e[c];
   }
-  const double u = eps / legal;
+  // eps * (1/legal) from a table: exactly the reference's eps / legal at eps = 1 (where
+  // the policy term vanishes and draws are bit-exact); policy weight in fp32
+  const double u = eps * inv_legal[legal];
+  const float kzf = (float)(1.0 - eps) * __frcp_rn(z);
+  const double kz = (double)kzf;
   double total = 0.0;
-  for (int c = 0; c < A; ++c) {
-    if (w[c] > 0.0 || Env::legal(P, s, c)) w[c] = (1.0 - eps) * w[c] / z + u;
-    total += w[c];
-  }
+#pragma unroll
+  for (int c = 0; c < AMAX; ++c)
+    if ((lm >> c) & 1u) total += kz * (double)e[c] + u;
   const double x = u01 * total;
   double acc = 0.0;
-  for (int c = 0; c < A; ++c) {
-    acc += w[c];
-    if (x < acc) return c;
-  }
-  for (int c = A - 1; c >= 0; --c)
-    if (w[c] > 0.0) return c;
-  return A - 1;
+  int pick = -1;
+#pragma unroll
+  for (int c = 0; c < AMAX; ++c)
+    if ((lm >> c) & 1u) {
+      acc += kz * (double)e[c] + u;
+      if (pick < 0 && x < acc) pick = c;
+    }
+  return pick >= 0 ? pick : 31 - __clz(lm);
 }
 
 // ---------------------------------------------------------------------------
@@ -156,22 +166,33 @@ struct RolloutArgs {
   DeviceBatch batch;
   uint32_t* stst;
   int32_t* work;
+  long long* phase;  // optional per-phase clock totals (gfnx_phase_timers), else nullptr
 };
 
+// H = 256 stages the A operand (h1, then h2) in two 128-column halves through one 32 KB
+// buffer (split-K: the MMA over the first half runs while the second half is produced),
+// which frees the shared memory that keeps W1 resident for the layer-1 row reads.
+template <int H>
+__host__ __device__ constexpr int rollout_acols() {
+  return H == 256 ? H / 2 : H;
+}
 template <int H, int NH>
-constexpr int rollout_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + NH * H * 2 + 1024;
+constexpr int rollout_smem_fixed() {
+  return H * H * 2 + NH * H * 2 + kTile * rollout_acols<H>() * 2 + 1024;
 }
 
-
-template <class Env, int H, int NH>
+template <class Env, int H, int NH, bool W1S>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* w2img = smem;                 // H x H bf16 (resident for the whole rollout)
-  uint8_t* atile = w2img + H * H * 2;    // 128 x H bf16 activations (h1, then h2)
-  uint8_t* whimg = atile + kTile * H * 2;  // head image [NH][H]
-  constexpr int HC = H / 2;
+  constexpr bool SPLIT = H == 256;
+  constexpr int AK = rollout_acols<H>();  // columns of the staged A operand
+  constexpr int HC = H / 2;               // columns owned by each thread of a row
+  uint8_t* w2img = smem;                  // H x H bf16 (resident for the whole rollout)
+  uint8_t* whimg = w2img + H * H * 2;     // head image [NH][H]
+  uint8_t* atile = whimg + NH * H * 2;    // 128 x AK bf16 activations
+  __nv_bfloat16* w1s = reinterpret_cast<__nv_bfloat16*>(atile + kTile * AK * 2);  // [O][H] if W1S
+  const __nv_bfloat16* w1 = W1S ? w1s : a.W.w1;
   __shared__ float h1init[H], b2s[H];
   __shared__ float bhs[NH];
   __shared__ Key skeys[128];
@@ -182,16 +203,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   __shared__ uint8_t row_init[kTile];
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
+  __shared__ unsigned long long smax;
+  __shared__ double inv_legal[NH + 1];
 
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, c0 = half * HC;
   const int T = P.T, A = P.A;
-  if (warp == 0) tmem_alloc<2 * H>(&tbase);
+  if (warp == 0) tmem_alloc<2 * H>(&tbase);  // [0, H) accumulator, [H, 2H) layer-1 pre-activation
   if (tid == 0) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
+    smax = 0;
   }
   __syncthreads();
   if (tid == 0) {
@@ -199,9 +223,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
     bulk_g2s_big(whimg, a.W.whead_f, NH * H * 2, &mbar);
   }
+  if (W1S) {  // W1 rows with 16-byte chunk c stored at c ^ (row & 7)
+    const uint4* src = reinterpret_cast<const uint4*>(a.W.w1);
+    uint4* dst = reinterpret_cast<uint4*>(w1s);
+    constexpr int CPR = H / 8;  // chunks per row
+    for (int i = tid; i < P.O * CPR; i += kThreads) {
+      const int f = i / CPR, c = i % CPR;
+      dst[f * CPR + (c ^ (f & 7))] = src[i];
+    }
+  }
   for (int t = tid; t < T && t < 128; t += kThreads) skeys[t] = fold_in(a.key, (uint64_t)t);
   for (int j = tid; j < H; j += kThreads) b2s[j] = a.W.b2[j];
   if (tid < NH) bhs[tid] = tid < A ? a.W.bf[tid] : (tid == A ? a.W.bfl[0] : 0.f);
+  if (tid <= NH) inv_legal[tid] = tid ? 1.0 / tid : 0.0;
   {  // h1init = b1 + x(s0) W1 (layer-1 pre-activation of the initial state)
     typename Env::State s0;
     Env::reset(P, s0);
@@ -218,10 +252,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   const uint32_t tmem = tbase;
   const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
 
+  // one MMA round: thread 0 issues `issue` and waits for completion; everyone re-syncs
+  auto mma_round = [&](auto&& issue) {
+    if (tid == 0) {
+      tc_fence_after();
+      issue();
+      umma_commit(&mbar);
+    }
+  };
+  auto mma_join = [&]() {
+    if (tid == 0) mbar_wait(&mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto publish = [&]() {  // generic-proxy smem writes -> visible to the tensor core
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+  };
+  // ReLU(acc + bias) of TMEM columns [col0, col0 + 32) -> bf16 into the staged A tile
+  auto stage32 = [&](uint32_t tcol, int acol, const float* bias) {
+    uint32_t r[32];
+    tmem_ld32(lane_base + tcol, r);
+    tmem_wait_ld();
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + (bias ? bias[2 * i] : 0.f), 0.f),
+                          fmaxf(__uint_as_float(r[2 * i + 1]) + (bias ? bias[2 * i + 1] : 0.f), 0.f));
+    st_row32(atile, row, acol, pk);
+  };
+
   typename Env::State s;
   Env::reset(P, s);
   int b = -1, tstep = 0;
-  bool active = false, bad = false;
+  bool active = false, bad = false, pending = false;
+  int bnext = 0;
   if (half == 0) {
     b = atomicAdd(a.work, 1);
     active = b < a.Bl;
@@ -230,13 +297,50 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     row_b[row] = b;
     row_t[row] = 0;
   }
-  while (__syncthreads_or(active)) {
-    // (1) layer-1 pre-activation (fp32 in TMEM columns [H, 2H)), own column half
+  long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+  auto mark = [&](int k) {
+    if (a.phase && tid == 0) {
+      const long long tnow = clock64();
+      ph[k] += tnow - tprev;
+      tprev = tnow;
+    }
+  };
+  int nact;
+  while ((nact = __syncthreads_count(active || pending)) > 0) {
+    mark(0);
+    if (a.phase && tid == 0) {
+      ph[6] += 1;
+      ph[7] += nact;
+      ph[8] += smax;
+      smax = 0;
+    }
+    // (1) layer-1 pre-activation (fp32 in TMEM columns [H, 2H)), own column half, updated
+    //     from the W1 rows of the features the last action changed (smem-resident W1 is
+    //     stored with its 16-byte chunks XOR-swizzled by row, so the 32 lanes of a warp -
+    //     32 different rows - spread over the banks)
     const bool init = row_init[row];
-    const int nd = row_nd[row];
+    const int nd = init ? 0 : row_nd[row];
+    int df[2] = {0, 0};
+    float dv[2] = {0.f, 0.f};
+#pragma unroll
+    for (int d = 0; d < 2; ++d)
+      if (d < nd) {
+        df[d] = row_df[row][d];
+        dv[d] = row_dv[row][d];
+      }
 #pragma unroll 1
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
+      // W1 rows of the (at most 2) changed features, fetched before the TMEM round trip
+      uint4 w[2][4];
+#pragma unroll
+      for (int d = 0; d < 2; ++d) {
+        const uint4* wr = reinterpret_cast<const uint4*>(w1 + (size_t)df[d] * H);
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          w[d][c] = d < nd ? (W1S ? wr[((col >> 3) + c) ^ (df[d] & 7)] : __ldg(wr + (col >> 3) + c))
+                           : make_uint4(0, 0, 0, 0);
+      }
       uint32_t r[32];
       tmem_ld32(lane_base + H + col, r);  // warp-collective: every lane executes it
       tmem_wait_ld();
@@ -244,76 +348,86 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
 #pragma unroll
         for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(h1init[col + i]);
       } else {
-        for (int d = 0; d < nd; ++d) {
-          const float dv = row_dv[row][d];
-          const uint4* wr = reinterpret_cast<const uint4*>(a.W.w1 + (size_t)row_df[row][d] * H + col);
-          uint4 w[4];
 #pragma unroll
-          for (int c = 0; c < 4; ++c) w[c] = __ldg(wr + c);
+        for (int d = 0; d < 2; ++d) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint32_t wv[4] = {w[c].x, w[c].y, w[c].z, w[c].w};
+            const uint32_t wv[4] = {w[d][c].x, w[d][c].y, w[d][c].z, w[d][c].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv * bf16_lo(wv[e]));
-              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv * bf16_hi(wv[e]));
+              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv[d] * bf16_lo(wv[e]));
+              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv[d] * bf16_hi(wv[e]));
+            }
+          }
+        }
+        // (more than 2 changed features: general path)
+        for (int d = 2; d < nd; ++d) {
+          const float dvx = row_dv[row][d];
+          const int fx = row_df[row][d];
+          const uint4* wr = reinterpret_cast<const uint4*>(w1 + (size_t)fx * H);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 x = W1S ? wr[((col >> 3) + c) ^ (fx & 7)] : __ldg(wr + (col >> 3) + c);
+            const uint32_t wv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dvx * bf16_lo(wv[e]));
+              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dvx * bf16_hi(wv[e]));
             }
           }
         }
       }
       tmem_st32(lane_base + H + col, r);
-      uint32_t pk[16];
+      if (!SPLIT || half == 0) {
+        uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
-      st_row32(atile, row, col, pk);
+        for (int i = 0; i < 16; ++i)
+          pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
+        st_row32(atile, row, col, pk);
+      }
     }
     tmem_wait_st();
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    // (2) hidden layer on the tensor cores: acc[128 x H] = relu(h1) W2^T
-    if (tid == 0) {
-      tc_fence_after();
-      mma_kk<H, H>(tmem, atile, w2img, false);
-      umma_commit(&mbar);
+    if (pending) {  // the refill claim issued at the last termination lands here
+      b = bnext;
+      active = b < a.Bl;
+      row_b[row] = active ? b : -1;
+      pending = false;
     }
-    // half-1 threads draw the row's uniform while the MMA runs (rng.cpp:64-66)
-    if (half == 1) {
+    publish();
+    mark(1);
+    // (2) hidden layer on the tensor cores: acc[128 x H] = relu(h1) W2^T (split-K for H=256)
+    mma_round([&] { mma_kk<H, AK>(tmem, atile, w2img, false); });
+    if (half == 1) {  // draw the row's uniform while the MMA runs (rng.cpp:64-66)
       const int rb = row_b[row];
-      row_u[row] = rb >= 0 && rb < a.Bl
-                       ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb)))
-                       : 0.0;
+      row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc_fence_after();
-    // (3) h2 = ReLU(acc + b2) -> bf16 tile (overwrites h1: the hidden MMA is complete)
+    mma_join();
+    if (SPLIT) {
+      if (half == 1)
 #pragma unroll 1
-    for (int q = 0; q < HC / 32; ++q) {
-      const int col = c0 + q * 32;
-      uint32_t r[32];
-      tmem_ld32(lane_base + col, r);
-      tmem_wait_ld();
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b2s[col + 2 * i], 0.f),
-                            fmaxf(__uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f));
-      st_row32(atile, row, col, pk);
+        for (int q = 0; q < HC / 32; ++q) stage32(H + c0 + q * 32, q * 32, nullptr);
+      publish();
+      mma_round([&] { mma_kk<H, AK>(tmem, atile, w2img + (AK / 64) * (H * 128), true); });
+      mma_join();
     }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
-    // (4) head on the tensor cores: logits[128 x NH] = h2 Wf (+ flow column, unused here)
-    if (tid == 0) {
-      tc_fence_after();
-      mma_kk<NH, H>(tmem, atile, whimg, false);
-      umma_commit(&mbar);
+    mark(2);
+    // (3) h2 = ReLU(acc + b2) -> staged bf16 tile, (4) head on the tensor cores
+    if (!SPLIT || half == 0)
+#pragma unroll 1
+      for (int q = 0; q < HC / 32; ++q) stage32(c0 + q * 32, c0 + q * 32, b2s + c0 + q * 32);
+    publish();
+    mark(3);
+    mma_round([&] { mma_kk<NH, AK>(tmem, atile, whimg, false); });
+    mma_join();
+    if (SPLIT) {  // head output sits in acc columns [0, NH): half 1 reads [HC, H)
+      if (half == 1)
+#pragma unroll 1
+        for (int q = 0; q < HC / 32; ++q) stage32(c0 + q * 32, q * 32, b2s + c0 + q * 32);
+      publish();
+      mma_round([&] { mma_kk<NH, AK>(tmem, atile, whimg + (AK / 64) * (NH * 128), true); });
+      mma_join();
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc_fence_after();
+    mark(4);
     float logit[NH];
     {
       uint32_t r[16];
@@ -326,8 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     tc_fence_before();
+    const long long ts0 = a.phase ? clock64() : 0;
     if (half == 0 && active) {
-      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], &bad);
+      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], inv_legal, &bad);
       if (act < 0) {
         active = false;
       } else {
@@ -351,8 +466,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
-          b = atomicAdd(a.work, 1);
-          active = b < a.Bl;
+          bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          pending = true;
+          active = false;
           Env::reset(P, s);
           tstep = 0;
           row_init[row] = 1;
@@ -364,7 +480,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         row_t[row] = tstep;
       }
     }
+    if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
+    mark(5);
   }
+  if (a.phase && tid == 0)
+    for (int k = 0; k < 9; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)ph[k]);
   if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
   __syncthreads();
   if (warp == 0) tmem_dealloc<2 * H>(tmem);
@@ -1188,17 +1308,28 @@ struct Kernels {
     a.batch = c.batch;
     a.stst = f.stst;
     a.work = f.work;
+    a.phase = c.phase;
     const int T = c.P.T;
     cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.nparents, 0, sizeof(uint16_t) * (size_t)c.Bl * T, c.stream);
     if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.lengths, 0, sizeof(int32_t) * c.Bl, c.stream);
     cudaMemsetAsync(f.work, 0, sizeof(int32_t), c.stream);
-    const int smem = rollout_smem_bytes<H, NH>();
-    set_smem_once(k_fast_rollout<Env, H, NH>, smem);
     const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
+    const int fixed = rollout_smem_fixed<H, NH>();
+    const int w1b = c.P.O * H * 2;
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_fast_rollout<Env, H, NH, true>);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
     ProfScope ps(c, "k_fast_rollout");
-    k_fast_rollout<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(a);
+    if (fixed + w1b + (int)fa.sharedSizeBytes <= optin) {  // W1 resident in smem
+      set_smem_once(k_fast_rollout<Env, H, NH, true>, fixed + w1b);
+      k_fast_rollout<Env, H, NH, true><<<grid, kThreads, fixed + w1b, c.stream>>>(a);
+    } else {
+      set_smem_once(k_fast_rollout<Env, H, NH, false>, fixed);
+      k_fast_rollout<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(a);
+    }
     c.launches++;
   }
   static void train(Ctx& c, bool apply, double lr) {
@@ -1444,4 +1575,72 @@ void fast_adam(Ctx& c, double lr) {
   if (bitseq) ls_sync_weights(c);
 }
 
+}  // namespace gfnx
+
+// ---------------------------------------------------------------------------
+// micro-benchmark hook: tcgen05.mma issue-to-completion rate on one SM (diagnostics)
+namespace gfnx {
+namespace {
+template <int N>
+__global__ void __launch_bounds__(128, 1) k_mma_rate(int reps, int mode, long long* out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  uint8_t* aimg = smem;                 // 128 x 256 bf16
+  uint8_t* bimg = smem + 128 * 256 * 2;  // N x 256 bf16
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < (128 + N) * 256 * 2 / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0x3c003c00u, 0x3c003c00u, 0, 0);
+  if (tid < 32) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    uint32_t ph = 0;
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      if (mode == 0) {  // 128 x N x 256 from K-major SW128 images
+        mma_kk<N, 256>(tbase + (r & 1) * 256, aimg, bimg, false);
+      } else {  // same FLOPs as 16 separate K=16 issues with commits in between
+        constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+        const uint32_t a0 = smem_u32(aimg), b0 = smem_u32(bimg);
+        for (int s = 0; s < 16; ++s) {
+          umma_bf16(tbase, umma_desc_sw128(a0 + (s >> 2) * (128 * 128) + (s & 3) * 32, 16, 1024),
+                    umma_desc_sw128(b0 + (s >> 2) * (N * 128) + (s & 3) * 32, 16, 1024), idesc, s > 0);
+        }
+      }
+      if (mode != 2 || r == reps - 1) {
+        umma_commit(&bar);
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
+    }
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (tid < 32) tmem_dealloc<512>(tbase);
+}
+}  // namespace
+
+void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out) {
+  long long* d;
+  cudaMalloc(&d, sizeof(long long) * grid);
+  const int smem = (128 + 256) * 256 * 2 + 1024;
+  if (n == 256) {
+    cudaFuncSetAttribute(k_mma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma_rate<256><<<grid, 128, smem>>>(reps, mode, d);
+  } else {
+    cudaFuncSetAttribute(k_mma_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma_rate<128><<<grid, 128, smem>>>(reps, mode, d);
+  }
+  cudaMemcpy(host_out, d, sizeof(long long) * grid, cudaMemcpyDeviceToHost);
+  cudaFree(d);
+}
 }  // namespace gfnx

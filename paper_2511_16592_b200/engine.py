@@ -84,6 +84,8 @@ def lib():
         L.gfnx_profile_read.restype = C.c_int32
         L.gfnx_profile_read.argtypes = [vp, vp, C.c_int32, vp, vp, C.c_int32]
         L.gfnx_counters.argtypes = [vp, vp, C.c_int32]
+        L.gfnx_phase_timers.argtypes = [vp, C.c_int32, vp, C.c_int32]
+        L.gfnx_test_mma_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp]
         L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
         _LIB = L
@@ -257,6 +259,15 @@ class Trainer:
         out = np.zeros(4, dtype=np.int64)
         self._check(lib().gfnx_counters(self.h, _p(out), 4))
         return [int(x) for x in out]
+
+    PHASES = ("loop_barrier", "layer1", "hidden_mma", "hidden_epilogue", "head_mma", "sample_step",
+              "tile_steps", "active_slot_steps", "sample_step_max")
+
+    def phase_timers(self, mode: int):
+        """Rollout phase clocks (diagnostic): 1 enable, 0 disable, 2 read + clear -> dict."""
+        out = np.zeros(len(self.PHASES), dtype=np.int64)
+        self._check(lib().gfnx_phase_timers(self.h, mode, _p(out), len(self.PHASES)))
+        return dict(zip(self.PHASES, (int(x) for x in out))) if mode == 2 else None
 
     def kernel_launches(self) -> int:
         return lib().gfnx_kernel_launches(self.h)

@@ -1,0 +1,21 @@
+#!/usr/bin/env python
+"""tcgen05.mma 128 x N x 256 rate on B200 (diagnostic for the rollout's per-step MMA)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2511_16592_b200 import engine  # noqa: E402
+
+L = engine.lib()
+for n in (128, 256):
+    for mode in (0, 1, 2):
+        for grid in (1, 148):
+            reps = 2000
+            out = np.zeros(grid, dtype=np.int64)
+            rc = L.gfnx_test_mma_rate(n, reps, mode, grid, out.ctypes.data)
+            assert rc == 0, engine.lib().gfnx_last_error(None)
+            cyc = out.mean() / reps
+            macs = 128 * n * 256
+            print(f"N={n} mode={mode} grid={grid}: {cyc:8.1f} cycles/MMA  {macs / cyc:7.0f} MAC/clk/SM")
