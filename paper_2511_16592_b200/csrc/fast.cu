@@ -510,19 +510,26 @@ struct TrainArgs {
   int objective;
 };
 
+// smem: W2 image | head image | staged A (split-K for H = 256, as in the rollout) | W1 (opt.)
 template <int H, int NH>
-constexpr int fwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + NH * H * 2 + 1024;
+constexpr int fwd_smem_fixed() {
+  return H * H * 2 + NH * H * 2 + kTile * rollout_acols<H>() * 2 + 1024;
 }
 
-template <class Env, int H, int NH>
+constexpr int kMaxSWFwd = 4;  // packed state words prefetched per row
+
+template <class Env, int H, int NH, bool W1S>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  uint8_t* w2img = smem;
-  uint8_t* atile = w2img + H * H * 2;
-  uint8_t* whimg = atile + kTile * H * 2;
+  constexpr bool SPLIT = H == 256;
+  constexpr int AK = rollout_acols<H>();
   constexpr int HC = H / 2;
+  uint8_t* w2img = smem;
+  uint8_t* whimg = w2img + H * H * 2;
+  uint8_t* atile = whimg + NH * H * 2;
+  __nv_bfloat16* w1s = reinterpret_cast<__nv_bfloat16*>(atile + kTile * AK * 2);
+  const __nv_bfloat16* w1 = W1S ? w1s : a.W.w1;
   __shared__ float b1s[H], b2s[H];
   __shared__ float bhs[NH];
   __shared__ uint64_t mbar;
@@ -546,6 +553,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
     bulk_g2s_big(whimg, a.W.whead_f, NH * H * 2, &mbar);
   }
+  if (W1S) {  // 16-byte chunk c of W1 row f stored at c ^ (f & 7) (bank spread, as the rollout)
+    const uint4* src = reinterpret_cast<const uint4*>(a.W.w1);
+    uint4* dst = reinterpret_cast<uint4*>(w1s);
+    constexpr int CPR = H / 8;
+    for (int i = tid; i < P.O * CPR; i += kThreads) {
+      const int f = i / CPR, c = i % CPR;
+      dst[f * CPR + (c ^ (f & 7))] = src[i];
+    }
+  }
   for (int j = tid; j < H; j += kThreads) {
     b1s[j] = a.W.b1[j];
     b2s[j] = a.W.b2[j];
@@ -558,21 +574,46 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   const uint32_t tmem = tbase;
   const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
   const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
+  auto mma_join = [&]() {
+    if (tid == 0) mbar_wait(&mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto publish = [&]() {
+    fence_proxy_async();
+    tc_fence_before();
+    __syncthreads();
+  };
+  // row record of a tile, fetched one tile ahead (row -> (b, t) -> packed state, action)
+  auto fetch = [&](int tile, uint32_t (&w)[kMaxSWFwd], int& act) {
+    const int r = tile * kTile + row;
+    act = 0;
+#pragma unroll
+    for (int i = 0; i < kMaxSWFwd; ++i) w[i] = 0;
+    if (r < R && tile < tiles) {
+      const size_t bt = (size_t)a.batch.row_bt[r];
+#pragma unroll
+      for (int i = 0; i < kMaxSWFwd; ++i)
+        if (i < P.SW) w[i] = a.stst[bt * P.SW + i];
+      act = a.batch.actions[bt];
+    }
+  };
+  uint32_t wn[kMaxSWFwd];
+  int actn;
+  fetch(blockIdx.x, wn, actn);
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int r = tile * kTile + row;
     const bool valid = r < R;
+    uint32_t wc[kMaxSWFwd];
+#pragma unroll
+    for (int i = 0; i < kMaxSWFwd; ++i) wc[i] = wn[i];
+    const int act = actn;
+    fetch(tile + gridDim.x, wn, actn);  // in flight during this tile
     typename Env::State s;
-    Env::reset(P, s);
-    int act = 0;
-    if (valid) {
-      const size_t bt = (size_t)a.batch.row_bt[r];
-      Env::unpack(P, a.stst + bt * P.SW, s);
-      act = a.batch.actions[bt];
-    }
-    if (tid == 0) bulk_wait_read0();  // previous tile's h2 store has left smem
-    __syncthreads();
-    // layer 1: sparse one-hot gather (fp32) -> bf16 ReLU tile, own column half.
-    // Features are collected first so the row loads of a chunk are issued back to back.
+    Env::unpack(P, wc, s);
+    // layer 1: sparse one-hot gather (fp32) -> bf16 ReLU; own column half. With split-K,
+    // half 1 keeps its packed values until the first K-half MMA has read the staged tile.
     int nf = 0;
     int fidx[kGatherMax];
     float fval[kGatherMax];
@@ -584,7 +625,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
           ++nf;
         }
       });
-#pragma unroll 1
+    uint32_t keep[SPLIT ? HC / 2 : 1];
+    if (tid == 0) bulk_wait_read0();  // previous tile's h2 stores have left smem
+    __syncthreads();
+#pragma unroll
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
       float v[32];
@@ -595,7 +639,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
         uint4 w[kGatherMax];
 #pragma unroll
         for (int k = 0; k < kGatherMax; ++k)
-          if (k < nf) w[k] = __ldg(reinterpret_cast<const uint4*>(a.W.w1 + (size_t)fidx[k] * H + col) + c);
+          if (k < nf) {
+            const uint4* wr = reinterpret_cast<const uint4*>(w1 + (size_t)fidx[k] * H);
+            w[k] = W1S ? wr[((col >> 3) + c) ^ (fidx[k] & 7)] : __ldg(wr + (col >> 3) + c);
+          }
 #pragma unroll
         for (int k = 0; k < kGatherMax; ++k)
           if (k < nf) {
@@ -615,26 +662,48 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
         mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
       if (valid) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
-      st_row32(atile, row, col, pk);
+      if (!SPLIT || half == 0) {
+        st_row32(atile, row, col, pk);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) keep[(q * 16 + i) % (SPLIT ? HC / 2 : 1)] = pk[i];
+      }
     }
-    fence_proxy_async();
-    tc_fence_before();
-    __syncthreads();
+    publish();
+    // hidden layer, K-half 0 (or all of K): h1 image out + MMA
     if (tid == 0) {
       tc_fence_after();
-      bulk_s2g(a.h1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+      bulk_s2g(a.h1 + (size_t)tile * kTile * H, atile, kTile * AK * 2);
       bulk_commit();
-      mma_kk<H, H>(tmem, atile, w2img, false);
+      mma_kk<H, AK>(tmem, atile, w2img, false);
       umma_commit(&mbar);
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc_fence_after();
+    mma_join();
+    if (SPLIT) {
+      if (tid == 0) bulk_wait_read0();
+      __syncthreads();
+      if (half == 1)
+#pragma unroll
+        for (int q = 0; q < HC / 32; ++q) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) pk[i] = keep[(q * 16 + i) % (SPLIT ? HC / 2 : 1)];
+          st_row32(atile, row, q * 32, pk);
+        }
+      publish();
+      if (tid == 0) {
+        tc_fence_after();
+        bulk_s2g(a.h1 + (size_t)tile * kTile * H + kTile * AK, atile, kTile * AK * 2);
+        bulk_commit();
+        mma_kk<H, AK>(tmem, atile, w2img + (AK / 64) * (H * 128), true);
+        umma_commit(&mbar);
+      }
+      mma_join();
+    }
     if (tid == 0) bulk_wait_read0();
     __syncthreads();
-    // epilogue: h2 (bf16-rounded) -> tile and ReLU mask
-#pragma unroll 1
-    for (int q = 0; q < HC / 32; ++q) {
+    // epilogue: h2 (bf16-rounded) -> staged tile + ReLU mask; head GEMM per K-half
+    auto h2_stage = [&](int q, int acol) {
       const int col = c0 + q * 32;
       uint32_t r32[32];
       tmem_ld32(lane_base + col, r32);
@@ -649,21 +718,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
         mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
       if (valid) a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
-      st_row32(atile, row, col, pk);
-    }
-    tc_fence_before();
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {  // h2 image out + head GEMM (logits and flow) on the tensor cores
+      st_row32(atile, row, acol, pk);
+    };
+    if (!SPLIT || half == 0)
+#pragma unroll 1
+      for (int q = 0; q < HC / 32; ++q) h2_stage(q, c0 + q * 32);
+    publish();
+    if (tid == 0) {
       tc_fence_after();
-      bulk_s2g(a.h2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+      bulk_s2g(a.h2 + (size_t)tile * kTile * H, atile, kTile * AK * 2);
       bulk_commit();
-      mma_kk<NH, H>(tmem, atile, whimg, false);
+      mma_kk<NH, AK>(tmem, atile, whimg, false);
       umma_commit(&mbar);
     }
-    mbar_wait(&mbar, phase);
-    phase ^= 1;
-    tc_fence_after();
+    mma_join();
+    if (SPLIT) {  // head output sits in acc columns [0, NH): half 1 reads [HC, H)
+      if (tid == 0) bulk_wait_read0();
+      __syncthreads();
+      if (half == 1)
+#pragma unroll 1
+        for (int q = 0; q < HC / 32; ++q) h2_stage(q, q * 32);
+      publish();
+      if (tid == 0) {
+        tc_fence_after();
+        bulk_s2g(a.h2 + (size_t)tile * kTile * H + kTile * AK, atile, kTile * AK * 2);
+        bulk_commit();
+        mma_kk<NH, AK>(tmem, atile, whimg + (AK / 64) * (NH * 128), true);
+        umma_commit(&mbar);
+      }
+      mma_join();
+    }
     float logit[NH];
     {
       uint32_t r16[16];
@@ -1355,11 +1439,21 @@ struct Kernels {
     ta.L = c.L;
     ta.objective = c.train.objective;
     const int grid = f.num_sms;
-    int smem = fwd_smem_bytes<H, NH>();
-    set_smem_once(k_fast_fwd<Env, H, NH>, smem);
     {
+      const int fixed = fwd_smem_fixed<H, NH>();
+      const int w1b = c.P.O * H * 2;
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, k_fast_fwd<Env, H, NH, true>);
+      int optin = 0;
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
       ProfScope ps(c, "k_fast_fwd");
-      k_fast_fwd<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(ta);
+      if (fixed + w1b + (int)fa.sharedSizeBytes <= optin && c.P.SW <= kMaxSWFwd) {
+        set_smem_once(k_fast_fwd<Env, H, NH, true>, fixed + w1b);
+        k_fast_fwd<Env, H, NH, true><<<grid, kThreads, fixed + w1b, c.stream>>>(ta);
+      } else {
+        set_smem_once(k_fast_fwd<Env, H, NH, false>, fixed);
+        k_fast_fwd<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(ta);
+      }
     }
     LossArgs la{};
     la.batch = c.batch;
@@ -1383,7 +1477,7 @@ struct Kernels {
     }
     k_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
-    smem = bwd_smem_bytes<H, NH>();
+    int smem = bwd_smem_bytes<H, NH>();
     set_smem_once(k_fast_bwd<Env, H, NH>, smem);
     {
       ProfScope ps(c, "k_fast_bwd");
