@@ -1701,6 +1701,13 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(int reps, int mode, long lo
     for (int r = 0; r < reps; ++r) {
       if (mode == 0) {  // 128 x N x 256 from K-major SW128 images
         mma_kk<N, 256>(tbase + (r & 1) * 256, aimg, bimg, false);
+      } else if (mode >= 3) {  // MN-major operands (weight-gradient shape), K = 256 rows
+        constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+        const uint32_t a0 = smem_u32(aimg), b0 = smem_u32(bimg);
+        const uint32_t lbo = mode == 3 ? 64 * 128 : 128 * 128;  // 64- or 128-row MN blocks
+        for (int k = 0; k < 16; ++k)
+          umma_bf16(tbase, umma_desc_sw128(a0 + (k & 3) * 2048, lbo, 1024),
+                    umma_desc_sw128(b0 + (k & 3) * 2048, lbo, 1024), idesc, k > 0);
       } else {  // same FLOPs as 16 separate K=16 issues with commits in between
         constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
         const uint32_t a0 = smem_u32(aimg), b0 = smem_u32(bimg);
@@ -1709,7 +1716,7 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(int reps, int mode, long lo
                     umma_desc_sw128(b0 + (s >> 2) * (N * 128) + (s & 3) * 32, 16, 1024), idesc, s > 0);
         }
       }
-      if (mode != 2 || r == reps - 1) {
+      if ((mode != 2 && mode != 4) || r == reps - 1) {
         umma_commit(&bar);
         mbar_wait(&bar, ph);
         ph ^= 1;

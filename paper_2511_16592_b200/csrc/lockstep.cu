@@ -127,7 +127,8 @@ struct LsState {
   int cgroups = 0;
   float* bpart2 = nullptr;                   // [cgroups][bw]
   float* wpart = nullptr;                    // [task][range][256][256]
-  int ntasks = 0, nranges = 0;
+  int ntasks = 0;
+  int first[kMaxTasks + 1] = {};             // wgrad CTAs of task k: [first[k], first[k+1])
   int t_dense = 0, t_head = 0, t_w1 = 0;     // first task of each kind
   double* lpart = nullptr;
   int loss_blocks = 0;
@@ -578,8 +579,10 @@ struct WgTask {
 struct WgArgs {
   EnvParams P;
   const uint32_t* stst;
-  int tilesR, nranges, ntasks;
+  int tilesR, ntasks;
+  int first[kMaxTasks + 1];  // CTAs [first[k], first[k+1]) split task k's rows into ranges
   float* wpart;
+  long long* phase;  // optional diagnostics (gfnx_phase_timers)
   WgTask task[kMaxTasks];
 };
 
@@ -598,11 +601,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_const
   __shared__ uint64_t full[kWStages], empty[kWStages], built[kWStages], done;
   __shared__ uint32_t tbase;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int task = blockIdx.x / a.nranges, range = blockIdx.x % a.nranges;
+  int task = 0;
+  while (task + 1 < a.ntasks && (int)blockIdx.x >= a.first[task + 1]) ++task;
+  const int nranges = a.first[task + 1] - a.first[task], range = blockIdx.x - a.first[task];
   const WgTask& tk = a.task[task];
   const bool onehot = tk.a == nullptr;
   const int halves = (onehot && tk.nf <= 128) ? 1 : 2;  // M' = 256 (2 x 128) or 128
-  const int per = (a.tilesR + a.nranges - 1) / a.nranges;
+  const int per = (a.tilesR + nranges - 1) / nranges;
   const int t0 = range * per, t1 = min(a.tilesR, t0 + per);
   const int nq = t1 > t0 ? 2 * (t1 - t0) : 0;  // 64-row stages
   const int SW = a.P.SW;
@@ -620,11 +625,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_const
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = tbase;
+  const long long tk0 = clock64();
+  long long* ph = a.phase ? a.phase + (onehot ? 0 : 8) : nullptr;
   if (warp == 0) {
     if (lane == 0) {  // ---- producer
+      long long tw = 0;
       for (int q = 0; q < nq; ++q) {
         const int slot = q % kWStages, tile = t0 + q / 2, h = q % 2;
+        const long long t0w = clock64();
         if (q >= kWStages) mbar_wait(&empty[slot], ((q / kWStages) - 1) & 1);
+        tw += clock64() - t0w;
         uint8_t* sa = smem + slot * kSlot;
         uint8_t* sb = sa + kWOp;
         const int st_bytes = kWStage * SW * 4;
@@ -635,14 +645,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_const
           wg_copy_half(sa, tk.a + (size_t)tile * (4 * kTile * 128), 0, h, &full[slot]);
         wg_copy_half(sb, tk.b + (size_t)tile * tk.b_kbs * (kTile * 128), tk.b_kb0, h, &full[slot]);
       }
+      if (ph) atomicAdd((unsigned long long*)ph + 4, (unsigned long long)tw);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = umma_idesc_bf16(128, 256, true, true);
+      long long tf = 0, tb = 0;
       for (int q = 0; q < nq; ++q) {
         const int slot = q % kWStages;
+        const long long t0w = clock64();
         mbar_wait(&full[slot], (q / kWStages) & 1);
+        const long long t1w = clock64();
         if (onehot) mbar_wait(&built[slot], (q / kWStages) & 1);
+        tf += t1w - t0w;
+        tb += clock64() - t1w;
         tc_fence_after();
         const uint32_t a0 = smem_u32(smem + slot * kSlot), b0 = a0 + kWOp;
         for (int hh = 0; hh < halves; ++hh)
@@ -653,35 +669,51 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_const
         umma_commit(&empty[slot]);
       }
       umma_commit(&done);
+      if (ph) {
+        atomicAdd((unsigned long long*)ph + 2, (unsigned long long)tf);
+        atomicAdd((unsigned long long*)ph + 3, (unsigned long long)tb);
+        atomicAdd((unsigned long long*)ph + 5, (unsigned long long)nq);
+      }
     }
   } else if (warp >= 4) {
     const int et = tid - 128;  // 0..255
     if (onehot) {  // ---- builders
-      const int row = et & 63, part = et >> 6;
+      long long tf = 0, tbld = 0;
       for (int q = 0; q < nq; ++q) {
         const int slot = q % kWStages;
         uint8_t* sa = smem + slot * kSlot;
+        const long long t0w = clock64();
         mbar_wait(&full[slot], (q / kWStages) & 1);  // slot free (producer waited) + states in
-        uint4* z = reinterpret_cast<uint4*>(sa + et * 128);
+        const long long t1w = clock64();
+        tf += t1w - t0w;
+        uint4* z = reinterpret_cast<uint4*>(sa);  // lane-contiguous 16-byte stores (no bank conflicts)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) z[i] = make_uint4(0, 0, 0, 0);
+        for (int i = 0; i < 8; ++i) z[i * 256 + et] = make_uint4(0, 0, 0, 0);
         epi_bar();
+        const int row = et & 63, part = et >> 6;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(sa + 2 * kWOp) + row * SW;
+        uint8_t* rowp = sa + row * 128;
+        const int rsw = row & 7;
         Lock<E>::block_features(a.P, w, tk.f0, part, [&](int f, float v) {
-          *reinterpret_cast<__nv_bfloat16*>(sa + (f >> 6) * (kWStage * 128) +
-                                            (sw128_offset(row, f & 63, kWStage) & (kWStage * 128 - 1))) =
-              __float2bfloat16(v);
+          const int c = f & 63;
+          *reinterpret_cast<__nv_bfloat16*>(rowp + (f >> 6) * (kWStage * 128) + ((((c >> 3) ^ rsw)) << 4) +
+                                            (c & 7) * 2) = __float2bfloat16(v);
         });
         fence_proxy_async();
         epi_bar();
         if (et == 0) mbar_arrive_local(&built[slot]);
+        tbld += clock64() - t1w;
+      }
+      if (ph && et == 0) {
+        atomicAdd((unsigned long long*)ph + 0, (unsigned long long)tf);
+        atomicAdd((unsigned long long*)ph + 1, (unsigned long long)tbld);
       }
     }
     // ---- epilogue: lane quarter x column half, both M'-halves
     const int ew = warp - 4, quarter = ew & 3, half = ew >> 2;
-    if (nq > 0) mbar_wait(&done, 0);
+    if (nq > 0) mbar_wait_sleep(&done, 0, 2000);
     tc_fence_after();
-    float* slab = a.wpart + ((size_t)task * a.nranges + range) * (256 * 256);
+    float* slab = a.wpart + (size_t)blockIdx.x * (256 * 256);
     for (int hh = 0; hh < 2; ++hh) {
       const int mrow = hh * 128 + quarter * 32 + lane;
       for (int q = 0; q < 4; ++q) {
@@ -701,6 +733,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_ls_wgrad(const __grid_const
     tc_fence_before();
   }
   __syncthreads();
+  if (ph && tid == 0) {
+    atomicAdd((unsigned long long*)ph + 6, (unsigned long long)(clock64() - tk0));
+    atomicAdd((unsigned long long*)ph + 7, 1ull);
+  }
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
@@ -719,7 +755,8 @@ struct RedArgs {
   const float* wpart;
   const float* bpart2;
   float* g;
-  int nranges, groups, bw, A, O, NL, t_dense, t_head, t_w1;
+  int groups, bw, A, O, NL, t_dense, t_head, t_w1;
+  int first[kMaxTasks + 1];
   MlpLayout L;
 };
 
@@ -729,7 +766,7 @@ __global__ void k_ls_reduce(RedArgs a) {
   if (e >= L.n_params) return;
   auto slab_sum = [&](int task, int m, int n) {
     float s = 0.f;
-    for (int r = 0; r < a.nranges; ++r) s += a.wpart[(((size_t)task * a.nranges + r) * 256 + m) * 256 + n];
+    for (int c = a.first[task]; c < a.first[task + 1]; ++c) s += a.wpart[((size_t)c * 256 + m) * 256 + n];
     return s;
   };
   auto bias_sum = [&](int col) {
@@ -917,9 +954,10 @@ void train_impl(Ctx& c) {
     wa.P = c.P;
     wa.stst = f.stst;
     wa.tilesR = f.tilesR;
-    wa.nranges = f.nranges;
     wa.ntasks = f.ntasks;
+    for (int k = 0; k <= f.ntasks; ++k) wa.first[k] = f.first[k];
     wa.wpart = f.wpart;
+    wa.phase = c.phase;
     int k = 0;
     for (int l = 1; l < NL; ++l)  // dW_{l+1} = h_l^T dz_{l+1}
       wa.task[k++] = WgTask{(const uint8_t*)f.h[l - 1], (const uint8_t*)f.dz[l], 4, 0, 0, 256};
@@ -930,14 +968,15 @@ void train_impl(Ctx& c) {
     const int smem = kWStages * (2 * kWOp + kWStBytes) + 1024;
     set_smem_once(k_ls_wgrad<E>, smem);
     ProfScope ps(c, "k_ls_wgrad");
-    k_ls_wgrad<E><<<f.ntasks * f.nranges, kGemmThreads, smem, c.stream>>>(wa);
+    k_ls_wgrad<E><<<f.first[f.ntasks], kGemmThreads, smem, c.stream>>>(wa);
     c.launches++;
   }
   {
     ProfScope ps(c, "k_ls_reduce");
     k_ls_colsum<<<dim3((f.bw + 255) / 256, f.cgroups), 256, 0, c.stream>>>(f.bpart, f.tilesR, f.bw, f.cgroups,
                                                                            f.bpart2);
-    RedArgs ra{f.wpart, f.bpart2, c.g32, f.nranges, f.cgroups, f.bw, f.A, f.O, NL, f.t_dense, f.t_head, f.t_w1, c.L};
+    RedArgs ra{f.wpart, f.bpart2, c.g32, f.cgroups, f.bw, f.A, f.O, NL, f.t_dense, f.t_head, f.t_w1, {}, c.L};
+    for (int k = 0; k <= f.ntasks; ++k) ra.first[k] = f.first[k];
     k_ls_reduce<<<(unsigned)((c.L.n_params + 255) / 256), 256, 0, c.stream>>>(ra);
     c.launches += 2;
   }
@@ -994,7 +1033,24 @@ void ls_init(Ctx& c) {
   f->t_w1 = f->t_head + f->NT;
   f->ntasks = f->t_w1 + f->OB;
   if (f->ntasks > kMaxTasks) raise_error(GFNX_ERR_CONFIG, "fast path: too many weight-gradient tasks");
-  f->nranges = std::max(1, f->num_sms / f->ntasks);
+  {  // CTAs per task proportional to its per-stage cost (one-hot operands are built in smem;
+     // their cost grows with the nonzeros per row inside the 256-feature block)
+    auto weight = [&](int k) {
+      if (k < f->t_w1) return 1.0;
+      if (c.env.kind != GFNX_ENV_ISING) return 1.1;
+      const int f0 = 256 * (k - f->t_w1);
+      const int sites = std::max(0, std::min(c.P.is_D, (f0 + 256 + 2) / 3) - f0 / 3);
+      return 1.0 + 3.0 * sites / 85.0;
+    };
+    double tot = 0.0;
+    for (int k = 0; k < f->ntasks; ++k) tot += weight(k);
+    int used = 0;
+    for (int k = 0; k < f->ntasks; ++k) {
+      f->first[k] = used;
+      used += std::max(1, (int)(f->num_sms * weight(k) / tot));
+    }
+    f->first[f->ntasks] = used;
+  }
   f->loss_blocks = (c.Bl + 255) / 256;
   f->bw = f->NL * kH + f->Ap;
   f->cgroups = std::min(256, std::max(1, f->tilesR / 16));
@@ -1028,7 +1084,7 @@ void ls_init(Ctx& c) {
   alloc(&f->coef, sizeof(float) * (size_t)f->R);
   alloc(&f->bpart, sizeof(float) * (size_t)f->tilesR * f->bw);
   alloc(&f->bpart2, sizeof(float) * (size_t)f->cgroups * f->bw);
-  alloc(&f->wpart, sizeof(float) * (size_t)f->ntasks * f->nranges * 256 * 256);
+  alloc(&f->wpart, sizeof(float) * (size_t)f->first[f->ntasks] * 256 * 256);
   alloc(&f->lpart, sizeof(double) * 2 * f->loss_blocks);
   ls_sync_weights(c);
 }

@@ -10,8 +10,8 @@ from paper_2511_16592_b200 import engine  # noqa: E402
 
 L = engine.lib()
 for n in (128, 256):
-    for mode in (0, 1, 2):
-        for grid in (1, 148):
+    for mode in (0, 1, 2, 3, 4):
+        for grid in (1,):
             reps = 2000
             out = np.zeros(grid, dtype=np.int64)
             rc = L.gfnx_test_mma_rate(n, reps, mode, grid, out.ctypes.data)
