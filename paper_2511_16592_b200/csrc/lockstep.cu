@@ -267,7 +267,7 @@ struct LogEpi : EpiBase {
 
 struct SampleArgs {
   EnvParams P;
-  Key key;
+  Key key;  // fold_in(rollout key, t)
   double eps;
   int b0, Bl, t, T, Ap, G;
   const __nv_bfloat16* logits;
@@ -287,10 +287,8 @@ GFNX_DEV double warp_sum_d(double x) {
 
 // warp per trajectory: two-level inverse CDF with the reference's single uniform
 template <class E>
-__global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + warp;
-  if (b >= a.Bl) return;
+GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
+  const int lane = threadIdx.x & 31;
   const EnvParams& P = a.P;
   const uint32_t* w = a.cur + (size_t)b * P.SW;
   // ---- group level (lane g <-> 128-column group g; G <= 32)
@@ -315,7 +313,8 @@ __global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
   for (int o = 16; o > 0; o >>= 1) legal += __shfl_xor_sync(0xffffffffu, legal, o);
   const double eps = a.eps;
   const double u_eps = legal > 0 ? eps / legal : 0.0;
-  const double mass = lcount > 0 ? (1.0 - eps) * gz / z + u_eps * lcount : 0.0;
+  const double kz = (1.0 - eps) / z;  // policy weight scale (0 at eps = 1: bit-exact draws)
+  const double mass = lcount > 0 ? kz * gz + u_eps * lcount : 0.0;
   double incl = mass;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -323,7 +322,6 @@ __global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
     if (lane >= o) incl += y;
   }
   const double total = __shfl_sync(0xffffffffu, incl, 31);
-  const double u01 = uniform_scalar(fold_in(fold_in(a.key, (uint64_t)a.t), (uint64_t)(a.b0 + b)));
   double x = u01 * total;
   const unsigned pos = __ballot_sync(0xffffffffu, mass > 0.0);
   const unsigned hit = __ballot_sync(0xffffffffu, mass > 0.0 && x < incl);
@@ -339,7 +337,7 @@ __global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
     double w4[4], ls = 0.0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      w4[e] = ((lm >> e) & 1u) ? (1.0 - eps) * (double)__expf(xs[e] - hi) / z + u_eps : 0.0;
+      w4[e] = ((lm >> e) & 1u) ? kz * (double)__expf(xs[e] - hi) + u_eps : 0.0;
       ls += w4[e];
     }
     double ci = ls;
@@ -399,6 +397,23 @@ __global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
       E::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
     }
     if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
+  }
+}
+
+constexpr int kSampleRows = 4;  // trajectories per warp (their uniforms drawn in parallel)
+
+template <class E>
+__global__ void __launch_bounds__(256) k_ls_sample(SampleArgs a) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int bw = (blockIdx.x * 8 + warp) * kSampleRows;
+  // rng.cpp:64-66 uniform of draw (t, b): lane j < kSampleRows draws row bw + j
+  const double uj = (lane < kSampleRows && bw + lane < a.Bl)
+                        ? uniform_scalar(fold_in(a.key, (uint64_t)(a.b0 + bw + lane)))
+                        : 0.0;
+#pragma unroll 1
+  for (int j = 0; j < kSampleRows; ++j) {
+    const double u01 = __shfl_sync(0xffffffffu, uj, j);
+    if (bw + j < a.Bl) sample_one<E>(a, bw + j, u01);
   }
 }
 
@@ -892,10 +907,10 @@ void rollout_impl(Ctx& c, Key key, double eps) {
     g.n_tiles = f.NT;
     typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl};
     launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
-    SampleArgs sa{c.P, key, eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst, f.last_act,
-                  f.rowbuf, c.batch};
+    SampleArgs sa{c.P, fold_in(key, (uint64_t)t), eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst,
+                  f.last_act, f.rowbuf, c.batch};
     ProfScope ps(c, "k_ls_sample");
-    k_ls_sample<E><<<(Bl + 7) / 8, 256, 0, c.stream>>>(sa);
+    k_ls_sample<E><<<(Bl + 8 * kSampleRows - 1) / (8 * kSampleRows), 256, 0, c.stream>>>(sa);
     c.launches++;
   }
 }
