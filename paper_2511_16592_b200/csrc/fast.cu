@@ -57,9 +57,31 @@ struct FastState {
   double* lpart = nullptr;            // [blocks][2] loss / dlogz partials
   double* lampow = nullptr;           // pow(lambda, k)
   int32_t* work = nullptr;            // rollout work counter
+  int32_t* frow_bt = nullptr;         // [max_tiles*128] row slot -> b*T + t (-1 = empty)
+  int32_t* bt_row = nullptr;          // [Bl*T] b*T + t -> row slot
+  int32_t* tilectr = nullptr;         // number of 128-row tiles of row slots
+  bool fused = false;                 // row slots hold the rollout's forward for the current weights
   int rs = 0;                         // rowbuf stride (floats)
   int loss_blocks = 0;
 };
+
+// row slots in trajectory order (row0[b] + t) when the training forward is recomputed
+__global__ void k_linear_rows(const int32_t* __restrict__ lengths, const int32_t* __restrict__ row0, int Bl,
+                              int T, const int32_t* counters, int32_t* frow_bt, int32_t* bt_row,
+                              int32_t* tilectr) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int R = counters[0];
+  const int tiles = (R + kTile - 1) / kTile;
+  if (b < Bl) {
+    const int L = lengths[b], r0 = row0[b];
+    for (int t = 0; t < L; ++t) {
+      frow_bt[r0 + t] = b * T + t;
+      bt_row[(size_t)b * T + t] = r0 + t;
+    }
+  }
+  if (b < kTile && R + b < tiles * kTile) frow_bt[R + b] = -1;
+  if (b == 0) *tilectr = tiles;
+}
 
 FastState& FS(Ctx& c) { return *static_cast<FastState*>(c.fast); }
 
@@ -98,12 +120,19 @@ Weights weights_of(Ctx& c) {
 // reference sampler (eps_uniform objectives.cpp:242-264 + categorical rng.cpp:87-100) on
 // the fp32 logits of one row: exp in fp32, mixture weights / cumulative sum in fp64 in the
 // reference's order (so eps = 1 draws are bit-exact), fully unrolled over AMAX (registers).
+// On return e[c] = exp(logit[c] - hi) over legal c (0 elsewhere), z = sum e, rz = 1 / z:
+// the masked log-softmax statistics of the row (lse = hi + log z) for the training record.
 template <class Env, int AMAX>
 GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const float (&logit)[AMAX],
-                        int A, double eps, double u01, const double* inv_legal, bool* bad) {
+                        int A, double eps, double u01, const double* inv_legal, bool* bad,
+                        float (&e)[AMAX], float& hi, float& z, float& rz) {
   uint32_t lm = 0;
   int legal = 0;
-  float hi = -INFINITY;
+  hi = -INFINITY;
+  z = 1.f;
+  rz = 1.f;
+#pragma unroll
+  for (int c = 0; c < AMAX; ++c) e[c] = 0.f;
 #pragma unroll
   for (int c = 0; c < AMAX; ++c)
     if (c < A && Env::legal(P, s, c)) {
@@ -115,17 +144,17 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
     *bad = true;
     return -1;
   }
-  float e[AMAX];
-  float z = 0.f;
+  z = 0.f;
 #pragma unroll
   for (int c = 0; c < AMAX; ++c) {
     e[c] = ((lm >> c) & 1u) ? __expf(logit[c] - hi) : 0.f;
     z += e[c];
   }
+  rz = __frcp_rn(z);
   // eps * (1/legal) from a table: exactly the reference's eps / legal at eps = 1 (where
   // the policy term vanishes and draws are bit-exact); policy weight in fp32
   const double u = eps * inv_legal[legal];
-  const float kzf = (float)(1.0 - eps) * __frcp_rn(z);
+  const float kzf = (float)(1.0 - eps) * rz;
   const double kz = (double)kzf;
   double total = 0.0;
 #pragma unroll
@@ -167,6 +196,14 @@ struct RolloutArgs {
   uint32_t* stst;
   int32_t* work;
   long long* phase;  // optional per-phase clock totals (gfnx_phase_timers), else nullptr
+  // fused training forward: every sampled row's h1 / h2 (bf16 tile images), ReLU masks and
+  // log-softmax statistics, in emission order; 128-row tiles are claimed from tilectr
+  __nv_bfloat16 *h1, *h2;
+  uint32_t *mask1, *mask2;
+  float* rowbuf;
+  int rs, flow;
+  int32_t *frow_bt, *bt_row, *tilectr;
+  int emit_mode;  // diagnostics (GFNX_EMIT_MODE): 0 full, 1 no row emission, 2 no masks, 3 no images
 };
 
 // H = 256 stages the A operand (h1, then h2) in two 128-column halves through one 32 KB
@@ -205,6 +242,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   __shared__ uint32_t tbase;
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
+  __shared__ int s_cur0, s_next;  // emission tiles: first claimed, next claimed
+  __shared__ uint4 row_m1[kTile][H / 128], row_m2[kTile][H / 128];  // ReLU masks of the round
 
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -216,8 +255,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
     smax = 0;
+    const int t0 = atomicAdd(a.tilectr, 2);
+    s_cur0 = t0;
+    s_next = t0 + 1;
   }
   __syncthreads();
+  // emission cursor (uniform over the CTA): rows of this CTA fill tile `cur` from `fill`,
+  // overflowing into the pre-claimed tile s_next
+  int cur = s_cur0, fill = 0;
   if (tid == 0) {
     mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
@@ -272,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     __syncthreads();
   };
   // ReLU(acc + bias) of TMEM columns [col0, col0 + 32) -> bf16 into the staged A tile
-  auto stage32 = [&](uint32_t tcol, int acol, const float* bias) {
+  auto stage32 = [&](uint32_t tcol, int acol, const float* bias, uint32_t* mword) {
     uint32_t r[32];
     tmem_ld32(lane_base + tcol, r);
     tmem_wait_ld();
@@ -281,6 +326,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     for (int i = 0; i < 16; ++i)
       pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + (bias ? bias[2 * i] : 0.f), 0.f),
                           fmaxf(__uint_as_float(r[2 * i + 1]) + (bias ? bias[2 * i + 1] : 0.f), 0.f));
+    if (mword) *mword = relu_mask16(pk);
     st_row32(atile, row, acol, pk);
   };
 
@@ -378,11 +424,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         }
       }
       tmem_st32(lane_base + H + col, r);
-      if (!SPLIT || half == 0) {
+      if (!SPLIT || half == 0) {  // (split: half 1 stages its columns after the first K-half MMA)
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
           pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
+        reinterpret_cast<uint32_t*>(row_m1[row])[col >> 5] = relu_mask16(pk);
         st_row32(atile, row, col, pk);
       }
     }
@@ -394,6 +441,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       pending = false;
     }
     publish();
+    // emission slot of this row (identical in both threads of the row): ballots of the
+    // four row quarters give the CTA-wide prefix without another barrier
+    bool my_valid = false;
+    int gslot = 0;
+    bool crossed = false;
+    int claim = 0;
+    {
+      int before = 0, n = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rb = row_b[q * 32 + lane];
+        const bool v = rb >= 0 && rb < a.Bl;
+        const uint32_t m = __ballot_sync(0xffffffffu, v);
+        n += __popc(m);
+        if (q < quarter) before += __popc(m);
+        if (q == quarter) {
+          before += __popc(m & ((1u << lane) - 1u));
+          my_valid = v;
+        }
+      }
+      const int nxt = s_next;
+      const int p = fill + before;
+      gslot = (p < kTile ? cur : nxt) * kTile + (p & (kTile - 1));
+      fill += n;
+      if (fill >= kTile) {
+        fill -= kTile;
+        cur = nxt;
+        crossed = true;
+      }
+      // the next tile is claimed now; s_next is rewritten in this round's sample phase,
+      // after every thread has read it above
+      if (crossed && tid == kThreads - 1) claim = atomicAdd(a.tilectr, 1);
+    }
+    // copy the 64 staged columns [half*64, half*64+64) of the A tile (logical columns
+    // col0 + ...) of this warp's 32 rows into their emission tile images + ReLU masks,
+    // overlapping the MMA. Eight lanes move one row's 128-byte line, so each store
+    // instruction writes four whole lines.
+    auto emit = [&](__nv_bfloat16* img, int col0) {
+      if (a.emit_mode == 1) return;
+      const int j = lane & 7;  // physical 16-byte chunk of the staged row
+#pragma unroll 4
+      for (int i = 0; i < 8; ++i) {
+        const int rl = 4 * i + (lane >> 3);
+        const int srow = quarter * 32 + rl;
+        const int gs = __shfl_sync(0xffffffffu, my_valid ? gslot : -1, rl);
+        const uint4 x = *reinterpret_cast<const uint4*>(atile + half * (kTile * 128) + srow * 128 + j * 16);
+        if (gs >= 0) {
+          const int prow = gs & (kTile - 1);
+          uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 +
+                         ((col0 >> 6) + half) * (kTile * 128) + prow * 128;
+          *reinterpret_cast<uint4*>(dst + (((j ^ (srow & 7)) ^ (prow & 7)) * 16)) = x;
+        }
+      }
+    };
     mark(1);
     // (2) hidden layer on the tensor cores: acc[128 x H] = relu(h1) W2^T (split-K for H=256)
     mma_round([&] { mma_kk<H, AK>(tmem, atile, w2img, false); });
@@ -401,30 +502,37 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       const int rb = row_b[row];
       row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
     }
+    emit(a.h1, 0);
     mma_join();
     if (SPLIT) {
       if (half == 1)
 #pragma unroll 1
-        for (int q = 0; q < HC / 32; ++q) stage32(H + c0 + q * 32, q * 32, nullptr);
+        for (int q = 0; q < HC / 32; ++q)
+          stage32(H + c0 + q * 32, q * 32, nullptr, reinterpret_cast<uint32_t*>(row_m1[row]) + ((c0 >> 5) + q));
       publish();
       mma_round([&] { mma_kk<H, AK>(tmem, atile, w2img + (AK / 64) * (H * 128), true); });
+      emit(a.h1, AK);
       mma_join();
     }
     mark(2);
     // (3) h2 = ReLU(acc + b2) -> staged bf16 tile, (4) head on the tensor cores
     if (!SPLIT || half == 0)
 #pragma unroll 1
-      for (int q = 0; q < HC / 32; ++q) stage32(c0 + q * 32, c0 + q * 32, b2s + c0 + q * 32);
+      for (int q = 0; q < HC / 32; ++q)
+        stage32(c0 + q * 32, c0 + q * 32, b2s + c0 + q * 32, reinterpret_cast<uint32_t*>(row_m2[row]) + ((c0 >> 5) + q));
     publish();
     mark(3);
     mma_round([&] { mma_kk<NH, AK>(tmem, atile, whimg, false); });
+    emit(a.h2, 0);
     mma_join();
     if (SPLIT) {  // head output sits in acc columns [0, NH): half 1 reads [HC, H)
       if (half == 1)
 #pragma unroll 1
-        for (int q = 0; q < HC / 32; ++q) stage32(c0 + q * 32, q * 32, b2s + c0 + q * 32);
+        for (int q = 0; q < HC / 32; ++q)
+          stage32(c0 + q * 32, q * 32, b2s + c0 + q * 32, reinterpret_cast<uint32_t*>(row_m2[row]) + ((c0 >> 5) + q));
       publish();
       mma_round([&] { mma_kk<NH, AK>(tmem, atile, whimg + (AK / 64) * (NH * 128), true); });
+      emit(a.h2, AK);
       mma_join();
     }
     mark(4);
@@ -442,11 +550,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     tc_fence_before();
     const long long ts0 = a.phase ? clock64() : 0;
     if (half == 0 && active) {
-      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], inv_legal, &bad);
+      float ex[NH], hi, z, rz;
+      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], inv_legal, &bad, ex, hi, z, rz);
       if (act < 0) {
         active = false;
+        a.frow_bt[gslot] = -1;
       } else {
         const size_t bt = (size_t)b * T + tstep;
+        {  // training-forward row record: masked log-softmax statistics (tape.cpp:177-213)
+          const float lse = hi + __logf(z);
+          float la = 0.f, ls = 0.f, fl = 0.f;
+#pragma unroll
+          for (int c = 0; c < NH; ++c) {
+            if (c == act) la = logit[c];
+            if (c == P.stop) ls = logit[c];
+            if (c == A) fl = logit[c];
+          }
+          la -= lse;
+          ls = P.stop >= 0 ? ls - lse : 0.f;
+          fl = a.flow ? fl : 0.f;
+          // record [probs (A) | lpa | lps | flow | pad] as 16-byte stores (rs % 4 == 0)
+          float4* out = reinterpret_cast<float4*>(a.rowbuf + (size_t)gslot * a.rs);
+#pragma unroll
+          for (int k = 0; k < NH + 4; k += 4) {
+            if (k < a.rs) {
+              float q[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int c = k + e;
+                q[e] = c < A ? (c < NH ? ex[c < NH ? c : 0] * rz : 0.f)
+                             : c == A ? la : c == A + 1 ? ls : c == A + 2 ? fl : 0.f;
+              }
+              out[k >> 2] = make_float4(q[0], q[1], q[2], q[3]);
+            }
+          }
+          a.frow_bt[gslot] = (int32_t)bt;
+          a.bt_row[bt] = gslot;
+        }
         Env::pack(P, s, a.stst + bt * P.SW);
         int n = 0;
         Env::delta_features(P, s, act, [&](int f, float v) {
@@ -480,12 +620,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         row_t[row] = tstep;
       }
     }
+    if (crossed && tid == kThreads - 1) s_next = claim;
+    if (half == 1 && my_valid && a.emit_mode != 1) {  // ReLU masks of the row (idle half)
+      uint4* m1 = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
+      uint4* m2 = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
+#pragma unroll
+      for (int k = 0; k < H / 128; ++k) {
+        m1[k] = row_m1[row][k];
+        m2[k] = row_m2[row][k];
+      }
+    }
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
     mark(5);
   }
   if (a.phase && tid == 0)
     for (int k = 0; k < 9; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)ph[k]);
   if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
+  {  // unused emission rows: rows [fill, 128) of `cur` and the whole pre-claimed tile
+    const int nxt = s_next;
+    const int slot = tid < kTile ? cur * kTile + tid : nxt * kTile + (tid - kTile);
+    if (tid >= fill) {
+      a.frow_bt[slot] = -1;
+      const int prow = slot & (kTile - 1);
+#pragma unroll
+      for (int blk = 0; blk < H / 64; ++blk) {
+        const size_t off = (size_t)(slot >> 7) * kTile * H * 2 + blk * (kTile * 128) + prow * 128;
+        uint4* d1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.h1) + off);
+        uint4* d2 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.h2) + off);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d1[j] = make_uint4(0, 0, 0, 0);
+          d2[j] = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+  }
   __syncthreads();
   if (warp == 0) tmem_dealloc<2 * H>(tmem);
 }
@@ -499,6 +668,8 @@ struct TrainArgs {
   DeviceBatch batch;
   int Bl;
   const uint32_t* stst;
+  const int32_t* frow_bt;   // row slot -> b * T + t, -1 = empty slot
+  const int32_t* tilectr;   // number of 128-row tiles of row slots
   __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
   uint32_t *mask1, *mask2;  // ReLU masks of h1 / h2, [rows][H/32]
   float* rowbuf;
@@ -539,8 +710,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, c0 = half * HC;
   const int A = P.A;
-  const int R = a.batch.counters[0];
-  const int tiles = (R + kTile - 1) / kTile;
+  const int tiles = *a.tilectr;
+  const int R = tiles * kTile;
   if ((int)blockIdx.x >= tiles) return;
   if (warp == 0) tmem_alloc<H>(&tbase);
   if (tid == 0) {
@@ -591,8 +762,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
     act = 0;
 #pragma unroll
     for (int i = 0; i < kMaxSWFwd; ++i) w[i] = 0;
-    if (r < R && tile < tiles) {
-      const size_t bt = (size_t)a.batch.row_bt[r];
+    if (r < R && tile < tiles && a.frow_bt[r] >= 0) {
+      const size_t bt = (size_t)a.frow_bt[r];
 #pragma unroll
       for (int i = 0; i < kMaxSWFwd; ++i)
         if (i < P.SW) w[i] = a.stst[bt * P.SW + i];
@@ -604,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
   fetch(blockIdx.x, wn, actn);
   for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
     const int r = tile * kTile + row;
-    const bool valid = r < R;
+    const bool valid = r < R && a.frow_bt[r] >= 0;
     uint32_t wc[kMaxSWFwd];
 #pragma unroll
     for (int i = 0; i < kMaxSWFwd; ++i) wc[i] = wn[i];
@@ -654,13 +825,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
             }
           }
       }
-      uint32_t pk[16], mb = 0;
+      uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        pk[i] = valid ? pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f)) : 0u;
-        mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
-        mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
-      }
+      for (int i = 0; i < 16; ++i) pk[i] = valid ? pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f)) : 0u;
+      const uint32_t mb = relu_mask16(pk);
       if (valid) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
       if (!SPLIT || half == 0) {
         st_row32(atile, row, col, pk);
@@ -708,15 +876,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
       uint32_t r32[32];
       tmem_ld32(lane_base + col, r32);
       tmem_wait_ld();
-      uint32_t pk[16], mb = 0;
+      uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const float x0 = fmaxf(__uint_as_float(r32[2 * i]) + b2s[col + 2 * i], 0.f);
         const float x1 = fmaxf(__uint_as_float(r32[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f);
         pk[i] = valid ? pack_bf16x2(x0, x1) : 0u;
-        mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
-        mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
       }
+      const uint32_t mb = relu_mask16(pk);
       if (valid) a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
       st_row32(atile, row, acol, pk);
     };
@@ -801,6 +968,7 @@ struct LossArgs {
   const double* neglog;
   const float* rowbuf;
   int rs;
+  const int32_t* bt_row;  // b * T + t -> row slot
   float* coef;
   double* lpart;
   const double* scalars;
@@ -811,17 +979,17 @@ __global__ void k_fast_loss(LossArgs a) {
   double loss = 0.0, dlogz = 0.0;
   if (b < a.Bl) {
     const int L = a.batch.lengths[b];
-    const int r0 = a.batch.row0[b];
+    const int32_t* rows = a.bt_row + (size_t)b * a.T;
     const uint16_t* np = a.batch.nparents + (size_t)b * a.T;
     const double logr = a.batch.log_rewards[b];
     const int* cnt = a.batch.counters;
     double norm = (double)a.B_global;
     if (a.objective == GFNX_OBJ_DB) norm = (double)cnt[4];
     if (a.objective == GFNX_OBJ_MDB) norm = (double)cnt[5];
-    auto lpa = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A]; };
-    auto lps = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A + 1]; };
-    auto flw = [&](int t) { return (double)a.rowbuf[(size_t)(r0 + t) * a.rs + a.A + 2]; };
-    auto C = [&](int t) { return a.coef + (size_t)(r0 + t) * 4; };
+    auto lpa = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A]; };
+    auto lps = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A + 1]; };
+    auto flw = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A + 2]; };
+    auto C = [&](int t) { return a.coef + (size_t)rows[t] * 4; };
     for (int t = 0; t < L; ++t) {
       float* c = C(t);
       c[0] = c[1] = c[2] = 0.f;
@@ -948,8 +1116,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   const int quarter = warp & 3, half = warp >> 2;
   const int row = quarter * 32 + lane, c0 = half * HC;
   const int A = P.A;
-  const int R = a.batch.counters[0];
-  const int tiles = (R + kTile - 1) / kTile;
+  const int tiles = *a.tilectr;
+  const int R = tiles * kTile;
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
   float acc_b1 = 0.f, acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j
   if ((int)blockIdx.x < tiles) {
@@ -973,7 +1141,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int r = tile * kTile + row;
-      const bool valid = r < R;
+      const int rbt = r < R ? a.frow_bt[r] : -1;
+      const bool valid = rbt >= 0;
       if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
       __syncthreads();
       uint32_t mk2[HC / 32], mk1[HC / 32];
@@ -989,7 +1158,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         int act = 0;
         float g_a = 0.f, g_s = 0.f, g_f = 0.f;
         if (valid) {
-          const size_t bt = (size_t)a.batch.row_bt[r];
+          const size_t bt = (size_t)rbt;
           Env::unpack(P, a.stst + bt * P.SW, s);
           act = a.batch.actions[bt];
           g_a = a.coef[(size_t)r * 4 + 0];
@@ -1053,8 +1222,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(((mk2[q] >> (2 * i)) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
-                              ((mk2[q] >> (2 * i + 1)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
+          pk[i] = pack_bf16x2(((mk2[q] >> i) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
+                              ((mk2[q] >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
       }
       fence_proxy_async();
@@ -1088,8 +1257,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(((mk1[q] >> (2 * i)) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
-                              ((mk1[q] >> (2 * i + 1)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
+          pk[i] = pack_bf16x2(((mk1[q] >> i) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
+                              ((mk1[q] >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
       }
       tc_fence_before();
@@ -1138,9 +1307,9 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   uint32_t* tbase = (uint32_t*)(mbar + 2);
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5;
-  const int T = P.T, A = P.A;
-  const int R = a.batch.counters[0];
-  const int tiles = (R + kTile - 1) / kTile;
+  const int A = P.A;
+  const int tiles = *a.tilectr;
+  const int R = tiles * kTile;
   const int per = (tiles + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
@@ -1204,9 +1373,9 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
 #pragma unroll
       for (int c = 0; c < 16; ++c)
         *reinterpret_cast<uint4*>(bufA + sw128_offset(tid, 8 * c, kTile)) = make_uint4(z4[0], z4[1], z4[2], z4[3]);
-      if (r < R) {
+      if (r < R && a.frow_bt[r] >= 0) {
         typename Env::State s;
-        Env::unpack(P, a.stst + (size_t)a.batch.row_bt[r] * P.SW, s);
+        Env::unpack(P, a.stst + (size_t)a.frow_bt[r] * P.SW, s);
         Env::features(P, s, [&](int f, double x) {
           *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, f, kTile)) = __float2bfloat16((float)x);
         });
@@ -1393,7 +1562,19 @@ struct Kernels {
     a.stst = f.stst;
     a.work = f.work;
     a.phase = c.phase;
+    a.h1 = f.h1;
+    a.h2 = f.h2;
+    a.mask1 = f.mask1;
+    a.mask2 = f.mask2;
+    a.rowbuf = f.rowbuf;
+    a.rs = f.rs;
+    a.flow = c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB;
+    a.frow_bt = f.frow_bt;
+    a.bt_row = f.bt_row;
+    a.tilectr = f.tilectr;
+    a.emit_mode = getenv("GFNX_EMIT_MODE") ? atoi(getenv("GFNX_EMIT_MODE")) : 0;
     const int T = c.P.T;
+    cudaMemsetAsync(f.tilectr, 0, sizeof(int32_t), c.stream);
     cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.nparents, 0, sizeof(uint16_t) * (size_t)c.Bl * T, c.stream);
     if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
@@ -1415,6 +1596,7 @@ struct Kernels {
       k_fast_rollout<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(a);
     }
     c.launches++;
+    f.fused = true;
   }
   static void train(Ctx& c, bool apply, double lr) {
     FastState& f = FS(c);
@@ -1424,6 +1606,8 @@ struct Kernels {
     ta.batch = c.batch;
     ta.Bl = c.Bl;
     ta.stst = f.stst;
+    ta.frow_bt = f.frow_bt;
+    ta.tilectr = f.tilectr;
     ta.h1 = f.h1;
     ta.h2 = f.h2;
     ta.dz1 = f.dz1;
@@ -1439,7 +1623,10 @@ struct Kernels {
     ta.L = c.L;
     ta.objective = c.train.objective;
     const int grid = f.num_sms;
-    {
+    if (!f.fused) {  // weights changed since the rollout: recompute the forward over the rows
+      k_linear_rows<<<(std::max(c.Bl, kTile) + 255) / 256, 256, 0, c.stream>>>(
+          c.batch.lengths, c.batch.row0, c.Bl, c.P.T, c.batch.counters, f.frow_bt, f.bt_row, f.tilectr);
+      c.launches++;
       const int fixed = fwd_smem_fixed<H, NH>();
       const int w1b = c.P.O * H * 2;
       cudaFuncAttributes fa{};
@@ -1454,6 +1641,7 @@ struct Kernels {
         set_smem_once(k_fast_fwd<Env, H, NH, false>, fixed);
         k_fast_fwd<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(ta);
       }
+      c.launches++;
     }
     LossArgs la{};
     la.batch = c.batch;
@@ -1468,6 +1656,7 @@ struct Kernels {
     la.neglog = c.d_neglog;
     la.rowbuf = f.rowbuf;
     la.rs = f.rs;
+    la.bt_row = f.bt_row;
     la.coef = f.coef;
     la.lpart = f.lpart;
     la.scalars = c.d_scalars;
@@ -1494,7 +1683,7 @@ struct Kernels {
       ProfScope ps(c, "k_reduce");
       k_reduce<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(f.wpart, grid, n, c.g32);
     }
-    c.launches += 6;
+    c.launches += 5;
     (void)apply;
     (void)lr;
   }
@@ -1554,8 +1743,10 @@ void fast_init(Ctx& c) {
   f->O = c.shape.obs_dim;
   const int T = c.P.T;
   f->max_rows = (int64_t)c.Bl * T;
-  f->max_tiles = (f->max_rows + kTile - 1) / kTile;
-  f->rs = f->A + 4;
+  // + 2 tiles per rollout CTA: partially filled / pre-claimed emission tiles
+  f->max_tiles = (f->max_rows + kTile - 1) / kTile + 2 * f->num_sms;
+  const int64_t slots = f->max_tiles * kTile;
+  f->rs = (f->A + 3 + 3) & ~3;  // probs[A], lpa, lps, flow, padded to 16 bytes
   f->loss_blocks = (c.Bl + 255) / 256;
   const size_t img = (size_t)f->max_tiles * kTile * H * 2;
   cuda_check(cudaMalloc(&f->w1, sizeof(__nv_bfloat16) * (size_t)f->O * H), "fast w1");
@@ -1572,10 +1763,14 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->dz1, img), "fast dz1");
   cuda_check(cudaMalloc(&f->dz2, img), "fast dz2");
   cuda_check(cudaMalloc(&f->dhead, (size_t)f->max_tiles * kTile * 64 * 2), "fast dhead");
-  cuda_check(cudaMalloc(&f->mask1, sizeof(uint32_t) * (size_t)f->max_rows * (H / 32)), "fast masks");
-  cuda_check(cudaMalloc(&f->mask2, sizeof(uint32_t) * (size_t)f->max_rows * (H / 32)), "fast masks");
-  cuda_check(cudaMalloc(&f->rowbuf, sizeof(float) * (size_t)(f->max_tiles * kTile) * f->rs), "fast rowbuf");
-  cuda_check(cudaMalloc(&f->coef, sizeof(float) * (size_t)f->max_rows * 4), "fast coef");
+  cuda_check(cudaMalloc(&f->mask1, sizeof(uint32_t) * (size_t)slots * (H / 32)), "fast masks");
+  cuda_check(cudaMalloc(&f->mask2, sizeof(uint32_t) * (size_t)slots * (H / 32)), "fast masks");
+  cuda_check(cudaMalloc(&f->rowbuf, sizeof(float) * (size_t)slots * f->rs), "fast rowbuf");
+  cuda_check(cudaMalloc(&f->coef, sizeof(float) * (size_t)slots * 4), "fast coef");
+  cuda_check(cudaMalloc(&f->frow_bt, sizeof(int32_t) * (size_t)slots), "fast rows");
+  cuda_check(cudaMalloc(&f->bt_row, sizeof(int32_t) * (size_t)f->max_rows), "fast rows");
+  cuda_check(cudaMalloc(&f->tilectr, sizeof(int32_t)), "fast rows");
+  cuda_check(cudaMemset(f->tilectr, 0, sizeof(int32_t)), "fast rows");
   cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
   cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
   cuda_check(cudaMalloc(&f->lpart, sizeof(double) * 2 * f->loss_blocks), "fast lpart");
@@ -1596,7 +1791,8 @@ void fast_free(Ctx& c) {
   if (!f) return;
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
                   f->mask1, f->mask2,
-                  f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work};
+                  f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work,
+                  f->frow_bt, f->bt_row, f->tilectr};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete f;
@@ -1608,6 +1804,7 @@ void fast_sync_weights(Ctx& c) {
     ls_sync_weights(c);
     return;
   }
+  FS(c).fused = false;
   AdamArgs a = adam_args(c);
   k_emit_images<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a);
   c.launches++;
@@ -1636,7 +1833,10 @@ void fast_adam(Ctx& c, double lr) {
   c.adam_t += 1;
   const bool bitseq = lockstep(c);
   AdamArgs a{};
-  if (!bitseq) a = adam_args(c);
+  if (!bitseq) {
+    a = adam_args(c);
+    FS(c).fused = false;
+  }
   a.p = c.p32;
   a.m = c.m32;
   a.v = c.v32;

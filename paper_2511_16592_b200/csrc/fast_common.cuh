@@ -42,6 +42,15 @@ GFNX_DEV void mma_mn(uint32_t d_tmem, const void* a_img, int m0, const void* b_i
   }
 }
 
+// ReLU mask of 32 consecutive bf16 columns packed as 16 bf16x2 words (values >= 0 or -0):
+// bit i <-> column 2i, bit 16 + i <-> column 2i + 1 (set when the value is nonzero).
+GFNX_DEV uint32_t relu_mask16(const uint32_t (&pk)[16]) {
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) m |= ((((pk[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu) >> 15) & 0x00010001u) << i;
+  return m;
+}
+
 // store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
 GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
 #pragma unroll

@@ -83,6 +83,28 @@ def test_fast_loss_and_grads_match_oracle_on_same_batch(name, kw):
     d.close()
 
 
+@pytest.mark.parametrize("name,kw", CASES)
+def test_fused_rollout_forward_matches_recomputed_forward(name, kw):
+    """The rollout emits every sampled row's activations (fused training forward). After
+    set_params the same batch is re-scored by the separate training-forward kernel; both
+    must give the same loss and gradient up to fp32 summation order in layer 1."""
+    e, t = _pair(name, **kw)
+    d = engine.Trainer(e, t)
+    o = O.Oracle(e, t)
+    p, z = o.params()
+    d.set_params(p, z)
+    d.forward_rollout(1, o.schedule("explore", 1))
+    l_fused = d.compute_grads()
+    g_fused, dz_fused = d.grads()
+    d.set_params(p, z)  # same weights: invalidates the rollout's activations
+    l_re = d.compute_grads()
+    g_re, dz_re = d.grads()
+    assert abs(l_fused - l_re) <= 1e-3 * abs(l_re) + 1e-6, (l_fused, l_re)
+    err, cos = _grad_close(g_fused, g_re)
+    assert err < 3e-2 and cos > 0.9995, (err, cos)
+    d.close()
+
+
 def test_fast_iteration_tracks_oracle_step():
     e, t = _pair("hypergrid_tb_b16")
     d = engine.Trainer(e, t)
