@@ -60,10 +60,76 @@ struct FastState {
   int32_t* frow_bt = nullptr;         // [max_tiles*128] row slot -> b*T + t (-1 = empty)
   int32_t* bt_row = nullptr;          // [Bl*T] b*T + t -> row slot
   int32_t* tilectr = nullptr;         // number of 128-row tiles of row slots
+  float* logits = nullptr;            // [slots][NH] rollout head outputs (fused forward)
   bool fused = false;                 // row slots hold the rollout's forward for the current weights
   int rs = 0;                         // rowbuf stride (floats)
   int loss_blocks = 0;
 };
+
+// training-forward record of every emitted row from the rollout's raw head outputs:
+// masked log-softmax (tape.cpp:177-213) -> probs[A], log pi(a|s), log pi(stop|s), flow
+template <class Env, int NH>
+__global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, const int16_t* __restrict__ actions,
+                            const int32_t* __restrict__ frow_bt, const int32_t* __restrict__ tilectr,
+                            const float* __restrict__ logits, float* __restrict__ rowbuf, int rs, int flow,
+                            int32_t* err) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= *tilectr * kTile) return;
+  const int bt = frow_bt[r];
+  if (bt < 0) return;
+  typename Env::State s;
+  Env::unpack(P, stst + (size_t)bt * P.SW, s);
+  const int act = actions[bt];
+  float lg[NH];
+  const float4* src = reinterpret_cast<const float4*>(logits + (size_t)r * NH);
+#pragma unroll
+  for (int k = 0; k < NH / 4; ++k) {
+    const float4 v = src[k];
+    lg[4 * k] = v.x;
+    lg[4 * k + 1] = v.y;
+    lg[4 * k + 2] = v.z;
+    lg[4 * k + 3] = v.w;
+  }
+  const int A = P.A;
+  uint32_t lm = 0;
+  float hi = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < NH; ++c)
+    if (c < A && Env::legal(P, s, c)) {
+      lm |= 1u << c;
+      hi = fmaxf(hi, lg[c]);
+    }
+  float e[NH], z = 0.f;
+#pragma unroll
+  for (int c = 0; c < NH; ++c) {
+    e[c] = ((lm >> c) & 1u) ? __expf(lg[c] - hi) : 0.f;
+    z += e[c];
+  }
+  const float lse = hi + __logf(z), rz = __frcp_rn(z);
+  float la = 0.f, ls = 0.f, fl = 0.f;
+#pragma unroll
+  for (int c = 0; c < NH; ++c) {
+    if (c == act) la = lg[c];
+    if (c == P.stop) ls = lg[c];
+    if (c == A) fl = lg[c];
+  }
+  la -= lse;
+  ls = P.stop >= 0 ? ls - lse : 0.f;
+  fl = flow ? fl : 0.f;
+  if (!isfinite(lse)) atomicExch(err, GFNX_ERR_NUMERIC);
+  float4* out = reinterpret_cast<float4*>(rowbuf + (size_t)r * rs);
+#pragma unroll
+  for (int k = 0; k < NH + 4; k += 4)
+    if (k < rs) {
+      float q[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = k + j;
+        q[j] = c < A ? (c < NH ? e[c < NH ? c : 0] * rz : 0.f) : c == A ? la : c == A + 1 ? ls : c == A + 2 ? fl : 0.f;
+      }
+      out[k >> 2] = make_float4(q[0], q[1], q[2], q[3]);
+    }
+}
 
 // row slots in trajectory order (row0[b] + t) when the training forward is recomputed
 __global__ void k_linear_rows(const int32_t* __restrict__ lengths, const int32_t* __restrict__ row0, int Bl,
@@ -203,6 +269,7 @@ struct RolloutArgs {
   float* rowbuf;
   int rs, flow;
   int32_t *frow_bt, *bt_row, *tilectr;
+  float* logits;  // [slot][NH] head outputs (logits, flow at column A), bias included
   int emit_mode;  // diagnostics (GFNX_EMIT_MODE): 0 full, 1 no row emission, 2 no masks, 3 no images
 };
 
@@ -557,33 +624,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         a.frow_bt[gslot] = -1;
       } else {
         const size_t bt = (size_t)b * T + tstep;
-        {  // training-forward row record: masked log-softmax statistics (tape.cpp:177-213)
-          const float lse = hi + __logf(z);
-          float la = 0.f, ls = 0.f, fl = 0.f;
-#pragma unroll
-          for (int c = 0; c < NH; ++c) {
-            if (c == act) la = logit[c];
-            if (c == P.stop) ls = logit[c];
-            if (c == A) fl = logit[c];
-          }
-          la -= lse;
-          ls = P.stop >= 0 ? ls - lse : 0.f;
-          fl = a.flow ? fl : 0.f;
-          // record [probs (A) | lpa | lps | flow | pad] as 16-byte stores (rs % 4 == 0)
-          float4* out = reinterpret_cast<float4*>(a.rowbuf + (size_t)gslot * a.rs);
-#pragma unroll
-          for (int k = 0; k < NH + 4; k += 4) {
-            if (k < a.rs) {
-              float q[4];
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int c = k + e;
-                q[e] = c < A ? (c < NH ? ex[c < NH ? c : 0] * rz : 0.f)
-                             : c == A ? la : c == A + 1 ? ls : c == A + 2 ? fl : 0.f;
-              }
-              out[k >> 2] = make_float4(q[0], q[1], q[2], q[3]);
-            }
-          }
+        {
           a.frow_bt[gslot] = (int32_t)bt;
           a.bt_row[bt] = gslot;
         }
@@ -621,7 +662,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
-    if (half == 1 && my_valid && a.emit_mode != 1) {  // ReLU masks of the row (idle half)
+    if (half == 1 && my_valid && a.emit_mode != 1) {  // raw logits + ReLU masks of the row (idle half)
+      float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
+#pragma unroll
+      for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
       uint4* m1 = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
       uint4* m2 = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
 #pragma unroll
@@ -1097,7 +1141,7 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 
 template <int H, int NH>
 constexpr int bwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + 1024;
+  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + 8192 + 1024;
 }
 
 template <class Env, int H, int NH>
@@ -1108,6 +1152,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   uint8_t* atile = wdimg + H * H * 2;        // dz tile
   uint8_t* htile = atile + kTile * H * 2;    // dhead tile [128][64]
   uint8_t* whd = htile + kTile * 64 * 2;     // head dgrad image [H][NH], non-swizzled
+  float* red = reinterpret_cast<float*>(whd + H * NH * 2);  // [kThreads * 8 / H][H] bias partials
   constexpr int HC = H / 2;
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
@@ -1119,7 +1164,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   const int tiles = *a.tilectr;
   const int R = tiles * kTile;
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
-  float acc_b1 = 0.f, acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j
+  float acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j (db1: k_fast_wgrad pass B)
   if ((int)blockIdx.x < tiles) {
     if (warp == 0) tmem_alloc<H>(&tbase);
     if (tid == 0) {
@@ -1167,32 +1212,30 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         }
         const float gsum = g_a + g_s;
         const float* pr = a.rowbuf + (size_t)r * a.rs;
-        uint32_t pk[32];
+        // only the NH head columns are written: the head dgrad MMA reads K = NH, and the
+        // wgrad pass C output columns >= NH (from stale smem) are never read back
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          float x[2];
+        for (int c8 = 0; c8 < NH / 8; ++c8) {
+          uint32_t pk[4];
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int c = 2 * i + e;
-            float v = 0.f;
-            if (valid && c < A && Env::legal(P, s, c)) {
-              v = -pr[c] * gsum;
-              if (c == act) v += g_a;
-              if (c == P.stop) v += g_s;
+          for (int i = 0; i < 4; ++i) {
+            float x[2];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int c = 8 * c8 + 2 * i + e;
+              float v = 0.f;
+              if (valid && c < A && Env::legal(P, s, c)) {
+                v = -pr[c] * gsum;
+                if (c == act) v += g_a;
+                if (c == P.stop) v += g_s;
+              }
+              if (c == A) v = g_f;
+              x[e] = v;
             }
-            if (c == A) v = g_f;
-            x[e] = v;
+            pk[i] = pack_bf16x2(x[0], x[1]);
           }
-          pk[i] = pack_bf16x2(x[0], x[1]);
+          *reinterpret_cast<uint4*>(htile + sw128_offset(row, 8 * c8, kTile)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          lo[i] = pk[i];
-          hi[i] = pk[16 + i];
-        }
-        st_row32(htile, row, 0, lo);
-        st_row32(htile, row, 32, hi);
       }
       fence_proxy_async();
       tc_fence_before();
@@ -1204,11 +1247,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         mma_k_sw128_none<H, NH>(tmem, htile, whd);
         umma_commit(&mbar);
       }
-      if (tid <= A) {  // head bias sums (fixed row order)
-        float sacc = 0.f;
+      if (tid <= A) {  // head bias sums (fixed row order, four interleaved partial sums)
+        float s4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 8
         for (int rr = 0; rr < kTile; ++rr)
-          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
-        acc_bh += sacc;
+          s4[rr & 3] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
+        acc_bh += (s4[0] + s4[1]) + (s4[2] + s4[3]);
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
@@ -1236,12 +1280,31 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
         umma_commit(&mbar);
       }
-      // bias sums of this tile in fixed row order (deterministic); overlaps the MMA
-      if (tid < H) {
-        float sacc = 0.f;
-        for (int rr = 0; rr < kTile; ++rr)
-          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(rr, tid, kTile)));
-        acc_b2 += sacc;
+      // db2 of this tile (deterministic, overlaps the MMA): thread = (row group, 8 columns)
+      // sums its rows with 16-byte loads, then a fixed-order sum over the row groups
+      {
+        constexpr int CG = H / 8, RG = kThreads / CG, RPG = kTile / RG;
+        const int cg = tid % CG, rg = tid / CG;
+        float sv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+        for (int i = 0; i < RPG; ++i) {
+          const uint4 q = *reinterpret_cast<const uint4*>(atile + sw128_offset(rg * RPG + i, 8 * cg, kTile));
+          const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            sv[2 * e] += bf16_lo(w[e]);
+            sv[2 * e + 1] += bf16_hi(w[e]);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) red[rg * H + 8 * cg + e] = sv[e];
+        __syncthreads();
+        if (tid < H) {
+          float t = 0.f;
+#pragma unroll
+          for (int g = 0; g < RG; ++g) t += red[g * H + tid];
+          acc_b2 += t;
+        }
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
@@ -1268,22 +1331,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         bulk_s2g(a.dz1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
         bulk_commit();
       }
-      if (tid < H) {
-        float sacc = 0.f;
-        for (int rr = 0; rr < kTile; ++rr)
-          sacc += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(atile + sw128_offset(rr, tid, kTile)));
-        acc_b1 += sacc;
-      }
     }
     if (tid == 0) bulk_wait0();
     __syncthreads();
     if (warp == 0) tmem_dealloc<H>(tmem);
   }
   // bias partials of this CTA (every CTA writes its slots, zeros when it had no tile)
-  if (tid < H) {
-    part[a.L.off_b[0] + tid] = acc_b1;
-    part[a.L.off_b[1] + tid] = acc_b2;
-  }
+  if (tid < H) part[a.L.off_b[1] + tid] = acc_b2;
   if (tid < A) part[a.L.off_fb + tid] = acc_bh;
   if (tid == A) part[a.L.off_flb] = acc_bh;
 }
@@ -1379,6 +1433,8 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
         Env::features(P, s, [&](int f, double x) {
           *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, f, kTile)) = __float2bfloat16((float)x);
         });
+        // constant feature O: its output row is db1 = sum_r dz1[r]
+        *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, P.O, kTile)) = __float2bfloat16(1.f);
       }
     }
     fence_proxy_async();
@@ -1399,8 +1455,8 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
     uint32_t r32[32];
     tmem_ld32(lane_base + q * 32, r32);
     tmem_wait_ld();
-    if (tid < P.O) {
-      float* dst = part + L.off_w[0] + (size_t)tid * H + q * 32;
+    if (tid <= P.O) {
+      float* dst = tid < P.O ? part + L.off_w[0] + (size_t)tid * H + q * 32 : part + L.off_b[0] + q * 32;
 #pragma unroll
       for (int i = 0; i < 32; ++i) dst[i] = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
     }
@@ -1572,6 +1628,7 @@ struct Kernels {
     a.frow_bt = f.frow_bt;
     a.bt_row = f.bt_row;
     a.tilectr = f.tilectr;
+    a.logits = f.logits;
     a.emit_mode = getenv("GFNX_EMIT_MODE") ? atoi(getenv("GFNX_EMIT_MODE")) : 0;
     const int T = c.P.T;
     cudaMemsetAsync(f.tilectr, 0, sizeof(int32_t), c.stream);
@@ -1642,6 +1699,13 @@ struct Kernels {
         k_fast_fwd<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(ta);
       }
       c.launches++;
+    } else {
+      ProfScope ps(c, "k_row_stats");
+      const int nslots = (int)(f.max_tiles * kTile);
+      k_row_stats<Env, NH><<<(nslots + 255) / 256, 256, 0, c.stream>>>(
+          c.P, f.stst, c.batch.actions, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
+          c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3);
+      c.launches++;
     }
     LossArgs la{};
     la.batch = c.batch;
@@ -1697,7 +1761,7 @@ bool supported(const Ctx& c, int* H) {
   if (c.L.dims[1] != c.L.dims[2]) return false;
   if (*H != 256 && *H != 128) return false;
   if (c.shape.num_actions + 1 > (c.env.kind == GFNX_ENV_HYPERGRID ? 16 : 32)) return false;
-  if (c.shape.obs_dim > 128) return false;
+  if (c.shape.obs_dim >= 128) return false;  // feature obs_dim carries db1 in the wgrad GEMM
   if (c.shape.max_traj_len > 128) return false;
   if (c.env.kind == GFNX_ENV_DAG) return *H == 128;
   return c.env.kind == GFNX_ENV_HYPERGRID;
@@ -1770,6 +1834,7 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->frow_bt, sizeof(int32_t) * (size_t)slots), "fast rows");
   cuda_check(cudaMalloc(&f->bt_row, sizeof(int32_t) * (size_t)f->max_rows), "fast rows");
   cuda_check(cudaMalloc(&f->tilectr, sizeof(int32_t)), "fast rows");
+  cuda_check(cudaMalloc(&f->logits, sizeof(float) * (size_t)slots * f->NH), "fast logits");
   cuda_check(cudaMemset(f->tilectr, 0, sizeof(int32_t)), "fast rows");
   cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
   cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
@@ -1792,7 +1857,7 @@ void fast_free(Ctx& c) {
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
                   f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work,
-                  f->frow_bt, f->bt_row, f->tilectr};
+                  f->frow_bt, f->bt_row, f->tilectr, f->logits};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete f;
