@@ -176,23 +176,30 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def kernel_work(name, rows, iters, H, A, O, n_params, nsm):
-    """Algorithmic FLOPs and bytes of one launch-set of `name`."""
+def kernel_work(name, rows, iters, H, A, O, n_params, nsm, batch=0, NH=16, SW=1):
+    """Algorithmic FLOPs and HBM bytes of one launch-set of `name` over `rows` real state rows
+    (DESIGN.md \u00a76). FLOPs count only the dense GEMMs over real rows (the one-hot layer 1
+    is a gather); bytes count each tensor the kernel must read or write once."""
     R = rows
-    if name == "k_fast_rollout":      # hidden GEMM per real (row, step); policy head is SIMT
-        return 2.0 * H * H * R, R * (2 + 4 + 4)
-    if name == "k_fast_fwd":          # layer 2 GEMM; writes h1, h2 bf16 rows + head stats
-        return 2.0 * H * H * R, R * (2 * H * 2 + (A + 4) * 4)
-    if name == "k_fast_bwd":          # dgrad GEMM; reads h1, h2, writes dz1, dz2, dhead
-        return 2.0 * H * H * R, R * (4 * H * 2 + 64 * 2 + (A + 8) * 4)
-    if name == "k_fast_wgrad":        # dW2 + dW_head GEMMs (dW1 is a one-hot scatter)
-        return 2.0 * R * (H * H + H * (A + 1)), R * (5 * H * 2 + 64 * 2) + nsm * n_params * 4
+    rs = ((A + 3) + 3) // 4 * 4
+    if name == "k_fast_rollout":      # hidden + head GEMM per (row, step) + fused training forward
+        fl = 2.0 * R * (H * H + H * (A + 1))
+        by = R * (2 * 2 * H + 2 * H // 8 + NH * 4 + 8 + 4 * SW + 4) + batch * (4 + 8 + 4 * SW)
+        return fl, by
+    if name == "k_row_stats":         # head outputs -> masked log-softmax record
+        return 0.0, R * (NH * 4 + 4 + 4 * SW + 2 + rs * 4)
+    if name == "k_fast_fwd":          # (only when weights changed after the rollout)
+        return 2.0 * R * (H * H + H * (A + 1)), R * (2 * H * 2 + 2 * H // 8 + rs * 4)
+    if name == "k_fast_bwd":          # head dgrad + hidden dgrad; writes dz1, dz2, dhead
+        return 2.0 * R * (H * H + H * (A + 1)), R * (2 * H // 8 + rs * 4 + 16 + 8 + 4 * SW + 2 * 2 * H + 64 * 2)
+    if name == "k_fast_wgrad":        # dW2 + dW_head GEMMs (dW1 + db1 one-hot GEMM counted as bytes)
+        return 2.0 * R * (H * H + H * (A + 1)), R * (4 * H * 2 + 64 * 2 + 4 + 4 * SW) + nsm * n_params * 4
     if name == "k_reduce":
         return 0.0, (nsm + 1) * n_params * 4 * iters
     if name == "k_fast_adam":
         return 0.0, 28.0 * n_params * iters
     if name == "k_fast_loss":
-        return 0.0, R * (3 * 4 + 16)
+        return 0.0, R * (3 * 4 + 16 + 4 + 2) + batch * 16
     return 0.0, 0.0
 
 
@@ -361,13 +368,13 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f)
     for name, (tot_ms, cnt) in prof.items():
-        fl, by = kernel_work(name, rows, K, H, A, O_, tr.n_params, 148)
+        fl, by = kernel_work(name, rows, K, H, A, O_, tr.n_params, 148, batch=args.batch * K)
         sec = tot_ms / 1e3
         kernels[name] = {"ms_total": round(tot_ms, 4), "launches": cnt,
                          "tflops": fl / sec / 1e12 if sec else None,
                          "gbs": by / sec / 1e9 if sec else None}
     if dom:
-        fl, by = kernel_work(dom, rows, K, H, A, O_, tr.n_params, 148)
+        fl, by = kernel_work(dom, rows, K, H, A, O_, tr.n_params, 148, batch=args.batch * K)
         sec = dom_ms[0] / 1e3
         ft = fl / sec / 1e12 / tens if sec else 0.0
         fb = by / sec / 1e9 / hbm if sec else 0.0
