@@ -236,6 +236,8 @@ gfnx_status gfnx_phase_timers(gfnx_ctx* ctx, int32_t mode, int64_t* out, int32_t
 /* tcgen05.mma 128 x n x 256 (bf16, SW128 smem operands) issue-to-completion clocks per CTA
  * for `reps` back-to-back MMAs (mode 0: wait after each, 1: K-split issue, 2: one wait). */
 gfnx_status gfnx_test_mma_rate(int32_t n, int32_t reps, int32_t mode, int32_t grid, int64_t* cycles);
+/* D[128x256] = A[128x256] B[256x256]^T (bf16 bits, row-major; A staged in tensor memory). */
+gfnx_status gfnx_test_ts_mma(const uint16_t* a, const uint16_t* b, float* d);
 gfnx_status gfnx_test_threefry(const uint64_t* keys_hi_lo, const uint64_t* ctr, int64_t n,
                                uint64_t* out);
 gfnx_status gfnx_test_uniform_fold(uint64_t key_hi, uint64_t key_lo, const uint64_t* idx,

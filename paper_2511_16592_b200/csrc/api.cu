@@ -914,6 +914,13 @@ gfnx_status gfnx_test_mma_rate(int32_t n, int32_t reps, int32_t mode, int32_t gr
   });
 }
 
+gfnx_status gfnx_test_ts_mma(const uint16_t* a, const uint16_t* b, float* d) {
+  return guard(nullptr, [&] {
+    test_ts_mma(a, b, d);
+    cuda_check(cudaGetLastError(), "ts mma");
+  });
+}
+
 gfnx_status gfnx_test_uniform_fold(uint64_t key_hi, uint64_t key_lo, const uint64_t* idx, int64_t n,
                                    double* out) {
   return guard(nullptr, [&] {

@@ -62,6 +62,7 @@ void ls_train(Ctx& c);
 
 // diagnostics — fast.cu
 void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out);
+void test_ts_mma(const uint16_t* a, const uint16_t* b, float* d);
 
 // shared small kernels — batch.cu
 void launch_row_scan(Ctx& c);

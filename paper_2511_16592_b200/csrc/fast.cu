@@ -704,6 +704,367 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_fast_rollout_ts: H = 256 rollout with every GEMM A operand in tensor memory.
+//
+// Layer 1 runs on the tensor cores as well: each row's observation (<= 128 features,
+// one-hot / 0-1 for hypergrid and DAG) is written into TMEM as the bf16 A operand of
+// obs W1 (W1^T resident in smem as a K-major image), so TMEM holds only the accumulator
+// [0, H) (layer 1, then the hidden layer), the packed bf16 activations [H, H + H/2)
+// (obs, then h1, then h2 - the A operand of the next MMA, "TS" form) and the head
+// accumulator [H + H/2, H + H/2 + NH). No shared-memory A tile: one MMA round per layer
+// (instead of two split-K halves), both threads of a row stage their column halves at once,
+// and no layer-1 state survives between steps. h1 / h2 rows are copied from TMEM into the
+// emission tiles while the next MMA runs.
+template <int H, int NH>
+constexpr int rollout_ts_smem_bytes() {
+  return H * H * 2 + NH * H * 2 + H * 128 * 2 + 1024;
+}
+
+template <class Env, int H, int NH>
+__global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) {
+  static_assert(H == 256, "TS rollout is the H = 256 path");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  constexpr int HC = H / 2;              // columns owned by each thread of a row
+  constexpr uint32_t TA = H;             // packed activation columns [H, H + H/2)
+  constexpr uint32_t TH = H + H / 2;     // head accumulator columns
+  uint8_t* w2img = smem;                 // H x H bf16 (resident)
+  uint8_t* whimg = w2img + H * H * 2;    // head image [NH][H]
+  uint8_t* w1img = whimg + NH * H * 2;   // W1^T image [H][128 features], K-major
+  __shared__ float b1s[H], b2s[H];
+  __shared__ float bhs[NH];
+  __shared__ Key skeys[128];
+  __shared__ double row_u[kTile];
+  __shared__ int row_b[kTile], row_t[kTile];
+  __shared__ uint2 row_fm[kTile][2];  // active 0/1 observation features (bit f), per column half
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
+  __shared__ unsigned long long smax;
+  __shared__ double inv_legal[NH + 1];
+  __shared__ int s_cur0, s_next;
+  __shared__ uint4 row_m1[kTile][H / 128], row_m2[kTile][H / 128];
+
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, c0 = half * HC;
+  const int T = P.T, A = P.A;
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+    smax = 0;
+    const int t0 = atomicAdd(a.tilectr, 2);
+    s_cur0 = t0;
+    s_next = t0 + 1;
+  }
+  __syncthreads();
+  int cur = s_cur0, fill = 0;
+  if (tid == 0) {
+    mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
+    bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
+    bulk_g2s_big(whimg, a.W.whead_f, NH * H * 2, &mbar);
+  }
+  // W1^T as the K-major B operand of obs W1: row n = hidden unit, K = 128 features (zero
+  // beyond obs_dim); thread pairs build one 16-byte chunk (8 features) of a unit's row
+  for (int i = tid; i < H * 16; i += kThreads) {
+    const int n = i % H, c = i / H;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int f0 = 8 * c + 2 * e;
+      const uint32_t lo = f0 < P.O ? __bfloat16_as_ushort(a.W.w1[(size_t)f0 * H + n]) : 0u;
+      const uint32_t hi = f0 + 1 < P.O ? __bfloat16_as_ushort(a.W.w1[(size_t)(f0 + 1) * H + n]) : 0u;
+      w[e] = lo | (hi << 16);
+    }
+    *reinterpret_cast<uint4*>(w1img + sw128_offset(n, 8 * c, H)) = make_uint4(w[0], w[1], w[2], w[3]);
+  }
+  fence_proxy_async();
+  for (int t = tid; t < T && t < 128; t += kThreads) skeys[t] = fold_in(a.key, (uint64_t)t);
+  for (int j = tid; j < H; j += kThreads) {
+    b1s[j] = a.W.b1[j];
+    b2s[j] = a.W.b2[j];
+  }
+  if (tid < NH) bhs[tid] = tid < A ? a.W.bf[tid] : (tid == A ? a.W.bfl[0] : 0.f);
+  if (tid <= NH) inv_legal[tid] = tid ? 1.0 / tid : 0.0;
+  mbar_wait(&mbar, 0);
+  uint32_t phase = 1;
+  tc_fence_after();
+  __syncthreads();
+  const uint32_t tmem = tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+
+  auto mma_join = [&]() {
+    if (tid == 0) mbar_wait(&mbar, phase);
+    phase ^= 1;
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto publish = [&]() {  // tcgen05.st of the A operand -> visible to the MMA issuer
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+  };
+  bool bad = false;
+  auto set_features = [&](const typename Env::State& st) {  // observation as a bit set
+    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    Env::features(P, st, [&](int f, double x) {
+      if (x != 1.0 || f >= 128) bad = true;  // this path takes 0/1 observations only
+#pragma unroll
+      for (int w = 0; w < 4; ++w)
+        if ((f >> 5) == w) m[w] |= 1u << (f & 31);
+    });
+    row_fm[row][0] = make_uint2(m[0], m[1]);
+    row_fm[row][1] = make_uint2(m[2], m[3]);
+  };
+
+  typename Env::State s;
+  Env::reset(P, s);
+  int b = -1, tstep = 0;
+  bool active = false, pending = false;
+  int bnext = 0;
+  if (half == 0) {
+    b = atomicAdd(a.work, 1);
+    active = b < a.Bl;
+    row_b[row] = b;
+    row_t[row] = 0;
+    set_features(s);
+  }
+  long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+  auto mark = [&](int k) {
+    if (a.phase && tid == 0) {
+      const long long tnow = clock64();
+      ph[k] += tnow - tprev;
+      tprev = tnow;
+    }
+  };
+  // copy this thread's 128 packed activation columns (two 64-feature blocks of its row)
+  // from TMEM into the row's emission slot of `img`
+  auto emit = [&](__nv_bfloat16* img, bool valid, int gs) {
+#pragma unroll 1
+    for (int j = 0; j < 2; ++j) {
+      uint32_t r[32];
+      tmem_ld32(lane_base + TA + (c0 >> 1) + 32 * j, r);
+      tmem_wait_ld();
+      if (valid && a.emit_mode != 1) {
+        const int prow = gs & (kTile - 1);
+        uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 +
+                       ((c0 >> 6) + j) * (kTile * 128) + prow * 128;
+#pragma unroll
+        for (int l = 0; l < 8; ++l)
+          *reinterpret_cast<uint4*>(dst + ((l ^ (prow & 7)) * 16)) =
+              make_uint4(r[4 * l], r[4 * l + 1], r[4 * l + 2], r[4 * l + 3]);
+      }
+    }
+  };
+  int nact;
+  while ((nact = __syncthreads_count(active || pending)) > 0) {
+    mark(0);
+    if (a.phase && tid == 0) {
+      ph[6] += 1;
+      ph[7] += nact;
+      ph[8] += smax;
+      smax = 0;
+    }
+    // (1) observation row (bf16, features [64*half, 64*half + 64) of this thread) into
+    //     the TMEM A columns; layer 1 = obs W1 on the tensor cores
+    {
+      const uint2 fm = row_fm[row][half];
+      uint32_t ob[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {  // bf16 1.0 = 0x3F80
+        const uint32_t w = i < 16 ? fm.x : fm.y, sh = 2 * (i & 15);
+        ob[i] = ((w >> sh) & 1u) * 0x3F80u | ((w >> (sh + 1)) & 1u) * 0x3F800000u;
+      }
+      tmem_st32(lane_base + TA + 32 * half, ob);
+    }
+    publish();
+    if (tid == 0) {
+      tc_fence_after();
+      mma_tk<H, 128>(tmem, tmem + TA, w1img, false);
+      umma_commit(&mbar);
+    }
+    mma_join();
+    // h1 = ReLU(acc + b1) -> packed into TMEM (the hidden MMA's A operand) + ReLU mask
+#pragma unroll 1
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
+      uint32_t r[32];
+      tmem_ld32(lane_base + col, r);
+      tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b1s[col + 2 * i], 0.f),
+                            fmaxf(__uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1], 0.f));
+      reinterpret_cast<uint32_t*>(row_m1[row])[col >> 5] = relu_mask16(pk);
+      tmem_st16(lane_base + TA + (col >> 1), pk);
+    }
+    if (pending) {  // the refill claim issued at the last termination lands here
+      b = bnext;
+      active = b < a.Bl;
+      row_b[row] = active ? b : -1;
+      pending = false;
+    }
+    publish();
+    bool my_valid = false;
+    int gslot = 0;
+    bool crossed = false;
+    int claim = 0;
+    {
+      int before = 0, n = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int rb = row_b[q * 32 + lane];
+        const bool v = rb >= 0 && rb < a.Bl;
+        const uint32_t m = __ballot_sync(0xffffffffu, v);
+        n += __popc(m);
+        if (q < quarter) before += __popc(m);
+        if (q == quarter) {
+          before += __popc(m & ((1u << lane) - 1u));
+          my_valid = v;
+        }
+      }
+      const int nxt = s_next;
+      const int p = fill + before;
+      gslot = (p < kTile ? cur : nxt) * kTile + (p & (kTile - 1));
+      fill += n;
+      if (fill >= kTile) {
+        fill -= kTile;
+        cur = nxt;
+        crossed = true;
+      }
+      if (crossed && tid == kThreads - 1) claim = atomicAdd(a.tilectr, 1);
+    }
+    mark(1);
+    // (2) hidden layer: acc[128 x H] = h1 W2^T, A from TMEM, one round
+    if (tid == 0) {
+      tc_fence_after();
+      mma_tk<H, H>(tmem, tmem + TA, w2img, false);
+      umma_commit(&mbar);
+    }
+    if (half == 1) {  // the row's uniform while the MMA runs (rng.cpp:64-66)
+      const int rb = row_b[row];
+      row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
+    }
+    emit(a.h1, my_valid, gslot);
+    mma_join();
+    mark(2);
+    // (3) h2 = ReLU(acc + b2) -> packed into TMEM (overwrites h1) + mask
+#pragma unroll 1
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
+      uint32_t r[32];
+      tmem_ld32(lane_base + col, r);
+      tmem_wait_ld();
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i)
+        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b2s[col + 2 * i], 0.f),
+                            fmaxf(__uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f));
+      reinterpret_cast<uint32_t*>(row_m2[row])[col >> 5] = relu_mask16(pk);
+      tmem_st16(lane_base + TA + (col >> 1), pk);
+    }
+    publish();
+    mark(3);
+    // (4) head (logits + flow) on the tensor cores
+    if (tid == 0) {
+      tc_fence_after();
+      mma_tk<NH, H>(tmem + TH, tmem + TA, whimg, false);
+      umma_commit(&mbar);
+    }
+    emit(a.h2, my_valid, gslot);
+    mma_join();
+    mark(4);
+    float logit[NH];
+    {
+      uint32_t r[16];
+      tmem_ld16(lane_base + TH, r);
+      tmem_wait_ld();
+#pragma unroll
+      for (int c = 0; c < NH; ++c) logit[c] = __uint_as_float(r[c]) + bhs[c];
+    }
+    tc_fence_before();
+    const long long ts0 = a.phase ? clock64() : 0;
+    if (half == 0 && active) {
+      float ex[NH], hi, z, rz;
+      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], inv_legal, &bad, ex, hi, z, rz);
+      if (act < 0) {
+        active = false;
+        a.frow_bt[gslot] = -1;
+      } else {
+        const size_t bt = (size_t)b * T + tstep;
+        a.frow_bt[gslot] = (int32_t)bt;
+        a.bt_row[bt] = gslot;
+        Env::pack(P, s, a.stst + bt * P.SW);
+        const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
+        const bool term = Env::step(P, s, act);
+        a.batch.actions[bt] = (int16_t)act;
+        a.batch.nparents[bt] = (uint16_t)Env::num_parents(P, s);
+        if (P.mdb && !term) a.batch.delta[bt] = Env::log_reward(P, s) - prev_r;
+        ++tstep;
+        if (term) {
+          a.batch.lengths[b] = tstep;
+          a.batch.log_rewards[b] = Env::log_reward(P, s);
+          Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
+          bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          pending = true;
+          active = false;
+          Env::reset(P, s);
+          tstep = 0;
+        } else if (tstep >= T) {
+          bad = true;
+          active = false;
+        }
+        set_features(s);
+        row_b[row] = active ? b : -1;
+        row_t[row] = tstep;
+      }
+    }
+    if (crossed && tid == kThreads - 1) s_next = claim;
+    if (half == 1 && my_valid && a.emit_mode != 1) {  // raw logits + ReLU masks of the row (idle half)
+      float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
+#pragma unroll
+      for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
+      uint4* m1 = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
+      uint4* m2 = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
+#pragma unroll
+      for (int k = 0; k < H / 128; ++k) {
+        m1[k] = row_m1[row][k];
+        m2[k] = row_m2[row][k];
+      }
+    }
+    if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
+    mark(5);
+  }
+  if (a.phase && tid == 0)
+    for (int k = 0; k < 9; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)ph[k]);
+  if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
+  {  // unused emission rows: rows [fill, 128) of `cur` and the whole pre-claimed tile
+    const int nxt = s_next;
+    const int slot = tid < kTile ? cur * kTile + tid : nxt * kTile + (tid - kTile);
+    if (tid >= fill) {
+      a.frow_bt[slot] = -1;
+      const int prow = slot & (kTile - 1);
+#pragma unroll
+      for (int blk = 0; blk < H / 64; ++blk) {
+        const size_t off = (size_t)(slot >> 7) * kTile * H * 2 + blk * (kTile * 128) + prow * 128;
+        uint4* d1 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.h1) + off);
+        uint4* d2 = reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(a.h2) + off);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          d1[j] = make_uint4(0, 0, 0, 0);
+          d2[j] = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// ---------------------------------------------------------------------------
 // k_fast_fwd: forward over the real rows (2 threads per row, as in the rollout)
 
 struct TrainArgs {
@@ -1645,6 +2006,18 @@ struct Kernels {
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
     ProfScope ps(c, "k_fast_rollout");
+    if constexpr (H == 256) {
+      const int tsb = rollout_ts_smem_bytes<H, NH>();
+      cudaFuncAttributes ft{};
+      cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH>);
+      if (tsb + (int)ft.sharedSizeBytes <= optin && !getenv("GFNX_ROLLOUT_SS")) {
+        set_smem_once(k_fast_rollout_ts<Env, H, NH>, tsb);
+        k_fast_rollout_ts<Env, H, NH><<<grid, kThreads, tsb, c.stream>>>(a);
+        c.launches++;
+        f.fused = true;
+        return;
+      }
+    }
     if (fixed + w1b + (int)fa.sharedSizeBytes <= optin) {  // W1 resident in smem
       set_smem_once(k_fast_rollout<Env, H, NH, true>, fixed + w1b);
       k_fast_rollout<Env, H, NH, true><<<grid, kThreads, fixed + w1b, c.stream>>>(a);
@@ -1994,6 +2367,75 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(int reps, int mode, long lo
   if (tid < 32) tmem_dealloc<512>(tbase);
 }
 }  // namespace
+
+namespace {
+// D[128 x 256] = A[128 x 256] B[256 x 256]^T with A staged in TMEM (bf16 pairs per column):
+// checks the TS operand layout the rollout relies on
+__global__ void __launch_bounds__(128, 1) k_test_ts(const uint32_t* A, const __nv_bfloat16* B, float* D) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* bimg = align1024(smem_raw);
+  __shared__ uint64_t mbar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  for (int i = tid; i < 256 * 256; i += 128) {
+    const int n = i / 256, k = i % 256;
+    *reinterpret_cast<__nv_bfloat16*>(bimg + sw128_offset(n, k, 256)) = B[i];
+  }
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase, lb = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int q = 0; q < 4; ++q) {  // row tid: 128 packed columns
+    uint32_t r[32];
+    for (int i = 0; i < 32; ++i) r[i] = A[tid * 128 + q * 32 + i];
+    tmem_st32(lb + 256 + q * 32, r);
+  }
+  tmem_wait_st();
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  if (tid == 0) {
+    tc_fence_after();
+    mma_tk<256, 256>(tmem, tmem + 256, bimg, false);
+    umma_commit(&mbar);
+    mbar_wait(&mbar, 0);
+  }
+  __syncthreads();
+  tc_fence_after();
+  for (int q = 0; q < 8; ++q) {
+    uint32_t r[32];
+    tmem_ld32(lb + q * 32, r);
+    tmem_wait_ld();
+    for (int i = 0; i < 32; ++i) D[tid * 256 + q * 32 + i] = __uint_as_float(r[i]);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+}  // namespace
+
+void test_ts_mma(const uint16_t* a, const uint16_t* b, float* d) {
+  uint32_t* da;
+  __nv_bfloat16* db;
+  float* dd;
+  cudaMalloc(&da, 128 * 256 * 2);
+  cudaMalloc(&db, 256 * 256 * 2);
+  cudaMalloc(&dd, 128 * 256 * 4);
+  cudaMemcpy(da, a, 128 * 256 * 2, cudaMemcpyHostToDevice);
+  cudaMemcpy(db, b, 256 * 256 * 2, cudaMemcpyHostToDevice);
+  const int smem = 256 * 256 * 2 + 1024;
+  cudaFuncSetAttribute(k_test_ts, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  k_test_ts<<<1, 128, smem>>>(da, db, dd);
+  cudaMemcpy(d, dd, 128 * 256 * 4, cudaMemcpyDeviceToHost);
+  cudaFree(da);
+  cudaFree(db);
+  cudaFree(dd);
+}
 
 void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out) {
   long long* d;

@@ -51,6 +51,19 @@ GFNX_DEV uint32_t relu_mask16(const uint32_t (&pk)[16]) {
   return m;
 }
 
+// D[128 x N] (+)= A[128 x K] * B[N x K]^T with A in TMEM (columns a_col.., K/2 of them)
+// and B a K-major 128B-swizzled image in smem.
+template <int N, int K>
+GFNX_DEV void mma_tk(uint32_t d_tmem, uint32_t a_tmem, const void* b_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t b0 = smem_u32(b_img);
+#pragma unroll
+  for (int s = 0; s < K / 16; ++s) {
+    const uint32_t bo = b0 + (s >> 2) * (N * 128) + (s & 3) * 32;
+    umma_bf16_ts(d_tmem, a_tmem + s * 8, umma_desc_sw128(bo, 16, 1024), idesc, (acc || s > 0) ? 1u : 0u);
+  }
+}
+
 // store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
 GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
 #pragma unroll

@@ -86,6 +86,7 @@ def lib():
         L.gfnx_counters.argtypes = [vp, vp, C.c_int32]
         L.gfnx_phase_timers.argtypes = [vp, C.c_int32, vp, C.c_int32]
         L.gfnx_test_mma_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp]
+        L.gfnx_test_ts_mma.argtypes = [vp, vp, vp]
         L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
         _LIB = L
