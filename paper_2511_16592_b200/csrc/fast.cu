@@ -726,8 +726,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   constexpr int HC = H / 2;              // columns owned by each thread of a row
-  constexpr uint32_t TA = H;             // packed activation columns [H, H + H/2)
-  constexpr uint32_t TH = H + H / 2;     // head accumulator columns
+  constexpr uint32_t TA = H;             // packed obs, then h1: columns [H, H + H/2)
+  constexpr uint32_t TA2 = H + H / 2;    // packed h2: columns [H + H/2, 2H)
+  constexpr uint32_t TH = 0;             // head accumulator: [0, NH) of the (consumed) accumulator
   uint8_t* w2img = smem;                 // H x H bf16 (resident)
   uint8_t* whimg = w2img + H * H * 2;    // head image [NH][H]
   uint8_t* w1img = whimg + NH * H * 2;   // W1^T image [H][128 features], K-major
@@ -742,7 +743,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
   __shared__ int s_cur0, s_next;
-  __shared__ uint4 row_m1[kTile][H / 128], row_m2[kTile][H / 128];
 
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -840,11 +840,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   };
   // copy this thread's 128 packed activation columns (two 64-feature blocks of its row)
   // from TMEM into the row's emission slot of `img`
-  auto emit = [&](__nv_bfloat16* img, bool valid, int gs) {
+  auto emit = [&](__nv_bfloat16* img, uint32_t ta, bool valid, int gs) {
 #pragma unroll 1
     for (int j = 0; j < 2; ++j) {
       uint32_t r[32];
-      tmem_ld32(lane_base + TA + (c0 >> 1) + 32 * j, r);
+      tmem_ld32(lane_base + ta + (c0 >> 1) + 32 * j, r);
       tmem_wait_ld();
       if (valid && a.emit_mode != 1) {
         const int prow = gs & (kTile - 1);
@@ -897,7 +897,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b1s[col + 2 * i], 0.f),
                             fmaxf(__uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1], 0.f));
-      reinterpret_cast<uint32_t*>(row_m1[row])[col >> 5] = relu_mask16(pk);
       tmem_st16(lane_base + TA + (col >> 1), pk);
     }
     if (pending) {  // the refill claim issued at the last termination lands here
@@ -947,10 +946,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       const int rb = row_b[row];
       row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
     }
-    emit(a.h1, my_valid, gslot);
+    emit(a.h1, TA, my_valid, gslot);
     mma_join();
     mark(2);
-    // (3) h2 = ReLU(acc + b2) -> packed into TMEM (overwrites h1) + mask
+    // (3) h2 = ReLU(acc + b2) -> packed into TMEM (own columns: h1 stays for its mask)
 #pragma unroll 1
     for (int q = 0; q < HC / 32; ++q) {
       const int col = c0 + q * 32;
@@ -962,18 +961,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       for (int i = 0; i < 16; ++i)
         pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b2s[col + 2 * i], 0.f),
                             fmaxf(__uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f));
-      reinterpret_cast<uint32_t*>(row_m2[row])[col >> 5] = relu_mask16(pk);
-      tmem_st16(lane_base + TA + (col >> 1), pk);
+      tmem_st16(lane_base + TA2 + (col >> 1), pk);
     }
     publish();
     mark(3);
     // (4) head (logits + flow) on the tensor cores
     if (tid == 0) {
       tc_fence_after();
-      mma_tk<NH, H>(tmem + TH, tmem + TA, whimg, false);
+      mma_tk<NH, H>(tmem + TH, tmem + TA2, whimg, false);
       umma_commit(&mbar);
     }
-    emit(a.h2, my_valid, gslot);
+    emit(a.h2, TA2, my_valid, gslot);
     mma_join();
     mark(4);
     float logit[NH];
@@ -1022,16 +1020,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       }
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
-    if (half == 1 && my_valid && a.emit_mode != 1) {  // raw logits + ReLU masks of the row (idle half)
-      float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
+    if (half == 1) {  // idle half while the row samples: raw head outputs + ReLU masks of h1, h2
+      if (my_valid && a.emit_mode != 1) {
+        float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
 #pragma unroll
-      for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
-      uint4* m1 = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
-      uint4* m2 = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
+        for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
+      }
+#pragma unroll 1
+      for (int m = 0; m < 2; ++m) {
+        uint32_t mw[H / 32];
 #pragma unroll
-      for (int k = 0; k < H / 128; ++k) {
-        m1[k] = row_m1[row][k];
-        m2[k] = row_m2[row][k];
+        for (int q = 0; q < H / 64; ++q) {  // 32 packed columns = 64 units per load
+          uint32_t r[32];
+          tmem_ld32(lane_base + (m ? TA2 : TA) + 32 * q, r);
+          tmem_wait_ld();
+          uint32_t lo[16], hi[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            lo[i] = r[i];
+            hi[i] = r[16 + i];
+          }
+          mw[2 * q] = relu_mask16(lo);
+          mw[2 * q + 1] = relu_mask16(hi);
+        }
+        if (my_valid && a.emit_mode != 1) {
+          uint4* dst = reinterpret_cast<uint4*>((m ? a.mask2 : a.mask1) + (size_t)gslot * (H / 32));
+#pragma unroll
+          for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
+        }
       }
     }
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
