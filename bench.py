@@ -310,9 +310,39 @@ def main():
     tr.run(0, W)
     tr.synchronize()
 
-    # ---- device-timed region: everything resident, CUDA events on the engine stream
+    # ---- end to end through the C ABI: per iteration, results copied to pinned host
+    # memory (gfnx_iteration_async + gfnx_slot_wait, two slots in flight) and consumed.
+    # Runs iterations W..W+K-1 first; the policy + Adam state are then restored so the
+    # device-timed region below replays exactly the same K iterations (same trajectories).
+    e2e = None
+    snap = (tr.params(), tr.adam_state())
     clocks = ClockSampler(local)
     clocks.start()
+    if not args.no_e2e:
+        comm.barrier()
+        tr.synchronize()
+        t0 = time.perf_counter()
+        d2h = 0
+        sink = 0.0
+        for i in range(K):
+            tr.iteration_async(W + i, i % 2)
+            if i > 0:
+                _, loss, res = tr.slot_wait((i - 1) % 2)
+                sink += loss + float(res["log_rewards"][0])
+                d2h = 8 + sum(v.nbytes for v in res.values())
+        _, loss, res = tr.slot_wait((K - 1) % 2)
+        tr.synchronize()
+        dt = comm.max(time.perf_counter() - t0)
+        e2e = {"value": args.batch * world * K / dt, "unit": UNIT,
+               "h2d_bytes_per_step": 24, "d2h_bytes_per_step": d2h,
+               "note": "gfnx_iteration_async per step: h2d = iteration index, lr, eps (kernel "
+                       "arguments); d2h = loss + lengths/log-rewards/terminal states into pinned "
+                       "host memory, consumed by the host every step; host wall clock"}
+    tr.set_params(*snap[0])
+    tr.set_adam_state(*snap[1])
+    tr.synchronize()
+
+    # ---- device-timed region: everything resident, CUDA events on the engine stream
     launches0 = tr.kernel_launches()
     rows0, rolls0 = tr.counters()[:2]
     tr.profile(True)
@@ -331,29 +361,6 @@ def main():
     rows = rows1 - rows0
     value = args.batch * world * K / (ms / 1e3)
 
-    # ---- end to end through the C ABI: per iteration, results copied to pinned host
-    # memory (gfnx_iteration_async + gfnx_slot_wait, two slots in flight) and consumed
-    e2e = None
-    if not args.no_e2e:
-        comm.barrier()
-        tr.synchronize()
-        t0 = time.perf_counter()
-        d2h = 0
-        sink = 0.0
-        for i in range(K):
-            tr.iteration_async(W + K + i, i % 2)
-            if i > 0:
-                _, loss, res = tr.slot_wait((i - 1) % 2)
-                sink += loss + float(res["log_rewards"][0])
-                d2h = 8 + sum(v.nbytes for v in res.values())
-        _, loss, res = tr.slot_wait((K - 1) % 2)
-        tr.synchronize()
-        dt = comm.max(time.perf_counter() - t0)
-        e2e = {"value": args.batch * world * K / dt, "unit": UNIT,
-               "h2d_bytes_per_step": 24, "d2h_bytes_per_step": d2h,
-               "note": "gfnx_iteration_async per step: h2d = iteration index, lr, eps (kernel "
-                       "arguments); d2h = loss + lengths/log-rewards/terminal states into pinned "
-                       "host memory, consumed by the host every step; host wall clock"}
     cl = clocks.stop()
 
     # ---- roofline of the dominant kernel

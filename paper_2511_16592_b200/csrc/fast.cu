@@ -1561,34 +1561,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     const uint32_t tmem = tbase;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     const bool flow = a.objective == GFNX_OBJ_DB || a.objective == GFNX_OBJ_SUBTB;
+    // per-row inputs of a tile, prefetched one tile ahead (the slot map two tiles ahead, so
+    // no load in flight depends on another): masks (both halves), and for half 0 the packed
+    // state, action, loss coefficients and softmax record
+    struct RowIn {
+      uint32_t mk2[HC / 32], mk1[HC / 32];
+      uint32_t sw[kMaxSWFwd];
+      int act;
+      float ga, gs, gf;
+      float pr[NH];
+    };
+    auto slot_of = [&](int tile) { const int r = tile * kTile + row; return tile < tiles && r < R ? a.frow_bt[r] : -1; };
+    auto load_row = [&](int tile, int rbt, RowIn& x) {
+      const int r = tile * kTile + row;
+      const bool v = rbt >= 0;
+#pragma unroll
+      for (int q = 0; q < HC / 32; ++q) {
+        x.mk2[q] = v ? a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+        x.mk1[q] = v ? a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (half == 0 && v && i < P.SW) ? a.stst[(size_t)rbt * P.SW + i] : 0u;
+      x.act = (half == 0 && v) ? a.batch.actions[rbt] : 0;
+      x.ga = (half == 0 && v) ? a.coef[(size_t)r * 4 + 0] : 0.f;
+      x.gs = (half == 0 && v) ? a.coef[(size_t)r * 4 + 1] : 0.f;
+      x.gf = (half == 0 && v && flow) ? a.coef[(size_t)r * 4 + 2] : 0.f;
+#pragma unroll
+      for (int c = 0; c < NH; ++c) x.pr[c] = (half == 0 && v && c < A) ? a.rowbuf[(size_t)r * a.rs + c] : 0.f;
+    };
+    int rbt_cur = slot_of(blockIdx.x), rbt_next = slot_of(blockIdx.x + gridDim.x);
+    RowIn nx;
+    load_row(blockIdx.x, rbt_cur, nx);
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int r = tile * kTile + row;
-      const int rbt = r < R ? a.frow_bt[r] : -1;
+      const int rbt = rbt_cur;
       const bool valid = rbt >= 0;
+      const RowIn cx = nx;
+      rbt_cur = rbt_next;
+      rbt_next = slot_of(tile + 2 * gridDim.x);
+      load_row(tile + gridDim.x, rbt_cur, nx);  // in flight during this tile
       if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
       __syncthreads();
       uint32_t mk2[HC / 32], mk1[HC / 32];
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
-        mk2[q] = valid ? a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
-        mk1[q] = valid ? a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+        mk2[q] = cx.mk2[q];
+        mk1[q] = cx.mk1[q];
       }
       if (half == 0) {
         // dlogits (masked log-softmax backward, tape.cpp:413-434): g_c - p_c * sum(g)
         typename Env::State s;
         Env::reset(P, s);
-        int act = 0;
-        float g_a = 0.f, g_s = 0.f, g_f = 0.f;
-        if (valid) {
-          const size_t bt = (size_t)rbt;
-          Env::unpack(P, a.stst + bt * P.SW, s);
-          act = a.batch.actions[bt];
-          g_a = a.coef[(size_t)r * 4 + 0];
-          g_s = a.coef[(size_t)r * 4 + 1];
-          g_f = flow ? a.coef[(size_t)r * 4 + 2] : 0.f;
-        }
+        if (valid) Env::unpack(P, cx.sw, s);
+        const int act = cx.act;
+        const float g_a = cx.ga, g_s = cx.gs, g_f = cx.gf;
         const float gsum = g_a + g_s;
-        const float* pr = a.rowbuf + (size_t)r * a.rs;
+        const float* pr = cx.pr;
         // only the NH head columns are written: the head dgrad MMA reads K = NH, and the
         // wgrad pass C output columns >= NH (from stale smem) are never read back
 #pragma unroll
