@@ -1100,6 +1100,7 @@ struct TrainArgs {
   int64_t n_params;
   MlpLayout L;
   int objective;
+  long long* phase;  // optional diagnostics: [9..11] wgrad pass clocks (thread 0, summed over CTAs)
 };
 
 // smem: W2 image | head image | staged A (split-K for H = 256, as in the rollout) | W1 (opt.)
@@ -1748,22 +1749,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_wgrad: dW2 = h1^T dz2, dW1 = obs^T dz1, dWhead = h2^T dhead  (K = rows)
+// k_fast_wgrad: dW2 = h1^T dz2, [dW1 | db1] = [obs | 1]^T dz1, dWhead = h2^T dhead (K = rows)
+//
+// The activation tile images are streamed as 64-row units through a 3-stage ring of
+// shared-memory stages (bulk copies on mbarriers, "full"), consumed by tcgen05.mma with
+// MN-major descriptors (LBO = 64 rows x 128 B between 64-feature blocks), and released by
+// the MMA's commit ("empty"): the loads of unit q + 2 are in flight while unit q multiplies.
+// One sequence runs through the three passes (A: h1/dz2, B: obs/dz1, C: h2/dhead); TMEM
+// holds one pass's accumulators, read back into the CTA's partial slab between passes.
+constexpr int kWgStages = 3;
+constexpr int kWgRows = 64;           // rows per unit
+constexpr int kWgStage = 65536;       // X operand [0, 32 KB), Y operand [32 KB, 64 KB)
 
 template <int H>
 constexpr int wgrad_smem_bytes() {
-  return 2 * kTile * H * 2 + 64 + 1024;
+  return kWgStages * kWgStage + 1024;
+}
+
+// D[128 x N] (+)= X'^T Y' over one 64-row unit: X' = features [m0, m0 + 128) of X, Y' = N
+// features of Y, both MN-major with 64-feature blocks of 64 rows x 128 B.
+template <int N>
+GFNX_DEV void mma_mn64(uint32_t d_tmem, const void* x_img, int m0, const void* y_img, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+  constexpr uint32_t LBO = kWgRows * 128;
+  const uint32_t x0 = smem_u32(x_img) + (m0 >> 6) * LBO, y0 = smem_u32(y_img);
+#pragma unroll
+  for (int s = 0; s < kWgRows / 16; ++s)
+    umma_bf16(d_tmem, umma_desc_sw128(x0 + s * 2048, LBO, 1024), umma_desc_sw128(y0 + s * 2048, LBO, 1024),
+              idesc, (acc || s > 0) ? 1u : 0u);
 }
 
 template <class Env, int H>
 __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint8_t* bufA = smem;
-  uint8_t* bufB = bufA + kTile * H * 2;
-  uint64_t* mbar = (uint64_t*)(bufB + kTile * H * 2);
-  uint64_t* mbar2 = mbar + 1;
-  uint32_t* tbase = (uint32_t*)(mbar + 2);
+  uint8_t* ring = align1024(smem_raw);
+  __shared__ uint64_t full[kWgStages], empty[kWgStages];
+  __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int A = P.A;
@@ -1771,137 +1792,188 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   const int R = tiles * kTile;
   const int per = (tiles + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
+  const int nu = t1 > t0 ? 2 * (t1 - t0) : 0;  // units per pass
+  const int NQ = 3 * nu;
   float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
   const MlpLayout& L = a.L;
-  if (warp == 0) tmem_alloc<512>(tbase);
+  constexpr int KH = H / 128;  // 128-feature M blocks of the h operands
+  if (warp == 0) tmem_alloc<512>(&tbase);
   if (tid == 0) {
-    mbar_init(mbar, 1);
-    mbar_init(mbar2, 1);
+    for (int i = 0; i < kWgStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tbase;
+  const uint32_t tmem = tbase;
   const uint32_t lane_base = tmem + ((uint32_t)(warp * 32) << 16);
-  uint32_t ph_load = 0, ph_mma = 0;
-  constexpr int kHalves = H / 128;
-
-  // ---- pass A: dW2[p][j] = sum_r h1[r][p] dz2[r][j]
-  for (int tile = t0; tile < t1; ++tile) {
-    if (tid == 0) {
-      mbar_arrive_expect_tx(mbar, 2 * kTile * H * 2);
-      bulk_g2s_big(bufA, a.h1 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
-      bulk_g2s_big(bufB, a.dz2 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
-      mbar_wait(mbar, ph_load);
-      tc_fence_after();
-#pragma unroll
-      for (int h = 0; h < kHalves; ++h) mma_mn<H>(tmem + h * H, bufA, 128 * h, bufB, tile > t0);
-      umma_commit(mbar2);
-      mbar_wait(mbar2, ph_mma);
+  auto X = [&](int st) { return ring + st * kWgStage; };
+  auto Y = [&](int st) { return ring + st * kWgStage + 32768; };
+  auto src = [&](const void* img, int u, int blk, int width) {  // 64-row unit u, 64-feature block blk
+    const int tile = t0 + (u >> 1), hh = u & 1;
+    return reinterpret_cast<const uint8_t*>(img) + (size_t)tile * kTile * width * 2 + blk * (kTile * 128) +
+           hh * (kWgRows * 128);
+  };
+  auto issue_load = [&](int q) {  // thread 0
+    const int st = q % kWgStages, p = q / nu, u = q % nu;
+    if (q >= kWgStages) mbar_wait(&empty[st], ((q / kWgStages) - 1) & 1);
+    constexpr uint32_t ub = kWgRows * 128;  // one 64-feature block of a unit
+    if (p == 0) {
+      mbar_arrive_expect_tx(&full[st], 2 * (H / 64) * ub);
+      for (int k = 0; k < H / 64; ++k) {
+        bulk_g2s(X(st) + k * ub, src(a.h1, u, k, H), ub, &full[st]);
+        bulk_g2s(Y(st) + k * ub, src(a.dz2, u, k, H), ub, &full[st]);
+      }
+    } else if (p == 1) {
+      mbar_arrive_expect_tx(&full[st], (H / 64) * ub);
+      for (int k = 0; k < H / 64; ++k) bulk_g2s(Y(st) + k * ub, src(a.dz1, u, k, H), ub, &full[st]);
+    } else {
+      mbar_arrive_expect_tx(&full[st], (H / 64) * ub + ub);
+      for (int k = 0; k < H / 64; ++k) bulk_g2s(X(st) + k * ub, src(a.h2, u, k, H), ub, &full[st]);
+      bulk_g2s(Y(st), src(a.dhead, u, 0, 64), ub, &full[st]);
     }
-    ph_load ^= 1;
-    ph_mma ^= 1;
-    __syncthreads();
-  }
-  tc_fence_after();
-  for (int h = 0; h < kHalves; ++h) {
-    const int p = 128 * h + tid;  // input feature of layer 2
-    for (int q = 0; q < H / 32; ++q) {
-      uint32_t r32[32];
-      tmem_ld32(lane_base + h * H + q * 32, r32);
-      tmem_wait_ld();
-      float* dst = part + L.off_w[1] + (size_t)p * H + q * 32;
+  };
+  // TMEM accumulators of pass p -> this CTA's partial slab (zeros when it had no rows)
+  auto readout = [&](int p) {
+    const bool any = nu > 0;
+    if (p == 0) {
+      for (int h = 0; h < KH; ++h) {
+        const int pr = 128 * h + tid;  // input feature of layer 2
+        for (int q = 0; q < H / 32; ++q) {
+          uint32_t r32[32];
+          tmem_ld32(lane_base + h * H + q * 32, r32);
+          tmem_wait_ld();
+          float* dst = part + L.off_w[1] + (size_t)pr * H + q * 32;
 #pragma unroll
-      for (int i = 0; i < 32; ++i) dst[i] = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-
-  // ---- pass B: dW1[f][j] = sum_r obs[r][f] dz1[r][j]   (obs one-hot, built in smem)
-  for (int tile = t0; tile < t1; ++tile) {
-    if (tid == 0) {
-      mbar_arrive_expect_tx(mbar, kTile * H * 2);
-      bulk_g2s_big(bufB, a.dz1 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
-    }
-    const int r = tile * kTile + tid;
-    {  // obs row (128 features) as bf16 one-hot
-      uint32_t z4[4] = {0, 0, 0, 0};
+          for (int i = 0; i < 32; ++i) dst[i] = any ? __uint_as_float(r32[i]) : 0.f;
+        }
+      }
+    } else if (p == 1) {
+      for (int q = 0; q < H / 32; ++q) {
+        uint32_t r32[32];
+        tmem_ld32(lane_base + q * 32, r32);
+        tmem_wait_ld();
+        if (tid <= P.O) {
+          float* dst = tid < P.O ? part + L.off_w[0] + (size_t)tid * H + q * 32 : part + L.off_b[0] + q * 32;
 #pragma unroll
-      for (int c = 0; c < 16; ++c)
-        *reinterpret_cast<uint4*>(bufA + sw128_offset(tid, 8 * c, kTile)) = make_uint4(z4[0], z4[1], z4[2], z4[3]);
-      if (r < R && a.frow_bt[r] >= 0) {
-        typename Env::State s;
-        Env::unpack(P, a.stst + (size_t)a.frow_bt[r] * P.SW, s);
-        Env::features(P, s, [&](int f, double x) {
-          *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, f, kTile)) = __float2bfloat16((float)x);
-        });
-        // constant feature O: its output row is db1 = sum_r dz1[r]
-        *reinterpret_cast<__nv_bfloat16*>(bufA + sw128_offset(tid, P.O, kTile)) = __float2bfloat16(1.f);
+          for (int i = 0; i < 32; ++i) dst[i] = any ? __uint_as_float(r32[i]) : 0.f;
+        }
+      }
+    } else {
+      for (int h = 0; h < KH; ++h) {
+        const int pr = 128 * h + tid;
+        for (int q = 0; q < 2; ++q) {
+          uint32_t r32[32];
+          tmem_ld32(lane_base + h * 64 + q * 32, r32);
+          tmem_wait_ld();
+          for (int i = 0; i < 32; ++i) {
+            const int c = q * 32 + i;
+            const float v = any ? __uint_as_float(r32[i]) : 0.f;
+            if (c < A) part[L.off_fw + (size_t)pr * A + c] = v;
+            else if (c == A) part[L.off_flw + pr] = v;
+          }
+        }
       }
     }
-    fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      mbar_wait(mbar, ph_load);
-      tc_fence_after();
-      mma_mn<H>(tmem, bufA, 0, bufB, tile > t0);
-      umma_commit(mbar2);
-      mbar_wait(mbar2, ph_mma);
-    }
-    ph_load ^= 1;
-    ph_mma ^= 1;
-    __syncthreads();
-  }
-  tc_fence_after();
-  for (int q = 0; q < H / 32; ++q) {  // tcgen05.ld is warp-collective: every lane executes it
-    uint32_t r32[32];
-    tmem_ld32(lane_base + q * 32, r32);
-    tmem_wait_ld();
-    if (tid <= P.O) {
-      float* dst = tid < P.O ? part + L.off_w[0] + (size_t)tid * H + q * 32 : part + L.off_b[0] + q * 32;
+  };
+  // one-hot observation rows of a unit (+ constant feature O) as the MN-major X operand:
+  // two threads per row, one 64-feature block each. The slot map is read two units ahead
+  // and the packed state one unit ahead, so building a unit waits on no global load.
+  auto ld_bt = [&](int u) {
+    if (u >= nu) return -1;
+    const int r = (t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
+    return r < R ? a.frow_bt[r] : -1;
+  };
+  auto ld_sw = [&](int bt, uint32_t (&w)[kMaxSWFwd]) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) dst[i] = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
+    for (int i = 0; i < kMaxSWFwd; ++i) w[i] = (bt >= 0 && i < P.SW) ? a.stst[(size_t)bt * P.SW + i] : 0u;
+  };
+  auto build_obs = [&](uint8_t* x, int bt, const uint32_t (&w)[kMaxSWFwd]) {
+    const int rl = tid & (kWgRows - 1), blk = tid >> 6;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      *reinterpret_cast<uint4*>(x + blk * (kWgRows * 128) + rl * 128 + c * 16) = make_uint4(0, 0, 0, 0);
+    if (bt >= 0) {
+      typename Env::State s;
+      Env::unpack(P, w, s);
+      auto put = [&](int f, float v) {
+        if ((f >> 6) == blk)
+          *reinterpret_cast<__nv_bfloat16*>(x + sw128_offset(rl, f, kWgRows)) = __float2bfloat16(v);
+      };
+      Env::features(P, s, [&](int f, double v) { put(f, (float)v); });
+      put(P.O, 1.f);  // its output row is db1 = sum_r dz1[r]
+    }
+  };
+  int ob_bt0 = ld_bt(0), ob_bt1 = ld_bt(1);  // pass B units 0 and 1, consumed much later
+  uint32_t ob_sw0[kMaxSWFwd];
+  ld_sw(ob_bt0, ob_sw0);
+  auto obs_next = [&](uint8_t* x, int u_after) {  // build the prefetched unit, advance prefetch
+    build_obs(x, ob_bt0, ob_sw0);
+    ob_bt0 = ob_bt1;
+    ld_sw(ob_bt0, ob_sw0);
+    ob_bt1 = ld_bt(u_after);
+  };
+
+  long long tclk = clock64();
+  auto pclock = [&](int k) {
+    if (a.phase && tid == 0) {
+      const long long t = clock64();
+      atomicAdd((unsigned long long*)a.phase + 9 + k, (unsigned long long)(t - tclk));
+      tclk = t;
+    }
+  };
+  if (tid == 0)
+    for (int q = 0; q < kWgStages - 1 && q < NQ; ++q) issue_load(q);
+  for (int q = 0; q < NQ; ++q) {
+    const int st = q % kWgStages, p = q / nu, u = q % nu;
+    if (u == 0 && q > 0) {  // pass boundary: accumulators of pass p - 1 -> slab
+      pclock(p - 1);
+      if (tid == 0) mbar_wait(&empty[(q - 1) % kWgStages], ((q - 1) / kWgStages) & 1);
+      __syncthreads();
+      tc_fence_after();
+      readout(p - 1);
+      if (p == 1) {  // first observation unit (every earlier MMA has completed)
+        obs_next(X(st), 2);
+        fence_proxy_async();
+      }
+      tc_fence_before();
+      __syncthreads();
+    }
+    if (tid == 0) {
+      mbar_wait(&full[st], (q / kWgStages) & 1);
+      tc_fence_after();
+      if (p == 0) {
+#pragma unroll
+        for (int h = 0; h < KH; ++h) mma_mn64<H>(tmem + h * H, X(st), 128 * h, Y(st), u > 0);
+      } else if (p == 1) {
+        mma_mn64<H>(tmem, X(st), 0, Y(st), u > 0);
+      } else {
+#pragma unroll
+        for (int h = 0; h < KH; ++h) mma_mn64<64>(tmem + h * 64, X(st), 128 * h, Y(st), u > 0);
+      }
+      umma_commit(&empty[st]);
+      if (q + kWgStages - 1 < NQ) issue_load(q + kWgStages - 1);
+    }
+    if (p == 1 && u + 1 < nu) {
+      // observation rows of the next unit while this one multiplies: stage (q + 1) was
+      // released (MMA q + 1 - S complete) before thread 0 issued its load last iteration
+      obs_next(X((q + 1) % kWgStages), u + 3);
+      fence_proxy_async();
+      __syncthreads();
     }
   }
-  tc_fence_before();
+  if (NQ > 0 && tid == 0) mbar_wait(&empty[(NQ - 1) % kWgStages], ((NQ - 1) / kWgStages) & 1);
+  pclock(2);
   __syncthreads();
   tc_fence_after();
-
-  // ---- pass C: dWf[p][c] = sum_r h2[r][p] dhead[r][c]   (c < A: logits, c == A: flow)
-  for (int tile = t0; tile < t1; ++tile) {
-    if (tid == 0) {
-      mbar_arrive_expect_tx(mbar, kTile * H * 2 + kTile * 64 * 2);
-      bulk_g2s_big(bufA, a.h2 + (size_t)tile * kTile * H, kTile * H * 2, mbar);
-      bulk_g2s_big(bufB, a.dhead + (size_t)tile * kTile * 64, kTile * 64 * 2, mbar);
-      mbar_wait(mbar, ph_load);
-      tc_fence_after();
-#pragma unroll
-      for (int h = 0; h < kHalves; ++h) mma_mn<64>(tmem + h * 64, bufA, 128 * h, bufB, tile > t0);
-      umma_commit(mbar2);
-      mbar_wait(mbar2, ph_mma);
-    }
-    ph_load ^= 1;
-    ph_mma ^= 1;
-    __syncthreads();
+  if (NQ == 0) {
+    readout(0);
+    readout(1);
   }
-  tc_fence_after();
-  for (int h = 0; h < kHalves; ++h) {
-    const int p = 128 * h + tid;
-    for (int q = 0; q < 2; ++q) {
-      uint32_t r32[32];
-      tmem_ld32(lane_base + h * 64 + q * 32, r32);
-      tmem_wait_ld();
-      for (int i = 0; i < 32; ++i) {
-        const int c = q * 32 + i;
-        const float v = t1 > t0 ? __uint_as_float(r32[i]) : 0.f;
-        if (c < A) part[L.off_fw + (size_t)p * A + c] = v;
-        else if (c == A) part[L.off_flw + p] = v;
-      }
-    }
-  }
+  readout(2);
   tc_fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc<512>(tmem);
@@ -2096,6 +2168,7 @@ struct Kernels {
     ta.n_params = c.L.n_params;
     ta.L = c.L;
     ta.objective = c.train.objective;
+    ta.phase = c.phase;
     const int grid = f.num_sms;
     if (!f.fused) {  // weights changed since the rollout: recompute the forward over the rows
       k_linear_rows<<<(std::max(c.Bl, kTile) + 255) / 256, 256, 0, c.stream>>>(

@@ -262,7 +262,8 @@ class Trainer:
         return [int(x) for x in out]
 
     PHASES = ("loop_barrier", "layer1", "hidden_mma", "hidden_epilogue", "head_mma", "sample_step",
-              "tile_steps", "active_slot_steps", "sample_step_max")
+              "tile_steps", "active_slot_steps", "sample_step_max", "wgrad_pass_a", "wgrad_pass_b",
+              "wgrad_pass_c")
 
     def phase_timers(self, mode: int):
         """Rollout phase clocks (diagnostic): 1 enable, 0 disable, 2 read + clear -> dict."""
