@@ -720,8 +720,9 @@ constexpr int rollout_ts_smem_bytes() {
   return H * H * 2 + NH * H * 2 + H * 128 * 2 + 1024;
 }
 
-template <class Env, int H, int NH>
+template <class Env, int H, int NH, int SA>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) {
+  static_assert(SA <= NH, "sampler width");
   static_assert(H == 256, "TS rollout is the H = 256 path");
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -985,8 +986,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     tc_fence_before();
     const long long ts0 = a.phase ? clock64() : 0;
     if (half == 0 && active) {
-      float ex[NH], hi, z, rz;
-      const int act = sample_row<Env, NH>(P, s, logit, A, a.eps, row_u[row], inv_legal, &bad, ex, hi, z, rz);
+      // the sampler runs over SA >= A columns only (SA = 8 for A <= 8)
+      float lgs[SA], ex[SA], hi, z, rz;
+#pragma unroll
+      for (int c = 0; c < SA; ++c) lgs[c] = logit[c];
+      const int act = sample_row<Env, SA>(P, s, lgs, A, a.eps, row_u[row], inv_legal, &bad, ex, hi, z, rz);
       if (act < 0) {
         active = false;
         a.frow_bt[gslot] = -1;
@@ -2125,10 +2129,15 @@ struct Kernels {
     if constexpr (H == 256) {
       const int tsb = rollout_ts_smem_bytes<H, NH>();
       cudaFuncAttributes ft{};
-      cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH>);
+      cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH, NH>);
       if (tsb + (int)ft.sharedSizeBytes <= optin && !getenv("GFNX_ROLLOUT_SS")) {
-        set_smem_once(k_fast_rollout_ts<Env, H, NH>, tsb);
-        k_fast_rollout_ts<Env, H, NH><<<grid, kThreads, tsb, c.stream>>>(a);
+        if (c.P.A <= 8) {
+          set_smem_once(k_fast_rollout_ts<Env, H, NH, 8>, tsb);
+          k_fast_rollout_ts<Env, H, NH, 8><<<grid, kThreads, tsb, c.stream>>>(a);
+        } else {
+          set_smem_once(k_fast_rollout_ts<Env, H, NH, NH>, tsb);
+          k_fast_rollout_ts<Env, H, NH, NH><<<grid, kThreads, tsb, c.stream>>>(a);
+        }
         c.launches++;
         f.fused = true;
         return;
