@@ -307,7 +307,11 @@ def main():
     nccl_id = comm.bcast_bytes(nccl_id) if world > 1 else None
     tr = engine.Trainer(e, t, device=local, rank=rank, world=world, nccl_id=nccl_id)
     W, K = max(args.warmup, 3), args.steps
-    tr.run(0, W)
+    tr.run(0, W - 2)
+    for i in (W - 2, W - 1):  # the last two warm-up iterations go through the e2e path (pinned slots)
+        tr.iteration_async(i, i % 2)
+    tr.slot_wait(W % 2)
+    tr.slot_wait((W + 1) % 2)
     tr.synchronize()
 
     # ---- end to end through the C ABI: per iteration, results copied to pinned host

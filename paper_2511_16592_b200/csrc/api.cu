@@ -141,7 +141,7 @@ __global__ void k_len_partials(const int32_t* __restrict__ lengths, int Bl, int2
   }
 }
 
-__global__ void k_len_scan_partials(int2* part, int nparts, int32_t* counters) {
+__global__ void k_len_scan_partials(int2* part, int nparts, int32_t* counters, int counts) {
   if (threadIdx.x != 0) return;
   int run = 0, run2 = 0;
   for (int i = 0; i < nparts; ++i) {  // <= 64 entries at B = 65536
@@ -150,6 +150,7 @@ __global__ void k_len_scan_partials(int2* part, int nparts, int32_t* counters) {
     run += p.x;
     run2 += p.y;
   }
+  if (!counts) return;
   long long* acc = reinterpret_cast<long long*>(counters + 8);
   acc[0] += run;
   acc[1] += 1;
@@ -173,12 +174,18 @@ __global__ void k_len_finish(const int32_t* __restrict__ lengths, int Bl, int T,
   if (blockIdx.x == gridDim.x - 1 && threadIdx.x == 0 && Bl % kScanBlock == 0) row0[Bl] = counters[0];
 }
 
-void launch_row_scan(Ctx& c) {
+void ensure_row0(Ctx& c) {
+  if (!c.rows_stale) return;
+  launch_row_scan(c, false);
+  c.rows_stale = false;
+}
+
+void launch_row_scan(Ctx& c, bool counts) {
   ProfScope ps(c, "k_row_scan");
   const int nb = (c.Bl + kScanBlock - 1) / kScanBlock;
   int2* part = reinterpret_cast<int2*>(c.batch.scan_part);
   k_len_partials<<<nb, kScanBlock, 0, c.stream>>>(c.batch.lengths, c.Bl, part);
-  k_len_scan_partials<<<1, 32, 0, c.stream>>>(part, nb, c.batch.counters);
+  k_len_scan_partials<<<1, 32, 0, c.stream>>>(part, nb, c.batch.counters, counts ? 1 : 0);
   k_len_finish<<<nb, kScanBlock, 0, c.stream>>>(c.batch.lengths, c.Bl, c.P.T, part, c.batch.row0,
                                                 c.batch.row_bt, c.batch.counters);
   c.launches += 3;
@@ -263,7 +270,12 @@ void do_rollout(Ctx& c, int64_t it, double eps) {
   cudaEventRecord(c.ev[0], c.stream);
   if (c.check_mode()) check_rollout(c, key, eps);
   else fast_rollout(c, key, eps);
-  launch_row_scan(c);
+  if (c.check_mode() || !fast_rollout_counts(c)) {
+    launch_row_scan(c);
+    c.rows_stale = false;
+  } else {
+    c.rows_stale = true;  // counts published by the rollout; row0 derived on demand
+  }
   if (c.world > 1) nccl_sum(c, c.batch.counters + 4, 2, ncclInt32);
   cudaEventRecord(c.ev[1], c.stream);
   cuda_check(cudaGetLastError(), "rollout launch");

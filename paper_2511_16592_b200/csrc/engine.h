@@ -65,7 +65,9 @@ void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out);
 void test_ts_mma(const uint16_t* a, const uint16_t* b, float* d);
 
 // shared small kernels — batch.cu
-void launch_row_scan(Ctx& c);
+void launch_row_scan(Ctx& c, bool counts = true);
+void ensure_row0(Ctx& c);              // row0 / row_bt of the resident batch (lazy after a fused rollout)
+bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row counts itself
 
 struct Ctx {
   gfnx_env_desc env{};
@@ -120,6 +122,7 @@ struct Ctx {
 
   // optional rollout phase clocks (env GFNX_PHASE_TIMERS=1 at create): [8] int64
   long long* phase = nullptr;
+  bool rows_stale = false;  // row0 / row_bt not derived for the resident batch yet
 
   // fast-mode state (opaque, fast.cu)
   void* fast = nullptr;

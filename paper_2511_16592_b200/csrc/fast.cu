@@ -63,7 +63,8 @@ struct FastState {
   float* logits = nullptr;            // [slots][NH] rollout head outputs (fused forward)
   bool fused = false;                 // row slots hold the rollout's forward for the current weights
   int rs = 0;                         // rowbuf stride (floats)
-  int loss_blocks = 0;
+  int loss_blocks = 0;                // per-thread loss (SubTB): 256 trajectories per block
+  int loss_wblocks = 0;               // warp-per-trajectory loss: 8 trajectories per block
 };
 
 // training-forward record of every emitted row from the rollout's raw head outputs:
@@ -252,6 +253,25 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 //       step the env, record, and refill finished slots from the global work counter.
 
 
+// row counts of a fused rollout (what k_row_scan derives from the lengths otherwise):
+// counters[0] = sum L, [1] = sum max(L - 1, 0), then the last CTA publishes [4], [5] and the
+// int64 running totals [8..9]; counters[12] is the CTA ticket
+GFNX_DEV void finish_counts(int32_t* counters, int rows, int rows_mdb) {
+  atomicAdd(counters + 0, rows);
+  atomicAdd(counters + 1, rows_mdb);
+  __threadfence();
+  if (atomicAdd(counters + 12, 1) == (int)gridDim.x - 1) {
+    __threadfence();
+    const int r0 = atomicAdd(counters + 0, 0), r1 = atomicAdd(counters + 1, 0);
+    counters[4] = r0;
+    counters[5] = r1;
+    long long* acc = reinterpret_cast<long long*>(counters + 8);
+    acc[0] += r0;
+    acc[1] += 1;
+    counters[12] = 0;
+  }
+}
+
 struct RolloutArgs {
   EnvParams P;
   Weights W;
@@ -310,6 +330,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
   __shared__ int s_cur0, s_next;  // emission tiles: first claimed, next claimed
+  __shared__ int s_nterm;          // trajectories finished by this CTA
   __shared__ uint4 row_m1[kTile][H / 128], row_m2[kTile][H / 128];  // ReLU masks of the round
 
   const EnvParams& P = a.P;
@@ -325,11 +346,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     const int t0 = atomicAdd(a.tilectr, 2);
     s_cur0 = t0;
     s_next = t0 + 1;
+    s_nterm = 0;
   }
   __syncthreads();
   // emission cursor (uniform over the CTA): rows of this CTA fill tile `cur` from `fill`,
   // overflowing into the pre-claimed tile s_next
-  int cur = s_cur0, fill = 0;
+  int cur = s_cur0, fill = 0, emitted = 0;
   if (tid == 0) {
     mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
@@ -532,6 +554,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       const int p = fill + before;
       gslot = (p < kTile ? cur : nxt) * kTile + (p & (kTile - 1));
       fill += n;
+      emitted += n;
       if (fill >= kTile) {
         fill -= kTile;
         cur = nxt;
@@ -648,6 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
           bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
           Env::reset(P, s);
@@ -700,6 +724,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     }
   }
   __syncthreads();
+  if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<2 * H>(tmem);
 }
 
@@ -744,6 +769,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
   __shared__ int s_cur0, s_next;
+  __shared__ int s_nterm;
 
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -758,9 +784,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     const int t0 = atomicAdd(a.tilectr, 2);
     s_cur0 = t0;
     s_next = t0 + 1;
+    s_nterm = 0;
   }
   __syncthreads();
-  int cur = s_cur0, fill = 0;
+  int cur = s_cur0, fill = 0, emitted = 0;
   if (tid == 0) {
     mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
@@ -929,6 +956,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       const int p = fill + before;
       gslot = (p < kTile ? cur : nxt) * kTile + (p & (kTile - 1));
       fill += n;
+      emitted += n;
       if (fill >= kTile) {
         fill -= kTile;
         cur = nxt;
@@ -1010,6 +1038,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
           bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
           Env::reset(P, s);
@@ -1081,6 +1110,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
@@ -1505,17 +1535,124 @@ __global__ void k_fast_loss(LossArgs a) {
   }
 }
 
+// TB / DB / MDB with one warp per trajectory (lanes over the steps): the per-step loads
+// are independent, so a trajectory costs two dependent loads instead of 2 L. Same
+// residuals and coefficients as k_fast_loss; partial sums in a fixed tree order.
+GFNX_DEV double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__global__ void k_fast_loss_warp(LossArgs a) {
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int nw = gridDim.x * (blockDim.x >> 5);
+  const int* cnt = a.batch.counters;
+  double norm = (double)a.B_global;
+  if (a.objective == GFNX_OBJ_DB) norm = (double)cnt[4];
+  if (a.objective == GFNX_OBJ_MDB) norm = (double)cnt[5];
+  double loss = 0.0, dlogz = 0.0;  // lane 0
+  for (int b = blockIdx.x * (blockDim.x >> 5) + wib; b < a.Bl; b += nw) {
+    const int L = a.batch.lengths[b];
+    const int32_t* rows = a.bt_row + (size_t)b * a.T;
+    const uint16_t* np = a.batch.nparents + (size_t)b * a.T;
+    const double logr = a.batch.log_rewards[b];
+    auto rec = [&](int t, int k) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A + k]; };
+    auto C = [&](int t) { return reinterpret_cast<float4*>(a.coef + (size_t)rows[t] * 4); };
+    if (a.objective == GFNX_OBJ_TB) {  // tb_loss objectives.cpp:120-142
+      const double w = 1.0 / norm;
+      double sd = 0.0;
+      for (int t = lane; t < L; t += 32) sd += rec(t, 0) - a.neglog[np[t]];
+      sd = warp_sum_d(sd);
+      const double res = sd + a.scalars[0] - logr;
+      const double g = 2.0 * res * w;
+      for (int t = lane; t < L; t += 32) *C(t) = make_float4((float)g, 0.f, 0.f, 0.f);
+      if (lane == 0) {
+        loss += res * res * w;
+        dlogz += g;
+      }
+    } else if (a.objective == GFNX_OBJ_DB) {  // transition_loss :94-118
+      double carry = 0.0, ls = 0.0;
+      for (int k0 = 0; k0 < L; k0 += 32) {
+        const int t = k0 + lane;
+        double g = 0.0;
+        if (t < L) {
+          const double d = rec(t, 0) - a.neglog[np[t]];
+          const double f1 = t + 1 < L ? rec(t + 1, 2) : logr;
+          const double res = rec(t, 2) - f1 + d;
+          const double w = (t == L - 1 ? a.terminal_penalty : 1.0) / norm;
+          ls += res * res * w;
+          g = 2.0 * res * w;
+        }
+        double gp = __shfl_up_sync(0xffffffffu, g, 1);
+        if (lane == 0) gp = carry;
+        if (t < L) *C(t) = make_float4((float)g, 0.f, (float)(g - gp), 0.f);
+        carry = __shfl_sync(0xffffffffu, g, 31);
+      }
+      ls = warp_sum_d(ls);
+      if (lane == 0) loss += ls;
+    } else {  // mdb_loss :186-226
+      const double w = 1.0 / norm;
+      double carry = 0.0, ls = 0.0;
+      for (int k0 = 0; k0 < L; k0 += 32) {
+        const int t = k0 + lane;
+        double g = 0.0;
+        if (t + 1 < L) {
+          const double res = rec(t, 0) + (rec(t + 1, 1) - rec(t, 1)) - a.neglog[np[t]] -
+                             a.batch.delta[(size_t)b * a.T + t];
+          ls += res * res * w;
+          g = 2.0 * res * w;
+        }
+        double gp = __shfl_up_sync(0xffffffffu, g, 1);
+        if (lane == 0) gp = carry;
+        if (t < L) *C(t) = make_float4((float)g, (float)(gp - g), 0.f, 0.f);
+        carry = __shfl_sync(0xffffffffu, g, 31);
+      }
+      ls = warp_sum_d(ls);
+      if (lane == 0) loss += ls;
+    }
+  }
+  __shared__ double red[2][32];
+  if (lane == 0) {
+    red[0][wib] = loss;
+    red[1][wib] = dlogz;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double l = 0.0, z = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) {
+      l += red[0][i];
+      z += red[1][i];
+    }
+    a.lpart[2 * blockIdx.x] = l;
+    a.lpart[2 * blockIdx.x + 1] = z;
+  }
+}
+
+// fixed-order two-level sum of the block partials (256 threads: strided, then a tree)
 __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalars, int tb,
                                 int32_t* err) {
-  if (threadIdx.x != 0) return;
+  __shared__ double red[2][256];
   double l = 0.0, z = 0.0;
-  for (int i = 0; i < nblocks; ++i) {
+  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
     l += lpart[2 * i];
     z += lpart[2 * i + 1];
   }
-  scalars[4] = l;
-  scalars[3] = tb ? z : 0.0;
-  if (!isfinite(l)) atomicExch(err, GFNX_ERR_NUMERIC);
+  red[0][threadIdx.x] = l;
+  red[1][threadIdx.x] = z;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) {
+      red[0][threadIdx.x] += red[0][threadIdx.x + off];
+      red[1][threadIdx.x] += red[1][threadIdx.x + off];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    scalars[4] = red[0][0];
+    scalars[3] = tb ? red[1][0] : 0.0;
+    if (!isfinite(red[0][0])) atomicExch(err, GFNX_ERR_NUMERIC);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2113,6 +2250,7 @@ struct Kernels {
     a.emit_mode = getenv("GFNX_EMIT_MODE") ? atoi(getenv("GFNX_EMIT_MODE")) : 0;
     const int T = c.P.T;
     cudaMemsetAsync(f.tilectr, 0, sizeof(int32_t), c.stream);
+    cudaMemsetAsync(c.batch.counters, 0, 2 * sizeof(int32_t), c.stream);  // finish_counts
     cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)c.Bl * T, c.stream);
     cudaMemsetAsync(c.batch.nparents, 0, sizeof(uint16_t) * (size_t)c.Bl * T, c.stream);
     if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
@@ -2180,6 +2318,7 @@ struct Kernels {
     ta.phase = c.phase;
     const int grid = f.num_sms;
     if (!f.fused) {  // weights changed since the rollout: recompute the forward over the rows
+      ensure_row0(c);
       k_linear_rows<<<(std::max(c.Bl, kTile) + 255) / 256, 256, 0, c.stream>>>(
           c.batch.lengths, c.batch.row0, c.Bl, c.P.T, c.batch.counters, f.frow_bt, f.bt_row, f.tilectr);
       c.launches++;
@@ -2225,9 +2364,11 @@ struct Kernels {
     la.scalars = c.d_scalars;
     {
       ProfScope ps(c, "k_fast_loss");
-      k_fast_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
+      if (c.train.objective == GFNX_OBJ_SUBTB) k_fast_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
+      else k_fast_loss_warp<<<f.loss_wblocks, 256, 0, c.stream>>>(la);
     }
-    k_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars,
+    k_loss_finalize<<<1, 256, 0, c.stream>>>(f.lpart, c.train.objective == GFNX_OBJ_SUBTB ? f.loss_blocks : f.loss_wblocks,
+                                              c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
     int smem = bwd_smem_bytes<H, NH>();
     set_smem_once(k_fast_bwd<Env, H, NH>, smem);
@@ -2285,6 +2426,8 @@ bool lockstep(const Ctx& c) { return c.env.kind == GFNX_ENV_BITSEQ || c.env.kind
 
 }  // namespace
 
+bool fast_rollout_counts(const Ctx& c) { return !lockstep(c); }
+
 void fast_init(Ctx& c) {
   if (lockstep(c)) {
     std::string why;
@@ -2311,6 +2454,7 @@ void fast_init(Ctx& c) {
   const int64_t slots = f->max_tiles * kTile;
   f->rs = (f->A + 3 + 3) & ~3;  // probs[A], lpa, lps, flow, padded to 16 bytes
   f->loss_blocks = (c.Bl + 255) / 256;
+  f->loss_wblocks = (c.Bl + 7) / 8;
   const size_t img = (size_t)f->max_tiles * kTile * H * 2;
   cuda_check(cudaMalloc(&f->w1, sizeof(__nv_bfloat16) * (size_t)f->O * H), "fast w1");
   cuda_check(cudaMalloc(&f->w2_fwd, sizeof(__nv_bfloat16) * H * H), "fast w2");
@@ -2337,7 +2481,7 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMemset(f->tilectr, 0, sizeof(int32_t)), "fast rows");
   cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
   cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
-  cuda_check(cudaMalloc(&f->lpart, sizeof(double) * 2 * f->loss_blocks), "fast lpart");
+  cuda_check(cudaMalloc(&f->lpart, sizeof(double) * 2 * std::max(f->loss_blocks, f->loss_wblocks)), "fast lpart");
   cuda_check(cudaMalloc(&f->work, sizeof(int32_t)), "fast work");
   std::vector<double> lp(T + 1);
   for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);

@@ -1,4 +1,4 @@
-timeout 900 python -m pytest tests/test_device_fast.py tests/test_ts_mma.py -x -q > gpurun_out/quick_tests.log 2>&1
+timeout 900 python -m pytest tests/test_device_fast.py tests/test_ts_mma.py tests/test_device_check.py -x -q > gpurun_out/quick_tests.log 2>&1
 timeout 300 python bench.py --steps 20 --no-cpu --secondary "dag_mdb_b8192,hypergrid_tb_b16" > gpurun_out/bench2.log 2>&1
 python profiles/rollout_phases.py > gpurun_out/phases_hg2.json 2>&1; cat gpurun_out/phases_hg2.json
 python -c "
