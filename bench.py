@@ -398,7 +398,7 @@ def main():
                     "unit": "GB/s", "frac": fb}
         roof["peak_source"] = peak_kind
         roof["share_of_step"] = dom_ms[0] / ms if ms else None
-        tr_k = (traffic or {}).get(dom)
+        tr_k = (traffic or {}).get(dom, (traffic or {}).get(dom + "_ts"))  # H = 256: k_fast_rollout_ts
         roof["traffic"] = tr_k
         roof["algorithmic_per_launch"] = {"flops": fl / per if per else None,
                                           "bytes": by / per if per else None}
