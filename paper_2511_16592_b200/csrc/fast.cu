@@ -253,6 +253,27 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 //       step the env, record, and refill finished slots from the global work counter.
 
 
+// one 128-byte row line (64 bf16 units = 16 packed words per 32 B pair... 32 words) of a
+// 128B-swizzled tile image, row `prow`: logical 16-byte chunk l lands at chunk l ^ (prow & 7);
+// stored as four 32-byte st.global.v8 (chunk pairs stay adjacent under the XOR)
+GFNX_DEV void st_line_sw128(uint8_t* line, int prow, const uint32_t (&r)[32]) {
+  const int x = prow & 7;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int p = (2 * m) ^ x;  // physical chunk of logical chunk 2m
+    const uint32_t* lo = r + 8 * m;      // logical chunk 2m (words 0..3) and 2m+1 (words 4..7)
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (x & 1) ? lo[4 + i] : lo[i];
+      v[4 + i] = (x & 1) ? lo[i] : lo[4 + i];
+    }
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(line + (p & ~1) * 16), "r"(v[0]),
+                 "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+  }
+}
+
 // row counts of a fused rollout (what k_row_scan derives from the lengths otherwise):
 // counters[0] = sum L, [1] = sum max(L - 1, 0), then the last CTA publishes [4], [5] and the
 // int64 running totals [8..9]; counters[12] is the CTA ticket
@@ -858,7 +879,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     row_t[row] = 0;
     set_features(s);
   }
-  long long ph[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+  long long ph[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0}, tprev = clock64();
+  auto sub = [&](int k, long long& t) {  // sub-phases of the sampling step (thread 0)
+    if (a.phase && tid == 0) {
+      const long long tn = clock64();
+      ph[k] += tn - t;
+      t = tn;
+    }
+  };
   auto mark = [&](int k) {
     if (a.phase && tid == 0) {
       const long long tnow = clock64();
@@ -878,10 +906,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         const int prow = gs & (kTile - 1);
         uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 +
                        ((c0 >> 6) + j) * (kTile * 128) + prow * 128;
-#pragma unroll
-        for (int l = 0; l < 8; ++l)
-          *reinterpret_cast<uint4*>(dst + ((l ^ (prow & 7)) * 16)) =
-              make_uint4(r[4 * l], r[4 * l + 1], r[4 * l + 2], r[4 * l + 3]);
+        st_line_sw128(dst, prow, r);
       }
     }
   };
@@ -1000,7 +1025,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       mma_tk<NH, H>(tmem + TH, tmem + TA2, whimg, false);
       umma_commit(&mbar);
     }
-    emit(a.h2, TA2, my_valid, gslot);
     mma_join();
     mark(4);
     float logit[NH];
@@ -1018,7 +1042,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       float lgs[SA], ex[SA], hi, z, rz;
 #pragma unroll
       for (int c = 0; c < SA; ++c) lgs[c] = logit[c];
+      long long tsub = ts0;
       const int act = sample_row<Env, SA>(P, s, lgs, A, a.eps, row_u[row], inv_legal, &bad, ex, hi, z, rz);
+      sub(9, tsub);
       if (act < 0) {
         active = false;
         a.frow_bt[gslot] = -1;
@@ -1047,47 +1073,72 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
           bad = true;
           active = false;
         }
+        sub(10, tsub);
         set_features(s);
+        sub(11, tsub);
         row_b[row] = active ? b : -1;
         row_t[row] = tstep;
       }
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
-    if (half == 1) {  // idle half while the row samples: raw head outputs + ReLU masks of h1, h2
+    if (half == 1) {  // idle half while the row samples: raw head outputs, h2 row, ReLU masks
       if (my_valid && a.emit_mode != 1) {
         float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
 #pragma unroll
         for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
       }
+      // ReLU mask of h1 (packed in TA) and the full h2 row (packed in TA2): emission + mask
+      uint32_t mw[H / 32];
 #pragma unroll 1
-      for (int m = 0; m < 2; ++m) {
-        uint32_t mw[H / 32];
+      for (int q = 0; q < H / 64; ++q) {  // 32 packed columns = 64 units per load
+        uint32_t r[32];
+        tmem_ld32(lane_base + TA + 32 * q, r);
+        tmem_wait_ld();
+        uint32_t lo[16], hi[16];
 #pragma unroll
-        for (int q = 0; q < H / 64; ++q) {  // 32 packed columns = 64 units per load
-          uint32_t r[32];
-          tmem_ld32(lane_base + (m ? TA2 : TA) + 32 * q, r);
-          tmem_wait_ld();
-          uint32_t lo[16], hi[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            lo[i] = r[i];
-            hi[i] = r[16 + i];
-          }
-          mw[2 * q] = relu_mask16(lo);
-          mw[2 * q + 1] = relu_mask16(hi);
+        for (int i = 0; i < 16; ++i) {
+          lo[i] = r[i];
+          hi[i] = r[16 + i];
         }
+        mw[2 * q] = relu_mask16(lo);
+        mw[2 * q + 1] = relu_mask16(hi);
+      }
+      if (my_valid && a.emit_mode != 1) {
+        uint4* dst = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
+#pragma unroll
+        for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
+      }
+      const int prow = gslot & (kTile - 1);
+#pragma unroll 1
+      for (int q = 0; q < H / 64; ++q) {  // 64-unit block q of h2
+        uint32_t r[32];
+        tmem_ld32(lane_base + TA2 + 32 * q, r);
+        tmem_wait_ld();
+        uint32_t lo[16], hi[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          lo[i] = r[i];
+          hi[i] = r[16 + i];
+        }
+        mw[2 * q] = relu_mask16(lo);
+        mw[2 * q + 1] = relu_mask16(hi);
         if (my_valid && a.emit_mode != 1) {
-          uint4* dst = reinterpret_cast<uint4*>((m ? a.mask2 : a.mask1) + (size_t)gslot * (H / 32));
-#pragma unroll
-          for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
+          uint8_t* dst = reinterpret_cast<uint8_t*>(a.h2) + (size_t)(gslot >> 7) * kTile * H * 2 + q * (kTile * 128) +
+                         prow * 128;
+          st_line_sw128(dst, prow, r);
         }
+      }
+      if (my_valid && a.emit_mode != 1) {
+        uint4* dst = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
+#pragma unroll
+        for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
       }
     }
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
     mark(5);
   }
   if (a.phase && tid == 0)
-    for (int k = 0; k < 9; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)ph[k]);
+    for (int k = 0; k < 12; ++k) atomicAdd((unsigned long long*)a.phase + (k < 9 ? k : k + 3), (unsigned long long)ph[k]);
   if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
   {  // unused emission rows: rows [fill, 128) of `cur` and the whole pre-claimed tile
     const int nxt = s_next;

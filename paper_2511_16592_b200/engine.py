@@ -263,7 +263,7 @@ class Trainer:
 
     PHASES = ("loop_barrier", "layer1", "hidden_mma", "hidden_epilogue", "head_mma", "sample_step",
               "tile_steps", "active_slot_steps", "sample_step_max", "wgrad_pass_a", "wgrad_pass_b",
-              "wgrad_pass_c")
+              "wgrad_pass_c", "sample_sampler", "sample_envstep", "sample_features")
 
     def phase_timers(self, mode: int):
         """Rollout phase clocks (diagnostic): 1 enable, 0 disable, 2 read + clear -> dict."""
