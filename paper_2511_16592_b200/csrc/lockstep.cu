@@ -57,6 +57,15 @@ struct Lock<BitseqEnv> {  // k = 8 (256-word slots), <= 32 slots
     const int tw = (P.bs_slots + 3) / 4;
     return ((w[tw] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
   }
+  // the state words legality depends on, cached in registers by the GEMM epilogues
+  static constexpr int kLW = 1;
+  GFNX_DEV static void load_lw(const EnvParams& P, const uint32_t* w, uint32_t (&lw)[kLW]) {
+    lw[0] = w[(P.bs_slots + 3) / 4];
+  }
+  GFNX_DEV static uint32_t legal32c(const EnvParams& P, const uint32_t (&lw)[kLW], int c0) {
+    if (c0 >= P.A) return 0u;
+    return ((lw[0] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
+  }
   // features with index in [f0, f0 + 256): put(f - f0, value); `part` of 4 splits the work
   template <class F>
   GFNX_DEV static void block_features(const EnvParams& P, const uint32_t* w, int f0, int part, F&& put) {
@@ -79,6 +88,26 @@ struct Lock<IsingEnv> {
     if (c0 >= P.A) return 0u;
     const int site0 = c0 >> 1;  // 16 sites, inside one assigned-word
     uint32_t x = ~(w[site0 >> 5] >> (site0 & 31)) & 0xffffu;
+    x = (x | (x << 8)) & 0x00FF00FFu;
+    x = (x | (x << 4)) & 0x0F0F0F0Fu;
+    x = (x | (x << 2)) & 0x33333333u;
+    x = (x | (x << 1)) & 0x55555555u;
+    x |= x << 1;
+    const int left = P.A - c0;
+    return left >= 32 ? x : (x & ((1u << left) - 1u));
+  }
+  static constexpr int kLW = 8;  // assigned-site words (<= 256 sites)
+  GFNX_DEV static void load_lw(const EnvParams& P, const uint32_t* w, uint32_t (&lw)[kLW]) {
+#pragma unroll
+    for (int k = 0; k < kLW; ++k) lw[k] = k < P.SW / 2 ? w[k] : 0u;
+  }
+  GFNX_DEV static uint32_t legal32c(const EnvParams& P, const uint32_t (&lw)[kLW], int c0) {
+    if (c0 >= P.A) return 0u;
+    const int site0 = c0 >> 1, wi = site0 >> 5;
+    uint32_t word = lw[0];
+#pragma unroll
+    for (int k = 1; k < kLW; ++k) word = wi == k ? lw[k] : word;
+    uint32_t x = ~(word >> (site0 & 31)) & 0xffffu;
     x = (x | (x << 8)) & 0x00FF00FFu;
     x = (x | (x << 4)) & 0x0F0F0F0Fu;
     x = (x | (x << 2)) & 0x33333333u;
@@ -228,29 +257,42 @@ struct LogEpi : EpiBase {
   };
   struct Local {
     float mx, s;
+    uint32_t lw[Lock<E>::kLW];
   };
-  static __device__ void begin(const Args&, int, int, int, int, Local& l) {
+  static __device__ void begin(const Args& e, int m, int, int row, int, Local& l) {
     l.mx = -INFINITY;
     l.s = 0.f;
+    const int b = m * kTile + row - e.row_base;
+    Lock<E>::load_lw(e.P, e.cur + (size_t)b * e.P.SW, l.lw);
   }
   static __device__ void apply(const Args& e, int m, int n, int row, int col0, float (&v)[32], float*, Local& l) {
     const int b = m * kTile + row - e.row_base;
     const int c = n * 256 + col0;
-    const uint32_t lm = Lock<E>::legal32(e.P, e.cur + (size_t)b * e.P.SW, c);
+    const uint32_t lm = Lock<E>::legal32c(e.P, l.lw, c);
     uint32_t pk[16];
     float cm = -INFINITY;
+    const float4* bb = reinterpret_cast<const float4*>(e.bf + c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 bq = __ldg(bb + i);
+      pk[2 * i] = pack_bf16x2(v[4 * i] + bq.x, v[4 * i + 1] + bq.y);
+      pk[2 * i + 1] = pack_bf16x2(v[4 * i + 2] + bq.z, v[4 * i + 3] + bq.w);
+    }
 #pragma unroll
     for (int i = 0; i < 16; ++i) {
-      pk[i] = pack_bf16x2(v[2 * i] + __ldg(e.bf + c + 2 * i), v[2 * i + 1] + __ldg(e.bf + c + 2 * i + 1));
       v[2 * i] = bf16_lo(pk[i]);
       v[2 * i + 1] = bf16_hi(pk[i]);
     }
 #pragma unroll
     for (int i = 0; i < 32; ++i)
       if ((lm >> i) & 1u) cm = fmaxf(cm, v[i]);
-    uint4* dst = reinterpret_cast<uint4*>(e.logits + (size_t)b * e.Ap + c);
+    uint8_t* dst = reinterpret_cast<uint8_t*>(e.logits + (size_t)b * e.Ap + c);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+    for (int q = 0; q < 2; ++q)
+      asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst + 32 * q), "r"(pk[8 * q]),
+                   "r"(pk[8 * q + 1]), "r"(pk[8 * q + 2]), "r"(pk[8 * q + 3]), "r"(pk[8 * q + 4]),
+                   "r"(pk[8 * q + 5]), "r"(pk[8 * q + 6]), "r"(pk[8 * q + 7])
+                   : "memory");
     if (lm == 0u) return;
     const float nm = fmaxf(l.mx, cm);
     float s = 0.f;
@@ -508,6 +550,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
   struct Local {
     float lse, g;
     int act;
+    uint32_t lw[Lock<E>::kLW];
   };
   static __device__ void begin(const Args& e, int m, int, int row, int, Local& l) {
     const size_t r = (size_t)m * kTile + row;
@@ -515,6 +558,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     l.lse = e.rowbuf[2 * r + 1];
     l.g = e.coef[r];
     l.act = e.actions[(size_t)b * e.T + t];
+    Lock<E>::load_lw(e.P, e.stst + r * e.P.SW, l.lw);
   }
   static __device__ void finish(const Args& e, int m, int n, const float* scratch) {
     const int c = threadIdx.x - 128;  // 256 epilogue threads, one output column each
@@ -525,11 +569,21 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
                                Local& l) {
     const size_t r = (size_t)m * kTile + row;
     const int c0 = n * 256 + col0;
-    const uint32_t lm = Lock<E>::legal32(e.P, e.stst + r * e.P.SW, c0);
+    const uint32_t lm = Lock<E>::legal32c(e.P, l.lw, c0);
     uint32_t pk[16];
+    float bias[32];
+    const float4* bb = reinterpret_cast<const float4*>(e.bf + c0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float4 bq = __ldg(bb + i);
+      bias[4 * i] = bq.x;
+      bias[4 * i + 1] = bq.y;
+      bias[4 * i + 2] = bq.z;
+      bias[4 * i + 3] = bq.w;
+    }
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const float x = __bfloat162float(__float2bfloat16(v[i] + __ldg(e.bf + c0 + i)));
+      const float x = __bfloat162float(__float2bfloat16(v[i] + bias[i]));
       float d = ((lm >> i) & 1u) ? -l.g * __expf(x - l.lse) : 0.f;
       if (c0 + i == l.act) d += l.g;
       v[i] = d;
