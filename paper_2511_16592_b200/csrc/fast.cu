@@ -253,6 +253,14 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
 //       step the env, record, and refill finished slots from the global work counter.
 
 
+// 8 consecutive fp32 words (32-byte aligned) in one st.global.v8; zeros when !keep
+GFNX_DEV void st_v8(float* dst, const uint32_t* r, bool keep) {
+  const uint32_t m = keep ? 0xffffffffu : 0u;
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0] & m), "r"(r[1] & m),
+               "r"(r[2] & m), "r"(r[3] & m), "r"(r[4] & m), "r"(r[5] & m), "r"(r[6] & m), "r"(r[7] & m)
+               : "memory");
+}
+
 // one 128-byte row line (64 bf16 units = 16 packed words per 32 B pair... 32 words) of a
 // 128B-swizzled tile image, row `prow`: logical 16-byte chunk l lands at chunk l ^ (prow & 7);
 // stored as four 32-byte st.global.v8 (chunk pairs stay adjacent under the XOR)
@@ -1183,6 +1191,7 @@ struct TrainArgs {
   float* coef;
   float* wpart;
   int64_t n_params;
+  int64_t pstride;  // per-CTA partial slab stride (n_params rounded up to 8 floats: 32-byte stores)
   MlpLayout L;
   int objective;
   long long* phase;  // optional diagnostics: [9..11] wgrad pass clocks (thread 0, summed over CTAs)
@@ -1733,7 +1742,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   const int A = P.A;
   const int tiles = *a.tilectr;
   const int R = tiles * kTile;
-  float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
+  float* part = a.wpart + (size_t)blockIdx.x * a.pstride;
   float acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j (db1: k_fast_wgrad pass B)
   if ((int)blockIdx.x < tiles) {
     if (warp == 0) tmem_alloc<H>(&tbase);
@@ -1986,7 +1995,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   const int t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
   const int nu = t1 > t0 ? 2 * (t1 - t0) : 0;  // units per pass
   const int NQ = 3 * nu;
-  float* part = a.wpart + (size_t)blockIdx.x * a.n_params;
+  float* part = a.wpart + (size_t)blockIdx.x * a.pstride;
   const MlpLayout& L = a.L;
   constexpr int KH = H / 128;  // 128-feature M blocks of the h operands
   if (warp == 0) tmem_alloc<512>(&tbase);
@@ -2040,7 +2049,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
           tmem_wait_ld();
           float* dst = part + L.off_w[1] + (size_t)pr * H + q * 32;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dst[i] = any ? __uint_as_float(r32[i]) : 0.f;
+          for (int i = 0; i < 32; i += 8) st_v8(dst + i, r32 + i, any);
         }
       }
     } else if (p == 1) {
@@ -2051,7 +2060,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
         if (tid <= P.O) {
           float* dst = tid < P.O ? part + L.off_w[0] + (size_t)tid * H + q * 32 : part + L.off_b[0] + q * 32;
 #pragma unroll
-          for (int i = 0; i < 32; ++i) dst[i] = any ? __uint_as_float(r32[i]) : 0.f;
+          for (int i = 0; i < 32; i += 8) st_v8(dst + i, r32 + i, any);
         }
       }
     } else {
@@ -2172,11 +2181,11 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
 }
 
 // fixed-order reduction over CTAs (deterministic)
-__global__ void k_reduce(const float* __restrict__ wpart, int nparts, int64_t n, float* g) {
+__global__ void k_reduce(const float* __restrict__ wpart, int nparts, int64_t n, int64_t stride, float* g) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   float s = 0.f;
-  for (int c = 0; c < nparts; ++c) s += wpart[(size_t)c * n + e];
+  for (int c = 0; c < nparts; ++c) s += wpart[(size_t)c * stride + e];
   g[e] = s;
 }
 
@@ -2364,10 +2373,16 @@ struct Kernels {
     ta.coef = f.coef;
     ta.wpart = f.wpart;
     ta.n_params = c.L.n_params;
+    ta.pstride = (c.L.n_params + 7) & ~(int64_t)7;
     ta.L = c.L;
     ta.objective = c.train.objective;
     ta.phase = c.phase;
-    const int grid = f.num_sms;
+    // CTAs of the training kernels: one per SM, but never more than the row tiles can
+    // occupy (emission tiles <= Bl*T/128 + 2 per rollout CTA); small batches (config #1,
+    // B = 16) then write and reduce only a few partial gradient slabs
+    const int64_t tiles_max = ((int64_t)c.Bl * c.P.T + kTile - 1) / kTile +
+                              2 * std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
+    const int grid = (int)std::min<int64_t>(f.num_sms, tiles_max);
     if (!f.fused) {  // weights changed since the rollout: recompute the forward over the rows
       ensure_row0(c);
       k_linear_rows<<<(std::max(c.Bl, kTile) + 255) / 256, 256, 0, c.stream>>>(
@@ -2436,7 +2451,7 @@ struct Kernels {
     const int64_t n = c.L.n_params;
     {
       ProfScope ps(c, "k_reduce");
-      k_reduce<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(f.wpart, grid, n, c.g32);
+      k_reduce<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(f.wpart, grid, n, ta.pstride, c.g32);
     }
     c.launches += 5;
     (void)apply;
@@ -2530,8 +2545,9 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->tilectr, sizeof(int32_t)), "fast rows");
   cuda_check(cudaMalloc(&f->logits, sizeof(float) * (size_t)slots * f->NH), "fast logits");
   cuda_check(cudaMemset(f->tilectr, 0, sizeof(int32_t)), "fast rows");
-  cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
-  cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * c.L.n_params), "fast wpart");
+  const size_t pstride = (size_t)((c.L.n_params + 7) & ~(int64_t)7);
+  cuda_check(cudaMalloc(&f->wpart, sizeof(float) * (size_t)f->num_sms * pstride), "fast wpart");
+  cuda_check(cudaMemset(f->wpart, 0, sizeof(float) * (size_t)f->num_sms * pstride), "fast wpart");
   cuda_check(cudaMalloc(&f->lpart, sizeof(double) * 2 * std::max(f->loss_blocks, f->loss_wblocks)), "fast lpart");
   cuda_check(cudaMalloc(&f->work, sizeof(int32_t)), "fast work");
   std::vector<double> lp(T + 1);
