@@ -2184,9 +2184,15 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
 __global__ void k_reduce(const float* __restrict__ wpart, int nparts, int64_t n, int64_t stride, float* g) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
-  float s = 0.f;
-  for (int c = 0; c < nparts; ++c) s += wpart[(size_t)c * stride + e];
-  g[e] = s;
+  // four interleaved partial sums (fixed order: deterministic), combined in a fixed tree
+  float s4[4] = {0.f, 0.f, 0.f, 0.f};
+  int c = 0;
+  for (; c + 4 <= nparts; c += 4) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) s4[k] += wpart[(size_t)(c + k) * stride + e];
+  }
+  for (; c < nparts; ++c) s4[0] += wpart[(size_t)c * stride + e];
+  g[e] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
 }
 
 // ---------------------------------------------------------------------------
