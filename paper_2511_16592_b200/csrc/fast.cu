@@ -1694,9 +1694,21 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
                                 int32_t* err) {
   __shared__ double red[2][256];
   double l = 0.0, z = 0.0;
-  for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
-    l += lpart[2 * i];
-    z += lpart[2 * i + 1];
+  const double2* lp = reinterpret_cast<const double2*>(lpart);
+  int i = threadIdx.x;
+  for (; i + 7 * (int)blockDim.x < nblocks; i += 8 * blockDim.x) {  // 8 loads in flight
+    double2 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = lp[i + k * blockDim.x];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      l += v[k].x;
+      z += v[k].y;
+    }
+  }
+  for (; i < nblocks; i += blockDim.x) {
+    l += lp[i].x;
+    z += lp[i].y;
   }
   red[0][threadIdx.x] = l;
   red[1][threadIdx.x] = z;
