@@ -231,13 +231,16 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
   struct Local {};
   static __device__ void apply(const Args& e, int m, int, int row, int col0, float (&v)[32], float*, Local&) {
     uint32_t pk[16], mb = 0;
+    const float4* bb = reinterpret_cast<const float4*>(e.b + col0);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      pk[i] = pack_bf16x2(fmaxf(v[2 * i] + __ldg(e.b + col0 + 2 * i), 0.f),
-                          fmaxf(v[2 * i + 1] + __ldg(e.b + col0 + 2 * i + 1), 0.f));
-      mb |= (bf16_lo(pk[i]) > 0.f ? 1u : 0u) << (2 * i);
-      mb |= (bf16_hi(pk[i]) > 0.f ? 1u : 0u) << (2 * i + 1);
+    for (int i = 0; i < 8; ++i) {
+      const float4 q = __ldg(bb + i);
+      pk[2 * i] = pack_bf16x2(fmaxf(v[4 * i] + q.x, 0.f), fmaxf(v[4 * i + 1] + q.y, 0.f));
+      pk[2 * i + 1] = pack_bf16x2(fmaxf(v[4 * i + 2] + q.z, 0.f), fmaxf(v[4 * i + 3] + q.w, 0.f));
     }
+#pragma unroll
+    for (int i = 0; i < 16; ++i)  // bit 2i / 2i+1 <-> columns 2i / 2i+1 (values >= 0: nonzero = active)
+      mb |= (((pk[i] & 0x7FFFu) + 0x7FFFu) >> 15 & 1u) << (2 * i) | (((pk[i] & 0x7FFF0000u) + 0x7FFF0000u) >> 31) << (2 * i + 1);
     st_row32(e.h + (size_t)m * (kTile * kH * 2), row, col0, pk);
     const size_t r = (size_t)m * kTile + row;
     *reinterpret_cast<uint32_t*>(e.mask + r * (kH / 8) + col0 / 8) = mb;
