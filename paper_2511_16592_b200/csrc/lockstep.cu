@@ -928,6 +928,420 @@ EmitArgs emit_args(Ctx& c) {
   return a;
 }
 
+// ---------------------------------------------------------------------------
+// k_ls_persist: the whole lockstep rollout (all T steps) in one persistent kernel, for
+// heads that fit one 256-column MMA (Ap <= 256: Ising, A = 2D). CTA k owns the 128-row
+// trajectory tiles k and k + gridDim.x (<= 2 per CTA); per step and tile:
+//   layer 1    incremental fp32 pre-activation (global, L2-resident) from the two
+//              features the last action changed -> ReLU -> packed bf16 A operand in TMEM
+//   layers 2.. tcgen05.mma with A from TMEM ("TS" form) against the layer's weight image,
+//              streamed into shared memory once per step and shared by both tiles
+//   head       same, logits in the accumulator; the row's two threads run the reference
+//              eps-uniform mixture + categorical (rng.cpp:87-100) over their 128 columns
+//              with the fp64 running sum carried from the first half to the second
+// Every output of the per-step pipeline is produced the same way (activation images +
+// ReLU masks of every layer, log pi(a)/lse record, states, actions), so training is shared.
+constexpr int kPersistMaxTiles = 2;
+
+struct PersistArgs {
+  EnvParams P;
+  Key key;
+  double eps;
+  int b0, Bl, T, NL, A, tilesB;
+  const __nv_bfloat16* w1;    // [O][H]
+  const float* h1init;        // [H]
+  float* preact;              // [Bl][H]
+  const uint8_t* wimg[kMaxNL + 1];  // [1..NL-1] hidden images, [NL] head image (128 KB each)
+  const float* bias[kMaxNL];  // [l] bias of layer l (l = 1..NL-1)
+  const float* bfp;           // head bias padded
+  uint8_t* h[kMaxNL];
+  uint8_t* mask[kMaxNL];
+  uint32_t* cur;
+  uint32_t* stst;
+  int32_t* last_act;
+  float* rowbuf;
+  DeviceBatch batch;
+};
+
+// ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
+GFNX_DEV uint32_t relu_mask32_seq(const uint32_t (&pk)[16]) {
+  uint32_t mb = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    mb |= (((pk[i] & 0x7FFFu) + 0x7FFFu) >> 15 & 1u) << (2 * i) |
+          (((pk[i] & 0x7FFF0000u) + 0x7FFF0000u) >> 31) << (2 * i + 1);
+  return mb;
+}
+
+GFNX_DEV void st_v8_words(uint8_t* dst, const uint32_t* r) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+               "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// one 128-byte line of a 128B-swizzled tile image (logical chunk l at l ^ (row & 7))
+GFNX_DEV void st_line_sw(uint8_t* line, int row, const uint32_t (&r)[32]) {
+  const int x = row & 7;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int p = (2 * m) ^ x;
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (x & 1) ? r[8 * m + 4 + i] : r[8 * m + i];
+      v[4 + i] = (x & 1) ? r[8 * m + i] : r[8 * m + 4 + i];
+    }
+    st_v8_words(line + (p & ~1) * 16, v);
+  }
+}
+
+template <class E>
+__global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* wbuf = align1024(smem_raw);  // one 256 x 256 weight image (128 KB)
+  __shared__ uint64_t mbar, wbar;
+  __shared__ uint32_t tbase;
+  __shared__ float h1i[kH];
+  __shared__ Key skeys[256];
+  __shared__ double row_u[kPersistMaxTiles][kTile];
+  __shared__ float xf[kTile][2];
+  __shared__ int xi[kTile][2];
+  __shared__ double xd[kTile];
+  __shared__ int xlast[kTile][2];
+  const EnvParams& P = a.P;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int quarter = warp & 3, half = warp >> 2;
+  const int row = quarter * 32 + lane, c0 = half * 128;
+  const int ntile = (a.tilesB - (int)blockIdx.x + gridDim.x - 1) / gridDim.x;  // 1 or 2
+  if (warp == 0) tmem_alloc<512>(&tbase);
+  if (tid == 0) {
+    mbar_init(&mbar, 1);
+    mbar_init(&wbar, 1);
+    fence_mbar_init();
+  }
+  for (int j = tid; j < kH; j += 256) h1i[j] = a.h1init[j];
+  for (int t = tid; t < a.T && t < 256; t += 256) skeys[t] = fold_in(a.key, (uint64_t)t);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tbase;
+  const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
+  uint32_t mph = 0, wph = 0;
+  auto load_w = [&](int l) {  // thread 0: weight image l into wbuf (previous users complete)
+    mbar_arrive_expect_tx(&wbar, kH * kH * 2);
+    bulk_g2s_big(wbuf, a.wimg[l], kH * kH * 2, &wbar);
+  };
+  auto mma_issue = [&](uint32_t d, uint32_t ta) {
+    if (tid == 0) {
+      tc_fence_after();
+      mma_tk<kH, kH>(d, ta, wbuf, false);
+      umma_commit(&mbar);
+    }
+  };
+  auto mma_wait = [&]() {
+    if (tid == 0) mbar_wait(&mbar, mph);
+    mph ^= 1;
+    __syncthreads();
+    tc_fence_after();
+  };
+  auto publish = [&]() {
+    tmem_wait_st();
+    tc_fence_before();
+    __syncthreads();
+  };
+  if (tid == 0) load_w(1);
+  const int T = a.T, Bl = a.Bl;
+  for (int t = 0; t < T; ++t) {
+    // ---- layer 1 for every tile of this CTA
+    for (int j = 0; j < ntile; ++j) {
+      const int tile = blockIdx.x + j * gridDim.x;
+      const int b = tile * kTile + row;
+      float* pre = a.preact + (size_t)b * kH + c0;
+      const size_t r = (size_t)t * Bl + b;
+      int f2[2] = {0, 0};
+      float cf[2] = {0.f, 0.f};
+      int nf = 0;
+      if (t > 0) {
+        typename E::State dummy;
+        E::delta_features(P, dummy, a.last_act[b], [&](int f, float coef) {
+          if (nf < 2) {
+            f2[nf] = f;
+            cf[nf] = coef;
+          }
+          ++nf;
+        });
+      }
+      uint32_t mw[4];
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {
+        const int col = q * 32;
+        float v[32];
+        if (t == 0) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = h1i[c0 + col + i];
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 p4 = *reinterpret_cast<const float4*>(pre + col + 4 * i);
+            v[4 * i] = p4.x;
+            v[4 * i + 1] = p4.y;
+            v[4 * i + 2] = p4.z;
+            v[4 * i + 3] = p4.w;
+          }
+#pragma unroll
+          for (int d = 0; d < 2; ++d)
+            if (d < nf) {
+              const uint4* wr = reinterpret_cast<const uint4*>(a.w1 + (size_t)f2[d] * kH + c0 + col);
+#pragma unroll
+              for (int c = 0; c < 4; ++c) {
+                const uint4 w4 = __ldg(wr + c);
+                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  v[8 * c + 2 * e] += cf[d] * bf16_lo(wv[e]);
+                  v[8 * c + 2 * e + 1] += cf[d] * bf16_hi(wv[e]);
+                }
+              }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(pre + col + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f));
+        mw[q] = relu_mask32_seq(pk);
+        tmem_st16(lane_base + kH + 128 * j + ((c0 + col) >> 1), pk);
+      }
+      *reinterpret_cast<uint4*>(a.mask[0] + r * (kH / 8) + half * 16) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+    }
+    publish();
+    // layer-1 images straight from TMEM (both halves, own 128 columns = two 64-col blocks)
+    for (int j = 0; j < ntile; ++j) {
+      const int tile = blockIdx.x + j * gridDim.x;
+      const size_t m = (size_t)t * a.tilesB + tile;
+#pragma unroll 1
+      for (int blk = 0; blk < 2; ++blk) {
+        uint32_t w32[32];
+        tmem_ld32(lane_base + kH + 128 * j + (c0 >> 1) + 32 * blk, w32);
+        tmem_wait_ld();
+        st_line_sw(a.h[0] + m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
+      }
+    }
+    // ---- hidden layers 2..NL: MMA per tile (A from TMEM), epilogue back into the same columns
+    for (int l = 1; l < a.NL; ++l) {
+      if (tid == 0) mbar_wait(&wbar, wph);
+      wph ^= 1;
+      for (int j = 0; j < ntile; ++j) {
+        const int tile = blockIdx.x + j * gridDim.x;
+        const int b = tile * kTile + row;
+        const size_t r = (size_t)t * Bl + b;
+        const size_t m = (size_t)t * a.tilesB + tile;
+        mma_issue(tmem, tmem + kH + 128 * j);
+        if (half == 1 && l == 1 && j < kPersistMaxTiles)  // the row's uniform while the MMA runs
+          row_u[j][row] = uniform_scalar(fold_in(skeys[t], (uint64_t)(a.b0 + b)));
+        mma_wait();
+        if (j == ntile - 1 && tid == 0) load_w(l + 1 < a.NL ? l + 1 : a.NL);  // wbuf free now
+        uint32_t mw[4];
+        const float* bl = a.bias[l];
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {
+          const int col = c0 + q * 32;
+          uint32_t rr[32];
+          tmem_ld32(lane_base + col, rr);
+          tmem_wait_ld();
+          uint32_t pk[16];
+          const float4* bb = reinterpret_cast<const float4*>(bl + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 bq = __ldg(bb + i);
+            pk[2 * i] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i]) + bq.x, 0.f),
+                                    fmaxf(__uint_as_float(rr[4 * i + 1]) + bq.y, 0.f));
+            pk[2 * i + 1] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i + 2]) + bq.z, 0.f),
+                                        fmaxf(__uint_as_float(rr[4 * i + 3]) + bq.w, 0.f));
+          }
+          mw[q] = relu_mask32_seq(pk);
+          tmem_st16(lane_base + kH + 128 * j + (col >> 1), pk);
+        }
+        *reinterpret_cast<uint4*>(a.mask[l] + r * (kH / 8) + half * 16) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        tmem_wait_st();
+#pragma unroll 1
+        for (int blk = 0; blk < 2; ++blk) {
+          uint32_t w32[32];
+          tmem_ld32(lane_base + kH + 128 * j + (c0 >> 1) + 32 * blk, w32);
+          tmem_wait_ld();
+          st_line_sw(a.h[l] + m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
+        }
+        publish();
+      }
+    }
+    // ---- head + sampling per tile. The row's two threads own 128 logit columns each.
+    //   P1  fp32 logits + bias -> bf16-rounded x (the values the training pass recomputes),
+    //       legality words, max over legal
+    //   P2  e = exp(x - hi) over legal, bf16 into the tile's consumed A columns,
+    //       z; then the mixture w = kz e + eps/legal summed in fp64 in column order:
+    //       first half, carry, second half (the reference's sequential running sum)
+    //   P3  search for the first column whose running sum exceeds u * total
+    if (tid == 0) mbar_wait(&wbar, wph);
+    wph ^= 1;
+    for (int j = 0; j < ntile; ++j) {
+      const int tile = blockIdx.x + j * gridDim.x;
+      const int b = tile * kTile + row;
+      const size_t r = (size_t)t * Bl + b;
+      mma_issue(tmem, tmem + kH + 128 * j);
+      const uint32_t* w = a.cur + (size_t)b * P.SW;
+      uint32_t lw[Lock<E>::kLW];
+      Lock<E>::load_lw(P, w, lw);
+      mma_wait();
+      if (j == ntile - 1 && tid == 0) load_w(1);  // next step's first hidden layer
+      uint32_t lmw[4];
+      float hi = -INFINITY;
+      int lcount = 0;
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {  // P1
+        const int col = c0 + q * 32;
+        uint32_t rr[32];
+        tmem_ld32(lane_base + col, rr);
+        tmem_wait_ld();
+        const uint32_t lm = Lock<E>::legal32c(P, lw, col);
+        lmw[q] = lm;
+        lcount += __popc(lm);
+        const float4* bb = reinterpret_cast<const float4*>(a.bfp + col);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 bq = __ldg(bb + i);
+          const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = 4 * i + e;
+            const float x = __bfloat162float(__float2bfloat16(__uint_as_float(rr[k]) + bv[e]));
+            rr[k] = __float_as_uint(x);
+            if ((lm >> k) & 1u) hi = fmaxf(hi, x);
+          }
+        }
+        tmem_st32(lane_base + col, rr);  // x (fp32 of the bf16 value) in place
+      }
+      xf[row][half] = hi;
+      xi[row][half] = lcount;
+      tmem_wait_st();
+      __syncthreads();
+      hi = fmaxf(xf[row][0], xf[row][1]);
+      const int legal = xi[row][0] + xi[row][1];
+      __syncthreads();
+      float zl = 0.f;
+      const uint32_t ta_e = lane_base + kH + 128 * j + (c0 >> 1);  // consumed A columns of this tile
+#pragma unroll 1
+      for (int q = 0; q < 4; ++q) {  // P2: e (bf16) into the tile's consumed A columns
+        const int col = c0 + q * 32;
+        uint32_t rr[32];
+        tmem_ld32(lane_base + col, rr);
+        tmem_wait_ld();
+        uint32_t pe[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const float e0 = ((lmw[q] >> (2 * k)) & 1u) ? __expf(__uint_as_float(rr[2 * k]) - hi) : 0.f;
+          const float e1 = ((lmw[q] >> (2 * k + 1)) & 1u) ? __expf(__uint_as_float(rr[2 * k + 1]) - hi) : 0.f;
+          zl += e0;
+          zl += e1;
+          pe[k] = pack_bf16x2(e0, e1);
+        }
+        tmem_st16(ta_e + 16 * q, pe);
+      }
+      xf[row][half] = zl;
+      tmem_wait_st();
+      __syncthreads();
+      const float z = xf[row][0] + xf[row][1];
+      const double u = legal > 0 ? a.eps / (double)legal : 0.0;
+      const double kz = (double)((float)(1.0 - a.eps) * __frcp_rn(z));
+      // fp64 running sum over this thread's legal columns from `acc`; optional search
+      auto run = [&](double acc, double x_target, int& pick, int& lastc) {
+        pick = -1;
+        lastc = -1;
+#pragma unroll 1
+        for (int h2 = 0; h2 < 2; ++h2) {  // 32 packed words = 64 columns per load
+          uint32_t rr[32];
+          tmem_ld32(ta_e + 32 * h2, rr);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 64; ++k) {
+            const int cc = 64 * h2 + k;  // column offset within this thread's half
+            if ((lmw[cc >> 5] >> (cc & 31)) & 1u) {
+              const float e = (k & 1) ? bf16_hi(rr[k >> 1]) : bf16_lo(rr[k >> 1]);
+              acc += kz * (double)e + u;
+              if (pick < 0 && x_target < acc) pick = c0 + cc;
+              lastc = c0 + cc;
+            }
+          }
+        }
+        return acc;
+      };
+      int pk_, lc_;
+      if (half == 0) xd[row] = run(0.0, -1.0, pk_, lc_);  // first half's total
+      __syncthreads();
+      const double carry = xd[row];
+      __syncthreads();
+      if (half == 1) xd[row] = run(carry, -1.0, pk_, lc_);  // the row total
+      __syncthreads();
+      const double xt = row_u[j][row] * xd[row];
+      int pick, lastc;
+      run(half == 0 ? 0.0 : carry, xt, pick, lastc);
+      xi[row][half] = pick;
+      xlast[row][half] = lastc;
+      __syncthreads();
+      const int p0 = xi[row][0], p1 = xi[row][1];
+      // rounding fallback: the last legal column (rng.cpp:97-99)
+      const int act = p0 >= 0 ? p0 : (p1 >= 0 ? p1 : (xlast[row][1] >= 0 ? xlast[row][1] : xlast[row][0]));
+      const float lse = hi + __logf(z);
+      {  // log pi(a) = x_a - lse, x_a (bf16-rounded logit) still in the accumulator columns
+        float xa = 0.f;
+        const int qa = act >= c0 && act < c0 + 128 ? ((act - c0) >> 5) : -1;
+#pragma unroll 1
+        for (int q = 0; q < 4; ++q) {  // warp-collective loads; the owner picks its column
+          uint32_t rr[32];
+          tmem_ld32(lane_base + c0 + q * 32, rr);
+          tmem_wait_ld();
+          if (q == qa) {
+#pragma unroll
+            for (int k = 0; k < 32; ++k)
+              if (c0 + q * 32 + k == act) xa = __uint_as_float(rr[k]);
+          }
+        }
+        if (qa >= 0) {
+          a.rowbuf[2 * r] = xa - lse;
+          a.rowbuf[2 * r + 1] = lse;
+        }
+      }
+      tc_fence_before();
+      if (half == 0) {  // record + env step
+        const size_t bt = (size_t)b * T + t;
+        if (act < 0 || legal == 0 || !(z > 0.f)) {
+          atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
+        } else {
+          for (int i = 0; i < P.SW; ++i) a.stst[r * P.SW + i] = w[i];
+          typename E::State s;
+          E::unpack(P, w, s);
+          const bool term = E::step(P, s, act);
+          E::pack(P, s, a.cur + (size_t)b * P.SW);
+          a.batch.actions[bt] = (int16_t)act;
+          a.batch.nparents[bt] = (uint16_t)E::num_parents(P, s);
+          a.last_act[b] = act;
+          if (term) {
+            a.batch.lengths[b] = t + 1;
+            a.batch.log_rewards[b] = E::log_reward(P, s);
+            E::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
+          }
+          if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
+        }
+      }
+      __syncthreads();
+    }
+  }
+  if (tid == 0) mbar_wait(&wbar, wph);  // the prefetched image has landed before exit
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
 template <class E>
 void rollout_impl(Ctx& c, Key key, double eps) {
   LsState& f = LS(c);
@@ -938,6 +1352,46 @@ void rollout_impl(Ctx& c, Key key, double eps) {
     k_ls_reset<<<(Bl * f.SW + 255) / 256, 256, 0, c.stream>>>(Bl * f.SW, f.cur);
     k_ls_h1init<E><<<1, kH, 0, c.stream>>>(c.P, f.w1, c.p32 + c.L.off_b[0], f.h1init);
     c.launches += 2;
+  }
+  // the whole rollout in one persistent kernel when the head fits one MMA and every CTA
+  // holds at most two trajectory tiles (GFNX_LS_STEPWISE=1 forces the per-step kernels)
+  const int grid = std::min(f.num_sms, f.tilesB);
+  if (f.NT == 1 && Bl % kTile == 0 && f.tilesB <= kPersistMaxTiles * grid && T <= 256 &&
+      !getenv("GFNX_LS_STEPWISE")) {
+    PersistArgs pa{};
+    pa.P = c.P;
+    pa.key = key;
+    pa.eps = eps;
+    pa.b0 = c.b0;
+    pa.Bl = Bl;
+    pa.T = T;
+    pa.NL = f.NL;
+    pa.A = f.A;
+    pa.tilesB = f.tilesB;
+    pa.w1 = f.w1;
+    pa.h1init = f.h1init;
+    pa.preact = f.preact;
+    for (int l = 1; l < f.NL; ++l) {
+      pa.wimg[l] = (const uint8_t*)f.wfw[l];
+      pa.bias[l] = c.p32 + c.L.off_b[l];
+    }
+    pa.wimg[f.NL] = (const uint8_t*)f.wff;
+    pa.bfp = f.bfp;
+    for (int l = 0; l < f.NL; ++l) {
+      pa.h[l] = (uint8_t*)f.h[l];
+      pa.mask[l] = f.mask[l];
+    }
+    pa.cur = f.cur;
+    pa.stst = f.stst;
+    pa.last_act = f.last_act;
+    pa.rowbuf = f.rowbuf;
+    pa.batch = c.batch;
+    const int smem = kH * kH * 2 + 1024;
+    set_smem_once(k_ls_persist<E>, smem);
+    ProfScope ps(c, "k_ls_persist");
+    k_ls_persist<E><<<grid, 256, smem, c.stream>>>(pa);
+    c.launches++;
+    return;
   }
   for (int t = 0; t < T; ++t) {
     {
