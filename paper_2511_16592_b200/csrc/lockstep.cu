@@ -961,6 +961,7 @@ struct PersistArgs {
   int32_t* last_act;
   float* rowbuf;
   DeviceBatch batch;
+  long long* phase;  // optional clocks (thread 0): [0] layer 1, [1] hidden layers, [2] head + sample
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
@@ -973,8 +974,10 @@ GFNX_DEV uint32_t relu_mask32_seq(const uint32_t (&pk)[16]) {
   return mb;
 }
 
+// (streaming store: evict-first in L2, so the activation images written once per step do
+// not push the per-row layer-1 state out of L2)
 GFNX_DEV void st_v8_words(uint8_t* dst, const uint32_t* r) {
-  asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+  asm volatile("st.global.cs.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(r[0]), "r"(r[1]), "r"(r[2]),
                "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
@@ -1008,6 +1011,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   __shared__ int xi[kTile][2];
   __shared__ double xd[kTile];
   __shared__ int xlast[kTile][2];
+  __shared__ int s_lact[kPersistMaxTiles][kTile];  // last action of each row (layer-1 delta)
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int quarter = warp & 3, half = warp >> 2;
@@ -1051,6 +1055,14 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   };
   if (tid == 0) load_w(1);
   const int T = a.T, Bl = a.Bl;
+  long long pc[3] = {0, 0, 0}, tclk = clock64();
+  auto pmark = [&](int k) {
+    if (a.phase && tid == 0) {
+      const long long tn = clock64();
+      pc[k] += tn - tclk;
+      tclk = tn;
+    }
+  };
   for (int t = 0; t < T; ++t) {
     // ---- layer 1 for every tile of this CTA
     for (int j = 0; j < ntile; ++j) {
@@ -1063,7 +1075,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       int nf = 0;
       if (t > 0) {
         typename E::State dummy;
-        E::delta_features(P, dummy, a.last_act[b], [&](int f, float coef) {
+        E::delta_features(P, dummy, s_lact[j][row], [&](int f, float coef) {
           if (nf < 2) {
             f2[nf] = f;
             cf[nf] = coef;
@@ -1071,39 +1083,52 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           ++nf;
         });
       }
-      uint32_t mw[4];
-#pragma unroll 1
-      for (int q = 0; q < 4; ++q) {
+      // 32-column chunks with the next chunk's pre-activation and W1 loads in flight
+      float pv[2][32];
+      uint4 wv[2][2][4];
+      auto load_chunk = [&](int q, float (&p32)[32], uint4 (&w8)[2][4]) {
         const int col = q * 32;
-        float v[32];
         if (t == 0) {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = h1i[c0 + col + i];
+          for (int i = 0; i < 32; ++i) p32[i] = h1i[c0 + col + i];
         } else {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 p4 = *reinterpret_cast<const float4*>(pre + col + 4 * i);
-            v[4 * i] = p4.x;
-            v[4 * i + 1] = p4.y;
-            v[4 * i + 2] = p4.z;
-            v[4 * i + 3] = p4.w;
+            p32[4 * i] = p4.x;
+            p32[4 * i + 1] = p4.y;
+            p32[4 * i + 2] = p4.z;
+            p32[4 * i + 3] = p4.w;
           }
-#pragma unroll
-          for (int d = 0; d < 2; ++d)
-            if (d < nf) {
-              const uint4* wr = reinterpret_cast<const uint4*>(a.w1 + (size_t)f2[d] * kH + c0 + col);
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                const uint4 w4 = __ldg(wr + c);
-                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  v[8 * c + 2 * e] += cf[d] * bf16_lo(wv[e]);
-                  v[8 * c + 2 * e + 1] += cf[d] * bf16_hi(wv[e]);
-                }
-              }
-            }
         }
+#pragma unroll
+        for (int d = 0; d < 2; ++d) {
+          const uint4* wr = reinterpret_cast<const uint4*>(a.w1 + (size_t)f2[d] * kH + c0 + col);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w8[d][c] = d < nf ? __ldg(wr + c) : make_uint4(0, 0, 0, 0);
+        }
+      };
+      uint32_t mw[4];
+      load_chunk(0, pv[0], wv[0]);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int col = q * 32;
+        if (q + 1 < 4) load_chunk(q + 1, pv[(q + 1) & 1], wv[(q + 1) & 1]);
+        float v[32];
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = pv[q & 1][i];
+#pragma unroll
+        for (int d = 0; d < 2; ++d)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint4 w4 = wv[q & 1][d][c];
+            const uint32_t wq[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              v[8 * c + 2 * e] += cf[d] * bf16_lo(wq[e]);
+              v[8 * c + 2 * e + 1] += cf[d] * bf16_hi(wq[e]);
+            }
+          }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
           *reinterpret_cast<float4*>(pre + col + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
@@ -1113,7 +1138,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         mw[q] = relu_mask32_seq(pk);
         tmem_st16(lane_base + kH + 128 * j + ((c0 + col) >> 1), pk);
       }
-      *reinterpret_cast<uint4*>(a.mask[0] + r * (kH / 8) + half * 16) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+      __stcs(reinterpret_cast<uint4*>(a.mask[0] + r * (kH / 8) + half * 16), make_uint4(mw[0], mw[1], mw[2], mw[3]));
     }
     publish();
     // layer-1 images straight from TMEM (both halves, own 128 columns = two 64-col blocks)
@@ -1128,6 +1153,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         st_line_sw(a.h[0] + m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
       }
     }
+    pmark(0);
     // ---- hidden layers 2..NL: MMA per tile (A from TMEM), epilogue back into the same columns
     for (int l = 1; l < a.NL; ++l) {
       if (tid == 0) mbar_wait(&wbar, wph);
@@ -1163,7 +1189,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           mw[q] = relu_mask32_seq(pk);
           tmem_st16(lane_base + kH + 128 * j + (col >> 1), pk);
         }
-        *reinterpret_cast<uint4*>(a.mask[l] + r * (kH / 8) + half * 16) = make_uint4(mw[0], mw[1], mw[2], mw[3]);
+        __stcs(reinterpret_cast<uint4*>(a.mask[l] + r * (kH / 8) + half * 16), make_uint4(mw[0], mw[1], mw[2], mw[3]));
         tmem_wait_st();
 #pragma unroll 1
         for (int blk = 0; blk < 2; ++blk) {
@@ -1175,6 +1201,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         publish();
       }
     }
+    pmark(1);
     // ---- head + sampling per tile. The row's two threads own 128 logit columns each.
     //   P1  fp32 logits + bias -> bf16-rounded x (the values the training pass recomputes),
     //       legality words, max over legal
@@ -1325,6 +1352,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           a.batch.actions[bt] = (int16_t)act;
           a.batch.nparents[bt] = (uint16_t)E::num_parents(P, s);
           a.last_act[b] = act;
+          s_lact[j][row] = act;
           if (term) {
             a.batch.lengths[b] = t + 1;
             a.batch.log_rewards[b] = E::log_reward(P, s);
@@ -1335,7 +1363,10 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       }
       __syncthreads();
     }
+    pmark(2);
   }
+  if (a.phase && tid == 0)
+    for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)pc[k]);
   if (tid == 0) mbar_wait(&wbar, wph);  // the prefetched image has landed before exit
   tc_fence_before();
   __syncthreads();
@@ -1386,6 +1417,7 @@ void rollout_impl(Ctx& c, Key key, double eps) {
     pa.last_act = f.last_act;
     pa.rowbuf = f.rowbuf;
     pa.batch = c.batch;
+    pa.phase = c.phase;
     const int smem = kH * kH * 2 + 1024;
     set_smem_once(k_ls_persist<E>, smem);
     ProfScope ps(c, "k_ls_persist");
