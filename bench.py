@@ -39,6 +39,7 @@ METRIC = "trajectories/sec (train iters/sec in config) — hypergrid 20^4 DB, B=
 UNIT = "trajectories/s"
 # secondary BASELINE configs measured after the headline (device-timed, resident inputs)
 SECONDARY = {
+    "hypergrid_subtb_b65536": dict(batch=65536, desc="hypergrid 20^4 SubTB (lambda 0.9), B=65536, MLP 2x256"),
     "bitseq_tb_b16384": dict(batch=16384, desc="bitseq n=120 k=8 NAR TB, MLP 2x256"),
     "ising_tb_b32768": dict(batch=32768, desc="Ising 10x10 TB, MLP 4x256"),
     "hypergrid_tb_b16": dict(batch=16, desc="hypergrid 20^4 TB, B=16, MLP 2x256"),
@@ -291,7 +292,7 @@ def main():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="trajectories per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--secondary", default="bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192",
+    ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()

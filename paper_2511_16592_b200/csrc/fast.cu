@@ -14,7 +14,7 @@
 //                   rows), layer-2 on tcgen05; stores bf16 activation tile images + per-row
 //                   head statistics (mlp_forward_tape nn.cpp:91-126, masked_log_softmax
 //                   tape.cpp:177-213)
-//   k_fast_loss     TB/DB/SubTB/MDB residuals and their analytic backward per trajectory
+//   k_fast_loss_warp TB/DB/SubTB/MDB residuals and their analytic backward, warp per trajectory
 //                   (objectives.cpp:94-226), deterministic block partials
 //   k_fast_bwd      head backward (SIMT), dgrad GEMM on tcgen05, ReLU masks, bias grads
 //   k_fast_wgrad    weight gradients as tcgen05 GEMMs whose K dimension is the row count:
@@ -1474,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_loss: one thread per trajectory
+// k_fast_loss_warp: residuals of every objective and their analytic backward
 
 struct LossArgs {
   DeviceBatch batch;
@@ -1490,121 +1490,21 @@ struct LossArgs {
   const double* scalars;
 };
 
-__global__ void k_fast_loss(LossArgs a) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  double loss = 0.0, dlogz = 0.0;
-  if (b < a.Bl) {
-    const int L = a.batch.lengths[b];
-    const int32_t* rows = a.bt_row + (size_t)b * a.T;
-    const uint16_t* np = a.batch.nparents + (size_t)b * a.T;
-    const double logr = a.batch.log_rewards[b];
-    const int* cnt = a.batch.counters;
-    double norm = (double)a.B_global;
-    if (a.objective == GFNX_OBJ_DB) norm = (double)cnt[4];
-    if (a.objective == GFNX_OBJ_MDB) norm = (double)cnt[5];
-    auto lpa = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A]; };
-    auto lps = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A + 1]; };
-    auto flw = [&](int t) { return (double)a.rowbuf[(size_t)rows[t] * a.rs + a.A + 2]; };
-    auto C = [&](int t) { return a.coef + (size_t)rows[t] * 4; };
-    for (int t = 0; t < L; ++t) {
-      float* c = C(t);
-      c[0] = c[1] = c[2] = 0.f;
-    }
-    if (a.objective == GFNX_OBJ_TB) {  // tb_loss objectives.cpp:120-142
-      const double w = 1.0 / norm;
-      double cum = 0.0;
-      for (int t = 0; t < L; ++t) cum += lpa(t) - a.neglog[np[t]];
-      const double res = cum + a.scalars[0] - logr;
-      loss = res * res * w;
-      const double g = 2.0 * res * w;
-      dlogz = g;
-      for (int t = 0; t < L; ++t) C(t)[0] = (float)g;
-    } else if (a.objective == GFNX_OBJ_DB) {  // transition_loss :94-118
-      double gprev = 0.0;
-      for (int t = 0; t < L; ++t) {
-        const double d = lpa(t) - a.neglog[np[t]];
-        const double f1 = t + 1 < L ? flw(t + 1) : logr;
-        const double res = flw(t) - f1 + d;
-        const double w = (t == L - 1 ? a.terminal_penalty : 1.0) / norm;
-        loss += res * res * w;
-        const double g = 2.0 * res * w;
-        C(t)[0] = (float)g;
-        C(t)[2] = (float)(g - gprev);
-        gprev = g;
-      }
-    } else if (a.objective == GFNX_OBJ_SUBTB) {  // subtb_loss :144-180
-      constexpr int kMaxT = 256;
-      double cum[kMaxT + 1], F[kMaxT + 1], gF[kMaxT + 1], gc[kMaxT + 1];
-      cum[0] = 0.0;
-      for (int t = 0; t < L; ++t) {
-        cum[t + 1] = cum[t] + (lpa(t) - a.neglog[np[t]]);
-        F[t] = flw(t);
-      }
-      F[L] = logr;
-      double nrm = 0.0;
-      for (int j = 0; j < L; ++j)
-        for (int k = j + 1; k <= L; ++k) nrm += a.lampow[k - j];
-      for (int k = 0; k <= L; ++k) gF[k] = gc[k] = 0.0;
-      for (int j = 0; j < L; ++j)
-        for (int k = j + 1; k <= L; ++k) {
-          const double w = a.lampow[k - j] / nrm / norm;
-          const double res = (F[j] - F[k]) + (cum[k] - cum[j]);
-          loss += res * res * w;
-          const double g = 2.0 * res * w;
-          gF[j] += g;
-          gF[k] -= g;
-          gc[k] += g;
-          gc[j] -= g;
-        }
-      double acc = 0.0;
-      for (int c = L; c >= 0; --c) {
-        if (c < L) {
-          C(c)[0] = (float)acc;
-          C(c)[2] = (float)gF[c];
-        }
-        acc += gc[c];
-      }
-    } else if (a.objective == GFNX_OBJ_MDB) {  // mdb_loss :186-226
-      const double w = 1.0 / norm;
-      for (int t = 0; t + 1 < L; ++t) {
-        const double res = lpa(t) + (lps(t + 1) - lps(t)) - a.neglog[np[t]] -
-                           a.batch.delta[(size_t)b * a.T + t];
-        loss += res * res * w;
-        const double g = 2.0 * res * w;
-        C(t)[0] += (float)g;
-        C(t + 1)[1] += (float)g;
-        C(t)[1] -= (float)g;
-      }
-    }
-  }
-  // deterministic block reduction
-  __shared__ double red[2][256];
-  red[0][threadIdx.x] = loss;
-  red[1][threadIdx.x] = dlogz;
-  __syncthreads();
-  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
-    if ((int)threadIdx.x < off) {
-      red[0][threadIdx.x] += red[0][threadIdx.x + off];
-      red[1][threadIdx.x] += red[1][threadIdx.x + off];
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    a.lpart[2 * blockIdx.x] = red[0][0];
-    a.lpart[2 * blockIdx.x + 1] = red[1][0];
-  }
-}
-
-// TB / DB / MDB with one warp per trajectory (lanes over the steps): the per-step loads
-// are independent, so a trajectory costs two dependent loads instead of 2 L. Same
-// residuals and coefficients as k_fast_loss; partial sums in a fixed tree order.
+// TB / DB / SubTB / MDB with one warp per trajectory (lanes over the steps, SubTB lanes over
+// the sub-trajectory starts then ends): the per-step loads are independent, so a trajectory
+// costs two dependent loads instead of 2 L (objectives.cpp:94-226); partial sums in a fixed
+// tree order.
 GFNX_DEV double warp_sum_d(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
+constexpr int kSubTBMaxT = 128;  // supported() caps max_traj_len at 128 on this path
+
 __global__ void k_fast_loss_warp(LossArgs a) {
+  __shared__ double sub_F[8][kSubTBMaxT + 1], sub_c[8][kSubTBMaxT + 1], sub_S[8][kSubTBMaxT + 1],
+      sub_T[8][kSubTBMaxT + 1];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = gridDim.x * (blockDim.x >> 5);
   const int* cnt = a.batch.counters;
@@ -1651,6 +1551,72 @@ __global__ void k_fast_loss_warp(LossArgs a) {
       }
       ls = warp_sum_d(ls);
       if (lane == 0) loss += ls;
+    } else if (a.objective == GFNX_OBJ_SUBTB) {  // subtb_loss :144-180, lanes over j then k
+      double* F = sub_F[wib];
+      double* cum = sub_c[wib];
+      double* Sg = sub_S[wib];
+      double* Tg = sub_T[wib];
+      double carry = 0.0;
+      for (int k0 = 0; k0 < L; k0 += 32) {  // F(s_t), cum = exclusive prefix of d
+        const int t = k0 + lane;
+        const double d = t < L ? rec(t, 0) - a.neglog[np[t]] : 0.0;
+        if (t < L) F[t] = rec(t, 2);
+        double incl = d;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (t < L) cum[t + 1] = carry + incl;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) {
+        F[L] = logr;
+        cum[0] = 0.0;
+      }
+      double nl = 0.0;  // norm_b = sum_{j<k<=L} lambda^(k-j) = sum_m (L+1-m) lambda^m
+      for (int m = 1 + lane; m <= L; m += 32) nl += (double)(L + 1 - m) * a.lampow[m];
+      const double nrm = warp_sum_d(nl);
+      __syncwarp();
+      double ls = 0.0;
+      for (int j = lane; j < L; j += 32) {  // S_j = sum_k g_jk (loss terms counted here)
+        double sj = 0.0;
+        for (int k = j + 1; k <= L; ++k) {
+          const double w = a.lampow[k - j] / nrm / norm;
+          const double res = (F[j] - F[k]) + (cum[k] - cum[j]);
+          ls += res * res * w;
+          sj += 2.0 * res * w;
+        }
+        Sg[j] = sj;
+      }
+      for (int k = lane; k <= L; k += 32) {  // T_k = sum_j g_jk
+        double tk = 0.0;
+        for (int j = 0; j < k; ++j) {
+          const double w = a.lampow[k - j] / nrm / norm;
+          const double res = (F[j] - F[k]) + (cum[k] - cum[j]);
+          tk += 2.0 * res * w;
+        }
+        Tg[k] = tk;
+      }
+      if (lane == 0) Sg[L] = 0.0;
+      __syncwarp();
+      // gF[c] = S_c - T_c, gc[c] = T_c - S_c; coefficient of log pi at step c: sum_{c' > c} gc[c']
+      double suf = 0.0;
+      for (int k0 = 0; k0 <= L; k0 += 32) {
+        const int c = L - k0 - lane;
+        const double v = c >= 0 ? Tg[c] - Sg[c] : 0.0;
+        double incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        if (c >= 0 && c < L) *C(c) = make_float4((float)(suf + incl - v), 0.f, (float)(Sg[c] - Tg[c]), 0.f);
+        suf += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      ls = warp_sum_d(ls);
+      if (lane == 0) loss += ls;
+      __syncwarp();
     } else {  // mdb_loss :186-226
       const double w = 1.0 / norm;
       double carry = 0.0, ls = 0.0;
@@ -2448,11 +2414,9 @@ struct Kernels {
     la.scalars = c.d_scalars;
     {
       ProfScope ps(c, "k_fast_loss");
-      if (c.train.objective == GFNX_OBJ_SUBTB) k_fast_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
-      else k_fast_loss_warp<<<f.loss_wblocks, 256, 0, c.stream>>>(la);
+      k_fast_loss_warp<<<f.loss_wblocks, 256, 0, c.stream>>>(la);
     }
-    k_loss_finalize<<<1, 256, 0, c.stream>>>(f.lpart, c.train.objective == GFNX_OBJ_SUBTB ? f.loss_blocks : f.loss_wblocks,
-                                              c.d_scalars,
+    k_loss_finalize<<<1, 256, 0, c.stream>>>(f.lpart, f.loss_wblocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
     int smem = bwd_smem_bytes<H, NH>();
     set_smem_once(k_fast_bwd<Env, H, NH>, smem);
