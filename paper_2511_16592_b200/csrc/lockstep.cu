@@ -31,6 +31,7 @@
 //   k_ls_colsum, k_ls_reduce   fixed-order reductions into the flat gradient; then Adam.
 #include <math.h>
 
+#include <type_traits>
 #include <vector>
 
 #include "engine.h"
@@ -136,6 +137,7 @@ struct LsState {
   __nv_bfloat16* wfw[kMaxNL] = {};           // layer l (1..NL-1): [H out][H in] image
   __nv_bfloat16* wdg[kMaxNL] = {};           // layer l: [H in][H out] image
   __nv_bfloat16* wff = nullptr;              // head fwd image: NT n-tiles x 4 K-blocks
+  uint8_t* l1img = nullptr;                  // Ising layer-1 delta image (persistent rollout)
   __nv_bfloat16* wfd = nullptr;              // head dgrad image: 1 n-tile x KBA K-blocks
   float* bfp = nullptr;                      // head bias padded to Ap
   float* h1init = nullptr;                   // [H]
@@ -951,7 +953,7 @@ struct PersistArgs {
   const __nv_bfloat16* w1;    // [O][H]
   const float* h1init;        // [H]
   float* preact;              // [Bl][H]
-  const uint8_t* wimg[kMaxNL + 1];  // [1..NL-1] hidden images, [NL] head image (128 KB each)
+  const uint8_t* wimg[kMaxNL + 1];  // [0] Ising layer-1 delta image, [1..NL-1] hidden, [NL] head
   const float* bias[kMaxNL];  // [l] bias of layer l (l = 1..NL-1)
   const float* bfp;           // head bias padded
   uint8_t* h[kMaxNL];
@@ -962,6 +964,9 @@ struct PersistArgs {
   float* rowbuf;
   DeviceBatch batch;
   long long* phase;  // optional clocks (thread 0): [0] layer 1, [1] hidden layers, [2] head + sample
+  // Ising: layer 1 as an MMA over the assigned-spin one-hot (feature 2 site + up) against
+  // W1[3s + u] - W1[3s + 2] (wimg[0]), bias = h1init: no per-row fp32 state between steps
+  int l1_mma;
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
@@ -1004,7 +1009,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   uint8_t* wbuf = align1024(smem_raw);  // one 256 x 256 weight image (128 KB)
   __shared__ uint64_t mbar, wbar;
   __shared__ uint32_t tbase;
-  __shared__ float h1i[kH];
+  __shared__ __align__(16) float h1i[kH];
   __shared__ Key skeys[256];
   __shared__ double row_u[kPersistMaxTiles][kTile];
   __shared__ float xf[kTile][2];
@@ -1053,7 +1058,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     tc_fence_before();
     __syncthreads();
   };
-  if (tid == 0) load_w(1);
+  if (tid == 0) load_w(a.l1_mma ? 0 : 1);
   const int T = a.T, Bl = a.Bl;
   long long pc[3] = {0, 0, 0}, tclk = clock64();
   auto pmark = [&](int k) {
@@ -1064,6 +1069,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     }
   };
   for (int t = 0; t < T; ++t) {
+    if (!a.l1_mma) {
     // ---- layer 1 for every tile of this CTA
     for (int j = 0; j < ntile; ++j) {
       const int tile = blockIdx.x + j * gridDim.x;
@@ -1153,9 +1159,11 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         st_line_sw(a.h[0] + m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
       }
     }
+    }
     pmark(0);
     // ---- hidden layers 2..NL: MMA per tile (A from TMEM), epilogue back into the same columns
-    for (int l = 1; l < a.NL; ++l) {
+    const int l0 = a.l1_mma ? 0 : 1;
+    for (int l = l0; l < a.NL; ++l) {
       if (tid == 0) mbar_wait(&wbar, wph);
       wph ^= 1;
       for (int j = 0; j < ntile; ++j) {
@@ -1163,13 +1171,35 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         const int b = tile * kTile + row;
         const size_t r = (size_t)t * Bl + b;
         const size_t m = (size_t)t * a.tilesB + tile;
+        if (l == 0) {  // assigned-spin one-hot of the row, features [128 half, +128): 64 packed columns
+          const uint32_t* w = a.cur + (size_t)b * P.SW;
+          const int nw = P.SW / 2;
+          const int w0 = 2 * half;  // sites [64 half, 64 half + 64) = state words 2 half, 2 half + 1
+          uint32_t asg[2], up[2];
+#pragma unroll
+          for (int k = 0; k < 2; ++k) {
+            asg[k] = w0 + k < nw ? w[w0 + k] : 0u;
+            up[k] = w0 + k < nw ? w[nw + w0 + k] : 0u;
+          }
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            uint32_t ob[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {  // site 64 half + 32 hh + i: (spin -1, spin +1) bf16 pair
+              const uint32_t as = (asg[hh] >> i) & 1u, u1 = (up[hh] >> i) & 1u;
+              ob[i] = (as & (u1 ^ 1u)) * 0x3F80u | (as & u1) * 0x3F800000u;
+            }
+            tmem_st32(lane_base + kH + 128 * j + 64 * half + 32 * hh, ob);
+          }
+          publish();
+        }
         mma_issue(tmem, tmem + kH + 128 * j);
-        if (half == 1 && l == 1 && j < kPersistMaxTiles)  // the row's uniform while the MMA runs
+        if (half == 1 && l == l0 && j < kPersistMaxTiles)  // the row's uniform while the MMA runs
           row_u[j][row] = uniform_scalar(fold_in(skeys[t], (uint64_t)(a.b0 + b)));
         mma_wait();
         if (j == ntile - 1 && tid == 0) load_w(l + 1 < a.NL ? l + 1 : a.NL);  // wbuf free now
         uint32_t mw[4];
-        const float* bl = a.bias[l];
+        const float* bl = l == 0 ? h1i : a.bias[l];  // (h1i in shared memory: generic loads)
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
           const int col = c0 + q * 32;
@@ -1180,7 +1210,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           const float4* bb = reinterpret_cast<const float4*>(bl + col);
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 bq = __ldg(bb + i);
+            const float4 bq = bb[i];
             pk[2 * i] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i]) + bq.x, 0.f),
                                     fmaxf(__uint_as_float(rr[4 * i + 1]) + bq.y, 0.f));
             pk[2 * i + 1] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i + 2]) + bq.z, 0.f),
@@ -1220,7 +1250,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       uint32_t lw[Lock<E>::kLW];
       Lock<E>::load_lw(P, w, lw);
       mma_wait();
-      if (j == ntile - 1 && tid == 0) load_w(1);  // next step's first hidden layer
+      if (j == ntile - 1 && tid == 0) load_w(a.l1_mma ? 0 : 1);  // next step's first layer
       uint32_t lmw[4];
       float hi = -INFINITY;
       int lcount = 0;
@@ -1373,6 +1403,18 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// Ising layer-1 operand: K-major image of D(n, 2s + u) = W1[3s + u][n] - W1[3s + 2][n]
+// (u = 0: spin -1, u = 1: spin +1; ising.cpp:122-129 feature order), zero beyond 2D
+__global__ void k_ls_ising_l1img(const __nv_bfloat16* w1, int D, uint8_t* img) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= kH * kH) return;
+  const int n = i / kH, k = i % kH, site = k >> 1, u = k & 1;
+  float v = 0.f;
+  if (site < D)
+    v = __bfloat162float(w1[(size_t)(3 * site + u) * kH + n]) - __bfloat162float(w1[(size_t)(3 * site + 2) * kH + n]);
+  *reinterpret_cast<__nv_bfloat16*>(img + sw128_offset(n, k, kH)) = __float2bfloat16(v);
+}
+
 template <class E>
 void rollout_impl(Ctx& c, Key key, double eps) {
   LsState& f = LS(c);
@@ -1407,6 +1449,13 @@ void rollout_impl(Ctx& c, Key key, double eps) {
       pa.bias[l] = c.p32 + c.L.off_b[l];
     }
     pa.wimg[f.NL] = (const uint8_t*)f.wff;
+    if (std::is_same<E, IsingEnv>::value && 2 * c.P.is_D <= kH && !getenv("GFNX_LS_L1_GATHER")) {
+      if (!f.l1img) cuda_check(cudaMalloc(&f.l1img, kH * kH * 2), "ising l1 image");
+      k_ls_ising_l1img<<<kH * kH / 256, 256, 0, c.stream>>>(f.w1, c.P.is_D, f.l1img);
+      c.launches++;
+      pa.wimg[0] = f.l1img;
+      pa.l1_mma = 1;
+    }
     pa.bfp = f.bfp;
     for (int l = 0; l < f.NL; ++l) {
       pa.h[l] = (uint8_t*)f.h[l];
@@ -1650,7 +1699,7 @@ void ls_init(Ctx& c) {
 void ls_free(Ctx& c) {
   LsState* f = static_cast<LsState*>(c.fast);
   if (!f) return;
-  std::vector<void*> ptrs = {f->w1, f->wff, f->wfd, f->bfp, f->h1init, f->preact, f->cur, f->stst, f->last_act,
+  std::vector<void*> ptrs = {f->w1, f->wff, f->wfd, f->l1img, f->bfp, f->h1init, f->preact, f->cur, f->stst, f->last_act,
                              f->logits, f->stats, f->dlog, f->rowbuf, f->coef, f->bpart, f->bpart2, f->wpart,
                              f->lpart};
   for (int l = 0; l < kMaxNL; ++l) {
