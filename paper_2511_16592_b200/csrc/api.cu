@@ -759,9 +759,17 @@ gfnx_status gfnx_export_batch(gfnx_ctx* h, gfnx_host_batch* out) {
     cuda_check(cudaStreamSynchronize(c.stream), "sync");
     const int Bl = c.Bl, T = c.P.T;
     const size_t bt = (size_t)Bl * T;
-    if (out->lengths) cuda_check(cudaMemcpy(out->lengths, c.batch.lengths, sizeof(int32_t) * Bl, cudaMemcpyDeviceToHost), "export");
+    // steps t >= L_b are padding (actions -1, log P_B and delta 0): the device does not keep
+    // them, the export derives them from the lengths
+    std::vector<int32_t> len(Bl);
+    cuda_check(cudaMemcpy(len.data(), c.batch.lengths, sizeof(int32_t) * Bl, cudaMemcpyDeviceToHost), "export");
+    if (out->lengths) memcpy(out->lengths, len.data(), sizeof(int32_t) * Bl);
     if (out->log_rewards) cuda_check(cudaMemcpy(out->log_rewards, c.batch.log_rewards, sizeof(double) * Bl, cudaMemcpyDeviceToHost), "export");
-    if (out->delta_log_reward) cuda_check(cudaMemcpy(out->delta_log_reward, c.batch.delta, sizeof(double) * bt, cudaMemcpyDeviceToHost), "export");
+    if (out->delta_log_reward) {
+      cuda_check(cudaMemcpy(out->delta_log_reward, c.batch.delta, sizeof(double) * bt, cudaMemcpyDeviceToHost), "export");
+      for (int b = 0; b < Bl; ++b)  // delta is defined for non-terminal steps t < L - 1
+        for (int t = std::max(len[b] - 1, 0); t < T; ++t) out->delta_log_reward[(size_t)b * T + t] = 0.0;
+    }
     if (out->terminal_state) cuda_check(cudaMemcpy(out->terminal_state, c.batch.term_state, sizeof(uint32_t) * Bl * c.P.SW, cudaMemcpyDeviceToHost), "export");
     if (!out->fwd_actions && !out->bwd_actions && !out->log_pb) return;
     std::vector<int16_t> a(bt);
@@ -771,7 +779,7 @@ gfnx_status gfnx_export_batch(gfnx_ctx* h, gfnx_host_batch* out) {
     HostEnv he;
     build_host_env(c.env, &he);
     for (size_t i = 0; i < bt; ++i) {
-      const int act = a[i];
+      const int act = (int)(i % T) < len[i / T] ? a[i] : -1;
       if (out->fwd_actions) out->fwd_actions[i] = act;
       if (out->bwd_actions) {
         int ba = -1;

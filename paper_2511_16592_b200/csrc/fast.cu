@@ -132,6 +132,15 @@ __global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, cons
     }
 }
 
+__global__ void k_rollout_reset(int32_t* tilectr, int32_t* counters, int32_t* work) {
+  if (threadIdx.x == 0) {
+    *tilectr = 0;
+    *work = 0;
+    counters[0] = 0;  // finish_counts
+    counters[1] = 0;
+  }
+}
+
 // row slots in trajectory order (row0[b] + t) when the training forward is recomputed
 __global__ void k_linear_rows(const int32_t* __restrict__ lengths, const int32_t* __restrict__ row0, int Bl,
                               int T, const int32_t* counters, int32_t* frow_bt, int32_t* bt_row,
@@ -2292,14 +2301,10 @@ struct Kernels {
     a.tilectr = f.tilectr;
     a.logits = f.logits;
     a.emit_mode = getenv("GFNX_EMIT_MODE") ? atoi(getenv("GFNX_EMIT_MODE")) : 0;
-    const int T = c.P.T;
-    cudaMemsetAsync(f.tilectr, 0, sizeof(int32_t), c.stream);
-    cudaMemsetAsync(c.batch.counters, 0, 2 * sizeof(int32_t), c.stream);  // finish_counts
-    cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)c.Bl * T, c.stream);
-    cudaMemsetAsync(c.batch.nparents, 0, sizeof(uint16_t) * (size_t)c.Bl * T, c.stream);
-    if (c.P.mdb) cudaMemsetAsync(c.batch.delta, 0, sizeof(double) * (size_t)c.Bl * T, c.stream);
-    cudaMemsetAsync(c.batch.lengths, 0, sizeof(int32_t) * c.Bl, c.stream);
-    cudaMemsetAsync(f.work, 0, sizeof(int32_t), c.stream);
+    // counters only: the per-step arrays beyond each trajectory's length are never read on
+    // the device (gfnx_export_batch pads them from the lengths)
+    k_rollout_reset<<<1, 32, 0, c.stream>>>(f.tilectr, c.batch.counters, f.work);
+    c.launches++;
     const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
     const int fixed = rollout_smem_fixed<H, NH>();
     const int w1b = c.P.O * H * 2;
