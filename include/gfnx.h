@@ -217,9 +217,10 @@ gfnx_status gfnx_last_phase_ms(const gfnx_ctx* ctx, double* rollout_ms, double* 
 /* CUDA events on the ctx stream (bench.py device timing): slots 0..15. */
 gfnx_status gfnx_event_record(gfnx_ctx* ctx, int32_t slot);
 gfnx_status gfnx_event_elapsed(gfnx_ctx* ctx, int32_t slot_a, int32_t slot_b, double* ms);
-/* Per-kernel CUDA-event brackets of every launch while enabled; profile_read returns the
- * number of distinct kernels, their '\n'-separated names, summed ms and launch counts,
- * and clears the record. */
+/* Per-kernel CUDA-event brackets while enabled (enable = 1: every launch, 2: the rollout
+ * kernel only, so the brackets do not perturb the rest of the iteration); profile_read
+ * returns the number of distinct kernels, their '\n'-separated names, summed ms and launch
+ * counts, and clears the record. */
 gfnx_status gfnx_profile(gfnx_ctx* ctx, int32_t enable);
 /* out[0] rows (states) processed since creation, out[1] rollouts, out[2] rows and out[3]
  * MDB transitions of the resident batch. */

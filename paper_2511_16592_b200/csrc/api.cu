@@ -66,6 +66,7 @@ void cuda_check(cudaError_t e, const char* what) {
 
 ProfScope::ProfScope(Ctx& ctx, const char* name) : c(ctx) {
   if (!c.profiling) return;
+  if (c.profile_rollout_only && strcmp(name, "k_fast_rollout") != 0 && strcmp(name, "k_ls_persist") != 0) return;
   auto take = [&]() {
     if (c.ev_pool.empty()) {
       cudaEvent_t e;
@@ -870,6 +871,7 @@ gfnx_status gfnx_phase_timers(gfnx_ctx* h, int32_t mode, int64_t* out, int32_t n
 
 gfnx_status gfnx_profile(gfnx_ctx* h, int32_t enable) {
   h->c.profiling = enable != 0;
+  h->c.profile_rollout_only = enable == 2;
   return GFNX_OK;
 }
 

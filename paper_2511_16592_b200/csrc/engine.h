@@ -142,6 +142,7 @@ struct Ctx {
     cudaEvent_t a, b;
   };
   bool profiling = false;
+  bool profile_rollout_only = false;  // gfnx_profile(ctx, 2): bracket the rollout kernel only
   std::vector<ProfRec> prof;
   std::vector<cudaEvent_t> ev_pool;
   double last_rollout_ms = 0.0, last_train_ms = 0.0;
