@@ -288,6 +288,7 @@ def ref_lib(kind: str = "port"):
         L.ref_threefry.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_void_p]
         L.ref_run_bench.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int,
                                     C.c_void_p, C.c_void_p]
+        L.ref_exact_divergence.argtypes = [C.c_void_p, C.c_void_p]
         _REF[kind] = L
     return _REF[kind]
 
@@ -356,6 +357,13 @@ class RefLib:
         loss = C.c_double()
         self._check(self.L.ref_iteration(self.h, it, C.byref(loss)))
         return loss.value
+
+    def exact_divergence(self):
+        """TV (hypergrid) / JSD (DAG) of the current policy's exact terminal marginal to the
+        target distribution, by the reference's exact enumeration (exact.hpp:76)."""
+        d = C.c_double()
+        self._check(self.L.ref_exact_divergence(self.h, C.byref(d)))
+        return d.value
 
 
 def ref_run_bench(env_name: str, kv: dict, kind: str = "fast"):

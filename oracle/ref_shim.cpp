@@ -14,6 +14,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "gfn/config.hpp"
@@ -23,6 +24,8 @@
 #include "gfn/envs/ising.hpp"
 #include "gfn/envs/sequences.hpp"
 #include "gfn/errors.hpp"
+#include "gfn/exact.hpp"
+#include "gfn/metrics.hpp"
 #include "gfn/nn.hpp"
 #include "gfn/objectives.hpp"
 #include "gfn/optim.hpp"
@@ -58,6 +61,10 @@ struct SessionBase {
   virtual void apply_adam(double lr) = 0;
   virtual const TrajectoryBatch& batch() const = 0;
   virtual MlpParams& policy() = 0;
+  // distance of the policy's exact terminal marginal (exact_policy_marginal, exact.hpp:76)
+  // to the target: TV for hypergrid (grid_exact_distribution), JSD for DAG
+  // (dag_exact_posterior) - the quantities of acceptance criteria 1 and 3
+  virtual double exact_divergence() { throw config_error("exact divergence: hypergrid and DAG only"); }
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -152,6 +159,17 @@ struct Session : SessionBase {
   }
   const TrajectoryBatch& batch() const override { return tb; }
   MlpParams& policy() override { return pol; }
+  double exact_divergence() override {
+    if constexpr (std::is_same_v<E, HypergridEnv>) {
+      auto graph = enumerate_state_graph(env, params);
+      return tv_distance(exact_policy_marginal(env, params, graph, pol), grid_exact_distribution(params));
+    } else if constexpr (std::is_same_v<E, DagEnv>) {
+      auto graph = enumerate_state_graph(env, params);
+      return jsd(exact_policy_marginal(env, params, graph, pol), dag_exact_posterior(*params.score));
+    } else {
+      return SessionBase::exact_divergence();
+    }
+  }
   std::vector<double>& grads() override { return g; }
   double& dlogz() override { return dz; }
   AdamState& opt_main() override { return om; }
@@ -336,6 +354,11 @@ int ref_iteration(void* h, int64_t it, double* loss) {
     *loss = rs->s->compute_grads();
     rs->s->apply_adam(lr);
   });
+}
+
+int ref_exact_divergence(void* h, double* out) {
+  auto* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] { *out = rs->s->exact_divergence(); });
 }
 
 double ref_uniform_fold(uint64_t hi, uint64_t lo, uint64_t idx) {
