@@ -62,9 +62,9 @@ struct SessionBase {
   virtual const TrajectoryBatch& batch() const = 0;
   virtual MlpParams& policy() = 0;
   // distance of the policy's exact terminal marginal (exact_policy_marginal, exact.hpp:76)
-  // to the target: TV for hypergrid (grid_exact_distribution), JSD for DAG
-  // (dag_exact_posterior) - the quantities of acceptance criteria 1 and 3
-  virtual double exact_divergence() { throw config_error("exact divergence: hypergrid and DAG only"); }
+  // to the target: TV for hypergrid (grid_exact_distribution) and Ising
+  // (ising_exact_distribution), JSD for DAG (dag_exact_posterior) - acceptance criteria 1, 3, 5
+  virtual double exact_divergence() { throw config_error("exact divergence: hypergrid, DAG and Ising only"); }
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -166,6 +166,9 @@ struct Session : SessionBase {
     } else if constexpr (std::is_same_v<E, DagEnv>) {
       auto graph = enumerate_state_graph(env, params);
       return jsd(exact_policy_marginal(env, params, graph, pol), dag_exact_posterior(*params.score));
+    } else if constexpr (std::is_same_v<E, IsingEnv>) {  // criterion 5 (acceptance.cpp:342-360)
+      auto graph = enumerate_state_graph(env, params);
+      return tv_distance(exact_policy_marginal(env, params, graph, pol), ising_exact_distribution(*params.coupling));
     } else {
       return SessionBase::exact_divergence();
     }

@@ -110,3 +110,33 @@ def test_dag_posterior_learned_like_reference_criterion3():
     tr.close()
     print(f"dag d=3 jsd {init:.4f} -> {best:.4f} after {250 * (k + 1)} iterations")
     assert best < 0.05, best
+
+
+def test_ising_sampler_learned_like_reference_criterion5():
+    """Acceptance criterion 5, sampling part (acceptance.cpp:342-360): Ising 3x3 toroidal
+    lattice (sigma 0.2), trajectory balance, eps 0.01, lr 1e-3, z_lr 0.1; the total-variation
+    distance of the policy's exact terminal marginal to the exact Boltzmann distribution
+    (reference enumeration on the device-trained parameters, every 250 iterations) must drop
+    below 0.1 within 6000 iterations. The device's Ising path is the 256-wide lockstep MLP
+    (the reference criterion uses 2x128) and runs batch 128 (the persistent rollout needs
+    whole 128-trajectory tiles; the reference uses 32)."""
+    from oracle import oracle as O
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    e = abi.env_desc(abi.ISING, is_side=3, is_sigma=0.2)
+    t = abi.train_desc(abi.ISING, batch=128, seed=4, hidden=(256, 256), lr=1e-3, objective="tb",
+                       z_lr=0.1, eps=0.01, iterations=6000)
+    tr = engine.Trainer(e, t)
+    ref = O.RefLib(e, t)
+    ref.set_params(*tr.params())
+    init = ref.exact_divergence()
+    best = 1.0
+    for k in range(24):
+        tr.run(250 * k, 250)
+        ref.set_params(*tr.params())
+        best = min(best, ref.exact_divergence())
+        if best < 0.08:
+            break
+    tr.close()
+    print(f"ising 3x3 tv {init:.4f} -> {best:.4f} after {250 * (k + 1)} iterations")
+    assert init > 0.1 and best < 0.1, (init, best)
