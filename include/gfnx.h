@@ -161,6 +161,11 @@ gfnx_status gfnx_get_adam_state(gfnx_ctx* ctx, double* m, double* v, int64_t* t,
 /* One forward rollout of this rank's trajectory slice for iteration `it`
  * (key fold_in(make_key(seed), 1000 + it), env_core.hpp:232-274) at exploration eps.
  * The batch stays resident on the device. */
+/* GFNCKPT1 checkpoint files, byte-compatible with the reference's save_checkpoint /
+ * load_checkpoint (checkpoint.cpp:11-107): policy (fp64), both Adam states, step counter. */
+gfnx_status gfnx_save_checkpoint(gfnx_ctx* ctx, const char* path, int64_t step);
+gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step);
+
 gfnx_status gfnx_rollout(gfnx_ctx* ctx, int64_t it, double eps);
 /* Loss + gradient over the resident batch, NCCL all-reduce (world > 1), Adam on
  * the main params with learning rate lr and (TB) on logZ with z_lr (train.cpp:164-192).

@@ -289,6 +289,8 @@ def ref_lib(kind: str = "port"):
         L.ref_run_bench.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int,
                                     C.c_void_p, C.c_void_p]
         L.ref_exact_divergence.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
+        L.ref_load_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         _REF[kind] = L
     return _REF[kind]
 
@@ -357,6 +359,14 @@ class RefLib:
         loss = C.c_double()
         self._check(self.L.ref_iteration(self.h, it, C.byref(loss)))
         return loss.value
+
+    def save_checkpoint(self, path, step):
+        self._check(self.L.ref_save_checkpoint(self.h, str(path).encode(), step))
+
+    def load_checkpoint(self, path):
+        st = C.c_int64()
+        self._check(self.L.ref_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
+        return st.value
 
     def exact_divergence(self):
         """TV (hypergrid) / JSD (DAG) of the current policy's exact terminal marginal to the

@@ -17,6 +17,7 @@
 #include <type_traits>
 #include <vector>
 
+#include "gfn/checkpoint.hpp"
 #include "gfn/config.hpp"
 #include "gfn/env_core.hpp"
 #include "gfn/envs/dag.hpp"
@@ -356,6 +357,30 @@ int ref_iteration(void* h, int64_t it, double* loss) {
     rs->s->rollout(it, eps);
     *loss = rs->s->compute_grads();
     rs->s->apply_adam(lr);
+  });
+}
+
+// the reference's own GFNCKPT1 writer / reader on the session's policy and Adam states
+int ref_save_checkpoint(void* h, const char* path, int64_t step) {
+  auto* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] {
+    Checkpoint c;
+    c.params = rs->s->policy();
+    c.opt_main = rs->s->opt_main();
+    c.opt_z = rs->s->opt_z();
+    c.step = step;
+    save_checkpoint(c, path);
+  });
+}
+
+int ref_load_checkpoint(void* h, const char* path, int64_t* step) {
+  auto* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] {
+    Checkpoint c = load_checkpoint(path);
+    rs->s->policy() = c.params;
+    rs->s->opt_main() = c.opt_main;
+    rs->s->opt_z() = c.opt_z;
+    *step = c.step;
   });
 }
 

@@ -619,6 +619,121 @@ gfnx_status gfnx_get_adam_state(gfnx_ctx* h, double* m, double* v, int64_t* t, d
   });
 }
 
+// ---------------------------------------------------------------------------
+// GFNCKPT1 checkpoints (checkpoint.cpp:11-107): magic, trunk depth, every Dense as
+// (rank, dims, fp64 values) for weight [in x out] and bias [out], fwd / bwd / flow heads,
+// log_z [1], then the main Adam state (t, tensor count, m tensors, v tensors), the log_z
+// Adam state and the step counter. Byte-compatible with the reference's save / load.
+namespace {
+constexpr char kCkptMagic[8] = {'G', 'F', 'N', 'C', 'K', 'P', 'T', '1'};
+
+struct CkptTensor {
+  std::vector<int64_t> shape;
+  int64_t off, n;
+};
+
+std::vector<CkptTensor> ckpt_tensors(const Ctx& c) {  // MlpParams::tensors() order (nn.cpp:8-19)
+  const MlpLayout& L = c.L;
+  std::vector<CkptTensor> v;
+  for (int l = 0; l < L.n_trunk; ++l) {
+    v.push_back({{L.dims[l], L.dims[l + 1]}, L.off_w[l], (int64_t)L.dims[l] * L.dims[l + 1]});
+    v.push_back({{L.dims[l + 1]}, L.off_b[l], L.dims[l + 1]});
+  }
+  const int64_t H = L.H(), A = c.shape.num_actions, Ab = c.shape.num_backward_actions;
+  v.push_back({{H, A}, L.off_fw, H * A});
+  v.push_back({{A}, L.off_fb, A});
+  v.push_back({{H, Ab}, L.off_bw, H * Ab});
+  v.push_back({{Ab}, L.off_bb, Ab});
+  v.push_back({{H, 1}, L.off_flw, H});
+  v.push_back({{1}, L.off_flb, 1});
+  return v;
+}
+
+void put_i64(std::FILE* f, int64_t x) { std::fwrite(&x, 8, 1, f); }
+int64_t get_i64(std::FILE* f) {
+  int64_t x = 0;
+  if (std::fread(&x, 8, 1, f) != 1) fail(GFNX_ERR_CONFIG, "checkpoint: truncated file");
+  return x;
+}
+void put_tensor(std::FILE* f, const std::vector<int64_t>& shape, const double* x, int64_t n) {
+  put_i64(f, (int64_t)shape.size());
+  for (int64_t d : shape) put_i64(f, d);
+  std::fwrite(x, sizeof(double), (size_t)n, f);
+}
+void get_tensor(std::FILE* f, const std::vector<int64_t>& shape, double* x, int64_t n) {
+  const int64_t rank = get_i64(f);
+  if (rank != (int64_t)shape.size()) fail(GFNX_ERR_CONFIG, "checkpoint: tensor rank does not match the model");
+  for (int64_t d : shape)
+    if (get_i64(f) != d) fail(GFNX_ERR_CONFIG, "checkpoint: tensor shape does not match the model");
+  if (std::fread(x, sizeof(double), (size_t)n, f) != (size_t)n) fail(GFNX_ERR_CONFIG, "checkpoint: truncated tensor data");
+}
+}  // namespace
+
+gfnx_status gfnx_save_checkpoint(gfnx_ctx* h, const char* path, int64_t step) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const int64_t n = c.L.n_params;
+    std::vector<double> p(n), m(n), v(n);
+    double z = 0, zm = 0, zv = 0;
+    int64_t t = 0, zt = 0;
+    if (gfnx_get_params(h, p.data(), n, &z) != GFNX_OK) fail(GFNX_ERR_CUDA, c.err);
+    if (gfnx_get_adam_state(h, m.data(), v.data(), &t, &zm, &zv, &zt) != GFNX_OK) fail(GFNX_ERR_CUDA, c.err);
+    std::FILE* f = std::fopen(path, "wb");
+    if (!f) fail(GFNX_ERR_CONFIG, std::string("checkpoint: cannot open for write: ") + path);
+    const auto ts = ckpt_tensors(c);
+    std::fwrite(kCkptMagic, 1, 8, f);
+    put_i64(f, c.L.n_trunk);
+    for (const auto& x : ts) put_tensor(f, x.shape, p.data() + x.off, x.n);
+    put_tensor(f, {1}, &z, 1);
+    put_i64(f, t);
+    put_i64(f, (int64_t)ts.size());
+    for (const auto& x : ts) put_tensor(f, x.shape, m.data() + x.off, x.n);
+    for (const auto& x : ts) put_tensor(f, x.shape, v.data() + x.off, x.n);
+    put_i64(f, zt);
+    put_i64(f, 1);
+    put_tensor(f, {1}, &zm, 1);
+    put_tensor(f, {1}, &zv, 1);
+    put_i64(f, step);
+    const bool ok = std::ferror(f) == 0;
+    std::fclose(f);
+    if (!ok) fail(GFNX_ERR_CONFIG, std::string("checkpoint: write failed: ") + path);
+  });
+}
+
+gfnx_status gfnx_load_checkpoint(gfnx_ctx* h, const char* path, int64_t* step) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const int64_t n = c.L.n_params;
+    std::vector<double> p(n), m(n), v(n);
+    double z = 0, zm = 0, zv = 0;
+    std::FILE* f = std::fopen(path, "rb");
+    if (!f) fail(GFNX_ERR_CONFIG, std::string("checkpoint: cannot open: ") + path);
+    struct Closer {
+      std::FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    char magic[8];
+    if (std::fread(magic, 1, 8, f) != 8 || memcmp(magic, kCkptMagic, 8) != 0)
+      fail(GFNX_ERR_CONFIG, std::string("checkpoint: bad magic in ") + path);
+    if (get_i64(f) != c.L.n_trunk) fail(GFNX_ERR_CONFIG, "checkpoint: trunk depth does not match the model");
+    const auto ts = ckpt_tensors(c);
+    for (const auto& x : ts) get_tensor(f, x.shape, p.data() + x.off, x.n);
+    get_tensor(f, {1}, &z, 1);
+    const int64_t t = get_i64(f);
+    if (get_i64(f) != (int64_t)ts.size()) fail(GFNX_ERR_CONFIG, "checkpoint: optimizer state does not match the model");
+    for (const auto& x : ts) get_tensor(f, x.shape, m.data() + x.off, x.n);
+    for (const auto& x : ts) get_tensor(f, x.shape, v.data() + x.off, x.n);
+    const int64_t zt = get_i64(f);
+    if (get_i64(f) != 1) fail(GFNX_ERR_CONFIG, "checkpoint: log_z optimizer state malformed");
+    get_tensor(f, {1}, &zm, 1);
+    get_tensor(f, {1}, &zv, 1);
+    const int64_t st = get_i64(f);
+    if (gfnx_set_params(h, p.data(), n, z) != GFNX_OK) fail(GFNX_ERR_CUDA, c.err);
+    if (gfnx_set_adam_state(h, m.data(), v.data(), t, zm, zv, zt) != GFNX_OK) fail(GFNX_ERR_CUDA, c.err);
+    if (step) *step = st;
+  });
+}
+
 gfnx_status gfnx_rollout(gfnx_ctx* h, int64_t it, double eps) {
   return guard(h, [&] {
     do_rollout(h->c, it, eps);

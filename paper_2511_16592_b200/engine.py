@@ -87,6 +87,8 @@ def lib():
         L.gfnx_phase_timers.argtypes = [vp, C.c_int32, vp, C.c_int32]
         L.gfnx_test_mma_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp]
         L.gfnx_test_ts_mma.argtypes = [vp, vp, vp]
+        L.gfnx_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_int64]
+        L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
         L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
         _LIB = L
@@ -168,6 +170,15 @@ class Trainer:
         m = np.ascontiguousarray(m, dtype=np.float64)
         v = np.ascontiguousarray(v, dtype=np.float64)
         self._check(lib().gfnx_set_adam_state(self.h, _p(m), _p(v), t, zm, zv, zt))
+
+    # -- GFNCKPT1 checkpoints (checkpoint.cpp:11-107) --
+    def save_checkpoint(self, path, step: int = 0):
+        self._check(lib().gfnx_save_checkpoint(self.h, str(path).encode(), step))
+
+    def load_checkpoint(self, path) -> int:
+        st = C.c_int64()
+        self._check(lib().gfnx_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
+        return st.value
 
     # -- the hot path --
     def forward_rollout(self, it: int, eps: float):
