@@ -166,6 +166,12 @@ gfnx_status gfnx_get_adam_state(gfnx_ctx* ctx, double* m, double* v, int64_t* t,
 gfnx_status gfnx_save_checkpoint(gfnx_ctx* ctx, const char* path, int64_t step);
 gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step);
 
+/* Exact terminal marginal of the current policy on the hypergrid (exact_policy_marginal,
+ * exact.hpp:76-113): one batched policy forward over every cell + a level-by-level DP on the
+ * device. marginal: n = side^dim doubles in row-major cell order (coordinate 0 fastest), or
+ * NULL; tv: total variation to R / Z (the `tv_exact` metric), or NULL. bf16 fast path. */
+gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_t n, double* tv);
+
 gfnx_status gfnx_rollout(gfnx_ctx* ctx, int64_t it, double eps);
 /* Loss + gradient over the resident batch, NCCL all-reduce (world > 1), Adam on
  * the main params with learning rate lr and (TB) on logZ with z_lr (train.cpp:164-192).

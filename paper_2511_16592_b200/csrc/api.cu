@@ -734,6 +734,39 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* h, const char* path, int64_t* step) {
   });
 }
 
+gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* h, double* marginal, int64_t n, double* tv) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (c.check_mode()) fail(GFNX_ERR_CONFIG, "exact terminal marginal: bf16 fast path only");
+    std::vector<double> pt;
+    fast_hg_marginal(c, &pt);
+    if (marginal) {
+      if (n != (int64_t)pt.size()) fail(GFNX_ERR_CONFIG, "exact terminal marginal: wrong buffer size");
+      memcpy(marginal, pt.data(), sizeof(double) * pt.size());
+    }
+    if (tv) {  // against R / Z over all cells (grid_exact_distribution, hypergrid.cpp:111-119)
+      const int d = c.env.hg_dim, side = c.env.hg_side;
+      std::vector<double> r(pt.size());
+      double zsum = 0.0;
+      for (size_t x = 0; x < pt.size(); ++x) {
+        int64_t y = (int64_t)x;
+        bool p1 = true, p2 = true;
+        for (int i = 0; i < d; ++i) {
+          const double a = fabs((double)(y % side) / (double)(side - 1) - 0.5);
+          y /= side;
+          p1 = p1 && 0.25 < a;
+          p2 = p2 && 0.3 < a && a < 0.4;
+        }
+        r[x] = c.env.hg_r0 + (p1 ? c.env.hg_r1 : 0.0) + (p2 ? c.env.hg_r2 : 0.0);
+        zsum += r[x];
+      }
+      double s = 0.0;
+      for (size_t x = 0; x < pt.size(); ++x) s += fabs(pt[x] - r[x] / zsum);
+      *tv = 0.5 * s;
+    }
+  });
+}
+
 gfnx_status gfnx_rollout(gfnx_ctx* h, int64_t it, double eps) {
   return guard(h, [&] {
     do_rollout(h->c, it, eps);

@@ -68,6 +68,7 @@ void test_ts_mma(const uint16_t* a, const uint16_t* b, float* d);
 void launch_row_scan(Ctx& c, bool counts = true);
 void ensure_row0(Ctx& c);              // row0 / row_bt of the resident batch (lazy after a fused rollout)
 bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row counts itself
+void fast_hg_marginal(Ctx& c, std::vector<double>* pt);  // exact terminal marginal (hypergrid)
 
 struct Ctx {
   gfnx_env_desc env{};

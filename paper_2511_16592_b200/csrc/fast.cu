@@ -24,6 +24,7 @@
 //                   operand images (adam_step optim.cpp:19-43)
 #include <math.h>
 
+#include <algorithm>
 #include <type_traits>
 #include <vector>
 
@@ -2274,6 +2275,23 @@ AdamArgs adam_args(Ctx& c) {
   return a;
 }
 
+// exact terminal marginal of the policy on the hypergrid (exact.hpp:76-113 restated for the
+// grid DAG): states in level order (level = sum of coordinates); P(s) = sum over the
+// parents s - e_i of P(s - e_i) pi(i | s - e_i) (a fixed-order gather, no atomics),
+// P_T(s) = P(s) pi(stop | s)
+__global__ void k_hg_marginal_level(int r0, int r1, const int32_t* __restrict__ parents, int dim,
+                                    const float* __restrict__ probs, int rs, int stop, double* P, double* PT) {
+  const int r = r0 + blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= r1) return;
+  double p = r == 0 ? 1.0 : 0.0;
+  for (int i = 0; i < dim; ++i) {
+    const int q = parents[(size_t)r * dim + i];
+    if (q >= 0) p += P[q] * (double)probs[(size_t)q * rs + i];
+  }
+  P[r] = p;
+  PT[r] = p * (double)probs[(size_t)r * rs + stop];
+}
+
 template <class Env, int H, int NH>
 struct Kernels {
   static void rollout(Ctx& c, Key key, double eps) {
@@ -2339,6 +2357,43 @@ struct Kernels {
     }
     c.launches++;
     f.fused = true;
+  }
+  // policy forward (masked softmax record) over `n` explicit packed states (eval buffers)
+  static void eval_forward(Ctx& c, const uint32_t* stst, const int32_t* rows, const int32_t* tiles,
+                           const int16_t* acts, __nv_bfloat16* h1, __nv_bfloat16* h2, uint32_t* m1,
+                           uint32_t* m2, float* rowbuf) {
+    FastState& f = FS(c);
+    TrainArgs ta{};
+    ta.P = c.P;
+    ta.W = weights_of(c);
+    ta.batch = c.batch;
+    ta.batch.actions = const_cast<int16_t*>(acts);
+    ta.Bl = c.Bl;
+    ta.stst = stst;
+    ta.frow_bt = rows;
+    ta.tilectr = tiles;
+    ta.h1 = h1;
+    ta.h2 = h2;
+    ta.mask1 = m1;
+    ta.mask2 = m2;
+    ta.rowbuf = rowbuf;
+    ta.rs = f.rs;
+    ta.L = c.L;
+    ta.objective = c.train.objective;
+    const int fixed = fwd_smem_fixed<H, NH>();
+    const int w1b = c.P.O * H * 2;
+    cudaFuncAttributes fa{};
+    cudaFuncGetAttributes(&fa, k_fast_fwd<Env, H, NH, true>);
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
+    if (fixed + w1b + (int)fa.sharedSizeBytes <= optin && c.P.SW <= kMaxSWFwd) {
+      set_smem_once(k_fast_fwd<Env, H, NH, true>, fixed + w1b);
+      k_fast_fwd<Env, H, NH, true><<<f.num_sms, kThreads, fixed + w1b, c.stream>>>(ta);
+    } else {
+      set_smem_once(k_fast_fwd<Env, H, NH, false>, fixed);
+      k_fast_fwd<Env, H, NH, false><<<f.num_sms, kThreads, fixed, c.stream>>>(ta);
+    }
+    c.launches++;
   }
   static void train(Ctx& c, bool apply, double lr) {
     FastState& f = FS(c);
@@ -2480,6 +2535,96 @@ bool lockstep(const Ctx& c) { return c.env.kind == GFNX_ENV_BITSEQ || c.env.kind
 }  // namespace
 
 bool fast_rollout_counts(const Ctx& c) { return !lockstep(c); }
+
+void fast_hg_marginal(Ctx& c, std::vector<double>* pt) {
+  if (c.env.kind != GFNX_ENV_HYPERGRID || lockstep(c))
+    raise_error(GFNX_ERR_CONFIG, "exact terminal marginal: hypergrid fast path only");
+  const int d = c.env.hg_dim, side = c.env.hg_side;
+  int64_t n = 1;
+  for (int i = 0; i < d; ++i) n *= side;
+  if (n > (1 << 24)) raise_error(GFNX_ERR_CONFIG, "exact terminal marginal: grid too large");
+  // cells in level order (sum of coordinates), packed states, parents per dimension
+  std::vector<int64_t> cells(n);
+  std::vector<int> lvl(n);
+  for (int64_t x = 0; x < n; ++x) {
+    int64_t y = x;
+    int sum = 0;
+    for (int i = 0; i < d; ++i) {
+      sum += (int)(y % side);
+      y /= side;
+    }
+    cells[x] = x;
+    lvl[x] = sum;
+  }
+  std::stable_sort(cells.begin(), cells.end(), [&](int64_t a, int64_t b) { return lvl[a] < lvl[b]; });
+  std::vector<int32_t> pos(n);
+  for (int64_t r = 0; r < n; ++r) pos[cells[r]] = (int32_t)r;
+  const int SW = c.P.SW;
+  std::vector<uint32_t> st((size_t)n * SW, 0u);
+  std::vector<int32_t> par((size_t)n * d, -1);
+  std::vector<int> level_start;
+  int64_t stride[8];
+  stride[0] = 1;
+  for (int i = 1; i < d; ++i) stride[i] = stride[i - 1] * side;
+  for (int64_t r = 0; r < n; ++r) {
+    const int64_t x = cells[r];
+    uint64_t cw = 0;
+    for (int i = 0; i < d; ++i) {
+      const int ci = (int)((x / stride[i]) % side);
+      cw |= (uint64_t)ci << (8 * i);
+      if (ci > 0) par[(size_t)r * d + i] = pos[x - stride[i]];
+    }
+    st[(size_t)r * SW] = (uint32_t)cw;
+    if (SW > 1) st[(size_t)r * SW + 1] = (uint32_t)(cw >> 32);
+    if (r == 0 || lvl[cells[r]] != lvl[cells[r - 1]]) level_start.push_back((int)r);
+  }
+  level_start.push_back((int)n);
+  FastState& f = FS(c);
+  const int64_t tiles = (n + kTile - 1) / kTile, slots = tiles * kTile;
+  std::vector<int32_t> rows(slots, -1);
+  for (int64_t r = 0; r < n; ++r) rows[r] = (int32_t)r;
+  const int32_t ntiles = (int32_t)tiles;
+  uint32_t* d_st;
+  int32_t *d_rows, *d_tiles, *d_par;
+  int16_t* d_act;
+  __nv_bfloat16 *d_h1, *d_h2;
+  uint32_t *d_m1, *d_m2;
+  float* d_rb;
+  double *d_P, *d_PT;
+  const int H = f.H;
+  cuda_check(cudaMalloc(&d_st, sizeof(uint32_t) * st.size()), "eval");
+  cuda_check(cudaMalloc(&d_rows, sizeof(int32_t) * slots), "eval");
+  cuda_check(cudaMalloc(&d_tiles, sizeof(int32_t)), "eval");
+  cuda_check(cudaMalloc(&d_par, sizeof(int32_t) * par.size()), "eval");
+  cuda_check(cudaMalloc(&d_act, sizeof(int16_t) * n), "eval");
+  cuda_check(cudaMalloc(&d_h1, sizeof(__nv_bfloat16) * slots * H), "eval");
+  cuda_check(cudaMalloc(&d_h2, sizeof(__nv_bfloat16) * slots * H), "eval");
+  cuda_check(cudaMalloc(&d_m1, sizeof(uint32_t) * slots * (H / 32)), "eval");
+  cuda_check(cudaMalloc(&d_m2, sizeof(uint32_t) * slots * (H / 32)), "eval");
+  cuda_check(cudaMalloc(&d_rb, sizeof(float) * slots * f.rs), "eval");
+  cuda_check(cudaMalloc(&d_P, sizeof(double) * n), "eval");
+  cuda_check(cudaMalloc(&d_PT, sizeof(double) * n), "eval");
+  cudaMemcpyAsync(d_st, st.data(), sizeof(uint32_t) * st.size(), cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * slots, cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_tiles, &ntiles, sizeof(int32_t), cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_par, par.data(), sizeof(int32_t) * par.size(), cudaMemcpyHostToDevice, c.stream);
+  cudaMemsetAsync(d_act, 0, sizeof(int16_t) * n, c.stream);
+  with_kernels(c, [&](auto k) {
+    decltype(k)::eval_forward(c, d_st, d_rows, d_tiles, d_act, d_h1, d_h2, d_m1, d_m2, d_rb);
+  });
+  for (size_t l = 0; l + 1 < level_start.size(); ++l) {
+    const int r0 = level_start[l], r1 = level_start[l + 1];
+    k_hg_marginal_level<<<(r1 - r0 + 255) / 256, 256, 0, c.stream>>>(r0, r1, d_par, d, d_rb, f.rs, c.P.stop, d_P, d_PT);
+  }
+  c.launches += (int64_t)level_start.size() - 1;
+  std::vector<double> ptr(n);
+  cuda_check(cudaMemcpyAsync(ptr.data(), d_PT, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "eval");
+  cuda_check(cudaStreamSynchronize(c.stream), "eval");
+  void* bufs[] = {d_st, d_rows, d_tiles, d_par, d_act, d_h1, d_h2, d_m1, d_m2, d_rb, d_P, d_PT};
+  for (void* b : bufs) cudaFree(b);
+  pt->assign(n, 0.0);
+  for (int64_t r = 0; r < n; ++r) (*pt)[cells[r]] = ptr[r];  // back to row-major cell order
+}
 
 void fast_init(Ctx& c) {
   if (lockstep(c)) {

@@ -88,6 +88,7 @@ def lib():
         L.gfnx_test_mma_rate.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, vp]
         L.gfnx_test_ts_mma.argtypes = [vp, vp, vp]
         L.gfnx_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_int64]
+        L.gfnx_exact_terminal_marginal.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
         L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
@@ -179,6 +180,13 @@ class Trainer:
         st = C.c_int64()
         self._check(lib().gfnx_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
         return st.value
+
+    def exact_terminal_marginal(self, n_cells: int):
+        """(marginal over cells, TV to R/Z) of the current policy (hypergrid, device DP)."""
+        m = np.zeros(n_cells)
+        tv = C.c_double()
+        self._check(lib().gfnx_exact_terminal_marginal(self.h, _p(m), n_cells, C.byref(tv)))
+        return m, tv.value
 
     # -- the hot path --
     def forward_rollout(self, it: int, eps: float):

@@ -140,3 +140,32 @@ def test_ising_sampler_learned_like_reference_criterion5():
     tr.close()
     print(f"ising 3x3 tv {init:.4f} -> {best:.4f} after {250 * (k + 1)} iterations")
     assert init > 0.1 and best < 0.1, (init, best)
+
+
+def test_device_exact_marginal_matches_reference_enumeration():
+    """gfnx_exact_terminal_marginal (device forward over every cell + level DP) against the
+    reference's exact_policy_marginal / grid_exact_distribution on the same parameters."""
+    from oracle import oracle as O
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    e = abi.env_desc(abi.HYPERGRID, hg_dim=D, hg_side=H)
+    t = abi.train_desc(abi.HYPERGRID, batch=16, objective="tb", seed=1)
+    tr = engine.Trainer(e, t)
+    ref = O.RefLib(e, t)
+    for k in range(3):
+        m, tv_dev = tr.exact_terminal_marginal(H ** D)
+        ref.set_params(*tr.params())
+        tv_ref = ref.exact_divergence()
+        assert abs(m.sum() - 1.0) < 1e-6
+        assert abs(tv_dev - tv_ref) < 1e-2, (k, tv_dev, tv_ref)  # bf16 policy vs fp64
+        tr.run(200 * k, 200)
+    tr.close()
+
+
+def test_device_exact_marginal_config2_grid():
+    """The 20^4 grid of BASELINE config #2: 160000 cells in one call, a distribution."""
+    e, t = abi.config("hypergrid_db_b65536", batch=1024)
+    tr = engine.Trainer(e, t)
+    m, tv_dev = tr.exact_terminal_marginal(20 ** 4)
+    assert abs(m.sum() - 1.0) < 1e-6 and 0.0 <= tv_dev <= 1.0 and np.all(m >= 0)
+    tr.close()
