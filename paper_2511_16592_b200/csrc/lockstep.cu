@@ -431,17 +431,34 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     a.rowbuf[2 * r] = xa - lse;
     a.rowbuf[2 * r + 1] = lse;
     for (int i = 0; i < P.SW; ++i) a.stst[r * P.SW + i] = w[i];
-    typename E::State s;
-    E::unpack(P, w, s);
-    const bool term = E::step(P, s, act);
-    E::pack(P, s, a.cur + (size_t)b * P.SW);
+    bool term;
+    int nparents;
+    uint32_t* cw = a.cur + (size_t)b * P.SW;
+    if constexpr (std::is_same<E, BitseqEnv>::value) {
+      // step in the packed domain (token byte + filled bit; sequences.cpp:257-267): no
+      // per-token unpack / pack on the serial path, full state only at termination
+      const int pos = act / P.bs_vocab, tw = (P.bs_slots + 3) / 4, sh = 8 * (pos & 3);
+      cw[pos >> 2] = (w[pos >> 2] & ~(0xffu << sh)) | ((uint32_t)(act % P.bs_vocab) << sh);
+      const uint32_t filled = w[tw] | (1u << pos);
+      cw[tw] = filled;
+      nparents = __popc(filled);
+      term = nparents == P.bs_slots;
+    } else {
+      typename E::State s;
+      E::unpack(P, w, s);
+      term = E::step(P, s, act);
+      E::pack(P, s, cw);
+      nparents = E::num_parents(P, s);
+    }
     a.batch.actions[bt] = (int16_t)act;
-    a.batch.nparents[bt] = (uint16_t)E::num_parents(P, s);
+    a.batch.nparents[bt] = (uint16_t)nparents;
     a.last_act[b] = act;
     if (term) {
+      typename E::State s;
+      E::unpack(P, cw, s);
       a.batch.lengths[b] = a.t + 1;
       a.batch.log_rewards[b] = E::log_reward(P, s);
-      E::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
+      for (int i = 0; i < P.SW; ++i) a.batch.term_state[(size_t)b * P.SW + i] = cw[i];
     }
     if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
   }
