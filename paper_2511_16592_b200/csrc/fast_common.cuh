@@ -72,6 +72,28 @@ GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) 
     *reinterpret_cast<uint4*>(img + sw128_offset(row, c0 + 8 * c, kTile)) = v;
   }
 }
+// the same 32 columns into a tile image in GLOBAL memory with two 32-byte stores (the chunk
+// pairs (2m, 2m+1) of a 64-column block stay adjacent under the XOR swizzle, halves swapped
+// when row & 1)
+GFNX_DEV void st_row32_g(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
+  const int x = row & 7;
+#pragma unroll
+  for (int m = 0; m < 2; ++m) {
+    const int l0 = ((c0 & 63) >> 3) + 2 * m;  // logical chunk (even)
+    const int p = l0 ^ x;
+    uint32_t v[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (x & 1) ? pk[8 * m + 4 + i] : pk[8 * m + i];
+      v[4 + i] = (x & 1) ? pk[8 * m + i] : pk[8 * m + 4 + i];
+    }
+    uint8_t* dst = img + (c0 >> 6) * (kTile * 128) + row * 128 + (p & ~1) * 16;
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(dst), "r"(v[0]), "r"(v[1]), "r"(v[2]),
+                 "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+  }
+}
+
 GFNX_DEV void ld_row32(const uint8_t* img, int row, int c0, float (&v)[32]) {
 #pragma unroll
   for (int c = 0; c < 4; ++c) {

@@ -243,7 +243,7 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
 #pragma unroll
     for (int i = 0; i < 16; ++i)  // bit 2i / 2i+1 <-> columns 2i / 2i+1 (values >= 0: nonzero = active)
       mb |= (((pk[i] & 0x7FFFu) + 0x7FFFu) >> 15 & 1u) << (2 * i) | (((pk[i] & 0x7FFF0000u) + 0x7FFF0000u) >> 31) << (2 * i + 1);
-    st_row32(e.h + (size_t)m * (kTile * kH * 2), row, col0, pk);
+    st_row32_g(e.h + (size_t)m * (kTile * kH * 2), row, col0, pk);
     const size_t r = (size_t)m * kTile + row;
     *reinterpret_cast<uint32_t*>(e.mask + r * (kH / 8) + col0 / 8) = mb;
   }
@@ -613,7 +613,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
 #pragma unroll
     for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
     uint8_t* blk = e.dlog + ((size_t)m * e.KBA + n * 4 + col0 / 64) * (kTile * 128);
-    st_row32(blk, row, col0 % 64, pk);
+    st_row32_g(blk, row, col0 % 64, pk);
     const float s = warp_colsum32(v);  // this warp's 32 rows, lane = column
     scratch[epi_quarter() * 256 + col0 + (threadIdx.x & 31)] = s;
   }
@@ -641,7 +641,7 @@ struct DgradEpi : EpiBase {  // masked by ReLU bits -> dz image + bias column su
     for (int i = 0; i < 32; ++i) v[i] = ((mk >> i) & 1u) ? v[i] : 0.f;
 #pragma unroll
     for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
-    st_row32(e.dz + (size_t)m * (kTile * kH * 2), row, col0, pk);
+    st_row32_g(e.dz + (size_t)m * (kTile * kH * 2), row, col0, pk);
     const float s = warp_colsum32(v);
     scratch[epi_quarter() * 256 + col0 + (threadIdx.x & 31)] = s;
   }
