@@ -26,8 +26,10 @@ namespace gfnx {
 namespace {
 
 constexpr int kStages = 4;
-constexpr int kGemmThreads = 384;
+constexpr int kGemmThreads = 384;   // k_ls_wgrad (8 epilogue warps)
 constexpr int kEpiThreads = 256;
+constexpr int kGemmEpiParts = 4;    // k_gemm: 16 epilogue warps = lane quarter x column quarter
+constexpr int kGemmKThreads = 128 + 128 * kGemmEpiParts;
 
 template <int BN, bool kResB>
 constexpr int gemm_smem_bytes() {
@@ -65,7 +67,7 @@ GFNX_DEV float warp_colsum32(float (&v)[32]) {
 //   struct Args; struct Local;
 //   begin(e, m, n, row, half, loc)                  once per (item, thread) before the chunks
 //   apply(e, m, n, row, col0, v[32], scratch, loc)  32 accumulator columns [col0, col0 + 32)
-//   row_done(e, m, n, row, half, loc)               after the thread's BN/2 columns
+//   row_done(e, m, n, row, part, scratch, loc)      after the thread's BN/4 columns (part 0..3)
 //   finish(e, m, n, scratch)                        after an epilogue barrier (all rows done);
 // `scratch` is a [4][BN] smem array of per-lane-quarter column partials for finish().
 struct EpiBase {
@@ -73,7 +75,7 @@ struct EpiBase {
   template <class Args, class Loc>
   static __device__ void begin(const Args&, int, int, int, int, Loc&) {}
   template <class Args, class Loc>
-  static __device__ void row_done(const Args&, int, int, int, int, Loc&) {}
+  static __device__ void row_done(const Args&, int, int, int, int, float*, Loc&) {}
   template <class Args>
   static __device__ void finish(const Args&, int, int, const float*) {}
 };
@@ -82,6 +84,7 @@ struct EpiBase {
 GFNX_DEV int epi_quarter() { return ((threadIdx.x >> 5) - 4) & 3; }
 
 GFNX_DEV void epi_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+GFNX_DEV void gemm_epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(128 * kGemmEpiParts) : "memory"); }
 
 struct ItemSeq {  // the items a CTA processes, in order
   int first, count, stride;
@@ -111,7 +114,7 @@ GFNX_DEV void item_mn(const GemmGeom& g, int item, int& m, int& n) {
 }
 
 template <int BN, bool kResB, class Epi>
-__global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmGeom g, typename Epi::Args e) {
+__global__ void __launch_bounds__(kGemmKThreads, 1) k_gemm(GemmGeom g, typename Epi::Args e) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   constexpr int kStageA = kTile * 128, kStageB = BN * 128;
@@ -198,8 +201,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmGeom g, typename E
         umma_commit(&tfull[buf]);
       }
     }
-  } else if (warp >= 4) {  // ---- epilogue
-    const int ew = warp - 4, quarter = ew & 3, half = ew >> 2;
+  } else if (warp >= 4) {  // ---- epilogue: 16 warps = TMEM lane quarter x column quarter
+    const int ew = warp - 4, quarter = ew & 3, part = ew >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
     for (int j = 0; j < seq.count; ++j) {
@@ -207,12 +210,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmGeom g, typename E
       item_mn<kResB>(g, seq.item(j), m, n);
       const uint32_t buf = j & 1;
       typename Epi::Local loc;
-      Epi::begin(e, m, n, row, half, loc);
+      Epi::begin(e, m, n, row, part, loc);
       mbar_wait(&tfull[buf], (j >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
-      for (int q = 0; q < BN / 64; ++q) {
-        const int col0 = half * (BN / 2) + q * 32;
+      for (int q = 0; q < BN / (32 * kGemmEpiParts); ++q) {
+        const int col0 = part * (BN / kGemmEpiParts) + q * 32;
         uint32_t r[32];
         tmem_ld32(lane_base + buf * BN + col0, r);
         tmem_wait_ld();
@@ -222,11 +225,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_gemm(GemmGeom g, typename E
         Epi::apply(e, m, n, row, col0, v, scratch, loc);
       }
       tc_fence_before();
-      Epi::row_done(e, m, n, row, half, loc);
-      epi_bar();
+      Epi::row_done(e, m, n, row, part, scratch, loc);
+      gemm_epi_bar();
       if (tid == 128) mbar_arrive_local(&tempty[buf]);
       Epi::finish(e, m, n, scratch);
-      epi_bar();
+      gemm_epi_bar();
     }
   }
   __syncthreads();
@@ -241,11 +244,11 @@ void launch_gemm(Ctx& c, const char* name, const GemmGeom& g, const typename Epi
   if (g.KB <= 4) {
     constexpr int smem = gemm_smem_bytes<BN, true>();
     set_smem_once(k_gemm<BN, true, Epi>, smem);
-    k_gemm<BN, true, Epi><<<grid, kGemmThreads, smem, c.stream>>>(g, e);
+    k_gemm<BN, true, Epi><<<grid, kGemmKThreads, smem, c.stream>>>(g, e);
   } else {
     constexpr int smem = gemm_smem_bytes<BN, false>();
     set_smem_once(k_gemm<BN, false, Epi>, smem);
-    k_gemm<BN, false, Epi><<<grid, kGemmThreads, smem, c.stream>>>(g, e);
+    k_gemm<BN, false, Epi><<<grid, kGemmKThreads, smem, c.stream>>>(g, e);
   }
   c.launches++;
 }

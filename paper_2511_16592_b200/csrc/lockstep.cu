@@ -306,9 +306,22 @@ struct LogEpi : EpiBase {
     l.s = l.s * __expf(l.mx - nm) + s;  // l.mx = -inf -> factor 0
     l.mx = nm;
   }
-  static __device__ void row_done(const Args& e, int m, int n, int row, int half, Local& l) {
+  // the four 64-column parts of a row leave (max, sum exp) partials in scratch; finish()
+  // merges the two parts of each 128-column group (online-softmax combine)
+  static __device__ void row_done(const Args&, int, int, int row, int part, float* scratch, Local& l) {
+    scratch[(row * 4 + part) * 2] = l.mx;
+    scratch[(row * 4 + part) * 2 + 1] = l.s;
+  }
+  static __device__ void finish(const Args& e, int m, int n, const float* scratch) {
+    const int c = threadIdx.x - 128;  // 256 of the 512 epilogue threads: (row, group)
+    if (c >= 2 * kTile) return;
+    const int row = c >> 1, g = c & 1;
+    const float m0 = scratch[(row * 4 + 2 * g) * 2], s0 = scratch[(row * 4 + 2 * g) * 2 + 1];
+    const float m1 = scratch[(row * 4 + 2 * g + 1) * 2], s1 = scratch[(row * 4 + 2 * g + 1) * 2 + 1];
+    const float mx = fmaxf(m0, m1);
+    const float sum = (m0 == -INFINITY ? 0.f : s0 * __expf(m0 - mx)) + (m1 == -INFINITY ? 0.f : s1 * __expf(m1 - mx));
     const int b = m * kTile + row - e.row_base;
-    e.stats[(size_t)b * e.G + 2 * n + half] = make_float2(l.mx, l.s);
+    e.stats[(size_t)b * e.G + 2 * n + g] = make_float2(mx, sum);
   }
 };
 
@@ -583,7 +596,8 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     Lock<E>::load_lw(e.P, e.stst + r * e.P.SW, l.lw);
   }
   static __device__ void finish(const Args& e, int m, int n, const float* scratch) {
-    const int c = threadIdx.x - 128;  // 256 epilogue threads, one output column each
+    const int c = threadIdx.x - 128;  // the first 256 epilogue threads, one output column each
+    if (c >= 256) return;
     const float s = scratch[c] + scratch[256 + c] + scratch[512 + c] + scratch[768 + c];
     e.bpart[(size_t)m * e.bw + e.boff + n * 256 + c] = s;
   }
@@ -629,6 +643,7 @@ struct DgradEpi : EpiBase {  // masked by ReLU bits -> dz image + bias column su
   struct Local {};
   static __device__ void finish(const Args& e, int m, int, const float* scratch) {
     const int c = threadIdx.x - 128;
+    if (c >= 256) return;
     const float s = scratch[c] + scratch[256 + c] + scratch[512 + c] + scratch[768 + c];
     e.bpart[(size_t)m * e.bw + e.boff + c] = s;
   }
