@@ -874,15 +874,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   };
   bool bad = false;
   auto set_features = [&](const typename Env::State& st) {  // observation as a bit set
-    uint32_t m[4] = {0u, 0u, 0u, 0u};
+    // two scalar 64-bit halves (a 4-word array gets indexed by f >> 5 and lands in local memory)
+    uint64_t lo = 0ull, hi = 0ull;
     Env::features(P, st, [&](int f, double x) {
       if (x != 1.0 || f >= 128) bad = true;  // this path takes 0/1 observations only
-#pragma unroll
-      for (int w = 0; w < 4; ++w)
-        if ((f >> 5) == w) m[w] |= 1u << (f & 31);
+      const uint64_t bit = 1ull << (f & 63);
+      lo |= f < 64 ? bit : 0ull;
+      hi |= f >= 64 ? bit : 0ull;
     });
-    row_fm[row][0] = make_uint2(m[0], m[1]);
-    row_fm[row][1] = make_uint2(m[2], m[3]);
+    row_fm[row][0] = make_uint2((uint32_t)lo, (uint32_t)(lo >> 32));
+    row_fm[row][1] = make_uint2((uint32_t)hi, (uint32_t)(hi >> 32));
   };
 
   typename Env::State s;
@@ -1106,8 +1107,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
       }
       // ReLU mask of h1 (packed in TA) and the full h2 row (packed in TA2): emission + mask
-      uint32_t mw[H / 32];
-#pragma unroll 1
+      uint32_t mw[H / 32];  // fully unrolled loops keep mw in registers
+#pragma unroll
       for (int q = 0; q < H / 64; ++q) {  // 32 packed columns = 64 units per load
         uint32_t r[32];
         tmem_ld32(lane_base + TA + 32 * q, r);
@@ -1127,7 +1128,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
       }
       const int prow = gslot & (kTile - 1);
-#pragma unroll 1
+#pragma unroll
       for (int q = 0; q < H / 64; ++q) {  // 64-unit block q of h2
         uint32_t r[32];
         tmem_ld32(lane_base + TA2 + 32 * q, r);
