@@ -411,16 +411,19 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     if (h2) {
       const int src = __ffs(h2) - 1;
       if (lane == src) {
+        // first positive column whose running sum passes x, else the last positive one
+        // (unrolled selects: w4 stays in registers)
         double acc = ci - ls;
-        pick = 3;
+        int first = -1, lastpos = 0;
+#pragma unroll
         for (int e = 0; e < 4; ++e) {
           acc += w4[e];
-          if (w4[e] > 0.0 && x < acc) {
-            pick = e;
-            break;
+          if (w4[e] > 0.0) {
+            if (first < 0 && x < acc) first = e;
+            lastpos = e;
           }
         }
-        while (pick > 0 && w4[pick] == 0.0) --pick;
+        pick = first >= 0 ? first : lastpos;
       }
       pick = __shfl_sync(0xffffffffu, pick, src);
       act = grp * 128 + src * 4 + pick;
@@ -1407,15 +1410,32 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
         } else {
           for (int i = 0; i < P.SW; ++i) a.stst[r * P.SW + i] = w[i];
-          typename E::State s;
-          E::unpack(P, w, s);
-          const bool term = E::step(P, s, act);
-          E::pack(P, s, a.cur + (size_t)b * P.SW);
+          uint32_t* cw = a.cur + (size_t)b * P.SW;
+          bool term;
+          int np;
+          if constexpr (std::is_same<E, IsingEnv>::value) {
+            // packed step (IsingEnv::step): assign site act / 2, spin up when act is odd;
+            // every step assigns one site, so count = t + 1
+            const int site = act >> 1, nw = P.SW / 2;
+            const uint32_t bit = 1u << (site & 31);
+            cw[site >> 5] = w[site >> 5] | bit;
+            if (act & 1) cw[nw + (site >> 5)] = w[nw + (site >> 5)] | bit;
+            np = t + 1;
+            term = np == P.is_D;
+          } else {
+            typename E::State s;
+            E::unpack(P, w, s);
+            term = E::step(P, s, act);
+            E::pack(P, s, cw);
+            np = E::num_parents(P, s);
+          }
           a.batch.actions[bt] = (int16_t)act;
-          a.batch.nparents[bt] = (uint16_t)E::num_parents(P, s);
+          a.batch.nparents[bt] = (uint16_t)np;
           a.last_act[b] = act;
           s_lact[j][row] = act;
           if (term) {
+            typename E::State s;
+            E::unpack(P, cw, s);
             a.batch.lengths[b] = t + 1;
             a.batch.log_rewards[b] = E::log_reward(P, s);
             E::pack(P, s, a.batch.term_state + (size_t)b * P.SW);

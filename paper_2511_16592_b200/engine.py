@@ -16,7 +16,8 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgfnx.so")
+# GFNX_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("GFNX_LIB") or os.path.join(HERE, "libgfnx.so")
 _LIB = None
 
 
