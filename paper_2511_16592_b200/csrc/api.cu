@@ -994,13 +994,16 @@ gfnx_status gfnx_counters(gfnx_ctx* h, int64_t* out, int32_t n) {
   });
 }
 
+// diagnostic clock slots: rollout [0..8], wgrad passes [9..11], sampler sub-phases [12..14],
+// bwd phases [15..20]
+constexpr int kPhaseSlots = 24;
+
 gfnx_status gfnx_phase_timers(gfnx_ctx* h, int32_t mode, int64_t* out, int32_t n) {
   return guard(h, [&] {
     Ctx& c = h->c;
     if (mode == 1) {
-      if (!c.phase) cuda_check(cudaMalloc(&c.phase, sizeof(long long) * 16), "phase timers");
-      // (16 slots)
-      cuda_check(cudaMemsetAsync(c.phase, 0, sizeof(long long) * 16, c.stream), "phase timers");
+      if (!c.phase) cuda_check(cudaMalloc(&c.phase, sizeof(long long) * kPhaseSlots), "phase timers");
+      cuda_check(cudaMemsetAsync(c.phase, 0, sizeof(long long) * kPhaseSlots, c.stream), "phase timers");
     } else if (mode == 0) {
       if (c.phase) {
         cudaStreamSynchronize(c.stream);
@@ -1008,10 +1011,10 @@ gfnx_status gfnx_phase_timers(gfnx_ctx* h, int32_t mode, int64_t* out, int32_t n
       }
       c.phase = nullptr;
     } else if (c.phase) {
-      long long v[16];
+      long long v[kPhaseSlots];
       cuda_check(cudaMemcpyAsync(v, c.phase, sizeof v, cudaMemcpyDeviceToHost, c.stream), "phase timers");
       cuda_check(cudaStreamSynchronize(c.stream), "sync");
-      for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
+      for (int i = 0; i < n && i < kPhaseSlots; ++i) out[i] = v[i];
       cuda_check(cudaMemsetAsync(c.phase, 0, sizeof v, c.stream), "phase timers");
     }
   });

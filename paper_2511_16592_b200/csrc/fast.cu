@@ -1709,7 +1709,7 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 
 template <int H, int NH>
 constexpr int bwd_smem_bytes() {
-  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + 8192 + 1024;
+  return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + kThreads * 8 * 4 + kThreads * 4 + 1024;
 }
 
 template <class Env, int H, int NH>
@@ -1721,6 +1721,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   uint8_t* htile = atile + kTile * H * 2;    // dhead tile [128][64]
   uint8_t* whd = htile + kTile * 64 * 2;     // head dgrad image [H][NH], non-swizzled
   float* red = reinterpret_cast<float*>(whd + H * NH * 2);  // [kThreads * 8 / H][H] bias partials
+  float* redh = red + kThreads * 8;                           // [kThreads / NH][NH] head bias partials
   constexpr int HC = H / 2;
   __shared__ uint64_t mbar;
   __shared__ uint32_t tbase;
@@ -1763,26 +1764,54 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       float pr[NH];
     };
     auto slot_of = [&](int tile) { const int r = tile * kTile + row; return tile < tiles && r < R ? a.frow_bt[r] : -1; };
+    // vector loads only: these rows are strided, so every load instruction of a warp touches
+    // 32 lines and the load/store unit, not the latency, bounds the prefetch
     auto load_row = [&](int tile, int rbt, RowIn& x) {
       const int r = tile * kTile + row;
-      const bool v = rbt >= 0;
-#pragma unroll
-      for (int q = 0; q < HC / 32; ++q) {
-        x.mk2[q] = v ? a.mask2[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
-        x.mk1[q] = v ? a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] : 0u;
+      const bool v = rbt >= 0, v0 = v && half == 0;
+      const size_t mo = (size_t)r * (H / 32) + half * (HC / 32);
+      if constexpr (HC / 32 == 4) {
+        const uint4 z = make_uint4(0u, 0u, 0u, 0u);
+        const uint4 m2 = v ? *reinterpret_cast<const uint4*>(a.mask2 + mo) : z;
+        const uint4 m1 = v ? *reinterpret_cast<const uint4*>(a.mask1 + mo) : z;
+        x.mk2[0] = m2.x; x.mk2[1] = m2.y; x.mk2[2] = m2.z; x.mk2[3] = m2.w;
+        x.mk1[0] = m1.x; x.mk1[1] = m1.y; x.mk1[2] = m1.z; x.mk1[3] = m1.w;
+      } else {
+        static_assert(HC / 32 == 2, "mask words per thread");
+        const uint2 z = make_uint2(0u, 0u);
+        const uint2 m2 = v ? *reinterpret_cast<const uint2*>(a.mask2 + mo) : z;
+        const uint2 m1 = v ? *reinterpret_cast<const uint2*>(a.mask1 + mo) : z;
+        x.mk2[0] = m2.x; x.mk2[1] = m2.y;
+        x.mk1[0] = m1.x; x.mk1[1] = m1.y;
       }
 #pragma unroll
-      for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (half == 0 && v && i < P.SW) ? a.stst[(size_t)rbt * P.SW + i] : 0u;
-      x.act = (half == 0 && v) ? a.batch.actions[rbt] : 0;
-      x.ga = (half == 0 && v) ? a.coef[(size_t)r * 4 + 0] : 0.f;
-      x.gs = (half == 0 && v) ? a.coef[(size_t)r * 4 + 1] : 0.f;
-      x.gf = (half == 0 && v && flow) ? a.coef[(size_t)r * 4 + 2] : 0.f;
+      for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (v0 && i < P.SW) ? a.stst[(size_t)rbt * P.SW + i] : 0u;
+      x.act = v0 ? a.batch.actions[rbt] : 0;
+      const float4 cf = v0 ? *reinterpret_cast<const float4*>(a.coef + (size_t)r * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+      x.ga = cf.x;
+      x.gs = cf.y;
+      x.gf = flow ? cf.z : 0.f;
+      const float4* pr4 = reinterpret_cast<const float4*>(a.rowbuf + (size_t)r * a.rs);
 #pragma unroll
-      for (int c = 0; c < NH; ++c) x.pr[c] = (half == 0 && v && c < A) ? a.rowbuf[(size_t)r * a.rs + c] : 0.f;
+      for (int c4 = 0; c4 < NH / 4; ++c4) {
+        const float4 q = (v0 && 4 * c4 < A) ? pr4[c4] : make_float4(0.f, 0.f, 0.f, 0.f);
+        x.pr[4 * c4] = q.x;
+        x.pr[4 * c4 + 1] = q.y;
+        x.pr[4 * c4 + 2] = q.z;
+        x.pr[4 * c4 + 3] = q.w;
+      }
     };
     int rbt_cur = slot_of(blockIdx.x), rbt_next = slot_of(blockIdx.x + gridDim.x);
     RowIn nx;
     load_row(blockIdx.x, rbt_cur, nx);
+    long long pc[7] = {0, 0, 0, 0, 0, 0, 0}, tclk = clock64();
+    auto pmark = [&](int k) {  // phase clocks (thread 0): slots 15..19, tiles in 20
+      if (a.phase && tid == 0) {
+        const long long tn = clock64();
+        pc[k] += tn - tclk;
+        tclk = tn;
+      }
+    };
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int r = tile * kTile + row;
       const int rbt = rbt_cur;
@@ -1791,8 +1820,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       rbt_cur = rbt_next;
       rbt_next = slot_of(tile + 2 * gridDim.x);
       load_row(tile + gridDim.x, rbt_cur, nx);  // in flight during this tile
-      if (tid == 0) bulk_wait_read0();  // previous tile's dz1 / dhead stores have left smem
-      __syncthreads();
+      pmark(6);
+      // (htile is free: the previous tile waited for its dhead / dz2 stores before dz1; the
+      // dz1 store drains from atile while dlogits and the head MMA run)
       uint32_t mk2[HC / 32], mk1[HC / 32];
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
@@ -1836,23 +1866,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       fence_proxy_async();
       tc_fence_before();
       __syncthreads();
+      pmark(0);
       if (tid == 0) {  // dh2 = dhead Wf^T (+ dflow wfl^T): 128 x H x NH on the tensor cores
         tc_fence_after();
         bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
         bulk_commit();
         mma_k_sw128_none<H, NH>(tmem, htile, whd);
         umma_commit(&mbar);
-      }
-      if (tid <= A) {  // head bias sums (fixed row order, four interleaved partial sums)
-        float s4[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 8
-        for (int rr = 0; rr < kTile; ++rr)
-          s4[rr & 3] += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(rr, tid, kTile)));
-        acc_bh += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+        bulk_wait_read0();  // the previous tile's dz1 store has left atile
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
       tc_fence_after();
+      __syncthreads();
+      pmark(1);
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
         const int col = c0 + q * 32;
@@ -1869,6 +1896,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       fence_proxy_async();
       tc_fence_before();
       __syncthreads();
+      pmark(2);
       if (tid == 0) {
         tc_fence_after();
         bulk_s2g(a.dz2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
@@ -1894,6 +1922,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         }
 #pragma unroll
         for (int e = 0; e < 8; ++e) red[rg * H + 8 * cg + e] = sv[e];
+        // head bias: thread = (16-row group, head column), fixed order
+        constexpr int HG = kThreads / NH, HR = kTile / HG;
+        const int hc = tid % NH, hg = tid / NH;
+        float hs = 0.f;
+#pragma unroll
+        for (int i = 0; i < HR; ++i)
+          hs += __bfloat162float(*reinterpret_cast<const __nv_bfloat16*>(htile + sw128_offset(hg * HR + i, hc, kTile)));
+        redh[hg * NH + hc] = hs;
         __syncthreads();
         if (tid < H) {
           float t = 0.f;
@@ -1901,12 +1937,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
           for (int g = 0; g < RG; ++g) t += red[g * H + tid];
           acc_b2 += t;
         }
+        if (tid <= A) {
+          float t = 0.f;
+#pragma unroll
+          for (int g = 0; g < HG; ++g) t += redh[g * NH + tid];
+          acc_bh += t;
+        }
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
       tc_fence_after();
       if (tid == 0) bulk_wait_read0();
       __syncthreads();
+      pmark(3);
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
         const int col = c0 + q * 32;
@@ -1927,7 +1970,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         bulk_s2g(a.dz1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
         bulk_commit();
       }
+      pmark(4);
+      pc[5] += 1;
     }
+    if (a.phase && tid == 0)
+      for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)a.phase + 15 + k, (unsigned long long)pc[k]);
     if (tid == 0) bulk_wait0();
     __syncthreads();
     if (warp == 0) tmem_dealloc<H>(tmem);
