@@ -915,20 +915,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   };
   // copy this thread's 128 packed activation columns (two 64-feature blocks of its row)
   // from TMEM into the row's emission slot of `img`
-  auto emit = [&](__nv_bfloat16* img, uint32_t ta, bool valid, int gs) {
-#pragma unroll 1
-    for (int j = 0; j < 2; ++j) {
-      uint32_t r[32];
-      tmem_ld32(lane_base + ta + (c0 >> 1) + 32 * j, r);
-      tmem_wait_ld();
-      if (valid && a.emit_mode != 1) {
-        const int prow = gs & (kTile - 1);
-        uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 +
-                       ((c0 >> 6) + j) * (kTile * 128) + prow * 128;
-        st_line_sw128(dst, prow, r);
-      }
+  // The emission stores are spread over the MMA waits of the step chain: h1 block 0 of the
+  // thread's half during the hidden MMA, block 1 during the head MMA; h2 blocks 0-1 by the
+  // idle half while the row samples, blocks 2-3 during the next step's layer-1 MMA (TA2
+  // holds h2 until the next hidden epilogue).
+  auto emit_block = [&](__nv_bfloat16* img, uint32_t ta, int blk, bool valid, int gs) {
+    uint32_t r[32];
+    tmem_ld32(lane_base + ta + 32 * blk, r);
+    tmem_wait_ld();
+    if (valid && a.emit_mode != 1) {
+      const int prow = gs & (kTile - 1);
+      uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 + blk * (kTile * 128) +
+                     prow * 128;
+      st_line_sw128(dst, prow, r);
     }
   };
+  bool h2_pend = false;  // h2 blocks 2-3 of the previous step's row slot still to emit
+  int h2_gs = 0;
   int nact;
   while ((nact = __syncthreads_count(active || pending)) > 0) {
     mark(0);
@@ -956,6 +959,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       mma_tk<H, 128>(tmem, tmem + TA, w1img, false);
       umma_commit(&mbar);
     }
+    emit_block(a.h2, TA2, 2 + half, h2_pend, h2_gs);  // (warp-collective TMEM load)
+    h2_pend = false;
     mma_join();
     // h1 = ReLU(acc + b1) -> packed into TMEM (the hidden MMA's A operand) + ReLU mask
 #pragma unroll 1
@@ -1019,7 +1024,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       const int rb = row_b[row];
       row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
     }
-    emit(a.h1, TA, my_valid, gslot);
+    emit_block(a.h1, TA, (c0 >> 6), my_valid, gslot);
     mma_join();
     mark(2);
     // (3) h2 = ReLU(acc + b2) -> packed into TMEM (own columns: h1 stays for its mask)
@@ -1044,6 +1049,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       mma_tk<NH, H>(tmem + TH, tmem + TA2, whimg, false);
       umma_commit(&mbar);
     }
+    emit_block(a.h1, TA, (c0 >> 6) + 1, my_valid, gslot);
     mma_join();
     mark(4);
     float logit[NH];
@@ -1141,7 +1147,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         }
         mw[2 * q] = relu_mask16(lo);
         mw[2 * q + 1] = relu_mask16(hi);
-        if (my_valid && a.emit_mode != 1) {
+        if (q < 2 && my_valid && a.emit_mode != 1) {
           uint8_t* dst = reinterpret_cast<uint8_t*>(a.h2) + (size_t)(gslot >> 7) * kTile * H * 2 + q * (kTile * 128) +
                          prow * 128;
           st_line_sw128(dst, prow, r);
@@ -1153,9 +1159,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
       }
     }
+    h2_pend = my_valid;
+    h2_gs = gslot;
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
     mark(5);
   }
+  emit_block(a.h2, TA2, 2 + half, h2_pend, h2_gs);  // the last step's deferred h2 blocks
   if (a.phase && tid == 0)
     for (int k = 0; k < 12; ++k) atomicAdd((unsigned long long*)a.phase + (k < 9 ? k : k + 3), (unsigned long long)ph[k]);
   if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
