@@ -861,10 +861,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   const uint32_t tmem = tbase;
   const uint32_t lane_base = tmem + ((uint32_t)(quarter * 32) << 16);
 
+  // every thread waits on the MMA's mbarrier itself (no CTA barrier): the next commit can
+  // only follow a publish() barrier, so no thread can miss a phase
   auto mma_join = [&]() {
-    if (tid == 0) mbar_wait(&mbar, phase);
+    mbar_wait(&mbar, phase);
     phase ^= 1;
-    __syncthreads();
     tc_fence_after();
   };
   auto publish = [&]() {  // tcgen05.st of the A operand -> visible to the MMA issuer
@@ -983,6 +984,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       pending = false;
     }
     publish();
+    // (2) hidden layer: acc[128 x H] = h1 W2^T, A from TMEM, one round (issued before the
+    //     emission-slot bookkeeping, which overlaps it)
+    if (tid == 0) {
+      tc_fence_after();
+      mma_tk<H, H>(tmem, tmem + TA, w2img, false);
+      umma_commit(&mbar);
+    }
     bool my_valid = false;
     int gslot = 0;
     bool crossed = false;
@@ -1014,12 +1022,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       if (crossed && tid == kThreads - 1) claim = atomicAdd(a.tilectr, 1);
     }
     mark(1);
-    // (2) hidden layer: acc[128 x H] = h1 W2^T, A from TMEM, one round
-    if (tid == 0) {
-      tc_fence_after();
-      mma_tk<H, H>(tmem, tmem + TA, w2img, false);
-      umma_commit(&mbar);
-    }
     if (half == 1) {  // the row's uniform while the MMA runs (rng.cpp:64-66)
       const int rb = row_b[row];
       row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
