@@ -1082,10 +1082,11 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       umma_commit(&mbar);
     }
   };
+  // every thread waits on the MMA's mbarrier (no CTA barrier): a publish() barrier
+  // separates consecutive commits, so no thread can miss a phase
   auto mma_wait = [&]() {
-    if (tid == 0) mbar_wait(&mbar, mph);
+    mbar_wait(&mbar, mph);
     mph ^= 1;
-    __syncthreads();
     tc_fence_after();
   };
   auto publish = [&]() {
