@@ -1197,6 +1197,21 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     }
     }
     pmark(0);
+    // activation image of (layer, tile) from its packed TMEM columns, deferred into the next
+    // MMA's wait (the columns stay intact until the next epilogue of the same tile)
+    int pend_l = -1, pend_j = 0;
+    size_t pend_m = 0;
+    auto emit_pending = [&]() {
+      if (pend_l < 0) return;
+#pragma unroll 1
+      for (int blk = 0; blk < 2; ++blk) {
+        uint32_t w32[32];
+        tmem_ld32(lane_base + kH + 128 * pend_j + (c0 >> 1) + 32 * blk, w32);
+        tmem_wait_ld();
+        st_line_sw(a.h[pend_l] + pend_m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
+      }
+      pend_l = -1;
+    };
     // ---- hidden layers 2..NL: MMA per tile (A from TMEM), epilogue back into the same columns
     const int l0 = a.l1_mma ? 0 : 1;
     for (int l = l0; l < a.NL; ++l) {
@@ -1232,6 +1247,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         mma_issue(tmem, tmem + kH + 128 * j);
         if (half == 1 && l == l0 && j < kPersistMaxTiles)  // the row's uniform while the MMA runs
           row_u[j][row] = uniform_scalar(fold_in(skeys[t], (uint64_t)(a.b0 + b)));
+        emit_pending();
         mma_wait();
         if (j == ntile - 1 && tid == 0) load_w(l + 1 < a.NL ? l + 1 : a.NL);  // wbuf free now
         uint32_t mw[4];
@@ -1256,14 +1272,9 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           tmem_st16(lane_base + kH + 128 * j + (col >> 1), pk);
         }
         __stcs(reinterpret_cast<uint4*>(a.mask[l] + r * (kH / 8) + half * 16), make_uint4(mw[0], mw[1], mw[2], mw[3]));
-        tmem_wait_st();
-#pragma unroll 1
-        for (int blk = 0; blk < 2; ++blk) {
-          uint32_t w32[32];
-          tmem_ld32(lane_base + kH + 128 * j + (c0 >> 1) + 32 * blk, w32);
-          tmem_wait_ld();
-          st_line_sw(a.h[l] + m * (kTile * kH * 2) + ((c0 >> 6) + blk) * (kTile * 128) + row * 128, row, w32);
-        }
+        pend_l = l;
+        pend_j = j;
+        pend_m = m;
         publish();
       }
     }
@@ -1285,6 +1296,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       const uint32_t* w = a.cur + (size_t)b * P.SW;
       uint32_t lw[Lock<E>::kLW];
       Lock<E>::load_lw(P, w, lw);
+      emit_pending();  // the last hidden layer's last tile
       mma_wait();
       if (j == ntile - 1 && tid == 0) load_w(a.l1_mma ? 0 : 1);  // next step's first layer
       uint32_t lmw[4];
