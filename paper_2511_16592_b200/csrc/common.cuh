@@ -88,6 +88,14 @@ GFNX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// ReLU + round-to-nearest bf16 pair in one cvt (cvt.rn.relu clamps negatives to +0):
+// the same bits as pack_bf16x2(fmaxf(lo, 0), fmaxf(hi, 0)) for every non-NaN input
+GFNX_DEV uint32_t pack_bf16x2_relu(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 GFNX_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 GFNX_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 

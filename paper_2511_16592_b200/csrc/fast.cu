@@ -973,8 +973,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b1s[col + 2 * i], 0.f),
-                            fmaxf(__uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1], 0.f));
+        pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + b1s[col + 2 * i],
+                                 __uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1]);
       tmem_st16(lane_base + TA + (col >> 1), pk);
     }
     if (pending) {  // the refill claim issued at the last termination lands here
@@ -1039,8 +1039,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + b2s[col + 2 * i], 0.f),
-                            fmaxf(__uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1], 0.f));
+        pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + b2s[col + 2 * i],
+                                 __uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1]);
       tmem_st16(lane_base + TA2 + (col >> 1), pk);
     }
     publish();
