@@ -452,8 +452,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     uint32_t pk[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i)
-      pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]) + (bias ? bias[2 * i] : 0.f), 0.f),
-                          fmaxf(__uint_as_float(r[2 * i + 1]) + (bias ? bias[2 * i + 1] : 0.f), 0.f));
+      pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + (bias ? bias[2 * i] : 0.f),
+                               __uint_as_float(r[2 * i + 1]) + (bias ? bias[2 * i + 1] : 0.f));
     if (mword) *mword = relu_mask16(pk);
     st_row32(atile, row, acol, pk);
   };
@@ -556,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(fmaxf(__uint_as_float(r[2 * i]), 0.f), fmaxf(__uint_as_float(r[2 * i + 1]), 0.f));
+          pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
         reinterpret_cast<uint32_t*>(row_m1[row])[col >> 5] = relu_mask16(pk);
         st_row32(atile, row, col, pk);
       }
@@ -1365,7 +1365,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_fwd(TrainArgs a) {
       }
       uint32_t pk[16];
 #pragma unroll
-      for (int i = 0; i < 16; ++i) pk[i] = valid ? pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f)) : 0u;
+      for (int i = 0; i < 16; ++i) pk[i] = valid ? pack_bf16x2_relu(v[2 * i], v[2 * i + 1]) : 0u;
       const uint32_t mb = relu_mask16(pk);
       if (valid) a.mask1[(size_t)r * (H / 32) + half * (HC / 32) + q] = mb;
       if (!SPLIT || half == 0) {

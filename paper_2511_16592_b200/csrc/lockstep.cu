@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
   uint32_t mb = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    pk[e] = pack_bf16x2(fmaxf(v[2 * e], 0.f), fmaxf(v[2 * e + 1], 0.f));
+    pk[e] = pack_bf16x2_relu(v[2 * e], v[2 * e + 1]);
     mb |= (bf16_lo(pk[e]) > 0.f ? 1u : 0u) << (2 * e);
     mb |= (bf16_hi(pk[e]) > 0.f ? 1u : 0u) << (2 * e + 1);
   }
@@ -237,8 +237,8 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float4 q = __ldg(bb + i);
-      pk[2 * i] = pack_bf16x2(fmaxf(v[4 * i] + q.x, 0.f), fmaxf(v[4 * i + 1] + q.y, 0.f));
-      pk[2 * i + 1] = pack_bf16x2(fmaxf(v[4 * i + 2] + q.z, 0.f), fmaxf(v[4 * i + 3] + q.w, 0.f));
+      pk[2 * i] = pack_bf16x2_relu(v[4 * i] + q.x, v[4 * i + 1] + q.y);
+      pk[2 * i + 1] = pack_bf16x2_relu(v[4 * i + 2] + q.z, v[4 * i + 3] + q.w);
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i)  // bit 2i / 2i+1 <-> columns 2i / 2i+1 (values >= 0: nonzero = active)
@@ -1176,7 +1176,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           *reinterpret_cast<float4*>(pre + col + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
         uint32_t pk[16];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(fmaxf(v[2 * i], 0.f), fmaxf(v[2 * i + 1], 0.f));
+        for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2_relu(v[2 * i], v[2 * i + 1]);
         mw[q] = relu_mask32_seq(pk);
         tmem_st16(lane_base + kH + 128 * j + ((c0 + col) >> 1), pk);
       }
@@ -1263,10 +1263,10 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 bq = bb[i];
-            pk[2 * i] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i]) + bq.x, 0.f),
-                                    fmaxf(__uint_as_float(rr[4 * i + 1]) + bq.y, 0.f));
-            pk[2 * i + 1] = pack_bf16x2(fmaxf(__uint_as_float(rr[4 * i + 2]) + bq.z, 0.f),
-                                        fmaxf(__uint_as_float(rr[4 * i + 3]) + bq.w, 0.f));
+            pk[2 * i] = pack_bf16x2_relu(__uint_as_float(rr[4 * i]) + bq.x,
+                                         __uint_as_float(rr[4 * i + 1]) + bq.y);
+            pk[2 * i + 1] = pack_bf16x2_relu(__uint_as_float(rr[4 * i + 2]) + bq.z,
+                                             __uint_as_float(rr[4 * i + 3]) + bq.w);
           }
           mw[q] = relu_mask32_seq(pk);
           tmem_st16(lane_base + kH + 128 * j + (col >> 1), pk);
