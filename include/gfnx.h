@@ -172,6 +172,16 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step)
  * NULL; tv: total variation to R / Z (the `tv_exact` metric), or NULL. bf16 fast path. */
 gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_t n, double* tv);
 
+/* Terminal-state FIFO of the `tv_buffer` metric, hypergrid (FifoBuffer, buffer.hpp:13-55,
+ * fed by buffer.push_batch(batch.terminal_keys), train.cpp:231). reset: new empty buffer of
+ * `capacity` >= 1 (the reference default is 200000); push: appends the resident batch's
+ * terminal states in trajectory order, oldest evicted first (stream-ordered, no host sync);
+ * tv_buffer: tv_distance(buffer.empirical(), grid_exact_distribution) (metrics.cpp:35-48)
+ * and the buffer size. Each rank's buffer holds its own trajectory slice. */
+gfnx_status gfnx_buffer_reset(gfnx_ctx* ctx, int64_t capacity);
+gfnx_status gfnx_buffer_push(gfnx_ctx* ctx);
+gfnx_status gfnx_tv_buffer(gfnx_ctx* ctx, int64_t* size, double* tv);
+
 gfnx_status gfnx_rollout(gfnx_ctx* ctx, int64_t it, double eps);
 /* Loss + gradient over the resident batch, NCCL all-reduce (world > 1), Adam on
  * the main params with learning rate lr and (TB) on logZ with z_lr (train.cpp:164-192).

@@ -499,6 +499,7 @@ void gfnx_destroy(gfnx_ctx* h) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
   if (c.fast) fast_free(c);
+  hg_buffer_free(c);
   if (c.phase) cudaFree(c.phase);
   void* ptrs[] = {c.d_modes, c.d_bs_logr, c.d_is_nbr, c.d_is_J, c.d_dag_cache, c.d_neglog,
                   c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars,
@@ -764,6 +765,22 @@ gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* h, double* marginal, int64_t 
       for (size_t x = 0; x < pt.size(); ++x) s += fabs(pt[x] - r[x] / zsum);
       *tv = 0.5 * s;
     }
+  });
+}
+
+gfnx_status gfnx_buffer_reset(gfnx_ctx* h, int64_t capacity) {
+  return guard(h, [&] { hg_buffer_reset(h->c, capacity); });
+}
+
+gfnx_status gfnx_buffer_push(gfnx_ctx* h) {
+  return guard(h, [&] { hg_buffer_push(h->c); });
+}
+
+gfnx_status gfnx_tv_buffer(gfnx_ctx* h, int64_t* size, double* tv) {
+  return guard(h, [&] {
+    const double v = hg_buffer_tv(h->c);
+    if (size) *size = h->c.tbuf.size;
+    if (tv) *tv = v;
   });
 }
 

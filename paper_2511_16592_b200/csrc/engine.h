@@ -69,6 +69,11 @@ void launch_row_scan(Ctx& c, bool counts = true);
 void ensure_row0(Ctx& c);              // row0 / row_bt of the resident batch (lazy after a fused rollout)
 bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row counts itself
 void fast_hg_marginal(Ctx& c, std::vector<double>* pt);  // exact terminal marginal (hypergrid)
+// tv_buffer metric (hypergrid): terminal-state FIFO + histogram on the device — fast.cu
+void hg_buffer_reset(Ctx& c, int64_t capacity);
+void hg_buffer_push(Ctx& c);
+double hg_buffer_tv(Ctx& c);
+void hg_buffer_free(Ctx& c);
 
 struct Ctx {
   gfnx_env_desc env{};
@@ -127,6 +132,17 @@ struct Ctx {
 
   // fast-mode state (opaque, fast.cu)
   void* fast = nullptr;
+
+  // terminal-state FIFO of the tv_buffer metric (FifoBuffer, buffer.hpp:13-55): ring of
+  // cell indices + per-cell counts on the device; head / size tracked on the host (every
+  // push appends exactly Bl items, stream-ordered)
+  struct TermBuffer {
+    int32_t* fifo = nullptr;  // [cap] cell index (coordinate 0 fastest)
+    int32_t* hist = nullptr;  // [cells] occurrences in the ring
+    double* p = nullptr;      // [cells] grid_exact_distribution probabilities
+    double* out = nullptr;    // [1] last tv
+    int64_t cap = 0, head = 0, size = 0, cells = 0;
+  } tbuf;
 
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t user_ev[16] = {};

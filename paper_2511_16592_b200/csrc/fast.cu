@@ -2685,6 +2685,129 @@ void fast_hg_marginal(Ctx& c, std::vector<double>* pt) {
   for (int64_t r = 0; r < n; ++r) (*pt)[cells[r]] = ptr[r];  // back to row-major cell order
 }
 
+// ---------------------------------------------------------------------------
+// tv_buffer (metrics.cpp:35-48 over the FifoBuffer of train.cpp:231, hypergrid)
+
+// append terminal states b in [b_lo, Bl) of the resident batch at ring positions
+// (head + b) % cap, evicting what those positions held (oldest-first, buffer.hpp:24-28); the
+// positions of one push are distinct, the counts are integer atomics (order-independent)
+__global__ void k_hg_buffer_push(const uint32_t* __restrict__ term, int SW, int dim, int side, int Bl, int b_lo,
+                                 int64_t head, int64_t cap, int64_t size, int32_t* fifo, int32_t* hist) {
+  const int b = b_lo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= Bl) return;
+  int64_t cell = 0, stride = 1;
+  for (int i = 0; i < dim; ++i) {  // packed state: byte i = coordinate i
+    cell += (int64_t)((term[(size_t)b * SW + (i >> 2)] >> (8 * (i & 3))) & 0xffu) * stride;
+    stride *= side;
+  }
+  const int64_t pos = (head + b) % cap;
+  if (size == cap || pos < size) atomicSub(hist + fifo[pos], 1);
+  fifo[pos] = (int32_t)cell;
+  atomicAdd(hist + cell, 1);
+}
+
+// tv_distance(empirical, exact) (metrics.cpp:35-48): 0.5 * (sum_x |phat_x - p_x| + 1 - covered),
+// fixed-order block reduction in fp64
+__global__ void __launch_bounds__(1024) k_hg_buffer_tv(const int32_t* __restrict__ hist, const double* __restrict__ p,
+                                                       int64_t cells, int64_t size, double* out) {
+  __shared__ double sa[1024], sc[1024];
+  double acc = 0.0, cov = 0.0;
+  for (int64_t x = threadIdx.x; x < cells; x += 1024) {
+    const int h = hist[x];
+    const double ph = h > 0 ? (double)h / (double)size : 0.0;
+    if (h > 0) cov += ph;
+    acc += fabs(ph - p[x]);
+  }
+  sa[threadIdx.x] = acc;
+  sc[threadIdx.x] = cov;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      sa[threadIdx.x] += sa[threadIdx.x + w];
+      sc[threadIdx.x] += sc[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = 0.5 * (sa[0] + (1.0 - sc[0]));
+}
+
+void hg_buffer_free(Ctx& c) {
+  Ctx::TermBuffer& t = c.tbuf;
+  for (void* q : {(void*)t.fifo, (void*)t.hist, (void*)t.p, (void*)t.out})
+    if (q) cudaFree(q);
+  t = Ctx::TermBuffer{};
+}
+
+void hg_buffer_reset(Ctx& c, int64_t capacity) {
+  if (c.env.kind != GFNX_ENV_HYPERGRID) raise_error(GFNX_ERR_CONFIG, "tv_buffer: hypergrid only");
+  if (capacity < 1) raise_error(GFNX_ERR_CONFIG, "FifoBuffer: capacity must be >= 1");
+  const int d = c.env.hg_dim, side = c.env.hg_side;
+  int64_t cells = 1;
+  for (int i = 0; i < d; ++i) cells *= side;
+  if (cells > (1 << 26) || capacity > (int64_t)1 << 31) raise_error(GFNX_ERR_CONFIG, "tv_buffer: too large");
+  hg_buffer_free(c);
+  Ctx::TermBuffer& t = c.tbuf;
+  t.cap = capacity;
+  t.cells = cells;
+  // grid_exact_distribution (hypergrid.cpp:121-140): exp(log reward) in the reference's
+  // enumeration order (last coordinate fastest), normalised by their running sum
+  std::vector<double> v(cells), p(cells);
+  std::vector<int> co(d, 0);
+  double z = 0.0;
+  for (int64_t n = 0; n < cells; ++n) {
+    uint32_t p1 = 1, p2 = 1;
+    int64_t x = 0, st = 1;
+    for (int i = 0; i < d; ++i) {
+      p1 &= (c.P.hg_f1[co[i] >> 5] >> (co[i] & 31)) & 1u;
+      p2 &= (c.P.hg_f2[co[i] >> 5] >> (co[i] & 31)) & 1u;
+      x += co[i] * st;
+      st *= side;
+    }
+    v[n] = exp(c.P.hg_logr[p1 | (p2 << 1)]);
+    z += v[n];
+    p[x] = v[n];
+    for (int i = d - 1; i >= 0; --i) {
+      if (++co[i] < side) break;
+      co[i] = 0;
+    }
+  }
+  for (double& q : p) q /= z;
+  cuda_check(cudaMalloc(&t.fifo, sizeof(int32_t) * capacity), "tv_buffer");
+  cuda_check(cudaMalloc(&t.hist, sizeof(int32_t) * cells), "tv_buffer");
+  cuda_check(cudaMalloc(&t.p, sizeof(double) * cells), "tv_buffer");
+  cuda_check(cudaMalloc(&t.out, sizeof(double)), "tv_buffer");
+  cuda_check(cudaMemsetAsync(t.hist, 0, sizeof(int32_t) * cells, c.stream), "tv_buffer");
+  cuda_check(cudaMemcpyAsync(t.p, p.data(), sizeof(double) * cells, cudaMemcpyHostToDevice, c.stream), "tv_buffer");
+  cuda_check(cudaStreamSynchronize(c.stream), "tv_buffer");
+}
+
+void hg_buffer_push(Ctx& c) {
+  Ctx::TermBuffer& t = c.tbuf;
+  if (!t.fifo) raise_error(GFNX_ERR_CONTRACT, "tv_buffer: gfnx_buffer_reset first");
+  if (!c.has_batch) raise_error(GFNX_ERR_CONTRACT, "tv_buffer: no resident batch");
+  const int Bl = c.Bl;
+  const int b_lo = (int64_t)Bl > t.cap ? Bl - (int)t.cap : 0;  // earlier items of the batch are overwritten
+  k_hg_buffer_push<<<(Bl - b_lo + 255) / 256, 256, 0, c.stream>>>(c.batch.term_state, c.P.SW, c.env.hg_dim,
+                                                                   c.env.hg_side, Bl, b_lo, t.head, t.cap, t.size,
+                                                                   t.fifo, t.hist);
+  c.launches++;
+  cuda_check(cudaGetLastError(), "tv_buffer push");
+  t.head = (t.head + Bl) % t.cap;
+  t.size = std::min(t.cap, t.size + Bl);
+}
+
+double hg_buffer_tv(Ctx& c) {
+  Ctx::TermBuffer& t = c.tbuf;
+  if (!t.fifo) raise_error(GFNX_ERR_CONTRACT, "tv_buffer: gfnx_buffer_reset first");
+  if (t.size == 0) raise_error(GFNX_ERR_CONTRACT, "FifoBuffer: empirical of empty buffer");
+  k_hg_buffer_tv<<<1, 1024, 0, c.stream>>>(t.hist, t.p, t.cells, t.size, t.out);
+  c.launches++;
+  double tv = 0.0;
+  cuda_check(cudaMemcpyAsync(&tv, t.out, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "tv_buffer");
+  cuda_check(cudaStreamSynchronize(c.stream), "tv_buffer");
+  return tv;
+}
+
 void fast_init(Ctx& c) {
   if (lockstep(c)) {
     std::string why;

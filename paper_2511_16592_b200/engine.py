@@ -90,6 +90,9 @@ def lib():
         L.gfnx_test_ts_mma.argtypes = [vp, vp, vp]
         L.gfnx_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_int64]
         L.gfnx_exact_terminal_marginal.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_buffer_reset.argtypes = [vp, C.c_int64]
+        L.gfnx_buffer_push.argtypes = [vp]
+        L.gfnx_tv_buffer.argtypes = [vp, vp, vp]
         L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
         L.gfnx_iteration_async.argtypes = [vp, C.c_int64, C.c_int32]
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
@@ -188,6 +191,20 @@ class Trainer:
         tv = C.c_double()
         self._check(lib().gfnx_exact_terminal_marginal(self.h, _p(m), n_cells, C.byref(tv)))
         return m, tv.value
+
+    def buffer_reset(self, capacity: int = 200000):
+        """New empty terminal-state FIFO (FifoBuffer, buffer.hpp:13-55) for `tv_buffer`."""
+        self._check(lib().gfnx_buffer_reset(self.h, capacity))
+
+    def buffer_push(self):
+        """buffer.push_batch(batch.terminal_keys) of the resident batch (train.cpp:231)."""
+        self._check(lib().gfnx_buffer_push(self.h))
+
+    def tv_buffer(self):
+        """(buffer size, tv_distance(buffer.empirical(), exact)) (metrics.cpp:35-48)."""
+        n, tv = C.c_int64(), C.c_double()
+        self._check(lib().gfnx_tv_buffer(self.h, C.byref(n), C.byref(tv)))
+        return n.value, tv.value
 
     # -- the hot path --
     def forward_rollout(self, it: int, eps: float):

@@ -59,11 +59,13 @@ def test_hypergrid_training_reaches_reference_tv_limit(objective):
     floor = np.mean([tv(np.bincount(rng.choice(len(p), BUFFER, p=p), minlength=len(p)).astype(float), p)
                      for _ in range(5)])
     tr = engine.Trainer(e, t)
+    tr.buffer_reset(BUFFER)  # the device-side tv_buffer FIFO, fed in stream order
     iters = 6250
     ring = np.zeros(BUFFER, dtype=np.int64)
     filled = 0
     for it in range(iters):
         tr.iteration_async(it, it % 2)
+        tr.buffer_push()
         if it > 0:
             _, loss, res = tr.slot_wait((it - 1) % 2)
             cells = cell_index(res["terminal_state"])
@@ -74,9 +76,11 @@ def test_hypergrid_training_reaches_reference_tv_limit(objective):
     for c in cell_index(res["terminal_state"]):
         ring[filled % BUFFER] = c
         filled += 1
+    n_dev, tv_dev = tr.tv_buffer()
     tr.close()
     assert np.isfinite(loss)
     d = tv(np.bincount(ring, minlength=len(p)).astype(float), p)
+    assert n_dev == BUFFER and abs(tv_dev - d) < 1e-9, (tv_dev, d)
     print(f"{objective}: tv {d:.4f} floor {floor:.4f} limit {1.5 * floor:.4f}")
     assert d <= 1.5 * floor, (objective, d, floor)
 
