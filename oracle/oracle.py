@@ -289,6 +289,7 @@ def ref_lib(kind: str = "port"):
         L.ref_run_bench.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_int,
                                     C.c_void_p, C.c_void_p]
         L.ref_exact_divergence.argtypes = [C.c_void_p, C.c_void_p]
+        L.ref_pearson.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_void_p]
         L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.ref_load_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         _REF[kind] = L
@@ -367,6 +368,12 @@ class RefLib:
         st = C.c_int64()
         self._check(self.L.ref_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
         return st.value
+
+    def pearson(self, step: int, mc: int = 10, test_seed: int = 1):
+        """The bitseq `pearson` metric of the current policy (train.cpp:440-454)."""
+        d = C.c_double()
+        self._check(self.L.ref_pearson(self.h, step, mc, test_seed, C.byref(d)))
+        return d.value
 
     def exact_divergence(self):
         """TV (hypergrid) / JSD (DAG) of the current policy's exact terminal marginal to the

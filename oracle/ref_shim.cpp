@@ -66,6 +66,10 @@ struct SessionBase {
   // to the target: TV for hypergrid (grid_exact_distribution) and Ising
   // (ising_exact_distribution), JSD for DAG (dag_exact_posterior) - acceptance criteria 1, 3, 5
   virtual double exact_divergence() { throw config_error("exact divergence: hypergrid, DAG and Ising only"); }
+  // the bitseq `pearson` metric (train.cpp:440-454): Pearson correlation of the Monte-Carlo
+  // terminal log-probabilities (mc_terminal_logprob, exact.hpp:229-241, `mc` backward samples)
+  // and the log-rewards over the builder's test set (generate_test_set, train.cpp:431-433)
+  virtual double pearson_metric(int64_t, int, uint64_t) { throw config_error("pearson: bitseq only"); }
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -172,6 +176,23 @@ struct Session : SessionBase {
       return tv_distance(exact_policy_marginal(env, params, graph, pol), ising_exact_distribution(*params.coupling));
     } else {
       return SessionBase::exact_divergence();
+    }
+  }
+  double pearson_metric(int64_t step, int mc, uint64_t test_seed) override {
+    if constexpr (std::is_same_v<E, SequenceEnv>) {
+      const auto* modes = dynamic_cast<const ModeSet*>(params.reward.get());
+      if (!modes) throw config_error("pearson: mode-set reward only");
+      const auto test_set = generate_test_set(*modes, fold_in(make_key(test_seed), 0x7E57));
+      const RngKey mkey = fold_in(fold_in(make_key(td.seed), 0x3E7A), step);
+      std::vector<double> log_p, log_r;
+      for (size_t i = 0; i < test_set.size(); ++i) {
+        auto inst = env.terminal_from_key(test_set[i], params);
+        log_p.push_back(mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, mc, fold_in(mkey, i)));
+        log_r.push_back(modes->log_reward(test_set[i]));
+      }
+      return pearson(log_p, log_r);
+    } else {
+      return SessionBase::pearson_metric(step, mc, test_seed);
     }
   }
   std::vector<double>& grads() override { return g; }
@@ -382,6 +403,11 @@ int ref_load_checkpoint(void* h, const char* path, int64_t* step) {
     rs->s->opt_z() = c.opt_z;
     *step = c.step;
   });
+}
+
+int ref_pearson(void* h, int64_t step, int mc, uint64_t test_seed, double* out) {
+  RefSession* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] { *out = rs->s->pearson_metric(step, mc, test_seed); });
 }
 
 int ref_exact_divergence(void* h, double* out) {

@@ -173,3 +173,32 @@ def test_device_exact_marginal_config2_grid():
     m, tv_dev = tr.exact_terminal_marginal(20 ** 4)
     assert abs(m.sum() - 1.0) < 1e-6 and 0.0 <= tv_dev <= 1.0 and np.all(m >= 0)
     tr.close()
+
+
+def test_bitseq_pearson_like_reference_criterion4():
+    """Acceptance criterion 4 (acceptance.cpp:274-340): bitseq NAR n = 8, k = 2 (4 slots, vocab
+    4), trajectory balance, MLP 2x256, lr 1e-3, z_lr 0.05, weight decay 1e-5, batch 16, eps 1e-3.
+    The builder's `pearson` metric (train.cpp:440-454: mc_terminal_logprob with 10 backward
+    samples per test string vs the log-reward, evaluated by the reference on the device-trained
+    parameters every 500 iterations) must reach 0.95. Reference: 0.9579 after 500 iterations.
+    The mode set is the builder's (generate_modes with fold_in(make_key(modes_seed), 0x30DE),
+    train.cpp:417-420); the acceptance test draws its own from make_key(15)."""
+    from oracle import oracle as O
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    e = abi.env_desc(abi.BITSEQ, bs_n_bits=8, bs_k=2)
+    t = abi.train_desc(abi.BITSEQ, batch=16, seed=3, iterations=50000)
+    tr = engine.Trainer(e, t)
+    ref = O.RefLib(e, t)
+    ref.set_params(*tr.params())
+    init = ref.pearson(0)
+    best = -1.0
+    for k in range(20):
+        tr.run(500 * k, 500)
+        ref.set_params(*tr.params())
+        best = max(best, ref.pearson(500 * (k + 1)))
+        if best >= 0.95:
+            break
+    tr.close()
+    print(f"bitseq n=8 k=2 pearson {init:.4f} -> {best:.4f} after {500 * (k + 1)} iterations")
+    assert best >= 0.95, (init, best)
