@@ -182,12 +182,14 @@ def test_bitseq_pearson_like_reference_criterion4():
     samples per test string vs the log-reward, evaluated by the reference on the device-trained
     parameters every 500 iterations) must reach 0.95. Reference: 0.9579 after 500 iterations.
     The mode set is the builder's (generate_modes with fold_in(make_key(modes_seed), 0x30DE),
-    train.cpp:417-420); the acceptance test draws its own from make_key(15)."""
+    train.cpp:417-420); the acceptance test draws its own from make_key(15). k = 2 runs on the
+    device's fp64 check path (the bf16 bitseq fast path is specialised to k = 8)."""
     from oracle import oracle as O
     if not O.ref_available("port"):
         pytest.skip("oracle/_ref not built")
     e = abi.env_desc(abi.BITSEQ, bs_n_bits=8, bs_k=2)
     t = abi.train_desc(abi.BITSEQ, batch=16, seed=3, iterations=50000)
+    t.precision = abi.PREC_FP64_CHECK  # the bf16 bitseq fast path is the k = 8 (256-word) one
     tr = engine.Trainer(e, t)
     ref = O.RefLib(e, t)
     ref.set_params(*tr.params())
