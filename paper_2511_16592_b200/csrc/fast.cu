@@ -1524,7 +1524,7 @@ GFNX_DEV double warp_sum_d(double v) {
 
 constexpr int kSubTBMaxT = 128;  // supported() caps max_traj_len at 128 on this path
 
-__global__ void k_fast_loss_warp(LossArgs a) {
+__global__ void __launch_bounds__(256, 4) k_fast_loss_warp(LossArgs a) {
   __shared__ double sub_F[8][kSubTBMaxT + 1], sub_c[8][kSubTBMaxT + 1], sub_S[8][kSubTBMaxT + 1],
       sub_T[8][kSubTBMaxT + 1];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
