@@ -108,13 +108,12 @@ __global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, cons
     z += e[c];
   }
   const float lse = hi + __logf(z), rz = __frcp_rn(z);
-  float la = 0.f, ls = 0.f, fl = 0.f;
-#pragma unroll
-  for (int c = 0; c < NH; ++c) {
-    if (c == act) la = lg[c];
-    if (c == P.stop) ls = lg[c];
-    if (c == A) fl = lg[c];
-  }
+  // the three picked columns straight from the (L1-resident) row: a select over lg[] by a
+  // runtime column compiles to a local-memory array
+  const float* lrow = logits + (size_t)r * NH;
+  float la = (act >= 0 && act < NH) ? lrow[act] : 0.f;
+  float ls = (P.stop >= 0 && P.stop < NH) ? lrow[P.stop] : 0.f;
+  float fl = A < NH ? lrow[A] : 0.f;
   la -= lse;
   ls = P.stop >= 0 ? ls - lse : 0.f;
   fl = flow ? fl : 0.f;
