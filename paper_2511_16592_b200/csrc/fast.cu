@@ -71,12 +71,9 @@ struct FastState {
 // training-forward record of every emitted row from the rollout's raw head outputs:
 // masked log-softmax (tape.cpp:177-213) -> probs[A], log pi(a|s), log pi(stop|s), flow
 template <class Env, int NH>
-__global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, const int16_t* __restrict__ actions,
-                            const int32_t* __restrict__ frow_bt, const int32_t* __restrict__ tilectr,
-                            const float* __restrict__ logits, float* __restrict__ rowbuf, int rs, int flow,
-                            int32_t* err) {
-  const int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r >= *tilectr * kTile) return;
+GFNX_DEV void row_stats_one(const EnvParams& P, const uint32_t* __restrict__ stst, const int16_t* __restrict__ actions,
+                            const int32_t* __restrict__ frow_bt, const float* __restrict__ logits,
+                            float* __restrict__ rowbuf, int rs, int flow, int32_t* err, int r) {
   const int bt = frow_bt[r];
   if (bt < 0) return;
   typename Env::State s;
@@ -130,6 +127,17 @@ __global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, cons
       }
       out[k >> 2] = make_float4(q[0], q[1], q[2], q[3]);
     }
+}
+
+// grid-stride over the used row slots (the slot count is known on the device only)
+template <class Env, int NH>
+__global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, const int16_t* __restrict__ actions,
+                            const int32_t* __restrict__ frow_bt, const int32_t* __restrict__ tilectr,
+                            const float* __restrict__ logits, float* __restrict__ rowbuf, int rs, int flow,
+                            int32_t* err) {
+  const int n = *tilectr * kTile;
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
+    row_stats_one<Env, NH>(P, stst, actions, frow_bt, logits, rowbuf, rs, flow, err, r);
 }
 
 __global__ void k_rollout_reset(int32_t* tilectr, int32_t* counters, int32_t* work) {
@@ -2508,7 +2516,7 @@ struct Kernels {
     } else {
       ProfScope ps(c, "k_row_stats");
       const int nslots = (int)(f.max_tiles * kTile);
-      k_row_stats<Env, NH><<<(nslots + 255) / 256, 256, 0, c.stream>>>(
+      k_row_stats<Env, NH><<<std::min((nslots + 255) / 256, f.num_sms * 8), 256, 0, c.stream>>>(
           c.P, f.stst, c.batch.actions, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
           c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3);
       c.launches++;
