@@ -927,7 +927,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   // thread's half during the hidden MMA, block 1 during the head MMA; h2 blocks 0-1 by the
   // idle half while the row samples, blocks 2-3 during the next step's layer-1 MMA (TA2
   // holds h2 until the next hidden epilogue).
-  auto emit_block = [&](__nv_bfloat16* img, uint32_t ta, int blk, bool valid, int gs) {
+  // ... and the block's two ReLU mask words (units [64 blk, 64 blk + 64)) go out with it
+  auto emit_block = [&](__nv_bfloat16* img, uint32_t* mask, uint32_t ta, int blk, bool valid, int gs) {
     uint32_t r[32];
     tmem_ld32(lane_base + ta + 32 * blk, r);
     tmem_wait_ld();
@@ -936,6 +937,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 + blk * (kTile * 128) +
                      prow * 128;
       st_line_sw128(dst, prow, r);
+      uint32_t lo[16], hi[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        lo[i] = r[i];
+        hi[i] = r[16 + i];
+      }
+      *reinterpret_cast<uint2*>(mask + (size_t)gs * (H / 32) + 2 * blk) = make_uint2(relu_mask16(lo), relu_mask16(hi));
     }
   };
   bool h2_pend = false;  // h2 blocks 2-3 of the previous step's row slot still to emit
@@ -967,7 +975,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       mma_tk<H, 128>(tmem, tmem + TA, w1img, false);
       umma_commit(&mbar);
     }
-    emit_block(a.h2, TA2, 2 + half, h2_pend, h2_gs);  // (warp-collective TMEM load)
+    emit_block(a.h2, a.mask2, TA2, 2 + half, h2_pend, h2_gs);  // (warp-collective TMEM load)
     h2_pend = false;
     mma_join();
     // h1 = ReLU(acc + b1) -> packed into TMEM (the hidden MMA's A operand) + ReLU mask
@@ -1033,7 +1041,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       const int rb = row_b[row];
       row_u[row] = rb >= 0 && rb < a.Bl ? uniform_scalar(fold_in(skeys[row_t[row]], (uint64_t)(a.b0 + rb))) : 0.0;
     }
-    emit_block(a.h1, TA, (c0 >> 6), my_valid, gslot);
+    emit_block(a.h1, a.mask1, TA, (c0 >> 6), my_valid, gslot);
     mma_join();
     mark(2);
     // (3) h2 = ReLU(acc + b2) -> packed into TMEM (own columns: h1 stays for its mask)
@@ -1058,7 +1066,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       mma_tk<NH, H>(tmem + TH, tmem + TA2, whimg, false);
       umma_commit(&mbar);
     }
-    emit_block(a.h1, TA, (c0 >> 6) + 1, my_valid, gslot);
+    emit_block(a.h1, a.mask1, TA, (c0 >> 6) + 1, my_valid, gslot);
     mma_join();
     mark(4);
     float logit[NH];
@@ -1115,65 +1123,21 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       }
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
-    if (half == 1) {  // idle half while the row samples: raw head outputs, h2 row, ReLU masks
+    if (half == 1) {  // idle half while the row samples: raw head outputs, h2 blocks 0-1
       if (my_valid && a.emit_mode != 1) {
         float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
 #pragma unroll
         for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
       }
-      // ReLU mask of h1 (packed in TA) and the full h2 row (packed in TA2): emission + mask
-      uint32_t mw[H / 32];  // fully unrolled loops keep mw in registers
-#pragma unroll
-      for (int q = 0; q < H / 64; ++q) {  // 32 packed columns = 64 units per load
-        uint32_t r[32];
-        tmem_ld32(lane_base + TA + 32 * q, r);
-        tmem_wait_ld();
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          lo[i] = r[i];
-          hi[i] = r[16 + i];
-        }
-        mw[2 * q] = relu_mask16(lo);
-        mw[2 * q + 1] = relu_mask16(hi);
-      }
-      if (my_valid && a.emit_mode != 1) {
-        uint4* dst = reinterpret_cast<uint4*>(a.mask1 + (size_t)gslot * (H / 32));
-#pragma unroll
-        for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
-      }
-      const int prow = gslot & (kTile - 1);
-#pragma unroll
-      for (int q = 0; q < H / 64; ++q) {  // 64-unit block q of h2
-        uint32_t r[32];
-        tmem_ld32(lane_base + TA2 + 32 * q, r);
-        tmem_wait_ld();
-        uint32_t lo[16], hi[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          lo[i] = r[i];
-          hi[i] = r[16 + i];
-        }
-        mw[2 * q] = relu_mask16(lo);
-        mw[2 * q + 1] = relu_mask16(hi);
-        if (q < 2 && my_valid && a.emit_mode != 1) {
-          uint8_t* dst = reinterpret_cast<uint8_t*>(a.h2) + (size_t)(gslot >> 7) * kTile * H * 2 + q * (kTile * 128) +
-                         prow * 128;
-          st_line_sw128(dst, prow, r);
-        }
-      }
-      if (my_valid && a.emit_mode != 1) {
-        uint4* dst = reinterpret_cast<uint4*>(a.mask2 + (size_t)gslot * (H / 32));
-#pragma unroll
-        for (int k = 0; k < H / 128; ++k) dst[k] = make_uint4(mw[4 * k], mw[4 * k + 1], mw[4 * k + 2], mw[4 * k + 3]);
-      }
+      emit_block(a.h2, a.mask2, TA2, 0, my_valid, gslot);  // h2 blocks 0-1 (2-3 follow next step)
+      emit_block(a.h2, a.mask2, TA2, 1, my_valid, gslot);
     }
     h2_pend = my_valid;
     h2_gs = gslot;
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
     mark(5);
   }
-  emit_block(a.h2, TA2, 2 + half, h2_pend, h2_gs);  // the last step's deferred h2 blocks
+  emit_block(a.h2, a.mask2, TA2, 2 + half, h2_pend, h2_gs);  // the last step's deferred h2 blocks
   if (a.phase && tid == 0)
     for (int k = 0; k < 12; ++k) atomicAdd((unsigned long long*)a.phase + (k < 9 ? k : k + 3), (unsigned long long)ph[k]);
   if (bad) atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
