@@ -440,10 +440,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       umma_commit(&mbar);
     }
   };
+  // H = 128: every thread waits on the MMA mbarrier itself (a warp only re-stages the A-tile
+  // rows it emitted, so a warp barrier orders them); the split-K H = 256 variant restages
+  // rows another warp may still be emitting and keeps the CTA barrier
   auto mma_join = [&]() {
-    if (tid == 0) mbar_wait(&mbar, phase);
+    if (SPLIT) {
+      if (tid == 0) mbar_wait(&mbar, phase);
+      __syncthreads();
+    } else {
+      mbar_wait(&mbar, phase);
+      __syncwarp();
+    }
     phase ^= 1;
-    __syncthreads();
     tc_fence_after();
   };
   auto publish = [&]() {  // generic-proxy smem writes -> visible to the tensor core
