@@ -2207,18 +2207,32 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
 }
 
 // fixed-order reduction over CTAs (deterministic)
-__global__ void k_reduce(const float* __restrict__ wpart, int nparts, int64_t n, int64_t stride, float* g) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  // four interleaved partial sums (fixed order: deterministic), combined in a fixed tree
+// block = 32 consecutive parameters x 8 partial groups: warp q sums partial slabs q, q + 8, ...
+// (four loads in flight, coalesced across the 32 parameters), then a fixed-order sum of the
+// 8 group totals (deterministic); the short per-thread chains keep the loads latency-hidden
+constexpr int kRedE = 32, kRedG = 8;
+__global__ void __launch_bounds__(kRedE * kRedG) k_reduce(const float* __restrict__ wpart, int nparts, int64_t n,
+                                                          int64_t stride, float* g) {
+  __shared__ float sg[kRedG][kRedE];
+  const int el = threadIdx.x % kRedE, grp = threadIdx.x / kRedE;
+  const int64_t e = (int64_t)blockIdx.x * kRedE + el;
   float s4[4] = {0.f, 0.f, 0.f, 0.f};
-  int c = 0;
-  for (; c + 4 <= nparts; c += 4) {
+  if (e < n) {
+    int c = grp;
+    for (; c + 3 * kRedG < nparts; c += 4 * kRedG) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) s4[k] += wpart[(size_t)(c + k) * stride + e];
+      for (int k = 0; k < 4; ++k) s4[k] += wpart[(size_t)(c + k * kRedG) * stride + e];
+    }
+    for (; c < nparts; c += kRedG) s4[0] += wpart[(size_t)c * stride + e];
   }
-  for (; c < nparts; ++c) s4[0] += wpart[(size_t)c * stride + e];
-  g[e] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  sg[grp][el] = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+  __syncthreads();
+  if (grp == 0 && e < n) {
+    float t = 0.f;
+#pragma unroll
+    for (int q = 0; q < kRedG; ++q) t += sg[q][el];
+    g[e] = t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -2531,7 +2545,8 @@ struct Kernels {
     const int64_t n = c.L.n_params;
     {
       ProfScope ps(c, "k_reduce");
-      k_reduce<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(f.wpart, grid, n, ta.pstride, c.g32);
+      k_reduce<<<(unsigned)((n + kRedE - 1) / kRedE), kRedE * kRedG, 0, c.stream>>>(f.wpart, grid, n, ta.pstride,
+                                                                                  c.g32);
     }
     c.launches += 5;
     (void)apply;
