@@ -172,6 +172,14 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step)
  * NULL; tv: total variation to R / Z (the `tv_exact` metric), or NULL. bf16 fast path. */
 gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_t n, double* tv);
 
+/* Monte-Carlo terminal log-probability (mc_terminal_logprob, exact.hpp:229-241) of n packed
+ * terminal hypergrid states under the current policy: num_samples backward trajectories each
+ * from the uniform backward policy, drawn as backward_rollout does with key
+ * {keys[2i], keys[2i+1]} (RngKey words, env_core.hpp:314-370), scored by one batched device
+ * policy forward; out[i] = logsumexp_k(log_pf - log_pb) - log(num_samples). bf16 fast path. */
+gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* ctx, const uint32_t* terminals, int64_t n, int32_t num_samples,
+                                     const uint64_t* keys, double* out);
+
 /* Terminal-state FIFO of the `tv_buffer` metric, hypergrid (FifoBuffer, buffer.hpp:13-55,
  * fed by buffer.push_batch(batch.terminal_keys), train.cpp:231). reset: new empty buffer of
  * `capacity` >= 1 (the reference default is 200000); push: appends the resident batch's

@@ -290,6 +290,7 @@ def ref_lib(kind: str = "port"):
                                     C.c_void_p, C.c_void_p]
         L.ref_exact_divergence.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_pearson.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_void_p]
+        L.ref_mc_logprob.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
         L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.ref_load_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         _REF[kind] = L
@@ -368,6 +369,15 @@ class RefLib:
         st = C.c_int64()
         self._check(self.L.ref_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
         return st.value
+
+    def mc_logprob(self, terminal_words, key, num_samples: int = 10):
+        """mc_terminal_logprob (exact.hpp:229-241) of one packed terminal (hypergrid),
+        key = (hi, lo) RngKey words."""
+        w = np.ascontiguousarray(terminal_words, dtype=np.uint32)
+        d = C.c_double()
+        self._check(self.L.ref_mc_logprob(self.h, w.ctypes.data_as(C.c_void_p), num_samples,
+                                          int(key[0]), int(key[1]), C.byref(d)))
+        return d.value
 
     def pearson(self, step: int, mc: int = 10, test_seed: int = 1):
         """The bitseq `pearson` metric of the current policy (train.cpp:440-454)."""

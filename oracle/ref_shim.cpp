@@ -70,6 +70,8 @@ struct SessionBase {
   // terminal log-probabilities (mc_terminal_logprob, exact.hpp:229-241, `mc` backward samples)
   // and the log-rewards over the builder's test set (generate_test_set, train.cpp:431-433)
   virtual double pearson_metric(int64_t, int, uint64_t) { throw config_error("pearson: bitseq only"); }
+  // mc_terminal_logprob (exact.hpp:229-241) of one packed terminal hypergrid state
+  virtual double mc_logprob(const uint32_t*, int, const RngKey&) { throw config_error("mc logprob: hypergrid only"); }
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -176,6 +178,22 @@ struct Session : SessionBase {
       return tv_distance(exact_policy_marginal(env, params, graph, pol), ising_exact_distribution(*params.coupling));
     } else {
       return SessionBase::exact_divergence();
+    }
+  }
+  double mc_logprob(const uint32_t* w, int K, const RngKey& key) override {
+    if constexpr (std::is_same_v<E, HypergridEnv>) {
+      typename E::Instance inst;
+      inst.coords.assign(params.dim, 0);
+      int sum = 0;
+      for (int i = 0; i < params.dim; ++i) {  // packed: byte i = coordinate i
+        inst.coords[i] = static_cast<int>((w[i >> 2] >> (8 * (i & 3))) & 0xffu);
+        sum += inst.coords[i];
+      }
+      inst.is_terminal = true;
+      inst.step_count = sum + 1;
+      return mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, K, key);
+    } else {
+      return SessionBase::mc_logprob(w, K, key);
     }
   }
   double pearson_metric(int64_t step, int mc, uint64_t test_seed) override {
@@ -402,6 +420,16 @@ int ref_load_checkpoint(void* h, const char* path, int64_t* step) {
     rs->s->opt_main() = c.opt_main;
     rs->s->opt_z() = c.opt_z;
     *step = c.step;
+  });
+}
+
+int ref_mc_logprob(void* h, const uint32_t* term, int K, uint64_t key_hi, uint64_t key_lo, double* out) {
+  RefSession* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] {
+    RngKey k;
+    k.hi = key_hi;
+    k.lo = key_lo;
+    *out = rs->s->mc_logprob(term, K, k);
   });
 }
 

@@ -768,6 +768,16 @@ gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* h, double* marginal, int64_t 
   });
 }
 
+gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* h, const uint32_t* terminals, int64_t n, int32_t num_samples,
+                                     const uint64_t* keys, double* out) {
+  return guard(h, [&] {
+    if (h->c.check_mode()) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: bf16 fast path only");
+    if (!terminals || !keys || !out) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: null buffer");
+    fast_mc_terminal_logprob(h->c, terminals, n, num_samples, keys, out);
+    check_device_error(h->c);
+  });
+}
+
 gfnx_status gfnx_buffer_reset(gfnx_ctx* h, int64_t capacity) {
   return guard(h, [&] { hg_buffer_reset(h->c, capacity); });
 }

@@ -70,6 +70,9 @@ void ensure_row0(Ctx& c);              // row0 / row_bt of the resident batch (l
 bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row counts itself
 void fast_hg_marginal(Ctx& c, std::vector<double>* pt);  // exact terminal marginal (hypergrid)
 // tv_buffer metric (hypergrid): terminal-state FIFO + histogram on the device — fast.cu
+// mc_terminal_logprob (exact.hpp:229-241), hypergrid fast path — fast.cu
+void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
+                              double* out);
 void hg_buffer_reset(Ctx& c, int64_t capacity);
 void hg_buffer_push(Ctx& c);
 double hg_buffer_tv(Ctx& c);

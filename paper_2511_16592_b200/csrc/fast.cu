@@ -2680,6 +2680,138 @@ void fast_hg_marginal(Ctx& c, std::vector<double>* pt) {
 }
 
 // ---------------------------------------------------------------------------
+// mc_terminal_logprob (exact.hpp:229-241) on the hypergrid fast path: K backward
+// trajectories per terminal under the uniform backward policy, drawn exactly as
+// backward_rollout does (env_core.hpp:314-370: step key fold_in(key, t), draw
+// categorical(fold_in(step_key, k)) over the legal backward actions, un-stop first), are
+// replayed forward (rollout_from_actions) through ONE batched policy forward on the device
+// (the training-forward kernel on explicit states: log pi(a|s) per transition); then
+// log p(x) ~= logsumexp_k(log_pf_k - log_pb_k) - log K. The walk is integer work on the
+// host; every policy evaluation runs on the GPU.
+void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
+                              double* out) {
+  if (c.env.kind != GFNX_ENV_HYPERGRID || lockstep(c))
+    raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: hypergrid fast path only");
+  if (n < 1 || K < 1) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
+  const int d = c.env.hg_dim, SW = c.P.SW, stop = c.P.stop;
+  std::vector<uint32_t> st;             // forward states (packed), one per transition
+  std::vector<int16_t> act;             // forward action of the transition
+  std::vector<int64_t> traj_end;        // exclusive row end of trajectory (i, k)
+  std::vector<double> log_pb;           // per trajectory: sum of log_pb_uniform
+  traj_end.reserve((size_t)n * K);
+  log_pb.reserve((size_t)n * K);
+  for (int64_t i = 0; i < n; ++i) {
+    uint64_t cw0 = terminals[(size_t)i * SW] | (SW > 1 ? (uint64_t)terminals[(size_t)i * SW + 1] << 32 : 0ull);
+    if (d < 8) cw0 &= (1ull << (8 * d)) - 1ull;
+    const Key key{keys[2 * i], keys[2 * i + 1]};
+    for (int k = 0; k < K; ++k) {
+      uint64_t cw = cw0;
+      bool term = true;
+      std::vector<uint64_t> rs;  // forward states, reversed
+      std::vector<int> ra;       // forward actions, reversed
+      double lpb = 0.0;
+      for (int t = 0;; ++t) {
+        int legal[kMaxHgDim + 1], nl = 0;  // backward_action_mask, hypergrid.cpp:52-61
+        if (term) {
+          legal[nl++] = d;  // un-stop
+        } else {
+          for (int j = 0; j < d; ++j)
+            if ((cw >> (8 * j)) & 0xffu) legal[nl++] = j;
+        }
+        if (nl == 0) break;
+        if (t > c.P.T) raise_error(GFNX_ERR_CONTRACT, "backward_rollout: did not reach the initial state");
+        // categorical over weights 1.0 on the legal actions (rng.cpp:87-100): the first
+        // legal action whose running count exceeds u * count
+        const double u = uniform_scalar(fold_in(fold_in(key, (uint64_t)t), (uint64_t)k)) * (double)nl;
+        int pick = legal[nl - 1];
+        double acc = 0.0;
+        for (int q = 0; q < nl; ++q) {
+          acc += 1.0;
+          if (u < acc) {
+            pick = legal[q];
+            break;
+          }
+        }
+        // log_pb_uniform of the forward transition s -> next: -log(num_parents(next))
+        HypergridEnv::State nx;
+        nx.cw = cw;
+        nx.step = 0;
+        nx.term = term;
+        lpb += -log((double)HypergridEnv::num_parents(c.P, nx));
+        if (pick == d) {  // backward_step_instance, hypergrid.cpp:34-41
+          term = false;
+          ra.push_back(stop);
+        } else {
+          cw -= 1ull << (8 * pick);
+          ra.push_back(pick);
+        }
+        rs.push_back(cw);
+      }
+      for (size_t q = rs.size(); q-- > 0;) {  // forward order
+        st.push_back((uint32_t)rs[q]);
+        if (SW > 1) st.push_back((uint32_t)(rs[q] >> 32));
+        for (int w = 2; w < SW; ++w) st.push_back(0u);
+        act.push_back((int16_t)ra[q]);
+      }
+      traj_end.push_back((int64_t)act.size());
+      log_pb.push_back(lpb);
+    }
+  }
+  const int64_t R = (int64_t)act.size();
+  if (R > (int64_t)1 << 30) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: too many transitions");
+  FastState& f = FS(c);
+  const int64_t tiles = (R + kTile - 1) / kTile, slots = tiles * kTile;
+  std::vector<int32_t> rows(slots, -1);
+  for (int64_t r = 0; r < R; ++r) rows[r] = (int32_t)r;
+  const int32_t ntiles = (int32_t)tiles;
+  const int H = f.H;
+  uint32_t* d_st;
+  int32_t *d_rows, *d_tiles;
+  int16_t* d_act;
+  __nv_bfloat16 *d_h1, *d_h2;
+  uint32_t *d_m1, *d_m2;
+  float* d_rb;
+  cuda_check(cudaMalloc(&d_st, sizeof(uint32_t) * st.size()), "mc");
+  cuda_check(cudaMalloc(&d_rows, sizeof(int32_t) * slots), "mc");
+  cuda_check(cudaMalloc(&d_tiles, sizeof(int32_t)), "mc");
+  cuda_check(cudaMalloc(&d_act, sizeof(int16_t) * R), "mc");
+  cuda_check(cudaMalloc(&d_h1, sizeof(__nv_bfloat16) * slots * H), "mc");
+  cuda_check(cudaMalloc(&d_h2, sizeof(__nv_bfloat16) * slots * H), "mc");
+  cuda_check(cudaMalloc(&d_m1, sizeof(uint32_t) * slots * (H / 32)), "mc");
+  cuda_check(cudaMalloc(&d_m2, sizeof(uint32_t) * slots * (H / 32)), "mc");
+  cuda_check(cudaMalloc(&d_rb, sizeof(float) * slots * f.rs), "mc");
+  cudaMemcpyAsync(d_st, st.data(), sizeof(uint32_t) * st.size(), cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * slots, cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_tiles, &ntiles, sizeof(int32_t), cudaMemcpyHostToDevice, c.stream);
+  cudaMemcpyAsync(d_act, act.data(), sizeof(int16_t) * R, cudaMemcpyHostToDevice, c.stream);
+  with_kernels(c, [&](auto kk) {
+    decltype(kk)::eval_forward(c, d_st, d_rows, d_tiles, d_act, d_h1, d_h2, d_m1, d_m2, d_rb);
+  });
+  std::vector<float> rb((size_t)R * f.rs);
+  cuda_check(cudaMemcpyAsync(rb.data(), d_rb, sizeof(float) * rb.size(), cudaMemcpyDeviceToHost, c.stream), "mc");
+  cuda_check(cudaStreamSynchronize(c.stream), "mc");
+  void* bufs[] = {d_st, d_rows, d_tiles, d_act, d_h1, d_h2, d_m1, d_m2, d_rb};
+  for (void* b : bufs) cudaFree(b);
+  // score_trajectories (objectives.cpp:294-316) + logsumexp (fp64, sample order)
+  int64_t r0 = 0;
+  std::vector<double> terms(K);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int k = 0; k < K; ++k) {
+      const int64_t j = i * K + k, r1 = traj_end[j];
+      double lpf = 0.0;
+      for (int64_t r = r0; r < r1; ++r) lpf += (double)rb[(size_t)r * f.rs + c.P.A];  // log pi(a|s)
+      terms[k] = lpf - log_pb[j];
+      r0 = r1;
+    }
+    double m = terms[0];
+    for (int k = 1; k < K; ++k) m = std::max(m, terms[k]);
+    double se = 0.0;
+    for (int k = 0; k < K; ++k) se += exp(terms[k] - m);
+    out[i] = m + log(se) - log((double)K);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // tv_buffer (metrics.cpp:35-48 over the FifoBuffer of train.cpp:231, hypergrid)
 
 // append terminal states b in [b_lo, Bl) of the resident batch at ring positions

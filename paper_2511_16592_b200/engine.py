@@ -91,6 +91,7 @@ def lib():
         L.gfnx_save_checkpoint.argtypes = [vp, C.c_char_p, C.c_int64]
         L.gfnx_exact_terminal_marginal.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_buffer_reset.argtypes = [vp, C.c_int64]
+        L.gfnx_mc_terminal_logprob.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp]
         L.gfnx_buffer_push.argtypes = [vp]
         L.gfnx_tv_buffer.argtypes = [vp, vp, vp]
         L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
@@ -191,6 +192,15 @@ class Trainer:
         tv = C.c_double()
         self._check(lib().gfnx_exact_terminal_marginal(self.h, _p(m), n_cells, C.byref(tv)))
         return m, tv.value
+
+    def mc_terminal_logprob(self, terminals, keys, num_samples: int = 10):
+        """mc_terminal_logprob (exact.hpp:229-241) of packed terminal states [n, state_words];
+        keys [n, 2] uint64 RngKey words (one backward-rollout key per terminal)."""
+        t = np.ascontiguousarray(terminals, dtype=np.uint32)
+        k = np.ascontiguousarray(keys, dtype=np.uint64)
+        out = np.zeros(len(t))
+        self._check(lib().gfnx_mc_terminal_logprob(self.h, _p(t), len(t), num_samples, _p(k), _p(out)))
+        return out
 
     def buffer_reset(self, capacity: int = 200000):
         """New empty terminal-state FIFO (FifoBuffer, buffer.hpp:13-55) for `tv_buffer`."""
