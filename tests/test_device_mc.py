@@ -35,6 +35,7 @@ def test_mc_logprob_matches_reference():
         dev = tr.mc_terminal_logprob(terms, keys, 10)
         want = np.array([ref.mc_logprob(terms[i], keys[i], 10) for i in range(len(cells))])
         assert np.all(np.isfinite(dev))
+        print(f"stage {stage}: max |device - reference| = {np.max(np.abs(dev - want)):.2e}")
         assert np.max(np.abs(dev - want)) < 5e-2, (stage, dev, want)  # bf16 policy vs fp64
         tr.run(0, 300)  # a trained, non-uniform policy for the second pass
     tr.close()
