@@ -173,7 +173,7 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step)
 gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_t n, double* tv);
 
 /* Monte-Carlo terminal log-probability (mc_terminal_logprob, exact.hpp:229-241) of n packed
- * terminal hypergrid states under the current policy: num_samples backward trajectories each
+ * terminal states (hypergrid, DAG) under the current policy: num_samples backward trajectories each
  * from the uniform backward policy, drawn as backward_rollout does with key
  * {keys[2i], keys[2i+1]} (RngKey words, env_core.hpp:314-370), scored by one batched device
  * policy forward; out[i] = logsumexp_k(log_pf - log_pb) - log(num_samples). bf16 fast path. */

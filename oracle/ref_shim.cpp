@@ -71,7 +71,7 @@ struct SessionBase {
   // and the log-rewards over the builder's test set (generate_test_set, train.cpp:431-433)
   virtual double pearson_metric(int64_t, int, uint64_t) { throw config_error("pearson: bitseq only"); }
   // mc_terminal_logprob (exact.hpp:229-241) of one packed terminal hypergrid state
-  virtual double mc_logprob(const uint32_t*, int, const RngKey&) { throw config_error("mc logprob: hypergrid only"); }
+  virtual double mc_logprob(const uint32_t*, int, const RngKey&) { throw config_error("mc logprob: hypergrid / DAG only"); }
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -191,6 +191,18 @@ struct Session : SessionBase {
       }
       inst.is_terminal = true;
       inst.step_count = sum + 1;
+      return mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, K, key);
+    } else if constexpr (std::is_same_v<E, DagEnv>) {  // packed: row u in half (u & 1) of word u >> 1
+      typename E::Instance inst;
+      const int d = params.d;
+      inst.adj.assign(d, 0u);
+      for (int u = 0; u < d; ++u) {
+        inst.adj[u] = (w[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+        inst.num_edges += __builtin_popcount(inst.adj[u]);
+      }
+      inst.closure_t = closure_from_adjacency(inst.adj);
+      inst.is_terminal = true;
+      inst.step_count = inst.num_edges + 1;
       return mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, K, key);
     } else {
       return SessionBase::mc_logprob(w, K, key);

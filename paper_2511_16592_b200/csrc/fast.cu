@@ -2680,48 +2680,68 @@ void fast_hg_marginal(Ctx& c, std::vector<double>* pt) {
 }
 
 // ---------------------------------------------------------------------------
-// mc_terminal_logprob (exact.hpp:229-241) on the hypergrid fast path: K backward
-// trajectories per terminal under the uniform backward policy, drawn exactly as
-// backward_rollout does (env_core.hpp:314-370: step key fold_in(key, t), draw
-// categorical(fold_in(step_key, k)) over the legal backward actions, un-stop first), are
-// replayed forward (rollout_from_actions) through ONE batched policy forward on the device
-// (the training-forward kernel on explicit states: log pi(a|s) per transition); then
-// log p(x) ~= logsumexp_k(log_pf_k - log_pb_k) - log K. The walk is integer work on the
-// host; every policy evaluation runs on the GPU.
-void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
-                              double* out) {
-  if (c.env.kind != GFNX_ENV_HYPERGRID || lockstep(c))
-    raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: hypergrid fast path only");
-  if (n < 1 || K < 1) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
-  const int d = c.env.hg_dim, SW = c.P.SW, stop = c.P.stop;
-  std::vector<uint32_t> st;             // forward states (packed), one per transition
-  std::vector<int16_t> act;             // forward action of the transition
-  std::vector<int64_t> traj_end;        // exclusive row end of trajectory (i, k)
-  std::vector<double> log_pb;           // per trajectory: sum of log_pb_uniform
-  traj_end.reserve((size_t)n * K);
-  log_pb.reserve((size_t)n * K);
+// backward_action_mask (hypergrid.cpp:52-61, dag.cpp:433-443) as the legal backward actions
+// in index order, and backward_step_instance (hypergrid.cpp:34-41, dag.cpp:407-417); the
+// forward action of a backward action is the same index (un-stop <-> stop) in both envs
+template <class Env>
+int bwd_legal(const EnvParams& P, const typename Env::State& s, int* out) {
+  if (s.term) {
+    out[0] = P.stop;
+    return 1;
+  }
+  int n = 0;
+  if constexpr (std::is_same<Env, HypergridEnv>::value) {
+    for (int j = 0; j < P.hg_dim; ++j)
+      if (s.c(j) > 0) out[n++] = j;
+  } else {
+    for (int a = 0; a < P.stop; ++a) {
+      int u, v;
+      DagEnv::edge(a, P.dag_d, u, v);
+      if ((s.adj.get(u) >> v) & 1) out[n++] = a;
+    }
+  }
+  return n;
+}
+
+template <class Env>
+void bwd_step(const EnvParams& P, typename Env::State& s, int a) {
+  if (a == P.stop) {
+    s.term = false;
+    return;
+  }
+  if constexpr (std::is_same<Env, HypergridEnv>::value) {
+    s.cw -= 1ull << (8 * a);
+  } else {  // remove the edge, rebuild the closure (closure_from_adjacency)
+    int u, v;
+    DagEnv::edge(a, P.dag_d, u, v);
+    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    DagEnv::pack(P, s, w);
+    w[u >> 1] &= ~(1u << (v + 16 * (u & 1)));
+    DagEnv::unpack(P, w, s);
+  }
+}
+
+template <class Env>
+void fast_mc_walks(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
+                   std::vector<uint32_t>& st, std::vector<int16_t>& act, std::vector<int64_t>& traj_end,
+                   std::vector<double>& log_pb) {
+  const int SW = c.P.SW;
+  std::vector<int> legal(std::max(c.P.A, 1) + 1);
   for (int64_t i = 0; i < n; ++i) {
-    uint64_t cw0 = terminals[(size_t)i * SW] | (SW > 1 ? (uint64_t)terminals[(size_t)i * SW + 1] << 32 : 0ull);
-    if (d < 8) cw0 &= (1ull << (8 * d)) - 1ull;
+    typename Env::State s0;
+    Env::unpack(c.P, terminals + (size_t)i * SW, s0);
+    s0.term = true;
     const Key key{keys[2 * i], keys[2 * i + 1]};
     for (int k = 0; k < K; ++k) {
-      uint64_t cw = cw0;
-      bool term = true;
-      std::vector<uint64_t> rs;  // forward states, reversed
+      typename Env::State s = s0;
+      std::vector<uint32_t> rs;  // forward states (packed), reversed
       std::vector<int> ra;       // forward actions, reversed
       double lpb = 0.0;
       for (int t = 0;; ++t) {
-        int legal[kMaxHgDim + 1], nl = 0;  // backward_action_mask, hypergrid.cpp:52-61
-        if (term) {
-          legal[nl++] = d;  // un-stop
-        } else {
-          for (int j = 0; j < d; ++j)
-            if ((cw >> (8 * j)) & 0xffu) legal[nl++] = j;
-        }
+        const int nl = bwd_legal<Env>(c.P, s, legal.data());
         if (nl == 0) break;
         if (t > c.P.T) raise_error(GFNX_ERR_CONTRACT, "backward_rollout: did not reach the initial state");
-        // categorical over weights 1.0 on the legal actions (rng.cpp:87-100): the first
-        // legal action whose running count exceeds u * count
+        // categorical over weights 1.0 on the legal actions (rng.cpp:87-100)
         const double u = uniform_scalar(fold_in(fold_in(key, (uint64_t)t), (uint64_t)k)) * (double)nl;
         int pick = legal[nl - 1];
         double acc = 0.0;
@@ -2732,31 +2752,45 @@ void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int 
             break;
           }
         }
-        // log_pb_uniform of the forward transition s -> next: -log(num_parents(next))
-        HypergridEnv::State nx;
-        nx.cw = cw;
-        nx.step = 0;
-        nx.term = term;
-        lpb += -log((double)HypergridEnv::num_parents(c.P, nx));
-        if (pick == d) {  // backward_step_instance, hypergrid.cpp:34-41
-          term = false;
-          ra.push_back(stop);
-        } else {
-          cw -= 1ull << (8 * pick);
-          ra.push_back(pick);
-        }
-        rs.push_back(cw);
+        // log_pb_uniform of the forward transition s' -> s: -log(num_parents(s))
+        lpb += -log((double)Env::num_parents(c.P, s));
+        bwd_step<Env>(c.P, s, pick);
+        const size_t o = rs.size();
+        rs.resize(o + SW);
+        Env::pack(c.P, s, rs.data() + o);
+        ra.push_back(pick);
       }
-      for (size_t q = rs.size(); q-- > 0;) {  // forward order
-        st.push_back((uint32_t)rs[q]);
-        if (SW > 1) st.push_back((uint32_t)(rs[q] >> 32));
-        for (int w = 2; w < SW; ++w) st.push_back(0u);
+      for (size_t q = ra.size(); q-- > 0;) {  // forward order
+        st.insert(st.end(), rs.begin() + q * SW, rs.begin() + (q + 1) * SW);
         act.push_back((int16_t)ra[q]);
       }
       traj_end.push_back((int64_t)act.size());
       log_pb.push_back(lpb);
     }
   }
+}
+
+// mc_terminal_logprob (exact.hpp:229-241) on the fast path (hypergrid, DAG): K backward
+// trajectories per terminal under the uniform backward policy, drawn exactly as
+// backward_rollout does (env_core.hpp:314-370: step key fold_in(key, t), draw
+// categorical(fold_in(step_key, k)) over the legal backward actions, un-stop first), are
+// replayed forward (rollout_from_actions) through ONE batched policy forward on the device
+// (the training-forward kernel on explicit states: log pi(a|s) per transition); then
+// log p(x) ~= logsumexp_k(log_pf_k - log_pb_k) - log K. The walk is integer work on the
+// host; every policy evaluation runs on the GPU.
+void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
+                              double* out) {
+  if ((c.env.kind != GFNX_ENV_HYPERGRID && c.env.kind != GFNX_ENV_DAG) || lockstep(c))
+    raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: hypergrid / DAG fast path only");
+  if (n < 1 || K < 1) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
+  std::vector<uint32_t> st;             // forward states (packed), one per transition
+  std::vector<int16_t> act;             // forward action of the transition
+  std::vector<int64_t> traj_end;        // exclusive row end of trajectory (i, k)
+  std::vector<double> log_pb;           // per trajectory: sum of log_pb_uniform
+  if (c.env.kind == GFNX_ENV_HYPERGRID)
+    fast_mc_walks<HypergridEnv>(c, terminals, n, K, keys, st, act, traj_end, log_pb);
+  else
+    fast_mc_walks<DagEnv>(c, terminals, n, K, keys, st, act, traj_end, log_pb);
   const int64_t R = (int64_t)act.size();
   if (R > (int64_t)1 << 30) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: too many transitions");
   FastState& f = FS(c);

@@ -57,3 +57,39 @@ def test_mc_estimator_within_three_sigma_of_exact_marginal():
     for j, (c0, c1) in enumerate(cells):
         mean, se = est[j].mean(), est[j].std(ddof=1) / np.sqrt(reps)
         assert abs(mean - marg[c0 + H * c1]) <= 3 * se + 1e-4, (j, mean, se, marg[c0 + H * c1])
+
+
+def test_mc_logprob_dag_matches_reference():
+    """DAG d = 4 (linear-Gaussian score): terminals are random DAGs (edges added in a random
+    topological order), packed as the device packs them (row u in half u & 1 of word u >> 1)."""
+    from oracle import oracle as O
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    d = 4
+    e = abi.env_desc(abi.DAG, dag_d=d, dag_score=abi.LINGAUSS)
+    t = abi.train_desc(abi.DAG, batch=64, seed=5, hidden=(128, 128), objective="mdb")
+    tr = engine.Trainer(e, t)
+    ref = O.RefLib(e, t)
+    rng = np.random.default_rng(3)
+    terms = []
+    for _ in range(12):
+        order = rng.permutation(d)
+        adj = np.zeros(d, dtype=np.uint32)
+        for i in range(d):
+            for j in range(i + 1, d):
+                if rng.random() < 0.5:
+                    adj[order[i]] |= 1 << int(order[j])
+        w = np.zeros(tr.state_words, dtype=np.uint32)
+        for u in range(d):
+            w[u >> 1] |= np.uint32(int(adj[u]) << (16 * (u & 1)))
+        terms.append(w)
+    terms = np.array(terms)
+    keys = rng.integers(0, 2**63, size=(len(terms), 2), dtype=np.uint64)
+    for stage in range(2):
+        ref.set_params(*tr.params())
+        dev = tr.mc_terminal_logprob(terms, keys, 8)
+        want = np.array([ref.mc_logprob(terms[i], keys[i], 8) for i in range(len(terms))])
+        print(f"dag stage {stage}: max |device - reference| = {np.max(np.abs(dev - want)):.2e}")
+        assert np.all(np.isfinite(dev)) and np.max(np.abs(dev - want)) < 5e-2, (stage, dev, want)
+        tr.run(0, 200)
+    tr.close()
