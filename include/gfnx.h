@@ -200,7 +200,8 @@ gfnx_status gfnx_compute_grads(gfnx_ctx* ctx, double* loss);
 gfnx_status gfnx_get_grads(gfnx_ctx* ctx, double* flat, int64_t n, double* d_log_z);
 /* Full iteration `it`: schedules, rollout, train step (train.cpp:224-229). */
 gfnx_status gfnx_iteration(gfnx_ctx* ctx, int64_t it, double* loss);
-/* n iterations it0..it0+n-1 fully on device (CUDA-graph replay); losses[n] may be NULL. */
+/* n iterations it0..it0+n-1 enqueued back to back on the ctx stream with no host
+ * synchronisation in between (stream-ordered launches, no CUDA graph); losses[n] may be NULL. */
 gfnx_status gfnx_run(gfnx_ctx* ctx, int64_t it0, int64_t n, double* losses);
 gfnx_status gfnx_synchronize(gfnx_ctx* ctx);
 
