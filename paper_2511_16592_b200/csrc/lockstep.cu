@@ -1045,6 +1045,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   __shared__ uint64_t mbar, wbar;
   __shared__ uint32_t tbase;
   __shared__ __align__(16) float h1i[kH];
+  __shared__ __align__(16) float bias_s[kMaxNL][kH];  // [0] = h1i's role for l1_mma; [l] = bias of layer l
   __shared__ Key skeys[256];
   __shared__ double row_u[kPersistMaxTiles][kTile];
   __shared__ float xf[kTile][2];
@@ -1063,7 +1064,11 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     mbar_init(&wbar, 1);
     fence_mbar_init();
   }
-  for (int j = tid; j < kH; j += 256) h1i[j] = a.h1init[j];
+  for (int j = tid; j < kH; j += 256) {
+    h1i[j] = a.h1init[j];
+    bias_s[0][j] = a.h1init[j];
+    for (int l = 1; l < a.NL; ++l) bias_s[l][j] = a.bias[l][j];
+  }
   for (int t = tid; t < a.T && t < 256; t += 256) skeys[t] = fold_in(a.key, (uint64_t)t);
   tc_fence_before();
   __syncthreads();
@@ -1251,7 +1256,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         mma_wait();
         if (j == ntile - 1 && tid == 0) load_w(l + 1 < a.NL ? l + 1 : a.NL);  // wbuf free now
         uint32_t mw[4];
-        const float* bl = l == 0 ? h1i : a.bias[l];  // (h1i in shared memory: generic loads)
+        const float* bl = bias_s[l];  // shared memory (a generic pointer into one array: LDS)
 #pragma unroll 1
         for (int q = 0; q < 4; ++q) {
           const int col = c0 + q * 32;
