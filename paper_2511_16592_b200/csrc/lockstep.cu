@@ -1045,7 +1045,8 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   __shared__ uint64_t mbar, wbar;
   __shared__ uint32_t tbase;
   __shared__ __align__(16) float h1i[kH];
-  __shared__ __align__(16) float bias_s[kMaxNL][kH];  // [0] = h1i's role for l1_mma; [l] = bias of layer l
+  __shared__ __align__(16) float bias_s[kMaxNL][kH];
+  __shared__ __align__(16) float bhead_s[kH];  // padded head bias (Ap <= 256)  // [0] = h1i's role for l1_mma; [l] = bias of layer l
   __shared__ Key skeys[256];
   __shared__ double row_u[kPersistMaxTiles][kTile];
   __shared__ float xf[kTile][2];
@@ -1068,6 +1069,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     h1i[j] = a.h1init[j];
     bias_s[0][j] = a.h1init[j];
     for (int l = 1; l < a.NL; ++l) bias_s[l][j] = a.bias[l][j];
+    bhead_s[j] = a.bfp[j];
   }
   for (int t = tid; t < a.T && t < 256; t += 256) skeys[t] = fold_in(a.key, (uint64_t)t);
   tc_fence_before();
@@ -1316,10 +1318,10 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         const uint32_t lm = Lock<E>::legal32c(P, lw, col);
         lmw[q] = lm;
         lcount += __popc(lm);
-        const float4* bb = reinterpret_cast<const float4*>(a.bfp + col);
+        const float4* bb = reinterpret_cast<const float4*>(bhead_s + col);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float4 bq = __ldg(bb + i);
+          const float4 bq = bb[i];
           const float bv[4] = {bq.x, bq.y, bq.z, bq.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
