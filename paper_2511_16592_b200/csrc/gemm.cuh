@@ -78,7 +78,13 @@ struct EpiBase {
   static __device__ void row_done(const Args&, int, int, int, int, float*, Loc&) {}
   template <class Args>
   static __device__ void finish(const Args&, int, int, const float*) {}
+  // per-column bias the epilogue reads (nullptr: none); k_gemm stages it in shared memory
+  template <class Args>
+  static __device__ const float* bias_src(const Args&) { return nullptr; }
+  template <class Args>
+  static __device__ void set_bias(Args&, const float*) {}
 };
+constexpr int kGemmBiasMax = 4096;  // columns of bias staged per CTA (bitseq: 3840)
 
 // column-partial slot of the calling epilogue thread
 GFNX_DEV int epi_quarter() { return ((threadIdx.x >> 5) - 4) & 3; }
@@ -123,9 +129,20 @@ __global__ void __launch_bounds__(kGemmKThreads, 1) k_gemm(GemmGeom g, typename 
   __shared__ uint64_t full[kStages], empty[kStages], tfull[2], tempty[2], bfull;
   __shared__ uint32_t tbase;
   __shared__ float scratch[4 * BN];
+  __shared__ __align__(16) float bias_s[kGemmBiasMax];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const ItemSeq seq = item_seq<kResB>(g.m_tiles * g.n_tiles);
   if (seq.count == 0) return;
+  // the epilogue's bias columns from shared memory (the epilogue's streaming stores would
+  // otherwise keep evicting them from L1)
+  typename Epi::Args el = e;
+  if (const float* bsrc = Epi::bias_src(e)) {
+    const int nb = g.n_tiles * BN;
+    if (nb <= kGemmBiasMax) {
+      for (int i = tid; i < nb; i += blockDim.x) bias_s[i] = bsrc[i];
+      Epi::set_bias(el, bias_s);
+    }
+  }
   if (warp == 0) tmem_alloc<2 * BN>(&tbase);
   if (tid == 32) {
     for (int s = 0; s < kStages; ++s) {
@@ -210,7 +227,7 @@ __global__ void __launch_bounds__(kGemmKThreads, 1) k_gemm(GemmGeom g, typename 
       item_mn<kResB>(g, seq.item(j), m, n);
       const uint32_t buf = j & 1;
       typename Epi::Local loc;
-      Epi::begin(e, m, n, row, part, loc);
+      Epi::begin(el, m, n, row, part, loc);
       mbar_wait(&tfull[buf], (j >> 1) & 1);
       tc_fence_after();
 #pragma unroll 1
@@ -222,13 +239,13 @@ __global__ void __launch_bounds__(kGemmKThreads, 1) k_gemm(GemmGeom g, typename 
         float v[32];
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-        Epi::apply(e, m, n, row, col0, v, scratch, loc);
+        Epi::apply(el, m, n, row, col0, v, scratch, loc);
       }
       tc_fence_before();
-      Epi::row_done(e, m, n, row, part, scratch, loc);
+      Epi::row_done(el, m, n, row, part, scratch, loc);
       gemm_epi_bar();
       if (tid == 128) mbar_arrive_local(&tempty[buf]);
-      Epi::finish(e, m, n, scratch);
+      Epi::finish(el, m, n, scratch);
       gemm_epi_bar();
     }
   }

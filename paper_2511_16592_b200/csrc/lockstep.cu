@@ -231,12 +231,14 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
     uint8_t* mask;
   };
   struct Local {};
+  static __device__ const float* bias_src(const Args& e) { return e.b; }
+  static __device__ void set_bias(Args& e, const float* b) { e.b = b; }
   static __device__ void apply(const Args& e, int m, int, int row, int col0, float (&v)[32], float*, Local&) {
     uint32_t pk[16], mb = 0;
     const float4* bb = reinterpret_cast<const float4*>(e.b + col0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 q = __ldg(bb + i);
+      const float4 q = bb[i];
       pk[2 * i] = pack_bf16x2_relu(v[4 * i] + q.x, v[4 * i + 1] + q.y);
       pk[2 * i + 1] = pack_bf16x2_relu(v[4 * i + 2] + q.z, v[4 * i + 3] + q.w);
     }
@@ -264,6 +266,8 @@ struct LogEpi : EpiBase {
     float mx, s;
     uint32_t lw[Lock<E>::kLW];
   };
+  static __device__ const float* bias_src(const Args& e) { return e.bf; }
+  static __device__ void set_bias(Args& e, const float* b) { e.bf = b; }
   static __device__ void begin(const Args& e, int m, int, int row, int, Local& l) {
     l.mx = -INFINITY;
     l.s = 0.f;
@@ -279,7 +283,7 @@ struct LogEpi : EpiBase {
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 bq = __ldg(bb + i);
+      const float4 bq = bb[i];
       pk[2 * i] = pack_bf16x2(v[4 * i] + bq.x, v[4 * i + 1] + bq.y);
       pk[2 * i + 1] = pack_bf16x2(v[4 * i + 2] + bq.z, v[4 * i + 3] + bq.w);
     }
@@ -590,6 +594,8 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     int act;
     uint32_t lw[Lock<E>::kLW];
   };
+  static __device__ const float* bias_src(const Args& e) { return e.bf; }
+  static __device__ void set_bias(Args& e, const float* b) { e.bf = b; }
   static __device__ void begin(const Args& e, int m, int, int row, int, Local& l) {
     const size_t r = (size_t)m * kTile + row;
     const int t = (int)(r / e.Bl), b = (int)(r % e.Bl);
@@ -614,7 +620,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-      const float4 bq = __ldg(bb + i);
+      const float4 bq = bb[i];
       bias[4 * i] = bq.x;
       bias[4 * i + 1] = bq.y;
       bias[4 * i + 2] = bq.z;
