@@ -116,3 +116,22 @@ def test_oracle_rejects_like_reference(oracle_built):
         O.Oracle(e, abi.train_desc(abi.BITSEQ))
     with pytest.raises(ValueError, match="mdb objective needs the stop action"):
         O.Oracle(abi.env_desc(abi.ISING), abi.train_desc(abi.ISING, objective="mdb"))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built (no /root/reference)")
+def test_reference_mc_logprob_and_pearson_shims(oracle_built):
+    """The shim entry points the GPU tests use as checkers: mc_terminal_logprob of the origin
+    cell has a single backward path (un-stop), so every sample equals log pi(stop | s0); the
+    bitseq pearson metric is a correlation in [-1, 1]."""
+    import numpy as np
+    from paper_2511_16592_b200 import abi
+    e = abi.env_desc(abi.HYPERGRID, hg_dim=2, hg_side=8)
+    t = abi.train_desc(abi.HYPERGRID, batch=16, objective="tb", seed=1)
+    ref = O.RefLib(e, t)
+    lp1 = ref.mc_logprob(np.array([0], np.uint32), (1, 2), 1)
+    lp8 = ref.mc_logprob(np.array([0], np.uint32), (3, 4), 8)
+    assert np.isfinite(lp1) and lp1 < 0.0 and abs(lp1 - lp8) < 1e-12
+    eb = abi.env_desc(abi.BITSEQ, bs_n_bits=8, bs_k=2)
+    tb = abi.train_desc(abi.BITSEQ, batch=16, objective="tb", seed=3)
+    r = O.RefLib(eb, tb).pearson(0)
+    assert -1.0 <= r <= 1.0
