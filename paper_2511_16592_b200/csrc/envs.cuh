@@ -380,7 +380,10 @@ struct DagEnv {
     // row u in 16-bit half (u & 1) of word u >> 1: the words are the halves of adj.lo/hi
     const uint32_t x[4] = {(uint32_t)s.adj.lo, (uint32_t)(s.adj.lo >> 32), (uint32_t)s.adj.hi,
                            (uint32_t)(s.adj.hi >> 32)};
-    for (int i = 0; i < P.SW; ++i) w[i] = i < 4 ? x[i] : 0u;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)  // (constant indices: x stays in registers)
+      if (i < P.SW) w[i] = x[i];
+    for (int i = 4; i < P.SW; ++i) w[i] = 0u;
   }
   // adjacency only; the transpose closure is rebuilt (closure_from_adjacency dag.cpp:331-346)
   __host__ __device__ static void unpack(const EnvParams& P, const uint32_t* w, State& s) {
