@@ -389,7 +389,9 @@ struct DagEnv {
   __host__ __device__ static void unpack(const EnvParams& P, const uint32_t* w, State& s) {
     reset(P, s);
     const int d = P.dag_d;
-    for (int u = 0; u < d; ++u) {
+#pragma unroll
+    for (int u = 0; u < kMaxDagD; ++u) {  // constant word indices: the caller's w stays in registers
+      if (u >= d) break;
       const uint32_t row = (w[u >> 1] >> (16 * (u & 1))) & 0xffffu;
       s.adj.orv(u, row);
 #ifdef __CUDA_ARCH__
