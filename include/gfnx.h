@@ -143,6 +143,18 @@ gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
                         int32_t rank, int32_t world, const void* nccl_id, gfnx_ctx** out);
 void gfnx_destroy(gfnx_ctx* ctx);
 gfnx_status gfnx_nccl_unique_id(void* out128);
+/* In-process communicator: the ranks of one job as threads of ONE process (one ctx per rank,
+ * one thread per ctx; the ranks may share a GPU or sit on peer-accessible GPUs of a node).
+ * The job's all-reduce is then a libgfnx kernel that reads every rank's buffer over peer
+ * memory and sums in rank order (deterministic, identical on every rank) instead of NCCL.
+ * Destroy the member ctxs before the group. Replaces nothing in the reference, which is
+ * single-process and single-threaded; it is the data-parallel plumbing of
+ * SURVEY §8(e) for single-process drivers and for testing world > 1 on one GPU. */
+typedef struct gfnx_group gfnx_group;
+gfnx_status gfnx_group_create(int32_t world, gfnx_group** out);
+gfnx_status gfnx_group_destroy(gfnx_group* group);
+gfnx_status gfnx_create_in_group(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
+                                 int32_t rank, gfnx_group* group, gfnx_ctx** out);
 /* Last error message for ctx (or of the last failed gfnx_create when ctx == NULL). */
 const char* gfnx_last_error(const gfnx_ctx* ctx);
 int32_t gfnx_abi_version(void);
@@ -198,6 +210,11 @@ gfnx_status gfnx_train_step(gfnx_ctx* ctx, double lr, double* loss);
 /* Same as gfnx_train_step without the Adam update (gradients kept for gfnx_get_grads). */
 gfnx_status gfnx_compute_grads(gfnx_ctx* ctx, double* loss);
 gfnx_status gfnx_get_grads(gfnx_ctx* ctx, double* flat, int64_t n, double* d_log_z);
+/* Per-row log pi_F(a_t | s_t) [local_batch * max_len], (b, t) order, 0 past each trajectory's
+ * end, of the policy the last training pass scored the resident batch with — the
+ * `masked_log_softmax` + `take` values of the reference tape (tape.cpp:177-245,
+ * objectives.cpp:67-69), for per-row parity checks. */
+gfnx_status gfnx_export_row_logpf(gfnx_ctx* ctx, double* out, int64_t n);
 /* Full iteration `it`: schedules, rollout, train step (train.cpp:224-229). */
 gfnx_status gfnx_iteration(gfnx_ctx* ctx, int64_t it, double* loss);
 /* n iterations it0..it0+n-1 enqueued back to back on the ctx stream with no host

@@ -1112,7 +1112,12 @@ static int record_from_actions(orc_trainer* tr, const int32_t* actions) {
 
 int32_t orc_replay(orc_trainer* tr, const int32_t* actions) { return record_from_actions(tr, actions); }
 
-int32_t orc_rollout(orc_trainer* tr, int64_t it, double eps) { /* env_core.hpp:232-274 */
+/* forward_rollout (env_core.hpp:232-274). use_policy == 0 is the eps = 1 rollout without
+ * the policy forward: eps_uniform (objectives.cpp:242-264) then gives (1 - 1) * p_i / z +
+ * 1 / legal = 1 / legal exactly for every finite logit row, so the draws do not depend on
+ * the MLP (the reference still evaluates it, only to reject non-finite logits). Used by the
+ * parity tests at the benchmarked batch sizes, where the fp64 MLP per state would dominate. */
+static int32_t rollout_impl(orc_trainer* tr, int64_t it, double eps, int use_policy) {
   if (eps < 0.0 || eps > 1.0) return fail(tr, "exploration eps must lie in [0,1]");
   const int T = tr->T, A = tr->A, nb = tr->nb;
   uint64_t root[2], key[2];
@@ -1135,9 +1140,13 @@ int32_t orc_rollout(orc_trainer* tr, int64_t it, double eps) { /* env_core.hpp:2
     orc_fold_in(key, (uint64_t)t, step_key); /* env_core.hpp:259 */
     for (int b = 0; b < nb; ++b) {
       if (cur[b].is_terminal) continue;
-      env_encode_obs(tr, &cur[b], obs);
       env_action_mask(tr, &cur[b], mask);
-      orc_mlp_forward(tr, obs, 1, logits, NULL); /* row-independent mlp_forward (nn.cpp:60-89) */
+      if (use_policy) {
+        env_encode_obs(tr, &cur[b], obs);
+        orc_mlp_forward(tr, obs, 1, logits, NULL); /* row-independent mlp_forward (nn.cpp:60-89) */
+      } else {
+        for (int i = 0; i < A; ++i) logits[i] = 0.0;
+      }
       for (int i = 0; i < A; ++i)
         if (!isfinite(logits[i])) rc = fail(tr, "forward_rollout: non-finite policy logits");
       if (rc) break;
@@ -1161,6 +1170,9 @@ int32_t orc_rollout(orc_trainer* tr, int64_t it, double eps) { /* env_core.hpp:2
   free(mask);
   return rc;
 }
+
+int32_t orc_rollout(orc_trainer* tr, int64_t it, double eps) { return rollout_impl(tr, it, eps, 1); }
+int32_t orc_rollout_uniform(orc_trainer* tr, int64_t it) { return rollout_impl(tr, it, 1.0, 0); }
 
 void orc_batch(const orc_trainer* tr, orc_batch_view* out) {
   out->nb = tr->nb;
@@ -1189,7 +1201,53 @@ void orc_local_counts(const orc_trainer* tr, int64_t* n_steps, int64_t* n_mdb) {
 /* Loss + analytic gradient (objectives.cpp:42-240 + tape.cpp:321-485)      */
 /* ====================================================================== */
 
-int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
+/* ---- bf16 operand model (TEST INFRASTRUCTURE: the numerics of the device's bf16 fast
+ * path, stated on top of this restatement so device-vs-model differences isolate
+ * implementation error from the bf16 operand rounding the design accepts) ---- */
+static double bf16r(double x) { /* fp32 then round-to-nearest-even to bf16 (cvt.rn.bf16.f32) */
+  float f = (float)x;
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return (double)f;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  u &= 0xffff0000u;
+  memcpy(&f, &u, 4);
+  return (double)f;
+}
+
+/* Trunk of one row under the model flags: weights from Pm; ORC_BFM_ACT rounds every post-ReLU
+ * activation to bf16; ORC_BFM_ISING_L1 forms layer 1 like the persistent Ising rollout
+ * (lockstep.cu k_ls_ising_l1img / k_ls_h1init): the all-unassigned pre-activation
+ * b1 + sum_s bf16(W1[3s+2]) plus, per assigned site, bf16(bf16(W1[3s+u]) - bf16(W1[3s+2])). */
+static void model_trunk_row(const orc_trainer* tr, const double* Pm, int flags, const orc_state* s,
+                            const double* obs, double** acts) {
+  const double* h = obs;
+  for (int l = 0; l < tr->n_trunk; ++l) {
+    const int out = tr->dims[l + 1];
+    if (l == 0 && (flags & ORC_BFM_ISING_L1) && tr->env.kind == GFNX_ENV_ISING) {
+      const double* W1 = tr->params + tr->off_w[0];
+      const double* b1 = tr->params + tr->off_b[0];
+      for (int j = 0; j < out; ++j) {
+        double z = b1[j];
+        for (int site = 0; site < tr->is_D; ++site) z += bf16r(W1[(size_t)(3 * site + 2) * out + j]);
+        for (int site = 0; site < tr->is_D; ++site) {
+          if (s->v[site] == 0) continue;
+          const int u = s->v[site] > 0 ? 1 : 0;
+          z += bf16r(bf16r(W1[(size_t)(3 * site + u) * out + j]) - bf16r(W1[(size_t)(3 * site + 2) * out + j]));
+        }
+        acts[0][j] = z < 0.0 ? 0.0 : z;
+      }
+    } else {
+      dense_row(h, tr->dims[l], Pm + tr->off_w[l], Pm + tr->off_b[l], out, acts[l], 1);
+    }
+    if (flags & ORC_BFM_ACT)
+      for (int j = 0; j < out; ++j) acts[l][j] = bf16r(acts[l][j]);
+    h = acts[l];
+  }
+}
+
+static int32_t compute_grads_impl(orc_trainer* tr, double norm, int flags, double* loss_out,
+                                  double* g, double* dlogz_out, double* row_logpf) {
   if (!tr->has_batch) return fail(tr, "train_step: no batch");
   const int T = tr->T, A = tr->A, nt = tr->n_trunk;
   const int H = tr->dims[nt];
@@ -1215,6 +1273,21 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
   double* glogp = (double*)calloc((size_t)R * A, sizeof(double));
   double* gflow = (double*)calloc((size_t)R, sizeof(double));
   double* acts[10];
+  /* parameters the matmuls read: the fp64 master, or (ORC_BFM_W) its weight matrices rounded
+   * to bf16 like the device's operand images; biases stay unrounded */
+  double* wq = NULL;
+  const double* Pm = tr->params;
+  if (flags & ORC_BFM_W) {
+    wq = (double*)malloc(sizeof(double) * tr->n_params);
+    memcpy(wq, tr->params, sizeof(double) * tr->n_params);
+    for (int l = 0; l < nt; ++l)
+      for (int64_t i = 0; i < (int64_t)tr->dims[l] * tr->dims[l + 1]; ++i)
+        wq[tr->off_w[l] + i] = bf16r(wq[tr->off_w[l] + i]);
+    for (int64_t i = 0; i < (int64_t)H * A; ++i) wq[tr->off_fw + i] = bf16r(wq[tr->off_fw + i]);
+    for (int64_t i = 0; i < (int64_t)H * tr->Ab; ++i) wq[tr->off_bw + i] = bf16r(wq[tr->off_bw + i]);
+    for (int64_t i = 0; i < H; ++i) wq[tr->off_flw + i] = bf16r(wq[tr->off_flw + i]);
+    Pm = wq;
+  }
   /* ---- forward: mlp_forward_tape (nn.cpp:91-126) + masked_log_softmax (tape.cpp:177-213) */
   for (int b = 0; b < tr->nb; ++b)
     for (int t = 0; t < tr->lengths[b]; ++t) {
@@ -1227,12 +1300,13 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
         acts[l] = act + (size_t)r * act_sz + o;
         o += tr->dims[l + 1];
       }
-      trunk_row(tr, obs + (size_t)r * tr->O, acts);
+      model_trunk_row(tr, Pm, flags, s, obs + (size_t)r * tr->O, acts);
       double* x = logp + (size_t)r * A;
-      dense_row(acts[nt - 1], H, tr->params + tr->off_fw, tr->params + tr->off_fb, A, x, 0);
+      dense_row(acts[nt - 1], H, Pm + tr->off_fw, Pm + tr->off_fb, A, x, 0);
+      if (flags & ORC_BFM_LOGIT)
+        for (int c = 0; c < A; ++c) x[c] = bf16r(x[c]);
       if (need_flow)
-        dense_row(acts[nt - 1], H, tr->params + tr->off_flw, tr->params + tr->off_flb, 1,
-                  flow + r, 0);
+        dense_row(acts[nt - 1], H, Pm + tr->off_flw, Pm + tr->off_flb, 1, flow + r, 0);
       const uint8_t* mr = mask + (size_t)r * A;
       double hi = -INFINITY;
       int legal = 0;
@@ -1242,7 +1316,7 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
           if (x[c] > hi) hi = x[c];
         }
       if (!isfinite(hi)) {
-        free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow);
+        free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow); free(wq);
         return fail(tr, "masked_log_softmax: non-finite logits");
       }
       double ssum = 0.0;
@@ -1362,7 +1436,7 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
         const int64_t r = row0[b] + t;
         const int a = tr->fwd_actions[(size_t)b * T + t];
         if (a == stop) {
-          free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow);
+          free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow); free(wq);
           return fail(tr, "stop action before trajectory end");
         }
         double res = logp[(size_t)r * A + a] +
@@ -1378,17 +1452,16 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
     }
   }
   if (!isfinite(loss)) {
-    free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow);
+    free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow); free(wq);
     return fail(tr, "training loss is not finite");
   }
   /* ---- backward through masked log-softmax (tape.cpp:413-434) and the MLP ---- */
-  memset(tr->grads, 0, sizeof(double) * tr->n_params);
+  memset(g, 0, sizeof(double) * tr->n_params);
   int maxw = 0;
   for (int l = 0; l <= nt; ++l) maxw = tr->dims[l] > maxw ? tr->dims[l] : maxw;
   double* gx = (double*)malloc(sizeof(double) * A);
   double* gh = (double*)malloc(sizeof(double) * maxw);
   double* gz = (double*)malloc(sizeof(double) * maxw);
-  double* g = tr->grads;
   for (int64_t r = 0; r < R; ++r) {
     const uint8_t* mr = mask + (size_t)r * A;
     const double* lp = logp + (size_t)r * A;
@@ -1397,6 +1470,11 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
     for (int c = 0; c < A; ++c)
       if (mr[c]) gsum += gr[c];
     for (int c = 0; c < A; ++c) gx[c] = mr[c] ? gr[c] - exp(lp[c]) * gsum : 0.0;
+    double gfl = need_flow ? gflow[r] : 0.0;
+    if (flags & ORC_BFM_GRAD) { /* bf16 dlogits / dflow operand images */
+      for (int c = 0; c < A; ++c) gx[c] = bf16r(gx[c]);
+      gfl = bf16r(gfl);
+    }
     int64_t o = 0;
     for (int l = 0; l < nt; ++l) {
       acts[l] = act + (size_t)r * act_sz + o;
@@ -1410,21 +1488,23 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
     }
     for (int j = 0; j < A; ++j) g[tr->off_fb + j] += gx[j];
     if (need_flow) {
-      for (int p = 0; p < H; ++p) g[tr->off_flw + p] += h[p] * gflow[r];
-      g[tr->off_flb] += gflow[r];
+      for (int p = 0; p < H; ++p) g[tr->off_flw + p] += h[p] * gfl;
+      g[tr->off_flb] += gfl;
     }
     /* dh = flow contribution then fwd contribution (reverse node order) */
     for (int p = 0; p < H; ++p) {
       double v = 0.0;
-      if (need_flow) v += gflow[r] * tr->params[tr->off_flw + p];
+      if (need_flow) v += gfl * Pm[tr->off_flw + p];
       double acc = 0.0;
-      const double* wr = tr->params + tr->off_fw + (size_t)p * A;
+      const double* wr = Pm + tr->off_fw + (size_t)p * A;
       for (int j = 0; j < A; ++j) acc += gx[j] * wr[j];
       gh[p] = v + acc;
     }
     for (int l = nt - 1; l >= 0; --l) {
       const int out = tr->dims[l + 1], in = tr->dims[l];
       for (int j = 0; j < out; ++j) gz[j] = acts[l][j] > 0.0 ? gh[j] : 0.0;
+      if (flags & ORC_BFM_GRAD)
+        for (int j = 0; j < out; ++j) gz[j] = bf16r(gz[j]);
       const double* hin = l > 0 ? acts[l - 1] : obs + (size_t)r * tr->O;
       for (int p = 0; p < in; ++p) {
         const double av = hin[p];
@@ -1433,7 +1513,7 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
       }
       for (int j = 0; j < out; ++j) g[tr->off_b[l] + j] += gz[j];
       if (l > 0) {
-        const double* W = tr->params + tr->off_w[l];
+        const double* W = Pm + tr->off_w[l];
         for (int p = 0; p < in; ++p) {
           double acc = 0.0;
           const double* wr = W + (size_t)p * out;
@@ -1443,10 +1523,62 @@ int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
       }
     }
   }
-  tr->dlogz = obj == GFNX_OBJ_TB ? dlogz : 0.0;
+  if (dlogz_out) *dlogz_out = obj == GFNX_OBJ_TB ? dlogz : 0.0;
+  if (row_logpf) {
+    memset(row_logpf, 0, sizeof(double) * (size_t)tr->nb * T);
+    for (int b = 0; b < tr->nb; ++b)
+      for (int t = 0; t < tr->lengths[b]; ++t)
+        row_logpf[(size_t)b * T + t] =
+            logp[(size_t)(row0[b] + t) * A + tr->fwd_actions[(size_t)b * T + t]];
+  }
   free(gx); free(gh); free(gz);
-  free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow);
+  free(row0); free(obs); free(act); free(logp); free(mask); free(flow); free(glogp); free(gflow); free(wq);
   if (loss_out) *loss_out = loss;
+  return 0;
+}
+
+int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss_out) {
+  return compute_grads_impl(tr, norm, 0, loss_out, tr->grads, &tr->dlogz, NULL);
+}
+
+int32_t orc_model_grads(orc_trainer* tr, double norm, int32_t flags, double* loss, double* grads,
+                        double* dlogz, double* row_logpf) {
+  double* g = (double*)malloc(sizeof(double) * tr->n_params);
+  const int32_t rc = compute_grads_impl(tr, norm, flags, loss, g, dlogz, row_logpf);
+  if (!rc && grads) memcpy(grads, g, sizeof(double) * tr->n_params);
+  free(g);
+  return rc;
+}
+
+/* The action the reference sampler (fp64 policy, eps_uniform + categorical with the
+ * reference key fold_in(fold_in(fold_in(root, 1000 + it), t), b0 + b), env_core.hpp:259-268)
+ * would draw at every real state of the RESIDENT batch (teacher forcing on its states);
+ * -1 past each trajectory's end. The device/oracle action-agreement rate at eps < 1. */
+int32_t orc_teacher_actions(orc_trainer* tr, int64_t it, double eps, int32_t* out) {
+  if (!tr->has_batch) return fail(tr, "teacher_actions: no batch");
+  const int T = tr->T, A = tr->A;
+  uint64_t root[2], key[2], step_key[2], dk[2];
+  orc_make_key(tr->tr.seed, root);
+  orc_fold_in(root, 1000 + (uint64_t)it, key);
+  double* obs = (double*)malloc(sizeof(double) * tr->O);
+  double* logits = (double*)malloc(sizeof(double) * A);
+  double* probs = (double*)malloc(sizeof(double) * A);
+  uint8_t* mask = (uint8_t*)malloc(A);
+  for (size_t i = 0; i < (size_t)tr->nb * T; ++i) out[i] = -1;
+  for (int t = 0; t < T; ++t) {
+    orc_fold_in(key, (uint64_t)t, step_key);
+    for (int b = 0; b < tr->nb; ++b) {
+      if (t >= tr->lengths[b]) continue;
+      const orc_state* s = tr->states + (size_t)b * (T + 1) + t;
+      env_encode_obs(tr, s, obs);
+      env_action_mask(tr, s, mask);
+      orc_mlp_forward(tr, obs, 1, logits, NULL);
+      if (orc_eps_uniform(logits, mask, A, eps, probs) <= 0) continue;
+      orc_fold_in(step_key, (uint64_t)(tr->b0 + b), dk);
+      out[(size_t)b * T + t] = orc_categorical(dk, probs, A);
+    }
+  }
+  free(obs); free(logits); free(probs); free(mask);
   return 0;
 }
 

@@ -59,6 +59,8 @@ void orc_set_adam(orc_trainer* tr, const double* m, const double* v, int64_t t, 
 
 /* forward_rollout + rollout_from_actions (env_core.hpp:166-274) for iteration it */
 int32_t orc_rollout(orc_trainer* tr, int64_t it, double eps);
+/* The eps = 1 rollout without evaluating the policy (the draws are exactly 1/#legal). */
+int32_t orc_rollout_uniform(orc_trainer* tr, int64_t it);
 /* Replace the resident batch by replaying explicit actions [nb * T] (-1 padded). */
 int32_t orc_replay(orc_trainer* tr, const int32_t* actions);
 /* Local normaliser counts: real transitions (DB) and MDB transitions. */
@@ -67,6 +69,19 @@ void orc_local_counts(const orc_trainer* tr, int64_t* n_steps, int64_t* n_mdb);
  * (B for TB/SubTB, n_steps for DB, n_mdb for MDB; <= 0: use local counts). */
 int32_t orc_compute_grads(orc_trainer* tr, double norm, double* loss);
 void orc_get_grads(const orc_trainer* tr, double* flat, double* dlogz);
+/* bf16 operand model of the device fast path (test infrastructure): the same loss/gradient
+ * with the rounding points of the bf16 kernels switched on by `flags`; flags == 0 is
+ * bit-identical to orc_compute_grads. Outputs: loss, grads [n_params], dlogz, and the
+ * per-row log pi_F(a_t | s_t) [nb * T] (0 past each end); any may be NULL. */
+#define ORC_BFM_W 1        /* weight matrices rounded to bf16 (operand images) */
+#define ORC_BFM_ACT 2      /* post-ReLU activations rounded to bf16 (activation images) */
+#define ORC_BFM_GRAD 4     /* dlogits, dflow and masked dz rounded to bf16 (gradient images) */
+#define ORC_BFM_LOGIT 8    /* logits rounded to bf16 (lockstep path's logits image) */
+#define ORC_BFM_ISING_L1 16 /* persistent Ising rollout's layer-1 delta image */
+int32_t orc_model_grads(orc_trainer* tr, double norm, int32_t flags, double* loss, double* grads,
+                        double* dlogz, double* row_logpf);
+/* Actions the fp64 reference sampler draws at every state of the resident batch [nb * T]. */
+int32_t orc_teacher_actions(orc_trainer* tr, int64_t it, double eps, int32_t* out);
 void orc_set_grads(orc_trainer* tr, const double* flat, double dlogz);
 /* Adam on main params (lr) and, for TB, on logZ (adam_z) — train.cpp:184-190 */
 void orc_apply_adam(orc_trainer* tr, double lr);

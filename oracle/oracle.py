@@ -53,6 +53,9 @@ def lib():
                                    C.c_double, C.c_int64]
         L.orc_rollout.argtypes = [C.c_void_p, C.c_int64, C.c_double]
         L.orc_replay.argtypes = [C.c_void_p, C.c_void_p]
+        L.orc_rollout_uniform.argtypes = [C.c_void_p, C.c_int64]
+        L.orc_model_grads.argtypes = [C.c_void_p, C.c_double, C.c_int32] + [C.c_void_p] * 4
+        L.orc_teacher_actions.argtypes = [C.c_void_p, C.c_int64, C.c_double, C.c_void_p]
         L.orc_local_counts.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
         L.orc_compute_grads.argtypes = [C.c_void_p, C.c_double, C.c_void_p]
         L.orc_apply_adam.argtypes = [C.c_void_p, C.c_double]
@@ -100,6 +103,12 @@ def fold_in(key, idx):
 def uniform_scalar(key):
     k = np.array(key, dtype=np.uint64)
     return lib().orc_uniform_scalar(_p(k))
+
+
+# bf16 operand model flags (gfn_oracle.h ORC_BFM_*)
+BFM_W, BFM_ACT, BFM_GRAD, BFM_LOGIT, BFM_ISING_L1 = 1, 2, 4, 8, 16
+BFM_FUSED = BFM_W | BFM_ACT | BFM_GRAD             # hypergrid / DAG fast path
+BFM_LOCKSTEP = BFM_FUSED | BFM_LOGIT                # bitseq, Ising per-step path
 
 
 def make_key(seed):
@@ -155,6 +164,24 @@ class Oracle:
 
     def rollout(self, it, eps):
         self._check(lib().orc_rollout(self.h, it, eps))
+
+    def rollout_uniform(self, it):
+        """eps = 1 rollout without the policy forward (identical draws, see gfn_oracle.c)."""
+        self._check(lib().orc_rollout_uniform(self.h, it))
+
+    def model_grads(self, flags, norm=0.0):
+        """bf16 operand model (BFM_* flags): (loss, grads, dlogz, row log pi_F [nb, T])."""
+        loss, dz = C.c_double(), C.c_double()
+        g = np.zeros(self.n_params)
+        lp = np.zeros((self.nb, self.shape.max_traj_len))
+        self._check(lib().orc_model_grads(self.h, norm, flags, C.byref(loss), _p(g), C.byref(dz), _p(lp)))
+        return loss.value, g, dz.value, lp
+
+    def teacher_actions(self, it, eps):
+        """Actions of the fp64 reference sampler at every state of the resident batch."""
+        out = np.zeros((self.nb, self.shape.max_traj_len), dtype=np.int32)
+        self._check(lib().orc_teacher_actions(self.h, it, eps, _p(out)))
+        return out
 
     def replay(self, actions):
         a = np.ascontiguousarray(actions, dtype=np.int32)

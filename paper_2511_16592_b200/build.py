@@ -19,6 +19,7 @@ UNITS = [
     ("check.cu", ["--fmad=false"]),
     ("fast.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
     ("lockstep.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
+    ("group.cu", []),
 ]
 HOST_UNITS = ["host.cpp"]
 

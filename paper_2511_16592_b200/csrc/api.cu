@@ -236,6 +236,7 @@ namespace {
 template <class F>
 gfnx_status guard(gfnx_ctx* ctx, F&& f) {
   try {
+    if (ctx && ctx->c.stream) cuda_check(cudaSetDevice(ctx->c.device), "cudaSetDevice");  // per calling thread
     f();
     return GFNX_OK;
   } catch (const Failure& e) {
@@ -258,8 +259,13 @@ void check_device_error(Ctx& c) {
   }
 }
 
+// the job's all-reduce (sum, in place, stream-ordered): in-process group or NCCL
 void nccl_sum(Ctx& c, void* buf, size_t n, ncclDataType_t t) {
   if (c.world <= 1) return;
+  if (c.group) {
+    group_allreduce(c, buf, n, t == ncclFloat64 ? kDtypeF64 : t == ncclFloat32 ? kDtypeF32 : kDtypeI32);
+    return;
+  }
   NcclApi& api = nccl_api();
   const ncclResult_t r = api.AllReduce(buf, buf, n, t, ncclSum, (ncclComm_t)c.nccl, c.stream);
   if (r != ncclSuccess) fail(GFNX_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
@@ -357,8 +363,9 @@ gfnx_status gfnx_nccl_unique_id(void* out128) {
   });
 }
 
-gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
-                        int32_t rank, int32_t world, const void* nccl_id, gfnx_ctx** out) {
+namespace {
+gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device, int32_t rank,
+                        int32_t world, const void* nccl_id, Group* group, gfnx_ctx** out) {
   *out = nullptr;
   auto* h = new gfnx_ctx();
   Ctx& c = h->c;
@@ -451,6 +458,8 @@ gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     std::vector<double> sc(8, 0.0);
     sc[0] = train->logz_init;
     cuda_check(cudaMemcpy(c.d_scalars, sc.data(), sizeof(double) * 8, cudaMemcpyHostToDevice), "scalars");
+    cuda_check(cudaMalloc(&c.d_steps, sizeof(int64_t) * 4), "steps");
+    cuda_check(cudaMemset(c.d_steps, 0, sizeof(int64_t) * 4), "steps");
     if (c.check_mode()) {
       cuda_check(cudaMalloc(&c.p64, sizeof(double) * n), "params");
       cuda_check(cudaMalloc(&c.g64, sizeof(double) * (n + 2)), "grads");
@@ -472,7 +481,11 @@ gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
       cuda_check(cudaMemset(c.v32, 0, sizeof(float) * n), "adam");
       fast_init(c);
     }
-    if (world > 1) {
+    if (group) {
+      if (group_world(group) != world) fail(GFNX_ERR_CONFIG, "group world differs from the ctx world");
+      group_join(c, group, rank);
+      c.group = group;
+    } else if (world > 1) {
       NcclApi& api = nccl_api();
       if (!api.ok) fail(GFNX_ERR_NCCL, "libnccl.so.2 not found");
       if (!nccl_id) fail(GFNX_ERR_CONFIG, "world > 1 needs an NCCL unique id");
@@ -492,22 +505,45 @@ gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
   *out = h;
   return GFNX_OK;
 }
+}  // namespace
+
+gfnx_status gfnx_create(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
+                        int32_t rank, int32_t world, const void* nccl_id, gfnx_ctx** out) {
+  return create_impl(env, train, device, rank, world, nccl_id, nullptr, out);
+}
+
+gfnx_status gfnx_group_create(int32_t world, gfnx_group** out) {
+  *out = nullptr;
+  return guard(nullptr, [&] { *out = reinterpret_cast<gfnx_group*>(group_new(world)); });
+}
+
+gfnx_status gfnx_group_destroy(gfnx_group* g) {
+  return guard(nullptr, [&] { group_delete(reinterpret_cast<Group*>(g)); });
+}
+
+gfnx_status gfnx_create_in_group(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device,
+                                 int32_t rank, gfnx_group* group, gfnx_ctx** out) {
+  if (!group) return GFNX_ERR_CONFIG;
+  Group* g = reinterpret_cast<Group*>(group);
+  return create_impl(env, train, device, rank, group_world(g), nullptr, g, out);
+}
 
 void gfnx_destroy(gfnx_ctx* h) {
   if (!h) return;
   Ctx& c = h->c;
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
+  if (c.group) group_leave(c, c.group, c.rank);
   if (c.fast) fast_free(c);
   hg_buffer_free(c);
   if (c.phase) cudaFree(c.phase);
   void* ptrs[] = {c.d_modes, c.d_bs_logr, c.d_is_nbr, c.d_is_J, c.d_dag_cache, c.d_neglog,
-                  c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars,
+                  c.p64, c.g64, c.m64, c.v64, c.p32, c.g32, c.m32, c.v32, c.d_scalars, c.d_steps,
                   c.batch.lengths, c.batch.actions, c.batch.log_rewards, c.batch.delta,
                   c.batch.nparents, c.batch.term_state, c.batch.row0, c.batch.counters,
                   c.batch.row_bt, c.batch.scan_part,
                   c.ck_obs, c.ck_act, c.ck_logp, c.ck_mask, c.ck_flow, c.ck_glogp, c.ck_gflow,
-                  c.ck_gz, c.ck_gx};
+                  c.ck_gz, c.ck_gx, c.ck_lampow, c.ck_gpair};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (auto& e : c.ev)
@@ -573,6 +609,8 @@ gfnx_status gfnx_set_adam_state(gfnx_ctx* h, const double* m, const double* v, i
   return guard(h, [&] {
     Ctx& c = h->c;
     const int64_t n = c.L.n_params;
+    // queued Adam kernels must not overwrite the restored state (the ctx stream is non-blocking)
+    cuda_check(cudaStreamSynchronize(c.stream), "sync");
     if (c.check_mode()) {
       if (m) cuda_check(cudaMemcpy(c.m64, m, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
       if (v) cuda_check(cudaMemcpy(c.v64, v, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
@@ -588,8 +626,8 @@ gfnx_status gfnx_set_adam_state(gfnx_ctx* h, const double* m, const double* v, i
     }
     double zs[2] = {z_m, z_v};
     cuda_check(cudaMemcpy(c.d_scalars + 1, zs, sizeof zs, cudaMemcpyHostToDevice), "adam z");
-    c.adam_t = t;
-    c.z_t = z_t;
+    const int64_t steps[4] = {t, z_t, 0, 0};
+    cuda_check(cudaMemcpy(c.d_steps, steps, sizeof steps, cudaMemcpyHostToDevice), "adam steps");
   });
 }
 
@@ -615,8 +653,10 @@ gfnx_status gfnx_get_adam_state(gfnx_ctx* h, double* m, double* v, int64_t* t, d
     cuda_check(cudaMemcpy(zs, c.d_scalars + 1, sizeof zs, cudaMemcpyDeviceToHost), "adam z");
     if (z_m) *z_m = zs[0];
     if (z_v) *z_v = zs[1];
-    if (t) *t = c.adam_t;
-    if (z_t) *z_t = c.z_t;
+    int64_t steps[4];
+    cuda_check(cudaMemcpy(steps, c.d_steps, sizeof steps, cudaMemcpyDeviceToHost), "adam steps");
+    if (t) *t = steps[0];
+    if (z_t) *z_t = steps[1];
   });
 }
 
@@ -832,6 +872,25 @@ gfnx_status gfnx_get_grads(gfnx_ctx* h, double* flat, int64_t n, double* d_log_z
   });
 }
 
+gfnx_status gfnx_export_row_logpf(gfnx_ctx* h, double* out, int64_t n) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n != (int64_t)c.Bl * c.P.T) fail(GFNX_ERR_CONFIG, "export_row_logpf: size mismatch (local_batch * max_len)");
+    if (!c.has_batch || !c.has_grads) fail(GFNX_ERR_CONTRACT, "export_row_logpf: no training pass on the resident batch");
+    double* d = nullptr;
+    cuda_check(cudaMallocAsync(&d, sizeof(double) * n, c.stream), "row logpf");
+    if (c.check_mode()) {
+      ensure_row0(c);
+      check_row_logpf(c, d);
+    } else {
+      fast_row_logpf(c, d);
+    }
+    cuda_check(cudaMemcpyAsync(out, d, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "row logpf");
+    cuda_check(cudaFreeAsync(d, c.stream), "row logpf");
+    cuda_check(cudaStreamSynchronize(c.stream), "row logpf");
+  });
+}
+
 gfnx_status gfnx_iteration(gfnx_ctx* h, int64_t it, double* loss) {
   return guard(h, [&] {
     Ctx& c = h->c;
@@ -839,6 +898,7 @@ gfnx_status gfnx_iteration(gfnx_ctx* h, int64_t it, double* loss) {
     const double eps = schedule_value(c.train.explore, it); // train.cpp:226
     do_rollout(c, it, eps);
     do_train(c, true, lr, loss);
+    if (!loss) check_device_error(c);  // a failed batch is reported by this call, not a later one
   });
 }
 

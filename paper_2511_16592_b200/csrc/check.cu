@@ -470,28 +470,42 @@ __global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* o
   }
 }
 
-// adam_step (optim.cpp:19-43); bias corrections computed on the host with glibc pow.
+// adam_step (optim.cpp:19-43). Bias corrections 1 - beta^t from the device-owned step
+// counters; a step whose iteration raised the device error word is skipped and not counted
+// (the reference throws before adam_step, train.cpp:174-183).
 __global__ void k_check_adam(double* p, const double* g, double* m, double* v, int64_t n,
-                             double lr, double b1, double b2, double eps, double wd, double bc1,
-                             double bc2, double* scalars, int do_z, double z_lr, double zbc1,
-                             double zbc2) {
+                             double lr, double b1, double b2, double eps, double wd, double* scalars,
+                             int do_z, double z_lr, int64_t* steps, const int32_t* err) {
+  __shared__ int skip;
+  __shared__ double bc[4];
+  if (threadIdx.x == 0) {
+    skip = *err != 0;
+    const double t = (double)(steps[0] + 1), zt = (double)(steps[1] + 1);
+    bc[0] = 1.0 - pow(b1, t);
+    bc[1] = 1.0 - pow(b2, t);
+    bc[2] = 1.0 - pow(b1, zt);
+    bc[3] = 1.0 - pow(b2, zt);
+  }
+  __syncthreads();
+  if (skip) return;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < n) {
     const double gj = g[j];
     m[j] = b1 * m[j] + (1.0 - b1) * gj;
     v[j] = b2 * v[j] + (1.0 - b2) * gj * gj;
-    const double mhat = m[j] / bc1;
-    const double vhat = v[j] / bc2;
+    const double mhat = m[j] / bc[0];
+    const double vhat = v[j] / bc[1];
     p[j] -= lr * (mhat / (sqrt(vhat) + eps) + wd * p[j]);
   }
   if (do_z && j == 0) {  // logZ: separate AdamState, weight decay 0 (train.cpp:125-128,186-190)
     const double gj = scalars[3];
     scalars[1] = b1 * scalars[1] + (1.0 - b1) * gj;
     scalars[2] = b2 * scalars[2] + (1.0 - b2) * gj * gj;
-    const double mhat = scalars[1] / zbc1;
-    const double vhat = scalars[2] / zbc2;
+    const double mhat = scalars[1] / bc[2];
+    const double vhat = scalars[2] / bc[3];
     scalars[0] -= z_lr * (mhat / (sqrt(vhat) + eps) + 0.0 * scalars[0]);
   }
+  adam_commit(steps, do_z);
 }
 
 template <class Env>
@@ -563,20 +577,16 @@ void check_train(Ctx& c, bool /*apply*/, double /*lr*/, double* /*loss*/) {
   }
   cudaMemsetAsync(c.ck_glogp, 0, sizeof(double) * (size_t)R * D.A, c.stream);
   cudaMemsetAsync(c.ck_gflow, 0, sizeof(double) * (size_t)R, c.stream);
-  static thread_local double* lampow = nullptr;  // pow(lambda, k), k = 0..T (glibc pow)
-  static thread_local double* gpair = nullptr;
-  static thread_local int cap_T = 0;
   const int T = c.shape.max_traj_len;
-  if (cap_T < T + 1) {
-    cudaFree(lampow);
-    cudaFree(gpair);
-    cuda_check(cudaMalloc(&lampow, sizeof(double) * (T + 1)), "lampow");
-    cuda_check(cudaMalloc(&gpair, sizeof(double) * ((size_t)(T + 1) * (T + 1) + 3 * (T + 1))), "gpair");
-    cap_T = T + 1;
+  if (!c.ck_lampow) {  // pow(lambda, k), k = 0..T (glibc pow), and the SubTB pair scratch
+    cuda_check(cudaMalloc(&c.ck_lampow, sizeof(double) * (T + 1)), "lampow");
+    cuda_check(cudaMalloc(&c.ck_gpair, sizeof(double) * ((size_t)(T + 1) * (T + 1) + 3 * (T + 1))), "gpair");
+    std::vector<double> lp(T + 1);
+    for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);
+    cuda_check(cudaMemcpy(c.ck_lampow, lp.data(), sizeof(double) * (T + 1), cudaMemcpyHostToDevice), "lampow");
   }
-  std::vector<double> lp(T + 1);
-  for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);
-  cudaMemcpyAsync(lampow, lp.data(), sizeof(double) * (T + 1), cudaMemcpyHostToDevice, c.stream);
+  double* lampow = c.ck_lampow;
+  double* gpair = c.ck_gpair;
   // global normaliser counts live in counters[4..5] (all-reduced by the caller when world > 1)
   k_check_loss<<<1, 1, 0, c.stream>>>(obj, D.A, T, c.B, c.train.terminal_penalty,
                                       c.shape.stop_action, lampow, c.d_neglog, c.batch, c.Bl,
@@ -593,20 +603,27 @@ void check_train(Ctx& c, bool /*apply*/, double /*lr*/, double* /*loss*/) {
 
 void check_adam(Ctx& c, double lr) {
   const gfnx_train_desc& s = c.train;
-  c.adam_t += 1;
-  const double bc1 = 1.0 - pow(s.beta1, (double)c.adam_t);
-  const double bc2 = 1.0 - pow(s.beta2, (double)c.adam_t);
   const int do_z = s.objective == GFNX_OBJ_TB;
-  double zbc1 = 1.0, zbc2 = 1.0;
-  if (do_z) {
-    c.z_t += 1;
-    zbc1 = 1.0 - pow(s.beta1, (double)c.z_t);
-    zbc2 = 1.0 - pow(s.beta2, (double)c.z_t);
-  }
   const int64_t n = c.L.n_params;
   k_check_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(
-      c.p64, c.g64, c.m64, c.v64, n, lr, s.beta1, s.beta2, s.adam_eps, s.weight_decay, bc1, bc2,
-      c.d_scalars, do_z, s.z_lr, zbc1, zbc2);
+      c.p64, c.g64, c.m64, c.v64, n, lr, s.beta1, s.beta2, s.adam_eps, s.weight_decay, c.d_scalars, do_z, s.z_lr,
+      c.d_steps, c.batch.counters + 3);
+  c.launches++;
+}
+
+namespace {
+__global__ void k_check_row_logpf(DeviceBatch batch, const double* __restrict__ logp, int A, int Bl, int T,
+                                  double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Bl * T) return;
+  const int b = i / T, t = i % T;
+  out[i] = t < batch.lengths[b] ? logp[(size_t)(batch.row0[b] + t) * A + batch.actions[i]] : 0.0;
+}
+}  // namespace
+
+void check_row_logpf(Ctx& c, double* out) {
+  const int n = c.Bl * c.P.T;
+  k_check_row_logpf<<<(n + 255) / 256, 256, 0, c.stream>>>(c.batch, c.ck_logp, c.P.A, c.Bl, c.P.T, out);
   c.launches++;
 }
 

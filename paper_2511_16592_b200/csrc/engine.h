@@ -38,6 +38,16 @@ struct DeviceBatch {
 };
 
 struct Ctx;
+struct Group;  // in-process communicator (group.cu)
+
+// element types of the job's all-reduces
+constexpr int kDtypeF32 = 0, kDtypeF64 = 1, kDtypeI32 = 2;
+Group* group_new(int world);
+int group_world(const Group* g);
+void group_delete(Group* g);
+void group_join(Ctx& c, Group* g, int rank);
+void group_leave(Ctx& c, Group* g, int rank);
+void group_allreduce(Ctx& c, void* buf, size_t n, int dtype);
 
 // check-mode (fp64 SIMT, reference operation order) — check.cu
 void check_rollout(Ctx& c, Key key, double eps);
@@ -51,6 +61,8 @@ void fast_rollout(Ctx& c, Key key, double eps);
 void fast_train(Ctx& c, bool apply, double lr, double* loss);  // gradients -> g32, scalars
 void fast_adam(Ctx& c, double lr);
 void fast_sync_weights(Ctx& c);  // fp32 master -> bf16 operand images
+void fast_row_logpf(Ctx& c, double* out);   // per-row log pi_F of the training record [Bl*T] (device)
+void check_row_logpf(Ctx& c, double* out);
 
 // fixed-length (lockstep) fast path for bitseq / Ising — lockstep.cu
 bool ls_supported(const Ctx& c, std::string* why);
@@ -59,6 +71,7 @@ void ls_free(Ctx& c);
 void ls_sync_weights(Ctx& c);
 void ls_rollout(Ctx& c, Key key, double eps);
 void ls_train(Ctx& c);
+void ls_row_logpf(Ctx& c, double* out);
 
 // diagnostics — fast.cu
 void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out);
@@ -87,7 +100,8 @@ struct Ctx {
   int device = 0, rank = 0, world = 1;
   int B = 0, Bl = 0, b0 = 0;  // global batch, local slice [b0, b0+Bl)
   cudaStream_t stream = nullptr;
-  void* nccl = nullptr;  // ncclComm_t
+  void* nccl = nullptr;  // ncclComm_t (one process per GPU)
+  Group* group = nullptr;  // or an in-process group (one thread per rank)
   std::string err;
   int64_t launches = 0;
 
@@ -110,7 +124,7 @@ struct Ctx {
   float* m32 = nullptr;
   float* v32 = nullptr;
   double* d_scalars = nullptr;  // [8]: log_z, z_m, z_v, dlogz, loss, norm, ...
-  int64_t adam_t = 0, z_t = 0;
+  int64_t* d_steps = nullptr;   // [4]: adam_t, z_t, commit ticket (device-owned, see adam_commit)
 
   DeviceBatch batch;
   bool has_batch = false;
@@ -127,6 +141,8 @@ struct Ctx {
   double* ck_gz = nullptr;
   double* ck_gx = nullptr;
   double* ck_pair = nullptr;
+  double* ck_lampow = nullptr;  // [T + 1] pow(lambda, k)
+  double* ck_gpair = nullptr;   // SubTB pair scratch
   int64_t ck_rows_cap = 0;
 
   // optional rollout phase clocks (env GFNX_PHASE_TIMERS=1 at create): [8] int64
@@ -177,6 +193,24 @@ struct ProfScope {
   ProfScope(Ctx& ctx, const char* name);
   ~ProfScope();
 };
+
+#ifdef __CUDACC__
+// Adam step commit: the last block of an Adam kernel to finish advances the device step
+// counters (every block read them at its start, before any block took a ticket).
+__device__ __forceinline__ void adam_commit(int64_t* steps, int do_z) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long k = atomicAdd(reinterpret_cast<unsigned long long*>(steps + 2), 1ull);
+    if (k == gridDim.x - 1) {
+      steps[0] += 1;
+      if (do_z) steps[1] += 1;
+      steps[2] = 0;
+      __threadfence();
+    }
+  }
+}
+#endif
 
 // error reporting from kernel TUs
 void cuda_check(cudaError_t e, const char* what);

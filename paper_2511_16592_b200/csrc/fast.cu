@@ -336,7 +336,6 @@ struct RolloutArgs {
   int rs, flow;
   int32_t *frow_bt, *bt_row, *tilectr;
   float* logits;  // [slot][NH] head outputs (logits, flow at column A), bias included
-  int emit_mode;  // diagnostics (GFNX_EMIT_MODE): 0 full, 1 no row emission, 2 no masks, 3 no images
 };
 
 // H = 256 stages the A operand (h1, then h2) in two 128-column halves through one 32 KB
@@ -623,7 +622,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     // overlapping the MMA. Eight lanes move one row's 128-byte line, so each store
     // instruction writes four whole lines.
     auto emit = [&](__nv_bfloat16* img, int col0) {
-      if (a.emit_mode == 1) return;
       const int j = lane & 7;  // physical 16-byte chunk of the staged row
 #pragma unroll 4
       for (int i = 0; i < 8; ++i) {
@@ -740,7 +738,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
-    if (half == 1 && my_valid && a.emit_mode != 1) {  // raw logits + ReLU masks of the row (idle half)
+    if (half == 1 && my_valid) {  // raw logits + ReLU masks of the row (idle half)
       float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
 #pragma unroll
       for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
@@ -940,7 +938,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     uint32_t r[32];
     tmem_ld32(lane_base + ta + 32 * blk, r);
     tmem_wait_ld();
-    if (valid && a.emit_mode != 1) {
+    if (valid) {
       const int prow = gs & (kTile - 1);
       uint8_t* dst = reinterpret_cast<uint8_t*>(img) + (size_t)(gs >> 7) * kTile * H * 2 + blk * (kTile * 128) +
                      prow * 128;
@@ -1132,7 +1130,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     }
     if (crossed && tid == kThreads - 1) s_next = claim;
     if (half == 1) {  // idle half while the row samples: raw head outputs, h2 blocks 0-1
-      if (my_valid && a.emit_mode != 1) {
+      if (my_valid) {
         float4* lg = reinterpret_cast<float4*>(a.logits + (size_t)gslot * NH);
 #pragma unroll
         for (int k = 0; k < NH / 4; ++k) lg[k] = make_float4(logit[4 * k], logit[4 * k + 1], logit[4 * k + 2], logit[4 * k + 3]);
@@ -2242,10 +2240,16 @@ struct AdamArgs {
   float *p, *m, *v;
   const float* g;
   int64_t n;
-  float lr, b1, b2, eps, wd, bc1, bc2;
+  float lr, b1, b2, eps, wd;
+  double beta1, beta2;      // bias corrections 1 - beta^t in fp64 (std::pow, optim.cpp:27-28)
   double* scalars;
   int do_z;
-  double z_lr, zb1, zb2, zeps, zbc1, zbc2;
+  double z_lr, zeps;
+  // device-owned step counters [adam_t, z_t, ticket]: a step is taken and counted only when
+  // the iteration's error word is clear, so a failed batch never reaches the parameters
+  // (the reference throws before adam_step, train.cpp:174-183)
+  int64_t* steps;
+  const int32_t* err;
   MlpLayout L;
   __nv_bfloat16 *w1, *w2f, *w2d, *whf, *whd;
   int H, O, A, NH;
@@ -2279,6 +2283,19 @@ __device__ __forceinline__ void emit_images(const AdamArgs& a, int64_t j, float 
 }
 
 __global__ void k_fast_adam(AdamArgs a) {
+  __shared__ int skip;
+  __shared__ float bc[2];
+  __shared__ double zbc[2];
+  if (threadIdx.x == 0) {
+    skip = *a.err != 0;
+    const double t = (double)(a.steps[0] + 1), zt = (double)(a.steps[1] + 1);
+    bc[0] = (float)(1.0 - pow(a.beta1, t));
+    bc[1] = (float)(1.0 - pow(a.beta2, t));
+    zbc[0] = 1.0 - pow(a.beta1, zt);
+    zbc[1] = 1.0 - pow(a.beta2, zt);
+  }
+  __syncthreads();
+  if (skip) return;
   const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (j < a.n) {
     const float gj = a.g[j];
@@ -2286,18 +2303,19 @@ __global__ void k_fast_adam(AdamArgs a) {
     const float v = a.b2 * a.v[j] + (1.f - a.b2) * gj * gj;
     a.m[j] = m;
     a.v[j] = v;
-    const float mhat = m / a.bc1, vhat = v / a.bc2;
+    const float mhat = m / bc[0], vhat = v / bc[1];
     const float pj = a.p[j] - a.lr * (mhat / (sqrtf(vhat) + a.eps) + a.wd * a.p[j]);
     a.p[j] = pj;
     emit_images(a, j, pj);
   }
   if (a.do_z && j == 0) {  // logZ keeps fp64 state (train.cpp:186-190)
     const double gj = a.scalars[3];
-    a.scalars[1] = a.zb1 * a.scalars[1] + (1.0 - a.zb1) * gj;
-    a.scalars[2] = a.zb2 * a.scalars[2] + (1.0 - a.zb2) * gj * gj;
-    const double mhat = a.scalars[1] / a.zbc1, vhat = a.scalars[2] / a.zbc2;
+    a.scalars[1] = a.beta1 * a.scalars[1] + (1.0 - a.beta1) * gj;
+    a.scalars[2] = a.beta2 * a.scalars[2] + (1.0 - a.beta2) * gj * gj;
+    const double mhat = a.scalars[1] / zbc[0], vhat = a.scalars[2] / zbc[1];
     a.scalars[0] -= a.z_lr * (mhat / (sqrt(vhat) + a.zeps));
   }
+  adam_commit(a.steps, a.do_z);
 }
 
 __global__ void k_emit_images(AdamArgs a) {
@@ -2370,7 +2388,6 @@ struct Kernels {
     a.bt_row = f.bt_row;
     a.tilectr = f.tilectr;
     a.logits = f.logits;
-    a.emit_mode = getenv("GFNX_EMIT_MODE") ? atoi(getenv("GFNX_EMIT_MODE")) : 0;
     // counters only: the per-step arrays beyond each trajectory's length are never read on
     // the device (gfnx_export_batch pads them from the lengths)
     k_rollout_reset<<<1, 32, 0, c.stream>>>(f.tilectr, c.batch.counters, f.work);
@@ -2387,7 +2404,7 @@ struct Kernels {
       const int tsb = rollout_ts_smem_bytes<H, NH>();
       cudaFuncAttributes ft{};
       cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH, NH>);
-      if (tsb + (int)ft.sharedSizeBytes <= optin && !getenv("GFNX_ROLLOUT_SS")) {
+      if (tsb + (int)ft.sharedSizeBytes <= optin) {
         if (c.P.A <= 8) {
           set_smem_once(k_fast_rollout_ts<Env, H, NH, 8>, tsb);
           k_fast_rollout_ts<Env, H, NH, 8><<<grid, kThreads, tsb, c.stream>>>(a);
@@ -2585,7 +2602,28 @@ void with_kernels(Ctx& c, F&& fn) {
 
 bool lockstep(const Ctx& c) { return c.env.kind == GFNX_ENV_BITSEQ || c.env.kind == GFNX_ENV_ISING; }
 
+// per-row log pi_F(a_t | s_t) of the training record, (b, t) order (0 past each end)
+__global__ void k_fast_row_logpf(const int32_t* __restrict__ lengths, const int32_t* __restrict__ bt_row,
+                                 const float* __restrict__ rowbuf, int rs, int A, int Bl, int T, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Bl * T) return;
+  const int b = i / T, t = i % T;
+  out[i] = t < lengths[b] ? (double)rowbuf[(size_t)bt_row[i] * rs + A] : 0.0;
+}
+
 }  // namespace
+
+void fast_row_logpf(Ctx& c, double* out) {
+  if (lockstep(c)) {
+    ls_row_logpf(c, out);
+    return;
+  }
+  FastState& f = FS(c);
+  const int n = c.Bl * c.P.T;
+  k_fast_row_logpf<<<(n + 255) / 256, 256, 0, c.stream>>>(c.batch.lengths, f.bt_row, f.rowbuf, f.rs, c.P.A, c.Bl,
+                                                          c.P.T, out);
+  c.launches++;
+}
 
 bool fast_rollout_counts(const Ctx& c) { return !lockstep(c); }
 
@@ -3079,7 +3117,6 @@ void fast_train(Ctx& c, bool apply, double lr, double* /*loss*/) {
 void fast_adam(Ctx& c, double lr) {
   const int64_t n = c.L.n_params;
   const gfnx_train_desc& s = c.train;
-  c.adam_t += 1;
   const bool bitseq = lockstep(c);
   AdamArgs a{};
   if (!bitseq) {
@@ -3096,20 +3133,15 @@ void fast_adam(Ctx& c, double lr) {
   a.lr = (float)lr;
   a.b1 = (float)s.beta1;
   a.b2 = (float)s.beta2;
+  a.beta1 = s.beta1;
+  a.beta2 = s.beta2;
   a.eps = (float)s.adam_eps;
   a.wd = (float)s.weight_decay;
-  a.bc1 = (float)(1.0 - pow(s.beta1, (double)c.adam_t));
-  a.bc2 = (float)(1.0 - pow(s.beta2, (double)c.adam_t));
   a.do_z = s.objective == GFNX_OBJ_TB;
-  if (a.do_z) {
-    c.z_t += 1;
-    a.z_lr = s.z_lr;
-    a.zb1 = s.beta1;
-    a.zb2 = s.beta2;
-    a.zeps = s.adam_eps;
-    a.zbc1 = 1.0 - pow(s.beta1, (double)c.z_t);
-    a.zbc2 = 1.0 - pow(s.beta2, (double)c.z_t);
-  }
+  a.z_lr = s.z_lr;
+  a.zeps = s.adam_eps;
+  a.steps = c.d_steps;
+  a.err = c.batch.counters + 3;
   {
     ProfScope ps(c, "k_fast_adam");
     k_fast_adam<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(a);

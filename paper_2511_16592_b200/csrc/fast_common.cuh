@@ -1,6 +1,9 @@
 // fast_common.cuh — tensor-core / bulk-copy helpers shared by the fast-path TUs.
 #pragma once
 
+#include <mutex>
+#include <tuple>
+
 #include <vector>
 
 #include "engine.h"
@@ -129,11 +132,16 @@ GFNX_DEV void mma_k_sw128_none(uint32_t d_tmem, const void* a_img, const void* b
 
 template <class K>
 void set_smem_once(K kernel, int smem) {
-  static std::vector<std::pair<const void*, int>> done;  // (kernel, bytes) already applied
+  // (kernel, device, bytes) already applied; ctxs may run on several host threads / GPUs
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
   for (auto& d : done)
-    if (d.first == (const void*)kernel && d.second >= smem) return;
+    if (std::get<0>(d) == (const void*)kernel && std::get<1>(d) == dev && std::get<2>(d) >= smem) return;
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  done.emplace_back((const void*)kernel, smem);
+  done.emplace_back((const void*)kernel, dev, smem);
 }
 
 

@@ -1507,8 +1507,7 @@ void rollout_impl(Ctx& c, Key key, double eps) {
   // the whole rollout in one persistent kernel when the head fits one MMA and every CTA
   // holds at most two trajectory tiles (GFNX_LS_STEPWISE=1 forces the per-step kernels)
   const int grid = std::min(f.num_sms, f.tilesB);
-  if (f.NT == 1 && Bl % kTile == 0 && f.tilesB <= kPersistMaxTiles * grid && T <= 256 &&
-      !getenv("GFNX_LS_STEPWISE")) {
+  if (f.NT == 1 && Bl % kTile == 0 && f.tilesB <= kPersistMaxTiles * grid && T <= 256) {
     PersistArgs pa{};
     pa.P = c.P;
     pa.key = key;
@@ -1527,7 +1526,7 @@ void rollout_impl(Ctx& c, Key key, double eps) {
       pa.bias[l] = c.p32 + c.L.off_b[l];
     }
     pa.wimg[f.NL] = (const uint8_t*)f.wff;
-    if (std::is_same<E, IsingEnv>::value && 2 * c.P.is_D <= kH && !getenv("GFNX_LS_L1_GATHER")) {
+    if (std::is_same<E, IsingEnv>::value && 2 * c.P.is_D <= kH) {
       if (!f.l1img) cuda_check(cudaMalloc(&f.l1img, kH * kH * 2), "ising l1 image");
       k_ls_ising_l1img<<<kH * kH / 256, 256, 0, c.stream>>>(f.w1, c.P.is_D, f.l1img);
       c.launches++;
@@ -1796,6 +1795,22 @@ void ls_free(Ctx& c) {
 void ls_sync_weights(Ctx& c) {
   EmitArgs a = emit_args(c);
   k_ls_emit<<<(unsigned)((a.n + 255) / 256), 256, 0, c.stream>>>(a);
+  c.launches++;
+}
+
+namespace {
+// rows are step-major (r = t * Bl + b); rowbuf[2 r] = log pi(a | s)
+__global__ void k_ls_row_logpf(const float* __restrict__ rowbuf, int Bl, int T, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Bl * T) return;
+  const int b = i / T, t = i % T;
+  out[i] = (double)rowbuf[2 * ((size_t)t * Bl + b)];
+}
+}  // namespace
+
+void ls_row_logpf(Ctx& c, double* out) {
+  const int n = c.Bl * LS(c).T;
+  k_ls_row_logpf<<<(n + 255) / 256, 256, 0, c.stream>>>(LS(c).rowbuf, c.Bl, LS(c).T, out);
   c.launches++;
 }
 

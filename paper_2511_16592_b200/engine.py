@@ -16,8 +16,7 @@ import numpy as np
 from . import abi
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# GFNX_LIB: an alternative build of the same library (A/B timing of kernel variants)
-LIB_PATH = os.environ.get("GFNX_LIB") or os.path.join(HERE, "libgfnx.so")
+LIB_PATH = os.path.join(HERE, "libgfnx.so")
 _LIB = None
 
 
@@ -55,6 +54,9 @@ def lib():
         L.gfnx_create.argtypes = [P(abi.EnvDesc), P(abi.TrainDesc), C.c_int32, C.c_int32,
                                   C.c_int32, vp, P(vp)]
         L.gfnx_destroy.argtypes = [vp]
+        L.gfnx_group_create.argtypes = [C.c_int32, P(vp)]
+        L.gfnx_group_destroy.argtypes = [vp]
+        L.gfnx_create_in_group.argtypes = [P(abi.EnvDesc), P(abi.TrainDesc), C.c_int32, C.c_int32, vp, P(vp)]
         L.gfnx_nccl_unique_id.argtypes = [vp]
         L.gfnx_env_shape_of.argtypes = [P(abi.EnvDesc), P(abi.EnvShape)]
         L.gfnx_default_env_desc.argtypes = [C.c_int32, P(abi.EnvDesc)]
@@ -68,6 +70,7 @@ def lib():
         L.gfnx_train_step.argtypes = [vp, C.c_double, vp]
         L.gfnx_compute_grads.argtypes = [vp, vp]
         L.gfnx_get_grads.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_export_row_logpf.argtypes = [vp, vp, C.c_int64]
         L.gfnx_iteration.argtypes = [vp, C.c_int64, vp]
         L.gfnx_run.argtypes = [vp, C.c_int64, C.c_int64, vp]
         L.gfnx_synchronize.argtypes = [vp]
@@ -123,16 +126,35 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
+class Group:
+    """In-process communicator (gfnx_group): `world` ranks driven by the threads of this
+    process; their all-reduce is libgfnx's peer-memory sum kernel instead of NCCL."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        _raise(lib().gfnx_group_create(world, C.byref(h)))
+        self.h, self.world = h, world
+
+    def close(self):
+        if getattr(self, "h", None):
+            _raise(lib().gfnx_group_destroy(self.h))
+            self.h = None
+
+
 class Trainer:
     """One rank's device engine (one gfnx_ctx)."""
 
     def __init__(self, env: abi.EnvDesc, train: abi.TrainDesc, device: int = 0, rank: int = 0,
-                 world: int = 1, nccl_id: bytes | None = None):
+                 world: int = 1, nccl_id: bytes | None = None, group: Group | None = None):
         self.env, self.train = env, train
         h = C.c_void_p()
-        idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
-        _raise(lib().gfnx_create(C.byref(env), C.byref(train), device, rank, world, idbuf,
-                                 C.byref(h)))
+        if group is not None:
+            _raise(lib().gfnx_create_in_group(C.byref(env), C.byref(train), device, rank, group.h,
+                                              C.byref(h)))
+        else:
+            idbuf = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+            _raise(lib().gfnx_create(C.byref(env), C.byref(train), device, rank, world, idbuf,
+                                     C.byref(h)))
         self.h = h
         n = C.c_int64()
         lib().gfnx_num_params(h, C.byref(n))
@@ -236,6 +258,12 @@ class Trainer:
         self._check(lib().gfnx_get_grads(self.h, _p(g), self.n_params, C.byref(dz)))
         return g, dz.value
 
+    def row_logpf(self):
+        """Per-row log pi_F(a_t | s_t) [local_batch, T] of the last training pass."""
+        out = np.zeros((self.local_batch, self.T))
+        self._check(lib().gfnx_export_row_logpf(self.h, _p(out), out.size))
+        return out
+
     def iteration(self, it: int, read_loss: bool = True):
         loss = C.c_double()
         self._check(lib().gfnx_iteration(self.h, it, C.byref(loss) if read_loss else None))
@@ -292,8 +320,9 @@ class Trainer:
         self._check(lib().gfnx_event_elapsed(self.h, a, b, C.byref(ms)))
         return ms.value
 
-    def profile(self, enable: bool):
-        self._check(lib().gfnx_profile(self.h, 1 if enable else 0))
+    def profile(self, mode: int):
+        """Per-kernel CUDA-event brackets: 0 off, 1 every kernel, 2 the rollout kernel only."""
+        self._check(lib().gfnx_profile(self.h, int(mode)))
 
     def profile_read(self):
         names = C.create_string_buffer(4096)
