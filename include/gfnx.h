@@ -215,6 +215,9 @@ gfnx_status gfnx_get_grads(gfnx_ctx* ctx, double* flat, int64_t n, double* d_log
  * `masked_log_softmax` + `take` values of the reference tape (tape.cpp:177-245,
  * objectives.cpp:67-69), for per-row parity checks. */
 gfnx_status gfnx_export_row_logpf(gfnx_ctx* ctx, double* out, int64_t n);
+/* Diagnostics (read-only): copy an internal device buffer of the lockstep fast path by name
+ * ("h<l>", "dz<l>", "mask<l>", "dlog", "rowbuf", "coef"); out == NULL returns the size. */
+gfnx_status gfnx_debug_buffer(gfnx_ctx* ctx, const char* name, void* out, int64_t cap, int64_t* bytes);
 /* Full iteration `it`: schedules, rollout, train step (train.cpp:224-229). */
 gfnx_status gfnx_iteration(gfnx_ctx* ctx, int64_t it, double* loss);
 /* n iterations it0..it0+n-1 enqueued back to back on the ctx stream with no host

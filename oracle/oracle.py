@@ -111,6 +111,25 @@ BFM_FUSED = BFM_W | BFM_ACT | BFM_GRAD             # hypergrid / DAG fast path
 BFM_LOCKSTEP = BFM_FUSED | BFM_LOGIT                # bitseq, Ising per-step path
 
 
+def param_tensors(oracle) -> list:
+    """(name, begin, end) of every tensor of the flat parameter vector in MlpParams::tensors()
+    order (nn.cpp:8-19): trunk W1, b1, ..., fwd head, bwd head, flow head."""
+    sh, t = oracle.shape, oracle.train
+    dims = [sh.obs_dim] + [t.hidden[i] for i in range(t.num_hidden)]
+    sizes = []
+    for i in range(t.num_hidden):
+        sizes += [(f"W{i + 1}", dims[i] * dims[i + 1]), (f"b{i + 1}", dims[i + 1])]
+    H = dims[-1]
+    for nm, k in (("fwd", sh.num_actions), ("bwd", sh.num_backward_actions), ("flow", 1)):
+        sizes += [(f"W{nm}", H * k), (f"b{nm}", k)]
+    out, off = [], 0
+    for nm, k in sizes:
+        out.append((nm, off, off + k))
+        off += k
+    assert off == oracle.n_params
+    return out
+
+
 def make_key(seed):
     return (0x9E3779B97F4A7C15, seed)
 

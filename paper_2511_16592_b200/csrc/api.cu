@@ -891,6 +891,22 @@ gfnx_status gfnx_export_row_logpf(gfnx_ctx* h, double* out, int64_t n) {
   });
 }
 
+gfnx_status gfnx_debug_buffer(gfnx_ctx* h, const char* name, void* out, int64_t cap, int64_t* bytes) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const void* p = nullptr;
+    size_t n = 0;
+    const bool lock = !c.check_mode() && (c.env.kind == GFNX_ENV_BITSEQ || c.env.kind == GFNX_ENV_ISING);
+    if (!lock || !ls_debug_buffer(c, name, &p, &n)) fail(GFNX_ERR_CONFIG, std::string("debug_buffer: unknown buffer ") + name);
+    if (bytes) *bytes = (int64_t)n;
+    if (out) {
+      if (cap < (int64_t)n) fail(GFNX_ERR_CONFIG, "debug_buffer: buffer too small");
+      cuda_check(cudaStreamSynchronize(c.stream), "sync");
+      cuda_check(cudaMemcpy(out, p, n, cudaMemcpyDeviceToHost), "debug_buffer");
+    }
+  });
+}
+
 gfnx_status gfnx_iteration(gfnx_ctx* h, int64_t it, double* loss) {
   return guard(h, [&] {
     Ctx& c = h->c;

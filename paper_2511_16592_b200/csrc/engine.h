@@ -72,6 +72,7 @@ void ls_sync_weights(Ctx& c);
 void ls_rollout(Ctx& c, Key key, double eps);
 void ls_train(Ctx& c);
 void ls_row_logpf(Ctx& c, double* out);
+bool ls_debug_buffer(Ctx& c, const std::string& name, const void** ptr, size_t* bytes);
 
 // diagnostics — fast.cu
 void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out);

@@ -30,6 +30,7 @@
 //                 MN-major tcgen05 over 64-row stages, warp-specialised
 //   k_ls_colsum, k_ls_reduce   fixed-order reductions into the flat gradient; then Adam.
 #include <math.h>
+#include <string.h>
 
 #include <type_traits>
 #include <vector>
@@ -1790,6 +1791,20 @@ void ls_free(Ctx& c) {
     if (p) cudaFree(p);
   delete f;
   c.fast = nullptr;
+}
+
+bool ls_debug_buffer(Ctx& c, const std::string& name, const void** ptr, size_t* bytes) {
+  LsState& f = LS(c);
+  const size_t img = (size_t)f.tilesR * kTile * kH * 2;
+  auto layer = [&](const char* pre) { return name.size() == strlen(pre) + 1 && name.compare(0, strlen(pre), pre) == 0 ? name.back() - '0' : -1; };
+  int l;
+  if ((l = layer("h")) >= 0 && l < f.NL) { *ptr = f.h[l]; *bytes = img; return true; }
+  if ((l = layer("dz")) >= 0 && l < f.NL) { *ptr = f.dz[l]; *bytes = img; return true; }
+  if ((l = layer("mask")) >= 0 && l < f.NL) { *ptr = f.mask[l]; *bytes = (size_t)f.R * (kH / 8); return true; }
+  if (name == "dlog") { *ptr = f.dlog; *bytes = (size_t)f.tilesR * f.KBA * (kTile * 128); return true; }
+  if (name == "rowbuf") { *ptr = f.rowbuf; *bytes = sizeof(float) * 2 * (size_t)f.R; return true; }
+  if (name == "coef") { *ptr = f.coef; *bytes = sizeof(float) * (size_t)f.R; return true; }
+  return false;
 }
 
 void ls_sync_weights(Ctx& c) {

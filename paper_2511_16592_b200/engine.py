@@ -71,6 +71,7 @@ def lib():
         L.gfnx_compute_grads.argtypes = [vp, vp]
         L.gfnx_get_grads.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_export_row_logpf.argtypes = [vp, vp, C.c_int64]
+        L.gfnx_debug_buffer.argtypes = [vp, C.c_char_p, vp, C.c_int64, P(C.c_int64)]
         L.gfnx_iteration.argtypes = [vp, C.c_int64, vp]
         L.gfnx_run.argtypes = [vp, C.c_int64, C.c_int64, vp]
         L.gfnx_synchronize.argtypes = [vp]
@@ -262,6 +263,14 @@ class Trainer:
         """Per-row log pi_F(a_t | s_t) [local_batch, T] of the last training pass."""
         out = np.zeros((self.local_batch, self.T))
         self._check(lib().gfnx_export_row_logpf(self.h, _p(out), out.size))
+        return out
+
+    def debug_buffer(self, name: str) -> np.ndarray:
+        """Raw bytes of an internal device buffer (diagnostics; see gfnx_debug_buffer)."""
+        n = C.c_int64()
+        self._check(lib().gfnx_debug_buffer(self.h, name.encode(), None, 0, C.byref(n)))
+        out = np.zeros(n.value, dtype=np.uint8)
+        self._check(lib().gfnx_debug_buffer(self.h, name.encode(), _p(out), n.value, C.byref(n)))
         return out
 
     def iteration(self, it: int, read_loss: bool = True):

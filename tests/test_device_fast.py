@@ -3,10 +3,9 @@
 * eps = 1 makes every legal action exactly 1/#legal in the reference sampler, so the
   fast rollout must reproduce the oracle's trajectories BIT-EXACTLY regardless of the
   bf16 policy (actions, lengths, terminal states, log-rewards, log P_B, MDB deltas).
-* For eps < 1 the device batch is replayed through the oracle (rollout_from_actions
-  semantics) and the loss / gradients of the SAME batch are compared at bf16 tolerance:
-  loss rtol 2e-2, gradient relative L2 error < 5e-2 and cosine > 0.998.
-* A full iteration (Adam) moves the parameters like the oracle's step (same tolerance).
+* Loss / gradient / per-row log pi parity on the same batch, with the stated tolerances, is in
+  tests/test_device_parity.py (bf16 operand model and fp64, benchmark batch sizes).
+* A full iteration (Adam) moves the parameters like the oracle's step.
 """
 import numpy as np
 import pytest
@@ -51,36 +50,6 @@ def _grad_close(gd, go):
     err = np.linalg.norm(gd - go) / max(np.linalg.norm(go), 1e-30)
     cos = float(gd @ go / max(np.linalg.norm(gd) * np.linalg.norm(go), 1e-30))
     return err, cos
-
-
-@pytest.mark.parametrize("name,kw", CASES)
-def test_fast_loss_and_grads_match_oracle_on_same_batch(name, kw):
-    e, t = _pair(name, **kw)
-    d = engine.Trainer(e, t)
-    o = O.Oracle(e, t)
-    p, z = o.params()
-    d.set_params(p, z)
-    for it in range(2):
-        eps = o.schedule("explore", it)
-        d.forward_rollout(it, eps)
-        bd = d.batch()
-        o.replay(bd["fwd_actions"])
-        _same_batch(bd, o.batch())
-        ld = d.compute_grads()
-        lo = o.compute_grads()
-        assert abs(ld - lo) <= 2e-2 * abs(lo) + 1e-6, (ld, lo)
-        gd, dzd = d.grads()
-        go, dzo = o.grads()
-        err, cos = _grad_close(gd, go)
-        assert err < 5e-2 and cos > 0.998, (err, cos)
-        if t.objective == abi.TB:
-            assert abs(dzd - dzo) <= 2e-2 * abs(dzo) + 1e-6
-        # one Adam step on both sides from identical state
-        lr = o.schedule("lr", it)
-        o.apply_adam(lr)
-        d.set_params(*o.params())
-        d.set_adam_state(*o.adam())
-    d.close()
 
 
 @pytest.mark.parametrize("name,kw", CASES)
@@ -168,7 +137,6 @@ def _ising(side, batch):
 
 
 LOCKSTEP_EPS1 = [("bitseq", lambda: _bitseq(120, 128)), ("ising", lambda: _ising(10, 128))]
-LOCKSTEP_GRAD = [("bitseq", lambda: _bitseq(48, 128)), ("ising", lambda: _ising(6, 256))]
 
 
 @pytest.mark.parametrize("name,mk", LOCKSTEP_EPS1)
@@ -216,31 +184,6 @@ def test_lockstep_sampler_matches_policy_distribution(name, mk):
     d.close()
 
 
-@pytest.mark.parametrize("name,mk", LOCKSTEP_GRAD)
-def test_lockstep_fast_loss_and_grads_match_oracle_on_same_batch(name, mk):
-    e, t = mk()
-    d = engine.Trainer(e, t)
-    o = O.Oracle(e, t)
-    d.set_params(*o.params())
-    for it in range(2):
-        d.forward_rollout(it, o.schedule("explore", it))
-        bd = d.batch()
-        o.replay(bd["fwd_actions"])
-        _same_batch(bd, o.batch())
-        ld = d.compute_grads()
-        lo = o.compute_grads()
-        assert abs(ld - lo) <= 2e-2 * abs(lo) + 1e-6, (ld, lo)
-        gd, dzd = d.grads()
-        go, dzo = o.grads()
-        err, cos = _grad_close(gd, go)
-        assert err < 5e-2 and cos > 0.998, (err, cos)
-        assert abs(dzd - dzo) <= 2e-2 * abs(dzo) + 1e-6
-        o.apply_adam(o.schedule("lr", it))
-        d.set_params(*o.params())
-        d.set_adam_state(*o.adam())
-    d.close()
-
-
 @pytest.mark.parametrize("name,mk,T", [("bitseq", lambda: _bitseq(120, 1024), 15),
                                       ("ising", lambda: _ising(10, 1024), 100)])
 def test_lockstep_fast_iterations_run(name, mk, T):
@@ -250,37 +193,6 @@ def test_lockstep_fast_iterations_run(name, mk, T):
     assert np.all(np.isfinite(losses))
     b = d.batch()
     assert np.all(b["lengths"] == T)
-    d.close()
-
-
-# ---- fused rollout forward: emission tiles at awkward batch sizes (partial tiles, one
-# CTA, fewer trajectories than slots) and every objective of the H = 256 path
-EDGE = [
-    ("hypergrid_db_b65536", dict(batch=300)),
-    ("hypergrid_db_b65536", dict(batch=129)),
-    ("hypergrid_tb_b16", dict(batch=1)),
-    ("hypergrid_db_b65536", dict(batch=4000, objective="tb")),
-    ("hypergrid_db_b65536", dict(batch=700, objective="mdb")),
-    ("hypergrid_db_b65536", dict(batch=640, hidden=[128, 128])),
-]
-
-
-@pytest.mark.parametrize("name,kw", EDGE)
-def test_fused_path_edge_batches_match_oracle(name, kw):
-    e, t = _pair(name, **kw)
-    d = engine.Trainer(e, t)
-    o = O.Oracle(e, t)
-    d.set_params(*o.params())
-    eps = o.schedule("explore", 2)
-    d.forward_rollout(2, eps)
-    bd = d.batch()
-    o.replay(bd["fwd_actions"])
-    _same_batch(bd, o.batch())
-    ld = d.compute_grads()
-    lo = o.compute_grads()
-    assert abs(ld - lo) <= 2e-2 * abs(lo) + 1e-6, (ld, lo)
-    err, cos = _grad_close(d.grads()[0], o.grads()[0])
-    assert err < 5e-2 and cos > 0.998, (err, cos)
     d.close()
 
 
