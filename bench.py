@@ -74,6 +74,49 @@ def secondary_runs(names, steps, warmup, local):
     return out
 
 
+STEADY_CKPT = os.path.join(ROOT, "profiles", "hypergrid_db_converged.ckpt")
+
+
+def steady_state_leg(e, t, local, W, K):
+    """The headline workload from a CONVERGED policy (GFNCKPT1 checkpoint trained on the device
+    by profiles/make_converged_ckpt.py): the trajectory length under the target policy is
+    ~39 steps instead of ~5 at initialisation, so traj/s drops and rows/s is the
+    comparable rate. Device-timed like the headline (CUDA events on the engine stream)."""
+    from paper_2511_16592_b200 import engine
+    if not os.path.exists(STEADY_CKPT):
+        return {"error": "profiles/hypergrid_db_converged.ckpt missing"}
+    tr = engine.Trainer(e, t, device=local)
+    step = tr.load_checkpoint(STEADY_CKPT)
+    _, tv0 = tr.exact_terminal_marginal(20 ** 4)
+    tr.run(step, W)
+    r0 = tr.counters()[0]
+    tr.synchronize()
+    tr.event_record(0)
+    tr.run(step + W, K)
+    tr.event_record(1)
+    tr.synchronize()
+    ms = tr.event_elapsed(0, 1)
+    rows = tr.counters()[0] - r0
+    B = t.batch_size
+    out = {"checkpoint": os.path.relpath(STEADY_CKPT, ROOT), "checkpoint_step": step, "tv_exact_at_load": tv0,
+           "trajectories_per_s": B * K / (ms / 1e3), "rows_per_s": rows / (ms / 1e3),
+           "iters_per_s": K / (ms / 1e3), "ms_per_iter": ms / K, "mean_traj_len": rows / (B * K),
+           "iteration_tensor_frac": 8.0 * m_row(256, 5) * rows / (ms / 1e3) / 1e12 / measured_peaks()[1]}
+    tr.close()
+    return out
+
+
+def reward_sweep_leg(local, hbm):
+    """batched terminal-reward kernels over 2^16..2^26 terminals."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("reward_sweep", os.path.join(ROOT, "profiles", "reward_sweep.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    res = mod.sweep(sizes=(1 << 16, 1 << 20, 1 << 24, 1 << 26), reps=10, device=local, peak_gbs=hbm)
+    return {k: [{"terminals": r["terminals"], "gbs": r["gbs"], "frac_hbm": r["frac_hbm"]} for r in v]
+            for k, v in res.items()}
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -177,30 +220,34 @@ def measured_peaks():
     return 6650.0, 1590.0, "fallback"
 
 
-def kernel_work(name, rows, iters, H, A, O, n_params, nsm, batch=0, NH=16, SW=1):
-    """Algorithmic FLOPs and HBM bytes of one launch-set of `name` over `rows` real state rows
-    (DESIGN.md \u00a76). FLOPs count only the dense GEMMs over real rows (the one-hot layer 1
-    is a gather); bytes count each tensor the kernel must read or write once."""
+def m_row(H, A, flow=True):
+    """SURVEY §8(d) MACs per state row of the layers after the one-hot layer 1 (a row gather
+    of W1, counted in bytes): hidden H x H plus the heads the objective uses (fwd [+ flow])."""
+    return H * H + H * (A + (1 if flow else 0))
+
+
+def kernel_work(name, rows, iters, H, A, n_params, batch=0, SW=1):
+    """SURVEY §8(d) ALGORITHMIC FLOPs and HBM bytes of `iters` launches of `name` over `rows`
+    real state rows in total (not the design's own materialisation):
+      tensor FLOPs   2 * M_row per row for each of the rollout forward, the dgrad and the wgrad
+                     (the training forward is fused into the rollout; §8(d) counts 8 M_row per
+                     row for the whole iteration: rollout fwd + training fwd + dgrad + wgrad)
+      HBM bytes      (i) 23 B per live (b, t) for the rollout/step (5 bf16 logits + state r/w +
+                     action + log-prob), (iv) 28 B per parameter for Adam, the loss record once"""
     R = rows
-    rs = ((A + 3) + 3) // 4 * 4
-    if name == "k_fast_rollout":      # hidden + head GEMM per (row, step) + fused training forward
-        fl = 2.0 * R * (H * H + H * (A + 1))
-        by = R * (2 * 2 * H + 2 * H // 8 + NH * 4 + 8 + 4 * SW + 4) + batch * (4 + 8 + 4 * SW)
-        return fl, by
-    if name == "k_row_stats":         # head outputs -> masked log-softmax record
-        return 0.0, R * (NH * 4 + 4 + 4 * SW + 2 + rs * 4)
-    if name == "k_fast_fwd":          # (only when weights changed after the rollout)
-        return 2.0 * R * (H * H + H * (A + 1)), R * (2 * H * 2 + 2 * H // 8 + rs * 4)
-    if name == "k_fast_bwd":          # head dgrad + hidden dgrad; writes dz1, dz2, dhead
-        return 2.0 * R * (H * H + H * (A + 1)), R * (2 * H // 8 + rs * 4 + 16 + 8 + 4 * SW + 2 * 2 * H + 64 * 2)
-    if name == "k_fast_wgrad":        # dW2 + dW_head GEMMs (dW1 + db1 one-hot GEMM counted as bytes)
-        return 2.0 * R * (H * H + H * (A + 1)), R * (4 * H * 2 + 64 * 2 + 4 + 4 * SW) + nsm * n_params * 4
+    M = m_row(H, A)
+    if name in ("k_fast_rollout", "k_fast_fwd"):
+        return 2.0 * M * R, (A * 2 + 2 * 4 + 1 + 4) * R + batch * (4 + 8 + 4 * SW)
+    if name in ("k_fast_bwd", "k_fast_wgrad"):
+        return 2.0 * M * R, 0.0
+    if name == "k_row_stats":
+        return 0.0, R * ((A + 1) * 4 + 4 * 4)
+    if name == "k_fast_loss":
+        return 0.0, R * (4 * 4 + 4 + 2) + batch * 16
     if name == "k_reduce":
-        return 0.0, (nsm + 1) * n_params * 4 * iters
+        return 0.0, 2 * n_params * 4 * iters
     if name == "k_fast_adam":
         return 0.0, 28.0 * n_params * iters
-    if name == "k_fast_loss":
-        return 0.0, R * (3 * 4 + 16 + 4 + 2) + batch * 16
     return 0.0, 0.0
 
 
@@ -245,7 +292,12 @@ def run_reference(args, world, rank):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (environment-generated trajectories)",
         "config": {"workload": CONFIG, "env": "hypergrid d=4 H=20", "objective": "db",
-                   "mlp": "2x256", "global_batch": PER_GPU_BATCH * args.gpus},
+                   "mlp": "2x256", "global_batch": batch * procs,
+                   "sample": f"{procs} processes x B={batch} (distinct seeds); the workload's "
+                             f"B={PER_GPU_BATCH * args.gpus} per iteration is infeasible on CPU "
+                             f"(~10^3 s / iteration, >100 GB of tape), per-trajectory cost is ~flat in B",
+                   "build": "reference sources, g++ -O3 -march=x86-64-v3 (FMA on; the shipped CMake "
+                            "flags use -march=native, not portable to the GPU box's host)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs,
                          "kind": "reference" if O.ref_available("fast") else "port",
                          "sample": f"{procs} processes x reference run_bench(hypergrid 20^4 DB, "
@@ -292,6 +344,8 @@ def main():
     ap.add_argument("--batch", type=int, default=PER_GPU_BATCH, help="trajectories per GPU")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-steady", action="store_true", help="skip the converged-checkpoint leg")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the reward-kernel B sweep")
     ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
@@ -380,9 +434,9 @@ def main():
 
     cl = clocks.stop()
 
-    # ---- roofline of the dominant kernel
+    # ---- roofline of the dominant kernel (SURVEY §8(d) algorithmic work / measured time)
     hbm, tens, peak_kind = measured_peaks()
-    H, A, O_ = 256, 5, 80
+    H, A = 256, 5
     dom, dom_ms = max(prof.items(), key=lambda kv: kv[1][0]) if prof else (None, (0, 0))
     roof = None
     kernels = {}
@@ -392,29 +446,37 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f)
     for name, (tot_ms, cnt) in prof.items():
-        fl, by = kernel_work(name, rows, K, H, A, O_, tr.n_params, 148, batch=args.batch * K)
+        fl, by = kernel_work(name, rows, K, H, A, tr.n_params, batch=args.batch * K)
         sec = tot_ms / 1e3
-        kernels[name] = {"ms_total": round(tot_ms, 4), "launches": cnt,
-                         "tflops": fl / sec / 1e12 if sec else None,
-                         "gbs": by / sec / 1e9 if sec else None}
+        kernels[name] = {"ms_total": round(tot_ms, 4), "launches": cnt, "share_of_step": round(tot_ms / ms, 4),
+                         "tflops": fl / sec / 1e12 if sec and fl else None,
+                         "gbs": by / sec / 1e9 if sec and by else None}
     if dom:
-        fl, by = kernel_work(dom, rows, K, H, A, O_, tr.n_params, 148, batch=args.batch * K)
+        fl, by = kernel_work(dom, rows, K, H, A, tr.n_params, batch=args.batch * K)
         sec = dom_ms[0] / 1e3
-        ft = fl / sec / 1e12 / tens if sec else 0.0
-        fb = by / sec / 1e9 / hbm if sec else 0.0
         per = dom_ms[1]
-        if ft >= fb:
+        if fl > 0:  # GEMM-dominated kernels: the tensor roof (bf16, sustained)
             roof = {"kernel": dom, "bound": "tensor", "achieved": fl / sec / 1e12, "peak": tens,
-                    "unit": "TFLOP/s", "frac": ft}
+                    "unit": "TFLOP/s", "frac": fl / sec / 1e12 / tens}
         else:
             roof = {"kernel": dom, "bound": "hbm", "achieved": by / sec / 1e9, "peak": hbm,
-                    "unit": "GB/s", "frac": fb}
-        roof["peak_source"] = peak_kind
+                    "unit": "GB/s", "frac": by / sec / 1e9 / hbm}
+        roof["peak_source"] = peak_kind + " (MEASURED_PEAKS.json: bf16 sustained, HBM copy)"
         roof["share_of_step"] = dom_ms[0] / ms if ms else None
-        tr_k = (traffic or {}).get(dom, (traffic or {}).get(dom + "_ts"))  # H = 256: k_fast_rollout_ts
-        roof["traffic"] = tr_k
-        roof["algorithmic_per_launch"] = {"flops": fl / per if per else None,
-                                          "bytes": by / per if per else None}
+        roof["algorithmic_per_launch"] = {"flops": fl / per if per else None, "bytes_8d_i": by / per if per else None,
+                                          "rows": rows / K, "flops_per_row": 2 * m_row(H, A)}
+        roof["hbm_frac_of_8d_i_bytes"] = by / sec / 1e9 / hbm if sec else None
+        tk = (traffic or {}).get(dom)
+        if tk:  # ncu --set full of a launch of the same command (profiles/ncu_capture.py)
+            roof["traffic"] = tk["dram_bytes"]
+            roof["traffic_per_row"] = tk["dram_bytes"] / max(tk["rows"], 1)
+            roof["traffic_source"] = tk.get("source")
+        else:
+            roof["traffic"] = None
+    # the whole iteration against the tensor roof: 8 M_row FLOPs per real row
+    it_flops = 8.0 * m_row(H, A) * rows
+    iteration_roof = {"flops_per_iter": it_flops / K, "achieved_tflops": it_flops / (ms / 1e3) / 1e12,
+                      "peak": tens, "frac": it_flops / (ms / 1e3) / 1e12 / tens}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -423,6 +485,19 @@ def main():
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"failed: {ex}"}
+
+    steady = None
+    if rank == 0 and world == 1 and not args.no_steady:
+        try:
+            steady = steady_state_leg(e, t, local, W, K)
+        except Exception as ex:  # reported, never fatal
+            steady = {"error": str(ex)[:300]}
+    sweep = None
+    if rank == 0 and world == 1 and not args.no_sweep:
+        try:
+            sweep = reward_sweep_leg(local, hbm)
+        except Exception as ex:  # reported, never fatal
+            sweep = {"error": str(ex)[:300]}
 
     secondary = None
     if rank == 0 and world == 1 and args.secondary:
@@ -440,7 +515,9 @@ def main():
                        "train_iters_per_sec": K / (ms / 1e3),
                        "mean_traj_len": rows / (args.batch * K) if K else None,
                        "l2": "working set > L2 (bf16 activation images ~2 KB per state row)"},
+            "rows_per_s": rows / (ms / 1e3), "iteration_roofline": iteration_roof,
             "e2e": e2e, "gpu_launches": launches, "roofline": roof, "kernels": kernels,
+            "steady_state": steady, "reward_sweep": sweep,
             "cpu_baseline": cpu, "clocks": cl, "secondary": secondary,
         }
         print(json.dumps(line))

@@ -215,6 +215,16 @@ gfnx_status gfnx_get_grads(gfnx_ctx* ctx, double* flat, int64_t n, double* d_log
  * `masked_log_softmax` + `take` values of the reference tape (tape.cpp:177-245,
  * objectives.cpp:67-69), for per-row parity checks. */
 gfnx_status gfnx_export_row_logpf(gfnx_ctx* ctx, double* out, int64_t n);
+/* Terminal log-rewards of packed states (the packed layout of gfnx_export_batch's
+ * terminal_state): log_reward_of of every env — hypergrid.cpp:111-119,
+ * ModeSet::log_reward sequences.cpp:50-55, ising_energy ising.cpp:40-51 (log R = -E),
+ * graph_log_reward dag.cpp:313-322 — bit-identical to the reference. Host buffers
+ * states[n][state_words], out[n]; raises GFNX_ERR_CONTRACT for a non-terminal state where the
+ * reference throws (incomplete Ising configuration / bit string). */
+gfnx_status gfnx_log_rewards(gfnx_ctx* ctx, const uint32_t* states, int64_t n, double* out);
+/* Same over DEVICE buffers, word-major states_soa[state_words][n] (coalesced), out[n];
+ * stream-ordered on the ctx stream, no synchronisation (errors at the next sync point). */
+gfnx_status gfnx_log_rewards_device(gfnx_ctx* ctx, const uint32_t* states_soa, int64_t n, double* out);
 /* Diagnostics (read-only): copy an internal device buffer of the lockstep fast path by name
  * ("h<l>", "dz<l>", "mask<l>", "dlog", "rowbuf", "coef"); out == NULL returns the size. */
 gfnx_status gfnx_debug_buffer(gfnx_ctx* ctx, const char* name, void* out, int64_t cap, int64_t* bytes);

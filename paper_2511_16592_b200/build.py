@@ -20,6 +20,7 @@ UNITS = [
     ("fast.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
     ("lockstep.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
     ("group.cu", []),
+    ("reward.cu", []),
 ]
 HOST_UNITS = ["host.cpp"]
 

@@ -429,6 +429,8 @@ gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     up(&c.d_dag_cache, he.dag_cache);
     up(&c.d_neglog, he.neglog);
     c.h_dag_cache = he.dag_cache;
+    c.h_is_nbr = he.is_nbr;
+    c.h_is_J = he.is_J;
     P.modes = c.d_modes;
     P.bs_logr = c.d_bs_logr;
     P.is_nbr = c.d_is_nbr;
@@ -534,6 +536,7 @@ void gfnx_destroy(gfnx_ctx* h) {
   if (c.stream) cudaStreamSynchronize(c.stream);
   if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
   if (c.group) group_leave(c, c.group, c.rank);
+  reward_free(c);
   if (c.fast) fast_free(c);
   hg_buffer_free(c);
   if (c.phase) cudaFree(c.phase);
@@ -904,6 +907,36 @@ gfnx_status gfnx_debug_buffer(gfnx_ctx* h, const char* name, void* out, int64_t 
       cuda_check(cudaStreamSynchronize(c.stream), "sync");
       cuda_check(cudaMemcpy(out, p, n, cudaMemcpyDeviceToHost), "debug_buffer");
     }
+  });
+}
+
+gfnx_status gfnx_log_rewards_device(gfnx_ctx* h, const uint32_t* states_soa, int64_t n, double* out) {
+  return guard(h, [&] {
+    if (n < 0) fail(GFNX_ERR_CONFIG, "log_rewards: negative count");
+    reward_soa(h->c, states_soa, n, out);
+  });
+}
+
+gfnx_status gfnx_log_rewards(gfnx_ctx* h, const uint32_t* states, int64_t n, double* out) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n < 0) fail(GFNX_ERR_CONFIG, "log_rewards: negative count");
+    if (n == 0) return;
+    const int SW = c.P.SW;
+    std::vector<uint32_t> soa((size_t)SW * n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < SW; ++k) soa[(size_t)k * n + i] = states[(size_t)i * SW + k];
+    uint32_t* d_st = nullptr;
+    double* d_out = nullptr;
+    cuda_check(cudaMallocAsync(&d_st, sizeof(uint32_t) * soa.size(), c.stream), "log_rewards");
+    cuda_check(cudaMallocAsync(&d_out, sizeof(double) * n, c.stream), "log_rewards");
+    cuda_check(cudaMemcpyAsync(d_st, soa.data(), sizeof(uint32_t) * soa.size(), cudaMemcpyHostToDevice, c.stream),
+               "log_rewards");
+    reward_soa(c, d_st, n, d_out);
+    cuda_check(cudaMemcpyAsync(out, d_out, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "log_rewards");
+    cudaFreeAsync(d_st, c.stream);
+    cudaFreeAsync(d_out, c.stream);
+    check_device_error(c);
   });
 }
 

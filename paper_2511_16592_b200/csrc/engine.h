@@ -80,6 +80,9 @@ void test_ts_mma(const uint16_t* a, const uint16_t* b, float* d);
 
 // shared small kernels — batch.cu
 void launch_row_scan(Ctx& c, bool counts = true);
+// batched terminal log-rewards over word-major packed states [SW][n] (device) — reward.cu
+void reward_soa(Ctx& c, const uint32_t* st, int64_t n, double* out);
+void reward_free(Ctx& c);
 void ensure_row0(Ctx& c);              // row0 / row_bt of the resident batch (lazy after a fused rollout)
 bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row counts itself
 void fast_hg_marginal(Ctx& c, std::vector<double>* pt);  // exact terminal marginal (hypergrid)
@@ -114,6 +117,9 @@ struct Ctx {
   double* d_dag_cache = nullptr;
   double* d_neglog = nullptr;
   std::vector<double> h_dag_cache;
+  std::vector<int16_t> h_is_nbr;  // [D][4] ascending neighbours (host copy, reward tables)
+  std::vector<double> h_is_J;
+  double* d_is_rowtab = nullptr;  // [D][16] Ising row sums per neighbour pattern (reward.cu)
 
   // parameters: fp64 master (check mode) or fp32 master (fast mode)
   double* p64 = nullptr;

@@ -71,6 +71,8 @@ def lib():
         L.gfnx_compute_grads.argtypes = [vp, vp]
         L.gfnx_get_grads.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_export_row_logpf.argtypes = [vp, vp, C.c_int64]
+        L.gfnx_log_rewards.argtypes = [vp, vp, C.c_int64, vp]
+        L.gfnx_log_rewards_device.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_debug_buffer.argtypes = [vp, C.c_char_p, vp, C.c_int64, P(C.c_int64)]
         L.gfnx_iteration.argtypes = [vp, C.c_int64, vp]
         L.gfnx_run.argtypes = [vp, C.c_int64, C.c_int64, vp]
@@ -264,6 +266,17 @@ class Trainer:
         out = np.zeros((self.local_batch, self.T))
         self._check(lib().gfnx_export_row_logpf(self.h, _p(out), out.size))
         return out
+
+    def log_rewards(self, states):
+        """log_reward_of for packed terminal states [n, state_words] (host arrays)."""
+        st = np.ascontiguousarray(states, dtype=np.uint32)
+        out = np.zeros(len(st))
+        self._check(lib().gfnx_log_rewards(self.h, _p(st), len(st), _p(out)))
+        return out
+
+    def log_rewards_device(self, states_soa_ptr: int, n: int, out_ptr: int):
+        """Device pointers: word-major states [state_words][n] -> out[n] (stream-ordered)."""
+        self._check(lib().gfnx_log_rewards_device(self.h, C.c_void_p(states_soa_ptr), n, C.c_void_p(out_ptr)))
 
     def debug_buffer(self, name: str) -> np.ndarray:
         """Raw bytes of an internal device buffer (diagnostics; see gfnx_debug_buffer)."""

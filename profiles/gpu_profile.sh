@@ -1,7 +1,15 @@
-# full bench line + ncu launch list + one ncu --set full capture of the hot kernels (round profile)
-R=${1:-r1}
-timeout 900 python bench.py > gpurun_out/bench_full_$R.log 2>&1
+# Round profile: full bench line, reference arm, ncu launch list of the bench's own command,
+# and one ncu --set full capture of the hot kernels of timed iteration W+J of the SAME command
+# (so roofline.traffic is a launch of the timed region). usage: bash profiles/gpu_profile.sh r2
+R=${1:-r2}; W=5; K=50; J=25
+timeout 900 python bench.py --steps $K --warmup $W > gpurun_out/bench_full_$R.log 2>&1
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv python bench.py --steps 50 --warmup 5 --no-cpu --no-e2e --secondary "" > /dev/null 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_fast_(rollout|bwd|wgrad|loss)|k_row_stats" --launch-skip 40 --launch-count 5 -o gpurun_out/full_$R python profiles/run_config.py hypergrid_db_b65536 --iters 12 > gpurun_out/ncu_full_$R.log 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$R.csv \
+  python bench.py --steps $K --warmup $W --no-cpu --no-e2e --no-steady --no-sweep --secondary "" > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_fast_(rollout|bwd|wgrad)" \
+  --launch-skip $((3 * (W + J))) --launch-count 3 -o gpurun_out/full_$R \
+  python bench.py --steps $K --warmup $W --no-cpu --no-e2e --no-steady --no-sweep --secondary "" > gpurun_out/ncu_full_$R.log 2>&1
+ROWS=$(python -c "import json; d=json.loads(open('gpurun_out/bench_full_$R.log').read().strip().splitlines()[-1]); print(d['roofline']['algorithmic_per_launch']['rows'])")
+python profiles/summarize_ncu.py gpurun_out/full_$R.ncu-rep profiles/${R}_ncu_summary.md $ROWS \
+  "ncu --set full, bench.py --steps $K --warmup $W timed iteration W+$J (rows = mean rows per timed iteration)"
 tail -2 gpurun_out/ncu_full_$R.log

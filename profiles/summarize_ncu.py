@@ -1,6 +1,12 @@
 """Summarise an ncu --set full report into profiles/ (markdown + per-kernel DRAM traffic json).
 
-usage: python profiles/summarize_ncu.py gpurun_out/prof_rN.ncu-rep profiles/rN_ncu_summary.md
+usage: python profiles/summarize_ncu.py gpurun_out/prof_rN.ncu-rep profiles/rN_ncu_summary.md \
+           [rows_per_launch] [source description]
+
+With rows_per_launch (the real state rows of the captured iteration, e.g. bench.py's rows / K of
+the same command), profiles/ncu_traffic.json gets per kernel {dram_bytes, rows, duration_us,
+source} so bench.py can set roofline.traffic and compare traffic per row with the algorithmic
+bytes per row.
 """
 import csv
 import io
@@ -25,7 +31,7 @@ METRICS = [
 ]
 
 
-def main(rep, out_md):
+def main(rep, out_md, rows=None, source=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -60,14 +66,20 @@ def main(rep, out_md):
             u = units[idx[m]]
             return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
         t = mbytes("dram__bytes_read.sum") + mbytes("dram__bytes_write.sum")
-        traffic.setdefault(short, []).append(t)
+        dur = float(r[idx["gpu__time_duration.sum"]].replace(",", ""))
+        dur *= {"ns": 1e-3, "us": 1.0, "usecond": 1.0, "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}.get(
+            units[idx["gpu__time_duration.sum"]], 1.0)
+        traffic.setdefault(short, []).append((t, dur))
     with open(out_md, "w") as f:
         f.write("\n".join(lines) + "\n")
     tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
     with open(tj, "w") as f:
-        json.dump({k: sum(v) / len(v) for k, v in traffic.items()}, f, indent=1)
+        json.dump({k: {"dram_bytes": sum(x for x, _ in v) / len(v), "duration_us": sum(d for _, d in v) / len(v),
+                       "launches": len(v), "rows": rows, "source": source or os.path.basename(rep)}
+                   for k, v in traffic.items()}, f, indent=1)
     print("\n".join(lines))
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], float(sys.argv[3]) if len(sys.argv) > 3 else None,
+         sys.argv[4] if len(sys.argv) > 4 else None)
