@@ -466,7 +466,7 @@ def main():
         roof["algorithmic_per_launch"] = {"flops": fl / per if per else None, "bytes_8d_i": by / per if per else None,
                                           "rows": rows / K, "flops_per_row": 2 * m_row(H, A)}
         roof["hbm_frac_of_8d_i_bytes"] = by / sec / 1e9 / hbm if sec else None
-        tk = (traffic or {}).get(dom)
+        tk = (traffic or {}).get(dom) or (traffic or {}).get(dom + "_ts")  # H = 256: k_fast_rollout_ts
         if tk:  # ncu --set full of a launch of the same command (profiles/ncu_capture.py)
             roof["traffic"] = tk["dram_bytes"]
             roof["traffic_per_row"] = tk["dram_bytes"] / max(tk["rows"], 1)

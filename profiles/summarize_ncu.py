@@ -31,7 +31,7 @@ METRICS = [
 ]
 
 
-def main(rep, out_md, rows=None, source=None):
+def main(rep, out_md, rows_per_launch=None, source=None):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units, data = rows[0], rows[1], rows[2:]
@@ -75,7 +75,7 @@ def main(rep, out_md, rows=None, source=None):
     tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
     with open(tj, "w") as f:
         json.dump({k: {"dram_bytes": sum(x for x, _ in v) / len(v), "duration_us": sum(d for _, d in v) / len(v),
-                       "launches": len(v), "rows": rows, "source": source or os.path.basename(rep)}
+                       "launches": len(v), "rows": rows_per_launch, "source": source or os.path.basename(rep)}
                    for k, v in traffic.items()}, f, indent=1)
     print("\n".join(lines))
 
