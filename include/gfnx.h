@@ -185,12 +185,29 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* ctx, const char* path, int64_t* step)
 gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_t n, double* tv);
 
 /* Monte-Carlo terminal log-probability (mc_terminal_logprob, exact.hpp:229-241) of n packed
- * terminal states (hypergrid, DAG) under the current policy: num_samples backward trajectories each
- * from the uniform backward policy, drawn as backward_rollout does with key
- * {keys[2i], keys[2i+1]} (RngKey words, env_core.hpp:314-370), scored by one batched device
- * policy forward; out[i] = logsumexp_k(log_pf - log_pb) - log(num_samples). bf16 fast path. */
+ * terminal states under the current policy, every env and precision: num_samples backward
+ * trajectories each from the uniform backward policy, walked on the device exactly as
+ * backward_rollout draws them with key {keys[2i], keys[2i+1]} (RngKey words,
+ * env_core.hpp:314-370), scored by the device policy forward (score_trajectories,
+ * objectives.cpp:294-316); out[i] = logsumexp_k(log_pf - log_pb) - log(num_samples).
+ * Hypergrid / DAG bf16: one batched forward over all transitions on eval buffers. Bitseq /
+ * Ising and fp64 check mode: teacher-forced batches of local_batch walks through the resident
+ * batch, which is consumed (call gfnx_rollout again before training). */
 gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* ctx, const uint32_t* terminals, int64_t n, int32_t num_samples,
                                      const uint64_t* keys, double* out);
+
+/* backward_rollout (env_core.hpp:314-370) under the uniform backward policy: n = local_batch
+ * packed terminal states (this rank's slice, gfnx_batch_dims) walked back to s0 on the device
+ * (draw b = first_traj + i of `key`), then replayed forward (rollout_from_actions) into the
+ * resident batch — gfnx_compute_grads / gfnx_train_step / gfnx_export_batch act on it.
+ * CONTRACT on a non-terminal state. */
+gfnx_status gfnx_backward_rollout(gfnx_ctx* ctx, const uint32_t* terminals, int64_t n, uint64_t key_hi,
+                                  uint64_t key_lo);
+
+/* rollout_from_actions (env_core.hpp:166-229): n = local_batch * max_traj_len forward actions
+ * (row b = trajectory b, -1 after its end) replayed into the resident batch. CONTRACT on an
+ * illegal action or a trajectory that does not terminate. */
+gfnx_status gfnx_rollout_from_actions(gfnx_ctx* ctx, const int32_t* actions, int64_t n);
 
 /* Terminal-state FIFO of the `tv_buffer` metric, hypergrid (FifoBuffer, buffer.hpp:13-55,
  * fed by buffer.push_batch(batch.terminal_keys), train.cpp:231). reset: new empty buffer of

@@ -337,6 +337,7 @@ def ref_lib(kind: str = "port"):
         L.ref_exact_divergence.argtypes = [C.c_void_p, C.c_void_p]
         L.ref_pearson.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_uint64, C.c_void_p]
         L.ref_mc_logprob.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p]
+        L.ref_backward_rollout.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_uint64, C.c_uint64]
         L.ref_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_int64]
         L.ref_load_checkpoint.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
         _REF[kind] = L
@@ -416,8 +417,16 @@ class RefLib:
         self._check(self.L.ref_load_checkpoint(self.h, str(path).encode(), C.byref(st)))
         return st.value
 
+    def backward_rollout(self, terminal_words, key):
+        """backward_rollout (env_core.hpp:314-370) of packed terminals [B, state_words] under
+        key = (hi, lo): becomes the session batch (batch() / compute_grads() act on it)."""
+        w = np.ascontiguousarray(terminal_words, dtype=np.uint32)
+        assert len(w) == self.B
+        self._check(self.L.ref_backward_rollout(self.h, w.ctypes.data_as(C.c_void_p), len(w),
+                                                int(key[0]), int(key[1])))
+
     def mc_logprob(self, terminal_words, key, num_samples: int = 10):
-        """mc_terminal_logprob (exact.hpp:229-241) of one packed terminal (hypergrid),
+        """mc_terminal_logprob (exact.hpp:229-241) of one packed terminal state,
         key = (hi, lo) RngKey words."""
         w = np.ascontiguousarray(terminal_words, dtype=np.uint32)
         d = C.c_double()

@@ -70,8 +70,11 @@ struct SessionBase {
   // terminal log-probabilities (mc_terminal_logprob, exact.hpp:229-241, `mc` backward samples)
   // and the log-rewards over the builder's test set (generate_test_set, train.cpp:431-433)
   virtual double pearson_metric(int64_t, int, uint64_t) { throw config_error("pearson: bitseq only"); }
-  // mc_terminal_logprob (exact.hpp:229-241) of one packed terminal hypergrid state
-  virtual double mc_logprob(const uint32_t*, int, const RngKey&) { throw config_error("mc logprob: hypergrid / DAG only"); }
+  // mc_terminal_logprob (exact.hpp:229-241) of one packed terminal state
+  virtual double mc_logprob(const uint32_t*, int, const RngKey&) = 0;
+  // backward_rollout (env_core.hpp:314-370) of n packed terminal states -> the session batch
+  virtual void backward_batch(const uint32_t*, int, const RngKey&) = 0;
+  virtual void set_packing(int state_words) = 0;
   virtual std::vector<double>& grads() = 0;
   virtual double& dlogz() = 0;
   virtual AdamState& opt_main() = 0;
@@ -180,10 +183,10 @@ struct Session : SessionBase {
       return SessionBase::exact_divergence();
     }
   }
-  double mc_logprob(const uint32_t* w, int K, const RngKey& key) override {
+  // the env's terminal instance of packed device state words (DESIGN.md §4 layouts)
+  typename E::Instance terminal_of(const uint32_t* w) const {
+    typename E::Instance inst = env.reset_instance(params);
     if constexpr (std::is_same_v<E, HypergridEnv>) {
-      typename E::Instance inst;
-      inst.coords.assign(params.dim, 0);
       int sum = 0;
       for (int i = 0; i < params.dim; ++i) {  // packed: byte i = coordinate i
         inst.coords[i] = static_cast<int>((w[i >> 2] >> (8 * (i & 3))) & 0xffu);
@@ -191,11 +194,8 @@ struct Session : SessionBase {
       }
       inst.is_terminal = true;
       inst.step_count = sum + 1;
-      return mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, K, key);
     } else if constexpr (std::is_same_v<E, DagEnv>) {  // packed: row u in half (u & 1) of word u >> 1
-      typename E::Instance inst;
       const int d = params.d;
-      inst.adj.assign(d, 0u);
       for (int u = 0; u < d; ++u) {
         inst.adj[u] = (w[u >> 1] >> (16 * (u & 1))) & 0xffffu;
         inst.num_edges += __builtin_popcount(inst.adj[u]);
@@ -203,11 +203,39 @@ struct Session : SessionBase {
       inst.closure_t = closure_from_adjacency(inst.adj);
       inst.is_terminal = true;
       inst.step_count = inst.num_edges + 1;
-      return mc_terminal_logprob(env, params, pol, loss.learned_backward, inst, K, key);
-    } else {
-      return SessionBase::mc_logprob(w, K, key);
+    } else if constexpr (std::is_same_v<E, SequenceEnv>) {  // token bytes, then the filled mask
+      const int slots = params.max_len, tw = (slots + 3) / 4;
+      std::string key;
+      for (int i = 0; i < slots; ++i) {
+        if (!((w[tw + (i >> 5)] >> (i & 31)) & 1u)) throw contract_violation("packed bitseq: empty slot");
+        const int tok = static_cast<int>((w[i >> 2] >> (8 * (i & 3))) & 0xffu);
+        for (int b = params.bit_block - 1; b >= 0; --b) key += ((tok >> b) & 1) ? '1' : '0';
+      }
+      inst = env.terminal_from_key(key, params);
+    } else {  // Ising: assigned mask words, then the up mask words
+      const int dim = params.coupling->dim();
+      std::vector<int8_t> spins(dim);
+      for (int i = 0; i < dim; ++i) {
+        const bool as = (w[i >> 5] >> (i & 31)) & 1u;
+        const bool up = (w[pk_half + (i >> 5)] >> (i & 31)) & 1u;
+        spins[i] = as ? (up ? 1 : -1) : 0;
+      }
+      inst = env.terminal_from_spins(spins, params);
     }
+    return inst;
   }
+  int pk_half = 0;  // Ising: word offset of the up mask in the packed state (state_words / 2)
+  double mc_logprob(const uint32_t* w, int K, const RngKey& key) override {
+    return mc_terminal_logprob(env, params, pol, loss.learned_backward, terminal_of(w), K, key);
+  }
+  void backward_batch(const uint32_t* w, int n, const RngKey& key) override {
+    EnvState<E> terms;
+    for (int i = 0; i < n; ++i) terms.push_back(terminal_of(w + (size_t)i * sw));
+    RolloutOptions ropt;
+    ropt.record_delta_log_reward = loss.objective == Objective::kMDB;
+    tb = backward_rollout(env, params, &pol, loss.learned_backward, terms, key, ropt);
+  }
+  int sw = 1;  // packed state words per state
   double pearson_metric(int64_t step, int mc, uint64_t test_seed) override {
     if constexpr (std::is_same_v<E, SequenceEnv>) {
       const auto* modes = dynamic_cast<const ModeSet*>(params.reward.get());
@@ -225,13 +253,17 @@ struct Session : SessionBase {
       return SessionBase::pearson_metric(step, mc, test_seed);
     }
   }
+  void set_packing(int state_words) override {
+    sw = state_words;
+    pk_half = state_words / 2;
+  }
   std::vector<double>& grads() override { return g; }
   double& dlogz() override { return dz; }
   AdamState& opt_main() override { return om; }
   AdamState& opt_z() override { return oz; }
 };
 
-std::unique_ptr<SessionBase> make_session(const gfnx_env_desc& e, const gfnx_train_desc& t) {
+std::unique_ptr<SessionBase> make_session_raw(const gfnx_env_desc& e, const gfnx_train_desc& t) {
   switch (e.kind) {
     case GFNX_ENV_HYPERGRID: {
       HypergridEnv::Params p;
@@ -285,6 +317,25 @@ std::unique_ptr<SessionBase> make_session(const gfnx_env_desc& e, const gfnx_tra
     }
   }
   throw config_error("unknown env kind");
+}
+
+std::unique_ptr<SessionBase> make_session(const gfnx_env_desc& e, const gfnx_train_desc& t) {
+  auto s = make_session_raw(e, t);
+  // packed device state words: hypergrid a byte per coordinate; bitseq token
+  // bytes + filled mask; Ising assigned + up masks; DAG 16-bit adjacency rows
+  int sw = 1;
+  switch (e.kind) {
+    case GFNX_ENV_HYPERGRID: sw = (e.hg_dim + 3) / 4; break;
+    case GFNX_ENV_BITSEQ: {
+      const int slots = e.bs_n_bits / e.bs_k;
+      sw = (slots + 3) / 4 + (slots + 31) / 32;
+      break;
+    }
+    case GFNX_ENV_ISING: sw = 2 * ((e.is_side * e.is_side + 31) / 32); break;
+    case GFNX_ENV_DAG: sw = (e.dag_d + 1) / 2; break;
+  }
+  s->set_packing(sw);
+  return s;
 }
 
 struct RefSession {
@@ -442,6 +493,16 @@ int ref_mc_logprob(void* h, const uint32_t* term, int K, uint64_t key_hi, uint64
     k.hi = key_hi;
     k.lo = key_lo;
     *out = rs->s->mc_logprob(term, K, k);
+  });
+}
+
+int ref_backward_rollout(void* h, const uint32_t* terms, int n, uint64_t key_hi, uint64_t key_lo) {
+  RefSession* rs = static_cast<RefSession*>(h);
+  return guard(rs, [&] {
+    RngKey k;
+    k.hi = key_hi;
+    k.lo = key_lo;
+    rs->s->backward_batch(terms, n, k);
   });
 }
 

@@ -21,6 +21,7 @@ UNITS = [
     ("lockstep.cu", ["-Xptxas", "-v"] if os.environ.get("GFNX_PTXAS_V") else []),
     ("group.cu", []),
     ("reward.cu", []),
+    ("walk.cu", []),
 ]
 HOST_UNITS = ["host.cpp"]
 

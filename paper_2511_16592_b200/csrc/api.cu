@@ -290,6 +290,17 @@ void do_rollout(Ctx& c, int64_t it, double eps) {
   c.has_grads = false;
 }
 
+// a teacher-forced batch just landed in the resident batch (rollout_from_actions): row
+// counts, the global normalisers, batch flags
+void finish_forced(Ctx& c) {
+  launch_row_scan(c);
+  c.rows_stale = false;
+  if (c.world > 1) nccl_sum(c, c.batch.counters + 4, 2, ncclInt32);
+  cuda_check(cudaGetLastError(), "forced rollout launch");
+  c.has_batch = true;
+  c.has_grads = false;
+}
+
 // gradient + (optionally) Adam; loss read back when loss != nullptr
 void do_train(Ctx& c, bool apply, double lr, double* loss) {
   if (!c.has_batch) fail(GFNX_ERR_CONTRACT, "train_step: no resident batch (call gfnx_rollout)");
@@ -814,10 +825,62 @@ gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* h, double* marginal, int64_t 
 gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* h, const uint32_t* terminals, int64_t n, int32_t num_samples,
                                      const uint64_t* keys, double* out) {
   return guard(h, [&] {
-    if (h->c.check_mode()) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: bf16 fast path only");
+    Ctx& c = h->c;
     if (!terminals || !keys || !out) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: null buffer");
-    fast_mc_terminal_logprob(h->c, terminals, n, num_samples, keys, out);
-    check_device_error(h->c);
+    if (n < 1 || num_samples < 1) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
+    uint32_t* d_t = nullptr;
+    uint64_t* d_k = nullptr;
+    double* d_o = nullptr;
+    cuda_check(cudaMallocAsync(&d_t, sizeof(uint32_t) * n * c.P.SW, c.stream), "mc");
+    cuda_check(cudaMallocAsync(&d_k, sizeof(uint64_t) * 2 * n, c.stream), "mc");
+    cuda_check(cudaMallocAsync(&d_o, sizeof(double) * n, c.stream), "mc");
+    cuda_check(cudaMemcpyAsync(d_t, terminals, sizeof(uint32_t) * n * c.P.SW, cudaMemcpyHostToDevice, c.stream), "mc");
+    cuda_check(cudaMemcpyAsync(d_k, keys, sizeof(uint64_t) * 2 * n, cudaMemcpyHostToDevice, c.stream), "mc");
+    const bool rows_path = !c.check_mode() && (c.env.kind == GFNX_ENV_HYPERGRID || c.env.kind == GFNX_ENV_DAG);
+    if (rows_path) fast_mc_terminal_logprob(c, d_t, n, num_samples, d_k, d_o);
+    else mc_terminal_logprob_chunked(c, d_t, n, num_samples, d_k, d_o);
+    cuda_check(cudaMemcpyAsync(out, d_o, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "mc");
+    for (void* p : {(void*)d_t, (void*)d_k, (void*)d_o}) cudaFreeAsync(p, c.stream);
+    check_device_error(c);
+  });
+}
+
+gfnx_status gfnx_backward_rollout(gfnx_ctx* h, const uint32_t* terminals, int64_t n, uint64_t key_hi,
+                                  uint64_t key_lo) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (!terminals) fail(GFNX_ERR_CONFIG, "backward_rollout: null buffer");
+    if (n != c.Bl) fail(GFNX_ERR_CONFIG, "backward_rollout: n must equal the local batch (gfnx_batch_dims)");
+    uint32_t* d_t = nullptr;
+    cuda_check(cudaMallocAsync(&d_t, sizeof(uint32_t) * n * c.P.SW, c.stream), "backward rollout");
+    cuda_check(cudaMemcpyAsync(d_t, terminals, sizeof(uint32_t) * n * c.P.SW, cudaMemcpyHostToDevice, c.stream),
+               "backward rollout");
+    backward_rollout(c, d_t, Key{key_hi, key_lo});
+    cudaFreeAsync(d_t, c.stream);
+    finish_forced(c);
+    check_device_error(c);
+  });
+}
+
+gfnx_status gfnx_rollout_from_actions(gfnx_ctx* h, const int32_t* actions, int64_t n) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    const int64_t nt = (int64_t)c.Bl * c.P.T;
+    if (!actions) fail(GFNX_ERR_CONFIG, "rollout_from_actions: null buffer");
+    if (n != nt) fail(GFNX_ERR_CONFIG, "rollout_from_actions: size must be local_batch * max_traj_len");
+    std::vector<int16_t> a16(nt);
+    for (int64_t i = 0; i < nt; ++i) {
+      if (actions[i] < -1 || actions[i] >= c.P.A) fail(GFNX_ERR_CONTRACT, "rollout_from_actions: action out of range");
+      a16[i] = (int16_t)actions[i];
+    }
+    int16_t* d_a = nullptr;
+    cuda_check(cudaMallocAsync(&d_a, sizeof(int16_t) * nt, c.stream), "rollout_from_actions");
+    cuda_check(cudaMemcpyAsync(d_a, a16.data(), sizeof(int16_t) * nt, cudaMemcpyHostToDevice, c.stream),
+               "rollout_from_actions");
+    forced_rollout(c, d_a);
+    cudaFreeAsync(d_a, c.stream);
+    finish_forced(c);
+    check_device_error(c);
   });
 }
 

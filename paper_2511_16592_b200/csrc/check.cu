@@ -64,7 +64,8 @@ __device__ void dense_block(const double* h, int in, const double* W, const doub
 template <class Env>
 __global__ void k_check_rollout(EnvParams P, DevLayout D, const double* __restrict__ params,
                                 Key key, double eps, int b0, int Bl, DeviceBatch batch,
-                                double* obs_scratch, double* logit_scratch, int32_t* err) {
+                                double* obs_scratch, double* logit_scratch, int32_t* err,
+                                const int16_t* __restrict__ forced) {
   const int b = blockIdx.x;
   if (b >= Bl) return;
   __shared__ typename Env::State s;
@@ -85,6 +86,31 @@ __global__ void k_check_rollout(EnvParams P, DevLayout D, const double* __restri
   }
   __syncthreads();
   for (int t = 0; t < T; ++t) {
+    if (forced) {  // rollout_from_actions (env_core.hpp:166-229): the action is given
+      if (threadIdx.x == 0) {
+        const int a = forced[(size_t)b * T + t];
+        s_done = 1;
+        if (a < 0 || a >= A || !Env::legal(P, s, a)) {
+          atomicExch(err, GFNX_ERR_CONTRACT);
+        } else {
+          const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
+          const bool term = Env::step(P, s, a);
+          batch.actions[(size_t)b * T + t] = (int16_t)a;
+          batch.nparents[(size_t)b * T + t] = (uint16_t)Env::num_parents(P, s);
+          if (P.mdb && !term) batch.delta[(size_t)b * T + t] = Env::log_reward(P, s) - prev_r;
+          if (term) {
+            batch.lengths[b] = t + 1;
+            batch.log_rewards[b] = Env::log_reward(P, s);
+            Env::pack(P, s, batch.term_state + (size_t)b * P.SW);
+          } else {
+            s_done = 0;
+          }
+        }
+      }
+      __syncthreads();
+      if (s_done) break;
+      continue;
+    }
     for (int i = threadIdx.x; i < P.O; i += blockDim.x) obs[i] = 0.0;
     __syncthreads();
     if (threadIdx.x == 0) Env::features(P, s, [&](int f, double v) { obs[f] = v; });
@@ -509,10 +535,10 @@ __global__ void k_check_adam(double* p, const double* g, double* m, double* v, i
 }
 
 template <class Env>
-void rollout_impl(Ctx& c, Key key, double eps) {
+void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
   const DevLayout D = make_dev_layout(c);
   k_check_rollout<Env><<<c.Bl, 256, 0, c.stream>>>(c.P, D, c.p64, key, eps, c.b0, c.Bl, c.batch,
-                                                    c.ck_obs, c.ck_logp, c.batch.counters + 3);
+                                                    c.ck_obs, c.ck_logp, c.batch.counters + 3, forced);
   c.launches++;
 }
 
@@ -552,13 +578,26 @@ void ensure_scratch(Ctx& c, int64_t rows) {
 
 }  // namespace
 
-void check_rollout(Ctx& c, Key key, double eps) {
+void check_rollout(Ctx& c, Key key, double eps, const int16_t* forced) {
   ensure_scratch(c, c.Bl);
   switch (c.env.kind) {
-    case GFNX_ENV_HYPERGRID: rollout_impl<HypergridEnv>(c, key, eps); break;
-    case GFNX_ENV_BITSEQ: rollout_impl<BitseqEnv>(c, key, eps); break;
-    case GFNX_ENV_ISING: rollout_impl<IsingEnv>(c, key, eps); break;
-    case GFNX_ENV_DAG: rollout_impl<DagEnv>(c, key, eps); break;
+    case GFNX_ENV_HYPERGRID: rollout_impl<HypergridEnv>(c, key, eps, forced); break;
+    case GFNX_ENV_BITSEQ: rollout_impl<BitseqEnv>(c, key, eps, forced); break;
+    case GFNX_ENV_ISING: rollout_impl<IsingEnv>(c, key, eps, forced); break;
+    case GFNX_ENV_DAG: rollout_impl<DagEnv>(c, key, eps, forced); break;
+  }
+}
+
+// the policy forward + masked log-softmax over the resident batch's rows (no loss): the
+// per-row log pi of a teacher-forced batch (score_trajectories, objectives.cpp:294-316)
+void check_forward(Ctx& c) {
+  const int R = (int)total_rows(c);
+  ensure_scratch(c, R);
+  switch (c.env.kind) {
+    case GFNX_ENV_HYPERGRID: fwd_impl<HypergridEnv>(c, R, 0); break;
+    case GFNX_ENV_BITSEQ: fwd_impl<BitseqEnv>(c, R, 0); break;
+    case GFNX_ENV_ISING: fwd_impl<IsingEnv>(c, R, 0); break;
+    case GFNX_ENV_DAG: fwd_impl<DagEnv>(c, R, 0); break;
   }
 }
 

@@ -50,7 +50,9 @@ void group_leave(Ctx& c, Group* g, int rank);
 void group_allreduce(Ctx& c, void* buf, size_t n, int dtype);
 
 // check-mode (fp64 SIMT, reference operation order) — check.cu
-void check_rollout(Ctx& c, Key key, double eps);
+// forced: [Bl * T] actions of a teacher-forced batch (rollout_from_actions), or null to sample
+void check_rollout(Ctx& c, Key key, double eps, const int16_t* forced = nullptr);
+void check_forward(Ctx& c);  // per-row log-softmax of the resident batch (check_row_logpf reads it)
 void check_train(Ctx& c, bool apply, double lr, double* loss);
 void check_adam(Ctx& c, double lr);
 
@@ -69,7 +71,7 @@ bool ls_supported(const Ctx& c, std::string* why);
 void ls_init(Ctx& c);
 void ls_free(Ctx& c);
 void ls_sync_weights(Ctx& c);
-void ls_rollout(Ctx& c, Key key, double eps);
+void ls_rollout(Ctx& c, Key key, double eps, const int16_t* forced = nullptr);
 void ls_train(Ctx& c);
 void ls_row_logpf(Ctx& c, double* out);
 bool ls_debug_buffer(Ctx& c, const std::string& name, const void** ptr, size_t* bytes);
@@ -88,8 +90,25 @@ bool fast_rollout_counts(const Ctx& c);  // the fast rollout publishes the row c
 void fast_hg_marginal(Ctx& c, std::vector<double>* pt);  // exact terminal marginal (hypergrid)
 // tv_buffer metric (hypergrid): terminal-state FIFO + histogram on the device — fast.cu
 // mc_terminal_logprob (exact.hpp:229-241), hypergrid fast path — fast.cu
-void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
-                              double* out);
+// (device buffers: terminals [n][SW], keys [n][2], out [n])
+void fast_mc_terminal_logprob(Ctx& c, const uint32_t* d_terms, int64_t n, int K, const uint64_t* d_keys,
+                              double* d_out);
+void fast_forced_rollout(Ctx& c, const int16_t* d_forced);  // rollout_from_actions, bf16 paths
+// backward walks, teacher-forced batches, MC terminal log-probabilities — walk.cu
+void launch_bwd_walk(Ctx& c, const uint32_t* d_terms, int n_walks, int64_t j0, int64_t N, int K,
+                     const uint64_t* d_keys, Key key, int64_t draw_base, int16_t* d_act, uint16_t* d_np,
+                     int32_t* d_len, uint32_t* d_stst);
+void launch_replay(Ctx& c, const int16_t* d_forced, uint32_t* d_stst);
+void exclusive_scan_i32(Ctx& c, const int32_t* d_in, int32_t* d_out, int n);
+void launch_walk_rows(Ctx& c, const int32_t* d_len, const int32_t* d_row0, int n, int32_t* d_rows,
+                      int32_t* d_tiles, int tile_rows);
+void launch_mc_terms_rows(Ctx& c, const float* rowbuf, int rs, const int32_t* d_row0, const uint16_t* d_np,
+                          const int32_t* d_len, int n, double* d_terms);
+void launch_mc_lse(Ctx& c, const double* d_terms, int n, int K, double* d_out);
+void forced_rollout(Ctx& c, const int16_t* d_forced);
+void backward_rollout(Ctx& c, const uint32_t* d_terms, Key key);
+void mc_terminal_logprob_chunked(Ctx& c, const uint32_t* d_terms, int64_t n, int K, const uint64_t* d_keys,
+                                 double* d_out);
 void hg_buffer_reset(Ctx& c, int64_t capacity);
 void hg_buffer_push(Ctx& c);
 double hg_buffer_tv(Ctx& c);

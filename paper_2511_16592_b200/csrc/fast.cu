@@ -2717,170 +2717,71 @@ void fast_hg_marginal(Ctx& c, std::vector<double>* pt) {
   for (int64_t r = 0; r < n; ++r) (*pt)[cells[r]] = ptr[r];  // back to row-major cell order
 }
 
-// ---------------------------------------------------------------------------
-// backward_action_mask (hypergrid.cpp:52-61, dag.cpp:433-443) as the legal backward actions
-// in index order, and backward_step_instance (hypergrid.cpp:34-41, dag.cpp:407-417); the
-// forward action of a backward action is the same index (un-stop <-> stop) in both envs
-template <class Env>
-int bwd_legal(const EnvParams& P, const typename Env::State& s, int* out) {
-  if (s.term) {
-    out[0] = P.stop;
-    return 1;
-  }
-  int n = 0;
-  if constexpr (std::is_same<Env, HypergridEnv>::value) {
-    for (int j = 0; j < P.hg_dim; ++j)
-      if (s.c(j) > 0) out[n++] = j;
-  } else {
-    for (int a = 0; a < P.stop; ++a) {
-      int u, v;
-      DagEnv::edge(a, P.dag_d, u, v);
-      if ((s.adj.get(u) >> v) & 1) out[n++] = a;
-    }
-  }
-  return n;
-}
-
-template <class Env>
-void bwd_step(const EnvParams& P, typename Env::State& s, int a) {
-  if (a == P.stop) {
-    s.term = false;
-    return;
-  }
-  if constexpr (std::is_same<Env, HypergridEnv>::value) {
-    s.cw -= 1ull << (8 * a);
-  } else {  // remove the edge, rebuild the closure (closure_from_adjacency)
-    int u, v;
-    DagEnv::edge(a, P.dag_d, u, v);
-    uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    DagEnv::pack(P, s, w);
-    w[u >> 1] &= ~(1u << (v + 16 * (u & 1)));
-    DagEnv::unpack(P, w, s);
-  }
-}
-
-template <class Env>
-void fast_mc_walks(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
-                   std::vector<uint32_t>& st, std::vector<int16_t>& act, std::vector<int64_t>& traj_end,
-                   std::vector<double>& log_pb) {
-  const int SW = c.P.SW;
-  std::vector<int> legal(std::max(c.P.A, 1) + 1);
-  for (int64_t i = 0; i < n; ++i) {
-    typename Env::State s0;
-    Env::unpack(c.P, terminals + (size_t)i * SW, s0);
-    s0.term = true;
-    const Key key{keys[2 * i], keys[2 * i + 1]};
-    for (int k = 0; k < K; ++k) {
-      typename Env::State s = s0;
-      std::vector<uint32_t> rs;  // forward states (packed), reversed
-      std::vector<int> ra;       // forward actions, reversed
-      double lpb = 0.0;
-      for (int t = 0;; ++t) {
-        const int nl = bwd_legal<Env>(c.P, s, legal.data());
-        if (nl == 0) break;
-        if (t > c.P.T) raise_error(GFNX_ERR_CONTRACT, "backward_rollout: did not reach the initial state");
-        // categorical over weights 1.0 on the legal actions (rng.cpp:87-100)
-        const double u = uniform_scalar(fold_in(fold_in(key, (uint64_t)t), (uint64_t)k)) * (double)nl;
-        int pick = legal[nl - 1];
-        double acc = 0.0;
-        for (int q = 0; q < nl; ++q) {
-          acc += 1.0;
-          if (u < acc) {
-            pick = legal[q];
-            break;
-          }
-        }
-        // log_pb_uniform of the forward transition s' -> s: -log(num_parents(s))
-        lpb += -log((double)Env::num_parents(c.P, s));
-        bwd_step<Env>(c.P, s, pick);
-        const size_t o = rs.size();
-        rs.resize(o + SW);
-        Env::pack(c.P, s, rs.data() + o);
-        ra.push_back(pick);
-      }
-      for (size_t q = ra.size(); q-- > 0;) {  // forward order
-        st.insert(st.end(), rs.begin() + q * SW, rs.begin() + (q + 1) * SW);
-        act.push_back((int16_t)ra[q]);
-      }
-      traj_end.push_back((int64_t)act.size());
-      log_pb.push_back(lpb);
-    }
-  }
-}
-
-// mc_terminal_logprob (exact.hpp:229-241) on the fast path (hypergrid, DAG): K backward
-// trajectories per terminal under the uniform backward policy, drawn exactly as
-// backward_rollout does (env_core.hpp:314-370: step key fold_in(key, t), draw
-// categorical(fold_in(step_key, k)) over the legal backward actions, un-stop first), are
-// replayed forward (rollout_from_actions) through ONE batched policy forward on the device
-// (the training-forward kernel on explicit states: log pi(a|s) per transition); then
-// log p(x) ~= logsumexp_k(log_pf_k - log_pb_k) - log K. The walk is integer work on the
-// host; every policy evaluation runs on the GPU.
-void fast_mc_terminal_logprob(Ctx& c, const uint32_t* terminals, int64_t n, int K, const uint64_t* keys,
-                              double* out) {
+// mc_terminal_logprob (exact.hpp:229-241) on the fast path (hypergrid, DAG): the N = n K
+// uniform backward walks run on the device (k_bwd_walk: the reference's Threefry draws,
+// env_core.hpp:314-370), laid out as explicit state rows; ONE batched policy forward over
+// every transition (the training-forward kernel on eval buffers) gives log pi(a|s); per walk
+// log P_F - log P_B in forward order, then the per-terminal logsumexp (k_mc_terms_rows,
+// k_mc_lse). The only host sync reads the row count to size the activation buffers.
+void fast_mc_terminal_logprob(Ctx& c, const uint32_t* d_terms_in, int64_t n, int K, const uint64_t* d_keys,
+                              double* d_out) {
   if ((c.env.kind != GFNX_ENV_HYPERGRID && c.env.kind != GFNX_ENV_DAG) || lockstep(c))
-    raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: hypergrid / DAG fast path only");
-  if (n < 1 || K < 1) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
-  std::vector<uint32_t> st;             // forward states (packed), one per transition
-  std::vector<int16_t> act;             // forward action of the transition
-  std::vector<int64_t> traj_end;        // exclusive row end of trajectory (i, k)
-  std::vector<double> log_pb;           // per trajectory: sum of log_pb_uniform
-  if (c.env.kind == GFNX_ENV_HYPERGRID)
-    fast_mc_walks<HypergridEnv>(c, terminals, n, K, keys, st, act, traj_end, log_pb);
-  else
-    fast_mc_walks<DagEnv>(c, terminals, n, K, keys, st, act, traj_end, log_pb);
-  const int64_t R = (int64_t)act.size();
-  if (R > (int64_t)1 << 30) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: too many transitions");
+    raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob (fast rows): hypergrid / DAG fast path only");
+  const int64_t N = n * K;
+  if (N > (1 << 24)) raise_error(GFNX_ERR_CONFIG, "mc terminal log-prob: too many walks");
+  const int T = c.P.T, SW = c.P.SW;
   FastState& f = FS(c);
-  const int64_t tiles = (R + kTile - 1) / kTile, slots = tiles * kTile;
-  std::vector<int32_t> rows(slots, -1);
-  for (int64_t r = 0; r < R; ++r) rows[r] = (int32_t)r;
-  const int32_t ntiles = (int32_t)tiles;
-  const int H = f.H;
-  uint32_t* d_st;
-  int32_t *d_rows, *d_tiles;
   int16_t* d_act;
+  uint16_t* d_np;
+  int32_t *d_len, *d_row0, *d_tiles, *d_rows;
+  uint32_t* d_st;
+  double* d_terms;
+  auto alloc = [&](auto** p, size_t bytes) { cuda_check(cudaMallocAsync((void**)p, bytes, c.stream), "mc"); };
+  alloc(&d_act, sizeof(int16_t) * N * T);
+  alloc(&d_np, sizeof(uint16_t) * N * T);
+  alloc(&d_len, sizeof(int32_t) * N);
+  alloc(&d_row0, sizeof(int32_t) * (N + 1));
+  alloc(&d_tiles, sizeof(int32_t));
+  alloc(&d_st, sizeof(uint32_t) * N * T * SW);
+  alloc(&d_terms, sizeof(double) * N);
+  launch_bwd_walk(c, d_terms_in, (int)N, 0, N, K, d_keys, Key{0, 0}, 0, d_act, d_np, d_len, d_st);
+  exclusive_scan_i32(c, d_len, d_row0, (int)N);
+  int32_t R = 0;
+  cuda_check(cudaMemcpyAsync(&R, d_row0 + N, sizeof R, cudaMemcpyDeviceToHost, c.stream), "mc");
+  cuda_check(cudaStreamSynchronize(c.stream), "mc");
+  const int64_t tiles = (R + kTile - 1) / kTile, slots = std::max<int64_t>(tiles, 1) * kTile;
+  const int H = f.H;
   __nv_bfloat16 *d_h1, *d_h2;
   uint32_t *d_m1, *d_m2;
   float* d_rb;
-  cuda_check(cudaMalloc(&d_st, sizeof(uint32_t) * st.size()), "mc");
-  cuda_check(cudaMalloc(&d_rows, sizeof(int32_t) * slots), "mc");
-  cuda_check(cudaMalloc(&d_tiles, sizeof(int32_t)), "mc");
-  cuda_check(cudaMalloc(&d_act, sizeof(int16_t) * R), "mc");
-  cuda_check(cudaMalloc(&d_h1, sizeof(__nv_bfloat16) * slots * H), "mc");
-  cuda_check(cudaMalloc(&d_h2, sizeof(__nv_bfloat16) * slots * H), "mc");
-  cuda_check(cudaMalloc(&d_m1, sizeof(uint32_t) * slots * (H / 32)), "mc");
-  cuda_check(cudaMalloc(&d_m2, sizeof(uint32_t) * slots * (H / 32)), "mc");
-  cuda_check(cudaMalloc(&d_rb, sizeof(float) * slots * f.rs), "mc");
-  cudaMemcpyAsync(d_st, st.data(), sizeof(uint32_t) * st.size(), cudaMemcpyHostToDevice, c.stream);
-  cudaMemcpyAsync(d_rows, rows.data(), sizeof(int32_t) * slots, cudaMemcpyHostToDevice, c.stream);
-  cudaMemcpyAsync(d_tiles, &ntiles, sizeof(int32_t), cudaMemcpyHostToDevice, c.stream);
-  cudaMemcpyAsync(d_act, act.data(), sizeof(int16_t) * R, cudaMemcpyHostToDevice, c.stream);
+  alloc(&d_rows, sizeof(int32_t) * slots);
+  alloc(&d_h1, sizeof(__nv_bfloat16) * slots * H);
+  alloc(&d_h2, sizeof(__nv_bfloat16) * slots * H);
+  alloc(&d_m1, sizeof(uint32_t) * slots * (H / 32));
+  alloc(&d_m2, sizeof(uint32_t) * slots * (H / 32));
+  alloc(&d_rb, sizeof(float) * slots * f.rs);
+  launch_walk_rows(c, d_len, d_row0, (int)N, d_rows, d_tiles, kTile);
   with_kernels(c, [&](auto kk) {
     decltype(kk)::eval_forward(c, d_st, d_rows, d_tiles, d_act, d_h1, d_h2, d_m1, d_m2, d_rb);
   });
-  std::vector<float> rb((size_t)R * f.rs);
-  cuda_check(cudaMemcpyAsync(rb.data(), d_rb, sizeof(float) * rb.size(), cudaMemcpyDeviceToHost, c.stream), "mc");
-  cuda_check(cudaStreamSynchronize(c.stream), "mc");
-  void* bufs[] = {d_st, d_rows, d_tiles, d_act, d_h1, d_h2, d_m1, d_m2, d_rb};
-  for (void* b : bufs) cudaFree(b);
-  // score_trajectories (objectives.cpp:294-316) + logsumexp (fp64, sample order)
-  int64_t r0 = 0;
-  std::vector<double> terms(K);
-  for (int64_t i = 0; i < n; ++i) {
-    for (int k = 0; k < K; ++k) {
-      const int64_t j = i * K + k, r1 = traj_end[j];
-      double lpf = 0.0;
-      for (int64_t r = r0; r < r1; ++r) lpf += (double)rb[(size_t)r * f.rs + c.P.A];  // log pi(a|s)
-      terms[k] = lpf - log_pb[j];
-      r0 = r1;
-    }
-    double m = terms[0];
-    for (int k = 1; k < K; ++k) m = std::max(m, terms[k]);
-    double se = 0.0;
-    for (int k = 0; k < K; ++k) se += exp(terms[k] - m);
-    out[i] = m + log(se) - log((double)K);
+  launch_mc_terms_rows(c, d_rb, f.rs, d_row0, d_np, d_len, (int)N, d_terms);
+  launch_mc_lse(c, d_terms, (int)n, K, d_out);
+  void* bufs[] = {d_act, d_np, d_len, d_row0, d_tiles, d_st, d_terms, d_rows, d_h1, d_h2, d_m1, d_m2, d_rb};
+  for (void* p : bufs) cudaFreeAsync(p, c.stream);
+}
+
+// rollout_from_actions (env_core.hpp:166-229) into the resident batch: lockstep paths take
+// the actions inside their rollout kernels; hypergrid / DAG replay the env (k_replay) and the
+// training pass recomputes the forward over the rows (the weights did not produce them)
+void fast_forced_rollout(Ctx& c, const int16_t* d_forced) {
+  if (lockstep(c)) {
+    ls_rollout(c, Key{0, 0}, 0.0, d_forced);
+    return;
   }
+  int H = 0;
+  if (!supported(c, &H)) with_kernels(c, [](auto) {});  // raises config_error
+  launch_replay(c, d_forced, FS(c).stst);
+  FS(c).fused = false;
 }
 
 // ---------------------------------------------------------------------------

@@ -342,6 +342,7 @@ struct SampleArgs {
   int32_t* last_act;
   float* rowbuf;
   DeviceBatch batch;
+  const int16_t* forced;  // [Bl * T] teacher-forced actions (rollout_from_actions) or null
 };
 
 GFNX_DEV double warp_sum_d(double x) {
@@ -443,6 +444,12 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
   if (lane == 0) {
     const size_t bt = (size_t)b * a.T + a.t;
     const size_t r = (size_t)a.t * a.Bl + b;
+    if (a.forced) {  // rollout_from_actions (env_core.hpp:166-229): the given action
+      act = a.forced[bt];
+      typename E::State s;
+      E::unpack(P, w, s);
+      if (act < 0 || act >= P.A || !E::legal(P, s, act)) act = -1;
+    }
     if (act < 0 || !(z > 0.0)) {
       atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
       return;
@@ -1009,6 +1016,7 @@ struct PersistArgs {
   // Ising: layer 1 as an MMA over the assigned-spin one-hot (feature 2 site + up) against
   // W1[3s + u] - W1[3s + 2] (wimg[0]), bias = h1init: no per-row fp32 state between steps
   int l1_mma;
+  const int16_t* forced;  // [Bl * T] teacher-forced actions (rollout_from_actions) or null
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
@@ -1409,7 +1417,15 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       __syncthreads();
       const int p0 = xi[row][0], p1 = xi[row][1];
       // rounding fallback: the last legal column (rng.cpp:97-99)
-      const int act = p0 >= 0 ? p0 : (p1 >= 0 ? p1 : (xlast[row][1] >= 0 ? xlast[row][1] : xlast[row][0]));
+      int act = p0 >= 0 ? p0 : (p1 >= 0 ? p1 : (xlast[row][1] >= 0 ? xlast[row][1] : xlast[row][0]));
+      bool forced_bad = false;
+      if (a.forced) {  // rollout_from_actions (env_core.hpp:166-229): the given action
+        act = a.forced[(size_t)b * T + t];
+        typename E::State fs;
+        E::unpack(P, w, fs);
+        forced_bad = act < 0 || act >= P.A || !E::legal(P, fs, act);
+        if (forced_bad) act = 0;
+      }
       const float lse = hi + __logf(z);
       {  // log pi(a) = x_a - lse, x_a (bf16-rounded logit) still in the accumulator columns
         float xa = 0.f;
@@ -1433,7 +1449,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       tc_fence_before();
       if (half == 0) {  // record + env step
         const size_t bt = (size_t)b * T + t;
-        if (act < 0 || legal == 0 || !(z > 0.f)) {
+        if (act < 0 || forced_bad || legal == 0 || !(z > 0.f)) {
           atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
         } else {
           for (int i = 0; i < P.SW; ++i) a.stst[r * P.SW + i] = w[i];
@@ -1495,7 +1511,7 @@ __global__ void k_ls_ising_l1img(const __nv_bfloat16* w1, int D, uint8_t* img) {
 }
 
 template <class E>
-void rollout_impl(Ctx& c, Key key, double eps) {
+void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
   LsState& f = LS(c);
   const int T = f.T, Bl = c.Bl;
   cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)Bl * T, c.stream);
@@ -1545,6 +1561,7 @@ void rollout_impl(Ctx& c, Key key, double eps) {
     pa.rowbuf = f.rowbuf;
     pa.batch = c.batch;
     pa.phase = c.phase;
+    pa.forced = forced;
     const int smem = kH * kH * 2 + 1024;
     set_smem_once(k_ls_persist<E>, smem);
     ProfScope ps(c, "k_ls_persist");
@@ -1578,7 +1595,7 @@ void rollout_impl(Ctx& c, Key key, double eps) {
     typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl};
     launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
     SampleArgs sa{c.P, fold_in(key, (uint64_t)t), eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst,
-                  f.last_act, f.rowbuf, c.batch};
+                  f.last_act, f.rowbuf, c.batch, forced};
     ProfScope ps(c, "k_ls_sample");
     k_ls_sample<E><<<(Bl + 8 * kSampleRows - 1) / (8 * kSampleRows), 256, 0, c.stream>>>(sa);
     c.launches++;
@@ -1829,11 +1846,11 @@ void ls_row_logpf(Ctx& c, double* out) {
   c.launches++;
 }
 
-void ls_rollout(Ctx& c, Key key, double eps) {
+void ls_rollout(Ctx& c, Key key, double eps, const int16_t* forced) {
   if (c.env.kind == GFNX_ENV_BITSEQ)
-    rollout_impl<BitseqEnv>(c, key, eps);
+    rollout_impl<BitseqEnv>(c, key, eps, forced);
   else
-    rollout_impl<IsingEnv>(c, key, eps);
+    rollout_impl<IsingEnv>(c, key, eps, forced);
 }
 
 void ls_train(Ctx& c) {

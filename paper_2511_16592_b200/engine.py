@@ -98,6 +98,8 @@ def lib():
         L.gfnx_exact_terminal_marginal.argtypes = [vp, vp, C.c_int64, vp]
         L.gfnx_buffer_reset.argtypes = [vp, C.c_int64]
         L.gfnx_mc_terminal_logprob.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp]
+        L.gfnx_backward_rollout.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.c_uint64]
+        L.gfnx_rollout_from_actions.argtypes = [vp, vp, C.c_int64]
         L.gfnx_buffer_push.argtypes = [vp]
         L.gfnx_tv_buffer.argtypes = [vp, vp, vp]
         L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
@@ -244,6 +246,17 @@ class Trainer:
     # -- the hot path --
     def forward_rollout(self, it: int, eps: float):
         self._check(lib().gfnx_rollout(self.h, it, eps))
+
+    def backward_rollout(self, terminals, key):
+        """backward_rollout (env_core.hpp:314-370) of local_batch packed terminal states
+        [n, state_words] under key = (hi, lo): the resident batch (forward orientation)."""
+        t = np.ascontiguousarray(terminals, dtype=np.uint32)
+        self._check(lib().gfnx_backward_rollout(self.h, _p(t), len(t), int(key[0]), int(key[1])))
+
+    def rollout_from_actions(self, actions):
+        """rollout_from_actions (env_core.hpp:166-229): actions [local_batch, T], -1 padded."""
+        a = np.ascontiguousarray(actions, dtype=np.int32)
+        self._check(lib().gfnx_rollout_from_actions(self.h, _p(a), a.size))
 
     def train_step(self, lr: float, read_loss: bool = True):
         loss = C.c_double()
