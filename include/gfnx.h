@@ -196,6 +196,52 @@ gfnx_status gfnx_exact_terminal_marginal(gfnx_ctx* ctx, double* marginal, int64_
 gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* ctx, const uint32_t* terminals, int64_t n, int32_t num_samples,
                                      const uint64_t* keys, double* out);
 
+/* The bitseq `pearson` metric (train.cpp:440-454) of the current policy, on the device: the
+ * builder's test set (generate_test_set, sequences.cpp:100-119, key
+ * fold_in(make_key(test_seed), 0x7E57); n_modes * n_bits strings), mc_samples-walk
+ * gfnx_mc_terminal_logprob of each with key fold_in(fold_in(fold_in(make_key(seed), 0x3E7A),
+ * step), i), Pearson correlation with the log-rewards (metrics.cpp:96-116). Consumes the
+ * resident batch like gfnx_mc_terminal_logprob does. NUMERIC on zero variance. */
+gfnx_status gfnx_pearson(gfnx_ctx* ctx, int64_t step, int32_t mc_samples, uint64_t test_seed, double* out);
+
+/* ---- EB-GFN (run_eb_gfn, train.cpp:875-1018) on an Ising ctx -----------------------------
+ * The ctx's env (is_side, is_sigma) is the TRUE coupling J* that generates the data; the
+ * sampler is trained with TB (train desc: batch_size = the sampler batch) on the energy of
+ * the learned coupling J (zero at start), which is fitted by contrastive divergence with
+ * MH-corrected back-and-forth proposals (ising.cpp:222-373). Everything per iteration runs
+ * on the device: mixture selection, data-backed backward walks, the mixed rollout (sampled
+ * + teacher-forced rows), train_step, the k-step back-and-forth proposals, MH acceptance,
+ * cd_gradient, the J update and neg_log_rmse. Data: ctx-generated with the reference's Gibbs
+ * sampler (gibbs_data_sampler, key fold_in(make_key(seed), 0x919B)) or caller supplied. */
+typedef struct gfnx_eb_desc {
+  int32_t data_samples;      /* env.data_samples (2000) */
+  int32_t k;                 /* eb.k: back-and-forth steps; <= 0 means D */
+  int64_t gibbs_burn_in;     /* gibbs.burn_in (2000) */
+  int64_t gibbs_thinning;    /* gibbs.thinning (10) */
+  int32_t gibbs_chains;      /* gibbs.chains (1) */
+  int32_t data_batch;        /* eb.data_batch; <= 0 means the sampler batch */
+  double gibbs_hottest_beta; /* gibbs.hottest_beta (0.2) */
+  double alpha;              /* eb.alpha: on-policy fraction of the sampler batch (0.5) */
+  double coupling_lr;        /* eb.coupling_lr (0.05) */
+  double coupling_lr_end;    /* eb.coupling_lr_end (= coupling_lr) */
+} gfnx_eb_desc;
+
+gfnx_status gfnx_eb_default_desc(gfnx_eb_desc* out);
+/* gibbs_data_sampler (ising.cpp:185-220) on toroidal_coupling(side, sigma) with key
+ * fold_in(make_key(seed), 0x919B) (train.cpp:905-906): n x side^2 spins (host, no ctx) */
+gfnx_status gfnx_ising_gibbs_data(int32_t side, double sigma, uint64_t seed, const gfnx_eb_desc* desc,
+                                  int8_t* out, int64_t n);
+/* data: NULL (Gibbs-sample data_samples states from J*) or n x D spins in {-1, +1} */
+gfnx_status gfnx_eb_init(gfnx_ctx* ctx, const gfnx_eb_desc* desc, const int8_t* data, int64_t n);
+/* iterations it0 .. it0 + n - 1; out (or NULL): per iteration {loss, logZ, neg_log_rmse,
+ * accepted proposals} (the metrics.csv columns of train.cpp:938-1003 before interval
+ * averaging) */
+gfnx_status gfnx_eb_run(gfnx_ctx* ctx, int64_t it0, int64_t n, double* out);
+/* j_model / j_true: D x D row-major (either may be NULL); init_nlr: neg_log_rmse at start */
+gfnx_status gfnx_eb_coupling(gfnx_ctx* ctx, double* j_model, double* j_true, int64_t n, double* init_nlr);
+/* the data set: n_samples x D spins (n_samples from gfnx_eb_init) */
+gfnx_status gfnx_eb_dataset(gfnx_ctx* ctx, int8_t* out, int64_t n);
+
 /* backward_rollout (env_core.hpp:314-370) under the uniform backward policy: n = local_batch
  * packed terminal states (this rank's slice, gfnx_batch_dims) walked back to s0 on the device
  * (draw b = first_traj + i of `key`), then replayed forward (rollout_from_actions) into the

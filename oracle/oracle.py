@@ -448,6 +448,38 @@ class RefLib:
         return d.value
 
 
+def ref_eb_gfn(kv: dict, out_dir: str):
+    """The reference's run_eb_gfn (train.cpp:875-1018) via its Config front door, in a separate
+    process (oracle/_ref/eb_driver). Returns (result dict, coupling [D, D], metrics rows
+    [(step, loss, logZ, nlr, accept_rate)]) read back from its %.17g output files."""
+    exe = os.path.join(HERE, "_ref", "eb_driver")
+    r = subprocess.run([exe, out_dir] + [f"{k}={v}" for k, v in kv.items()], capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr)
+    init, best, final, loss = (float(x) for x in r.stdout.split())
+    with open(os.path.join(out_dir, "coupling.txt")) as f:
+        lines = f.read().strip().split("\n")[1:]
+    J = np.array([[float(v) for v in ln.split()] for ln in lines])
+    rows = []
+    with open(os.path.join(out_dir, "metrics.csv")) as f:
+        for ln in f.read().strip().split("\n")[1:]:
+            rows.append(tuple(float(v) for v in ln.split(",")))
+    return dict(init_nlr=init, best_nlr=best, final_nlr=final, final_loss=loss), J, rows
+
+
+def ref_gibbs_data(side: int, sigma: float, seed: int, n: int, burn_in: int = 2000, thinning: int = 10,
+                   chains: int = 1, hottest_beta: float = 0.2, kind: str = "port"):
+    """gibbs_data_sampler (ising.cpp:185-220) with key fold_in(make_key(seed), 0x919B)."""
+    L = ref_lib(kind)
+    L.ref_gibbs_data.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_int64, C.c_int64, C.c_int64, C.c_int,
+                                 C.c_double, C.c_void_p]
+    out = np.zeros((n, side * side), dtype=np.int8)
+    rc = L.ref_gibbs_data(side, sigma, seed, n, burn_in, thinning, chains, hottest_beta, _p(out))
+    if rc != 0:
+        raise RuntimeError(L.ref_last_error(None).decode())
+    return out
+
+
 def ref_run_bench(env_name: str, kv: dict, kind: str = "fast"):
     """The reference's own run_bench (train.cpp:294-334) via its Config front door."""
     L = ref_lib(kind)

@@ -525,6 +525,22 @@ void ref_threefry(uint64_t hi, uint64_t lo, uint64_t c0, uint64_t c1, uint64_t* 
   out[1] = w[1];
 }
 
+// gibbs_data_sampler (ising.cpp:185-220) on toroidal_coupling(side, sigma): n x D spins
+int ref_gibbs_data(int side, double sigma, uint64_t seed, int64_t n, int64_t burn_in, int64_t thinning,
+                   int chains, double hottest_beta, int8_t* out) {
+  return guard(nullptr, [&] {
+    GibbsConfig gc;
+    gc.burn_in = burn_in;
+    gc.thinning = thinning;
+    gc.num_chains = chains;
+    gc.hottest_beta = hottest_beta;
+    auto d = gibbs_data_sampler(toroidal_coupling(side, sigma), fold_in(make_key(seed), 0x919B), n, gc);
+    size_t o = 0;
+    for (const auto& v : d)
+      for (int8_t x : v) out[o++] = x;
+  });
+}
+
 // The reference's own benchmark harness (run_bench -> bench_scenario, train.cpp:294-334,
 // 801-809) through its Config front door. Returns mean it/s (and 3-sigma stderr).
 int ref_run_bench(const char* env_name, const char* const* keys, const char* const* values,

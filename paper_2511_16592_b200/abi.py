@@ -72,6 +72,13 @@ class HostBatch(C.Structure):
                 ("terminal_state", C.POINTER(C.c_uint32))]
 
 
+class EbDesc(C.Structure):  # gfnx_eb_desc
+    _fields_ = [("data_samples", C.c_int32), ("k", C.c_int32), ("gibbs_burn_in", C.c_int64),
+                ("gibbs_thinning", C.c_int64), ("gibbs_chains", C.c_int32), ("data_batch", C.c_int32),
+                ("gibbs_hottest_beta", C.c_double), ("alpha", C.c_double), ("coupling_lr", C.c_double),
+                ("coupling_lr_end", C.c_double)]
+
+
 class SlotView(C.Structure):
     _fields_ = [("it", C.c_int64), ("loss", C.c_double), ("n", C.c_int32),
                 ("state_words", C.c_int32), ("lengths", C.POINTER(C.c_int32)),

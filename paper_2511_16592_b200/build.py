@@ -22,6 +22,7 @@ UNITS = [
     ("group.cu", []),
     ("reward.cu", []),
     ("walk.cu", []),
+    ("eb.cu", ["--fmad=false"]),
 ]
 HOST_UNITS = ["host.cpp"]
 

@@ -7,6 +7,7 @@
 #include <nccl.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <string>
 #include <vector>
@@ -548,6 +549,7 @@ void gfnx_destroy(gfnx_ctx* h) {
   if (c.nccl) nccl_api().CommDestroy((ncclComm_t)c.nccl);
   if (c.group) group_leave(c, c.group, c.rank);
   reward_free(c);
+  eb_free(c);
   if (c.fast) fast_free(c);
   hg_buffer_free(c);
   if (c.phase) cudaFree(c.phase);
@@ -845,6 +847,91 @@ gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* h, const uint32_t* terminals, int
   });
 }
 
+gfnx_status gfnx_pearson(gfnx_ctx* h, int64_t step, int32_t mc_samples, uint64_t test_seed, double* out) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (!out) fail(GFNX_ERR_CONFIG, "pearson: null buffer");
+    if (mc_samples < 1) fail(GFNX_ERR_CONFIG, "pearson: mc_samples must be >= 1");
+    double* d = nullptr;
+    cuda_check(cudaMallocAsync(&d, sizeof(double), c.stream), "pearson");
+    bitseq_pearson(c, step, mc_samples, test_seed, d);
+    cuda_check(cudaMemcpyAsync(out, d, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "pearson");
+    cudaFreeAsync(d, c.stream);
+    check_device_error(c);
+  });
+}
+
+gfnx_status gfnx_eb_default_desc(gfnx_eb_desc* out) {
+  if (!out) return GFNX_ERR_CONFIG;
+  eb_default_desc(out);
+  return GFNX_OK;
+}
+
+gfnx_status gfnx_ising_gibbs_data(int32_t side, double sigma, uint64_t seed, const gfnx_eb_desc* desc,
+                                  int8_t* out, int64_t n) {
+  return guard(nullptr, [&] {
+    if (!desc || !out) fail(GFNX_ERR_CONFIG, "gibbs: null buffer");
+    if (side < 2) fail(GFNX_ERR_CONFIG, "ising: lattice side must be >= 2");
+    if (desc->gibbs_chains < 1) fail(GFNX_ERR_CONFIG, "gibbs: need at least one chain");
+    if (desc->gibbs_thinning < 1 || n < 0) fail(GFNX_ERR_CONFIG, "gibbs: bad sample counts");
+    const int D = side * side;
+    const auto d = ising_gibbs_data(ising_dense_coupling(side, sigma), D, fold_in(make_key(seed), 0x919B), n,
+                                    desc->gibbs_burn_in, desc->gibbs_thinning, desc->gibbs_chains,
+                                    desc->gibbs_hottest_beta);
+    std::copy(d.begin(), d.end(), out);
+  });
+}
+
+gfnx_status gfnx_eb_init(gfnx_ctx* h, const gfnx_eb_desc* desc, const int8_t* data, int64_t n) {
+  return guard(h, [&] {
+    if (!desc) fail(GFNX_ERR_CONFIG, "eb-gfn: null desc");
+    cuda_check(cudaStreamSynchronize(h->c.stream), "sync");
+    eb_init(h->c, *desc, data, n);
+    h->c.has_batch = false;
+    h->c.has_grads = false;
+  });
+}
+
+// run_eb_gfn's loop body (train.cpp:940-1003): the sampler update on the mixed batch
+// (forward rollout of the on-policy rows + backward_rollout of the data rows, one device
+// rollout with teacher-forced rows), then the energy-model update
+gfnx_status gfnx_eb_run(gfnx_ctx* h, int64_t it0, int64_t n, double* out) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if (n < 0) fail(GFNX_ERR_CONFIG, "eb-gfn: negative iteration count");
+    eb_ensure_metrics(c, std::max<int64_t>(n, 1));
+    const Key root = make_key(c.train.seed);
+    for (int64_t i = 0; i < n; ++i) {
+      const int64_t it = it0 + i;
+      const Key it_key = fold_in(root, 1000 + (uint64_t)it);
+      const double eps = schedule_value(c.train.explore, it);
+      const double lr = schedule_value(c.train.lr, it);
+      const int16_t* forced = eb_pre(c, it_key);
+      if (c.check_mode()) check_rollout(c, fold_in(it_key, 3), eps, forced);
+      else ls_rollout(c, fold_in(it_key, 3), eps, forced);
+      finish_forced(c);
+      do_train(c, true, lr, nullptr);
+      eb_post(c, it_key, eb_coupling_lr(c, it), i);
+    }
+    if (out && n > 0)
+      cuda_check(cudaMemcpyAsync(out, eb_metrics(c), sizeof(double) * 4 * n, cudaMemcpyDeviceToHost, c.stream),
+                 "eb metrics");
+    check_device_error(c);
+  });
+}
+
+gfnx_status gfnx_eb_coupling(gfnx_ctx* h, double* j_model, double* j_true, int64_t n, double* init_nlr) {
+  return guard(h, [&] {
+    Ctx& c = h->c;
+    if ((j_model || j_true) && n != (int64_t)c.P.is_D * c.P.is_D) fail(GFNX_ERR_CONFIG, "eb coupling: n must be D*D");
+    eb_coupling(c, j_model, j_true, init_nlr);
+  });
+}
+
+gfnx_status gfnx_eb_dataset(gfnx_ctx* h, int8_t* out, int64_t n) {
+  return guard(h, [&] { eb_dataset(h->c, out, n); });
+}
+
 gfnx_status gfnx_backward_rollout(gfnx_ctx* h, const uint32_t* terminals, int64_t n, uint64_t key_hi,
                                   uint64_t key_lo) {
   return guard(h, [&] {
@@ -871,6 +958,7 @@ gfnx_status gfnx_rollout_from_actions(gfnx_ctx* h, const int32_t* actions, int64
     std::vector<int16_t> a16(nt);
     for (int64_t i = 0; i < nt; ++i) {
       if (actions[i] < -1 || actions[i] >= c.P.A) fail(GFNX_ERR_CONTRACT, "rollout_from_actions: action out of range");
+      if (i % c.P.T == 0 && actions[i] < 0) fail(GFNX_ERR_CONTRACT, "rollout_from_actions: empty trajectory");
       a16[i] = (int16_t)actions[i];
     }
     int16_t* d_a = nullptr;

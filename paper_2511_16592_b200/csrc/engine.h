@@ -107,6 +107,18 @@ void launch_mc_terms_rows(Ctx& c, const float* rowbuf, int rs, const int32_t* d_
 void launch_mc_lse(Ctx& c, const double* d_terms, int n, int K, double* d_out);
 void forced_rollout(Ctx& c, const int16_t* d_forced);
 void backward_rollout(Ctx& c, const uint32_t* d_terms, Key key);
+// EB-GFN (run_eb_gfn, train.cpp:875-1018) — eb.cu
+void eb_default_desc(gfnx_eb_desc* d);
+void eb_init(Ctx& c, const gfnx_eb_desc& d, const int8_t* data, int64_t n);
+void eb_free(Ctx& c);
+void eb_ensure_metrics(Ctx& c, int64_t n);
+const int16_t* eb_pre(Ctx& c, Key it_key);
+void eb_post(Ctx& c, Key it_key, double j_lr, int64_t i);
+const double* eb_metrics(Ctx& c);
+double eb_coupling_lr(Ctx& c, int64_t it);
+void eb_coupling(Ctx& c, double* jm, double* jt, double* init_nlr);
+int64_t eb_dataset(Ctx& c, int8_t* out, int64_t n);
+void bitseq_pearson(Ctx& c, int64_t step, int mc, uint64_t test_seed, double* d_out);
 void mc_terminal_logprob_chunked(Ctx& c, const uint32_t* d_terms, int64_t n, int K, const uint64_t* d_keys,
                                  double* d_out);
 void hg_buffer_reset(Ctx& c, int64_t capacity);
@@ -177,6 +189,8 @@ struct Ctx {
 
   // fast-mode state (opaque, fast.cu)
   void* fast = nullptr;
+  // EB-GFN state (opaque, eb.cu)
+  void* eb = nullptr;
 
   // terminal-state FIFO of the tv_buffer metric (FifoBuffer, buffer.hpp:13-55): ring of
   // cell indices + per-cell counts on the device; head / size tracked on the host (every

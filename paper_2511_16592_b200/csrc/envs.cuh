@@ -43,6 +43,7 @@ struct EnvParams {
   int is_D;
   const int16_t* is_nbr;        // [D][4] ascending neighbour indices (-1 pad)
   const double* is_J;           // [D][4] coupling values
+  const double* is_Jd;          // [D][D] dense coupling (EB-GFN's learned model) or null
   // dag
   int dag_d;
   const double* dag_cache;      // [d][2^d]
@@ -255,6 +256,14 @@ struct IsingEnv {
   // neighbour list since the remaining terms are exact zeros (ising.cpp:40-51).
   __host__ __device__ static double log_reward(const EnvParams& P, const State& s) {
     double quad = 0.0;
+    if (P.is_Jd) {  // dense ising_energy (ising.cpp:40-51): the EB-GFN model coupling
+      for (int a = 0; a < P.is_D; ++a) {
+        double row = 0.0;
+        for (int b = 0; b < P.is_D; ++b) row += P.is_Jd[(size_t)a * P.is_D + b] * (double)spin(s, b);
+        quad += (double)spin(s, a) * row;
+      }
+      return -(-quad);
+    }
     for (int a = 0; a < P.is_D; ++a) {
       double row = 0.0;
       for (int q = 0; q < 4; ++q) {

@@ -402,6 +402,83 @@ void init_params(const gfnx_train_desc& t, const MlpLayout& L, int A, int Ab,
   dense(L.off_flw, L.H(), 1);
 }
 
+std::vector<double> ising_dense_coupling(int side, double sigma) {  // toroidal_coupling ising.cpp:15-31
+  const int D = side * side;
+  std::vector<double> J((size_t)D * D, 0.0);
+  auto site = [side](int r, int c) { return ((r + side) % side) * side + (c + side) % side; };
+  const int dr[4] = {1, -1, 0, 0}, dc[4] = {0, 0, 1, -1};
+  for (int r = 0; r < side; ++r)
+    for (int c = 0; c < side; ++c) {
+      const int a = site(r, c);
+      for (int q = 0; q < 4; ++q) {
+        const int b = site(r + dr[q], c + dc[q]);
+        if (a != b) J[(size_t)a * D + b] = sigma;
+      }
+    }
+  return J;
+}
+
+namespace {
+double dense_energy(const std::vector<int8_t>& s, const std::vector<double>& J, int D) {  // ising.cpp:40-51
+  double quad = 0.0;
+  for (int a = 0; a < D; ++a) {
+    double row = 0.0;
+    for (int b = 0; b < D; ++b) row += J[(size_t)a * D + b] * s[b];
+    quad += s[a] * row;
+  }
+  return -quad;
+}
+}  // namespace
+
+// gibbs_data_sampler (ising.cpp:185-220) with gibbs_sweep / heat_bath_prob_up (:162-183):
+// heat-bath sweeps of chain 0 (+ parallel tempering when chains > 1), burn-in, thinning.
+// One-time synthetic data generation for EB-GFN (train.cpp:899-907), like build_dag's data.
+std::vector<int8_t> ising_gibbs_data(const std::vector<double>& J, int D, Key key, int64_t n_samples,
+                                     int64_t burn_in, int64_t thinning, int chains, double hottest_beta) {
+  std::vector<double> betas(chains, 1.0);
+  for (int c = 1; c < chains; ++c) {
+    const double frac = (double)c / (chains - 1);
+    betas[c] = exp(log(1.0) + frac * (log(hottest_beta)));
+  }
+  std::vector<std::vector<int8_t>> state(chains, std::vector<int8_t>(D));
+  std::vector<double> u(D);
+  for (int c = 0; c < chains; ++c) {
+    random_uniform(fold_in(fold_in(key, 7777), (uint64_t)c), (size_t)D, u.data());
+    for (int a = 0; a < D; ++a) state[c][a] = u[a] < 0.5 ? -1 : 1;
+  }
+  std::vector<int8_t> out;
+  out.reserve((size_t)n_samples * D);
+  int64_t sweep = 0, got = 0;
+  while (got < n_samples) {
+    const Key sweep_key = fold_in(key, (uint64_t)sweep);
+    for (int c = 0; c < chains; ++c) {
+      const Key ck = fold_in(sweep_key, (uint64_t)c);
+      std::vector<int8_t>& sp = state[c];
+      for (int site = 0; site < D; ++site) {
+        double h = 0.0;
+        for (int b = 0; b < D; ++b)
+          if (b != site) h += J[(size_t)site * D + b] * sp[b];
+        const double p_up = 1.0 / (1.0 + exp(-4.0 * betas[c] * h));
+        sp[site] = uniform_scalar(fold_in(ck, (uint64_t)site)) < p_up ? 1 : -1;
+      }
+    }
+    if (chains > 1) {
+      for (int c = (int)(sweep % 2); c + 1 < chains; c += 2) {
+        const double e_lo = dense_energy(state[c], J, D);
+        const double e_hi = dense_energy(state[c + 1], J, D);
+        const double log_a = (betas[c] - betas[c + 1]) * (e_lo - e_hi);
+        if (log(uniform_scalar(fold_in(fold_in(sweep_key, 999), (uint64_t)c))) < log_a) std::swap(state[c], state[c + 1]);
+      }
+    }
+    ++sweep;
+    if (sweep > burn_in && (sweep - burn_in) % thinning == 0) {
+      out.insert(out.end(), state[0].begin(), state[0].end());
+      ++got;
+    }
+  }
+  return out;
+}
+
 double schedule_value(const gfnx_schedule& s, int64_t step) {
   if (s.warmup > 0 && step < s.warmup) return s.start_value * (double)step / (double)s.warmup;
   const double prog = s.horizon > 0 ? std::min(1.0, (double)(step - s.warmup) / (double)s.horizon) : 1.0;

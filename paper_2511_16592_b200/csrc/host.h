@@ -41,6 +41,12 @@ void make_layout(const gfnx_train_desc& t, const gfnx_env_shape& s, MlpLayout* L
 void init_params(const gfnx_train_desc& t, const MlpLayout& L, int A, int Ab,
                  std::vector<double>* params);
 double schedule_value(const gfnx_schedule& s, int64_t step);  // optim.cpp:45-66
+// EB-GFN setup (train.cpp:890-920): the true toroidal coupling as a dense [D][D] matrix and the
+// Gibbs data sampler over it (samples [n][D], spins +-1)
+std::vector<double> ising_dense_coupling(int side, double sigma);
+struct Key;
+std::vector<int8_t> ising_gibbs_data(const std::vector<double>& J, int D, Key key, int64_t n_samples,
+                                     int64_t burn_in, int64_t thinning, int chains, double hottest_beta);
 void resolve_schedule(gfnx_schedule* s, int64_t iterations);  // train.cpp:98-101
 void default_env(int kind, gfnx_env_desc* e);
 void default_train(int kind, gfnx_train_desc* t);

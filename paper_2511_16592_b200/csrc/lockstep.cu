@@ -342,7 +342,7 @@ struct SampleArgs {
   int32_t* last_act;
   float* rowbuf;
   DeviceBatch batch;
-  const int16_t* forced;  // [Bl * T] teacher-forced actions (rollout_from_actions) or null
+  const int16_t* forced;  // [Bl * T] teacher-forced actions (rows starting with -1 are sampled) or null
 };
 
 GFNX_DEV double warp_sum_d(double x) {
@@ -444,7 +444,7 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
   if (lane == 0) {
     const size_t bt = (size_t)b * a.T + a.t;
     const size_t r = (size_t)a.t * a.Bl + b;
-    if (a.forced) {  // rollout_from_actions (env_core.hpp:166-229): the given action
+    if (a.forced && a.forced[(size_t)b * a.T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
       act = a.forced[bt];
       typename E::State s;
       E::unpack(P, w, s);
@@ -1016,7 +1016,7 @@ struct PersistArgs {
   // Ising: layer 1 as an MMA over the assigned-spin one-hot (feature 2 site + up) against
   // W1[3s + u] - W1[3s + 2] (wimg[0]), bias = h1init: no per-row fp32 state between steps
   int l1_mma;
-  const int16_t* forced;  // [Bl * T] teacher-forced actions (rollout_from_actions) or null
+  const int16_t* forced;  // [Bl * T] teacher-forced actions (rows starting with -1 are sampled) or null
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
@@ -1419,7 +1419,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       // rounding fallback: the last legal column (rng.cpp:97-99)
       int act = p0 >= 0 ? p0 : (p1 >= 0 ? p1 : (xlast[row][1] >= 0 ? xlast[row][1] : xlast[row][0]));
       bool forced_bad = false;
-      if (a.forced) {  // rollout_from_actions (env_core.hpp:166-229): the given action
+      if (a.forced && a.forced[(size_t)b * T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
         act = a.forced[(size_t)b * T + t];
         typename E::State fs;
         E::unpack(P, w, fs);

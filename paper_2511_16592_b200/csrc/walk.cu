@@ -181,7 +181,107 @@ void env_dispatch(const Ctx& c, F&& fn) {
   }
 }
 
+// generate_test_set (sequences.cpp:100-119): for every mode m and flips f < n, the mode
+// string with f distinct positions flipped, chosen by a partial Fisher-Yates shuffle whose
+// draw counter runs across items (item (m, f) starts at draw m n(n-1)/2 + f(f-1)/2); written
+// as packed terminal states (k-bit tokens MSB first, all slots filled) + the item keys
+// fold_in(mkey, i) of the pearson metric (train.cpp:446-448)
+__global__ void k_bs_testset(EnvParams P, Key key, Key mkey, uint32_t* __restrict__ terms, uint64_t* __restrict__ keys) {
+  const int n = P.bs_nbits;
+  const int item = blockIdx.x * blockDim.x + threadIdx.x;
+  if (item >= P.n_modes * n) return;
+  const int m = item / n, f = item % n;
+  uint64_t bits[kMaxModeWords];
+  for (int w = 0; w < kMaxModeWords; ++w) bits[w] = w < P.bs_words ? P.modes[(size_t)m * P.bs_words + w] : 0ull;
+  uint16_t pos[kMaxModeWords * 64];
+  for (int i = 0; i < n; ++i) pos[i] = (uint16_t)i;
+  uint64_t draw = (uint64_t)m * ((uint64_t)n * (n - 1) / 2) + (uint64_t)f * (f - 1) / 2;
+  for (int i = 0; i < f; ++i) {
+    const int r = n - i;  // random_range (rng.cpp:82-85)
+    const int j = i + (int)(uniform_scalar(fold_in(key, draw++)) * r) % r;
+    const uint16_t x = pos[i];
+    pos[i] = pos[j];
+    pos[j] = x;
+    const int b = pos[i];
+    bits[b >> 6] ^= 1ull << (63 - (b & 63));
+  }
+  uint32_t* w = terms + (size_t)item * P.SW;
+  for (int q = 0; q < P.SW; ++q) w[q] = 0u;
+  const int tw = (P.bs_slots + 3) / 4;
+  for (int s = 0; s < P.bs_slots; ++s) {
+    uint32_t tok = 0;
+    for (int b = 0; b < P.bs_k; ++b) {
+      const int i = s * P.bs_k + b;
+      tok = (tok << 1) | (uint32_t)((bits[i >> 6] >> (63 - (i & 63))) & 1ull);
+    }
+    w[s >> 2] |= tok << (8 * (s & 3));
+    w[tw + (s >> 5)] |= 1u << (s & 31);
+  }
+  const Key k = fold_in(mkey, (uint64_t)item);
+  keys[2 * (size_t)item] = k.hi;
+  keys[2 * (size_t)item + 1] = k.lo;
+}
+
+__global__ void k_bs_log_reward(EnvParams P, const uint32_t* __restrict__ terms, int n, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  BitseqEnv::State s;
+  BitseqEnv::unpack(P, terms + (size_t)i * P.SW, s);
+  out[i] = BitseqEnv::log_reward(P, s);
+}
+
+// pearson (metrics.cpp:96-116), sequential in the reference's order
+__global__ void k_pearson(const double* __restrict__ xs, const double* __restrict__ ys, int n, double* out,
+                          int32_t* err) {
+  const double nn = (double)n;
+  double mx = 0.0, my = 0.0;
+  for (int i = 0; i < n; ++i) {
+    mx += xs[i];
+    my += ys[i];
+  }
+  mx /= nn;
+  my /= nn;
+  double sxy = 0.0, sxx = 0.0, syy = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const double dx = xs[i] - mx, dy = ys[i] - my;
+    sxy += dx * dy;
+    sxx += dx * dx;
+    syy += dy * dy;
+  }
+  if (!(sxx > 0.0) || !(syy > 0.0)) {
+    atomicExch(err, GFNX_ERR_NUMERIC);  // pearson: zero variance
+    *out = 0.0;
+    return;
+  }
+  *out = sxy / sqrt(sxx * syy);
+}
+
 }  // namespace
+
+// the bitseq `pearson` metric (train.cpp:440-454): Pearson correlation of the device MC
+// terminal log-probabilities (mc samples per string) and the log-rewards over the builder's
+// test set (generate_test_set with key fold_in(make_key(test_seed), 0x7E57)); result in d_out
+void bitseq_pearson(Ctx& c, int64_t step, int mc, uint64_t test_seed, double* d_out) {
+  if (c.env.kind != GFNX_ENV_BITSEQ) raise_error(GFNX_ERR_CONFIG, "pearson: bitseq only");
+  const int n = c.P.n_modes * c.P.bs_nbits;
+  if (n < 2) raise_error(GFNX_ERR_CONTRACT, "pearson: need two equal-length series");
+  uint32_t* d_t = nullptr;
+  uint64_t* d_k = nullptr;
+  double *d_lp = nullptr, *d_lr = nullptr;
+  cuda_check(cudaMallocAsync(&d_t, sizeof(uint32_t) * (size_t)n * c.P.SW, c.stream), "pearson");
+  cuda_check(cudaMallocAsync(&d_k, sizeof(uint64_t) * 2 * (size_t)n, c.stream), "pearson");
+  cuda_check(cudaMallocAsync(&d_lp, sizeof(double) * (size_t)n, c.stream), "pearson");
+  cuda_check(cudaMallocAsync(&d_lr, sizeof(double) * (size_t)n, c.stream), "pearson");
+  const Key tkey = fold_in(make_key(test_seed), 0x7E57);
+  const Key mkey = fold_in(fold_in(make_key(c.train.seed), 0x3E7A), (uint64_t)step);
+  k_bs_testset<<<(n + 127) / 128, 128, 0, c.stream>>>(c.P, tkey, mkey, d_t, d_k);
+  k_bs_log_reward<<<(n + 127) / 128, 128, 0, c.stream>>>(c.P, d_t, n, d_lr);
+  c.launches += 2;
+  mc_terminal_logprob_chunked(c, d_t, n, mc, d_k, d_lp);
+  k_pearson<<<1, 1, 0, c.stream>>>(d_lp, d_lr, n, d_out, c.batch.counters + 3);
+  c.launches++;
+  for (void* p : {(void*)d_t, (void*)d_k, (void*)d_lp, (void*)d_lr}) cudaFreeAsync(p, c.stream);
+}
 
 void launch_bwd_walk(Ctx& c, const uint32_t* d_terms, int n_walks, int64_t j0, int64_t N, int K,
                      const uint64_t* d_keys, Key key, int64_t draw_base, int16_t* d_act, uint16_t* d_np,

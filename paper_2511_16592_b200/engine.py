@@ -100,6 +100,13 @@ def lib():
         L.gfnx_mc_terminal_logprob.argtypes = [vp, vp, C.c_int64, C.c_int32, vp, vp]
         L.gfnx_backward_rollout.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.c_uint64]
         L.gfnx_rollout_from_actions.argtypes = [vp, vp, C.c_int64]
+        L.gfnx_pearson.argtypes = [vp, C.c_int64, C.c_int32, C.c_uint64, vp]
+        L.gfnx_eb_default_desc.argtypes = [P(abi.EbDesc)]
+        L.gfnx_eb_init.argtypes = [vp, P(abi.EbDesc), vp, C.c_int64]
+        L.gfnx_eb_run.argtypes = [vp, C.c_int64, C.c_int64, vp]
+        L.gfnx_eb_coupling.argtypes = [vp, vp, vp, C.c_int64, vp]
+        L.gfnx_eb_dataset.argtypes = [vp, vp, C.c_int64]
+        L.gfnx_ising_gibbs_data.argtypes = [C.c_int32, C.c_double, C.c_uint64, P(abi.EbDesc), vp, C.c_int64]
         L.gfnx_buffer_push.argtypes = [vp]
         L.gfnx_tv_buffer.argtypes = [vp, vp, vp]
         L.gfnx_load_checkpoint.argtypes = [vp, C.c_char_p, vp]
@@ -107,6 +114,25 @@ def lib():
         L.gfnx_slot_wait.argtypes = [vp, C.c_int32, P(abi.SlotView)]
         _LIB = L
     return _LIB
+
+
+def eb_desc(**kw):
+    """run_eb_gfn's defaults (train.cpp:899-913) as a gfnx_eb_desc, with overrides."""
+    d = abi.EbDesc()
+    lib().gfnx_eb_default_desc(C.byref(d))
+    for k, v in kw.items():
+        if not hasattr(d, k):
+            raise KeyError(k)
+        setattr(d, k, v)
+    return d
+
+
+def ising_gibbs_data(side: int, sigma: float, seed: int, n: int, desc=None):
+    """gibbs_data_sampler (ising.cpp:185-220) on the true toroidal coupling: [n, side^2] spins."""
+    d = desc if desc is not None else eb_desc()
+    out = np.zeros((n, side * side), dtype=np.int8)
+    _raise(lib().gfnx_ising_gibbs_data(side, sigma, seed, C.byref(d), _p(out), n))
+    return out
 
 
 def _p(a):
@@ -252,6 +278,41 @@ class Trainer:
         [n, state_words] under key = (hi, lo): the resident batch (forward orientation)."""
         t = np.ascontiguousarray(terminals, dtype=np.uint32)
         self._check(lib().gfnx_backward_rollout(self.h, _p(t), len(t), int(key[0]), int(key[1])))
+
+    def pearson(self, step: int, mc: int = 10, test_seed: int = 1) -> float:
+        """The bitseq `pearson` metric (train.cpp:440-454), entirely on the device."""
+        d = C.c_double()
+        self._check(lib().gfnx_pearson(self.h, step, mc, test_seed, C.byref(d)))
+        return d.value
+
+    # -- EB-GFN (run_eb_gfn, train.cpp:875-1018) --
+    def eb_init(self, desc=None, data=None):
+        """Start an EB-GFN run (Ising ctx); data: None (Gibbs sampler) or [n, D] spins."""
+        d = desc if desc is not None else eb_desc()
+        if data is None:
+            self._check(lib().gfnx_eb_init(self.h, C.byref(d), None, 0))
+        else:
+            a = np.ascontiguousarray(data, dtype=np.int8)
+            self._check(lib().gfnx_eb_init(self.h, C.byref(d), _p(a), len(a)))
+
+    def eb_run(self, it0: int, n: int):
+        """Iterations it0..it0+n-1; returns [n, 4] rows (loss, logZ, neg_log_rmse, accepted)."""
+        out = np.zeros((n, 4))
+        self._check(lib().gfnx_eb_run(self.h, it0, n, _p(out)))
+        return out
+
+    def eb_coupling(self):
+        """(J_model, J_true, initial neg_log_rmse)."""
+        D = self.env.is_side * self.env.is_side
+        jm, jt, z = np.zeros((D, D)), np.zeros((D, D)), C.c_double()
+        self._check(lib().gfnx_eb_coupling(self.h, _p(jm), _p(jt), D * D, C.byref(z)))
+        return jm, jt, z.value
+
+    def eb_dataset(self, n: int):
+        D = self.env.is_side * self.env.is_side
+        out = np.zeros((n, D), dtype=np.int8)
+        self._check(lib().gfnx_eb_dataset(self.h, _p(out), out.size))
+        return out
 
     def rollout_from_actions(self, actions):
         """rollout_from_actions (env_core.hpp:166-229): actions [local_batch, T], -1 padded."""

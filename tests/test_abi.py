@@ -5,6 +5,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 from paper_2511_16592_b200 import abi, engine
@@ -33,13 +34,14 @@ def test_struct_layouts_match_header(tmp_path):
     c.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "gfnx.h"\nint main(){'
                  'printf("%zu %zu %zu %zu %zu %zu %zu\\n", sizeof(gfnx_env_desc), sizeof(gfnx_train_desc),'
                  'sizeof(gfnx_schedule), sizeof(gfnx_env_shape), sizeof(gfnx_host_batch),'
-                 'offsetof(gfnx_train_desc, explore), offsetof(gfnx_env_desc, dag_data_seed));return 0;}')
+                 'offsetof(gfnx_train_desc, explore), offsetof(gfnx_env_desc, dag_data_seed));'
+                 'printf("%zu %zu\\n", sizeof(gfnx_eb_desc), offsetof(gfnx_eb_desc, coupling_lr_end));return 0;}')
     exe = tmp_path / "sz"
     subprocess.run(["gcc", "-I" + os.path.dirname(HEADER), str(c), "-o", str(exe)], check=True)
     got = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True).stdout.split()]
     want = [C.sizeof(abi.EnvDesc), C.sizeof(abi.TrainDesc), C.sizeof(abi.Schedule),
             C.sizeof(abi.EnvShape), C.sizeof(abi.HostBatch), abi.TrainDesc.explore.offset,
-            abi.EnvDesc.dag_data_seed.offset]
+            abi.EnvDesc.dag_data_seed.offset, C.sizeof(abi.EbDesc), abi.EbDesc.coupling_lr_end.offset]
     assert got == want
 
 
@@ -68,3 +70,21 @@ def test_config_errors_without_gpu():
         engine.env_shape(abi.env_desc(abi.HYPERGRID, hg_r0=0.0))
     with pytest.raises(engine.config_error, match="k must divide"):
         engine.env_shape(abi.env_desc(abi.BITSEQ, bs_n_bits=12, bs_k=5))
+
+
+def test_eb_defaults_and_host_gibbs_sampler_match_reference():
+    """run_eb_gfn's defaults (train.cpp:899-913) and the host Gibbs data sampler used by
+    gfnx_eb_init (gibbs_data_sampler ising.cpp:185-220, key fold_in(make_key(seed), 0x919B))
+    against the compiled reference: identical spins, with and without parallel tempering."""
+    d = engine.eb_desc()
+    assert (d.data_samples, d.k, d.gibbs_burn_in, d.gibbs_thinning, d.gibbs_chains, d.data_batch) == \
+        (2000, 0, 2000, 10, 1, 0)
+    assert (d.gibbs_hottest_beta, d.alpha, d.coupling_lr, d.coupling_lr_end) == (0.2, 0.5, 0.05, 0.05)
+    from oracle import oracle as O
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    for side, sigma, seed, chains in ((3, 0.2, 5, 1), (4, 0.35, 1, 3)):
+        d = engine.eb_desc(gibbs_burn_in=200, gibbs_thinning=3, gibbs_chains=chains)
+        dev = engine.ising_gibbs_data(side, sigma, seed, 150, d)
+        ref = O.ref_gibbs_data(side, sigma, seed, 150, burn_in=200, thinning=3, chains=chains)
+        assert np.array_equal(dev, ref), (side, chains)

@@ -158,3 +158,18 @@ def test_mc_terminal_logprob_all_envs(name, check, tol):
     print(f"{name} check={check}: max |device - reference| = {err:.2e}")
     assert np.all(np.isfinite(dev)) and err <= tol * max(1.0, np.max(np.abs(want))), (dev, want)
     tr.close()
+
+
+def test_pearson_bitseq_k8_bf16_vs_check_mode():
+    """The device `pearson` metric on the bf16 k = 8 lockstep path (n = 48: 6 slots, 2880 test
+    strings x 10 walks) against the fp64 check mode on the same parameters."""
+    e, t = _cfg("bitseq_k8", False)
+    e2, t2 = _cfg("bitseq_k8", True)
+    fast, chk = engine.Trainer(e, t), engine.Trainer(e2, t2)
+    fast.run(0, 30)
+    chk.set_params(*fast.params())
+    pf, pc = fast.pearson(30, 10), chk.pearson(30, 10)
+    print(f"pearson bf16 {pf:.5f} fp64 {pc:.5f}")
+    assert -1.0 <= pf <= 1.0 and abs(pf - pc) <= 2e-2, (pf, pc)
+    fast.close()
+    chk.close()
