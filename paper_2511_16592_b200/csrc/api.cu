@@ -449,8 +449,10 @@ gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     P.is_J = c.d_is_J;
     P.dag_cache = c.d_dag_cache;
     P.neglog = c.d_neglog;
-    // batch
-    const int T = P.T, Bl = c.Bl;
+    // batch (the lockstep paths lay out whole 128-trajectory tiles: pad rows past Bl)
+    const bool lockstep_env = env->kind == GFNX_ENV_BITSEQ || env->kind == GFNX_ENV_ISING;
+    c.Bcap = (lockstep_env && train->precision != GFNX_PREC_FP64_CHECK) ? (c.Bl + 127) / 128 * 128 : c.Bl;
+    const int T = P.T, Bl = c.Bcap;
     DeviceBatch& bt = c.batch;
     cuda_check(cudaMalloc(&bt.lengths, sizeof(int32_t) * Bl), "batch");
     cuda_check(cudaMalloc(&bt.actions, sizeof(int16_t) * (size_t)Bl * T), "batch");

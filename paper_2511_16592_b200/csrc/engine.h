@@ -134,6 +134,7 @@ struct Ctx {
   MlpLayout L{};
   int device = 0, rank = 0, world = 1;
   int B = 0, Bl = 0, b0 = 0;  // global batch, local slice [b0, b0+Bl)
+  int Bcap = 0;               // trajectory capacity of the batch arrays (>= Bl: lockstep pads to 128)
   cudaStream_t stream = nullptr;
   void* nccl = nullptr;  // ncclComm_t (one process per GPU)
   Group* group = nullptr;  // or an in-process group (one thread per rank)

@@ -334,7 +334,7 @@ struct SampleArgs {
   EnvParams P;
   Key key;  // fold_in(rollout key, t)
   double eps;
-  int b0, Bl, t, T, Ap, G;
+  int b0, Bl, t, T, Ap, G;  // Bl: padded row stride (a multiple of 128)
   const __nv_bfloat16* logits;
   const float2* stats;
   uint32_t* cur;
@@ -342,7 +342,8 @@ struct SampleArgs {
   int32_t* last_act;
   float* rowbuf;
   DeviceBatch batch;
-  const int16_t* forced;  // [Bl * T] teacher-forced actions (rows starting with -1 are sampled) or null
+  const int16_t* forced;  // [nreal * T] teacher-forced actions (rows starting with -1 are sampled) or null
+  int nreal;              // real trajectories (rows >= nreal pad the batch to a multiple of 128)
 };
 
 GFNX_DEV double warp_sum_d(double x) {
@@ -444,7 +445,7 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
   if (lane == 0) {
     const size_t bt = (size_t)b * a.T + a.t;
     const size_t r = (size_t)a.t * a.Bl + b;
-    if (a.forced && a.forced[(size_t)b * a.T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
+    if (a.forced && b < a.nreal && a.forced[(size_t)b * a.T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
       act = a.forced[bt];
       typename E::State s;
       E::unpack(P, w, s);
@@ -530,7 +531,8 @@ __global__ void k_ls_reset(int n, uint32_t* cur) {
 
 struct LossArgs {
   DeviceBatch batch;
-  int Bl, T;
+  int Bl, T;  // Bl: padded row stride; trajectories >= nreal are pad rows (coefficient 0)
+  int nreal;
   double B_global;
   const double* neglog;
   const float* rowbuf;
@@ -542,7 +544,9 @@ struct LossArgs {
 __global__ void k_ls_loss(LossArgs a) {  // tb_loss objectives.cpp:120-142
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   double loss = 0.0, dlogz = 0.0;
-  if (b < a.Bl) {
+  if (b >= a.nreal && b < a.Bl)
+    for (int t = 0; t < a.T; ++t) a.coef[(size_t)t * a.Bl + b] = 0.f;
+  if (b < a.nreal) {
     const double w = 1.0 / a.B_global;
     double cum = 0.0;
     for (int t = 0; t < a.T; ++t) {
@@ -1016,7 +1020,8 @@ struct PersistArgs {
   // Ising: layer 1 as an MMA over the assigned-spin one-hot (feature 2 site + up) against
   // W1[3s + u] - W1[3s + 2] (wimg[0]), bias = h1init: no per-row fp32 state between steps
   int l1_mma;
-  const int16_t* forced;  // [Bl * T] teacher-forced actions (rows starting with -1 are sampled) or null
+  const int16_t* forced;  // [nreal * T] teacher-forced actions (rows starting with -1 are sampled) or null
+  int nreal;              // real trajectories (the rest pad the batch to a multiple of 128)
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
@@ -1419,7 +1424,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       // rounding fallback: the last legal column (rng.cpp:97-99)
       int act = p0 >= 0 ? p0 : (p1 >= 0 ? p1 : (xlast[row][1] >= 0 ? xlast[row][1] : xlast[row][0]));
       bool forced_bad = false;
-      if (a.forced && a.forced[(size_t)b * T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
+      if (a.forced && b < a.nreal && a.forced[(size_t)b * T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
         act = a.forced[(size_t)b * T + t];
         typename E::State fs;
         E::unpack(P, w, fs);
@@ -1513,7 +1518,7 @@ __global__ void k_ls_ising_l1img(const __nv_bfloat16* w1, int D, uint8_t* img) {
 template <class E>
 void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
   LsState& f = LS(c);
-  const int T = f.T, Bl = c.Bl;
+  const int T = f.T, Bl = f.Bl;  // padded batch (c.Bl real trajectories first)
   cudaMemsetAsync(c.batch.actions, 0xFF, sizeof(int16_t) * (size_t)Bl * T, c.stream);
   {
     ProfScope ps(c, "k_ls_init");
@@ -1562,6 +1567,7 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
     pa.batch = c.batch;
     pa.phase = c.phase;
     pa.forced = forced;
+    pa.nreal = c.Bl;
     const int smem = kH * kH * 2 + 1024;
     set_smem_once(k_ls_persist<E>, smem);
     ProfScope ps(c, "k_ls_persist");
@@ -1595,7 +1601,7 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
     typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl};
     launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
     SampleArgs sa{c.P, fold_in(key, (uint64_t)t), eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst,
-                  f.last_act, f.rowbuf, c.batch, forced};
+                  f.last_act, f.rowbuf, c.batch, forced, c.Bl};
     ProfScope ps(c, "k_ls_sample");
     k_ls_sample<E><<<(Bl + 8 * kSampleRows - 1) / (8 * kSampleRows), 256, 0, c.stream>>>(sa);
     c.launches++;
@@ -1605,9 +1611,9 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
 template <class E>
 void train_impl(Ctx& c) {
   LsState& f = LS(c);
-  const int Bl = c.Bl, NL = f.NL;
+  const int Bl = f.Bl, NL = f.NL;
   {
-    LossArgs la{c.batch, Bl, f.T, (double)c.B, c.d_neglog, f.rowbuf, f.coef, f.lpart, c.d_scalars};
+    LossArgs la{c.batch, Bl, f.T, c.Bl, (double)c.B, c.d_neglog, f.rowbuf, f.coef, f.lpart, c.d_scalars};
     ProfScope ps(c, "k_ls_loss");
     k_ls_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
     k_ls_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars, c.batch.counters + 3);
@@ -1708,7 +1714,6 @@ bool ls_supported(const Ctx& c, std::string* why) {
   }
   if (c.P.SW > 16) return no("fast path supports <= 16 packed state words");
   if ((c.P.A + 255) / 256 * 2 > 32) return no("fast path supports <= 4096 actions");
-  if (c.Bl % kTile != 0) return no("bitseq/Ising fast path needs a per-rank batch that is a multiple of 128");
   return true;
 }
 
@@ -1726,9 +1731,9 @@ void ls_init(Ctx& c) {
   f->OB = (f->O + 255) / 256;
   f->T = c.P.T;
   f->SW = c.P.SW;
-  f->Bl = c.Bl;
-  f->R = c.Bl * f->T;
-  f->tilesB = c.Bl / kTile;
+  f->Bl = (c.Bl + kTile - 1) / kTile * kTile;  // lockstep rows pad the batch to whole 128-row tiles
+  f->R = f->Bl * f->T;
+  f->tilesB = f->Bl / kTile;
   f->tilesR = f->R / kTile;
   f->t_dense = 0;
   f->t_head = f->NL - 1;
@@ -1753,7 +1758,7 @@ void ls_init(Ctx& c) {
     }
     f->first[f->ntasks] = used;
   }
-  f->loss_blocks = (c.Bl + 255) / 256;
+  f->loss_blocks = (f->Bl + 255) / 256;
   f->bw = f->NL * kH + f->Ap;
   f->cgroups = std::min(256, std::max(1, f->tilesR / 16));
   const size_t img = (size_t)f->tilesR * kTile * kH * 2;
@@ -1770,17 +1775,17 @@ void ls_init(Ctx& c) {
   alloc(&f->wfd, sizeof(__nv_bfloat16) * (size_t)f->Ap * kH);
   alloc(&f->bfp, sizeof(float) * f->Ap);
   alloc(&f->h1init, sizeof(float) * kH);
-  alloc(&f->preact, sizeof(float) * (size_t)c.Bl * kH);
-  alloc(&f->cur, sizeof(uint32_t) * (size_t)c.Bl * f->SW);
+  alloc(&f->preact, sizeof(float) * (size_t)f->Bl * kH);
+  alloc(&f->cur, sizeof(uint32_t) * (size_t)f->Bl * f->SW);
   alloc(&f->stst, sizeof(uint32_t) * (size_t)f->R * f->SW);
-  alloc(&f->last_act, sizeof(int32_t) * c.Bl);
+  alloc(&f->last_act, sizeof(int32_t) * f->Bl);
   for (int l = 0; l < f->NL; ++l) {
     alloc(&f->h[l], img);
     alloc(&f->dz[l], img);
     alloc(&f->mask[l], (size_t)f->R * (kH / 8));
   }
-  alloc(&f->logits, sizeof(__nv_bfloat16) * (size_t)c.Bl * f->Ap);
-  alloc(&f->stats, sizeof(float2) * (size_t)c.Bl * f->G);
+  alloc(&f->logits, sizeof(__nv_bfloat16) * (size_t)f->Bl * f->Ap);
+  alloc(&f->stats, sizeof(float2) * (size_t)f->Bl * f->G);
   alloc(&f->dlog, (size_t)f->tilesR * f->KBA * (kTile * 128));
   alloc(&f->rowbuf, sizeof(float) * 2 * (size_t)f->R);
   alloc(&f->coef, sizeof(float) * (size_t)f->R);
@@ -1831,18 +1836,18 @@ void ls_sync_weights(Ctx& c) {
 }
 
 namespace {
-// rows are step-major (r = t * Bl + b); rowbuf[2 r] = log pi(a | s)
-__global__ void k_ls_row_logpf(const float* __restrict__ rowbuf, int Bl, int T, double* out) {
+// rows are step-major (r = t * stride + b); rowbuf[2 r] = log pi(a | s)
+__global__ void k_ls_row_logpf(const float* __restrict__ rowbuf, int Bl, int stride, int T, double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= Bl * T) return;
   const int b = i / T, t = i % T;
-  out[i] = (double)rowbuf[2 * ((size_t)t * Bl + b)];
+  out[i] = (double)rowbuf[2 * ((size_t)t * stride + b)];
 }
 }  // namespace
 
 void ls_row_logpf(Ctx& c, double* out) {
   const int n = c.Bl * LS(c).T;
-  k_ls_row_logpf<<<(n + 255) / 256, 256, 0, c.stream>>>(LS(c).rowbuf, c.Bl, LS(c).T, out);
+  k_ls_row_logpf<<<(n + 255) / 256, 256, 0, c.stream>>>(LS(c).rowbuf, c.Bl, LS(c).Bl, LS(c).T, out);
   c.launches++;
 }
 
