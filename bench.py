@@ -44,6 +44,9 @@ SECONDARY = {
     "ising_tb_b32768": dict(batch=32768, desc="Ising 10x10 TB, MLP 4x256"),
     "hypergrid_tb_b16": dict(batch=16, desc="hypergrid 20^4 TB, B=16, MLP 2x256"),
     "dag_mdb_b8192": dict(batch=8192, desc="DAG d=5 BGe MDB, MLP 2x128"),
+    # the headline workload in deterministic mode (static per-CTA ranges, bit-identical reruns)
+    "hypergrid_db_b65536_det": dict(batch=65536, config="hypergrid_db_b65536", det=1,
+                                    desc="hypergrid 20^4 DB, B=65536, MLP 2x256, deterministic=1"),
 }
 
 
@@ -53,8 +56,9 @@ def secondary_runs(names, steps, warmup, local):
     for name in names:
         spec = SECONDARY[name]
         try:
-            e, t = abi.config(name, batch=spec["batch"])
+            e, t = abi.config(spec.get("config", name), batch=spec["batch"])
             t.iterations = 1_000_000
+            t.deterministic = spec.get("det", 0)
             tr = engine.Trainer(e, t, device=local)
             tr.run(0, warmup)
             tr.synchronize()
@@ -346,7 +350,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-steady", action="store_true", help="skip the converged-checkpoint leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the reward-kernel B sweep")
-    ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192",
+    ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,"
+                                           "dag_mdb_b8192,hypergrid_db_b65536_det",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()

@@ -118,7 +118,11 @@ typedef struct gfnx_train_desc {
   int64_t iterations;                          /* only used to resolve schedule horizons */
   uint64_t seed;
   int32_t precision; /* gfnx_precision */
-  int32_t pad_;
+  /* bf16 hypergrid / DAG path: 1 = run-to-run bit-identical results (static per-CTA
+   * trajectory ranges and row regions instead of work stealing, as the reference's
+   * byte-identical runs require, test_config_train.cpp:80-122); 0 = dynamic (faster).
+   * fp64 check mode and the lockstep paths are always deterministic. */
+  int32_t deterministic;
 } gfnx_train_desc;
 
 /* Per-environment defaults of the reference drivers (train.cpp:43-62, 105-137, 353-657). */

@@ -55,7 +55,7 @@ class TrainDesc(C.Structure):
         ("weight_decay", C.c_double), ("z_lr", C.c_double),
         ("lr", Schedule), ("explore", Schedule),
         ("iterations", C.c_int64), ("seed", C.c_uint64),
-        ("precision", C.c_int32), ("pad_", C.c_int32),
+        ("precision", C.c_int32), ("deterministic", C.c_int32),
     ]
 
 

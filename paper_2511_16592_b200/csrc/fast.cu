@@ -61,6 +61,9 @@ struct FastState {
   int32_t* frow_bt = nullptr;         // [max_tiles*128] row slot -> b*T + t (-1 = empty)
   int32_t* bt_row = nullptr;          // [Bl*T] b*T + t -> row slot
   int32_t* tilectr = nullptr;         // number of 128-row tiles of row slots
+  int32_t* det_used = nullptr;        // deterministic mode: filled tiles per rollout CTA
+  int32_t* tile_list = nullptr;       // deterministic mode: training tile -> emission tile
+  int det_per = 0, det_mt = 0, det_grid = 0;
   float* logits = nullptr;            // [slots][NH] rollout head outputs (fused forward)
   bool fused = false;                 // row slots hold the rollout's forward for the current weights
   int rs = 0;                         // rowbuf stride (floats)
@@ -134,11 +137,34 @@ template <class Env, int NH>
 __global__ void k_row_stats(EnvParams P, const uint32_t* __restrict__ stst, const int16_t* __restrict__ actions,
                             const int32_t* __restrict__ frow_bt, const int32_t* __restrict__ tilectr,
                             const float* __restrict__ logits, float* __restrict__ rowbuf, int rs, int flow,
-                            int32_t* err) {
+                            int32_t* err, const int32_t* __restrict__ tile_list) {
   const int n = *tilectr * kTile;
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x)
-    row_stats_one<Env, NH>(P, stst, actions, frow_bt, logits, rowbuf, rs, flow, err, r);
+    row_stats_one<Env, NH>(P, stst, actions, frow_bt, logits, rowbuf, rs, flow, err,
+                           tile_list ? tile_list[r >> 7] * kTile + (r & (kTile - 1)) : r);
 }
+
+// deterministic mode: the filled tiles of every rollout CTA's region, in CTA order, as the
+// training pass's tile list (the partially filled last tile's spare rows are empty slots)
+__global__ void k_det_tiles(const int32_t* __restrict__ used, int nctas, int mt, int32_t* __restrict__ list,
+                            int32_t* tilectr) {
+  __shared__ int off[1025];
+  if (threadIdx.x == 0) {
+    int o = 0;
+    for (int k = 0; k < nctas; ++k) {
+      off[k] = o;
+      o += used[k];
+    }
+    off[nctas] = o;
+    *tilectr = o;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nctas; k += blockDim.x)
+    for (int i = 0; i < used[k]; ++i) list[off[k] + i] = k * mt + i;
+}
+
+// logical training tile i -> emission tile (identity unless the deterministic list is set)
+GFNX_DEV int phys_tile(const int32_t* list, int i) { return list ? list[i] : i; }
 
 __global__ void k_rollout_reset(int32_t* tilectr, int32_t* counters, int32_t* work) {
   if (threadIdx.x == 0) {
@@ -336,6 +362,10 @@ struct RolloutArgs {
   int rs, flow;
   int32_t *frow_bt, *bt_row, *tilectr;
   float* logits;  // [slot][NH] head outputs (logits, flow at column A), bias included
+  // deterministic mode: CTA k simulates trajectories [k per, (k+1) per) and emits into its
+  // own tiles [k mt, (k+1) mt); det_used[k] = tiles it filled (k_det_tiles lists them)
+  int det, per, mt;
+  int32_t* det_used;
 };
 
 // H = 256 stages the A operand (h1, then h2) in two 128-column halves through one 32 KB
@@ -375,6 +405,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
   __shared__ int s_cur0, s_next;  // emission tiles: first claimed, next claimed
+  __shared__ int s_pq[4];          // deterministic refills: finished rows per row quarter
   __shared__ int s_nterm;          // trajectories finished by this CTA
   __shared__ uint4 row_m1[kTile][H / 128], row_m2[kTile][H / 128];  // ReLU masks of the round
 
@@ -388,7 +419,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
     smax = 0;
-    const int t0 = atomicAdd(a.tilectr, 2);
+    const int t0 = a.det ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
+    for (int q = 0; q < 4; ++q) s_pq[q] = 0;
     s_cur0 = t0;
     s_next = t0 + 1;
     s_nterm = 0;
@@ -397,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   // emission cursor (uniform over the CTA): rows of this CTA fill tile `cur` from `fill`,
   // overflowing into the pre-claimed tile s_next
   int cur = s_cur0, fill = 0, emitted = 0;
+  int nclaim = s_cur0 + 2;  // deterministic mode: next tile of this CTA's region
   if (tid == 0) {
     mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
@@ -477,9 +510,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   int b = -1, tstep = 0;
   bool active = false, bad = false, pending = false;
   int bnext = 0;
+  // deterministic mode: a static trajectory range [beg, bend) per CTA, slot row r starts
+  // with beg + r, finished rows refill in row order (ballot ranks), no work stealing
+  const int beg = a.det ? (int)blockIdx.x * a.per : 0;
+  const int bend = a.det ? min(a.Bl, beg + a.per) : a.Bl;
+  int dbase = beg + kTile;
+  unsigned pm_prev = 0u;
   if (half == 0) {
-    b = atomicAdd(a.work, 1);
-    active = b < a.Bl;
+    b = a.det ? beg + row : atomicAdd(a.work, 1);
+    active = b < bend;
     row_init[row] = 1;
     row_nd[row] = 0;
     row_b[row] = b;
@@ -576,9 +615,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     tmem_wait_st();
+    if (a.det) {  // refill ranks: finished rows of the last step in row order
+      const int tot = s_pq[0] + s_pq[1] + s_pq[2] + s_pq[3];
+      if (pending) {
+        int rank = __popc(pm_prev & ((1u << lane) - 1u));
+        for (int q = 0; q < quarter; ++q) rank += s_pq[q];
+        bnext = dbase + rank;
+      }
+      dbase += tot;
+    }
     if (pending) {  // the refill claim issued at the last termination lands here
       b = bnext;
-      active = b < a.Bl;
+      active = b < bend;
       row_b[row] = active ? b : -1;
       pending = false;
     }
@@ -615,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
       // the next tile is claimed now; s_next is rewritten in this round's sample phase,
       // after every thread has read it above
-      if (crossed && tid == kThreads - 1) claim = atomicAdd(a.tilectr, 1);
+      if (crossed && tid == kThreads - 1) claim = a.det ? nclaim++ : atomicAdd(a.tilectr, 1);
     }
     // copy the 64 staged columns [half*64, half*64+64) of the A tile (logical columns
     // col0 + ...) of this warp's 32 rows into their emission tile images + ReLU masks,
@@ -722,7 +770,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
-          bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          if (!a.det) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
           atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
@@ -751,6 +799,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
+    if (a.det) {  // this step's finished rows, ranked at the next refill
+      pm_prev = __ballot_sync(0xffffffffu, pending);
+      if (lane == 0 && half == 0) s_pq[quarter] = __popc(pm_prev);
+    }
     mark(5);
   }
   if (a.phase && tid == 0)
@@ -776,6 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     }
   }
   __syncthreads();
+  if (tid == 0 && a.det) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
   if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<2 * H>(tmem);
 }
@@ -821,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   __shared__ unsigned long long smax;
   __shared__ double inv_legal[NH + 1];
   __shared__ int s_cur0, s_next;
+  __shared__ int s_pq[4];  // deterministic refills: finished rows per row quarter
   __shared__ int s_nterm;
 
   const EnvParams& P = a.P;
@@ -833,13 +887,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     mbar_init(&mbar, 1);
     fence_mbar_init();
     smax = 0;
-    const int t0 = atomicAdd(a.tilectr, 2);
+    const int t0 = a.det ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
+    for (int q = 0; q < 4; ++q) s_pq[q] = 0;
     s_cur0 = t0;
     s_next = t0 + 1;
     s_nterm = 0;
   }
   __syncthreads();
   int cur = s_cur0, fill = 0, emitted = 0;
+  int nclaim = s_cur0 + 2;  // deterministic mode: next tile of this CTA's region
   if (tid == 0) {
     mbar_arrive_expect_tx(&mbar, H * H * 2 + NH * H * 2);
     bulk_g2s_big(w2img, a.W.w2_fwd, H * H * 2, &mbar);
@@ -905,9 +961,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   int b = -1, tstep = 0;
   bool active = false, pending = false;
   int bnext = 0;
+  // deterministic mode: a static trajectory range [beg, bend) per CTA, slot row r starts
+  // with beg + r, finished rows refill in row order (ballot ranks), no work stealing
+  const int beg = a.det ? (int)blockIdx.x * a.per : 0;
+  const int bend = a.det ? min(a.Bl, beg + a.per) : a.Bl;
+  int dbase = beg + kTile;
+  unsigned pm_prev = 0u;
   if (half == 0) {
-    b = atomicAdd(a.work, 1);
-    active = b < a.Bl;
+    b = a.det ? beg + row : atomicAdd(a.work, 1);
+    active = b < bend;
     row_b[row] = b;
     row_t[row] = 0;
     set_features(s);
@@ -998,9 +1060,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
                                  __uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1]);
       tmem_st16(lane_base + TA + (col >> 1), pk);
     }
+    if (a.det) {  // refill ranks: finished rows of the last step in row order
+      const int tot = s_pq[0] + s_pq[1] + s_pq[2] + s_pq[3];
+      if (pending) {
+        int rank = __popc(pm_prev & ((1u << lane) - 1u));
+        for (int q = 0; q < quarter; ++q) rank += s_pq[q];
+        bnext = dbase + rank;
+      }
+      dbase += tot;
+    }
     if (pending) {  // the refill claim issued at the last termination lands here
       b = bnext;
-      active = b < a.Bl;
+      active = b < bend;
       row_b[row] = active ? b : -1;
       pending = false;
     }
@@ -1040,7 +1111,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         cur = nxt;
         crossed = true;
       }
-      if (crossed && tid == kThreads - 1) claim = atomicAdd(a.tilectr, 1);
+      if (crossed && tid == kThreads - 1) claim = a.det ? nclaim++ : atomicAdd(a.tilectr, 1);
     }
     mark(1);
     if (half == 1) {  // the row's uniform while the MMA runs (rng.cpp:64-66)
@@ -1111,7 +1182,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
-          bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          if (!a.det) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
           atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
@@ -1141,6 +1212,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     h2_pend = my_valid;
     h2_gs = gslot;
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
+    if (a.det) {  // this step's finished rows, ranked at the next refill
+      pm_prev = __ballot_sync(0xffffffffu, pending);
+      if (lane == 0 && half == 0) s_pq[quarter] = __popc(pm_prev);
+    }
     mark(5);
   }
   emit_block(a.h2, a.mask2, TA2, 2 + half, h2_pend, h2_gs);  // the last step's deferred h2 blocks
@@ -1168,6 +1243,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0 && a.det) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
   if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
@@ -1183,6 +1259,7 @@ struct TrainArgs {
   const uint32_t* stst;
   const int32_t* frow_bt;   // row slot -> b * T + t, -1 = empty slot
   const int32_t* tilectr;   // number of 128-row tiles of row slots
+  const int32_t* tile_list; // deterministic mode: training tile -> emission tile, or null
   __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
   uint32_t *mask1, *mask2;  // ReLU masks of h1 / h2, [rows][H/32]
   float* rowbuf;
@@ -1751,11 +1828,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       float ga, gs, gf;
       float pr[NH];
     };
-    auto slot_of = [&](int tile) { const int r = tile * kTile + row; return tile < tiles && r < R ? a.frow_bt[r] : -1; };
+    auto slot_of = [&](int tile) { return tile < tiles ? a.frow_bt[phys_tile(a.tile_list, tile) * kTile + row] : -1; };
     // vector loads only: these rows are strided, so every load instruction of a warp touches
     // 32 lines and the load/store unit, not the latency, bounds the prefetch
     auto load_row = [&](int tile, int rbt, RowIn& x) {
-      const int r = tile * kTile + row;
+      const int r = (tile < tiles ? phys_tile(a.tile_list, tile) : 0) * kTile + row;
       const bool v = rbt >= 0, v0 = v && half == 0;
       const size_t mo = (size_t)r * (H / 32) + half * (HC / 32);
       if constexpr (HC / 32 == 4) {
@@ -1801,7 +1878,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       }
     };
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int r = tile * kTile + row;
+      const int pt = phys_tile(a.tile_list, tile);  // emission tile of this training tile
       const int rbt = rbt_cur;
       const bool valid = rbt >= 0;
       const RowIn cx = nx;
@@ -1857,7 +1934,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       pmark(0);
       if (tid == 0) {  // dh2 = dhead Wf^T (+ dflow wfl^T): 128 x H x NH on the tensor cores
         tc_fence_after();
-        bulk_s2g(a.dhead + (size_t)tile * kTile * 64, htile, kTile * 64 * 2);
+        bulk_s2g(a.dhead + (size_t)pt * kTile * 64, htile, kTile * 64 * 2);
         bulk_commit();
         mma_k_sw128_none<H, NH>(tmem, htile, whd);
         umma_commit(&mbar);
@@ -1887,7 +1964,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       pmark(2);
       if (tid == 0) {
         tc_fence_after();
-        bulk_s2g(a.dz2 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+        bulk_s2g(a.dz2 + (size_t)pt * kTile * H, atile, kTile * H * 2);
         bulk_commit();
         mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
         umma_commit(&mbar);
@@ -1955,7 +2032,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       fence_proxy_async();
       __syncthreads();
       if (tid == 0) {
-        bulk_s2g(a.dz1 + (size_t)tile * kTile * H, atile, kTile * H * 2);
+        bulk_s2g(a.dz1 + (size_t)pt * kTile * H, atile, kTile * H * 2);
         bulk_commit();
       }
       pmark(4);
@@ -2038,7 +2115,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   auto X = [&](int st) { return ring + st * kWgStage; };
   auto Y = [&](int st) { return ring + st * kWgStage + 32768; };
   auto src = [&](const void* img, int u, int blk, int width) {  // 64-row unit u, 64-feature block blk
-    const int tile = t0 + (u >> 1), hh = u & 1;
+    const int tile = phys_tile(a.tile_list, t0 + (u >> 1)), hh = u & 1;
     return reinterpret_cast<const uint8_t*>(img) + (size_t)tile * kTile * width * 2 + blk * (kTile * 128) +
            hh * (kWgRows * 128);
   };
@@ -2109,8 +2186,8 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   // and the packed state one unit ahead, so building a unit waits on no global load.
   auto ld_bt = [&](int u) {
     if (u >= nu) return -1;
-    const int r = (t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
-    return r < R ? a.frow_bt[r] : -1;
+    const int r = phys_tile(a.tile_list, t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
+    return a.frow_bt[r];
   };
   auto ld_sw = [&](int bt, uint32_t (&w)[kMaxSWFwd]) {
 #pragma unroll
@@ -2388,11 +2465,18 @@ struct Kernels {
     a.bt_row = f.bt_row;
     a.tilectr = f.tilectr;
     a.logits = f.logits;
+    a.det = c.train.deterministic ? 1 : 0;
     // counters only: the per-step arrays beyond each trajectory's length are never read on
     // the device (gfnx_export_batch pads them from the lengths)
     k_rollout_reset<<<1, 32, 0, c.stream>>>(f.tilectr, c.batch.counters, f.work);
     c.launches++;
     const int grid = std::min(f.num_sms, (c.Bl + kTile - 1) / kTile);
+    if (a.det) {  // static ranges and regions (fast_init sized the slots for grid * mt tiles)
+      a.per = f.det_per;
+      a.mt = f.det_mt;
+      a.det_used = f.det_used;
+      if (grid != f.det_grid) raise_error(GFNX_ERR_CONFIG, "deterministic rollout: grid mismatch");
+    }
     const int fixed = rollout_smem_fixed<H, NH>();
     const int w1b = c.P.O * H * 2;
     cudaFuncAttributes fa{};
@@ -2414,6 +2498,7 @@ struct Kernels {
         }
         c.launches++;
         f.fused = true;
+        det_list(c, grid);
         return;
       }
     }
@@ -2426,6 +2511,13 @@ struct Kernels {
     }
     c.launches++;
     f.fused = true;
+    det_list(c, grid);
+  }
+  static void det_list(Ctx& c, int grid) {
+    FastState& f = FS(c);
+    if (!c.train.deterministic) return;
+    k_det_tiles<<<1, 256, 0, c.stream>>>(f.det_used, grid, f.det_mt, f.tile_list, f.tilectr);
+    c.launches++;
   }
   // policy forward (masked softmax record) over `n` explicit packed states (eval buffers)
   static void eval_forward(Ctx& c, const uint32_t* stst, const int32_t* rows, const int32_t* tiles,
@@ -2474,6 +2566,7 @@ struct Kernels {
     ta.stst = f.stst;
     ta.frow_bt = f.frow_bt;
     ta.tilectr = f.tilectr;
+    ta.tile_list = (f.fused && c.train.deterministic) ? f.tile_list : nullptr;
     ta.h1 = f.h1;
     ta.h2 = f.h2;
     ta.dz1 = f.dz1;
@@ -2521,7 +2614,8 @@ struct Kernels {
       const int nslots = (int)(f.max_tiles * kTile);
       k_row_stats<Env, NH><<<std::min((nslots + 255) / 256, f.num_sms * 8), 256, 0, c.stream>>>(
           c.P, f.stst, c.batch.actions, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
-          c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3);
+          c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3,
+          ta.tile_list);
       c.launches++;
     }
     LossArgs la{};
@@ -2930,6 +3024,14 @@ void fast_init(Ctx& c) {
   f->max_rows = (int64_t)c.Bl * T;
   // + 2 tiles per rollout CTA: partially filled / pre-claimed emission tiles
   f->max_tiles = (f->max_rows + kTile - 1) / kTile + 2 * f->num_sms;
+  if (c.train.deterministic) {  // static per-CTA regions: per trajectories of <= T rows each
+    f->det_grid = std::min(f->num_sms, (c.Bl + kTile - 1) / kTile);
+    f->det_per = (c.Bl + f->det_grid - 1) / f->det_grid;
+    f->det_mt = (int)(((int64_t)f->det_per * T + kTile - 1) / kTile) + 2;
+    f->max_tiles = std::max<int64_t>(f->max_tiles, (int64_t)f->det_grid * f->det_mt);
+    cuda_check(cudaMalloc(&f->det_used, sizeof(int32_t) * f->det_grid), "fast det");
+    cuda_check(cudaMalloc(&f->tile_list, sizeof(int32_t) * f->max_tiles), "fast det");
+  }
   const int64_t slots = f->max_tiles * kTile;
   f->rs = (f->A + 3 + 3) & ~3;  // probs[A], lpa, lps, flow, padded to 16 bytes
   f->loss_blocks = (c.Bl + 255) / 256;
@@ -2980,7 +3082,7 @@ void fast_free(Ctx& c) {
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
                   f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work,
-                  f->frow_bt, f->bt_row, f->tilectr, f->logits};
+                  f->frow_bt, f->bt_row, f->tilectr, f->logits, f->det_used, f->tile_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete f;

@@ -358,6 +358,7 @@ std::string validate_train(const gfnx_train_desc& t, const gfnx_env_shape& s) {
   for (int l = 0; l < t.num_hidden; ++l)
     if (t.hidden[l] < 1 || t.hidden[l] > 512) return "mlp_init: hidden width must lie in [1, 512]";
   if (t.batch_size < 1) return "forward_rollout: num_envs must be >= 1";
+  if (t.deterministic != 0 && t.deterministic != 1) return "deterministic must be 0 or 1";
   if (t.precision != GFNX_PREC_BF16 && t.precision != GFNX_PREC_FP64_CHECK)
     return "unknown precision";
   return "";
