@@ -134,6 +134,9 @@ struct LsState {
   int num_sms = 0;
   int NL = 2, A = 0, Ap = 0, NT = 0, G = 0, O = 0, OB = 0, T = 0, KBA = 0;
   int Bl = 0, R = 0, tilesB = 0, tilesR = 0, SW = 0;
+  int flow = 0;                              // DB / SubTB: log-flow head = head column A
+  float* flowv = nullptr;                    // [R] log F(s) of every row (fp32, before rounding)
+  float* gflow = nullptr;                    // [R] dL / dlog F(s)
   __nv_bfloat16* w1 = nullptr;               // [O][H] row-major
   __nv_bfloat16* wfw[kMaxNL] = {};           // layer l (1..NL-1): [H out][H in] image
   __nv_bfloat16* wdg[kMaxNL] = {};           // layer l: [H in][H out] image
@@ -163,6 +166,7 @@ struct LsState {
   int first[kMaxTasks + 1] = {};             // wgrad CTAs of task k: [first[k], first[k+1])
   int t_dense = 0, t_head = 0, t_w1 = 0;     // first task of each kind
   double* lpart = nullptr;
+  double* lampow = nullptr;                  // SubTB: pow(lambda, k), k = 0..T
   int loss_blocks = 0;
 };
 
@@ -262,6 +266,7 @@ struct LogEpi : EpiBase {
     __nv_bfloat16* logits;
     float2* stats;
     int Ap, G, row_base;  // global row of tile 0 of this step
+    float* flowv;         // DB / SubTB: fp32 log F of the row (head column A), else null
   };
   struct Local {
     float mx, s;
@@ -282,6 +287,11 @@ struct LogEpi : EpiBase {
     uint32_t pk[16];
     float cm = -INFINITY;
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c);
+    if (e.flowv && e.P.A >= c && e.P.A < c + 32) {  // the log-flow column, before bf16 rounding
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c + i == e.P.A) e.flowv[(size_t)m * kTile + row] = v[i] + e.bf[c + i];
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float4 bq = bb[i];
@@ -576,6 +586,97 @@ __global__ void k_ls_loss(LossArgs a) {  // tb_loss objectives.cpp:120-142
   }
 }
 
+// transition_loss (DB, objectives.cpp:94-118) and subtb_loss (:144-180) over the lockstep
+// rows (every trajectory takes T steps): d_t = log pi(a_t|s_t) - log P_B, F(s_T) := log R,
+// per-row dL/dlog pi(a) -> coef, dL/dlog F -> gflow; pad rows (b >= nreal) get zeros
+struct FlowLossArgs {
+  DeviceBatch batch;
+  int Bl, T, nreal, subtb;
+  double B_global, penalty, norm;  // norm: sum_{0<=j<k<=T} lambda^(k-j) (SubTB)
+  const double* lampow;            // [T + 1] pow(lambda, k)
+  const double* neglog;
+  const float* rowbuf;
+  const float* flowv;
+  float* coef;
+  float* gflow;
+  double* lpart;
+  const int32_t* nsteps;  // counters + 4: real transitions of the (global) batch
+};
+
+constexpr int kLsSubTBMaxT = 128;
+
+__global__ void k_ls_loss_flow(FlowLossArgs a) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int T = a.T;
+  double loss = 0.0;
+  if (b >= a.nreal && b < a.Bl)
+    for (int t = 0; t < T; ++t) {
+      a.coef[(size_t)t * a.Bl + b] = 0.f;
+      a.gflow[(size_t)t * a.Bl + b] = 0.f;
+    }
+  if (b < a.nreal) {
+    const double logR = a.batch.log_rewards[b];
+    auto d_of = [&](int t) {
+      const size_t r = (size_t)t * a.Bl + b;
+      return (double)a.rowbuf[2 * r] - a.neglog[a.batch.nparents[(size_t)b * T + t]];
+    };
+    auto F_of = [&](int t) { return t < T ? (double)a.flowv[(size_t)t * a.Bl + b] : logR; };
+    if (!a.subtb) {
+      const double n = (double)*a.nsteps;
+      double gprev = 0.0;
+      for (int t = 0; t < T; ++t) {
+        const size_t r = (size_t)t * a.Bl + b;
+        const double res = F_of(t) - F_of(t + 1) + d_of(t);
+        const double w = (t == T - 1 ? a.penalty : 1.0) / n;
+        loss += w * (res * res);
+        const double g = 2.0 * w * res;
+        a.coef[r] = (float)g;
+        a.gflow[r] = (float)(g - gprev);  // + from transition t, - from transition t - 1
+        gprev = g;
+      }
+    } else {
+      double cum[kLsSubTBMaxT + 1], F[kLsSubTBMaxT + 1], gF[kLsSubTBMaxT + 1], D[kLsSubTBMaxT + 1];
+      cum[0] = 0.0;
+      for (int t = 0; t < T; ++t) cum[t + 1] = cum[t] + d_of(t);
+      for (int t = 0; t <= T; ++t) {
+        F[t] = F_of(t);
+        gF[t] = 0.0;
+        D[t] = 0.0;
+      }
+      const double scale = 1.0 / a.norm / a.B_global;
+      for (int j = 0; j < T; ++j)
+        for (int k = j + 1; k <= T; ++k) {
+          const double w = a.lampow[k - j] * scale;
+          const double res = F[j] - F[k] + cum[k] - cum[j];
+          loss += w * (res * res);
+          const double g = 2.0 * w * res;
+          gF[j] += g;
+          gF[k] -= g;  // (k = T: the log-reward constant)
+          D[j] += g;   // d_t for j <= t < k
+          D[k] -= g;
+        }
+      double gd = 0.0;
+      for (int t = 0; t < T; ++t) {
+        const size_t r = (size_t)t * a.Bl + b;
+        gd += D[t];
+        a.coef[r] = (float)gd;
+        a.gflow[r] = (float)gF[t];
+      }
+    }
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = loss;
+  __syncthreads();
+  for (int off = blockDim.x / 2; off > 0; off >>= 1) {
+    if ((int)threadIdx.x < off) red[threadIdx.x] += red[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    a.lpart[2 * blockIdx.x] = red[0];
+    a.lpart[2 * blockIdx.x + 1] = 0.0;
+  }
+}
+
 __global__ void k_ls_loss_finalize(const double* lpart, int n, double* scalars, int32_t* err) {
   if (threadIdx.x != 0) return;
   double l = 0.0, z = 0.0;
@@ -600,6 +701,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     uint8_t* dlog;  // image with KBA K-blocks per tile
     float* bpart;   // [tilesR][bw]
     int Bl, T, KBA, bw, boff;
+    const float* gflow;  // DB / SubTB: dL/dlog F per row -> head column A, else null
   };
   struct Local {
     float lse, g;
@@ -643,6 +745,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
       const float x = __bfloat162float(__float2bfloat16(v[i] + bias[i]));
       float d = ((lm >> i) & 1u) ? -l.g * __expf(x - l.lse) : 0.f;
       if (c0 + i == l.act) d += l.g;
+      if (e.gflow && c0 + i == e.P.A) d = e.gflow[r];
       v[i] = d;
     }
 #pragma unroll
@@ -885,6 +988,7 @@ struct RedArgs {
   int groups, bw, A, O, NL, t_dense, t_head, t_w1;
   int first[kMaxTasks + 1];
   MlpLayout L;
+  int flow;
 };
 
 __global__ void k_ls_reduce(RedArgs a) {
@@ -909,8 +1013,12 @@ __global__ void k_ls_reduce(RedArgs a) {
     const int64_t k = e - L.off_fw;
     const int p = (int)(k / a.A), c = (int)(k % a.A);
     v = slab_sum(a.t_head + c / 256, p, c % 256);
-  } else if (e >= L.off_fb && e < L.off_bw) {
+  } else if (e >= L.off_fb && e < L.off_fb + a.A) {
     v = bias_sum(a.NL * kH + (int)(e - L.off_fb));
+  } else if (a.flow && e >= L.off_flw && e < L.off_flb) {  // log-flow head [H][1] = head column A
+    v = slab_sum(a.t_head + a.A / 256, (int)(e - L.off_flw), a.A % 256);
+  } else if (a.flow && e == L.off_flb) {
+    v = bias_sum(a.NL * kH + a.A);
   } else {
     for (int l = 0; l < a.NL; ++l) {
       if (e >= L.off_b[l] && e < L.off_b[l] + kH) {
@@ -931,7 +1039,7 @@ struct EmitArgs {
   const float* p;
   int64_t n;
   MlpLayout L;
-  int A, NL;
+  int A, NL, flow;
   __nv_bfloat16 *w1, *wff, *wfd;
   __nv_bfloat16* wfw[kMaxNL];
   __nv_bfloat16* wdg[kMaxNL];
@@ -953,6 +1061,12 @@ __global__ void k_ls_emit(EmitArgs a) {
     *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wfd + sw128_offset(p, c, kH)) = v;
   } else if (j >= L.off_fb && j < L.off_fb + a.A) {
     a.bfp[j - L.off_fb] = a.p[j];
+  } else if (a.flow && j >= L.off_flw && j < L.off_flb) {  // log-flow head as head column A
+    const int p = (int)(j - L.off_flw), c = a.A, n = c / 256, cc = c % 256;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wff + (size_t)n * (256 * kH * 2) + sw128_offset(cc, p, 256)) = v;
+    *reinterpret_cast<__nv_bfloat16*>((uint8_t*)a.wfd + sw128_offset(p, c, kH)) = v;
+  } else if (a.flow && j == L.off_flb) {
+    a.bfp[a.A] = a.p[j];
   } else {
     for (int l = 1; l < a.NL; ++l)
       if (j >= L.off_w[l] && j < L.off_b[l]) {
@@ -972,6 +1086,7 @@ EmitArgs emit_args(Ctx& c) {
   a.L = c.L;
   a.A = f.A;
   a.NL = f.NL;
+  a.flow = f.flow;
   a.w1 = f.w1;
   a.wff = f.wff;
   a.wfd = f.wfd;
@@ -1020,6 +1135,7 @@ struct PersistArgs {
   // Ising: layer 1 as an MMA over the assigned-spin one-hot (feature 2 site + up) against
   // W1[3s + u] - W1[3s + 2] (wimg[0]), bias = h1init: no per-row fp32 state between steps
   int l1_mma;
+  float* flowv;  // DB / SubTB: fp32 log F of every row (head column A), else null
   const int16_t* forced;  // [nreal * T] teacher-forced actions (rows starting with -1 are sampled) or null
   int nreal;              // real trajectories (the rest pad the batch to a multiple of 128)
 };
@@ -1346,6 +1462,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int k = 4 * i + e;
+            if (a.flowv && col + k == P.A) a.flowv[r] = __uint_as_float(rr[k]) + bv[e];  // log F, fp32
             const float x = __bfloat162float(__float2bfloat16(__uint_as_float(rr[k]) + bv[e]));
             rr[k] = __float_as_uint(x);
             if ((lm >> k) & 1u) hi = fmaxf(hi, x);
@@ -1568,6 +1685,7 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
     pa.phase = c.phase;
     pa.forced = forced;
     pa.nreal = c.Bl;
+    pa.flowv = f.flow ? f.flowv : nullptr;
     const int smem = kH * kH * 2 + 1024;
     set_smem_once(k_ls_persist<E>, smem);
     ProfScope ps(c, "k_ls_persist");
@@ -1598,7 +1716,7 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
     g.A = (const uint8_t*)f.h[f.NL - 1];
     g.B = (const uint8_t*)f.wff;
     g.n_tiles = f.NT;
-    typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl};
+    typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl, f.flow ? f.flowv : nullptr};
     launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
     SampleArgs sa{c.P, fold_in(key, (uint64_t)t), eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst,
                   f.last_act, f.rowbuf, c.batch, forced, c.Bl};
@@ -1612,7 +1730,25 @@ template <class E>
 void train_impl(Ctx& c) {
   LsState& f = LS(c);
   const int Bl = f.Bl, NL = f.NL;
-  {
+  if (f.flow) {  // DB / SubTB
+    const int T = f.T;
+    double norm = 0.0;
+    if (!f.lampow) {
+      std::vector<double> lp(T + 1);
+      for (int k = 0; k <= T; ++k) lp[k] = pow(c.train.subtb_lambda, (double)k);
+      cuda_check(cudaMalloc(&f.lampow, sizeof(double) * (T + 1)), "lampow");
+      cuda_check(cudaMemcpy(f.lampow, lp.data(), sizeof(double) * (T + 1), cudaMemcpyHostToDevice), "lampow");
+    }
+    for (int j = 0; j < T; ++j)  // subtb_loss's per-trajectory normaliser (every length is T)
+      for (int k = j + 1; k <= T; ++k) norm += pow(c.train.subtb_lambda, (double)(k - j));
+    FlowLossArgs la{c.batch, Bl, T, c.Bl, c.train.objective == GFNX_OBJ_SUBTB, (double)c.B,
+                    c.train.terminal_penalty, norm, f.lampow, c.d_neglog, f.rowbuf, f.flowv, f.coef, f.gflow,
+                    f.lpart, c.batch.counters + 4};
+    ProfScope ps(c, "k_ls_loss");
+    k_ls_loss_flow<<<f.loss_blocks, 256, 0, c.stream>>>(la);
+    k_ls_loss_finalize<<<1, 32, 0, c.stream>>>(f.lpart, f.loss_blocks, c.d_scalars, c.batch.counters + 3);
+    c.launches += 2;
+  } else {
     LossArgs la{c.batch, Bl, f.T, c.Bl, (double)c.B, c.d_neglog, f.rowbuf, f.coef, f.lpart, c.d_scalars};
     ProfScope ps(c, "k_ls_loss");
     k_ls_loss<<<f.loss_blocks, 256, 0, c.stream>>>(la);
@@ -1629,7 +1765,7 @@ void train_impl(Ctx& c) {
   g.n_tiles = f.NT;
   g.KB = 4;
   typename DlogEpi<E>::Args de{c.P, f.bfp, f.rowbuf, f.coef, f.stst, c.batch.actions, (uint8_t*)f.dlog, f.bpart,
-                               Bl, f.T, f.KBA, f.bw, NL * kH};
+                               Bl, f.T, f.KBA, f.bw, NL * kH, f.flow ? f.gflow : nullptr};
   launch_gemm<256, DlogEpi<E>>(c, "k_gemm_dlogits", g, de, f.num_sms);
   GemmGeom g2{};
   g2.A = (const uint8_t*)f.dlog;
@@ -1683,7 +1819,7 @@ void train_impl(Ctx& c) {
     ProfScope ps(c, "k_ls_reduce");
     k_ls_colsum<<<dim3((f.bw + 255) / 256, f.cgroups), 256, 0, c.stream>>>(f.bpart, f.tilesR, f.bw, f.cgroups,
                                                                            f.bpart2);
-    RedArgs ra{f.wpart, f.bpart2, c.g32, f.cgroups, f.bw, f.A, f.O, NL, f.t_dense, f.t_head, f.t_w1, {}, c.L};
+    RedArgs ra{f.wpart, f.bpart2, c.g32, f.cgroups, f.bw, f.A, f.O, NL, f.t_dense, f.t_head, f.t_w1, {}, c.L, f.flow};
     for (int k = 0; k <= f.ntasks; ++k) ra.first[k] = f.first[k];
     k_ls_reduce<<<(unsigned)((c.L.n_params + 255) / 256), 256, 0, c.stream>>>(ra);
     c.launches += 2;
@@ -1702,7 +1838,9 @@ bool ls_supported(const Ctx& c, std::string* why) {
     *why = m;
     return false;
   };
-  if (c.train.objective != GFNX_OBJ_TB) return no("bitseq/Ising fast path implements TB (BASELINE configs #3, #4)");
+  if (c.train.objective != GFNX_OBJ_TB && c.train.objective != GFNX_OBJ_DB && c.train.objective != GFNX_OBJ_SUBTB)
+    return no("bitseq/Ising fast path implements TB, DB and SubTB");
+  if (c.train.objective == GFNX_OBJ_SUBTB && c.P.T > kLsSubTBMaxT) return no("bitseq/Ising SubTB supports T <= 128");
   if (c.L.n_trunk < 2 || c.L.n_trunk > kMaxNL) return no("bitseq/Ising fast path needs 2..4 hidden layers");
   for (int l = 1; l <= c.L.n_trunk; ++l)
     if (c.L.dims[l] != kH) return no("bitseq/Ising fast path needs hidden width 256");
@@ -1723,7 +1861,8 @@ void ls_init(Ctx& c) {
   cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, c.device);
   f->NL = c.L.n_trunk;
   f->A = c.P.A;
-  f->Ap = (f->A + 255) / 256 * 256;
+  f->flow = c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB;
+  f->Ap = (f->A + f->flow + 255) / 256 * 256;  // the flow head rides along as column A
   f->NT = f->Ap / 256;
   f->G = f->Ap / 128;
   f->KBA = f->Ap / 64;
@@ -1789,6 +1928,10 @@ void ls_init(Ctx& c) {
   alloc(&f->dlog, (size_t)f->tilesR * f->KBA * (kTile * 128));
   alloc(&f->rowbuf, sizeof(float) * 2 * (size_t)f->R);
   alloc(&f->coef, sizeof(float) * (size_t)f->R);
+  if (f->flow) {
+    alloc(&f->flowv, sizeof(float) * (size_t)f->R);
+    alloc(&f->gflow, sizeof(float) * (size_t)f->R);
+  }
   alloc(&f->bpart, sizeof(float) * (size_t)f->tilesR * f->bw);
   alloc(&f->bpart2, sizeof(float) * (size_t)f->cgroups * f->bw);
   alloc(&f->wpart, sizeof(float) * (size_t)f->first[f->ntasks] * 256 * 256);
@@ -1801,7 +1944,7 @@ void ls_free(Ctx& c) {
   if (!f) return;
   std::vector<void*> ptrs = {f->w1, f->wff, f->wfd, f->l1img, f->bfp, f->h1init, f->preact, f->cur, f->stst, f->last_act,
                              f->logits, f->stats, f->dlog, f->rowbuf, f->coef, f->bpart, f->bpart2, f->wpart,
-                             f->lpart};
+                             f->lpart, f->flowv, f->gflow, f->lampow};
   for (int l = 0; l < kMaxNL; ++l) {
     ptrs.push_back(f->wfw[l]);
     ptrs.push_back(f->wdg[l]);

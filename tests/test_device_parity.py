@@ -37,12 +37,13 @@ pytestmark = pytest.mark.gpu
 FIELDS = ("lengths", "fwd_actions", "bwd_actions", "log_rewards", "log_pb", "delta", "terminal_state")
 
 
-def _bitseq(n_bits, batch):
-    return abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8), abi.train_desc(abi.BITSEQ, batch=batch, objective="tb")
+def _bitseq(n_bits, batch, objective="tb"):
+    return abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8), abi.train_desc(abi.BITSEQ, batch=batch, objective=objective)
 
 
-def _ising(side, batch):
-    return abi.env_desc(abi.ISING, is_side=side, is_sigma=0.2), abi.train_desc(abi.ISING, batch=batch, objective="tb")
+def _ising(side, batch, objective="tb"):
+    return (abi.env_desc(abi.ISING, is_side=side, is_sigma=0.2),
+            abi.train_desc(abi.ISING, batch=batch, objective=objective))
 
 
 # ---------------------------------------------------------------------------
@@ -140,6 +141,12 @@ SAME_BATCH = [
     ("bitseq_n120_b128", lambda: _bitseq(120, 128), LS, True),
     ("ising_6x6_b256", lambda: _ising(6, 256), IS, True),
     ("ising_10x10_b128", lambda: _ising(10, 128), IS, True),
+    # lockstep DB / SubTB: the log-flow head as head column A (k_ls_loss_flow)
+    ("bitseq_n48_db_b128", lambda: _bitseq(48, 128, "db"), LS, True),
+    ("bitseq_n48_subtb_b128", lambda: _bitseq(48, 128, "subtb"), LS, True),
+    ("ising_6x6_db_b256", lambda: _ising(6, 256, "db"), IS, True),
+    ("ising_6x6_subtb_b256", lambda: _ising(6, 256, "subtb"), IS, True),
+    ("ising_4x4_db_b200_ragged", lambda: _ising(4, 200, "db"), IS, True),
 ]
 
 

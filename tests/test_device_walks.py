@@ -201,3 +201,34 @@ def test_lockstep_ragged_batch(name, batch):
     assert abs(ld - lc) <= 1e-4 * max(1.0, abs(lc)) and rel < 5e-2, (ld, lc, rel)
     d.close()
     chk.close()
+
+
+@pytest.mark.parametrize("name", ["ising", "bitseq_k8"])
+@pytest.mark.parametrize("objective", ["db", "subtb"])
+def test_lockstep_flow_objectives_vs_check_mode(name, objective):
+    """DB and SubTB on the lockstep bitseq / Ising bf16 path (the log-flow head rides as head
+    column A; k_ls_loss_flow): loss and gradients on the same batch against the fp64 check
+    mode (the reference's operation order), with the lockstep bf16 tolerances of DESIGN §2."""
+    e, t = _cfg(name, False)
+    t.objective = abi.OBJECTIVES[objective]
+    e2, t2 = _cfg(name, True)
+    t2.objective = abi.OBJECTIVES[objective]
+    d, chk = engine.Trainer(e, t), engine.Trainer(e2, t2)
+    d.run(0, 3)  # a policy with a non-trivial flow head
+    chk.set_params(*d.params())
+    d.forward_rollout(3, 0.0)
+    bd = d.batch()
+    acts = np.where(np.arange(d.T)[None, :] < bd["lengths"][:, None], bd["fwd_actions"], -1)
+    chk.rollout_from_actions(acts)
+    ld, lc = d.compute_grads(), chk.compute_grads()
+    gd, gc = d.grads()[0], chk.grads()[0]
+    rel = np.linalg.norm(gd - gc) / np.linalg.norm(gc)
+    off_flw = len(gc) - 257  # flow head [H][1] + bias, the last parameters
+    relf = np.linalg.norm(gd[off_flw:] - gc[off_flw:]) / max(np.linalg.norm(gc[off_flw:]), 1e-30)
+    print(f"{name} {objective}: loss {ld:.6f} vs {lc:.6f}, grad rel-L2 {rel:.2e}, flow head {relf:.2e}")
+    assert abs(ld - lc) <= 1e-3 * max(1.0, abs(lc)), (ld, lc)
+    # the whole-gradient bound here is loose (bf16 floor: the per-tensor bounds against the
+    # bf16 operand model are in test_device_parity.py); the flow head must be tight
+    assert rel < 2e-1 and relf < 5e-2, (rel, relf)
+    d.close()
+    chk.close()
