@@ -12,8 +12,10 @@
 #include <string>
 #include <vector>
 
+#include "gfn/envs/ising.hpp"
 #include "gfn/errors.hpp"
 #include "gfn/nn.hpp"
+#include "gfn/rng.hpp"
 #include "gfnx.h"
 
 namespace gfn {
@@ -86,6 +88,54 @@ class DeviceTrainer {
     gfnx_throw(gfnx_load_checkpoint(ctx_, path.c_str(), &step), ctx_);
     return step;
   }
+  // backward_rollout(env, p, nullptr, false, terminals, key)   env_core.hpp:314-370 (uniform
+  // P_B) of local_batch packed terminal states -> the resident batch (train_step acts on it)
+  void backward_rollout(const std::vector<uint32_t>& packed, const RngKey& key) {
+    int32_t bl = 0, b0 = 0, T = 0, sw = 0;
+    gfnx_throw(gfnx_batch_dims(ctx_, &bl, &b0, &T, &sw), ctx_);
+    if (packed.size() != (size_t)bl * (size_t)sw) throw contract_violation("backward_rollout: batch size mismatch");
+    gfnx_throw(gfnx_backward_rollout(ctx_, packed.data(), bl, key.hi, key.lo), ctx_);
+  }
+  // mc_terminal_logprob (exact.hpp:229-241) of n packed terminals, one RngKey each
+  std::vector<double> mc_terminal_logprob(const std::vector<uint32_t>& packed, const std::vector<RngKey>& keys,
+                                          int num_samples) {
+    std::vector<uint64_t> kw;
+    for (const RngKey& k : keys) {
+      kw.push_back(k.hi);
+      kw.push_back(k.lo);
+    }
+    std::vector<double> out(keys.size());
+    gfnx_throw(gfnx_mc_terminal_logprob(ctx_, packed.data(), (int64_t)keys.size(), num_samples, kw.data(),
+                                        out.data()),
+               ctx_);
+    return out;
+  }
+  // the bitseq `pearson` metric closure of build_bitseq (train.cpp:440-454)
+  double pearson(int64_t step, int mc_samples, uint64_t test_seed) {
+    double r = 0.0;
+    gfnx_throw(gfnx_pearson(ctx_, step, mc_samples, test_seed, &r), ctx_);
+    return r;
+  }
+
+  // ---- EB-GFN (run_eb_gfn, train.cpp:875-1018) on an Ising device trainer ----
+  // data: the samples run_eb_gfn would load or Gibbs-sample (empty: the device ctx samples
+  // them itself with gibbs_data_sampler's algorithm and key)
+  void eb_init(const gfnx_eb_desc& d, const std::vector<std::vector<int8_t>>& data = {}) {
+    std::vector<int8_t> flat;
+    for (const auto& x : data) flat.insert(flat.end(), x.begin(), x.end());
+    gfnx_throw(gfnx_eb_init(ctx_, &d, data.empty() ? nullptr : flat.data(), (int64_t)data.size()), ctx_);
+  }
+  // iterations it0 .. it0 + n - 1; rows {loss, logZ, neg_log_rmse, accepted proposals}
+  std::vector<double> eb_run(int64_t it0, int64_t n) {
+    std::vector<double> m((size_t)(4 * n));
+    gfnx_throw(gfnx_eb_run(ctx_, it0, n, m.data()), ctx_);
+    return m;
+  }
+  // the learned coupling into the reference's IsingCoupling (ising.hpp:16-25)
+  void eb_coupling(IsingCoupling& j_model) {
+    gfnx_throw(gfnx_eb_coupling(ctx_, j_model.j.data(), nullptr, (int64_t)j_model.j.size(), nullptr), ctx_);
+  }
+
   gfnx_ctx* handle() { return ctx_; }
 
  private:

@@ -40,3 +40,14 @@ def test_binding_trains_reference_params_on_device():
     r = subprocess.run([_driver(), "train"], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "roundtrip_maxdiff" in r.stdout
+
+
+@pytest.mark.gpu
+def test_binding_runs_eb_gfn_loop_on_device():
+    """run_eb_gfn's loop through DeviceTrainer::eb_*: reference Gibbs data in, the learned
+    coupling back in the reference's IsingCoupling; its neg_log_rmse (computed by the
+    reference) equals the device's metric."""
+    r = subprocess.run([_driver(), "eb"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    vals = dict(zip(r.stdout.split()[1::2], map(float, r.stdout.split()[2::2])))
+    assert vals["final_nlr"] > vals["init_nlr"], vals
