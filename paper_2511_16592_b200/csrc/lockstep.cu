@@ -303,9 +303,16 @@ struct LogEpi : EpiBase {
       v[2 * i] = bf16_lo(pk[i]);
       v[2 * i + 1] = bf16_hi(pk[i]);
     }
+    if constexpr (std::is_same<E, BitseqEnv>::value) {  // legality is per 256-column slot
+      if (lm) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i)
-      if ((lm >> i) & 1u) cm = fmaxf(cm, v[i]);
+        for (int i = 0; i < 32; ++i) cm = fmaxf(cm, v[i]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if ((lm >> i) & 1u) cm = fmaxf(cm, v[i]);
+    }
     uint8_t* dst = reinterpret_cast<uint8_t*>(e.logits + (size_t)b * e.Ap + c);
 #pragma unroll
     for (int q = 0; q < 2; ++q)
@@ -316,8 +323,13 @@ struct LogEpi : EpiBase {
     if (lm == 0u) return;
     const float nm = fmaxf(l.mx, cm);
     float s = 0.f;
+    if constexpr (std::is_same<E, BitseqEnv>::value) {  // all 32 columns legal here
 #pragma unroll
-    for (int i = 0; i < 32; ++i) s += ((lm >> i) & 1u) ? __expf(v[i] - nm) : 0.f;
+      for (int i = 0; i < 32; ++i) s += __expf(v[i] - nm);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) s += ((lm >> i) & 1u) ? __expf(v[i] - nm) : 0.f;
+    }
     l.s = l.s * __expf(l.mx - nm) + s;  // l.mx = -inf -> factor 0
     l.mx = nm;
   }
@@ -745,8 +757,13 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
       const float x = __bfloat162float(__float2bfloat16(v[i] + bias[i]));
       float d = ((lm >> i) & 1u) ? -l.g * __expf(x - l.lse) : 0.f;
       if (c0 + i == l.act) d += l.g;
-      if (e.gflow && c0 + i == e.P.A) d = e.gflow[r];
       v[i] = d;
+    }
+    if (e.gflow && (unsigned)(e.P.A - c0) < 32u) {  // the log-flow column (warp-uniform test)
+      const float gf = e.gflow[r];
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (c0 + i == e.P.A) v[i] = gf;
     }
 #pragma unroll
     for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);

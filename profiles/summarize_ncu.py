@@ -72,6 +72,9 @@ def main(rep, out_md, rows_per_launch=None, source=None):
         traffic.setdefault(short, []).append((t, dur))
     with open(out_md, "w") as f:
         f.write("\n".join(lines) + "\n")
+    if os.environ.get("NCU_NO_TRAFFIC"):  # secondary configs: keep the headline's traffic record
+        print("\n".join(lines))
+        return
     tj = os.path.join(os.path.dirname(out_md), "ncu_traffic.json")
     with open(tj, "w") as f:
         json.dump({k: {"dram_bytes": sum(x for x, _ in v) / len(v), "duration_us": sum(d for _, d in v) / len(v),
