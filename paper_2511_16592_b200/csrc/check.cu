@@ -14,6 +14,7 @@
 
 #include "engine.h"
 #include "check_common.cuh"
+#include "walk.cuh"
 
 namespace gfnx {
 
@@ -171,16 +172,19 @@ __device__ int find_traj(const int32_t* row0, int Bl, int r) {
   return lo;
 }
 
+// bwd = 1: the learned backward policy's pass (mlp_forward_tape's bwd head at s_{t+1},
+// nn.cpp:111-121, masked by backward_action_mask): row r = step t of its trajectory holds
+// s_{t+1}, D carries the bwd head's offsets with A = Ab, bidx[r] = the step's backward action
 template <class Env>
 __global__ void k_check_fwd(EnvParams P, DevLayout D, const double* __restrict__ params,
                             DeviceBatch batch, int Bl, int R, int need_flow, double* obs_out,
                             double* act_out, double* logp_out, uint8_t* mask_out,
-                            double* flow_out, int32_t* err) {
+                            double* flow_out, int32_t* err, int bwd, int32_t* bidx) {
   const int r = blockIdx.x;
   if (r >= R) return;
   __shared__ typename Env::State s;
   __shared__ double red;
-  const int T = P.T, A = P.A;
+  const int T = P.T, A = bwd ? P.Ab : P.A;
   double* obs = obs_out + (size_t)r * P.O;
   double* act = act_out + (size_t)r * D.act_sz;
   double* x = logp_out + (size_t)r * A;
@@ -189,12 +193,14 @@ __global__ void k_check_fwd(EnvParams P, DevLayout D, const double* __restrict__
     const int b = find_traj(batch.row0, Bl, r);
     const int t = r - batch.row0[b];
     Env::reset(P, s);
-    for (int q = 0; q < t; ++q) Env::step(P, s, batch.actions[(size_t)b * T + q]);
+    for (int q = 0; q < t + bwd; ++q) Env::step(P, s, batch.actions[(size_t)b * T + q]);
+    if (bwd) bidx[r] = Env::backward_action(P, batch.actions[(size_t)b * T + t]);
   }
   for (int i = threadIdx.x; i < P.O; i += blockDim.x) obs[i] = 0.0;
   __syncthreads();
   if (threadIdx.x == 0) Env::features(P, s, [&](int f, double v) { obs[f] = v; });
-  for (int i = threadIdx.x; i < A; i += blockDim.x) mask[i] = Env::legal(P, s, i) ? 1 : 0;
+  for (int i = threadIdx.x; i < A; i += blockDim.x)
+    mask[i] = (bwd ? bwd_legal<Env>(P, s, i) : Env::legal(P, s, i)) ? 1 : 0;
   __syncthreads();
   const double* h = obs;
   int in = P.O;
@@ -237,8 +243,12 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
                              int stop, const double* lampow, const double* neglog,
                              DeviceBatch batch, int Bl, const int32_t* gcounts,
                              const double* logp, const double* flow, double* glogp,
-                             double* gflow, double* gpair, double* scalars, int32_t* err) {
+                             double* gflow, double* gpair, double* scalars, int32_t* err,
+                             int Ab, const double* blogp, const int32_t* bidx, double* bglogp) {
+  // learned backward policy (blogp != null): log P_B = the bwd head's masked log-softmax at
+  // s_{t+1} (step_log_ratio objectives.cpp:57-70: pf - pb), gradient -g into bglogp
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  auto pb_idx = [&](int64_t r) { return r * Ab + bidx[r]; };
   const double log_z = scalars[0];
   double norm = (double)B_global;
   if (obj == GFNX_OBJ_DB) norm = (double)gcounts[0];
@@ -253,16 +263,21 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
     if (obj == GFNX_OBJ_TB) {
       const double w = 1.0 / norm;
       double cum = 0.0;
-      for (int t = 0; t < L; ++t) cum += logp[(r0 + t) * A + acts[t]] + -neglog[np[t]];
+      for (int t = 0; t < L; ++t)
+        cum += blogp ? logp[(r0 + t) * A + acts[t]] - blogp[pb_idx(r0 + t)]
+                     : logp[(r0 + t) * A + acts[t]] + -neglog[np[t]];
       const double res = (cum + log_z) + -logr;
       loss += res * res * w;
       const double g = 2.0 * res * w;
       dlogz += g;
-      for (int t = 0; t < L; ++t) glogp[(r0 + t) * A + acts[t]] += g;
+      for (int t = 0; t < L; ++t) {
+        glogp[(r0 + t) * A + acts[t]] += g;
+        if (blogp) bglogp[pb_idx(r0 + t)] += -g;
+      }
     } else if (obj == GFNX_OBJ_DB) {
       for (int t = 0; t < L; ++t) {
         const int64_t r = r0 + t;
-        const double d = logp[r * A + acts[t]] + -neglog[np[t]];
+        const double d = blogp ? logp[r * A + acts[t]] - blogp[pb_idx(r)] : logp[r * A + acts[t]] + -neglog[np[t]];
         const double f1 = (t + 1 < L) ? flow[r + 1] : logr;
         const double res = (flow[r] - f1) + d;
         const double w = (t == L - 1 ? terminal_penalty : 1.0) / norm;
@@ -271,6 +286,7 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
         gflow[r] += g;
         if (t + 1 < L) gflow[r + 1] += -g;
         glogp[r * A + acts[t]] += g;
+        if (blogp) bglogp[pb_idx(r)] += -g;
       }
     } else if (obj == GFNX_OBJ_SUBTB) {
       double* cum = gpair;                       // [T+1]
@@ -279,7 +295,8 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
       double* gp = gpair + 3 * (T + 1);          // [(T+1)^2]
       cum[0] = 0.0;
       for (int t = 0; t < L; ++t) {
-        cum[t + 1] = cum[t] + (logp[(r0 + t) * A + acts[t]] + -neglog[np[t]]);
+        cum[t + 1] = cum[t] + (blogp ? logp[(r0 + t) * A + acts[t]] - blogp[pb_idx(r0 + t)]
+                                     : logp[(r0 + t) * A + acts[t]] + -neglog[np[t]]);
         F[t] = flow[r0 + t];
       }
       F[L] = logr;
@@ -314,7 +331,10 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
         for (int k = j + 1; k <= L; ++k) gcum[j] += -gp[n++];
       double acc = 0.0;  // exclusive_row_cumsum backward (tape.cpp:448-461)
       for (int c = L; c >= 0; --c) {
-        if (c < L) glogp[(r0 + c) * A + acts[c]] += acc;
+        if (c < L) {
+          glogp[(r0 + c) * A + acts[c]] += acc;
+          if (blogp) bglogp[pb_idx(r0 + c)] += -acc;
+        }
         acc += gcum[c];
       }
     } else if (obj == GFNX_OBJ_MDB) {
@@ -324,13 +344,14 @@ __global__ void k_check_loss(int obj, int A, int T, int B_global, double termina
         const int a = acts[t];
         if (a == stop) atomicExch(err, GFNX_ERR_CONTRACT);
         double res = logp[r * A + a] + (logp[(r + 1) * A + stop] - logp[r * A + stop]);
-        res = res + -neglog[np[t]];
+        res = blogp ? res - blogp[pb_idx(r)] : res + -neglog[np[t]];
         res = res + -batch.delta[(size_t)b * T + t];
         loss += res * res * w;
         const double g = 2.0 * res * w;
         glogp[r * A + a] += g;
         glogp[(r + 1) * A + stop] += g;
         glogp[r * A + stop] += -g;
+        if (blogp) bglogp[pb_idx(r)] += -g;
       }
     }
   }
@@ -398,9 +419,13 @@ __global__ void k_check_bwd(DevLayout D, const double* __restrict__ params, int 
 
 // One thread per parameter element, rows accumulated sequentially in (b, t) order:
 // matmul_tn_acc (tensor.cpp:92-102) and the add_rowvec bias backward (tape.cpp:380-389).
+// (learned backward: a second row set — the s_{t+1} rows of the bwd head — adds to the trunk
+// and owns the bwd head; R2 = 0 otherwise)
 __global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* obs,
                               const double* act, const double* gx, const double* gz,
-                              const double* gflow, double* grads) {
+                              const double* gflow, double* grads, int R2, const double* obs2,
+                              const double* act2, const double* gx2, const double* gz2, int64_t off_bw,
+                              int64_t off_bb, int Ab) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int A = D.A;
   // trunk weights / biases
@@ -415,6 +440,10 @@ __global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* o
         const double av = l == 0 ? obs[(size_t)r * D.O + p] : act[(size_t)r * D.act_sz + D.act_off[l - 1] + p];
         acc += av * gz[(size_t)r * D.act_sz + D.act_off[l] + j];
       }
+      for (int r = 0; r < R2; ++r) {
+        const double av = l == 0 ? obs2[(size_t)r * D.O + p] : act2[(size_t)r * D.act_sz + D.act_off[l - 1] + p];
+        acc += av * gz2[(size_t)r * D.act_sz + D.act_off[l] + j];
+      }
       grads[e] = acc;
       return;
     }
@@ -422,6 +451,7 @@ __global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* o
       const int j = (int)(e - D.off_b[l]);
       double acc = 0.0;
       for (int r = 0; r < R; ++r) acc += gz[(size_t)r * D.act_sz + D.act_off[l] + j];
+      for (int r = 0; r < R2; ++r) acc += gz2[(size_t)r * D.act_sz + D.act_off[l] + j];
       grads[e] = acc;
       return;
     }
@@ -453,6 +483,20 @@ __global__ void k_check_wgrad(DevLayout D, int R, int need_flow, const double* o
   if (need_flow && e == D.off_flb) {
     double acc = 0.0;
     for (int r = 0; r < R; ++r) acc += gflow[r];
+    grads[e] = acc;
+  }
+  if (R2 > 0 && e >= off_bw && e < off_bw + (int64_t)H * Ab) {  // bwd head [H][Ab]
+    const int64_t q = e - off_bw;
+    const int p = (int)(q / Ab), j = (int)(q % Ab);
+    double acc = 0.0;
+    for (int r = 0; r < R2; ++r) acc += act2[(size_t)r * D.act_sz + last + p] * gx2[(size_t)r * Ab + j];
+    grads[e] = acc;
+    return;
+  }
+  if (R2 > 0 && e >= off_bb && e < off_bb + Ab) {
+    const int j = (int)(e - off_bb);
+    double acc = 0.0;
+    for (int r = 0; r < R2; ++r) acc += gx2[(size_t)r * Ab + j];
     grads[e] = acc;
   }
 }
@@ -503,13 +547,29 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
   c.launches++;
 }
 
+// the learned backward head as the "head" of DevLayout (A = Ab, nn.cpp:111-121 bwd leaves)
+DevLayout bwd_layout(const Ctx& c) {
+  DevLayout d = make_dev_layout(c);
+  d.off_fw = c.L.off_bw;
+  d.off_fb = c.L.off_bb;
+  d.A = c.shape.num_backward_actions;
+  return d;
+}
+
 template <class Env>
 void fwd_impl(Ctx& c, int R, int need_flow) {
   const DevLayout D = make_dev_layout(c);
   k_check_fwd<Env><<<R, 256, 0, c.stream>>>(c.P, D, c.p64, c.batch, c.Bl, R, need_flow, c.ck_obs,
                                             c.ck_act, c.ck_logp, c.ck_mask, c.ck_flow,
-                                            c.batch.counters + 3);
+                                            c.batch.counters + 3, 0, nullptr);
   c.launches++;
+  if (c.train.learned_backward) {  // the bwd head over the s_{t+1} rows
+    const DevLayout Db = bwd_layout(c);
+    k_check_fwd<Env><<<R, 256, 0, c.stream>>>(c.P, Db, c.p64, c.batch, c.Bl, R, 0, c.ck_bobs, c.ck_bact,
+                                              c.ck_blogp, c.ck_bmask, nullptr, c.batch.counters + 3, 1,
+                                              c.ck_bidx);
+    c.launches++;
+  }
 }
 
 void ensure_scratch(Ctx& c, int64_t rows) {
@@ -534,6 +594,19 @@ void ensure_scratch(Ctx& c, int64_t rows) {
   cuda_check(cudaMalloc(&c.ck_gflow, sizeof(double) * n), "check scratch");
   cuda_check(cudaMalloc(&c.ck_gz, sizeof(double) * n * D.act_sz), "check scratch");
   cuda_check(cudaMalloc(&c.ck_gx, sizeof(double) * n * D.A), "check scratch");
+  if (c.train.learned_backward) {
+    const int Ab = c.shape.num_backward_actions;
+    void* old[] = {c.ck_bobs, c.ck_bact, c.ck_blogp, c.ck_bmask, c.ck_bglogp, c.ck_bgx, c.ck_bgz, c.ck_bidx};
+    for (void* p : old) cudaFree(p);
+    cuda_check(cudaMalloc(&c.ck_bobs, sizeof(double) * n * D.O), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bact, sizeof(double) * n * D.act_sz), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_blogp, sizeof(double) * n * Ab), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bmask, n * Ab), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bglogp, sizeof(double) * n * Ab), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bgx, sizeof(double) * n * Ab), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bgz, sizeof(double) * n * D.act_sz), "check scratch");
+    cuda_check(cudaMalloc(&c.ck_bidx, sizeof(int32_t) * n), "check scratch");
+  }
   c.ck_rows_cap = n;
 }
 
@@ -577,6 +650,9 @@ void check_train(Ctx& c, bool /*apply*/, double /*lr*/, double* /*loss*/) {
   }
   cudaMemsetAsync(c.ck_glogp, 0, sizeof(double) * (size_t)R * D.A, c.stream);
   cudaMemsetAsync(c.ck_gflow, 0, sizeof(double) * (size_t)R, c.stream);
+  const bool lb = c.train.learned_backward != 0;
+  const int Ab = c.shape.num_backward_actions;
+  if (lb) cudaMemsetAsync(c.ck_bglogp, 0, sizeof(double) * (size_t)R * Ab, c.stream);
   const int T = c.shape.max_traj_len;
   if (!c.ck_lampow) {  // pow(lambda, k), k = 0..T (glibc pow), and the SubTB pair scratch
     cuda_check(cudaMalloc(&c.ck_lampow, sizeof(double) * (T + 1)), "lampow");
@@ -591,13 +667,20 @@ void check_train(Ctx& c, bool /*apply*/, double /*lr*/, double* /*loss*/) {
   k_check_loss<<<1, 1, 0, c.stream>>>(obj, D.A, T, c.B, c.train.terminal_penalty,
                                       c.shape.stop_action, lampow, c.d_neglog, c.batch, c.Bl,
                                       c.batch.counters + 4, c.ck_logp, c.ck_flow, c.ck_glogp,
-                                      c.ck_gflow, gpair, c.d_scalars, c.batch.counters + 3);
+                                      c.ck_gflow, gpair, c.d_scalars, c.batch.counters + 3, Ab,
+                                      lb ? c.ck_blogp : nullptr, c.ck_bidx, c.ck_bglogp);
   k_check_bwd<<<R, 256, 0, c.stream>>>(D, c.p64, R, need_flow, c.ck_act, c.ck_logp, c.ck_mask,
                                        c.ck_glogp, c.ck_gflow, c.ck_gx, c.ck_gz);
+  if (lb) {  // bwd head + trunk over the s_{t+1} rows
+    k_check_bwd<<<R, 256, 0, c.stream>>>(bwd_layout(c), c.p64, R, 0, c.ck_bact, c.ck_blogp, c.ck_bmask,
+                                         c.ck_bglogp, nullptr, c.ck_bgx, c.ck_bgz);
+    c.launches++;
+  }
   cudaMemsetAsync(c.g64, 0, sizeof(double) * c.L.n_params, c.stream);
   const int64_t n = c.L.n_params;
   k_check_wgrad<<<(unsigned)((n + 127) / 128), 128, 0, c.stream>>>(
-      D, R, need_flow, c.ck_obs, c.ck_act, c.ck_gx, c.ck_gz, c.ck_gflow, c.g64);
+      D, R, need_flow, c.ck_obs, c.ck_act, c.ck_gx, c.ck_gz, c.ck_gflow, c.g64, lb ? R : 0, c.ck_bobs,
+      c.ck_bact, c.ck_bgx, c.ck_bgz, c.L.off_bw, c.L.off_bb, Ab);
   c.launches += 3;
 }
 

@@ -406,6 +406,7 @@ void eb_init(Ctx& c, const gfnx_eb_desc& d, const int8_t* data, int64_t n) {
   if (c.env.kind != GFNX_ENV_ISING) raise_error(GFNX_ERR_CONFIG, "eb-gfn: Ising env only");
   if (c.train.objective != GFNX_OBJ_TB) raise_error(GFNX_ERR_CONFIG, "eb-gfn: the sampler objective must be tb");
   if (c.world != 1) raise_error(GFNX_ERR_CONFIG, "eb-gfn: single-rank loop");
+  if (c.train.learned_backward) raise_error(GFNX_ERR_CONFIG, "eb-gfn: uniform backward policy only on the device");
   const int D = c.P.is_D;
   if (d.k > D) raise_error(GFNX_ERR_CONFIG, "back_and_forth: k must lie in [0, D]");
   if (!(d.alpha >= 0.0 && d.alpha <= 1.0)) raise_error(GFNX_ERR_CONFIG, "eb-gfn: alpha must lie in [0, 1]");

@@ -182,6 +182,11 @@ struct Ctx {
   double* ck_pair = nullptr;
   double* ck_lampow = nullptr;  // [T + 1] pow(lambda, k)
   double* ck_gpair = nullptr;   // SubTB pair scratch
+  // learned backward policy (check mode): the bwd head's rows (s_{t+1} of every step)
+  double *ck_bobs = nullptr, *ck_bact = nullptr, *ck_blogp = nullptr, *ck_bglogp = nullptr, *ck_bgx = nullptr,
+         *ck_bgz = nullptr;
+  uint8_t* ck_bmask = nullptr;
+  int32_t* ck_bidx = nullptr;
   int64_t ck_rows_cap = 0;
 
   // optional rollout phase clocks (env GFNX_PHASE_TIMERS=1 at create): [8] int64

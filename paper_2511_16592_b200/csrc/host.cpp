@@ -349,7 +349,9 @@ std::string build_host_env(const gfnx_env_desc& e, HostEnv* out) {
 std::string validate_train(const gfnx_train_desc& t, const gfnx_env_shape& s) {
   if (t.objective == GFNX_OBJ_FLDB) return "fldb objective is out of scope (phylo only)";
   if (t.objective < 0 || t.objective > 4) return "unknown objective";
-  if (t.learned_backward) return "learned backward policy is not on the device path";
+  if (t.learned_backward != 0 && t.learned_backward != 1) return "learned_backward must be 0 or 1";
+  if (t.learned_backward && t.precision != GFNX_PREC_FP64_CHECK)
+    return "learned backward policy: fp64 check mode only (the bf16 paths use the uniform P_B)";
   if (t.objective == GFNX_OBJ_MDB && s.stop_action < 0)
     return "mdb objective needs the stop action index";
   if (t.objective == GFNX_OBJ_SUBTB && (t.subtb_lambda <= 0.0 || t.subtb_lambda > 1.0))

@@ -96,6 +96,26 @@ __host__ __device__ inline int bwd_pick(const EnvParams& P, const typename Env::
   }
 }
 
+// backward_action_mask entry ab at s (hypergrid.cpp:52-61, dag.cpp:433-443,
+// sequences.cpp:348-350, ising.cpp:104-107)
+template <class Env>
+__host__ __device__ inline bool bwd_legal(const EnvParams& P, const typename Env::State& s, int ab) {
+  if constexpr (std::is_same<Env, HypergridEnv>::value) {
+    if (s.term) return ab == P.stop;
+    return ab >= 0 && ab < P.hg_dim && s.c(ab) > 0;
+  } else if constexpr (std::is_same<Env, DagEnv>::value) {
+    if (s.term) return ab == P.stop;
+    if (ab < 0 || ab >= P.stop) return false;
+    int u, v;
+    DagEnv::edge(ab, P.dag_d, u, v);
+    return (s.adj.get(u) >> v) & 1;
+  } else if constexpr (std::is_same<Env, BitseqEnv>::value) {
+    return ab >= 0 && ab < P.bs_slots && ((s.filled >> ab) & 1);
+  } else {
+    return ab >= 0 && ab < P.is_D && ((s.asg[ab >> 5] >> (ab & 31)) & 1);
+  }
+}
+
 // one backward step s -> s' under backward action ab; returns the forward action s' -> s
 template <class Env>
 __host__ __device__ inline int bwd_apply(const EnvParams& P, typename Env::State& s, int ab) {
