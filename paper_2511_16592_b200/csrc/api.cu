@@ -831,7 +831,6 @@ gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* h, const uint32_t* terminals, int
                                      const uint64_t* keys, double* out) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (c.train.learned_backward) fail(GFNX_ERR_CONFIG, "backward walks use the uniform P_B (learned_backward = 0)");
     if (!terminals || !keys || !out) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: null buffer");
     if (n < 1 || num_samples < 1) fail(GFNX_ERR_CONFIG, "mc terminal log-prob: empty batch");
     uint32_t* d_t = nullptr;
@@ -854,7 +853,6 @@ gfnx_status gfnx_mc_terminal_logprob(gfnx_ctx* h, const uint32_t* terminals, int
 gfnx_status gfnx_pearson(gfnx_ctx* h, int64_t step, int32_t mc_samples, uint64_t test_seed, double* out) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (c.train.learned_backward) fail(GFNX_ERR_CONFIG, "backward walks use the uniform P_B (learned_backward = 0)");
     if (!out) fail(GFNX_ERR_CONFIG, "pearson: null buffer");
     if (mc_samples < 1) fail(GFNX_ERR_CONFIG, "pearson: mc_samples must be >= 1");
     double* d = nullptr;
@@ -941,7 +939,6 @@ gfnx_status gfnx_backward_rollout(gfnx_ctx* h, const uint32_t* terminals, int64_
                                   uint64_t key_lo) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (c.train.learned_backward) fail(GFNX_ERR_CONFIG, "backward walks use the uniform P_B (learned_backward = 0)");
     if (!terminals) fail(GFNX_ERR_CONFIG, "backward_rollout: null buffer");
     if (n != c.Bl) fail(GFNX_ERR_CONFIG, "backward_rollout: n must equal the local batch (gfnx_batch_dims)");
     uint32_t* d_t = nullptr;

@@ -695,6 +695,112 @@ void check_adam(Ctx& c, double lr) {
 }
 
 namespace {
+// backward_rollout with the learned backward policy (env_core.hpp:331-359, learned branch):
+// one block per walk, the bwd head's logits at the current state (fp64, reference order),
+// eps_uniform(bwd_logits, backward mask, Ab, 0.0) then categorical(fold_in(step_key, b));
+// walk j <-> global walk g = min(j0 + j, N - 1), terminal g / K, draw as k_bwd_walk's
+template <class Env>
+__global__ void k_check_bwd_walk(EnvParams P, DevLayout Db, const double* __restrict__ params,
+                                 const uint32_t* __restrict__ terms, int n_walks, int64_t j0, int64_t N, int K,
+                                 const uint64_t* __restrict__ keys, Key key, int64_t draw_base, int T,
+                                 int16_t* __restrict__ act, uint16_t* __restrict__ np, int32_t* __restrict__ len,
+                                 double* obs_scratch, double* logit_scratch, int32_t* err) {
+  const int j = blockIdx.x;
+  if (j >= n_walks) return;
+  __shared__ typename Env::State s;
+  __shared__ double hbuf[2][512];
+  __shared__ int s_L, s_bad;
+  const int Ab = P.Ab;
+  double* obs = obs_scratch + (size_t)j * P.O;
+  double* w = logit_scratch + (size_t)j * Ab;
+  const int64_t g = j0 + j < N ? j0 + j : N - 1;
+  const int64_t i = g / K;
+  const Key base = keys ? Key{keys[2 * (size_t)i], keys[2 * (size_t)i + 1]} : key;
+  const uint64_t draw = keys ? (uint64_t)(g % K) : (uint64_t)(draw_base + g);
+  int16_t* a_out = act + (size_t)j * T;
+  uint16_t* n_out = np + (size_t)j * T;
+  if (threadIdx.x == 0) {
+    unpack_terminal<Env>(P, terms + (size_t)i * P.SW, s);
+    s_bad = terminal_ok<Env>(P, s) ? 0 : GFNX_ERR_CONTRACT;
+    s_L = s_bad ? 0 : walk_length<Env>(P, s);
+    len[j] = s_L;
+    for (int t = s_L; t < T; ++t) {
+      a_out[t] = -1;
+      n_out[t] = 0;
+    }
+  }
+  __syncthreads();
+  const int L = s_L;
+  for (int t = 0; t < L; ++t) {
+    for (int q = threadIdx.x; q < P.O; q += blockDim.x) obs[q] = 0.0;
+    __syncthreads();
+    if (threadIdx.x == 0) Env::features(P, s, [&](int f, double v) { obs[f] = v; });
+    __syncthreads();
+    const double* h = obs;
+    int in = P.O;
+    for (int l = 0; l < Db.n_trunk; ++l) {
+      double* z = hbuf[l & 1];
+      dense_block(h, in, params + Db.off_w[l], params + Db.off_b[l], Db.dims[l + 1], z, true);
+      __syncthreads();
+      h = z;
+      in = Db.dims[l + 1];
+    }
+    dense_block(h, in, params + Db.off_fw, params + Db.off_fb, Ab, w, false);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int legal = 0;  // eps_uniform(bwd_logits, mask, ab, 0.0) (objectives.cpp:242-264)
+      double hi = -INFINITY;
+      for (int c = 0; c < Ab; ++c)
+        if (bwd_legal<Env>(P, s, c)) {
+          ++legal;
+          if (w[c] > hi) hi = w[c];
+        }
+      if (legal == 0 || !isfinite(hi)) {
+        s_bad = legal == 0 ? GFNX_ERR_CONTRACT : GFNX_ERR_NUMERIC;
+      } else {
+        double z = 0.0;
+        for (int c = 0; c < Ab; ++c) {
+          if (bwd_legal<Env>(P, s, c)) {
+            const double p = exp(w[c] - hi);
+            w[c] = p;
+            z += p;
+          } else {
+            w[c] = 0.0;
+          }
+        }
+        const double u = 0.0 / legal;
+        double total = 0.0;
+        for (int c = 0; c < Ab; ++c) {
+          if (bwd_legal<Env>(P, s, c)) w[c] = (1.0 - 0.0) * w[c] / z + u;
+          total += w[c];
+        }
+        const double uu = uniform_scalar(fold_in(fold_in(base, (uint64_t)t), draw)) * total;
+        int ab = -1;
+        double acc = 0.0;
+        for (int c = 0; c < Ab; ++c) {
+          acc += w[c];
+          if (uu < acc) {
+            ab = c;
+            break;
+          }
+        }
+        if (ab < 0)
+          for (int c = Ab - 1; c >= 0; --c)
+            if (w[c] > 0.0) {
+              ab = c;
+              break;
+            }
+        const int f = L - 1 - t;
+        n_out[f] = (uint16_t)legal;
+        a_out[f] = (int16_t)bwd_apply<Env>(P, s, ab);
+      }
+    }
+    __syncthreads();
+    if (s_bad) break;
+  }
+  if (threadIdx.x == 0 && s_bad) atomicExch(err, s_bad);
+}
+
 __global__ void k_check_row_logpf(DeviceBatch batch, const double* __restrict__ logp, int A, int Bl, int T,
                                   double* out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -703,6 +809,53 @@ __global__ void k_check_row_logpf(DeviceBatch batch, const double* __restrict__ 
   out[i] = t < batch.lengths[b] ? logp[(size_t)(batch.row0[b] + t) * A + batch.actions[i]] : 0.0;
 }
 }  // namespace
+
+void check_bwd_walk(Ctx& c, const uint32_t* d_terms, int n_walks, int64_t j0, int64_t N, int K,
+                    const uint64_t* d_keys, Key key, int64_t draw_base, int16_t* d_act, uint16_t* d_np,
+                    int32_t* d_len) {
+  if (n_walks <= 0) return;
+  double *obs = nullptr, *logit = nullptr;
+  cuda_check(cudaMallocAsync(&obs, sizeof(double) * (size_t)n_walks * c.P.O, c.stream), "bwd walk");
+  cuda_check(cudaMallocAsync(&logit, sizeof(double) * (size_t)n_walks * c.P.Ab, c.stream), "bwd walk");
+  const DevLayout Db = bwd_layout(c);
+  auto go = [&](auto e) {
+    using Env = decltype(e);
+    k_check_bwd_walk<Env><<<n_walks, 256, 0, c.stream>>>(c.P, Db, c.p64, d_terms, n_walks, j0, N, K, d_keys, key,
+                                                          draw_base, c.P.T, d_act, d_np, d_len, obs, logit,
+                                                          c.batch.counters + 3);
+  };
+  switch (c.env.kind) {
+    case GFNX_ENV_HYPERGRID: go(HypergridEnv{}); break;
+    case GFNX_ENV_BITSEQ: go(BitseqEnv{}); break;
+    case GFNX_ENV_ISING: go(IsingEnv{}); break;
+    case GFNX_ENV_DAG: go(DagEnv{}); break;
+  }
+  c.launches++;
+  cudaFreeAsync(obs, c.stream);
+  cudaFreeAsync(logit, c.stream);
+}
+
+namespace {
+// per-row learned log P_B of the last check_forward, (b, t) order (0 past each end)
+__global__ void k_check_row_logpb(DeviceBatch batch, const double* __restrict__ blogp,
+                                  const int32_t* __restrict__ bidx, int Ab, int Bl, int T, double* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= Bl * T) return;
+  const int b = i / T, t = i % T;
+  if (t >= batch.lengths[b]) {
+    out[i] = 0.0;
+    return;
+  }
+  const int64_t r = batch.row0[b] + t;
+  out[i] = blogp[r * Ab + bidx[r]];
+}
+}  // namespace
+
+void check_row_logpb(Ctx& c, double* out) {
+  const int n = c.Bl * c.P.T;
+  k_check_row_logpb<<<(n + 255) / 256, 256, 0, c.stream>>>(c.batch, c.ck_blogp, c.ck_bidx, c.P.Ab, c.Bl, c.P.T, out);
+  c.launches++;
+}
 
 void check_row_logpf(Ctx& c, double* out) {
   const int n = c.Bl * c.P.T;

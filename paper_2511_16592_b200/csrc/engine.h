@@ -53,6 +53,11 @@ void group_allreduce(Ctx& c, void* buf, size_t n, int dtype);
 // forced: [Bl * T] actions of a teacher-forced batch (rollout_from_actions), or null to sample
 void check_rollout(Ctx& c, Key key, double eps, const int16_t* forced = nullptr);
 void check_forward(Ctx& c);  // per-row log-softmax of the resident batch (check_row_logpf reads it)
+// learned backward policy (check mode): walks sampled from the bwd head, per-row log P_B
+void check_bwd_walk(Ctx& c, const uint32_t* d_terms, int n_walks, int64_t j0, int64_t N, int K,
+                    const uint64_t* d_keys, Key key, int64_t draw_base, int16_t* d_act, uint16_t* d_np,
+                    int32_t* d_len);
+void check_row_logpb(Ctx& c, double* out);
 void check_train(Ctx& c, bool apply, double lr, double* loss);
 void check_adam(Ctx& c, double lr);
 

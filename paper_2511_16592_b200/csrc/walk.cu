@@ -114,16 +114,17 @@ __global__ void k_replay(EnvParams P, const int16_t* __restrict__ forced, int Bl
 }
 
 // per walk j of a chunk: log P_F(tau) - log P_B(tau | x), both summed in forward order
-// (score_trajectories objectives.cpp:294-316 over the row log-probabilities [n][T])
-__global__ void k_mc_terms(const double* __restrict__ row_logpf, const uint16_t* __restrict__ np,
-                           const int32_t* __restrict__ len, const double* __restrict__ neglog, int n, int T,
-                           double* __restrict__ out) {
+// (score_trajectories objectives.cpp:294-316 over the row log-probabilities [n][T]); log P_B
+// is the uniform -log(#parents) or, with the learned backward policy, row_logpb
+__global__ void k_mc_terms(const double* __restrict__ row_logpf, const double* __restrict__ row_logpb,
+                           const uint16_t* __restrict__ np, const int32_t* __restrict__ len,
+                           const double* __restrict__ neglog, int n, int T, double* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= n) return;
   double lpf = 0.0, lpb = 0.0;
   for (int t = 0; t < len[j]; ++t) {
     lpf += row_logpf[(size_t)j * T + t];
-    lpb += neglog[np[(size_t)j * T + t]];
+    lpb += row_logpb ? row_logpb[(size_t)j * T + t] : neglog[np[(size_t)j * T + t]];
   }
   out[j] = lpf - lpb;
 }
@@ -287,6 +288,10 @@ void launch_bwd_walk(Ctx& c, const uint32_t* d_terms, int n_walks, int64_t j0, i
                      const uint64_t* d_keys, Key key, int64_t draw_base, int16_t* d_act, uint16_t* d_np,
                      int32_t* d_len, uint32_t* d_stst) {
   if (n_walks <= 0) return;
+  if (c.train.learned_backward) {  // walks sampled from the policy's backward head (check mode)
+    check_bwd_walk(c, d_terms, n_walks, j0, N, K, d_keys, key, draw_base, d_act, d_np, d_len);
+    return;
+  }
   env_dispatch(c, [&](auto e) {
     using Env = decltype(e);
     k_bwd_walk<Env><<<(n_walks + 127) / 128, 128, 0, c.stream>>>(c.P, d_terms, n_walks, j0, N, K, d_keys, key,
@@ -371,6 +376,9 @@ void mc_terminal_logprob_chunked(Ctx& c, const uint32_t* d_terms, int64_t n, int
   cuda_check(cudaMallocAsync(&d_np, sizeof(uint16_t) * (size_t)Bl * T, c.stream), "mc");
   cuda_check(cudaMallocAsync(&d_len, sizeof(int32_t) * (size_t)Bl, c.stream), "mc");
   cuda_check(cudaMallocAsync(&d_row, sizeof(double) * (size_t)Bl * T, c.stream), "mc");
+  double* d_rowb = nullptr;  // learned backward policy: per-row log P_B of the bwd head
+  if (c.train.learned_backward)
+    cuda_check(cudaMallocAsync(&d_rowb, sizeof(double) * (size_t)Bl * T, c.stream), "mc");
   cuda_check(cudaMallocAsync(&d_terms_all, sizeof(double) * (size_t)((N + Bl - 1) / Bl) * Bl, c.stream), "mc");
   for (int64_t j0 = 0; j0 < N; j0 += Bl) {
     launch_bwd_walk(c, d_terms, Bl, j0, N, K, d_keys, Key{0, 0}, 0, d_act, d_np, d_len, nullptr);
@@ -380,15 +388,18 @@ void mc_terminal_logprob_chunked(Ctx& c, const uint32_t* d_terms, int64_t n, int
     if (c.check_mode()) {
       check_forward(c);
       check_row_logpf(c, d_row);
+      if (d_rowb) check_row_logpb(c, d_rowb);
     } else {
       fast_row_logpf(c, d_row);
     }
-    k_mc_terms<<<(Bl + 127) / 128, 128, 0, c.stream>>>(d_row, d_np, d_len, c.d_neglog, Bl, T, d_terms_all + j0);
+    k_mc_terms<<<(Bl + 127) / 128, 128, 0, c.stream>>>(d_row, d_rowb, d_np, d_len, c.d_neglog, Bl, T,
+                                                       d_terms_all + j0);
     c.launches++;
   }
   launch_mc_lse(c, d_terms_all, (int)n, K, d_out);
   for (void* p : {(void*)d_act, (void*)d_np, (void*)d_len, (void*)d_row, (void*)d_terms_all})
     cudaFreeAsync(p, c.stream);
+  if (d_rowb) cudaFreeAsync(d_rowb, c.stream);
   c.has_batch = false;  // the resident batch now holds the last chunk of walks
   c.has_grads = false;
 }

@@ -84,3 +84,33 @@ def test_learned_backward_rejected_on_bf16_paths():
     t.learned_backward = 1
     with pytest.raises(engine.config_error, match="learned backward"):
         engine.Trainer(e, t)
+
+
+@pytest.mark.parametrize("name,mk", [CASES[0], CASES[3], CASES[4], CASES[5]])
+def test_learned_backward_walks_and_mc_match_reference(name, mk):
+    """backward_rollout sampling from the learned backward head (env_core.hpp:331-359) and
+    mc_terminal_logprob scored with it (exact.hpp:229-241, score_trajectories learned branch),
+    against the reference on the same parameters and keys."""
+    if not O.ref_available("port"):
+        pytest.skip("oracle/_ref not built")
+    e, t = mk()
+    t.learned_backward = 1
+    t.precision = abi.PREC_FP64_CHECK
+    d = engine.Trainer(e, t)
+    ref = O.RefLib(e, t)
+    d.run(0, 5)  # a non-uniform backward head
+    ref.set_params(*d.params())
+    d.forward_rollout(7, 1.0)
+    terms = d.batch(("terminal_state",))["terminal_state"].copy()
+    key = (0xABCDEF, 0x12345)
+    d.backward_rollout(terms, key)
+    ref.backward_rollout(terms, key)
+    bd, br = d.batch(), ref.batch(d.T)
+    for k in ("lengths", "fwd_actions", "log_rewards", "log_pb"):
+        assert np.array_equal(bd[k], br[k]), (name, k)
+    rng = np.random.default_rng(1)
+    keys = rng.integers(0, 2**63, size=(len(terms), 2), dtype=np.uint64)
+    dev = d.mc_terminal_logprob(terms, keys, 4)
+    want = np.array([ref.mc_logprob(terms[i], keys[i], 4) for i in range(len(terms))])
+    assert np.max(np.abs(dev - want)) <= 1e-9 * max(1.0, np.max(np.abs(want))), np.max(np.abs(dev - want))
+    d.close()
