@@ -138,8 +138,9 @@ __global__ void k_eb_pick(Key it_key, int db, int N, const uint32_t* __restrict_
 }
 
 // policy logits of state s into w[A] (mlp_forward, nn.cpp:60-89; every thread of the block)
+// (Dl = the bwd-head layout with nout = Ab for the learned backward policy)
 __device__ void policy_logits(const EnvParams& P, const DevLayout& Dl, const double* params, const IsingEnv::State& s,
-                              double* obs, double (*hbuf)[512], double* w) {
+                              double* obs, double (*hbuf)[512], double* w, int nout) {
   for (int i = threadIdx.x; i < P.O; i += blockDim.x) obs[i] = 0.0;
   __syncthreads();
   if (threadIdx.x == 0) IsingEnv::features(P, s, [&](int f, double v) { obs[f] = v; });
@@ -153,24 +154,26 @@ __device__ void policy_logits(const EnvParams& P, const DevLayout& Dl, const dou
     h = z;
     in = Dl.dims[l + 1];
   }
-  dense_block(h, in, params + Dl.off_fw, params + Dl.off_fb, P.A, w, false);
+  dense_block(h, in, params + Dl.off_fw, params + Dl.off_fb, nout, w, false);
   __syncthreads();
 }
 
 // eps_uniform(logits, action_mask, A, 0.0) (objectives.cpp:242-264) in place; false on a
 // non-finite maximum / no legal action (numeric_error / contract_violation)
-__device__ bool eps0_probs(const EnvParams& P, const IsingEnv::State& s, double* w) {
+__device__ bool eps0_probs(const EnvParams& P, const IsingEnv::State& s, double* w, bool bwd = false) {
+  const int n = bwd ? P.Ab : P.A;
+  auto ok = [&](int i) { return bwd ? (bool)((s.asg[i >> 5] >> (i & 31)) & 1u) : IsingEnv::legal(P, s, i); };
   int legal = 0;
   double hi = -INFINITY;
-  for (int i = 0; i < P.A; ++i)
-    if (IsingEnv::legal(P, s, i)) {
+  for (int i = 0; i < n; ++i)
+    if (ok(i)) {
       ++legal;
       if (w[i] > hi) hi = w[i];
     }
   if (legal == 0 || !isfinite(hi)) return false;
   double z = 0.0;
-  for (int i = 0; i < P.A; ++i) {
-    if (IsingEnv::legal(P, s, i)) {
+  for (int i = 0; i < n; ++i) {
+    if (ok(i)) {
       const double p = exp(w[i] - hi);
       w[i] = p;
       z += p;
@@ -179,8 +182,8 @@ __device__ bool eps0_probs(const EnvParams& P, const IsingEnv::State& s, double*
     }
   }
   const double u = 0.0 / legal;
-  for (int i = 0; i < P.A; ++i)
-    if (IsingEnv::legal(P, s, i)) w[i] = (1.0 - 0.0) * w[i] / z + u;
+  for (int i = 0; i < n; ++i)
+    if (ok(i)) w[i] = (1.0 - 0.0) * w[i] / z + u;
   return true;
 }
 
@@ -208,7 +211,7 @@ __device__ void unassign(IsingEnv::State& s, int site) {  // backward_step_insta
 
 __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ params, Key key, int k,
                          const uint32_t* __restrict__ xs, uint32_t* __restrict__ props, double* __restrict__ logratio,
-                         double* obs_scratch, double* logit_scratch, int32_t* err) {
+                         double* obs_scratch, double* logit_scratch, int32_t* err, int learned, DevLayout Db) {
   const int b = blockIdx.x;
   const int D = P.is_D, half = P.SW / 2;
   __shared__ IsingEnv::State s, partial;
@@ -216,7 +219,7 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
   __shared__ int16_t removed[kMaxIsingD], added[kMaxIsingD];
   __shared__ int bad;
   double* obs = obs_scratch + (size_t)b * P.O;
-  double* w = logit_scratch + (size_t)b * P.A;
+  double* w = logit_scratch + (size_t)b * (P.A > P.Ab ? P.A : P.Ab);
   const uint32_t* x = xs + (size_t)b * P.SW;
   double lr = 0.0;  // thread 0
   if (threadIdx.x == 0) {
@@ -225,7 +228,7 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
     s.term = true;
     s.step = s.count;
     // phase 1: k backward steps under the uniform backward policy, - log P_B(tau | x)
-    for (int step = 0; step < k; ++step) {
+    for (int step = 0; step < k && !learned; ++step) {
       const int nl = s.count;
       const Key sk = fold_in(fold_in(key, 100), (uint64_t)step);
       int q = (int)(uniform_scalar(fold_in(sk, (uint64_t)b)) * (double)nl);
@@ -235,12 +238,46 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
       unassign(s, site);
       removed[step] = (int16_t)site;
     }
-    partial = s;
   }
+  __syncthreads();
+  for (int step = 0; step < k && learned; ++step) {  // phase 1 under the learned backward head
+    policy_logits(P, Db, params, s, obs, hbuf, w, P.Ab);
+    if (threadIdx.x == 0) {
+      if (!eps0_probs(P, s, w, true)) bad = GFNX_ERR_NUMERIC;
+      double total = 0.0;  // categorical (rng.cpp:87-100)
+      for (int i = 0; i < P.Ab; ++i) total += w[i];
+      const Key sk = fold_in(fold_in(key, 100), (uint64_t)step);
+      const double uu = uniform_scalar(fold_in(sk, (uint64_t)b)) * total;
+      int site = -1;
+      double acc = 0.0;
+      for (int i = 0; i < P.Ab; ++i) {
+        acc += w[i];
+        if (uu < acc) {
+          site = i;
+          break;
+        }
+      }
+      if (site < 0)
+        for (int i = P.Ab - 1; i >= 0; --i)
+          if (w[i] > 0.0) {
+            site = i;
+            break;
+          }
+      if (site < 0) {
+        bad = GFNX_ERR_CONTRACT;
+        site = nth_assigned(s, D, 0);
+      }
+      lr -= log(w[site] / total);
+      unassign(s, site);
+      removed[step] = (int16_t)site;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) partial = s;
   __syncthreads();
   // phase 2: forward replay of tau from the partial state, + log P_F(tau)
   for (int step = 0; step < k; ++step) {
-    policy_logits(P, Dl, params, s, obs, hbuf, w);
+    policy_logits(P, Dl, params, s, obs, hbuf, w, P.A);
     if (threadIdx.x == 0) {
       if (!eps0_probs(P, s, w)) bad = GFNX_ERR_NUMERIC;
       const int site = removed[k - 1 - step];
@@ -254,7 +291,7 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
   if (threadIdx.x == 0) s = partial;
   __syncthreads();
   for (int step = 0; step < k; ++step) {
-    policy_logits(P, Dl, params, s, obs, hbuf, w);
+    policy_logits(P, Dl, params, s, obs, hbuf, w, P.A);
     if (threadIdx.x == 0) {
       if (!eps0_probs(P, s, w)) bad = GFNX_ERR_NUMERIC;
       double total = 0.0;  // categorical (rng.cpp:87-100)
@@ -289,10 +326,23 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
   if (threadIdx.x == 0) {
     IsingEnv::pack(P, s, props + (size_t)b * P.SW);
     // phase 4: the uniform backward score of tau' from x', + log P_B(tau' | x')
-    for (int step = 0; step < k; ++step) {
+    for (int step = 0; step < k && !learned; ++step) {
       lr += -log((double)s.count);
       unassign(s, added[k - 1 - step]);
     }
+  }
+  __syncthreads();
+  for (int step = 0; step < k && learned; ++step) {  // phase 4 under the learned backward head
+    policy_logits(P, Db, params, s, obs, hbuf, w, P.Ab);
+    if (threadIdx.x == 0) {
+      if (!eps0_probs(P, s, w, true)) bad = GFNX_ERR_NUMERIC;
+      const int site = added[k - 1 - step];
+      lr += log(w[site]);
+      unassign(s, site);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     logratio[b] = lr;
     if (bad) atomicExch(err, bad);
   }
@@ -406,7 +456,6 @@ void eb_init(Ctx& c, const gfnx_eb_desc& d, const int8_t* data, int64_t n) {
   if (c.env.kind != GFNX_ENV_ISING) raise_error(GFNX_ERR_CONFIG, "eb-gfn: Ising env only");
   if (c.train.objective != GFNX_OBJ_TB) raise_error(GFNX_ERR_CONFIG, "eb-gfn: the sampler objective must be tb");
   if (c.world != 1) raise_error(GFNX_ERR_CONFIG, "eb-gfn: single-rank loop");
-  if (c.train.learned_backward) raise_error(GFNX_ERR_CONFIG, "eb-gfn: uniform backward policy only on the device");
   const int D = c.P.is_D;
   if (d.k > D) raise_error(GFNX_ERR_CONFIG, "back_and_forth: k must lie in [0, D]");
   if (!(d.alpha >= 0.0 && d.alpha <= 1.0)) raise_error(GFNX_ERR_CONFIG, "eb-gfn: alpha must lie in [0, 1]");
@@ -457,7 +506,7 @@ void eb_init(Ctx& c, const gfnx_eb_desc& d, const int8_t* data, int64_t n) {
   alloc(&e->logratio, sizeof(double) * db);
   alloc(&e->take, sizeof(int32_t) * db);
   alloc(&e->obs, sizeof(double) * (size_t)db * c.P.O);
-  alloc(&e->logit, sizeof(double) * (size_t)db * c.P.A);
+  alloc(&e->logit, sizeof(double) * (size_t)db * std::max(c.P.A, c.P.Ab));
   if (!c.check_mode()) alloc(&e->p64, sizeof(double) * c.L.n_params);
   cuda_check(cudaMemcpy(e->data, packed.data(), sizeof(uint32_t) * packed.size(), cudaMemcpyHostToDevice), "eb data");
   cuda_check(cudaMemcpy(e->Jt, jt.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice), "eb J*");
@@ -497,9 +546,13 @@ void eb_post(Ctx& c, Key it_key, double j_lr, int64_t i) {
     params = e.p64;
   }
   const DevLayout Dl = make_dev_layout(c);
+  DevLayout Db = Dl;  // the learned backward head (LossConfig::learned_backward)
+  Db.off_fw = c.L.off_bw;
+  Db.off_fb = c.L.off_bb;
+  Db.A = c.P.Ab;
   k_eb_pick<<<(e.db + 127) / 128, 128, 0, c.stream>>>(it_key, e.db, e.N, e.data, e.SW, e.xs);
   k_eb_bnf<<<e.db, 256, 0, c.stream>>>(c.P, Dl, params, fold_in(it_key, 6), e.k, e.xs, e.props, e.logratio, e.obs,
-                                       e.logit, c.batch.counters + 3);
+                                       e.logit, c.batch.counters + 3, c.train.learned_backward, Db);
   k_eb_mh<<<(e.db + 127) / 128, 128, 0, c.stream>>>(it_key, e.db, c.P, e.Jm, e.xs, e.props, e.logratio, e.acc,
                                                     e.take);
   k_eb_cd<<<1, 1024, 0, c.stream>>>(e.db, c.P, e.xs, e.acc, e.take, e.Jm, e.Jt, e.grad, j_lr, c.d_scalars,

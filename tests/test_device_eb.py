@@ -23,24 +23,28 @@ from paper_2511_16592_b200 import abi, engine
 pytestmark = pytest.mark.gpu
 
 
-def _ctx(side, sigma, batch, hidden, iterations, seed, check=True):
+def _ctx(side, sigma, batch, hidden, iterations, seed, check=True, learned=0):
     e = abi.env_desc(abi.ISING, is_side=side, is_sigma=sigma)
     t = abi.train_desc(abi.ISING, batch=batch, hidden=hidden, iterations=iterations, seed=seed)
+    t.learned_backward = learned
     if check:
         t.precision = abi.PREC_FP64_CHECK
     return engine.Trainer(e, t)
 
 
-def test_eb_check_mode_matches_reference_run():
-    """test_config_train.cpp:344-361's configuration (k = 4, data batch 16) on the device."""
+@pytest.mark.parametrize("learned", [0, 1])
+def test_eb_check_mode_matches_reference_run(learned):
+    """test_config_train.cpp:344-361's configuration (k = 4, data batch 16) on the device; with
+    learned = 1 the sampler's learned backward head drives the data walks, the training log P_B
+    and the back-and-forth proposals (objective.learned_backward)."""
     if not O.ref_available("port"):
         pytest.skip("oracle/_ref not built")
     kv = {"env.side": 2, "env.sigma": 0.3, "env.data_samples": 100, "gibbs.burn_in": 100,
           "train.iterations": 30, "train.batch_size": 8, "mlp.hidden": "16", "eval.interval": 10,
-          "eb.k": 4, "eb.data_batch": 16}
+          "eb.k": 4, "eb.data_batch": 16, "objective.learned_backward": "true" if learned else "false"}
     out = tempfile.mkdtemp(prefix="ebref_")
     res, J_ref, rows = O.ref_eb_gfn(kv, out)
-    tr = _ctx(2, 0.3, 8, (16,), 30, 0)
+    tr = _ctx(2, 0.3, 8, (16,), 30, 0, learned=learned)
     tr.eb_init(engine.eb_desc(data_samples=100, gibbs_burn_in=100, k=4, data_batch=16))
     m = tr.eb_run(0, 30)
     jm, jt, init_nlr = tr.eb_coupling()
