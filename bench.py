@@ -41,6 +41,7 @@ UNIT = "trajectories/s"
 SECONDARY = {
     "hypergrid_subtb_b65536": dict(batch=65536, desc="hypergrid 20^4 SubTB (lambda 0.9), B=65536, MLP 2x256"),
     "bitseq_tb_b16384": dict(batch=16384, desc="bitseq n=120 k=8 NAR TB, MLP 2x256"),
+    "bitseq_ar_tb_b16384": dict(batch=16384, desc="bitseq n=120 k=8 autoregressive (fixed) TB, MLP 2x256"),
     "ising_tb_b32768": dict(batch=32768, desc="Ising 10x10 TB, MLP 4x256"),
     "hypergrid_tb_b16": dict(batch=16, desc="hypergrid 20^4 TB, B=16, MLP 2x256"),
     "dag_mdb_b8192": dict(batch=8192, desc="DAG d=5 BGe MDB, MLP 2x128"),
@@ -350,8 +351,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-steady", action="store_true", help="skip the converged-checkpoint leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the reward-kernel B sweep")
-    ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,ising_tb_b32768,hypergrid_tb_b16,"
-                                           "dag_mdb_b8192,hypergrid_db_b65536_det",
+    ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,bitseq_ar_tb_b16384,"
+                                           "ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192,hypergrid_db_b65536_det",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()

@@ -85,7 +85,7 @@ typedef struct gfnx_env_desc {
   int32_t bs_k;
   double bs_beta;
   int32_t bs_num_modes;
-  int32_t pad1_;
+  int32_t bs_scheme;   /* SeqScheme: 0 non-autoregressive (build_bitseq), 1 autoregressive fixed */
   uint64_t bs_modes_seed;
   /* ising (build_ising, train.cpp:637-657): toroidal coupling sigma * A_N */
   int32_t is_side;

@@ -575,9 +575,9 @@ static double env_step(const orc_trainer* tr, orc_state* s, int a) {
       }
       s->v[a] += 1;
       return 0.0;
-    case GFNX_ENV_BITSEQ: { /* sequences.cpp:257-267 (non-autoregressive) */
-      const int pos = a / tr->bs_vocab;
-      s->v[pos] = a % tr->bs_vocab;
+    case GFNX_ENV_BITSEQ: { /* sequences.cpp:236-267: non-autoregressive or AR fixed */
+      const int pos = tr->env.bs_scheme ? s->count : a / tr->bs_vocab;
+      s->v[pos] = tr->env.bs_scheme ? a : a % tr->bs_vocab;
       s->count += 1;
       if (s->count == tr->bs_slots) {
         s->is_terminal = 1;
@@ -621,7 +621,11 @@ static void env_action_mask(const orc_trainer* tr, const orc_state* s, uint8_t* 
       for (int i = 0; i < tr->env.hg_dim; ++i) out[i] = s->v[i] < tr->env.hg_side - 1;
       out[tr->stop] = 1;
       break;
-    case GFNX_ENV_BITSEQ: /* sequences.cpp:321-325 */
+    case GFNX_ENV_BITSEQ: /* sequences.cpp:302-327 */
+      if (tr->env.bs_scheme) {
+        if (!s->is_terminal) memset(out, 1, tr->bs_vocab);
+        break;
+      }
       for (int p = 0; p < tr->bs_slots; ++p)
         if (s->v[p] < 0) memset(out + p * tr->bs_vocab, 1, tr->bs_vocab);
       break;
@@ -656,7 +660,8 @@ static int env_num_parents(const orc_trainer* tr, const orc_state* s) {
       for (int i = 0; i < tr->env.hg_dim; ++i) c += s->v[i] > 0;
       return c;
     }
-    case GFNX_ENV_BITSEQ: return s->count;  /* sequences.cpp:354-360 (NAR) */
+    case GFNX_ENV_BITSEQ: /* sequences.cpp:329-352: NAR filled slots, AR fixed remove-last */
+      return tr->env.bs_scheme ? (s->count > 0) : s->count;
     case GFNX_ENV_ISING: return s->count;   /* ising.cpp:104-107 */
     case GFNX_ENV_DAG: {                    /* dag.cpp:433-443 */
       if (s->is_terminal) return 1;
@@ -671,7 +676,7 @@ static int env_num_parents(const orc_trainer* tr, const orc_state* s) {
 static int env_backward_action(const orc_trainer* tr, int a) {
   switch (tr->env.kind) {
     case GFNX_ENV_HYPERGRID: return a;                   /* hypergrid.cpp:63-73 */
-    case GFNX_ENV_BITSEQ: return a / tr->bs_vocab;       /* sequences.cpp:368-373 */
+    case GFNX_ENV_BITSEQ: return tr->env.bs_scheme ? 0 : a / tr->bs_vocab; /* sequences.cpp:354-373 */
     case GFNX_ENV_ISING: return a / 2;                   /* ising.cpp:109-114 */
     case GFNX_ENV_DAG: return a;                         /* dag.cpp:445-455 */
   }
@@ -916,8 +921,12 @@ orc_trainer* orc_create(const gfnx_env_desc* env, const gfnx_train_desc* train, 
       tr->bs_slots = env->bs_n_bits / env->bs_k;
       tr->bs_vocab = 1 << env->bs_k;
       if (tr->bs_slots > ORC_MAX_SLOTS) rc = fail(tr, "bitseq: too many slots");
-      tr->A = tr->bs_slots * tr->bs_vocab;
-      tr->Ab = tr->bs_slots;
+      if (env->bs_scheme != 0 && env->bs_scheme != 1) {
+        rc = fail(tr, "bitseq: scheme must be 0 (non-autoregressive) or 1 (autoregressive fixed)");
+        break;
+      }
+      tr->A = env->bs_scheme ? tr->bs_vocab : tr->bs_slots * tr->bs_vocab;
+      tr->Ab = env->bs_scheme ? 1 : tr->bs_slots;
       tr->O = tr->bs_slots * (tr->bs_vocab + 1) + 1;
       tr->T = tr->bs_slots;
       tr->stop = -1;

@@ -280,7 +280,7 @@ std::unique_ptr<SessionBase> make_session_raw(const gfnx_env_desc& e, const gfnx
           e.bs_n_bits, e.bs_beta, e.bs_num_modes, fold_in(make_key(e.bs_modes_seed), 0x30DE)));
       modes->beta = e.bs_beta;
       SequenceEnv::Params p;
-      p.scheme = SeqScheme::kNonAutoregressive;
+      p.scheme = e.bs_scheme == 1 ? SeqScheme::kAutoregressiveFixed : SeqScheme::kNonAutoregressive;
       p.max_len = e.bs_n_bits / e.bs_k;
       p.vocab = 1 << e.bs_k;
       p.bit_block = e.bs_k;

@@ -35,7 +35,7 @@ class EnvDesc(C.Structure):
         ("hg_dim", C.c_int32), ("hg_side", C.c_int32), ("pad0_", C.c_int32),
         ("hg_r0", C.c_double), ("hg_r1", C.c_double), ("hg_r2", C.c_double),
         ("bs_n_bits", C.c_int32), ("bs_k", C.c_int32), ("bs_beta", C.c_double),
-        ("bs_num_modes", C.c_int32), ("pad1_", C.c_int32), ("bs_modes_seed", C.c_uint64),
+        ("bs_num_modes", C.c_int32), ("bs_scheme", C.c_int32), ("bs_modes_seed", C.c_uint64),
         ("is_side", C.c_int32), ("pad2_", C.c_int32), ("is_sigma", C.c_double),
         ("dag_d", C.c_int32), ("dag_score", C.c_int32),
         ("dag_alpha_mu", C.c_double), ("dag_alpha_w", C.c_double),
@@ -174,6 +174,9 @@ def config(name: str, **kw):
         t = train_desc(HYPERGRID, batch=65536, objective=name.split("_")[1])
     elif name == "bitseq_tb_b16384":      # config #3 (k=8 NAR; reference caps k at 6)
         e = env_desc(BITSEQ, bs_n_bits=120, bs_k=8)
+        t = train_desc(BITSEQ, batch=16384, objective="tb")
+    elif name == "bitseq_ar_tb_b16384":   # config #3 as written: k=8 autoregressive (fixed length)
+        e = env_desc(BITSEQ, bs_n_bits=120, bs_k=8, bs_scheme=1)
         t = train_desc(BITSEQ, batch=16384, objective="tb")
     elif name == "ising_tb_b32768":       # config #4
         e = env_desc(ISING, is_side=10, is_sigma=0.2)

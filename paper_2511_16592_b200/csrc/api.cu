@@ -426,6 +426,7 @@ gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     P.bs_nbits = env->bs_n_bits;
     P.bs_words = he.mode_words;
     P.n_modes = he.n_modes;
+    P.bs_ar = env->kind == GFNX_ENV_BITSEQ && env->bs_scheme == 1;
     P.is_D = he.is_D;
     P.dag_d = env->dag_d;
     auto up = [&](auto** dst, const auto& vec) {

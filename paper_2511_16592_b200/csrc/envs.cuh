@@ -37,6 +37,7 @@ struct EnvParams {
   double hg_logr[4];            // log(r0 + r1*p1 + r2*p2) for (p1, p2) in {0,1}^2, index p1 | 2 p2
   // bitseq (non-autoregressive, k-bit words)
   int bs_slots, bs_vocab, bs_k, bs_nbits, bs_words, n_modes;
+  int bs_ar;                    // SeqScheme::kAutoregressiveFixed: tokens appended left to right
   const uint64_t* modes;        // [n_modes][bs_words], string bit i -> word i/64, bit 63 - i%64
   const double* bs_logr;        // [n_bits + 1]: -beta * d / n_bits
   // ising
@@ -135,14 +136,17 @@ struct BitseqEnv {
     s.step = 0;
     s.term = false;
   }
+  // action_mask (sequences.cpp:302-327): NAR every word of every empty slot; AR fixed every
+  // token until terminal
   __host__ __device__ static bool legal(const EnvParams& P, const State& s, int a) {
     if (s.term) return false;
+    if (P.bs_ar) return a >= 0 && a < P.bs_vocab;
     return !((s.filled >> (a / P.bs_vocab)) & 1);
   }
-  __host__ __device__ static bool step(const EnvParams& P, State& s, int a) {
+  __host__ __device__ static bool step(const EnvParams& P, State& s, int a) {  // sequences.cpp:236-267
     s.step += 1;
-    const int pos = a / P.bs_vocab;
-    s.tok[pos] = (uint8_t)(a % P.bs_vocab);
+    const int pos = P.bs_ar ? s.count : a / P.bs_vocab;
+    s.tok[pos] = (uint8_t)(P.bs_ar ? a : a % P.bs_vocab);
     s.filled |= 1ull << pos;
     s.count += 1;
     if (s.count == P.bs_slots) {
@@ -151,8 +155,11 @@ struct BitseqEnv {
     }
     return false;
   }
-  __host__ __device__ static int num_parents(const EnvParams&, const State& s) { return s.count; }
-  __host__ __device__ static int backward_action(const EnvParams& P, int a) { return a / P.bs_vocab; }
+  // #legal backward actions (sequences.cpp:329-352): NAR the filled slots, AR remove-last
+  __host__ __device__ static int num_parents(const EnvParams& P, const State& s) {
+    return P.bs_ar ? (s.count > 0 ? 1 : 0) : s.count;
+  }
+  __host__ __device__ static int backward_action(const EnvParams& P, int a) { return P.bs_ar ? 0 : a / P.bs_vocab; }
   // min Hamming distance to the mode set (ModeSet::log_reward sequences.cpp:50-55)
   __host__ __device__ static int best_distance(const EnvParams& P, const State& s) {
     uint64_t bits[kMaxModeWords];
@@ -205,11 +212,12 @@ struct BitseqEnv {
       f(i * width + (((s.filled >> i) & 1) ? s.tok[i] : P.bs_vocab), 1.0);
     f(P.bs_slots * width, (double)s.count / P.bs_slots);
   }
+  // (AR: the action fills slot s.count of the state it is taken in)
   template <class F>
-  __host__ __device__ static void delta_features(const EnvParams& P, const State&, int a, F&& f) {
-    const int width = P.bs_vocab + 1, pos = a / P.bs_vocab;
+  __host__ __device__ static void delta_features(const EnvParams& P, const State& s, int a, F&& f) {
+    const int width = P.bs_vocab + 1, pos = P.bs_ar ? s.count : a / P.bs_vocab;
     f(pos * width + P.bs_vocab, -1.0f);
-    f(pos * width + a % P.bs_vocab, 1.0f);
+    f(pos * width + (P.bs_ar ? a : a % P.bs_vocab), 1.0f);
     f(P.bs_slots * width, 1.0f / (float)P.bs_slots);
   }
 };

@@ -271,14 +271,18 @@ std::string build_host_env(const gfnx_env_desc& e, HostEnv* out) {
       max_parents = e.hg_dim;
       break;
     }
-    case GFNX_ENV_BITSEQ: {  // build_bitseq (train.cpp:381-427), NAR scheme
+    case GFNX_ENV_BITSEQ: {  // build_bitseq (train.cpp:381-427): NAR, or the AR-fixed scheme
       if (e.bs_k < 1 || e.bs_k > 8 || e.bs_n_bits % e.bs_k != 0)
         return "bitseq: k must divide n_bits (1 <= k <= 8)";
+      if (e.bs_scheme != 0 && e.bs_scheme != 1)
+        return "bitseq: scheme must be 0 (non-autoregressive) or 1 (autoregressive fixed)";
       out->bs_slots = e.bs_n_bits / e.bs_k;
       out->bs_vocab = 1 << e.bs_k;
       if (out->bs_slots > kMaxSlots) return "bitseq: n_bits / k exceeds device cap (64 slots)";
-      s.num_actions = out->bs_slots * out->bs_vocab;
-      s.num_backward_actions = out->bs_slots;
+      // num_actions / num_backward_actions (sequences.cpp:200-218): NAR pos * vocab + word over
+      // every slot, one remove-per-slot backward action; AR fixed: the next token, remove-last
+      s.num_actions = e.bs_scheme ? out->bs_vocab : out->bs_slots * out->bs_vocab;
+      s.num_backward_actions = e.bs_scheme ? 1 : out->bs_slots;
       s.obs_dim = out->bs_slots * (out->bs_vocab + 1) + 1;
       s.max_traj_len = out->bs_slots;
       s.stop_action = -1;

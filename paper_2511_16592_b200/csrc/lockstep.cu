@@ -56,6 +56,7 @@ template <>
 struct Lock<BitseqEnv> {  // k = 8 (256-word slots), <= 32 slots
   GFNX_DEV static uint32_t legal32(const EnvParams& P, const uint32_t* w, int c0) {
     if (c0 >= P.A) return 0u;
+    if (P.bs_ar) return 0xffffffffu;  // AR fixed: every token (rows are never terminal here)
     const int tw = (P.bs_slots + 3) / 4;
     return ((w[tw] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
   }
@@ -66,6 +67,7 @@ struct Lock<BitseqEnv> {  // k = 8 (256-word slots), <= 32 slots
   }
   GFNX_DEV static uint32_t legal32c(const EnvParams& P, const uint32_t (&lw)[kLW], int c0) {
     if (c0 >= P.A) return 0u;
+    if (P.bs_ar) return 0xffffffffu;
     return ((lw[0] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
   }
   // features with index in [f0, f0 + 256): put(f - f0, value); `part` of 4 splits the work
@@ -202,6 +204,7 @@ __global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
     v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
     v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
     typename E::State dummy;
+    dummy.count = a.t - 1;  // the last action was taken with t - 1 filled slots (bitseq AR position)
     E::delta_features(a.P, dummy, a.last_act[b], [&](int f, float coef) {
       const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.w1 + (size_t)f * kH) + lane);
       const uint32_t x[4] = {q.x, q.y, q.z, q.w};
@@ -488,12 +491,13 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     if constexpr (std::is_same<E, BitseqEnv>::value) {
       // step in the packed domain (token byte + filled bit; sequences.cpp:257-267): no
       // per-token unpack / pack on the serial path, full state only at termination
-      const int pos = act / P.bs_vocab, tw = (P.bs_slots + 3) / 4, sh = 8 * (pos & 3);
-      cw[pos >> 2] = (w[pos >> 2] & ~(0xffu << sh)) | ((uint32_t)(act % P.bs_vocab) << sh);
+      const int tw = (P.bs_slots + 3) / 4;
+      const int pos = P.bs_ar ? __popc(w[tw]) : act / P.bs_vocab, sh = 8 * (pos & 3);  // AR: next slot
+      cw[pos >> 2] = (w[pos >> 2] & ~(0xffu << sh)) | ((uint32_t)(P.bs_ar ? act : act % P.bs_vocab) << sh);
       const uint32_t filled = w[tw] | (1u << pos);
       cw[tw] = filled;
-      nparents = __popc(filled);
-      term = nparents == P.bs_slots;
+      nparents = P.bs_ar ? 1 : __popc(filled);
+      term = __popc(filled) == P.bs_slots;
     } else {
       typename E::State s;
       E::unpack(P, w, s);
@@ -1663,7 +1667,8 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
   // the whole rollout in one persistent kernel when the head fits one MMA and every CTA
   // holds at most two trajectory tiles (GFNX_LS_STEPWISE=1 forces the per-step kernels)
   const int grid = std::min(f.num_sms, f.tilesB);
-  if (f.NT == 1 && Bl % kTile == 0 && f.tilesB <= kPersistMaxTiles * grid && T <= 256) {
+  if (std::is_same<E, IsingEnv>::value && f.NT == 1 && Bl % kTile == 0 && f.tilesB <= kPersistMaxTiles * grid &&
+      T <= 256) {
     PersistArgs pa{};
     pa.P = c.P;
     pa.key = key;

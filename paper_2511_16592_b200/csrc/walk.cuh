@@ -56,7 +56,7 @@ __host__ __device__ inline int bwd_count(const EnvParams& P, const typename Env:
     for (int u = 0; u < P.dag_d; ++u) n += popc32(s.adj.get(u));
     return n;
   } else if constexpr (std::is_same<Env, BitseqEnv>::value) {
-    return popc64(s.filled);
+    return P.bs_ar ? (s.count > 0 ? 1 : 0) : popc64(s.filled);
   } else {
     int n = 0;
     for (int w = 0; w < (P.is_D + 31) / 32; ++w) n += popc32(s.asg[w]);
@@ -85,7 +85,7 @@ __host__ __device__ inline int bwd_pick(const EnvParams& P, const typename Env::
     }
     return -1;
   } else if constexpr (std::is_same<Env, BitseqEnv>::value) {
-    return nth_bit64(s.filled, q);
+    return P.bs_ar ? 0 : nth_bit64(s.filled, q);
   } else {
     for (int w = 0; w < (P.is_D + 31) / 32; ++w) {
       const int n = popc32(s.asg[w]);
@@ -110,6 +110,7 @@ __host__ __device__ inline bool bwd_legal(const EnvParams& P, const typename Env
     DagEnv::edge(ab, P.dag_d, u, v);
     return (s.adj.get(u) >> v) & 1;
   } else if constexpr (std::is_same<Env, BitseqEnv>::value) {
+    if (P.bs_ar) return ab == 0 && s.count > 0;
     return ab >= 0 && ab < P.bs_slots && ((s.filled >> ab) & 1);
   } else {
     return ab >= 0 && ab < P.is_D && ((s.asg[ab >> 5] >> (ab & 31)) & 1);
@@ -143,12 +144,13 @@ __host__ __device__ inline int bwd_apply(const EnvParams& P, typename Env::State
     DagEnv::unpack(Q, w, s);  // closure_from_adjacency
     return ab;
   } else if constexpr (std::is_same<Env, BitseqEnv>::value) {
-    const int tok = s.tok[ab];
-    s.filled &= ~(1ull << ab);
-    s.tok[ab] = 0;
+    const int pos = P.bs_ar ? s.count - 1 : ab;  // AR: remove-last (get_forward_action = the token)
+    const int tok = s.tok[pos];
+    s.filled &= ~(1ull << pos);
+    s.tok[pos] = 0;
     s.count -= 1;
     s.term = false;
-    return ab * P.bs_vocab + tok;
+    return P.bs_ar ? tok : pos * P.bs_vocab + tok;
   } else {
     const uint32_t bit = 1u << (ab & 31);
     const int up = (s.up[ab >> 5] & bit) ? 1 : 0;

@@ -45,6 +45,11 @@ CASES = {
                          abi.train_desc(abi.BITSEQ, batch=16, objective="tb"), 2),
     "bitseq_n8k2_db_b16": (abi.env_desc(abi.BITSEQ, bs_n_bits=8, bs_k=2),
                            abi.train_desc(abi.BITSEQ, batch=16, objective="db"), 3),
+    # the autoregressive-fixed scheme (SeqScheme::kAutoregressiveFixed, sequences.cpp:236-352)
+    "bitseq_ar_k6_tb_b16": (abi.env_desc(abi.BITSEQ, bs_n_bits=120, bs_k=6, bs_scheme=1),
+                            abi.train_desc(abi.BITSEQ, batch=16, objective="tb"), 2),
+    "bitseq_ar_n16k4_subtb_b16": (abi.env_desc(abi.BITSEQ, bs_n_bits=16, bs_k=4, bs_scheme=1),
+                                  abi.train_desc(abi.BITSEQ, batch=16, objective="subtb"), 3),
     "ising_n10_tb_b8": (abi.env_desc(abi.ISING, is_side=10, is_sigma=0.2),
                         abi.train_desc(abi.ISING, batch=8, objective="tb"), 2),
     "ising_n3_subtb_b16": (abi.env_desc(abi.ISING, is_side=3, is_sigma=0.2),

@@ -37,8 +37,9 @@ pytestmark = pytest.mark.gpu
 FIELDS = ("lengths", "fwd_actions", "bwd_actions", "log_rewards", "log_pb", "delta", "terminal_state")
 
 
-def _bitseq(n_bits, batch, objective="tb"):
-    return abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8), abi.train_desc(abi.BITSEQ, batch=batch, objective=objective)
+def _bitseq(n_bits, batch, objective="tb", scheme=0):
+    return (abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8, bs_scheme=scheme),
+            abi.train_desc(abi.BITSEQ, batch=batch, objective=objective))
 
 
 def _ising(side, batch, objective="tb"):
@@ -55,6 +56,7 @@ BENCH_SIZES = [
     ("ising_b32768_two_tiles", lambda: _ising(10, 32768)),                    # k_ls_persist, 2 tiles / CTA
     ("ising_b38912_stepwise", lambda: _ising(10, 38912)),                     # > 296 tiles: per-step path
     ("bitseq_n120_b16384", lambda: _bitseq(120, 16384)),
+    ("bitseq_ar_n120_b16384", lambda: _bitseq(120, 16384, scheme=1)),  # config #3 as written (AR)
 ]
 
 
@@ -141,6 +143,9 @@ SAME_BATCH = [
     ("bitseq_n120_b128", lambda: _bitseq(120, 128), LS, True),
     ("ising_6x6_b256", lambda: _ising(6, 256), IS, True),
     ("ising_10x10_b128", lambda: _ising(10, 128), IS, True),
+    # the autoregressive-fixed bitseq scheme (A = 256: one head tile)
+    ("bitseq_ar_n120_b128", lambda: _bitseq(120, 128, scheme=1), LS, True),
+    ("bitseq_ar_n48_db_b200", lambda: _bitseq(48, 200, "db", scheme=1), LS, True),
     # lockstep DB / SubTB: the log-flow head as head column A (k_ls_loss_flow)
     ("bitseq_n48_db_b128", lambda: _bitseq(48, 128, "db"), LS, True),
     ("bitseq_n48_subtb_b128", lambda: _bitseq(48, 128, "subtb"), LS, True),

@@ -42,6 +42,12 @@ def _cfg(name, check):
     elif name == "bitseq_k8":
         e = abi.env_desc(abi.BITSEQ, bs_n_bits=48, bs_k=8)
         t = abi.train_desc(abi.BITSEQ, batch=128, objective="tb", seed=6)
+    elif name == "bitseq_ar_k6":
+        e = abi.env_desc(abi.BITSEQ, bs_n_bits=24, bs_k=6, bs_scheme=1)
+        t = abi.train_desc(abi.BITSEQ, batch=128, objective="tb", seed=6)
+    elif name == "bitseq_ar_k8":
+        e = abi.env_desc(abi.BITSEQ, bs_n_bits=48, bs_k=8, bs_scheme=1)
+        t = abi.train_desc(abi.BITSEQ, batch=128, objective="tb", seed=6)
     elif name == "ising":
         e = abi.env_desc(abi.ISING, is_side=4, is_sigma=0.2)
         t = abi.train_desc(abi.ISING, batch=128, objective="tb", seed=7, hidden=(256, 256))
@@ -59,7 +65,7 @@ def _terminals(tr, it=0, eps=1.0):
 
 
 REF_CASES = [("hypergrid", True), ("hypergrid", False), ("hypergrid_db", False), ("dag_mdb", True),
-             ("dag_mdb", False), ("bitseq_k6", True), ("ising", True), ("ising", False)]
+             ("dag_mdb", False), ("bitseq_k6", True), ("bitseq_ar_k6", True), ("ising", True), ("ising", False)]
 
 
 @pytest.mark.parametrize("name,check", REF_CASES)
@@ -88,9 +94,10 @@ def test_backward_rollout_bitexact_vs_reference(name, check):
     tr.close()
 
 
-def test_backward_rollout_bitseq_k8_matches_check_mode():
-    e, t = _cfg("bitseq_k8", False)
-    e2, t2 = _cfg("bitseq_k8", True)
+@pytest.mark.parametrize("name", ["bitseq_k8", "bitseq_ar_k8"])
+def test_backward_rollout_bitseq_k8_matches_check_mode(name):
+    e, t = _cfg(name, False)
+    e2, t2 = _cfg(name, True)
     fast, chk = engine.Trainer(e, t), engine.Trainer(e2, t2)
     chk.set_params(*fast.params())
     terms = _terminals(fast)
@@ -137,7 +144,8 @@ def test_rollout_from_actions_rejects_illegal():
 
 
 @pytest.mark.parametrize("name,check,tol", [("hypergrid", True, 1e-9), ("dag_mdb", True, 1e-9),
-                                            ("bitseq_k6", True, 1e-9), ("ising", True, 1e-9),
+                                            ("bitseq_k6", True, 1e-9), ("bitseq_ar_k6", True, 1e-9),
+                                            ("ising", True, 1e-9),
                                             ("ising", False, 5e-2)])
 def test_mc_terminal_logprob_all_envs(name, check, tol):
     if not O.ref_available("port"):
