@@ -163,8 +163,13 @@ __global__ void k_det_tiles(const int32_t* __restrict__ used, int nctas, int mt,
     for (int i = 0; i < used[k]; ++i) list[off[k] + i] = k * mt + i;
 }
 
-// logical training tile i -> emission tile (identity unless the deterministic list is set)
-GFNX_DEV int phys_tile(const int32_t* list, int i) { return list ? list[i] : i; }
+// logical training tile i -> emission tile: the deterministic mode's list (LIST instantiations
+// only, so the default kernels carry no list code), else the identity
+template <bool LIST>
+GFNX_DEV int phys_tile(const int32_t* list, int i) {
+  if constexpr (LIST) return list[i];
+  return i;
+}
 
 __global__ void k_rollout_reset(int32_t* tilectr, int32_t* counters, int32_t* work) {
   if (threadIdx.x == 0) {
@@ -380,7 +385,7 @@ constexpr int rollout_smem_fixed() {
   return H * H * 2 + NH * H * 2 + kTile * rollout_acols<H>() * 2 + 1024;
 }
 
-template <class Env, int H, int NH, bool W1S>
+template <class Env, int H, int NH, bool W1S, bool DET>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -419,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     mbar_init(&mbar, 1);
     fence_mbar_init();
     smax = 0;
-    const int t0 = a.det ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
+    const int t0 = DET ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
     for (int q = 0; q < 4; ++q) s_pq[q] = 0;
     s_cur0 = t0;
     s_next = t0 + 1;
@@ -512,12 +517,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   int bnext = 0;
   // deterministic mode: a static trajectory range [beg, bend) per CTA, slot row r starts
   // with beg + r, finished rows refill in row order (ballot ranks), no work stealing
-  const int beg = a.det ? (int)blockIdx.x * a.per : 0;
-  const int bend = a.det ? min(a.Bl, beg + a.per) : a.Bl;
+  const int beg = DET ? (int)blockIdx.x * a.per : 0;
+  const int bend = DET ? min(a.Bl, beg + a.per) : a.Bl;
   int dbase = beg + kTile;
   unsigned pm_prev = 0u;
   if (half == 0) {
-    b = a.det ? beg + row : atomicAdd(a.work, 1);
+    b = DET ? beg + row : atomicAdd(a.work, 1);
     active = b < bend;
     row_init[row] = 1;
     row_nd[row] = 0;
@@ -615,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     tmem_wait_st();
-    if (a.det) {  // refill ranks: finished rows of the last step in row order
+    if constexpr (DET) {  // refill ranks: finished rows of the last step in row order
       const int tot = s_pq[0] + s_pq[1] + s_pq[2] + s_pq[3];
       if (pending) {
         int rank = __popc(pm_prev & ((1u << lane) - 1u));
@@ -663,7 +668,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
       // the next tile is claimed now; s_next is rewritten in this round's sample phase,
       // after every thread has read it above
-      if (crossed && tid == kThreads - 1) claim = a.det ? nclaim++ : atomicAdd(a.tilectr, 1);
+      if (crossed && tid == kThreads - 1) claim = DET ? nclaim++ : atomicAdd(a.tilectr, 1);
     }
     // copy the 64 staged columns [half*64, half*64+64) of the A tile (logical columns
     // col0 + ...) of this warp's 32 rows into their emission tile images + ReLU masks,
@@ -770,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
-          if (!a.det) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          if constexpr (!DET) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
           atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
@@ -799,7 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
       }
     }
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
-    if (a.det) {  // this step's finished rows, ranked at the next refill
+    if constexpr (DET) {  // this step's finished rows, ranked at the next refill
       pm_prev = __ballot_sync(0xffffffffu, pending);
       if (lane == 0 && half == 0) s_pq[quarter] = __popc(pm_prev);
     }
@@ -828,7 +833,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     }
   }
   __syncthreads();
-  if (tid == 0 && a.det) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
+  if (tid == 0 && DET) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
   if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<2 * H>(tmem);
 }
@@ -850,7 +855,7 @@ constexpr int rollout_ts_smem_bytes() {
   return H * H * 2 + NH * H * 2 + H * 128 * 2 + 1024;
 }
 
-template <class Env, int H, int NH, int SA>
+template <class Env, int H, int NH, int SA, bool DET>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) {
   static_assert(SA <= NH, "sampler width");
   static_assert(H == 256, "TS rollout is the H = 256 path");
@@ -887,7 +892,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     mbar_init(&mbar, 1);
     fence_mbar_init();
     smax = 0;
-    const int t0 = a.det ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
+    const int t0 = DET ? (int)blockIdx.x * a.mt : atomicAdd(a.tilectr, 2);
     for (int q = 0; q < 4; ++q) s_pq[q] = 0;
     s_cur0 = t0;
     s_next = t0 + 1;
@@ -963,12 +968,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   int bnext = 0;
   // deterministic mode: a static trajectory range [beg, bend) per CTA, slot row r starts
   // with beg + r, finished rows refill in row order (ballot ranks), no work stealing
-  const int beg = a.det ? (int)blockIdx.x * a.per : 0;
-  const int bend = a.det ? min(a.Bl, beg + a.per) : a.Bl;
+  const int beg = DET ? (int)blockIdx.x * a.per : 0;
+  const int bend = DET ? min(a.Bl, beg + a.per) : a.Bl;
   int dbase = beg + kTile;
   unsigned pm_prev = 0u;
   if (half == 0) {
-    b = a.det ? beg + row : atomicAdd(a.work, 1);
+    b = DET ? beg + row : atomicAdd(a.work, 1);
     active = b < bend;
     row_b[row] = b;
     row_t[row] = 0;
@@ -1060,7 +1065,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
                                  __uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1]);
       tmem_st16(lane_base + TA + (col >> 1), pk);
     }
-    if (a.det) {  // refill ranks: finished rows of the last step in row order
+    if constexpr (DET) {  // refill ranks: finished rows of the last step in row order
       const int tot = s_pq[0] + s_pq[1] + s_pq[2] + s_pq[3];
       if (pending) {
         int rank = __popc(pm_prev & ((1u << lane) - 1u));
@@ -1111,7 +1116,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         cur = nxt;
         crossed = true;
       }
-      if (crossed && tid == kThreads - 1) claim = a.det ? nclaim++ : atomicAdd(a.tilectr, 1);
+      if (crossed && tid == kThreads - 1) claim = DET ? nclaim++ : atomicAdd(a.tilectr, 1);
     }
     mark(1);
     if (half == 1) {  // the row's uniform while the MMA runs (rng.cpp:64-66)
@@ -1182,7 +1187,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
           a.batch.lengths[b] = tstep;
           a.batch.log_rewards[b] = Env::log_reward(P, s);
           Env::pack(P, s, a.batch.term_state + (size_t)b * P.SW);
-          if (!a.det) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
+          if constexpr (!DET) bnext = atomicAdd(a.work, 1);  // consumed after the next layer-1 phase
           atomicAdd(&s_nterm, 1);
           pending = true;
           active = false;
@@ -1212,7 +1217,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     h2_pend = my_valid;
     h2_gs = gslot;
     if (a.phase && half == 0) atomicMax(&smax, (unsigned long long)(clock64() - ts0));
-    if (a.det) {  // this step's finished rows, ranked at the next refill
+    if constexpr (DET) {  // this step's finished rows, ranked at the next refill
       pm_prev = __ballot_sync(0xffffffffu, pending);
       if (lane == 0 && half == 0) s_pq[quarter] = __popc(pm_prev);
     }
@@ -1243,7 +1248,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   }
   tc_fence_before();
   __syncthreads();
-  if (tid == 0 && a.det) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
+  if (tid == 0 && DET) a.det_used[blockIdx.x] = cur - s_cur0 + (fill > 0 ? 1 : 0);
   if (tid == 0) finish_counts(a.batch.counters, emitted, emitted - s_nterm);
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
@@ -1777,7 +1782,7 @@ constexpr int bwd_smem_bytes() {
   return H * H * 2 + kTile * H * 2 + kTile * 64 * 2 + H * NH * 2 + kThreads * 8 * 4 + kThreads * 4 + 1024;
 }
 
-template <class Env, int H, int NH>
+template <class Env, int H, int NH, bool LIST>
 __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -1828,11 +1833,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       float ga, gs, gf;
       float pr[NH];
     };
-    auto slot_of = [&](int tile) { return tile < tiles ? a.frow_bt[phys_tile(a.tile_list, tile) * kTile + row] : -1; };
+    auto slot_of = [&](int tile) { return tile < tiles ? a.frow_bt[phys_tile<LIST>(a.tile_list, tile) * kTile + row] : -1; };
     // vector loads only: these rows are strided, so every load instruction of a warp touches
     // 32 lines and the load/store unit, not the latency, bounds the prefetch
     auto load_row = [&](int tile, int rbt, RowIn& x) {
-      const int r = (tile < tiles ? phys_tile(a.tile_list, tile) : 0) * kTile + row;
+      const int r = (tile < tiles ? phys_tile<LIST>(a.tile_list, tile) : 0) * kTile + row;
       const bool v = rbt >= 0, v0 = v && half == 0;
       const size_t mo = (size_t)r * (H / 32) + half * (HC / 32);
       if constexpr (HC / 32 == 4) {
@@ -1878,7 +1883,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       }
     };
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
-      const int pt = phys_tile(a.tile_list, tile);  // emission tile of this training tile
+      const int pt = phys_tile<LIST>(a.tile_list, tile);  // emission tile of this training tile
       const int rbt = rbt_cur;
       const bool valid = rbt >= 0;
       const RowIn cx = nx;
@@ -2081,7 +2086,7 @@ GFNX_DEV void mma_mn64(uint32_t d_tmem, const void* x_img, int m0, const void* y
               idesc, (acc || s > 0) ? 1u : 0u);
 }
 
-template <class Env, int H>
+template <class Env, int H, bool LIST>
 __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* ring = align1024(smem_raw);
@@ -2115,7 +2120,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   auto X = [&](int st) { return ring + st * kWgStage; };
   auto Y = [&](int st) { return ring + st * kWgStage + 32768; };
   auto src = [&](const void* img, int u, int blk, int width) {  // 64-row unit u, 64-feature block blk
-    const int tile = phys_tile(a.tile_list, t0 + (u >> 1)), hh = u & 1;
+    const int tile = phys_tile<LIST>(a.tile_list, t0 + (u >> 1)), hh = u & 1;
     return reinterpret_cast<const uint8_t*>(img) + (size_t)tile * kTile * width * 2 + blk * (kTile * 128) +
            hh * (kWgRows * 128);
   };
@@ -2186,7 +2191,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   // and the packed state one unit ahead, so building a unit waits on no global load.
   auto ld_bt = [&](int u) {
     if (u >= nu) return -1;
-    const int r = phys_tile(a.tile_list, t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
+    const int r = phys_tile<LIST>(a.tile_list, t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
     return a.frow_bt[r];
   };
   auto ld_sw = [&](int bt, uint32_t (&w)[kMaxSWFwd]) {
@@ -2439,6 +2444,18 @@ __global__ void k_hg_marginal_level(int r0, int r1, const int32_t* __restrict__ 
   PT[r] = p * (double)probs[(size_t)r * rs + stop];
 }
 
+// the deterministic / work-stealing instantiation of a rollout kernel
+template <void (*KD)(RolloutArgs), void (*KN)(RolloutArgs)>
+void launch_det(const RolloutArgs& a, int grid, int smem, cudaStream_t st) {
+  if (a.det) {
+    set_smem_once(KD, smem);
+    KD<<<grid, kThreads, smem, st>>>(a);
+  } else {
+    set_smem_once(KN, smem);
+    KN<<<grid, kThreads, smem, st>>>(a);
+  }
+}
+
 template <class Env, int H, int NH>
 struct Kernels {
   static void rollout(Ctx& c, Key key, double eps) {
@@ -2480,21 +2497,21 @@ struct Kernels {
     const int fixed = rollout_smem_fixed<H, NH>();
     const int w1b = c.P.O * H * 2;
     cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, k_fast_rollout<Env, H, NH, true>);
+    cudaFuncGetAttributes(&fa, k_fast_rollout<Env, H, NH, true, false>);
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device);
     ProfScope ps(c, "k_fast_rollout");
     if constexpr (H == 256) {
       const int tsb = rollout_ts_smem_bytes<H, NH>();
       cudaFuncAttributes ft{};
-      cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH, NH>);
+      cudaFuncGetAttributes(&ft, k_fast_rollout_ts<Env, H, NH, NH, false>);
       if (tsb + (int)ft.sharedSizeBytes <= optin) {
         if (c.P.A <= 8) {
-          set_smem_once(k_fast_rollout_ts<Env, H, NH, 8>, tsb);
-          k_fast_rollout_ts<Env, H, NH, 8><<<grid, kThreads, tsb, c.stream>>>(a);
+          launch_det<k_fast_rollout_ts<Env, H, NH, 8, true>, k_fast_rollout_ts<Env, H, NH, 8, false>>(
+              a, grid, tsb, c.stream);
         } else {
-          set_smem_once(k_fast_rollout_ts<Env, H, NH, NH>, tsb);
-          k_fast_rollout_ts<Env, H, NH, NH><<<grid, kThreads, tsb, c.stream>>>(a);
+          launch_det<k_fast_rollout_ts<Env, H, NH, NH, true>, k_fast_rollout_ts<Env, H, NH, NH, false>>(
+              a, grid, tsb, c.stream);
         }
         c.launches++;
         f.fused = true;
@@ -2503,11 +2520,11 @@ struct Kernels {
       }
     }
     if (fixed + w1b + (int)fa.sharedSizeBytes <= optin) {  // W1 resident in smem
-      set_smem_once(k_fast_rollout<Env, H, NH, true>, fixed + w1b);
-      k_fast_rollout<Env, H, NH, true><<<grid, kThreads, fixed + w1b, c.stream>>>(a);
+      launch_det<k_fast_rollout<Env, H, NH, true, true>, k_fast_rollout<Env, H, NH, true, false>>(a, grid, fixed + w1b,
+                                                                                               c.stream);
     } else {
-      set_smem_once(k_fast_rollout<Env, H, NH, false>, fixed);
-      k_fast_rollout<Env, H, NH, false><<<grid, kThreads, fixed, c.stream>>>(a);
+      launch_det<k_fast_rollout<Env, H, NH, false, true>, k_fast_rollout<Env, H, NH, false, false>>(a, grid, fixed,
+                                                                                                 c.stream);
     }
     c.launches++;
     f.fused = true;
@@ -2642,16 +2659,21 @@ struct Kernels {
     k_loss_finalize<<<1, 256, 0, c.stream>>>(f.lpart, f.loss_wblocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
     int smem = bwd_smem_bytes<H, NH>();
-    set_smem_once(k_fast_bwd<Env, H, NH>, smem);
+    const bool list = ta.tile_list != nullptr;
+    if (list) set_smem_once(k_fast_bwd<Env, H, NH, true>, smem);
+    else set_smem_once(k_fast_bwd<Env, H, NH, false>, smem);
     {
       ProfScope ps(c, "k_fast_bwd");
-      k_fast_bwd<Env, H, NH><<<grid, kThreads, smem, c.stream>>>(ta);
+      if (list) k_fast_bwd<Env, H, NH, true><<<grid, kThreads, smem, c.stream>>>(ta);
+      else k_fast_bwd<Env, H, NH, false><<<grid, kThreads, smem, c.stream>>>(ta);
     }
     smem = wgrad_smem_bytes<H>();
-    set_smem_once(k_fast_wgrad<Env, H>, smem);
+    if (list) set_smem_once(k_fast_wgrad<Env, H, true>, smem);
+    else set_smem_once(k_fast_wgrad<Env, H, false>, smem);
     {
       ProfScope ps(c, "k_fast_wgrad");
-      k_fast_wgrad<Env, H><<<grid, kTile, smem, c.stream>>>(ta);
+      if (list) k_fast_wgrad<Env, H, true><<<grid, kTile, smem, c.stream>>>(ta);
+      else k_fast_wgrad<Env, H, false><<<grid, kTile, smem, c.stream>>>(ta);
     }
     const int64_t n = c.L.n_params;
     {
