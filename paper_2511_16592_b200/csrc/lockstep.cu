@@ -62,12 +62,13 @@ struct Lock<BitseqEnv> {  // k = 8 (256-word slots), <= 32 slots
   }
   // the state words legality depends on, cached in registers by the GEMM epilogues
   static constexpr int kLW = 1;
+  // (AR fixed: no slot is ever blocked before the end, so the cached word is 0 and every
+  //  column < A reads as legal, branch-free in the per-chunk test)
   GFNX_DEV static void load_lw(const EnvParams& P, const uint32_t* w, uint32_t (&lw)[kLW]) {
-    lw[0] = w[(P.bs_slots + 3) / 4];
+    lw[0] = P.bs_ar ? 0u : w[(P.bs_slots + 3) / 4];
   }
   GFNX_DEV static uint32_t legal32c(const EnvParams& P, const uint32_t (&lw)[kLW], int c0) {
     if (c0 >= P.A) return 0u;
-    if (P.bs_ar) return 0xffffffffu;
     return ((lw[0] >> (c0 >> 8)) & 1u) ? 0u : 0xffffffffu;
   }
   // features with index in [f0, f0 + 256): put(f - f0, value); `part` of 4 splits the work
@@ -203,9 +204,7 @@ __global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
     const float4 p0 = *reinterpret_cast<const float4*>(pre), p1 = *reinterpret_cast<const float4*>(pre + 4);
     v[0] = p0.x; v[1] = p0.y; v[2] = p0.z; v[3] = p0.w;
     v[4] = p1.x; v[5] = p1.y; v[6] = p1.z; v[7] = p1.w;
-    typename E::State dummy;
-    dummy.count = a.t - 1;  // the last action was taken with t - 1 filled slots (bitseq AR position)
-    E::delta_features(a.P, dummy, a.last_act[b], [&](int f, float coef) {
+    auto add_row = [&](int f, float coef) {
       const uint4 q = __ldg(reinterpret_cast<const uint4*>(a.w1 + (size_t)f * kH) + lane);
       const uint32_t x[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
@@ -213,7 +212,19 @@ __global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
         v[2 * e] += coef * bf16_lo(x[e]);
         v[2 * e + 1] += coef * bf16_hi(x[e]);
       }
-    });
+    };
+    if constexpr (std::is_same<E, BitseqEnv>::value) {
+      // BitseqEnv::delta_features: the last action's slot leaves "empty" for its token
+      // (NAR: slot act / V; AR fixed: slot t - 1, the token is the action), count feature + 1/S
+      const int V = a.P.bs_vocab, W = V + 1, act = a.last_act[b];
+      const int pos = a.P.bs_ar ? a.t - 1 : act / V, tok = a.P.bs_ar ? act : act - pos * V;
+      add_row(pos * W + V, -1.0f);
+      add_row(pos * W + tok, 1.0f);
+      add_row(a.P.bs_slots * W, 1.0f / (float)a.P.bs_slots);
+    } else {
+      typename E::State dummy;
+      E::delta_features(a.P, dummy, a.last_act[b], add_row);
+    }
   }
   *reinterpret_cast<float4*>(pre) = make_float4(v[0], v[1], v[2], v[3]);
   *reinterpret_cast<float4*>(pre + 4) = make_float4(v[4], v[5], v[6], v[7]);
@@ -260,7 +271,7 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
 };
 
 // +bf -> bf16 logits row-major [Bl][Ap] and masked (max, sum exp) per 128-column group
-template <class E>
+template <class E, bool FLOW = false>  // FLOW: DB / SubTB capture the log-flow column
 struct LogEpi : EpiBase {
   struct Args {
     EnvParams P;
@@ -290,7 +301,7 @@ struct LogEpi : EpiBase {
     uint32_t pk[16];
     float cm = -INFINITY;
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c);
-    if (e.flowv && e.P.A >= c && e.P.A < c + 32) {  // the log-flow column, before bf16 rounding
+    if (FLOW && e.P.A >= c && e.P.A < c + 32) {  // the log-flow column, before bf16 rounding
 #pragma unroll
       for (int i = 0; i < 32; ++i)
         if (c + i == e.P.A) e.flowv[(size_t)m * kTile + row] = v[i] + e.bf[c + i];
@@ -471,10 +482,8 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     const size_t bt = (size_t)b * a.T + a.t;
     const size_t r = (size_t)a.t * a.Bl + b;
     if (a.forced && b < a.nreal && a.forced[(size_t)b * a.T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
-      act = a.forced[bt];
-      typename E::State s;
-      E::unpack(P, w, s);
-      if (act < 0 || act >= P.A || !E::legal(P, s, act)) act = -1;
+      act = a.forced[bt];  // legality from the packed words (no unpacked State on the stack)
+      if (act < 0 || act >= P.A || !((Lock<E>::legal32(P, w, act & ~31) >> (act & 31)) & 1u)) act = -1;
     }
     if (act < 0 || !(z > 0.0)) {
       atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
@@ -705,7 +714,7 @@ __global__ void k_ls_loss_finalize(const double* lpart, int n, double* scalars, 
   if (!isfinite(l)) atomicExch(err, GFNX_ERR_NUMERIC);
 }
 
-template <class E>
+template <class E, bool FLOW = false>  // FLOW: DB / SubTB write the log-flow column's gradient
 struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile column sums
   struct Args {
     EnvParams P;
@@ -763,7 +772,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
       if (c0 + i == l.act) d += l.g;
       v[i] = d;
     }
-    if (e.gflow && (unsigned)(e.P.A - c0) < 32u) {  // the log-flow column (warp-uniform test)
+    if (FLOW && (unsigned)(e.P.A - c0) < 32u) {  // the log-flow column (warp-uniform test)
       const float gf = e.gflow[r];
 #pragma unroll
       for (int i = 0; i < 32; ++i)
@@ -1476,6 +1485,11 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         lmw[q] = lm;
         lcount += __popc(lm);
         const float4* bb = reinterpret_cast<const float4*>(bhead_s + col);
+        if (a.flowv && (unsigned)(P.A - col) < 32u) {  // log F (head column A), fp32, warp-uniform test
+#pragma unroll
+          for (int k = 0; k < 32; ++k)
+            if (col + k == P.A) a.flowv[r] = __uint_as_float(rr[k]) + bhead_s[col + k];
+        }
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const float4 bq = bb[i];
@@ -1483,7 +1497,6 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int k = 4 * i + e;
-            if (a.flowv && col + k == P.A) a.flowv[r] = __uint_as_float(rr[k]) + bv[e];  // log F, fp32
             const float x = __bfloat162float(__float2bfloat16(__uint_as_float(rr[k]) + bv[e]));
             rr[k] = __float_as_uint(x);
             if ((lm >> k) & 1u) hi = fmaxf(hi, x);
@@ -1564,9 +1577,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
       bool forced_bad = false;
       if (a.forced && b < a.nreal && a.forced[(size_t)b * T] >= 0) {  // rollout_from_actions (env_core.hpp:166-229)
         act = a.forced[(size_t)b * T + t];
-        typename E::State fs;
-        E::unpack(P, w, fs);
-        forced_bad = act < 0 || act >= P.A || !E::legal(P, fs, act);
+        forced_bad = act < 0 || act >= P.A || !((Lock<E>::legal32(P, w, act & ~31) >> (act & 31)) & 1u);
         if (forced_bad) act = 0;
       }
       const float lse = hi + __logf(z);
@@ -1738,8 +1749,13 @@ void rollout_impl(Ctx& c, Key key, double eps, const int16_t* forced) {
     g.A = (const uint8_t*)f.h[f.NL - 1];
     g.B = (const uint8_t*)f.wff;
     g.n_tiles = f.NT;
-    typename LogEpi<E>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl, f.flow ? f.flowv : nullptr};
-    launch_gemm<256, LogEpi<E>>(c, "k_gemm_logits", g, le, f.num_sms);
+    if (f.flow) {
+      typename LogEpi<E, true>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl, f.flowv};
+      launch_gemm<256, LogEpi<E, true>>(c, "k_gemm_logits", g, le, f.num_sms);
+    } else {
+      typename LogEpi<E, false>::Args le{c.P, f.bfp, f.cur, f.logits, f.stats, f.Ap, f.G, t * Bl, nullptr};
+      launch_gemm<256, LogEpi<E, false>>(c, "k_gemm_logits", g, le, f.num_sms);
+    }
     SampleArgs sa{c.P, fold_in(key, (uint64_t)t), eps, c.b0, Bl, t, T, f.Ap, f.G, f.logits, f.stats, f.cur, f.stst,
                   f.last_act, f.rowbuf, c.batch, forced, c.Bl};
     ProfScope ps(c, "k_ls_sample");
@@ -1786,9 +1802,14 @@ void train_impl(Ctx& c) {
   g.m_tiles = f.tilesR;
   g.n_tiles = f.NT;
   g.KB = 4;
-  typename DlogEpi<E>::Args de{c.P, f.bfp, f.rowbuf, f.coef, f.stst, c.batch.actions, (uint8_t*)f.dlog, f.bpart,
-                               Bl, f.T, f.KBA, f.bw, NL * kH, f.flow ? f.gflow : nullptr};
-  launch_gemm<256, DlogEpi<E>>(c, "k_gemm_dlogits", g, de, f.num_sms);
+  auto dlog = [&](auto epi) {
+    using Epi = decltype(epi);
+    typename Epi::Args de{c.P, f.bfp, f.rowbuf, f.coef, f.stst, c.batch.actions, (uint8_t*)f.dlog, f.bpart,
+                          Bl, f.T, f.KBA, f.bw, NL * kH, f.flow ? f.gflow : nullptr};
+    launch_gemm<256, Epi>(c, "k_gemm_dlogits", g, de, f.num_sms);
+  };
+  if (f.flow) dlog(DlogEpi<E, true>{});
+  else dlog(DlogEpi<E, false>{});
   GemmGeom g2{};
   g2.A = (const uint8_t*)f.dlog;
   g2.a_kb = f.KBA;
