@@ -10,6 +10,9 @@ ncu --set full --clock-control none --import-source on -k regex:"k_fast_(rollout
   --launch-skip $((3 * (W + J))) --launch-count 3 -o gpurun_out/full_$R \
   python bench.py --steps $K --warmup $W --no-cpu --no-e2e --no-steady --no-sweep --secondary "" > gpurun_out/ncu_full_$R.log 2>&1
 ROWS=$(python -c "import json; d=json.loads(open('gpurun_out/bench_full_$R.log').read().strip().splitlines()[-1]); print(d['roofline']['algorithmic_per_launch']['rows'])")
-python profiles/summarize_ncu.py gpurun_out/full_$R.ncu-rep profiles/${R}_ncu_summary.md $ROWS \
+python profiles/summarize_ncu.py gpurun_out/full_$R.ncu-rep gpurun_out/${R}_ncu_summary.md $ROWS \
   "ncu --set full, bench.py --steps $K --warmup $W timed iteration W+$J (rows = mean rows per timed iteration)"
 tail -2 gpurun_out/ncu_full_$R.log
+cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json  # (summarize_ncu.py wrote it on the box)
+bash profiles/ncu_brief.sh gpurun_out/full_$R.ncu-rep > gpurun_out/${R}_ncu_brief.txt 2>&1
+mkdir -p /tmp/ncu_reps && mv gpurun_out/*.ncu-rep /tmp/ncu_reps/  # keep the merge-back under 64 MiB
