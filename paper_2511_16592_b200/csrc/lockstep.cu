@@ -478,6 +478,7 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     }
   }
   // ---- record + env step (lane 0)
+  bool fin = false;  // lane 0: the step entered a terminal state (its reward below, warp-wide)
   if (lane == 0) {
     const size_t bt = (size_t)b * a.T + a.t;
     const size_t r = (size_t)a.t * a.Bl + b;
@@ -487,8 +488,13 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     }
     if (act < 0 || !(z > 0.0)) {
       atomicExch(a.batch.counters + 3, GFNX_ERR_CONTRACT);
-      return;
+      act = -1;
     }
+  }
+  if (__shfl_sync(0xffffffffu, act, 0) < 0) return;  // (warp-uniform)
+  if (lane == 0) {
+    const size_t bt = (size_t)b * a.T + a.t;
+    const size_t r = (size_t)a.t * a.Bl + b;
     const float xa = __bfloat162float(a.logits[(size_t)b * a.Ap + act]);
     const float lse = hi + __logf((float)z);
     a.rowbuf[2 * r] = xa - lse;
@@ -518,13 +524,49 @@ GFNX_DEV void sample_one(const SampleArgs& a, int b, double u01) {
     a.batch.nparents[bt] = (uint16_t)nparents;
     a.last_act[b] = act;
     if (term) {
-      typename E::State s;
-      E::unpack(P, cw, s);
       a.batch.lengths[b] = a.t + 1;
-      a.batch.log_rewards[b] = E::log_reward(P, s);
       for (int i = 0; i < P.SW; ++i) a.batch.term_state[(size_t)b * P.SW + i] = cw[i];
+      fin = true;
+      if (!(std::is_same<E, BitseqEnv>::value && P.bs_words <= 2)) {
+        typename E::State s;
+        E::unpack(P, cw, s);
+        a.batch.log_rewards[b] = E::log_reward(P, s);
+      }
     }
     if (!isfinite(lse)) atomicExch(a.batch.counters + 3, GFNX_ERR_NUMERIC);
+  }
+  if constexpr (std::is_same<E, BitseqEnv>::value) {
+    // ModeSet::log_reward (sequences.cpp:50-55) with the whole warp: lane s < slots places
+    // token s's k bits (MSB first) into the <= 128-bit string, lane m takes modes m, m + 32,
+    // ... (Hamming distance by popcount), warp min -> -beta * d / n (tabulated)
+    if (P.bs_words <= 2 && __shfl_sync(0xffffffffu, fin ? 1 : 0, 0)) {
+      __syncwarp();  // lane 0's new state words are visible to the warp
+      const uint32_t* cw = a.cur + (size_t)b * P.SW;
+      uint64_t lo = 0ull, hi = 0ull;
+      if (lane < P.bs_slots) {
+        const uint32_t tok = (cw[lane >> 2] >> (8 * (lane & 3))) & 0xffu;
+        for (int j = 0; j < P.bs_k; ++j) {
+          const int pos = lane * P.bs_k + j;  // string bit pos <- token bit k - 1 - j
+          const uint64_t bit = (uint64_t)((tok >> (P.bs_k - 1 - j)) & 1u) << (63 - (pos & 63));
+          if (pos < 64) lo |= bit;
+          else hi |= bit;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        lo |= __shfl_xor_sync(0xffffffffu, lo, o);
+        hi |= __shfl_xor_sync(0xffffffffu, hi, o);
+      }
+      int best = P.bs_nbits + 1;
+      for (int m = lane; m < P.n_modes; m += 32) {
+        const uint64_t* md = P.modes + (size_t)m * P.bs_words;
+        const int h = __popcll(lo ^ md[0]) + (P.bs_words > 1 ? __popcll(hi ^ md[1]) : 0);
+        best = h < best ? h : best;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(0xffffffffu, best, o));
+      if (lane == 0) a.batch.log_rewards[b] = P.bs_logr[best];
+    }
   }
 }
 
