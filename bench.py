@@ -48,6 +48,11 @@ SECONDARY = {
     # the headline workload in deterministic mode (static per-CTA ranges, bit-identical reruns)
     "hypergrid_db_b65536_det": dict(batch=65536, config="hypergrid_db_b65536", det=1,
                                     desc="hypergrid 20^4 DB, B=65536, MLP 2x256, deterministic=1"),
+    # EB-GFN (run_eb_gfn): the paper's Ising setting (PAPER Table 1: N = 10, TB, B = 256, MLP
+    # 4x256, 26.4 it/s for JAX gfnx on a GPU); k = D back-and-forth steps, data batch 256
+    "eb_gfn_ising10_b256": dict(batch=256, eb=True,
+                                desc="EB-GFN Ising 10x10, TB sampler B=256 MLP 4x256 (bf16 lockstep), "
+                                     "k=100, data batch 256; it/s (PAPER: 26.4 it/s, JAX gfnx)"),
 }
 
 
@@ -56,6 +61,9 @@ def secondary_runs(names, steps, warmup, local):
     out = {}
     for name in names:
         spec = SECONDARY[name]
+        if spec.get("eb"):
+            out[name] = eb_leg(spec, steps, warmup, local)
+            continue
         try:
             e, t = abi.config(spec.get("config", name), batch=spec["batch"])
             t.iterations = 1_000_000
@@ -77,6 +85,31 @@ def secondary_runs(names, steps, warmup, local):
         except Exception as ex:  # reported, never fatal
             out[name] = {"error": str(ex)[:300]}
     return out
+
+
+def eb_leg(spec, steps, warmup, local):
+    """EB-GFN iterations/s on the device (gfnx_eb_run: mixture rollout, train step, k-step
+    back-and-forth proposals, MH, CD update per iteration), CUDA events on the engine stream."""
+    from paper_2511_16592_b200 import abi, engine
+    try:
+        e = abi.env_desc(abi.ISING, is_side=10, is_sigma=0.2)
+        t = abi.train_desc(abi.ISING, batch=spec["batch"], iterations=1_000_000)
+        tr = engine.Trainer(e, t, device=local)
+        tr.eb_init(engine.eb_desc(data_batch=spec["batch"]))
+        tr.eb_run(0, warmup)
+        tr.synchronize()
+        tr.event_record(0)
+        m = tr.eb_run(warmup, steps)
+        tr.event_record(1)
+        tr.synchronize()
+        ms = tr.event_elapsed(0, 1)
+        _, _, init_nlr = tr.eb_coupling()
+        tr.close()
+        return {"workload": spec["desc"], "iters_per_s": steps / (ms / 1e3), "ms_per_iter": ms / steps,
+                "trajectories_per_s": spec["batch"] * steps / (ms / 1e3),
+                "neg_log_rmse": [round(init_nlr, 4), round(float(m[-1, 2]), 4)]}
+    except Exception as ex:  # reported, never fatal
+        return {"error": str(ex)[:300]}
 
 
 STEADY_CKPT = os.path.join(ROOT, "profiles", "hypergrid_db_converged.ckpt")
@@ -352,7 +385,8 @@ def main():
     ap.add_argument("--no-steady", action="store_true", help="skip the converged-checkpoint leg")
     ap.add_argument("--no-sweep", action="store_true", help="skip the reward-kernel B sweep")
     ap.add_argument("--secondary", default="hypergrid_subtb_b65536,bitseq_tb_b16384,bitseq_ar_tb_b16384,"
-                                           "ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192,hypergrid_db_b65536_det",
+                                           "ising_tb_b32768,hypergrid_tb_b16,dag_mdb_b8192,hypergrid_db_b65536_det,"
+                                           "eb_gfn_ising10_b256",
                     help="comma list of secondary configs (device-timed), '' to skip")
     args = ap.parse_args()
     world, rank, local = dist_env()

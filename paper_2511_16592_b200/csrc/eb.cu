@@ -13,6 +13,8 @@
 //   k_eb_bnf      back_and_forth_batch (ising.cpp:252-360): k uniform backward steps, the
 //                 forward replay of tau scored by the policy, k fresh policy steps (tau'),
 //                 the uniform backward score of tau'; fp64 SIMT in the reference's order
+//                 (check mode); k_eb_bnf_fast: the same on the bf16 sampler's fp32 weights
+//                 with block-parallel layers, softmax and draw (bf16 mode)
 //   k_eb_mh       MH acceptance with the current J (mh_accept ising.cpp:369-373, dense
 //                 ising_energy :40-51)
 //   k_eb_cd       cd_gradient (ising.cpp:222-250: per element in data order, then the
@@ -45,7 +47,6 @@ struct EbState {
   uint32_t *xs = nullptr, *props = nullptr, *acc = nullptr;  // [db][SW]
   double* logratio = nullptr;  // [db]
   int32_t* take = nullptr;     // [db]
-  double* p64 = nullptr;       // fp64 policy parameters (bf16 ctx: converted each iteration)
   double *obs = nullptr, *logit = nullptr;  // [db][O], [db][A] scratch of the proposal kernel
   double* metrics = nullptr;   // [cap][4]
   int64_t cap = 0;
@@ -348,42 +349,283 @@ __global__ void k_eb_bnf(EnvParams P, DevLayout Dl, const double* __restrict__ p
   }
 }
 
-__global__ void k_eb_mh(Key it_key, int db, const EnvParams P, const double* __restrict__ Jm,
-                        const uint32_t* __restrict__ xs, const uint32_t* __restrict__ props,
-                        const double* __restrict__ logratio, uint32_t* __restrict__ acc, int32_t* __restrict__ take) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= db) return;
-  const int half = P.SW / 2;
-  const uint32_t* x = xs + (size_t)b * P.SW;
-  const uint32_t* y = props + (size_t)b * P.SW;
-  const double ex = dense_energy(x, half, Jm, P.is_D);
-  const double ep = dense_energy(y, half, Jm, P.is_D);
-  const double log_a = -ep + ex + logratio[b];  // mh_accept ising.cpp:369-373
-  bool t = log_a >= 0.0;
-  if (!t) t = log(uniform_scalar(fold_in(fold_in(it_key, 7), (uint64_t)b))) < log_a;
-  take[b] = t ? 1 : 0;
-  for (int q = 0; q < P.SW; ++q) acc[(size_t)b * P.SW + q] = t ? y[q] : x[q];
-}
+// ---- bf16 mode: the proposal's policy evaluations in fp32 on the block (the sampler is the
+// bf16 policy, so the fp64 reference order buys nothing here): layer 1 as the sum of the D
+// active one-hot rows (ising.cpp:122-129 features), dense layers with four independent
+// accumulators per output, softmax statistics and the inverse-CDF draw by block reductions /
+// a block scan in fp64 instead of thread 0's serial loops.
+constexpr int kBnfThreads = 256;
 
-__global__ void __launch_bounds__(1024) k_eb_cd(int db, const EnvParams P, const uint32_t* __restrict__ xs,
-                                                const uint32_t* __restrict__ ys, const int32_t* __restrict__ take,
-                                                double* Jm, const double* __restrict__ Jt, double* g, double j_lr,
-                                                const double* __restrict__ scalars, double* metrics_row) {
-  const int D = P.is_D, half = P.SW / 2, n = D * D;
-  const double scale = 1.0 / (double)db;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {  // cd_gradient: grad_J E(x) = -x x^T
-    const int a = e / D, c = e % D;
-    double acc = 0.0;
-    if (a != c)
-      for (int i = 0; i < db; ++i) {
-        const uint32_t* x = xs + (size_t)i * P.SW;
-        const uint32_t* y = ys + (size_t)i * P.SW;
-        acc += scale * (-(double)spin_of(x, half, a) * (double)spin_of(x, half, c) +
-                        (double)spin_of(y, half, a) * (double)spin_of(y, half, c));
-      }
-    g[e] = acc;
+__device__ float block_reduce_f(float v, float* red, bool is_max) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float y = __shfl_xor_sync(0xffffffffu, v, o);
+    v = is_max ? fmaxf(v, y) : v + y;
   }
   __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = red[0];
+  for (int q = 1; q < kBnfThreads / 32; ++q) t = is_max ? fmaxf(t, red[q]) : t + red[q];
+  return t;
+}
+
+// logits of state s (fp32) into lg[nout]; h[2][512] fp32 scratch
+__device__ void policy_logits_f32(const EnvParams& P, const DevLayout& Dl, const float* __restrict__ params,
+                                  const IsingEnv::State& s, float (*h)[512], float* lg, int nout) {
+  const int H1 = Dl.dims[1];
+  for (int j = threadIdx.x; j < H1; j += blockDim.x) {  // layer 1: b1 + sum of the active rows
+    float acc[4] = {params[Dl.off_b[0] + j], 0.f, 0.f, 0.f};
+    for (int i = 0; i < P.is_D; ++i) {
+      const int v = IsingEnv::spin(s, i);
+      const int f = 3 * i + (v == 0 ? 2 : (v > 0 ? 1 : 0));
+      acc[i & 3] += params[Dl.off_w[0] + (size_t)f * H1 + j];
+    }
+    h[0][j] = fmaxf((acc[0] + acc[1]) + (acc[2] + acc[3]), 0.f);
+  }
+  __syncthreads();
+  int in = H1, cur = 0;
+  auto dense = [&](int64_t off_w, int64_t off_b, int out, const float* x, float* y, bool relu) {
+    for (int j = threadIdx.x; j < out; j += blockDim.x) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* W = params + off_w + j;
+      int p = 0;
+      for (; p + 3 < in; p += 4) {
+        acc[0] += x[p] * W[(size_t)p * out];
+        acc[1] += x[p + 1] * W[(size_t)(p + 1) * out];
+        acc[2] += x[p + 2] * W[(size_t)(p + 2) * out];
+        acc[3] += x[p + 3] * W[(size_t)(p + 3) * out];
+      }
+      for (; p < in; ++p) acc[0] += x[p] * W[(size_t)p * out];
+      const float z = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + params[off_b + j];
+      y[j] = relu ? fmaxf(z, 0.f) : z;
+    }
+  };
+  for (int l = 1; l < Dl.n_trunk; ++l) {
+    dense(Dl.off_w[l], Dl.off_b[l], Dl.dims[l + 1], h[cur], h[cur ^ 1], true);
+    __syncthreads();
+    cur ^= 1;
+    in = Dl.dims[l + 1];
+  }
+  dense(Dl.off_fw, Dl.off_fb, nout, h[cur], lg, false);
+  __syncthreads();
+}
+
+// log pi(a | s) of every action (masked log-softmax, eps = 0) -> logp[A]; returns nothing
+__device__ void masked_logp_f32(const EnvParams& P, const IsingEnv::State& s, const float* lg, float* logp,
+                                float* red) {
+  float hi = -INFINITY;
+  for (int c = threadIdx.x; c < P.A; c += blockDim.x)
+    if (IsingEnv::legal(P, s, c)) hi = fmaxf(hi, lg[c]);
+  hi = block_reduce_f(hi, red, true);
+  float z = 0.f;
+  for (int c = threadIdx.x; c < P.A; c += blockDim.x)
+    if (IsingEnv::legal(P, s, c)) z += __expf(lg[c] - hi);
+  z = block_reduce_f(z, red, false);
+  const float lse = hi + __logf(z);
+  for (int c = threadIdx.x; c < P.A; c += blockDim.x) logp[c] = IsingEnv::legal(P, s, c) ? lg[c] - lse : -INFINITY;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBnfThreads) k_eb_bnf_fast(EnvParams P, DevLayout Dl, const float* __restrict__ params,
+                                                            Key key, int k, const uint32_t* __restrict__ xs,
+                                                            uint32_t* __restrict__ props,
+                                                            double* __restrict__ logratio, int32_t* err) {
+  const int b = blockIdx.x;
+  const int D = P.is_D, half = P.SW / 2;
+  __shared__ IsingEnv::State s, partial;
+  __shared__ float h[2][512];
+  __shared__ float lg[512], logp[512];
+  __shared__ float red[kBnfThreads / 32];
+  __shared__ double scan[kBnfThreads];
+  __shared__ int16_t removed[kMaxIsingD], added[kMaxIsingD];
+  __shared__ int s_pick;
+  const uint32_t* x = xs + (size_t)b * P.SW;
+  double lr = 0.0;  // thread 0
+  if (threadIdx.x == 0) {  // phase 1: k uniform backward steps, - log P_B(tau | x)
+    IsingEnv::unpack(P, x, s);
+    s.term = true;
+    s.step = s.count;
+    for (int step = 0; step < k; ++step) {
+      const int nl = s.count;
+      const Key sk = fold_in(fold_in(key, 100), (uint64_t)step);
+      int q = (int)(uniform_scalar(fold_in(sk, (uint64_t)b)) * (double)nl);
+      if (q >= nl) q = nl - 1;
+      const int site = nth_assigned(s, D, q);
+      lr -= log(1.0 / (double)nl);
+      unassign(s, site);
+      removed[step] = (int16_t)site;
+    }
+    partial = s;
+  }
+  __syncthreads();
+  for (int step = 0; step < k; ++step) {  // phase 2: forward replay of tau, + log P_F(tau)
+    policy_logits_f32(P, Dl, params, s, h, lg, P.A);
+    masked_logp_f32(P, s, lg, logp, red);
+    if (threadIdx.x == 0) {
+      const int site = removed[k - 1 - step];
+      const int action = 2 * site + (spin_of(x, half, site) > 0 ? 1 : 0);
+      lr += (double)logp[action];
+      IsingEnv::step(P, s, action);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) s = partial;
+  __syncthreads();
+  for (int step = 0; step < k; ++step) {  // phase 3: k fresh policy steps (tau'), - log P_F(tau')
+    policy_logits_f32(P, Dl, params, s, h, lg, P.A);
+    masked_logp_f32(P, s, lg, logp, red);
+    // categorical (rng.cpp:87-100) over p_c = exp(logp_c): fp64 block scan in column order
+    const Key sk = fold_in(fold_in(key, 300), (uint64_t)step);
+    const double u01 = uniform_scalar(fold_in(sk, (uint64_t)b));
+    double carry = 0.0;
+    if (threadIdx.x == 0) s_pick = -1;
+    for (int c0 = 0; c0 < P.A; c0 += kBnfThreads) {
+      const int c = c0 + threadIdx.x;
+      const double wv = c < P.A && logp[c] > -INFINITY ? (double)__expf(logp[c]) : 0.0;
+      scan[threadIdx.x] = wv;
+      __syncthreads();
+      for (int o = 1; o < kBnfThreads; o <<= 1) {  // inclusive Hillis-Steele scan
+        const double y = threadIdx.x >= o ? scan[threadIdx.x - o] : 0.0;
+        __syncthreads();
+        scan[threadIdx.x] += y;
+        __syncthreads();
+      }
+      scan[threadIdx.x] += carry;
+      __syncthreads();
+      carry = scan[kBnfThreads - 1];
+      __syncthreads();
+      // the pick needs the total: keep this chunk's running sums (h is free scratch here;
+      // its 4 KB hold A <= 512 doubles)
+      if (c < P.A) reinterpret_cast<double*>(h)[c] = scan[threadIdx.x];
+      __syncthreads();
+    }
+    const double total = carry;
+    const double target = u01 * total;
+    for (int c = threadIdx.x; c < P.A; c += blockDim.x) {
+      const double incl = reinterpret_cast<const double*>(h)[c];
+      const double excl = c > 0 ? reinterpret_cast<const double*>(h)[c - 1] : 0.0;
+      if (incl > excl && target < incl && target >= excl) atomicMax(&s_pick, c);  // the unique crossing column
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int a = s_pick;
+      if (a < 0)  // rounding fallback: the last legal column
+        for (int c = P.A - 1; c >= 0; --c)
+          if (logp[c] > -INFINITY) {
+            a = c;
+            break;
+          }
+      if (a < 0) {
+        atomicExch(err, GFNX_ERR_CONTRACT);
+        a = 0;
+      }
+      lr -= (double)logp[a];
+      IsingEnv::step(P, s, a);
+      added[step] = (int16_t)(a / 2);
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    IsingEnv::pack(P, s, props + (size_t)b * P.SW);
+    for (int step = 0; step < k; ++step) {  // phase 4: the uniform backward score of tau' from x'
+      lr += -log((double)s.count);
+      unassign(s, added[k - 1 - step]);
+    }
+    logratio[b] = lr;
+  }
+}
+
+// one block per sample: thread a computes row a of both energies (sequential over b, the
+// reference's order), thread 0 then folds quad += s_a * row_a in a order -> bit-exact
+__global__ void __launch_bounds__(128) k_eb_mh(Key it_key, int db, const EnvParams P, const double* __restrict__ Jm,
+                                               const uint32_t* __restrict__ xs, const uint32_t* __restrict__ props,
+                                               const double* __restrict__ logratio, uint32_t* __restrict__ acc,
+                                               int32_t* __restrict__ take) {
+  const int b = blockIdx.x;
+  if (b >= db) return;
+  const int D = P.is_D, half = P.SW / 2;
+  const uint32_t* x = xs + (size_t)b * P.SW;
+  const uint32_t* y = props + (size_t)b * P.SW;
+  __shared__ double rx[kMaxIsingD], ry[kMaxIsingD];
+  __shared__ int8_t sx[kMaxIsingD], sy[kMaxIsingD];
+  for (int i = threadIdx.x; i < D; i += blockDim.x) {
+    sx[i] = (int8_t)spin_of(x, half, i);
+    sy[i] = (int8_t)spin_of(y, half, i);
+  }
+  __syncthreads();
+  for (int a = threadIdx.x; a < D; a += blockDim.x) {  // ising_energy's row sums (ising.cpp:44-48)
+    const double* J = Jm + (size_t)a * D;
+    double r1 = 0.0, r2 = 0.0;
+    for (int c = 0; c < D; ++c) {
+      r1 += J[c] * (double)sx[c];
+      r2 += J[c] * (double)sy[c];
+    }
+    rx[a] = r1;
+    ry[a] = r2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double qx = 0.0, qy = 0.0;
+    for (int a = 0; a < D; ++a) {
+      qx += (double)sx[a] * rx[a];
+      qy += (double)sy[a] * ry[a];
+    }
+    const double ex = -qx, ep = -qy;
+    const double log_a = -ep + ex + logratio[b];  // mh_accept ising.cpp:369-373
+    bool t = log_a >= 0.0;
+    if (!t) t = log(uniform_scalar(fold_in(fold_in(it_key, 7), (uint64_t)b))) < log_a;
+    take[b] = t ? 1 : 0;
+    for (int q = 0; q < P.SW; ++q) acc[(size_t)b * P.SW + q] = t ? y[q] : x[q];
+  }
+}
+
+// cd_gradient's per-element sums (ising.cpp:230-240: grad[a][b] += scale * (-x_a x_b + y_a y_b)
+// over the data in order): the batch's spins are staged in shared memory, thread per element
+constexpr int kCdThreads = 256, kCdGrid = 148, kCdMaxSmem = 96 * 1024;
+__global__ void __launch_bounds__(kCdThreads) k_eb_cd_grad(int db, int chunk, const EnvParams P,
+                                                           const uint32_t* __restrict__ xs,
+                                                           const uint32_t* __restrict__ ys, double* __restrict__ g) {
+  extern __shared__ int8_t sp[];  // [chunk][D] data spins, then [chunk][D] accepted spins
+  const int D = P.is_D, half = P.SW / 2, n = D * D;
+  const double scale = 1.0 / (double)db;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};  // elements e0 + k * stride of this thread (n <= 4 * stride)
+  const int e0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  for (int i0 = 0; i0 < db; i0 += chunk) {  // samples in order, chunk by chunk
+    const int m = min(chunk, db - i0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < m * D; q += blockDim.x) {
+      const int i = q / D, c = q % D;
+      sp[q] = (int8_t)spin_of(xs + (size_t)(i0 + i) * P.SW, half, c);
+      sp[m * D + q] = (int8_t)spin_of(ys + (size_t)(i0 + i) * P.SW, half, c);
+    }
+    __syncthreads();
+    const int8_t* X = sp;
+    const int8_t* Y = sp + m * D;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int e = e0 + k * stride;
+      if (e >= n) break;
+      const int a = e / D, c = e % D;
+      if (a == c) continue;
+      double v = acc[k];
+      for (int i = 0; i < m; ++i)
+        v += scale * (-(double)X[i * D + a] * (double)X[i * D + c] + (double)Y[i * D + a] * (double)Y[i * D + c]);
+      acc[k] = v;
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+    if (e0 + k * stride < n) g[e0 + k * stride] = acc[k];
+}
+
+// symmetrisation, J -= lr_J * grad, neg_log_rmse (ising.cpp:241-250, 375-386), the metrics row
+__global__ void __launch_bounds__(1024) k_eb_cd_update(int db, const EnvParams P, const int32_t* __restrict__ take,
+                                                       double* Jm, const double* __restrict__ Jt, double* g,
+                                                       double j_lr, const double* __restrict__ scalars,
+                                                       double* metrics_row) {
+  const int D = P.is_D, n = D * D;
   for (int e = threadIdx.x; e < n; e += blockDim.x) {  // symmetrize
     const int a = e / D, c = e % D;
     if (c < a) {
@@ -411,10 +653,6 @@ __global__ void __launch_bounds__(1024) k_eb_cd(int db, const EnvParams P, const
   }
 }
 
-__global__ void k_eb_f32_to_f64(const float* a, double* b, int64_t n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) b[i] = (double)a[i];
-}
 
 double host_nlr(const std::vector<double>& jt, const std::vector<double>& jm, int D) {
   double acc = 0.0;
@@ -446,7 +684,7 @@ void eb_free(Ctx& c) {
   if (!c.eb) return;
   EbState& e = *static_cast<EbState*>(c.eb);
   void* ptrs[] = {e.data, e.Jm, e.Jt, e.grad, e.nfwd, e.terms, e.wact, e.wnp, e.wlen, e.forced, e.xs, e.props,
-                  e.acc, e.logratio, e.take, e.p64, e.obs, e.logit, e.metrics};
+                  e.acc, e.logratio, e.take, e.obs, e.logit, e.metrics};
   for (void* p : ptrs) cudaFree(p);
   delete &e;
   c.eb = nullptr;
@@ -507,7 +745,6 @@ void eb_init(Ctx& c, const gfnx_eb_desc& d, const int8_t* data, int64_t n) {
   alloc(&e->take, sizeof(int32_t) * db);
   alloc(&e->obs, sizeof(double) * (size_t)db * c.P.O);
   alloc(&e->logit, sizeof(double) * (size_t)db * std::max(c.P.A, c.P.Ab));
-  if (!c.check_mode()) alloc(&e->p64, sizeof(double) * c.L.n_params);
   cuda_check(cudaMemcpy(e->data, packed.data(), sizeof(uint32_t) * packed.size(), cudaMemcpyHostToDevice), "eb data");
   cuda_check(cudaMemcpy(e->Jt, jt.data(), sizeof(double) * D * D, cudaMemcpyHostToDevice), "eb J*");
   cuda_check(cudaMemset(e->Jm, 0, sizeof(double) * D * D), "eb J");  // zero_coupling
@@ -538,26 +775,30 @@ const int16_t* eb_pre(Ctx& c, Key it_key) {
 // the energy-model half of iteration it (train.cpp:974-995), metrics into row i
 void eb_post(Ctx& c, Key it_key, double j_lr, int64_t i) {
   EbState& e = EB(c);
-  const double* params = c.p64;
-  if (!c.check_mode()) {
-    const int64_t n = c.L.n_params;
-    k_eb_f32_to_f64<<<(unsigned)((n + 255) / 256), 256, 0, c.stream>>>(c.p32, e.p64, n);
-    c.launches++;
-    params = e.p64;
-  }
   const DevLayout Dl = make_dev_layout(c);
   DevLayout Db = Dl;  // the learned backward head (LossConfig::learned_backward)
   Db.off_fw = c.L.off_bw;
   Db.off_fb = c.L.off_bb;
   Db.A = c.P.Ab;
   k_eb_pick<<<(e.db + 127) / 128, 128, 0, c.stream>>>(it_key, e.db, e.N, e.data, e.SW, e.xs);
-  k_eb_bnf<<<e.db, 256, 0, c.stream>>>(c.P, Dl, params, fold_in(it_key, 6), e.k, e.xs, e.props, e.logratio, e.obs,
-                                       e.logit, c.batch.counters + 3, c.train.learned_backward, Db);
-  k_eb_mh<<<(e.db + 127) / 128, 128, 0, c.stream>>>(it_key, e.db, c.P, e.Jm, e.xs, e.props, e.logratio, e.acc,
-                                                    e.take);
-  k_eb_cd<<<1, 1024, 0, c.stream>>>(e.db, c.P, e.xs, e.acc, e.take, e.Jm, e.Jt, e.grad, j_lr, c.d_scalars,
-                                     e.metrics + 4 * i);
-  c.launches += 4;
+  if (c.check_mode()) {  // fp64, the reference's operation order (bit-exact with run_eb_gfn)
+    k_eb_bnf<<<e.db, 256, 0, c.stream>>>(c.P, Dl, c.p64, fold_in(it_key, 6), e.k, e.xs, e.props, e.logratio, e.obs,
+                                         e.logit, c.batch.counters + 3, c.train.learned_backward, Db);
+  } else {  // the bf16 sampler's fp32 master weights, block-parallel evaluation
+    k_eb_bnf_fast<<<e.db, kBnfThreads, 0, c.stream>>>(c.P, Dl, c.p32, fold_in(it_key, 6), e.k, e.xs, e.props,
+                                                      e.logratio, c.batch.counters + 3);
+  }
+  k_eb_mh<<<e.db, 128, 0, c.stream>>>(it_key, e.db, c.P, e.Jm, e.xs, e.props, e.logratio, e.acc, e.take);
+  const int chunk = std::min(e.db, kCdMaxSmem / (2 * e.D));
+  static bool cd_attr = false;
+  if (!cd_attr) {
+    cudaFuncSetAttribute(k_eb_cd_grad, cudaFuncAttributeMaxDynamicSharedMemorySize, kCdMaxSmem);
+    cd_attr = true;
+  }
+  k_eb_cd_grad<<<kCdGrid, kCdThreads, 2 * chunk * e.D, c.stream>>>(e.db, chunk, c.P, e.xs, e.acc, e.grad);
+  k_eb_cd_update<<<1, 1024, 0, c.stream>>>(e.db, c.P, e.take, e.Jm, e.Jt, e.grad, j_lr, c.d_scalars,
+                                           e.metrics + 4 * i);
+  c.launches += 5;
 }
 
 const double* eb_metrics(Ctx& c) { return EB(c).metrics; }
