@@ -95,6 +95,17 @@ GFNX_DEV uint32_t pack_bf16x2_relu(float lo, float hi) {
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// ReLU(acc + bias) of an fp32 accumulator pair (raw TMEM words) as one packed bf16 pair:
+// one FADD2 (add.rn.f32x2, IEEE fp32 per lane like FADD) + one cvt
+GFNX_DEV uint32_t bias_relu_pack(uint32_t a_lo, uint32_t a_hi, float2 b) {
+  unsigned long long x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "r"(a_lo), "r"(a_hi));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
+  return pack_bf16x2_relu(lo, hi);
+}
 
 GFNX_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 GFNX_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }

@@ -868,7 +868,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
   uint8_t* w2img = smem;                 // H x H bf16 (resident)
   uint8_t* whimg = w2img + H * H * 2;    // head image [NH][H]
   uint8_t* w1img = whimg + NH * H * 2;   // W1^T image [H][128 features], K-major
-  __shared__ float b1s[H], b2s[H];
+  __shared__ __align__(16) float b1s[H];
+  __shared__ __align__(16) float b2s[H];
   __shared__ float bhs[NH];
   __shared__ Key skeys[128];
   __shared__ double row_u[kTile];
@@ -1019,6 +1020,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
       *reinterpret_cast<uint2*>(mask + (size_t)gs * (H / 32) + 2 * blk) = make_uint2(relu_mask16(lo), relu_mask16(hi));
     }
   };
+  // ReLU(acc + bias) of the thread's HC accumulator columns -> packed bf16 at TMEM column
+  // dst: two 32-column loads in flight per wait (the TMEM load latency is paid HC / 64 times)
+  auto epilogue = [&](const float* bias, uint32_t dst) {
+#pragma unroll 1
+    for (int q = 0; q < HC / 64; ++q) {
+      const int col = c0 + q * 64;
+      uint32_t r0[32], r1[32];
+      tmem_ld32(lane_base + col, r0);
+      tmem_ld32(lane_base + col + 32, r1);
+      tmem_wait_ld();
+      const float2* b2 = reinterpret_cast<const float2*>(bias + col);
+      uint32_t pk[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = bias_relu_pack(r0[2 * i], r0[2 * i + 1], b2[i]);
+      tmem_st16(lane_base + dst + (col >> 1), pk);
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = bias_relu_pack(r1[2 * i], r1[2 * i + 1], b2[16 + i]);
+      tmem_st16(lane_base + dst + ((col + 32) >> 1), pk);
+    }
+  };
   bool h2_pend = false;  // h2 blocks 2-3 of the previous step's row slot still to emit
   int h2_gs = 0;
   int nact;
@@ -1045,26 +1066,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     publish();
     if (tid == 0) {
       tc_fence_after();
-      mma_tk<H, 128>(tmem, tmem + TA, w1img, false);
+      mma_tk_k<H>(tmem, tmem + TA, w1img, (P.O + 15) & ~15);
       umma_commit(&mbar);
     }
     emit_block(a.h2, a.mask2, TA2, 2 + half, h2_pend, h2_gs);  // (warp-collective TMEM load)
     h2_pend = false;
     mma_join();
     // h1 = ReLU(acc + b1) -> packed into TMEM (the hidden MMA's A operand) + ReLU mask
-#pragma unroll 1
-    for (int q = 0; q < HC / 32; ++q) {
-      const int col = c0 + q * 32;
-      uint32_t r[32];
-      tmem_ld32(lane_base + col, r);
-      tmem_wait_ld();
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + b1s[col + 2 * i],
-                                 __uint_as_float(r[2 * i + 1]) + b1s[col + 2 * i + 1]);
-      tmem_st16(lane_base + TA + (col >> 1), pk);
-    }
+    epilogue(b1s, TA);
     if constexpr (DET) {  // refill ranks: finished rows of the last step in row order
       const int tot = s_pq[0] + s_pq[1] + s_pq[2] + s_pq[3];
       if (pending) {
@@ -1127,19 +1136,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
     mma_join();
     mark(2);
     // (3) h2 = ReLU(acc + b2) -> packed into TMEM (own columns: h1 stays for its mask)
-#pragma unroll 1
-    for (int q = 0; q < HC / 32; ++q) {
-      const int col = c0 + q * 32;
-      uint32_t r[32];
-      tmem_ld32(lane_base + col, r);
-      tmem_wait_ld();
-      uint32_t pk[16];
-#pragma unroll
-      for (int i = 0; i < 16; ++i)
-        pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + b2s[col + 2 * i],
-                                 __uint_as_float(r[2 * i + 1]) + b2s[col + 2 * i + 1]);
-      tmem_st16(lane_base + TA2 + (col >> 1), pk);
-    }
+    epilogue(b2s, TA2);
     publish();
     mark(3);
     // (4) head (logits + flow) on the tensor cores
@@ -3207,6 +3204,9 @@ __global__ void __launch_bounds__(128, 1) k_mma_rate(int reps, int mode, long lo
     for (int r = 0; r < reps; ++r) {
       if (mode == 0) {  // 128 x N x 256 from K-major SW128 images
         mma_kk<N, 256>(tbase + (r & 1) * 256, aimg, bimg, false);
+      } else if (mode == 5) {  // A from TMEM (the rollout's TS form), D in [0, N)
+        mma_tk<N, 256>(tbase, tbase + 256, bimg, false);
+
       } else if (mode >= 3) {  // MN-major operands (weight-gradient shape), K = 256 rows
         constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
         const uint32_t a0 = smem_u32(aimg), b0 = smem_u32(bimg);
@@ -3312,6 +3312,12 @@ void test_mma_rate(int n, int reps, int mode, int grid, long long* host_out) {
   if (n == 256) {
     cudaFuncSetAttribute(k_mma_rate<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mma_rate<256><<<grid, 128, smem>>>(reps, mode, d);
+  } else if (n == 16) {
+    cudaFuncSetAttribute(k_mma_rate<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma_rate<16><<<grid, 128, smem>>>(reps, mode, d);
+  } else if (n == 32) {
+    cudaFuncSetAttribute(k_mma_rate<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    k_mma_rate<32><<<grid, 128, smem>>>(reps, mode, d);
   } else {
     cudaFuncSetAttribute(k_mma_rate<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     k_mma_rate<128><<<grid, 128, smem>>>(reps, mode, d);

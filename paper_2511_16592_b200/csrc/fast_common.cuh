@@ -67,6 +67,19 @@ GFNX_DEV void mma_tk(uint32_t d_tmem, uint32_t a_tmem, const void* b_img, bool a
   }
 }
 
+// the same with a runtime K (multiple of 16, <= the image's K): layer 1 reads only the
+// obs_dim features that exist (hypergrid 4x20: K = 80, 5 instead of 8 K-steps)
+template <int N>
+GFNX_DEV void mma_tk_k(uint32_t d_tmem, uint32_t a_tmem, const void* b_img, int k) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, false, false);
+  const uint32_t b0 = smem_u32(b_img);
+#pragma unroll 1
+  for (int s = 0; s < k / 16; ++s) {
+    const uint32_t bo = b0 + (s >> 2) * (N * 128) + (s & 3) * 32;
+    umma_bf16_ts(d_tmem, a_tmem + s * 8, umma_desc_sw128(bo, 16, 1024), idesc, s > 0 ? 1u : 0u);
+  }
+}
+
 // store 32 consecutive bf16 columns [c0, c0+32) of row `row` into a 128-row tile image
 GFNX_DEV void st_row32(uint8_t* img, int row, int c0, const uint32_t (&pk)[16]) {
 #pragma unroll
