@@ -335,6 +335,68 @@ void do_train(Ctx& c, bool apply, double lr, double* loss) {
 
 }  // namespace
 
+namespace {
+// The bf16 fast paths run fixed hidden widths: lockstep (bitseq / Ising) 256 per layer,
+// hypergrid two equal layers of 128 or 256, DAG two of 128. A narrower network runs there
+// zero-padded: the extra units have zero weights in and out and zero bias, so they stay
+// exactly 0 through ReLU (their products add exact zeros to the real units' tensor-core
+// sums), their ReLU masks are 0, every gradient into them is exactly 0 and Adam (with or
+// without weight decay) keeps them at 0 — the real units compute what the requested widths
+// compute. The ABI (params, grads, Adam state, checkpoints) keeps the user's layout.
+void pad_layout(Ctx& c) {
+  const int kind = c.env.kind, nh = c.train.num_hidden;
+  int maxw = 0;
+  for (int l = 0; l < nh; ++l) maxw = std::max(maxw, (int)c.train.hidden[l]);
+  int target = 0;
+  if (kind == GFNX_ENV_BITSEQ || kind == GFNX_ENV_ISING) {
+    if (maxw <= 256 && nh >= 2) target = 256;
+  } else if (nh == 2) {
+    if (kind == GFNX_ENV_DAG) target = maxw <= 128 ? 128 : 0;
+    else target = maxw <= 128 ? 128 : maxw <= 256 ? 256 : 0;
+  }
+  if (!target) return;  // unsupported widths: the fast path's own check reports them
+  bool same = true;
+  for (int l = 0; l < nh; ++l) same = same && c.train.hidden[l] == target;
+  if (same) return;
+  gfnx_train_desc tp = c.train;
+  for (int l = 0; l < nh; ++l) tp.hidden[l] = target;
+  make_layout(tp, c.shape, &c.L);
+  const MlpLayout &X = c.Lx, &D = c.L;
+  c.xmap.assign(X.n_params, -1);
+  auto block = [&](int64_t xo, int64_t dof, int rows, int cols, int dcols) {  // [rows][cols]
+    for (int i = 0; i < rows; ++i)
+      for (int j = 0; j < cols; ++j) c.xmap[xo + (int64_t)i * cols + j] = dof + (int64_t)i * dcols + j;
+  };
+  for (int l = 0; l < nh; ++l) {
+    block(X.off_w[l], D.off_w[l], X.dims[l], X.dims[l + 1], D.dims[l + 1]);
+    block(X.off_b[l], D.off_b[l], 1, X.dims[l + 1], D.dims[l + 1]);
+  }
+  const int A = c.shape.num_actions, Ab = c.shape.num_backward_actions, H = X.H();
+  block(X.off_fw, D.off_fw, H, A, A);
+  block(X.off_fb, D.off_fb, 1, A, A);
+  block(X.off_bw, D.off_bw, H, Ab, Ab);
+  block(X.off_bb, D.off_bb, 1, Ab, Ab);
+  block(X.off_flw, D.off_flw, H, 1, 1);
+  block(X.off_flb, D.off_flb, 1, 1, 1);
+}
+}  // namespace
+
+// user-layout vector -> device-layout vector (padding zero), and back
+std::vector<double> to_device_layout(const Ctx& c, const double* x) {
+  if (c.xmap.empty()) return std::vector<double>(x, x + c.L.n_params);
+  std::vector<double> d(c.L.n_params, 0.0);
+  for (int64_t i = 0; i < c.Lx.n_params; ++i) d[c.xmap[i]] = x[i];
+  return d;
+}
+template <class T>
+void to_user_layout(const Ctx& c, const T* d, double* x) {
+  if (c.xmap.empty()) {
+    for (int64_t i = 0; i < c.L.n_params; ++i) x[i] = d[i];
+  } else {
+    for (int64_t i = 0; i < c.Lx.n_params; ++i) x[i] = d[c.xmap[i]];
+  }
+}
+
 extern "C" {
 
 int32_t gfnx_abi_version(void) { return GFNX_ABI_VERSION; }
@@ -375,6 +437,7 @@ gfnx_status gfnx_nccl_unique_id(void* out128) {
   });
 }
 
+
 namespace {
 gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, int32_t device, int32_t rank,
                         int32_t world, const void* nccl_id, Group* group, gfnx_ctx** out) {
@@ -393,7 +456,9 @@ gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     if (!err.empty()) fail(GFNX_ERR_CONFIG, err);
     resolve_schedule(&c.train.lr, c.train.iterations);
     resolve_schedule(&c.train.explore, c.train.iterations);
-    make_layout(c.train, c.shape, &c.L);
+    make_layout(c.train, c.shape, &c.Lx);
+    c.L = c.Lx;
+    if (train->precision != GFNX_PREC_FP64_CHECK) pad_layout(c);
     c.device = device;
     c.rank = rank;
     c.world = world;
@@ -469,7 +534,8 @@ gfnx_status create_impl(const gfnx_env_desc* env, const gfnx_train_desc* train, 
     cuda_check(cudaMemset(bt.counters, 0, sizeof(int32_t) * 16), "batch");
     // parameters
     std::vector<double> p0;
-    init_params(c.train, c.L, P.A, P.Ab, &p0);
+    init_params(c.train, c.Lx, P.A, P.Ab, &p0);  // the reference's mlp_init at the user's widths
+    p0 = to_device_layout(c, p0.data());
     const int64_t n = c.L.n_params;
     cuda_check(cudaMalloc(&c.d_scalars, sizeof(double) * 8), "scalars");
     std::vector<double> sc(8, 0.0);
@@ -584,19 +650,20 @@ void gfnx_destroy(gfnx_ctx* h) {
 }
 
 gfnx_status gfnx_num_params(const gfnx_ctx* h, int64_t* n) {
-  *n = h->c.L.n_params;
+  *n = h->c.Lx.n_params;
   return GFNX_OK;
 }
 
 gfnx_status gfnx_set_params(gfnx_ctx* h, const double* flat, int64_t n, double log_z) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "set_params: size mismatch");
+    if (n != c.Lx.n_params) fail(GFNX_ERR_CONFIG, "set_params: size mismatch");
     if (c.check_mode()) {
       cuda_check(cudaMemcpyAsync(c.p64, flat, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream), "params");
     } else {
-      std::vector<float> f(flat, flat + n);
-      cuda_check(cudaMemcpyAsync(c.p32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice, c.stream), "params");
+      const std::vector<double> d = to_device_layout(c, flat);
+      std::vector<float> f(d.begin(), d.end());
+      cuda_check(cudaMemcpyAsync(c.p32, f.data(), sizeof(float) * f.size(), cudaMemcpyHostToDevice, c.stream), "params");
       cuda_check(cudaStreamSynchronize(c.stream), "sync");
       fast_sync_weights(c);
     }
@@ -608,15 +675,15 @@ gfnx_status gfnx_set_params(gfnx_ctx* h, const double* flat, int64_t n, double l
 gfnx_status gfnx_get_params(gfnx_ctx* h, double* flat, int64_t n, double* log_z) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "get_params: size mismatch");
+    if (n != c.Lx.n_params) fail(GFNX_ERR_CONFIG, "get_params: size mismatch");
     if (flat) {
       if (c.check_mode()) {
         cuda_check(cudaMemcpyAsync(flat, c.p64, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "params");
       } else {
-        std::vector<float> f(n);
-        cuda_check(cudaMemcpyAsync(f.data(), c.p32, sizeof(float) * n, cudaMemcpyDeviceToHost, c.stream), "params");
+        std::vector<float> f(c.L.n_params);
+        cuda_check(cudaMemcpyAsync(f.data(), c.p32, sizeof(float) * f.size(), cudaMemcpyDeviceToHost, c.stream), "params");
         cuda_check(cudaStreamSynchronize(c.stream), "sync");
-        for (int64_t i = 0; i < n; ++i) flat[i] = f[i];
+        to_user_layout(c, f.data(), flat);
       }
     }
     if (log_z) cuda_check(cudaMemcpyAsync(log_z, c.d_scalars, sizeof(double), cudaMemcpyDeviceToHost, c.stream), "logz");
@@ -635,14 +702,14 @@ gfnx_status gfnx_set_adam_state(gfnx_ctx* h, const double* m, const double* v, i
       if (m) cuda_check(cudaMemcpy(c.m64, m, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
       if (v) cuda_check(cudaMemcpy(c.v64, v, sizeof(double) * n, cudaMemcpyHostToDevice), "adam");
     } else {
-      if (m) {
-        std::vector<float> f(m, m + n);
-        cuda_check(cudaMemcpy(c.m32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "adam");
-      }
-      if (v) {
-        std::vector<float> f(v, v + n);
-        cuda_check(cudaMemcpy(c.v32, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "adam");
-      }
+      auto put = [&](const double* x, float* dst) {
+        if (!x) return;
+        const std::vector<double> d = to_device_layout(c, x);
+        std::vector<float> f(d.begin(), d.end());
+        cuda_check(cudaMemcpy(dst, f.data(), sizeof(float) * n, cudaMemcpyHostToDevice), "adam");
+      };
+      put(m, c.m32);
+      put(v, c.v32);
     }
     double zs[2] = {z_m, z_v};
     cuda_check(cudaMemcpy(c.d_scalars + 1, zs, sizeof zs, cudaMemcpyHostToDevice), "adam z");
@@ -664,7 +731,7 @@ gfnx_status gfnx_get_adam_state(gfnx_ctx* h, double* m, double* v, int64_t* t, d
       } else {
         std::vector<float> f(n);
         cuda_check(cudaMemcpy(f.data(), s32, sizeof(float) * n, cudaMemcpyDeviceToHost), "adam");
-        for (int64_t i = 0; i < n; ++i) dst[i] = f[i];
+        to_user_layout(c, f.data(), dst);
       }
     };
     get(m, c.m64, c.m32);
@@ -694,7 +761,7 @@ struct CkptTensor {
 };
 
 std::vector<CkptTensor> ckpt_tensors(const Ctx& c) {  // MlpParams::tensors() order (nn.cpp:8-19)
-  const MlpLayout& L = c.L;
+  const MlpLayout& L = c.Lx;
   std::vector<CkptTensor> v;
   for (int l = 0; l < L.n_trunk; ++l) {
     v.push_back({{L.dims[l], L.dims[l + 1]}, L.off_w[l], (int64_t)L.dims[l] * L.dims[l + 1]});
@@ -733,7 +800,7 @@ void get_tensor(std::FILE* f, const std::vector<int64_t>& shape, double* x, int6
 gfnx_status gfnx_save_checkpoint(gfnx_ctx* h, const char* path, int64_t step) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    const int64_t n = c.L.n_params;
+    const int64_t n = c.Lx.n_params;
     std::vector<double> p(n), m(n), v(n);
     double z = 0, zm = 0, zv = 0;
     int64_t t = 0, zt = 0;
@@ -743,7 +810,7 @@ gfnx_status gfnx_save_checkpoint(gfnx_ctx* h, const char* path, int64_t step) {
     if (!f) fail(GFNX_ERR_CONFIG, std::string("checkpoint: cannot open for write: ") + path);
     const auto ts = ckpt_tensors(c);
     std::fwrite(kCkptMagic, 1, 8, f);
-    put_i64(f, c.L.n_trunk);
+    put_i64(f, c.Lx.n_trunk);
     for (const auto& x : ts) put_tensor(f, x.shape, p.data() + x.off, x.n);
     put_tensor(f, {1}, &z, 1);
     put_i64(f, t);
@@ -764,7 +831,7 @@ gfnx_status gfnx_save_checkpoint(gfnx_ctx* h, const char* path, int64_t step) {
 gfnx_status gfnx_load_checkpoint(gfnx_ctx* h, const char* path, int64_t* step) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    const int64_t n = c.L.n_params;
+    const int64_t n = c.Lx.n_params;
     std::vector<double> p(n), m(n), v(n);
     double z = 0, zm = 0, zv = 0;
     std::FILE* f = std::fopen(path, "rb");
@@ -776,7 +843,7 @@ gfnx_status gfnx_load_checkpoint(gfnx_ctx* h, const char* path, int64_t* step) {
     char magic[8];
     if (std::fread(magic, 1, 8, f) != 8 || memcmp(magic, kCkptMagic, 8) != 0)
       fail(GFNX_ERR_CONFIG, std::string("checkpoint: bad magic in ") + path);
-    if (get_i64(f) != c.L.n_trunk) fail(GFNX_ERR_CONFIG, "checkpoint: trunk depth does not match the model");
+    if (get_i64(f) != c.Lx.n_trunk) fail(GFNX_ERR_CONFIG, "checkpoint: trunk depth does not match the model");
     const auto ts = ckpt_tensors(c);
     for (const auto& x : ts) get_tensor(f, x.shape, p.data() + x.off, x.n);
     get_tensor(f, {1}, &z, 1);
@@ -1014,16 +1081,16 @@ gfnx_status gfnx_compute_grads(gfnx_ctx* h, double* loss) {
 gfnx_status gfnx_get_grads(gfnx_ctx* h, double* flat, int64_t n, double* d_log_z) {
   return guard(h, [&] {
     Ctx& c = h->c;
-    if (n != c.L.n_params) fail(GFNX_ERR_CONFIG, "get_grads: size mismatch");
+    if (n != c.Lx.n_params) fail(GFNX_ERR_CONFIG, "get_grads: size mismatch");
     if (!c.has_grads) fail(GFNX_ERR_CONTRACT, "get_grads: no gradients computed");
     cuda_check(cudaStreamSynchronize(c.stream), "sync");
     if (flat) {
       if (c.check_mode()) {
         cuda_check(cudaMemcpy(flat, c.g64, sizeof(double) * n, cudaMemcpyDeviceToHost), "grads");
       } else {
-        std::vector<float> f(n);
-        cuda_check(cudaMemcpy(f.data(), c.g32, sizeof(float) * n, cudaMemcpyDeviceToHost), "grads");
-        for (int64_t i = 0; i < n; ++i) flat[i] = f[i];
+        std::vector<float> f(c.L.n_params);
+        cuda_check(cudaMemcpy(f.data(), c.g32, sizeof(float) * f.size(), cudaMemcpyDeviceToHost), "grads");
+        to_user_layout(c, f.data(), flat);
       }
     }
     if (d_log_z) cuda_check(cudaMemcpy(d_log_z, c.d_scalars + 3, sizeof(double), cudaMemcpyDeviceToHost), "dlogz");

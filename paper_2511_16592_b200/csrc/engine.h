@@ -136,7 +136,9 @@ struct Ctx {
   gfnx_train_desc train{};
   gfnx_env_shape shape{};
   EnvParams P{};
-  MlpLayout L{};
+  MlpLayout L{};   // device layout (bf16 fast paths: hidden widths zero-padded to the kernel's)
+  MlpLayout Lx{};  // the user's layout (MlpParams::tensors() of the requested widths): the ABI
+  std::vector<int64_t> xmap;  // user parameter index -> device index (empty: same layout)
   int device = 0, rank = 0, world = 1;
   int B = 0, Bl = 0, b0 = 0;  // global batch, local slice [b0, b0+Bl)
   int Bcap = 0;               // trajectory capacity of the batch arrays (>= Bl: lockstep pads to 128)

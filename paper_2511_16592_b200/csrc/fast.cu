@@ -2703,8 +2703,8 @@ void with_kernels(Ctx& c, F&& fn) {
   int H = 0;
   if (!supported(c, &H))
     raise_error(GFNX_ERR_CONFIG,
-                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (H=128/256) and DAG (H=128) in "
-                "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
+                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (widths <= 256) and DAG "
+                "(widths <= 128); use precision=GFNX_PREC_FP64_CHECK for other configurations");
   if (c.env.kind == GFNX_ENV_HYPERGRID) {
     if (H == 256) fn(Kernels<HypergridEnv, 256, 16>{});
     else fn(Kernels<HypergridEnv, 128, 16>{});
@@ -3031,8 +3031,8 @@ void fast_init(Ctx& c) {
   int H = 0;
   if (!supported(c, &H))
     raise_error(GFNX_ERR_CONFIG,
-                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (H=128/256) and DAG (H=128) in "
-                "this build; use precision=GFNX_PREC_FP64_CHECK for other configurations");
+                "bf16 fast path supports 2-hidden-layer MLPs on hypergrid (widths <= 256) and DAG "
+                "(widths <= 128); use precision=GFNX_PREC_FP64_CHECK for other configurations");
   auto* f = new FastState();
   c.fast = f;
   cudaDeviceGetAttribute(&f->num_sms, cudaDevAttrMultiProcessorCount, c.device);

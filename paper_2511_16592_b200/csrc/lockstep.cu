@@ -1928,7 +1928,7 @@ bool ls_supported(const Ctx& c, std::string* why) {
   if (c.train.objective == GFNX_OBJ_SUBTB && c.P.T > kLsSubTBMaxT) return no("bitseq/Ising SubTB supports T <= 128");
   if (c.L.n_trunk < 2 || c.L.n_trunk > kMaxNL) return no("bitseq/Ising fast path needs 2..4 hidden layers");
   for (int l = 1; l <= c.L.n_trunk; ++l)
-    if (c.L.dims[l] != kH) return no("bitseq/Ising fast path needs hidden width 256");
+    if (c.L.dims[l] != kH) return no("bitseq/Ising fast path needs hidden widths <= 256");
   if (kind == GFNX_ENV_BITSEQ) {
     if (c.P.bs_vocab != 256) return no("bitseq fast path needs k = 8 (256-word slots)");
     if (c.P.bs_slots > 32) return no("bitseq fast path supports <= 32 slots");

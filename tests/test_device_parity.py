@@ -37,14 +37,14 @@ pytestmark = pytest.mark.gpu
 FIELDS = ("lengths", "fwd_actions", "bwd_actions", "log_rewards", "log_pb", "delta", "terminal_state")
 
 
-def _bitseq(n_bits, batch, objective="tb", scheme=0):
+def _bitseq(n_bits, batch, objective="tb", scheme=0, **kw):
     return (abi.env_desc(abi.BITSEQ, bs_n_bits=n_bits, bs_k=8, bs_scheme=scheme),
-            abi.train_desc(abi.BITSEQ, batch=batch, objective=objective))
+            abi.train_desc(abi.BITSEQ, batch=batch, objective=objective, **kw))
 
 
-def _ising(side, batch, objective="tb"):
+def _ising(side, batch, objective="tb", **kw):
     return (abi.env_desc(abi.ISING, is_side=side, is_sigma=0.2),
-            abi.train_desc(abi.ISING, batch=batch, objective=objective))
+            abi.train_desc(abi.ISING, batch=batch, objective=objective, **kw))
 
 
 # ---------------------------------------------------------------------------
@@ -152,6 +152,15 @@ SAME_BATCH = [
     ("ising_6x6_db_b256", lambda: _ising(6, 256, "db"), IS, True),
     ("ising_6x6_subtb_b256", lambda: _ising(6, 256, "subtb"), IS, True),
     ("ising_4x4_db_b200_ragged", lambda: _ising(4, 200, "db"), IS, True),
+    # narrower MLPs than the kernels' widths run zero-padded (api.cu pad_layout): the
+    # reference's acceptance-criterion-5 Ising network (2 x 128, batch 32), mixed widths,
+    # hypergrid / DAG below 128
+    ("ising_3x3_h128_b32", lambda: _ising(3, 32, hidden=(128, 128)), IS, True),
+    ("ising_6x6_h64_96_160_db_b96", lambda: _ising(6, 96, "db", hidden=(64, 96, 160)), IS, True),
+    ("bitseq_n48_h128_b128", lambda: _bitseq(48, 128, hidden=(128, 128)), LS, True),
+    ("hypergrid_h64_b512", lambda: abi.config("hypergrid_db_b65536", batch=512, hidden=[64, 64]), F, False),
+    ("hypergrid_h100_200_b512", lambda: abi.config("hypergrid_db_b65536", batch=512, hidden=[100, 200]), F, False),
+    ("dag_h64_mdb_b256", lambda: abi.config("dag_mdb_b8192", batch=256, hidden=[64, 64]), F, False),
 ]
 
 
