@@ -83,6 +83,15 @@ GFNX_DEV uint32_t smem_u32(const void* p) {
 
 GFNX_DEV uint32_t lane_id() { return threadIdx.x & 31; }
 
+// 2^x on the SFU with flush-to-zero (one MUFU.EX2, no subnormal range fix-ups); results
+// below 2^-126 become 0 — for softmax terms exp(x - lse) that never matter
+GFNX_DEV float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float kLog2e = 1.4426950408889634f;
+
 GFNX_DEV uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);

@@ -335,16 +335,16 @@ struct LogEpi : EpiBase {
                    "r"(pk[8 * q + 5]), "r"(pk[8 * q + 6]), "r"(pk[8 * q + 7])
                    : "memory");
     if (lm == 0u) return;
-    const float nm = fmaxf(l.mx, cm);
+    const float nm = fmaxf(l.mx, cm), nm2 = -nm * kLog2e;
     float s = 0.f;
     if constexpr (std::is_same<E, BitseqEnv>::value) {  // all 32 columns legal here
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s += __expf(v[i] - nm);
+      for (int i = 0; i < 32; ++i) s += ex2_ftz(fmaf(v[i], kLog2e, nm2));
     } else {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) s += ((lm >> i) & 1u) ? __expf(v[i] - nm) : 0.f;
+      for (int i = 0; i < 32; ++i) s += ((lm >> i) & 1u) ? ex2_ftz(fmaf(v[i], kLog2e, nm2)) : 0.f;
     }
-    l.s = l.s * __expf(l.mx - nm) + s;  // l.mx = -inf -> factor 0
+    l.s = l.s * ex2_ftz((l.mx - nm) * kLog2e) + s;  // l.mx = -inf -> factor 0
     l.mx = nm;
   }
   // the four 64-column parts of a row leave (max, sum exp) partials in scratch; finish()
@@ -796,6 +796,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     const size_t r = (size_t)m * kTile + row;
     const int c0 = n * 256 + col0;
     const uint32_t lm = Lock<E>::legal32c(e.P, l.lw, c0);
+    const float nl2 = -l.lse * kLog2e;
     uint32_t pk[16];
     float bias[32];
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c0);
@@ -810,7 +811,7 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const float x = __bfloat162float(__float2bfloat16(v[i] + bias[i]));
-      float d = ((lm >> i) & 1u) ? -l.g * __expf(x - l.lse) : 0.f;
+      float d = ((lm >> i) & 1u) ? -l.g * ex2_ftz(fmaf(x, kLog2e, nl2)) : 0.f;
       if (c0 + i == l.act) d += l.g;
       v[i] = d;
     }
