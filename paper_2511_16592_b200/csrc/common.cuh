@@ -104,6 +104,16 @@ GFNX_DEV uint32_t pack_bf16x2_relu(float lo, float hi) {
   asm("cvt.rn.relu.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
+// (a0, a1) += s * (the two bf16 halves of w) as one FFMA2 (fma.rn.f32x2: per lane the same
+// single rounding as FFMA)
+GFNX_DEV void fma2_bf16(uint32_t& a0, uint32_t& a1, float s, uint32_t w) {
+  unsigned long long acc, m, sv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(acc) : "r"(a0), "r"(a1));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "r"(w << 16), "r"(w & 0xffff0000u));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+  asm("fma.rn.f32x2 %0, %1, %2, %0;" : "+l"(acc) : "l"(sv), "l"(m));
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(a0), "=r"(a1) : "l"(acc));
+}
 // ReLU(acc + bias) of an fp32 accumulator pair (raw TMEM words) as one packed bf16 pair:
 // one FADD2 (add.rn.f32x2, IEEE fp32 per lane like FADD) + one cvt
 GFNX_DEV uint32_t bias_relu_pack(uint32_t a_lo, uint32_t a_hi, float2 b) {

@@ -397,7 +397,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
   uint8_t* atile = whimg + NH * H * 2;    // 128 x AK bf16 activations
   __nv_bfloat16* w1s = reinterpret_cast<__nv_bfloat16*>(atile + kTile * AK * 2);  // [O][H] if W1S
   const __nv_bfloat16* w1 = W1S ? w1s : a.W.w1;
-  __shared__ float h1init[H], b2s[H];
+  __shared__ __align__(16) float h1init[H];
+  __shared__ __align__(16) float b2s[H];
   __shared__ float bhs[NH];
   __shared__ Key skeys[128];
   __shared__ double row_u[kTile];
@@ -502,10 +503,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
     tmem_ld32(lane_base + tcol, r);
     tmem_wait_ld();
     uint32_t pk[16];
+    if (bias) {
+      const float2* b2 = reinterpret_cast<const float2*>(bias);
 #pragma unroll
-    for (int i = 0; i < 16; ++i)
-      pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]) + (bias ? bias[2 * i] : 0.f),
-                               __uint_as_float(r[2 * i + 1]) + (bias ? bias[2 * i + 1] : 0.f));
+      for (int i = 0; i < 16; ++i) pk[i] = bias_relu_pack(r[2 * i], r[2 * i + 1], b2[i]);
+    } else {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) pk[i] = pack_bf16x2_relu(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+    }
     if (mword) *mword = relu_mask16(pk);
     st_row32(atile, row, acol, pk);
   };
@@ -586,10 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           for (int c = 0; c < 4; ++c) {
             const uint32_t wv[4] = {w[d][c].x, w[d][c].y, w[d][c].z, w[d][c].w};
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              r[8 * c + 2 * e] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e]) + dv[d] * bf16_lo(wv[e]));
-              r[8 * c + 2 * e + 1] = __float_as_uint(__uint_as_float(r[8 * c + 2 * e + 1]) + dv[d] * bf16_hi(wv[e]));
-            }
+            for (int e = 0; e < 4; ++e) fma2_bf16(r[8 * c + 2 * e], r[8 * c + 2 * e + 1], dv[d], wv[e]);
           }
         }
         // (more than 2 changed features: general path)

@@ -10,7 +10,11 @@ from paper_2511_16592_b200 import abi, engine
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("name,kw", [("hypergrid_tb_b16", {}), ("dag_mdb_b8192", dict(batch=64))])
+@pytest.mark.parametrize("name,kw", [
+    ("hypergrid_tb_b16", {}), ("dag_mdb_b8192", dict(batch=64)),
+    # narrower MLPs run zero-padded on the device; files carry the user's widths
+    ("hypergrid_tb_b16", dict(hidden=[64, 48])), ("ising_tb_b32768", dict(batch=32, hidden=[128, 96])),
+])
 def test_checkpoint_round_trip_with_reference(tmp_path, name, kw):
     if not O.ref_available("port"):
         pytest.skip("oracle/_ref not built")
