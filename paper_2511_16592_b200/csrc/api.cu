@@ -1354,7 +1354,7 @@ gfnx_status gfnx_counters(gfnx_ctx* h, int64_t* out, int32_t n) {
 
 // diagnostic clock slots: rollout [0..8], wgrad passes [9..11], sampler sub-phases [12..14],
 // bwd phases [15..20]
-constexpr int kPhaseSlots = 24;
+constexpr int kPhaseSlots = 32;
 
 gfnx_status gfnx_phase_timers(gfnx_ctx* h, int32_t mode, int64_t* out, int32_t n) {
   return guard(h, [&] {

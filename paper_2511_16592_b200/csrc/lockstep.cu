@@ -243,6 +243,23 @@ __global__ void __launch_bounds__(256) k_ls_layer1(L1Args a) {
   a.mask1[r * (kH / 8) + lane] = (uint8_t)mb;
 }
 
+// ReLU mask of 32 consecutive bf16 columns (16 packed pairs, values >= 0 or +0), bit k <->
+// column k (set when nonzero): the two flags of pair i land at bits i / 16 + i in 4
+// instructions per pair, then one bit interleave of the two halves (Hacker's Delight 7-2)
+GFNX_DEV uint32_t relu_mask32_seq(const uint32_t (&pk)[16]) {
+  uint32_t x = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const uint32_t y = (pk[i] & 0x7FFF7FFFu) + 0x7FFF7FFFu;  // flags at bit 15 (column 2i), 31 (2i + 1)
+    x |= (y >> (15 - i)) & (0x00010001u << i);
+  }
+  x = ((x & 0x0000FF00u) << 8) | ((x >> 8) & 0x0000FF00u) | (x & 0xFF0000FFu);
+  x = ((x & 0x00F000F0u) << 4) | ((x >> 4) & 0x00F000F0u) | (x & 0xF00FF00Fu);
+  x = ((x & 0x0C0C0C0Cu) << 2) | ((x >> 2) & 0x0C0C0C0Cu) | (x & 0xC3C3C3C3u);
+  x = ((x & 0x22222222u) << 1) | ((x >> 1) & 0x22222222u) | (x & 0x99999999u);
+  return x;
+}
+
 struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
   struct Args {
     const float* b;
@@ -253,17 +270,15 @@ struct HidEpi : EpiBase {  // +b, ReLU -> h image + mask
   static __device__ const float* bias_src(const Args& e) { return e.b; }
   static __device__ void set_bias(Args& e, const float* b) { e.b = b; }
   static __device__ void apply(const Args& e, int m, int, int row, int col0, float (&v)[32], float*, Local&) {
-    uint32_t pk[16], mb = 0;
+    uint32_t pk[16];
     const float4* bb = reinterpret_cast<const float4*>(e.b + col0);
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const float4 q = bb[i];
-      pk[2 * i] = pack_bf16x2_relu(v[4 * i] + q.x, v[4 * i + 1] + q.y);
-      pk[2 * i + 1] = pack_bf16x2_relu(v[4 * i + 2] + q.z, v[4 * i + 3] + q.w);
+      pk[2 * i] = bias_relu_pack(__float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]), make_float2(q.x, q.y));
+      pk[2 * i + 1] = bias_relu_pack(__float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3]), make_float2(q.z, q.w));
     }
-#pragma unroll
-    for (int i = 0; i < 16; ++i)  // bit 2i / 2i+1 <-> columns 2i / 2i+1 (values >= 0: nonzero = active)
-      mb |= (((pk[i] & 0x7FFFu) + 0x7FFFu) >> 15 & 1u) << (2 * i) | (((pk[i] & 0x7FFF0000u) + 0x7FFF0000u) >> 31) << (2 * i + 1);
+    const uint32_t mb = relu_mask32_seq(pk);  // bit k <-> column col0 + k
     st_row32_g(e.h + (size_t)m * (kTile * kH * 2), row, col0, pk);
     const size_t r = (size_t)m * kTile + row;
     *reinterpret_cast<uint32_t*>(e.mask + r * (kH / 8) + col0 / 8) = mb;
@@ -1214,14 +1229,6 @@ struct PersistArgs {
 };
 
 // ReLU bit mask of 32 columns in the lockstep byte-mask order (bit i of the word <-> column i)
-GFNX_DEV uint32_t relu_mask32_seq(const uint32_t (&pk)[16]) {
-  uint32_t mb = 0;
-#pragma unroll
-  for (int i = 0; i < 16; ++i)
-    mb |= (((pk[i] & 0x7FFFu) + 0x7FFFu) >> 15 & 1u) << (2 * i) |
-          (((pk[i] & 0x7FFF0000u) + 0x7FFF0000u) >> 31) << (2 * i + 1);
-  return mb;
-}
 
 // (streaming store: evict-first in L2, so the activation images written once per step do
 // not push the per-row layer-1 state out of L2)
@@ -1313,6 +1320,14 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   if (tid == 0) load_w(a.l1_mma ? 0 : 1);
   const int T = a.T, Bl = a.Bl;
   long long pc[3] = {0, 0, 0}, tclk = clock64();
+  long long hs[3] = {0, 0, 0}, hclk = 0;  // hidden-layer sub-phases (image wait, MMA, epilogue)
+  auto hmark = [&](int k) {
+    if (a.phase && tid == 0) {
+      const long long tn = clock64();
+      if (k >= 0) hs[k] += tn - hclk;
+      hclk = tn;
+    }
+  };
   auto pmark = [&](int k) {
     if (a.phase && tid == 0) {
       const long long tn = clock64();
@@ -1431,8 +1446,10 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
     // ---- hidden layers 2..NL: MMA per tile (A from TMEM), epilogue back into the same columns
     const int l0 = a.l1_mma ? 0 : 1;
     for (int l = l0; l < a.NL; ++l) {
+      hmark(-1);
       if (tid == 0) mbar_wait(&wbar, wph);
       wph ^= 1;
+      hmark(0);
       for (int j = 0; j < ntile; ++j) {
         const int tile = blockIdx.x + j * gridDim.x;
         const int b = tile * kTile + row;
@@ -1465,6 +1482,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
           row_u[j][row] = uniform_scalar(fold_in(skeys[t], (uint64_t)(a.b0 + b)));
         emit_pending();
         mma_wait();
+        hmark(1);
         if (j == ntile - 1 && tid == 0) load_w(l + 1 < a.NL ? l + 1 : a.NL);  // wbuf free now
         uint32_t mw[4];
         const float* bl = bias_s[l];  // shared memory (a generic pointer into one array: LDS)
@@ -1479,10 +1497,8 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
             const float4 bq = bb[i];
-            pk[2 * i] = pack_bf16x2_relu(__uint_as_float(rr[4 * i]) + bq.x,
-                                         __uint_as_float(rr[4 * i + 1]) + bq.y);
-            pk[2 * i + 1] = pack_bf16x2_relu(__uint_as_float(rr[4 * i + 2]) + bq.z,
-                                             __uint_as_float(rr[4 * i + 3]) + bq.w);
+            pk[2 * i] = bias_relu_pack(rr[4 * i], rr[4 * i + 1], make_float2(bq.x, bq.y));
+            pk[2 * i + 1] = bias_relu_pack(rr[4 * i + 2], rr[4 * i + 3], make_float2(bq.z, bq.w));
           }
           mw[q] = relu_mask32_seq(pk);
           tmem_st16(lane_base + kH + 128 * j + (col >> 1), pk);
@@ -1492,6 +1508,7 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
         pend_j = j;
         pend_m = m;
         publish();
+        hmark(2);
       }
     }
     pmark(1);
@@ -1689,6 +1706,8 @@ __global__ void __launch_bounds__(256, 1) k_ls_persist(PersistArgs a) {
   }
   if (a.phase && tid == 0)
     for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)a.phase + k, (unsigned long long)pc[k]);
+  if (a.phase && tid == 0)
+    for (int k = 0; k < 3; ++k) atomicAdd((unsigned long long*)a.phase + 22 + k, (unsigned long long)hs[k]);
   if (tid == 0) mbar_wait(&wbar, wph);  // the prefetched image has landed before exit
   tc_fence_before();
   __syncthreads();

@@ -436,7 +436,8 @@ class Trainer:
     PHASES = ("loop_barrier", "layer1", "hidden_mma", "hidden_epilogue", "head_mma", "sample_step",
               "tile_steps", "active_slot_steps", "sample_step_max", "wgrad_pass_a", "wgrad_pass_b",
               "wgrad_pass_c", "sample_sampler", "sample_envstep", "sample_features", "bwd_wait_dlogits",
-              "bwd_head", "bwd_dz2", "bwd_w2mma_db2", "bwd_dz1", "bwd_tiles", "bwd_rowload")
+              "bwd_head", "bwd_dz2", "bwd_w2mma_db2", "bwd_dz1", "bwd_tiles", "bwd_rowload",
+              "persist_hid_wimg", "persist_hid_mma", "persist_hid_epi")
 
     def phase_timers(self, mode: int):
         """Rollout phase clocks (diagnostic): 1 enable, 0 disable, 2 read + clear -> dict."""

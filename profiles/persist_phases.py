@@ -20,5 +20,7 @@ names = list(ph.keys())
 steps = e.is_side * e.is_side if hasattr(e, "is_side") else 1
 for k, n in zip(range(3), ("layer1", "hidden", "head_sample")):
     print(n, round(ph[names[k]] / 3 / 148 / steps / 1965.0, 2), "us per step per CTA")
+for n in ("persist_hid_wimg", "persist_hid_mma", "persist_hid_epi"):
+    print(" ", n, round(ph[n] / 3 / 148 / steps / 1965.0, 2), "us per step per CTA")
 print("persist ms/launch", tr.profile_read().get("k_ls_persist", (0, 1))[0] / 3)
 tr.close()
