@@ -25,6 +25,7 @@ import json
 import os
 import statistics
 import subprocess
+import threading
 import sys
 import time
 
@@ -218,21 +219,43 @@ class ClockSampler:
         self.p = None
 
     def start(self):
+        """Launch the sampler and wait (<= 5 s) for its first line: nvidia-smi needs ~0.5-1 s
+        to start, longer than a short timed region."""
+        self.lines, self.i0 = [], 0
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-lms", "100", "-i", str(self.gpu)],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.p = None
+            return
+
+        def pump():
+            for line in self.p.stdout:
+                self.lines.append(line)
+
+        self.t = threading.Thread(target=pump, daemon=True)
+        self.t.start()
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 5.0 and self.p.poll() is None:
+            time.sleep(0.02)
+        self.i0 = len(self.lines)  # samples from here on fall inside the measured region
 
     def stop(self):
         if not self.p:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t0 = time.time()  # at least one sample taken after the region started
+        while len(self.lines) <= self.i0 and time.time() - t0 < 1.0 and self.p.poll() is None:
+            time.sleep(0.02)
         self.p.terminate()
-        out, _ = self.p.communicate(timeout=10)
+        try:
+            self.p.wait(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.t.join(timeout=5)
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in out.strip().splitlines():
+        for line in self.lines[self.i0:]:
             f = [x.strip() for x in line.split(",")]
             if len(f) < 8:
                 continue
