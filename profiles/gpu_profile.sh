@@ -13,6 +13,6 @@ ROWS=$(python -c "import json; d=json.loads(open('gpurun_out/bench_full_$R.log')
 python profiles/summarize_ncu.py gpurun_out/full_$R.ncu-rep gpurun_out/${R}_ncu_summary.md $ROWS \
   "ncu --set full, bench.py --steps $K --warmup $W timed iteration W+$J (rows = mean rows per timed iteration)"
 tail -2 gpurun_out/ncu_full_$R.log
-cp profiles/ncu_traffic.json gpurun_out/ncu_traffic.json  # (summarize_ncu.py wrote it on the box)
+# (summarize_ncu.py writes gpurun_out/ncu_traffic.json next to the summary: copy it into profiles/)
 bash profiles/ncu_brief.sh gpurun_out/full_$R.ncu-rep > gpurun_out/${R}_ncu_brief.txt 2>&1
 mkdir -p /tmp/ncu_reps && mv gpurun_out/*.ncu-rep /tmp/ncu_reps/  # keep the merge-back under 64 MiB
