@@ -1582,9 +1582,10 @@ GFNX_DEV double warp_sum_d(double v) {
 
 constexpr int kSubTBMaxT = 128;  // supported() caps max_traj_len at 128 on this path
 
-__global__ void __launch_bounds__(256, 4) k_fast_loss_warp(LossArgs a) {
-  __shared__ double sub_F[8][kSubTBMaxT + 1], sub_c[8][kSubTBMaxT + 1], sub_S[8][kSubTBMaxT + 1],
-      sub_T[8][kSubTBMaxT + 1];
+// SUBTB: the only objective with per-warp shared scratch (34 KB per block); the others run
+// 8 blocks per SM (register-bound at 32 registers)
+template <bool SUBTB>
+__global__ void __launch_bounds__(256, SUBTB ? 4 : 8) k_fast_loss_warp(LossArgs a) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int nw = gridDim.x * (blockDim.x >> 5);
   const int* cnt = a.batch.counters;
@@ -1631,7 +1632,9 @@ __global__ void __launch_bounds__(256, 4) k_fast_loss_warp(LossArgs a) {
       }
       ls = warp_sum_d(ls);
       if (lane == 0) loss += ls;
-    } else if (a.objective == GFNX_OBJ_SUBTB) {  // subtb_loss :144-180, lanes over j then k
+    } else if constexpr (SUBTB) {  // subtb_loss :144-180, lanes over j then k
+      __shared__ double sub_F[8][kSubTBMaxT + 1], sub_c[8][kSubTBMaxT + 1], sub_S[8][kSubTBMaxT + 1],
+          sub_T[8][kSubTBMaxT + 1];
       double* F = sub_F[wib];
       double* cum = sub_c[wib];
       double* Sg = sub_S[wib];
@@ -2653,7 +2656,8 @@ struct Kernels {
     la.scalars = c.d_scalars;
     {
       ProfScope ps(c, "k_fast_loss");
-      k_fast_loss_warp<<<f.loss_wblocks, 256, 0, c.stream>>>(la);
+      if (c.train.objective == GFNX_OBJ_SUBTB) k_fast_loss_warp<true><<<f.loss_wblocks, 256, 0, c.stream>>>(la);
+      else k_fast_loss_warp<false><<<f.loss_wblocks, 256, 0, c.stream>>>(la);
     }
     k_loss_finalize<<<1, 256, 0, c.stream>>>(f.lpart, f.loss_wblocks, c.d_scalars,
                                              c.train.objective == GFNX_OBJ_TB, c.batch.counters + 3);
