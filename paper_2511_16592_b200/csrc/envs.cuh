@@ -81,9 +81,29 @@ struct HypergridEnv {
   }
   __host__ __device__ static int num_parents(const EnvParams& P, const State& s) {
     if (s.term) return 1;
-    int n = 0;
-    for (int i = 0; i < P.hg_dim; ++i) n += s.c(i) > 0;
-    return n;
+    // nonzero coordinate bytes (bytes >= hg_dim are 0): high bit of ((b & 0x7f) + 0x7f) | b
+    const uint64_t L7 = 0x7f7f7f7f7f7f7f7full;
+    const uint64_t nz = (((s.cw & L7) + L7) | s.cw) & 0x8080808080808080ull;
+#ifdef __CUDA_ARCH__
+    return __popcll(nz);
+#else
+    return __builtin_popcountll(nz);
+#endif
+  }
+  // every legal forward action as a bit mask (bit a <-> action a), SWAR over the coordinate
+  // bytes: for c < 128 and side - 1 <= 128 the byte (c | 0x80) - (side - 1) keeps its high bit
+  // iff c >= side - 1; the multiply gathers the per-byte flags into bits 0..7
+  __host__ __device__ static uint32_t legal_mask(const EnvParams& P, const State& s) {
+    if (s.term) return 0u;
+    uint32_t m = 0;
+    if (P.hg_side <= 128) {
+      const uint64_t H = 0x8080808080808080ull;
+      const uint64_t ge = ((s.cw | H) - 0x0101010101010101ull * (uint64_t)(P.hg_side - 1)) & H;
+      m = (uint32_t)((((~ge & H) >> 7) * 0x0102040810204080ull) >> 56) & ((1u << P.hg_dim) - 1u);
+    } else {
+      for (int i = 0; i < P.hg_dim; ++i) m |= (s.c(i) < P.hg_side - 1 ? 1u : 0u) << i;
+    }
+    return m | (1u << P.stop);
   }
   __host__ __device__ static int backward_action(const EnvParams&, int a) { return a; }
   __host__ __device__ static double log_reward(const EnvParams& P, const State& s) {

@@ -71,6 +71,21 @@ struct FastState {
   int loss_wblocks = 0;               // warp-per-trajectory loss: 8 trajectories per block
 };
 
+// legal forward actions among the first AMAX columns as a bit mask (hypergrid: SWAR)
+template <class Env, int AMAX>
+GFNX_DEV uint32_t legal_bits(const EnvParams& P, const typename Env::State& s, int A) {
+  if constexpr (std::is_same<Env, HypergridEnv>::value) {
+    return Env::legal_mask(P, s) & (A >= 32 ? 0xffffffffu : ((1u << A) - 1u)) &
+           (AMAX >= 32 ? 0xffffffffu : ((1u << AMAX) - 1u));
+  } else {
+    uint32_t lm = 0;
+#pragma unroll
+    for (int c = 0; c < AMAX; ++c)
+      if (c < A && Env::legal(P, s, c)) lm |= 1u << c;
+    return lm;
+  }
+}
+
 // training-forward record of every emitted row from the rollout's raw head outputs:
 // masked log-softmax (tape.cpp:177-213) -> probs[A], log pi(a|s), log pi(stop|s), flow
 template <class Env, int NH>
@@ -93,14 +108,11 @@ GFNX_DEV void row_stats_one(const EnvParams& P, const uint32_t* __restrict__ sts
     lg[4 * k + 3] = v.w;
   }
   const int A = P.A;
-  uint32_t lm = 0;
+  const uint32_t lm = legal_bits<Env, NH>(P, s, A);
   float hi = -INFINITY;
 #pragma unroll
   for (int c = 0; c < NH; ++c)
-    if (c < A && Env::legal(P, s, c)) {
-      lm |= 1u << c;
-      hi = fmaxf(hi, lg[c]);
-    }
+    if ((lm >> c) & 1u) hi = fmaxf(hi, lg[c]);
   float e[NH], z = 0.f;
 #pragma unroll
   for (int c = 0; c < NH; ++c) {
@@ -241,8 +253,8 @@ template <class Env, int AMAX>
 GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const float (&logit)[AMAX],
                         int A, double eps, double u01, const double* inv_legal, bool* bad,
                         float (&e)[AMAX], float& hi, float& z, float& rz) {
-  uint32_t lm = 0;
-  int legal = 0;
+  const uint32_t lm = legal_bits<Env, AMAX>(P, s, A);
+  const int legal = __popc(lm);
   hi = -INFINITY;
   z = 1.f;
   rz = 1.f;
@@ -250,11 +262,7 @@ GFNX_DEV int sample_row(const EnvParams& P, const typename Env::State& s, const 
   for (int c = 0; c < AMAX; ++c) e[c] = 0.f;
 #pragma unroll
   for (int c = 0; c < AMAX; ++c)
-    if (c < A && Env::legal(P, s, c)) {
-      lm |= 1u << c;
-      ++legal;
-      hi = fmaxf(hi, logit[c]);
-    }
+    if ((lm >> c) & 1u) hi = fmaxf(hi, logit[c]);
   if (legal == 0 || !isfinite(hi)) {
     *bad = true;
     return -1;
