@@ -641,10 +641,14 @@ void gfnx_destroy(gfnx_ctx* h) {
     cudaEventDestroy(r.b);
   }
   for (auto e : c.ev_pool) cudaEventDestroy(e);
+  if (c.copy_stream) cudaStreamSynchronize(c.copy_stream);
   for (auto& s : c.slots) {
     if (s.host) cudaFreeHost(s.host);
+    if (s.dev) cudaFree(s.dev);
     if (s.done) cudaEventDestroy(s.done);
+    if (s.staged) cudaEventDestroy(s.staged);
   }
+  if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
   if (c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }
@@ -1189,30 +1193,56 @@ namespace {
 size_t slot_bytes(const Ctx& c) {
   return 16 + sizeof(int32_t) * c.Bl + sizeof(double) * c.Bl + sizeof(uint32_t) * (size_t)c.Bl * c.P.SW;
 }
+
 }  // namespace
+
+namespace gfnx {
+// one launch gathers an iteration's results into the slot's device staging buffer (the
+// layout of the pinned host slot), so the next iteration may overwrite the batch while the
+// device->host copy runs on the copy stream
+__global__ void k_slot_stage(uint32_t* __restrict__ dst, const double* __restrict__ loss,
+                             const int32_t* __restrict__ err, const int32_t* __restrict__ len,
+                             const double* __restrict__ logr, const uint32_t* __restrict__ term, int Bl, int SW) {
+  const size_t n1 = (size_t)Bl, n2 = 2 * (size_t)Bl, n3 = (size_t)Bl * SW, total = 4 + n1 + n2 + n3;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    uint32_t v;
+    if (i < 2) v = reinterpret_cast<const uint32_t*>(loss)[i];
+    else if (i == 2) v = (uint32_t)*err;
+    else if (i == 3) v = 0u;
+    else if (i < 4 + n1) v = (uint32_t)len[i - 4];
+    else if (i < 4 + n1 + n2) v = reinterpret_cast<const uint32_t*>(logr)[i - 4 - n1];
+    else v = term[i - 4 - n1 - n2];
+    dst[i] = v;
+  }
+}
+}  // namespace gfnx
 
 gfnx_status gfnx_iteration_async(gfnx_ctx* h, int64_t it, int32_t slot) {
   return guard(h, [&] {
     Ctx& c = h->c;
     if (slot < 0 || slot > 1) fail(GFNX_ERR_CONFIG, "slot must be 0 or 1");
     Ctx::Slot& s = c.slots[slot];
+    const size_t nb = slot_bytes(c);
     if (!s.host) {
-      cuda_check(cudaHostAlloc((void**)&s.host, slot_bytes(c), cudaHostAllocDefault), "pinned slot");
+      cuda_check(cudaHostAlloc((void**)&s.host, nb, cudaHostAllocDefault), "pinned slot");
+      cuda_check(cudaMalloc(&s.dev, nb), "slot staging");
       cuda_check(cudaEventCreateWithFlags(&s.done, cudaEventDisableTiming), "slot event");
+      cuda_check(cudaEventCreateWithFlags(&s.staged, cudaEventDisableTiming), "slot event");
     }
+    if (!c.copy_stream) cuda_check(cudaStreamCreateWithFlags(&c.copy_stream, cudaStreamNonBlocking), "copy stream");
     do_rollout(c, it, schedule_value(c.train.explore, it));
     do_train(c, true, schedule_value(c.train.lr, it), nullptr);
-    uint8_t* p = s.host;
-    cudaMemcpyAsync(p, c.d_scalars + 4, sizeof(double), cudaMemcpyDeviceToHost, c.stream);
-    cudaMemcpyAsync(p + 8, c.batch.counters + 3, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream);
-    p += 16;
-    cudaMemcpyAsync(p, c.batch.lengths, sizeof(int32_t) * c.Bl, cudaMemcpyDeviceToHost, c.stream);
-    p += sizeof(int32_t) * c.Bl;
-    cudaMemcpyAsync(p, c.batch.log_rewards, sizeof(double) * c.Bl, cudaMemcpyDeviceToHost, c.stream);
-    p += sizeof(double) * c.Bl;
-    cudaMemcpyAsync(p, c.batch.term_state, sizeof(uint32_t) * (size_t)c.Bl * c.P.SW,
-                    cudaMemcpyDeviceToHost, c.stream);
-    cuda_check(cudaEventRecord(s.done, c.stream), "slot record");
+    // the staging buffer of this slot is free once its previous device->host copy is done
+    if (s.it >= 0) cuda_check(cudaStreamWaitEvent(c.stream, s.done, 0), "slot reuse");
+    const size_t words = nb / 4;
+    k_slot_stage<<<(unsigned)std::min<size_t>((words + 255) / 256, 4 * 148), 256, 0, c.stream>>>(
+        reinterpret_cast<uint32_t*>(s.dev), c.d_scalars + 4, c.batch.counters + 3, c.batch.lengths,
+        c.batch.log_rewards, c.batch.term_state, c.Bl, c.P.SW);
+    c.launches++;
+    cuda_check(cudaEventRecord(s.staged, c.stream), "slot record");
+    cuda_check(cudaStreamWaitEvent(c.copy_stream, s.staged, 0), "slot copy");
+    cuda_check(cudaMemcpyAsync(s.host, s.dev, nb, cudaMemcpyDeviceToHost, c.copy_stream), "slot copy");
+    cuda_check(cudaEventRecord(s.done, c.copy_stream), "slot record");
     s.it = it;
   });
 }

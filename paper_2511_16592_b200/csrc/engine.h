@@ -221,10 +221,12 @@ struct Ctx {
   // pinned staging slots for gfnx_iteration_async
   struct Slot {
     uint8_t* host = nullptr;  // [loss f64 | err i32 pad | lengths | log_rewards | term_state]
-    cudaEvent_t done = nullptr;
+    uint8_t* dev = nullptr;   // the same bytes staged on the device (one gather kernel)
+    cudaEvent_t staged = nullptr, done = nullptr;
     int64_t it = -1;
   };
   Slot slots[2];
+  cudaStream_t copy_stream = nullptr;  // slot device->host copies, off the compute stream
   // per-kernel CUDA-event profiling (bench.py roofline): records (name, start, stop)
   struct ProfRec {
     const char* name;
