@@ -59,6 +59,9 @@ struct FastState {
   double* lampow = nullptr;           // pow(lambda, k)
   int32_t* work = nullptr;            // rollout work counter
   int32_t* frow_bt = nullptr;         // [max_tiles*128] row slot -> b*T + t (-1 = empty)
+  uint32_t* slot_st = nullptr;        // [max_tiles*128][SW] packed state of each row slot
+  int16_t* slot_act = nullptr;        // [max_tiles*128] its action (the training pass reads
+                                      // both coalesced instead of through frow_bt)
   int32_t* bt_row = nullptr;          // [Bl*T] b*T + t -> row slot
   int32_t* tilectr = nullptr;         // number of 128-row tiles of row slots
   int32_t* det_used = nullptr;        // deterministic mode: filled tiles per rollout CTA
@@ -95,8 +98,8 @@ GFNX_DEV void row_stats_one(const EnvParams& P, const uint32_t* __restrict__ sts
   const int bt = frow_bt[r];
   if (bt < 0) return;
   typename Env::State s;
-  Env::unpack(P, stst + (size_t)bt * P.SW, s);
-  const int act = actions[bt];
+  Env::unpack(P, stst + (size_t)r * P.SW, s);  // the slot-ordered copies (coalesced)
+  const int act = actions[r];
   float lg[NH];
   const float4* src = reinterpret_cast<const float4*>(logits + (size_t)r * NH);
 #pragma unroll
@@ -195,15 +198,19 @@ __global__ void k_rollout_reset(int32_t* tilectr, int32_t* counters, int32_t* wo
 // row slots in trajectory order (row0[b] + t) when the training forward is recomputed
 __global__ void k_linear_rows(const int32_t* __restrict__ lengths, const int32_t* __restrict__ row0, int Bl,
                               int T, const int32_t* counters, int32_t* frow_bt, int32_t* bt_row,
-                              int32_t* tilectr) {
+                              int32_t* tilectr, const uint32_t* __restrict__ stst, const int16_t* __restrict__ acts,
+                              int SW, uint32_t* slot_st, int16_t* slot_act) {
   const int b = blockIdx.x * blockDim.x + threadIdx.x;
   const int R = counters[0];
   const int tiles = (R + kTile - 1) / kTile;
   if (b < Bl) {
     const int L = lengths[b], r0 = row0[b];
     for (int t = 0; t < L; ++t) {
-      frow_bt[r0 + t] = b * T + t;
-      bt_row[(size_t)b * T + t] = r0 + t;
+      const size_t bt = (size_t)b * T + t;
+      frow_bt[r0 + t] = (int32_t)bt;
+      bt_row[bt] = r0 + t;
+      for (int i = 0; i < SW; ++i) slot_st[(size_t)(r0 + t) * SW + i] = stst[bt * SW + i];
+      slot_act[r0 + t] = acts[bt];
     }
   }
   if (b < kTile && R + b < tiles * kTile) frow_bt[R + b] = -1;
@@ -365,6 +372,8 @@ struct RolloutArgs {
   int b0, Bl;
   DeviceBatch batch;
   uint32_t* stst;
+  uint32_t* slot_st;  // the same state + action again at the row's emission slot
+  int16_t* slot_act;
   int32_t* work;
   long long* phase;  // optional per-phase clock totals (gfnx_phase_timers), else nullptr
   // fused training forward: every sampled row's h1 / h2 (bf16 tile images), ReLU masks and
@@ -767,6 +776,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout(RolloutArgs a) {
           a.bt_row[bt] = gslot;
         }
         Env::pack(P, s, a.stst + bt * P.SW);
+        Env::pack(P, s, a.slot_st + (size_t)gslot * P.SW);
+        a.slot_act[gslot] = (int16_t)act;
         int n = 0;
         Env::delta_features(P, s, act, [&](int f, float v) {
           row_df[row][n] = f;
@@ -1184,6 +1195,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_rollout_ts(RolloutArgs a) 
         a.frow_bt[gslot] = (int32_t)bt;
         a.bt_row[bt] = gslot;
         Env::pack(P, s, a.stst + bt * P.SW);
+        Env::pack(P, s, a.slot_st + (size_t)gslot * P.SW);
+        a.slot_act[gslot] = (int16_t)act;
         const double prev_r = P.mdb ? Env::log_reward(P, s) : 0.0;
         const bool term = Env::step(P, s, act);
         a.batch.actions[bt] = (int16_t)act;
@@ -1274,6 +1287,8 @@ struct TrainArgs {
   const int32_t* tile_list; // deterministic mode: training tile -> emission tile, or null
   __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
   uint32_t *mask1, *mask2;  // ReLU masks of h1 / h2, [rows][H/32]
+  const uint32_t* slot_st;  // slot-ordered packed states / actions (training path only)
+  const int16_t* slot_act;
   float* rowbuf;
   int rs;
   float* coef;
@@ -1865,8 +1880,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         x.mk1[0] = m1.x; x.mk1[1] = m1.y;
       }
 #pragma unroll
-      for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (v0 && i < P.SW) ? a.stst[(size_t)rbt * P.SW + i] : 0u;
-      x.act = v0 ? a.batch.actions[rbt] : 0;
+      for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (v0 && i < P.SW) ? a.slot_st[(size_t)r * P.SW + i] : 0u;
+      x.act = v0 ? a.slot_act[r] : 0;
       const float4 cf = v0 ? *reinterpret_cast<const float4*>(a.coef + (size_t)r * 4) : make_float4(0.f, 0.f, 0.f, 0.f);
       x.ga = cf.x;
       x.gs = cf.y;
@@ -2490,6 +2505,8 @@ struct Kernels {
     a.flow = c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB;
     a.frow_bt = f.frow_bt;
     a.bt_row = f.bt_row;
+    a.slot_st = f.slot_st;
+    a.slot_act = f.slot_act;
     a.tilectr = f.tilectr;
     a.logits = f.logits;
     a.det = c.train.deterministic ? 1 : 0;
@@ -2601,6 +2618,8 @@ struct Kernels {
     ta.dhead = f.dhead;
     ta.mask1 = f.mask1;
     ta.mask2 = f.mask2;
+    ta.slot_st = f.slot_st;
+    ta.slot_act = f.slot_act;
     ta.rowbuf = f.rowbuf;
     ta.rs = f.rs;
     ta.coef = f.coef;
@@ -2619,7 +2638,8 @@ struct Kernels {
     if (!f.fused) {  // weights changed since the rollout: recompute the forward over the rows
       ensure_row0(c);
       k_linear_rows<<<(std::max(c.Bl, kTile) + 255) / 256, 256, 0, c.stream>>>(
-          c.batch.lengths, c.batch.row0, c.Bl, c.P.T, c.batch.counters, f.frow_bt, f.bt_row, f.tilectr);
+          c.batch.lengths, c.batch.row0, c.Bl, c.P.T, c.batch.counters, f.frow_bt, f.bt_row, f.tilectr,
+          f.stst, c.batch.actions, c.P.SW, f.slot_st, f.slot_act);
       c.launches++;
       const int fixed = fwd_smem_fixed<H, NH>();
       const int w1b = c.P.O * H * 2;
@@ -2640,7 +2660,7 @@ struct Kernels {
       ProfScope ps(c, "k_row_stats");
       const int nslots = (int)(f.max_tiles * kTile);
       k_row_stats<Env, NH><<<std::min((nslots + 255) / 256, f.num_sms * 8), 256, 0, c.stream>>>(
-          c.P, f.stst, c.batch.actions, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
+          c.P, f.slot_st, f.slot_act, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
           c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3,
           ta.tile_list);
       c.launches++;
@@ -3089,6 +3109,8 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->rowbuf, sizeof(float) * (size_t)slots * f->rs), "fast rowbuf");
   cuda_check(cudaMalloc(&f->coef, sizeof(float) * (size_t)slots * 4), "fast coef");
   cuda_check(cudaMalloc(&f->frow_bt, sizeof(int32_t) * (size_t)slots), "fast rows");
+  cuda_check(cudaMalloc(&f->slot_st, sizeof(uint32_t) * (size_t)slots * c.P.SW), "fast rows");
+  cuda_check(cudaMalloc(&f->slot_act, sizeof(int16_t) * (size_t)slots), "fast rows");
   cuda_check(cudaMalloc(&f->bt_row, sizeof(int32_t) * (size_t)f->max_rows), "fast rows");
   cuda_check(cudaMalloc(&f->tilectr, sizeof(int32_t)), "fast rows");
   cuda_check(cudaMalloc(&f->logits, sizeof(float) * (size_t)slots * f->NH), "fast logits");
@@ -3115,7 +3137,7 @@ void fast_free(Ctx& c) {
   void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
                   f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work,
-                  f->frow_bt, f->bt_row, f->tilectr, f->logits, f->det_used, f->tile_list};
+                  f->frow_bt, f->slot_st, f->slot_act, f->bt_row, f->tilectr, f->logits, f->det_used, f->tile_list};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete f;
