@@ -2214,14 +2214,16 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   // one-hot observation rows of a unit (+ constant feature O) as the MN-major X operand:
   // two threads per row, one 64-feature block each. The slot map is read two units ahead
   // and the packed state one unit ahead, so building a unit waits on no global load.
+  // (ld_bt returns the physical row when it holds a state, else -1; the packed state is read
+  // from its slot-ordered copy, coalesced)
   auto ld_bt = [&](int u) {
     if (u >= nu) return -1;
     const int r = phys_tile<LIST>(a.tile_list, t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
-    return a.frow_bt[r];
+    return a.frow_bt[r] >= 0 ? r : -1;
   };
-  auto ld_sw = [&](int bt, uint32_t (&w)[kMaxSWFwd]) {
+  auto ld_sw = [&](int r, uint32_t (&w)[kMaxSWFwd]) {
 #pragma unroll
-    for (int i = 0; i < kMaxSWFwd; ++i) w[i] = (bt >= 0 && i < P.SW) ? a.stst[(size_t)bt * P.SW + i] : 0u;
+    for (int i = 0; i < kMaxSWFwd; ++i) w[i] = (r >= 0 && i < P.SW) ? a.slot_st[(size_t)r * P.SW + i] : 0u;
   };
   auto build_obs = [&](uint8_t* x, int bt, const uint32_t (&w)[kMaxSWFwd]) {
     const int rl = tid & (kWgRows - 1), blk = tid >> 6;
