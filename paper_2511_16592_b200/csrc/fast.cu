@@ -2661,7 +2661,7 @@ struct Kernels {
     } else {
       ProfScope ps(c, "k_row_stats");
       const int nslots = (int)(f.max_tiles * kTile);
-      k_row_stats<Env, NH><<<std::min((nslots + 255) / 256, f.num_sms * 8), 256, 0, c.stream>>>(
+      k_row_stats<Env, NH><<<std::min((nslots + 255) / 256, f.num_sms * 32), 256, 0, c.stream>>>(
           c.P, f.slot_st, f.slot_act, f.frow_bt, f.tilectr, f.logits, f.rowbuf, f.rs,
           c.train.objective == GFNX_OBJ_DB || c.train.objective == GFNX_OBJ_SUBTB, c.batch.counters + 3,
           ta.tile_list);
