@@ -1800,7 +1800,23 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_bwd: dlogits, head dgrad and W2 dgrad on the tensor cores, ReLU masks, bias grads
+// k_fast_bwd: dlogits, head dgrad and W2 dgrad on the tensor cores, ReLU masks, bias grads,
+// and [dW1 | db1] = [obs | 1]^T dz1 while dz1 is still in shared memory (dz1 never goes to
+// HBM): the one-hot observation rows of 64-row units are built in the dhead tile (free once
+// the head MMA and the dhead store are done) and multiplied against the dz tile in place
+
+// D[128 features x N] (+)= obs_u^T dz[rows 64u .. 64u + 63]: obs unit image [2 feature
+// blocks][64 rows][128 B] (MN-major, LBO 8 KB), dz tile [N / 64 blocks][128 rows][128 B]
+// (MN-major, LBO 16 KB), K = 64 rows in four K = 16 steps
+template <int N>
+GFNX_DEV void mma_obs_dz(uint32_t d_tmem, const void* obs_img, const void* dz_img, int u, bool acc) {
+  constexpr uint32_t idesc = umma_idesc_bf16(128, N, true, true);
+  const uint32_t a0 = smem_u32(obs_img), b0 = smem_u32(dz_img) + u * 64 * 128;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    umma_bf16(d_tmem, umma_desc_sw128(a0 + s * 2048, 64 * 128, 1024), umma_desc_sw128(b0 + s * 2048, kTile * 128, 1024),
+              idesc, (acc || s > 0) ? 1u : 0u);
+}
 
 template <int H, int NH>
 constexpr int bwd_smem_bytes() {
@@ -1818,7 +1834,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   float* red = reinterpret_cast<float*>(whd + H * NH * 2);  // [kThreads * 8 / H][H] bias partials
   float* redh = red + kThreads * 8;                           // [kThreads / NH][NH] head bias partials
   constexpr int HC = H / 2;
-  __shared__ uint64_t mbar;
+  __shared__ uint64_t mbar, mbar1;  // mbar1: the second obs unit's dW1 MMA (htile reuse)
   __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1830,9 +1846,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   float* part = a.wpart + (size_t)blockIdx.x * a.pstride;
   float acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j (db1: k_fast_wgrad pass B)
   if ((int)blockIdx.x < tiles) {
-    if (warp == 0) tmem_alloc<H>(&tbase);
+    if (warp == 0) tmem_alloc<2 * H>(&tbase);  // [0, H): dgrad accumulators, [H, 2H): dW1 | db1
     if (tid == 0) {
       mbar_init(&mbar, 1);
+      mbar_init(&mbar1, 1);
       fence_mbar_init();
     }
     __syncthreads();
@@ -1907,6 +1924,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         tclk = tn;
       }
     };
+    // one-hot observation row rl of a 64-row unit in htile (+ constant feature O: its output
+    // row is db1 = sum_r dz1[r]); the row's own thread zeroes it (chunks rotated by row, no
+    // bank conflicts) and writes its features
+    auto build_obs_row = [&](int rl, bool v, const uint32_t (&w)[kMaxSWFwd]) {
+#pragma unroll
+      for (int blk = 0; blk < 2; ++blk)
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(htile + blk * (64 * 128) + rl * 128 + ((c + rl) & 7) * 16) = make_uint4(0, 0, 0, 0);
+      if (v) {
+        typename Env::State s;
+        Env::unpack(P, w, s);
+        auto put = [&](int f, float x) {
+          *reinterpret_cast<__nv_bfloat16*>(htile + sw128_offset(rl, f, 64)) = __float2bfloat16(x);
+        };
+        Env::features(P, s, [&](int f, double x) { put(f, (float)x); });
+        put(P.O, 1.f);
+      }
+    };
+    bool w1_pending = false, w1_acc = false;
+    uint32_t phase1 = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int pt = phys_tile<LIST>(a.tile_list, tile);  // emission tile of this training tile
       const int rbt = rbt_cur;
@@ -1916,8 +1954,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       rbt_next = slot_of(tile + 2 * gridDim.x);
       load_row(tile + gridDim.x, rbt_cur, nx);  // in flight during this tile
       pmark(6);
-      // (htile is free: the previous tile waited for its dhead / dz2 stores before dz1; the
-      // dz1 store drains from atile while dlogits and the head MMA run)
+      // htile is free once the previous tile's second dW1 MMA has read its obs unit (atile:
+      // every earlier MMA has completed when this tile's head MMA commits)
+      if (w1_pending) {
+        if (half == 0) mbar_wait(&mbar1, phase1);
+        phase1 ^= 1;
+        w1_pending = false;
+      }
       uint32_t mk2[HC / 32], mk1[HC / 32];
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
@@ -1968,7 +2011,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         bulk_commit();
         mma_k_sw128_none<H, NH>(tmem, htile, whd);
         umma_commit(&mbar);
-        bulk_wait_read0();  // the previous tile's dz1 store has left atile
       }
       mbar_wait(&mbar, phase);
       phase ^= 1;
@@ -2058,21 +2100,57 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
                               ((mk1[q] >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
       }
+      if (half == 0 && quarter < 2) build_obs_row(row, valid, cx.sw);  // obs unit 0 (rows 0..63)
       tc_fence_before();
       fence_proxy_async();
       __syncthreads();
-      if (tid == 0) {
-        bulk_s2g(a.dz1 + (size_t)pt * kTile * H, atile, kTile * H * 2);
-        bulk_commit();
+      if (tid == 0) {  // [dW1 | db1] += [obs | 1]^T dz1 over rows 0..63
+        tc_fence_after();
+        mma_obs_dz<H>(tmem + H, htile, atile, 0, w1_acc);
+        umma_commit(&mbar);
       }
+      mbar_wait(&mbar, phase);
+      phase ^= 1;
+      if (half == 0 && quarter >= 2) build_obs_row(row - 64, valid, cx.sw);  // obs unit 1
+      fence_proxy_async();
+      __syncthreads();
+      if (tid == 0) {  // rows 64..127; completion waited before htile / atile are rewritten
+        tc_fence_after();
+        mma_obs_dz<H>(tmem + H, htile, atile, 1, true);
+        umma_commit(&mbar1);
+      }
+      w1_pending = true;
+      w1_acc = true;
       pmark(4);
       pc[5] += 1;
     }
     if (a.phase && tid == 0)
       for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)a.phase + 15 + k, (unsigned long long)pc[k]);
+    if (w1_pending) mbar_wait(&mbar1, phase1);
+    tc_fence_after();
+    // [dW1 | db1] of this CTA -> its partial slab: TMEM lane = input feature f (<= O), the two
+    // halves read their column halves
+#pragma unroll 1
+    for (int q = 0; q < HC / 32; ++q) {
+      const int col = c0 + q * 32;
+      uint32_t r32[32];
+      tmem_ld32(lane_base + H + col, r32);
+      tmem_wait_ld();
+      if (row <= P.O) {
+        float* dst = row < P.O ? part + a.L.off_w[0] + (size_t)row * H + col : part + a.L.off_b[0] + col;
+#pragma unroll
+        for (int i = 0; i < 32; i += 8) st_v8(dst + i, r32 + i, true);
+      }
+    }
     if (tid == 0) bulk_wait0();
+    tc_fence_before();
     __syncthreads();
-    if (warp == 0) tmem_dealloc<H>(tmem);
+    if (warp == 0) tmem_dealloc<2 * H>(tmem);
+  } else {  // no tile: zero [dW1 | db1] partials
+    for (int i = tid; i < (P.O + 1) * H; i += kThreads) {
+      const int f = i / H, j = i % H;
+      part[f < P.O ? a.L.off_w[0] + (size_t)f * H + j : a.L.off_b[0] + j] = 0.f;
+    }
   }
   // bias partials of this CTA (every CTA writes its slots, zeros when it had no tile)
   if (tid < H) part[a.L.off_b[1] + tid] = acc_b2;
@@ -2081,14 +2159,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
 }
 
 // ---------------------------------------------------------------------------
-// k_fast_wgrad: dW2 = h1^T dz2, [dW1 | db1] = [obs | 1]^T dz1, dWhead = h2^T dhead (K = rows)
+// k_fast_wgrad: dW2 = h1^T dz2, dWhead = h2^T dhead (K = rows; [dW1 | db1] is k_fast_bwd's)
 //
 // The activation tile images are streamed as 64-row units through a 3-stage ring of
 // shared-memory stages (bulk copies on mbarriers, "full"), consumed by tcgen05.mma with
 // MN-major descriptors (LBO = 64 rows x 128 B between 64-feature blocks), and released by
 // the MMA's commit ("empty"): the loads of unit q + 2 are in flight while unit q multiplies.
-// One sequence runs through the three passes (A: h1/dz2, B: obs/dz1, C: h2/dhead); TMEM
-// holds one pass's accumulators, read back into the CTA's partial slab between passes.
+// One sequence runs through the two passes (A: h1/dz2, C: h2/dhead); TMEM holds one pass's
+// accumulators, read back into the CTA's partial slab between passes.
 constexpr int kWgStages = 3;
 constexpr int kWgRows = 64;           // rows per unit
 constexpr int kWgStage = 65536;       // X operand [0, 32 KB), Y operand [32 KB, 64 KB)
@@ -2125,7 +2203,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   const int per = (tiles + gridDim.x - 1) / gridDim.x;
   const int t0 = blockIdx.x * per, t1 = min(tiles, t0 + per);
   const int nu = t1 > t0 ? 2 * (t1 - t0) : 0;  // units per pass
-  const int NQ = 3 * nu;
+  const int NQ = 2 * nu;
   float* part = a.wpart + (size_t)blockIdx.x * a.pstride;
   const MlpLayout& L = a.L;
   constexpr int KH = H / 128;  // 128-feature M blocks of the h operands
@@ -2150,7 +2228,7 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
            hh * (kWgRows * 128);
   };
   auto issue_load = [&](int q) {  // thread 0
-    const int st = q % kWgStages, p = q / nu, u = q % nu;
+    const int st = q % kWgStages, p = 2 * (q / nu), u = q % nu;
     if (q >= kWgStages) mbar_wait(&empty[st], ((q / kWgStages) - 1) & 1);
     constexpr uint32_t ub = kWgRows * 128;  // one 64-feature block of a unit
     if (p == 0) {
@@ -2159,9 +2237,6 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
         bulk_g2s(X(st) + k * ub, src(a.h1, u, k, H), ub, &full[st]);
         bulk_g2s(Y(st) + k * ub, src(a.dz2, u, k, H), ub, &full[st]);
       }
-    } else if (p == 1) {
-      mbar_arrive_expect_tx(&full[st], (H / 64) * ub);
-      for (int k = 0; k < H / 64; ++k) bulk_g2s(Y(st) + k * ub, src(a.dz1, u, k, H), ub, &full[st]);
     } else {
       mbar_arrive_expect_tx(&full[st], (H / 64) * ub + ub);
       for (int k = 0; k < H / 64; ++k) bulk_g2s(X(st) + k * ub, src(a.h2, u, k, H), ub, &full[st]);
@@ -2183,17 +2258,6 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
           for (int i = 0; i < 32; i += 8) st_v8(dst + i, r32 + i, any);
         }
       }
-    } else if (p == 1) {
-      for (int q = 0; q < H / 32; ++q) {
-        uint32_t r32[32];
-        tmem_ld32(lane_base + q * 32, r32);
-        tmem_wait_ld();
-        if (tid <= P.O) {
-          float* dst = tid < P.O ? part + L.off_w[0] + (size_t)tid * H + q * 32 : part + L.off_b[0] + q * 32;
-#pragma unroll
-          for (int i = 0; i < 32; i += 8) st_v8(dst + i, r32 + i, any);
-        }
-      }
     } else {
       for (int h = 0; h < KH; ++h) {
         const int pr = 128 * h + tid;
@@ -2211,46 +2275,6 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
       }
     }
   };
-  // one-hot observation rows of a unit (+ constant feature O) as the MN-major X operand:
-  // two threads per row, one 64-feature block each. The slot map is read two units ahead
-  // and the packed state one unit ahead, so building a unit waits on no global load.
-  // (ld_bt returns the physical row when it holds a state, else -1; the packed state is read
-  // from its slot-ordered copy, coalesced)
-  auto ld_bt = [&](int u) {
-    if (u >= nu) return -1;
-    const int r = phys_tile<LIST>(a.tile_list, t0 + (u >> 1)) * kTile + (u & 1) * kWgRows + (tid & (kWgRows - 1));
-    return a.frow_bt[r] >= 0 ? r : -1;
-  };
-  auto ld_sw = [&](int r, uint32_t (&w)[kMaxSWFwd]) {
-#pragma unroll
-    for (int i = 0; i < kMaxSWFwd; ++i) w[i] = (r >= 0 && i < P.SW) ? a.slot_st[(size_t)r * P.SW + i] : 0u;
-  };
-  auto build_obs = [&](uint8_t* x, int bt, const uint32_t (&w)[kMaxSWFwd]) {
-    const int rl = tid & (kWgRows - 1), blk = tid >> 6;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      *reinterpret_cast<uint4*>(x + blk * (kWgRows * 128) + rl * 128 + c * 16) = make_uint4(0, 0, 0, 0);
-    if (bt >= 0) {
-      typename Env::State s;
-      Env::unpack(P, w, s);
-      auto put = [&](int f, float v) {
-        if ((f >> 6) == blk)
-          *reinterpret_cast<__nv_bfloat16*>(x + sw128_offset(rl, f, kWgRows)) = __float2bfloat16(v);
-      };
-      Env::features(P, s, [&](int f, double v) { put(f, (float)v); });
-      put(P.O, 1.f);  // its output row is db1 = sum_r dz1[r]
-    }
-  };
-  int ob_bt0 = ld_bt(0), ob_bt1 = ld_bt(1);  // pass B units 0 and 1, consumed much later
-  uint32_t ob_sw0[kMaxSWFwd];
-  ld_sw(ob_bt0, ob_sw0);
-  auto obs_next = [&](uint8_t* x, int u_after) {  // build the prefetched unit, advance prefetch
-    build_obs(x, ob_bt0, ob_sw0);
-    ob_bt0 = ob_bt1;
-    ld_sw(ob_bt0, ob_sw0);
-    ob_bt1 = ld_bt(u_after);
-  };
-
   long long tclk = clock64();
   auto pclock = [&](int k) {
     if (a.phase && tid == 0) {
@@ -2262,17 +2286,13 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
   if (tid == 0)
     for (int q = 0; q < kWgStages - 1 && q < NQ; ++q) issue_load(q);
   for (int q = 0; q < NQ; ++q) {
-    const int st = q % kWgStages, p = q / nu, u = q % nu;
-    if (u == 0 && q > 0) {  // pass boundary: accumulators of pass p - 1 -> slab
-      pclock(p - 1);
+    const int st = q % kWgStages, p = 2 * (q / nu), u = q % nu;
+    if (u == 0 && q > 0) {  // pass boundary: accumulators of pass A -> slab
+      pclock(0);
       if (tid == 0) mbar_wait(&empty[(q - 1) % kWgStages], ((q - 1) / kWgStages) & 1);
       __syncthreads();
       tc_fence_after();
-      readout(p - 1);
-      if (p == 1) {  // first observation unit (every earlier MMA has completed)
-        obs_next(X(st), 2);
-        fence_proxy_async();
-      }
+      readout(0);
       tc_fence_before();
       __syncthreads();
     }
@@ -2282,8 +2302,6 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
       if (p == 0) {
 #pragma unroll
         for (int h = 0; h < KH; ++h) mma_mn64<H>(tmem + h * H, X(st), 128 * h, Y(st), u > 0);
-      } else if (p == 1) {
-        mma_mn64<H>(tmem, X(st), 0, Y(st), u > 0);
       } else {
 #pragma unroll
         for (int h = 0; h < KH; ++h) mma_mn64<64>(tmem + h * 64, X(st), 128 * h, Y(st), u > 0);
@@ -2291,22 +2309,12 @@ __global__ void __launch_bounds__(kTile, 1) k_fast_wgrad(TrainArgs a) {
       umma_commit(&empty[st]);
       if (q + kWgStages - 1 < NQ) issue_load(q + kWgStages - 1);
     }
-    if (p == 1 && u + 1 < nu) {
-      // observation rows of the next unit while this one multiplies: stage (q + 1) was
-      // released (MMA q + 1 - S complete) before thread 0 issued its load last iteration
-      obs_next(X((q + 1) % kWgStages), u + 3);
-      fence_proxy_async();
-      __syncthreads();
-    }
   }
   if (NQ > 0 && tid == 0) mbar_wait(&empty[(NQ - 1) % kWgStages], ((NQ - 1) / kWgStages) & 1);
   pclock(2);
   __syncthreads();
   tc_fence_after();
-  if (NQ == 0) {
-    readout(0);
-    readout(1);
-  }
+  if (NQ == 0) readout(0);
   readout(2);
   tc_fence_before();
   __syncthreads();
