@@ -49,7 +49,7 @@ struct FastState {
   __nv_bfloat16* whead_d = nullptr;   // image [H][NH] non-swizzled (head dgrad)
   int NH = 16;
   uint32_t* stst = nullptr;           // [Bl*T][SW] state before each step
-  __nv_bfloat16 *h1 = nullptr, *h2 = nullptr, *dz1 = nullptr, *dz2 = nullptr;  // tile images
+  __nv_bfloat16 *h1 = nullptr, *h2 = nullptr, *dz2 = nullptr;  // tile images
   __nv_bfloat16* dhead = nullptr;     // tile images [tiles][128][64]
   uint32_t *mask1 = nullptr, *mask2 = nullptr;  // ReLU bit masks [rows][H/32]
   float* rowbuf = nullptr;            // per row: probs[A], lpa, lps, flow, pad
@@ -1285,7 +1285,7 @@ struct TrainArgs {
   const int32_t* frow_bt;   // row slot -> b * T + t, -1 = empty slot
   const int32_t* tilectr;   // number of 128-row tiles of row slots
   const int32_t* tile_list; // deterministic mode: training tile -> emission tile, or null
-  __nv_bfloat16 *h1, *h2, *dz1, *dz2, *dhead;
+  __nv_bfloat16 *h1, *h2, *dz2, *dhead;
   uint32_t *mask1, *mask2;  // ReLU masks of h1 / h2, [rows][H/32]
   const uint32_t* slot_st;  // slot-ordered packed states / actions (training path only)
   const int16_t* slot_act;
@@ -1802,8 +1802,10 @@ __global__ void k_loss_finalize(const double* lpart, int nblocks, double* scalar
 // ---------------------------------------------------------------------------
 // k_fast_bwd: dlogits, head dgrad and W2 dgrad on the tensor cores, ReLU masks, bias grads,
 // and [dW1 | db1] = [obs | 1]^T dz1 while dz1 is still in shared memory (dz1 never goes to
-// HBM): the one-hot observation rows of 64-row units are built in the dhead tile (free once
-// the head MMA and the dhead store are done) and multiplied against the dz tile in place
+// HBM): the one-hot observation rows of the two 64-row units are built in the dhead tile
+// (free once the head MMA and the dhead store are done) and in the first 16 KB of the W2
+// dgrad image (re-fetched from L2 during the next tile's dlogits / head MMA), and multiplied
+// against the dz tile in place
 
 // D[128 features x N] (+)= obs_u^T dz[rows 64u .. 64u + 63]: obs unit image [2 feature
 // blocks][64 rows][128 B] (MN-major, LBO 8 KB), dz tile [N / 64 blocks][128 rows][128 B]
@@ -1834,7 +1836,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   float* red = reinterpret_cast<float*>(whd + H * NH * 2);  // [kThreads * 8 / H][H] bias partials
   float* redh = red + kThreads * 8;                           // [kThreads / NH][NH] head bias partials
   constexpr int HC = H / 2;
-  __shared__ uint64_t mbar, mbar1;  // mbar1: the second obs unit's dW1 MMA (htile reuse)
+  __shared__ uint64_t mbar, mbar1, mbarw;  // mbar1: the dW1 MMAs; mbarw: the W2 image patch
   __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1850,6 +1852,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     if (tid == 0) {
       mbar_init(&mbar, 1);
       mbar_init(&mbar1, 1);
+      mbar_init(&mbarw, 1);
       fence_mbar_init();
     }
     __syncthreads();
@@ -1924,27 +1927,27 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         tclk = tn;
       }
     };
-    // one-hot observation row rl of a 64-row unit in htile (+ constant feature O: its output
+    // one-hot observation row rl of a 64-row unit image x (+ constant feature O: its output
     // row is db1 = sum_r dz1[r]); the row's own thread zeroes it (chunks rotated by row, no
     // bank conflicts) and writes its features
-    auto build_obs_row = [&](int rl, bool v, const uint32_t (&w)[kMaxSWFwd]) {
+    auto build_obs_row = [&](uint8_t* x, int rl, bool v, const uint32_t (&w)[kMaxSWFwd]) {
 #pragma unroll
       for (int blk = 0; blk < 2; ++blk)
 #pragma unroll
         for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(htile + blk * (64 * 128) + rl * 128 + ((c + rl) & 7) * 16) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(x + blk * (64 * 128) + rl * 128 + ((c + rl) & 7) * 16) = make_uint4(0, 0, 0, 0);
       if (v) {
         typename Env::State s;
         Env::unpack(P, w, s);
-        auto put = [&](int f, float x) {
-          *reinterpret_cast<__nv_bfloat16*>(htile + sw128_offset(rl, f, 64)) = __float2bfloat16(x);
+        auto put = [&](int f, float y) {
+          *reinterpret_cast<__nv_bfloat16*>(x + sw128_offset(rl, f, 64)) = __float2bfloat16(y);
         };
         Env::features(P, s, [&](int f, double x) { put(f, (float)x); });
         put(P.O, 1.f);
       }
     };
-    bool w1_pending = false, w1_acc = false;
-    uint32_t phase1 = 0;
+    bool w1_pending = false, w1_acc = false, w2_patch = false;
+    uint32_t phase1 = 0, phasew = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int pt = phys_tile<LIST>(a.tile_list, tile);  // emission tile of this training tile
       const int rbt = rbt_cur;
@@ -1958,6 +1961,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       // every earlier MMA has completed when this tile's head MMA commits)
       if (w1_pending) {
         if (half == 0) mbar_wait(&mbar1, phase1);
+        if (tid == 0) {  // restore the W2 image's first 16 KB (obs unit 1 of the previous tile)
+          mbar_arrive_expect_tx(&mbarw, 16384);
+          bulk_g2s(wdimg, a.W.w2_dgrad, 16384, &mbarw);
+        }
+        w2_patch = true;
         phase1 ^= 1;
         w1_pending = false;
       }
@@ -2038,6 +2046,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         tc_fence_after();
         bulk_s2g(a.dz2 + (size_t)pt * kTile * H, atile, kTile * H * 2);
         bulk_commit();
+        if (w2_patch) {
+          mbar_wait(&mbarw, phasew);
+          phasew ^= 1;
+        }
         mma_kk<H, H>(tmem, atile, wdimg, false);  // dh1 = dz2 W2^T
         umma_commit(&mbar);
       }
@@ -2100,23 +2112,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
                               ((mk1[q] >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
       }
-      if (half == 0 && quarter < 2) build_obs_row(row, valid, cx.sw);  // obs unit 0 (rows 0..63)
+      // obs units: rows 0..63 in htile, rows 64..127 in the W2 image's first 16 KB (its W2
+      // MMA has completed)
+      if (half == 0) build_obs_row(quarter < 2 ? htile : wdimg, row & 63, valid, cx.sw);
       tc_fence_before();
       fence_proxy_async();
       __syncthreads();
-      if (tid == 0) {  // [dW1 | db1] += [obs | 1]^T dz1 over rows 0..63
+      if (tid == 0) {  // [dW1 | db1] += [obs | 1]^T dz1; completion waited before htile / the
+                       // W2 image / atile are rewritten
         tc_fence_after();
         mma_obs_dz<H>(tmem + H, htile, atile, 0, w1_acc);
-        umma_commit(&mbar);
-      }
-      mbar_wait(&mbar, phase);
-      phase ^= 1;
-      if (half == 0 && quarter >= 2) build_obs_row(row - 64, valid, cx.sw);  // obs unit 1
-      fence_proxy_async();
-      __syncthreads();
-      if (tid == 0) {  // rows 64..127; completion waited before htile / atile are rewritten
-        tc_fence_after();
-        mma_obs_dz<H>(tmem + H, htile, atile, 1, true);
+        mma_obs_dz<H>(tmem + H, wdimg, atile, 1, true);
         umma_commit(&mbar1);
       }
       w1_pending = true;
@@ -2623,7 +2629,6 @@ struct Kernels {
     ta.tile_list = (f.fused && c.train.deterministic) ? f.tile_list : nullptr;
     ta.h1 = f.h1;
     ta.h2 = f.h2;
-    ta.dz1 = f.dz1;
     ta.dz2 = f.dz2;
     ta.dhead = f.dhead;
     ta.mask1 = f.mask1;
@@ -3111,7 +3116,6 @@ void fast_init(Ctx& c) {
   cuda_check(cudaMalloc(&f->stst, sizeof(uint32_t) * (size_t)c.Bl * T * c.P.SW), "fast stst");
   cuda_check(cudaMalloc(&f->h1, img), "fast h1");
   cuda_check(cudaMalloc(&f->h2, img), "fast h2");
-  cuda_check(cudaMalloc(&f->dz1, img), "fast dz1");
   cuda_check(cudaMalloc(&f->dz2, img), "fast dz2");
   cuda_check(cudaMalloc(&f->dhead, (size_t)f->max_tiles * kTile * 64 * 2), "fast dhead");
   cuda_check(cudaMalloc(&f->mask1, sizeof(uint32_t) * (size_t)slots * (H / 32)), "fast masks");
@@ -3144,7 +3148,7 @@ void fast_free(Ctx& c) {
   }
   FastState* f = static_cast<FastState*>(c.fast);
   if (!f) return;
-  void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz1, f->dz2, f->dhead,
+  void* ptrs[] = {f->w1, f->w2_fwd, f->w2_dgrad, f->whead_f, f->whead_d, f->stst, f->h1, f->h2, f->dz2, f->dhead,
                   f->mask1, f->mask2,
                   f->rowbuf, f->coef, f->wpart, f->lpart, f->lampow, f->work,
                   f->frow_bt, f->slot_st, f->slot_act, f->bt_row, f->tilectr, f->logits, f->det_used, f->tile_list};
