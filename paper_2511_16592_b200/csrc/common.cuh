@@ -126,6 +126,35 @@ GFNX_DEV uint32_t bias_relu_pack(uint32_t a_lo, uint32_t a_hi, float2 b) {
   return pack_bf16x2_relu(lo, hi);
 }
 
+// (a + b) of an fp32 pair rounded to a packed bf16 pair: one FADD2 + one cvt, the same bits
+// as pack_bf16x2(a.x + b.x, a.y + b.y)
+GFNX_DEV uint32_t add_pack_bf16x2(float a_lo, float a_hi, float b_lo, float b_hi) {
+  unsigned long long x, y;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(a_lo), "f"(a_hi));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(y) : "f"(b_lo), "f"(b_hi));
+  asm("add.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(y));
+  float lo, hi;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(x));
+  return pack_bf16x2(lo, hi);
+}
+// (x0 s + t, x1 s + t) as one FFMA2 and (x0 s, x1 s) as one FMUL2: per lane the same single
+// rounding as fmaf / an fp32 multiply
+GFNX_DEV void ffma2_st(float& x0, float& x1, float s, float t) {
+  unsigned long long x, sv, tv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(tv) : "f"(t));
+  asm("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x) : "l"(sv), "l"(tv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x));
+}
+GFNX_DEV void fmul2_s(float& x0, float& x1, float s) {
+  unsigned long long x, sv;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+  asm("mov.b64 %0, {%1, %1};" : "=l"(sv) : "f"(s));
+  asm("mul.rn.f32x2 %0, %0, %1;" : "+l"(x) : "l"(sv));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x0), "=f"(x1) : "l"(x));
+}
+
 GFNX_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
 GFNX_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
 

@@ -813,22 +813,27 @@ struct DlogEpi : EpiBase {  // recomputed logits -> dlogits image + per-tile col
     const uint32_t lm = Lock<E>::legal32c(e.P, l.lw, c0);
     const float nl2 = -l.lse * kLog2e;
     uint32_t pk[16];
-    float bias[32];
     const float4* bb = reinterpret_cast<const float4*>(e.bf + c0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < 8; ++i) {  // bf16 logits: FADD2 + one cvt per pair
       const float4 bq = bb[i];
-      bias[4 * i] = bq.x;
-      bias[4 * i + 1] = bq.y;
-      bias[4 * i + 2] = bq.z;
-      bias[4 * i + 3] = bq.w;
+      pk[2 * i] = add_pack_bf16x2(v[4 * i], v[4 * i + 1], bq.x, bq.y);
+      pk[2 * i + 1] = add_pack_bf16x2(v[4 * i + 2], v[4 * i + 3], bq.z, bq.w);
     }
+    // -g softmax = -g 2^(x log2e - lse log2e): FFMA2, two MUFU.EX2, FMUL2 per pair (the same
+    // roundings as the scalar fmaf / multiply)
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const float x = __bfloat162float(__float2bfloat16(v[i] + bias[i]));
-      float d = ((lm >> i) & 1u) ? -l.g * ex2_ftz(fmaf(x, kLog2e, nl2)) : 0.f;
-      if (c0 + i == l.act) d += l.g;
-      v[i] = d;
+    for (int i = 0; i < 16; ++i) {
+      float x0 = bf16_lo(pk[i]), x1 = bf16_hi(pk[i]);
+      ffma2_st(x0, x1, kLog2e, nl2);
+      x0 = ex2_ftz(x0);
+      x1 = ex2_ftz(x1);
+      fmul2_s(x0, x1, -l.g);
+      float d0 = ((lm >> (2 * i)) & 1u) ? x0 : 0.f, d1 = ((lm >> (2 * i + 1)) & 1u) ? x1 : 0.f;
+      if (c0 + 2 * i == l.act) d0 += l.g;
+      if (c0 + 2 * i + 1 == l.act) d1 += l.g;
+      v[2 * i] = d0;
+      v[2 * i + 1] = d1;
     }
     if (FLOW && (unsigned)(e.P.A - c0) < 32u) {  // the log-flow column (warp-uniform test)
       const float gf = e.gflow[r];
