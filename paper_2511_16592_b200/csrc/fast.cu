@@ -16,9 +16,10 @@
 //                   tape.cpp:177-213)
 //   k_fast_loss_warp TB/DB/SubTB/MDB residuals and their analytic backward, warp per trajectory
 //                   (objectives.cpp:94-226), deterministic block partials
-//   k_fast_bwd      head backward (SIMT), dgrad GEMM on tcgen05, ReLU masks, bias grads
-//   k_fast_wgrad    weight gradients as tcgen05 GEMMs whose K dimension is the row count:
-//                   the activation tile images are read MN-major straight from HBM
+//   k_fast_bwd      head backward (SIMT), dgrad GEMMs on tcgen05, ReLU masks, bias grads, and
+//                   [dW1 | db1] = [obs | 1]^T dz1 on tcgen05 while dz1 is in shared memory
+//   k_fast_wgrad    dW2 / dWhead as tcgen05 GEMMs whose K dimension is the row count: the
+//                   activation tile images are read MN-major straight from HBM
 //   k_reduce        fixed-order reduction of per-CTA partial gradients (deterministic)
 //   k_fast_adam     fused Adam over the flat fp32 parameters + logZ, re-emitting the bf16
 //                   operand images (adam_step optim.cpp:19-43)
@@ -2741,7 +2742,7 @@ bool supported(const Ctx& c, int* H) {
   if (c.L.dims[1] != c.L.dims[2]) return false;
   if (*H != 256 && *H != 128) return false;
   if (c.shape.num_actions + 1 > (c.env.kind == GFNX_ENV_HYPERGRID ? 16 : 32)) return false;
-  if (c.shape.obs_dim >= 128) return false;  // feature obs_dim carries db1 in the wgrad GEMM
+  if (c.shape.obs_dim >= 128) return false;  // feature obs_dim carries db1 in the bwd dW1 GEMM
   if (c.shape.max_traj_len > 128) return false;
   if (c.env.kind == GFNX_ENV_DAG) return *H == 128;
   return c.env.kind == GFNX_ENV_HYPERGRID;
