@@ -260,17 +260,36 @@ void check_device_error(Ctx& c) {
   }
 }
 
-// the job's all-reduce (sum, in place, stream-ordered): in-process group or NCCL
-void nccl_sum(Ctx& c, void* buf, size_t n, ncclDataType_t t) {
+// the job's all-reduce (sum, in place, stream-ordered on `st`, default the compute stream):
+// in-process group or NCCL
+void nccl_sum(Ctx& c, void* buf, size_t n, ncclDataType_t t, cudaStream_t st = nullptr) {
   if (c.world <= 1) return;
+  if (!st) st = c.stream;
   if (c.group) {
-    group_allreduce(c, buf, n, t == ncclFloat64 ? kDtypeF64 : t == ncclFloat32 ? kDtypeF32 : kDtypeI32);
+    group_allreduce(c, buf, n, t == ncclFloat64 ? kDtypeF64 : t == ncclFloat32 ? kDtypeF32 : kDtypeI32, st);
     return;
   }
   NcclApi& api = nccl_api();
-  const ncclResult_t r = api.AllReduce(buf, buf, n, t, ncclSum, (ncclComm_t)c.nccl, c.stream);
+  const ncclResult_t r = api.AllReduce(buf, buf, n, t, ncclSum, (ncclComm_t)c.nccl, st);
   if (r != ncclSuccess) fail(GFNX_ERR_NCCL, std::string("ncclAllReduce: ") + api.GetErrorString(r));
 }
+
+}  // namespace
+
+void gfnx::grad_bucket_async(Ctx& c, float* g, int64_t n) {
+  if (c.world <= 1 || n <= 0) return;
+  if (!c.comm_stream) {
+    cuda_check(cudaStreamCreateWithFlags(&c.comm_stream, cudaStreamNonBlocking), "comm stream");
+    for (auto& e : c.comm_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "comm event");
+  }
+  cuda_check(cudaEventRecord(c.comm_ev[0], c.stream), "bucket ready");
+  cuda_check(cudaStreamWaitEvent(c.comm_stream, c.comm_ev[0], 0), "bucket wait");
+  nccl_sum(c, g, (size_t)n, ncclFloat32, c.comm_stream);
+  cuda_check(cudaEventRecord(c.comm_ev[1], c.comm_stream), "bucket done");
+  c.grad_bucket0 = n;
+}
+
+namespace {
 
 void do_rollout(Ctx& c, int64_t it, double eps) {
   if (eps < 0.0 || eps > 1.0) fail(GFNX_ERR_CONFIG, "exploration eps must lie in [0,1]");
@@ -316,8 +335,11 @@ void do_train(Ctx& c, bool apply, double lr, double* loss) {
     if (apply) check_adam(c, lr);
   } else {
     fast_train(c, apply, lr, loss);
-    if (c.world > 1) {
-      nccl_sum(c, c.g32, (size_t)n, ncclFloat32);
+    if (c.world > 1) {  // the early bucket (fast_train: dW1 | db1 behind wgrad), then the rest
+      const int64_t n0 = c.grad_bucket0;
+      if (n0 > 0) cuda_check(cudaStreamWaitEvent(c.stream, c.comm_ev[1], 0), "bucket join");
+      c.grad_bucket0 = 0;
+      nccl_sum(c, c.g32 + n0, (size_t)(n - n0), ncclFloat32);
       nccl_sum(c, c.d_scalars + 3, 2, ncclFloat64);
     }
     if (apply) fast_adam(c, lr);
@@ -649,6 +671,12 @@ void gfnx_destroy(gfnx_ctx* h) {
     if (s.staged) cudaEventDestroy(s.staged);
   }
   if (c.copy_stream) cudaStreamDestroy(c.copy_stream);
+  if (c.comm_stream) {
+    cudaStreamSynchronize(c.comm_stream);
+    cudaStreamDestroy(c.comm_stream);
+  }
+  for (auto e : c.comm_ev)
+    if (e) cudaEventDestroy(e);
   if (c.stream) cudaStreamDestroy(c.stream);
   delete h;
 }

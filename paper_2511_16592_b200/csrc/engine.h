@@ -47,7 +47,11 @@ int group_world(const Group* g);
 void group_delete(Group* g);
 void group_join(Ctx& c, Group* g, int rank);
 void group_leave(Ctx& c, Group* g, int rank);
-void group_allreduce(Ctx& c, void* buf, size_t n, int dtype);
+void group_allreduce(Ctx& c, void* buf, size_t n, int dtype, cudaStream_t s);
+// world > 1: all-reduce the gradient bucket g[0, n) on the comm stream once the compute
+// stream's work so far is done (SURVEY §8(e) bucketed all-reduce behind the backward); the
+// rest of the gradient follows in do_train after the compute stream joins — api.cu
+void grad_bucket_async(Ctx& c, float* g, int64_t n);
 
 // check-mode (fp64 SIMT, reference operation order) — check.cu
 // forced: [Bl * T] actions of a teacher-forced batch (rollout_from_actions), or null to sample
@@ -227,6 +231,9 @@ struct Ctx {
   };
   Slot slots[2];
   cudaStream_t copy_stream = nullptr;  // slot device->host copies, off the compute stream
+  cudaStream_t comm_stream = nullptr;  // world > 1: the early gradient bucket's all-reduce
+  cudaEvent_t comm_ev[2] = {nullptr, nullptr};
+  int64_t grad_bucket0 = 0;            // gradient entries [0, grad_bucket0) already in flight
   // per-kernel CUDA-event profiling (bench.py roofline): records (name, start, stop)
   struct ProfRec {
     const char* name;

@@ -2714,6 +2714,17 @@ struct Kernels {
       if (list) k_fast_bwd<Env, H, NH, true><<<grid, kThreads, smem, c.stream>>>(ta);
       else k_fast_bwd<Env, H, NH, false><<<grid, kThreads, smem, c.stream>>>(ta);
     }
+    const int64_t n = c.L.n_params;
+    // world > 1: [dW1 | db1] (the parameters before W2) is final after k_fast_bwd — reduce it
+    // and start its all-reduce on the comm stream while k_fast_wgrad runs
+    const int64_t nA = c.world > 1 ? c.L.off_w[1] : 0;
+    if (nA > 0) {
+      ProfScope ps(c, "k_reduce");
+      k_reduce<<<(unsigned)((nA + kRedE - 1) / kRedE), kRedE * kRedG, 0, c.stream>>>(f.wpart, grid, nA, ta.pstride,
+                                                                                     c.g32);
+      c.launches++;
+      grad_bucket_async(c, c.g32, nA);
+    }
     smem = wgrad_smem_bytes<H>();
     if (list) set_smem_once(k_fast_wgrad<Env, H, true>, smem);
     else set_smem_once(k_fast_wgrad<Env, H, false>, smem);
@@ -2722,11 +2733,10 @@ struct Kernels {
       if (list) k_fast_wgrad<Env, H, true><<<grid, kTile, smem, c.stream>>>(ta);
       else k_fast_wgrad<Env, H, false><<<grid, kTile, smem, c.stream>>>(ta);
     }
-    const int64_t n = c.L.n_params;
     {
       ProfScope ps(c, "k_reduce");
-      k_reduce<<<(unsigned)((n + kRedE - 1) / kRedE), kRedE * kRedG, 0, c.stream>>>(f.wpart, grid, n, ta.pstride,
-                                                                                  c.g32);
+      k_reduce<<<(unsigned)((n - nA + kRedE - 1) / kRedE), kRedE * kRedG, 0, c.stream>>>(
+          f.wpart + nA, grid, n - nA, ta.pstride, c.g32 + nA);
     }
     c.launches += 5;
     (void)apply;

@@ -128,9 +128,9 @@ void group_leave(Ctx& c, Group* g, int rank) {
   (void)c;
 }
 
-// Sum of `buf` over the group, in place on every rank (stream-ordered on c.stream). Every
+// Sum of `buf` over the group, in place on every rank (stream-ordered on `st`). Every
 // member must call it with the same n / dtype in the same order (a collective).
-void group_allreduce(Ctx& c, void* buf, size_t n, int dtype) {
+void group_allreduce(Ctx& c, void* buf, size_t n, int dtype, cudaStream_t st) {
   Group* g = c.group;
   Group::Member& me = g->m[c.rank];
   const size_t bytes = n * dtype_size(dtype);
@@ -140,27 +140,27 @@ void group_allreduce(Ctx& c, void* buf, size_t n, int dtype) {
     me.scratch_bytes = bytes;
   }
   me.buf = buf;
-  cuda_check(cudaEventRecord(me.ready, c.stream), "group ready");
+  cuda_check(cudaEventRecord(me.ready, st), "group ready");
   g->barrier();
   Srcs s{};
   for (int q = 0; q < g->world; ++q) {
     s.p[q] = g->m[q].buf;
-    if (q != c.rank) cuda_check(cudaStreamWaitEvent(c.stream, g->m[q].ready, 0), "group wait");
+    if (q != c.rank) cuda_check(cudaStreamWaitEvent(st, g->m[q].ready, 0), "group wait");
   }
   const int threads = 256;
   const int blocks = (int)std::min<size_t>((n + threads - 1) / threads, 4 * 148);
   if (dtype == kDtypeF64)
-    k_group_sum<double><<<blocks, threads, 0, c.stream>>>(s, g->world, n, static_cast<double*>(me.scratch));
+    k_group_sum<double><<<blocks, threads, 0, st>>>(s, g->world, n, static_cast<double*>(me.scratch));
   else if (dtype == kDtypeF32)
-    k_group_sum<float><<<blocks, threads, 0, c.stream>>>(s, g->world, n, static_cast<float*>(me.scratch));
+    k_group_sum<float><<<blocks, threads, 0, st>>>(s, g->world, n, static_cast<float*>(me.scratch));
   else
-    k_group_sum<int32_t><<<blocks, threads, 0, c.stream>>>(s, g->world, n, static_cast<int32_t*>(me.scratch));
+    k_group_sum<int32_t><<<blocks, threads, 0, st>>>(s, g->world, n, static_cast<int32_t*>(me.scratch));
   c.launches++;
-  cuda_check(cudaEventRecord(me.done, c.stream), "group done");
+  cuda_check(cudaEventRecord(me.done, st), "group done");
   g->barrier();
   for (int q = 0; q < g->world; ++q)
-    if (q != c.rank) cuda_check(cudaStreamWaitEvent(c.stream, g->m[q].done, 0), "group wait");
-  cuda_check(cudaMemcpyAsync(buf, me.scratch, bytes, cudaMemcpyDeviceToDevice, c.stream), "group copy");
+    if (q != c.rank) cuda_check(cudaStreamWaitEvent(st, g->m[q].done, 0), "group wait");
+  cuda_check(cudaMemcpyAsync(buf, me.scratch, bytes, cudaMemcpyDeviceToDevice, st), "group copy");
 }
 
 }  // namespace gfnx
