@@ -1837,7 +1837,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   float* red = reinterpret_cast<float*>(whd + H * NH * 2);  // [kThreads * 8 / H][H] bias partials
   float* redh = red + kThreads * 8;                           // [kThreads / NH][NH] head bias partials
   constexpr int HC = H / 2;
-  __shared__ uint64_t mbar, mbar1, mbarw;  // mbar1: the dW1 MMAs; mbarw: the W2 image patch
+  __shared__ uint64_t mbar, mbar1, mbar2, mbarw;  // mbar1 / mbar2: the dW1 MMAs of the htile /
+                                                  // W2-window obs units; mbarw: the W2 patch
   __shared__ uint32_t tbase;
   const EnvParams& P = a.P;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -1853,6 +1854,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     if (tid == 0) {
       mbar_init(&mbar, 1);
       mbar_init(&mbar1, 1);
+      mbar_init(&mbar2, 1);
       mbar_init(&mbarw, 1);
       fence_mbar_init();
     }
@@ -1948,7 +1950,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       }
     };
     bool w1_pending = false, w1_acc = false, w2_patch = false;
-    uint32_t phase1 = 0, phasew = 0;
+    uint32_t phase1 = 0, phase2 = 0, phasew = 0;
     for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
       const int pt = phys_tile<LIST>(a.tile_list, tile);  // emission tile of this training tile
       const int rbt = rbt_cur;
@@ -1960,16 +1962,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       pmark(6);
       // htile is free once the previous tile's second dW1 MMA has read its obs unit (atile:
       // every earlier MMA has completed when this tile's head MMA commits)
-      if (w1_pending) {
-        if (half == 0) mbar_wait(&mbar1, phase1);
-        if (tid == 0) {  // restore the W2 image's first 16 KB (obs unit 1 of the previous tile)
-          mbar_arrive_expect_tx(&mbarw, 16384);
-          bulk_g2s(wdimg, a.W.w2_dgrad, 16384, &mbarw);
-        }
-        w2_patch = true;
-        phase1 ^= 1;
-        w1_pending = false;
-      }
+      const bool prev_w1 = w1_pending;
+      w1_pending = false;
       uint32_t mk2[HC / 32], mk1[HC / 32];
 #pragma unroll
       for (int q = 0; q < HC / 32; ++q) {
@@ -1987,28 +1981,34 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         const float* pr = cx.pr;
         // only the NH head columns are written: the head dgrad MMA reads K = NH, and the
         // wgrad pass C output columns >= NH (from stale smem) are never read back
+        uint32_t pk[NH / 2];
 #pragma unroll
-        for (int c8 = 0; c8 < NH / 8; ++c8) {
-          uint32_t pk[4];
+        for (int i = 0; i < NH / 2; ++i) {
+          float x[2];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float x[2];
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int c = 8 * c8 + 2 * i + e;
-              float v = 0.f;
-              if (valid && c < A && Env::legal(P, s, c)) {
-                v = -pr[c] * gsum;
-                if (c == act) v += g_a;
-                if (c == P.stop) v += g_s;
-              }
-              if (c == A) v = g_f;
-              x[e] = v;
+          for (int e = 0; e < 2; ++e) {
+            const int c = 2 * i + e;
+            float v = 0.f;
+            if (valid && c < A && Env::legal(P, s, c)) {
+              v = -pr[c] * gsum;
+              if (c == act) v += g_a;
+              if (c == P.stop) v += g_s;
             }
-            pk[i] = pack_bf16x2(x[0], x[1]);
+            if (c == A) v = g_f;
+            x[e] = v;
           }
-          *reinterpret_cast<uint4*>(htile + sw128_offset(row, 8 * c8, kTile)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          pk[i] = pack_bf16x2(x[0], x[1]);
         }
+        // htile is free once the previous tile's first dW1 MMA group has read its obs unit
+        if (prev_w1) mbar_wait(&mbar1, phase1);
+#pragma unroll
+        for (int c8 = 0; c8 < NH / 8; ++c8)
+          *reinterpret_cast<uint4*>(htile + sw128_offset(row, 8 * c8, kTile)) =
+              make_uint4(pk[4 * c8], pk[4 * c8 + 1], pk[4 * c8 + 2], pk[4 * c8 + 3]);
+      }
+      if (prev_w1) {
+        phase1 ^= 1;
+        w2_patch = true;
       }
       fence_proxy_async();
       tc_fence_before();
@@ -2020,7 +2020,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         bulk_commit();
         mma_k_sw128_none<H, NH>(tmem, htile, whd);
         umma_commit(&mbar);
+        if (prev_w1) {  // restore the W2 image's first 16 KB once the second dW1 group has read it
+          mbar_wait(&mbar2, phase2);
+          mbar_arrive_expect_tx(&mbarw, 16384);
+          bulk_g2s(wdimg, a.W.w2_dgrad, 16384, &mbarw);
+        }
       }
+      if (prev_w1) phase2 ^= 1;
       mbar_wait(&mbar, phase);
       phase ^= 1;
       tc_fence_after();
@@ -2123,8 +2129,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
                        // W2 image / atile are rewritten
         tc_fence_after();
         mma_obs_dz<H>(tmem + H, htile, atile, 0, w1_acc);
+        umma_commit(&mbar1);  // htile free (the next tile's dlogits wait on it)
         mma_obs_dz<H>(tmem + H, wdimg, atile, 1, true);
-        umma_commit(&mbar1);
+        umma_commit(&mbar2);  // W2 window free (and every earlier MMA complete)
       }
       w1_pending = true;
       w1_acc = true;
@@ -2133,7 +2140,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     }
     if (a.phase && tid == 0)
       for (int k = 0; k < 7; ++k) atomicAdd((unsigned long long*)a.phase + 15 + k, (unsigned long long)pc[k]);
-    if (w1_pending) mbar_wait(&mbar1, phase1);
+    if (w1_pending) mbar_wait(&mbar2, phase2);  // covers both dW1 groups
     tc_fence_after();
     // [dW1 | db1] of this CTA -> its partial slab: TMEM lane = input feature f (<= O), the two
     // halves read their column halves
