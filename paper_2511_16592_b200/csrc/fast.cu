@@ -1848,7 +1848,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
   const int tiles = *a.tilectr;
   const int R = tiles * kTile;
   float* part = a.wpart + (size_t)blockIdx.x * a.pstride;
-  float acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j (db1: k_fast_wgrad pass B)
+  float acc_b2 = 0.f, acc_bh = 0.f;  // thread j owns bias column j (db1: the dW1 GEMM's feature O)
   if ((int)blockIdx.x < tiles) {
     if (warp == 0) tmem_alloc<2 * H>(&tbase);  // [0, H): dgrad accumulators, [H, 2H): dW1 | db1
     if (tid == 0) {
@@ -1945,7 +1945,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         auto put = [&](int f, float y) {
           *reinterpret_cast<__nv_bfloat16*>(x + sw128_offset(rl, f, 64)) = __float2bfloat16(y);
         };
-        Env::features(P, s, [&](int f, double x) { put(f, (float)x); });
+        Env::features(P, s, [&](int f, double val) { put(f, (float)val); });
         put(P.O, 1.f);
       }
     };
@@ -1960,8 +1960,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       rbt_next = slot_of(tile + 2 * gridDim.x);
       load_row(tile + gridDim.x, rbt_cur, nx);  // in flight during this tile
       pmark(6);
-      // htile is free once the previous tile's second dW1 MMA has read its obs unit (atile:
-      // every earlier MMA has completed when this tile's head MMA commits)
+      // the previous tile's dW1 MMA groups may still run: htile is rewritten (dlogits) after the
+      // first group's mbarrier, the W2 window after the second's; atile only after this tile's
+      // head MMA, whose commit covers every earlier MMA
       const bool prev_w1 = w1_pending;
       w1_pending = false;
       uint32_t mk2[HC / 32], mk1[HC / 32];
