@@ -1876,6 +1876,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
     // state, action, loss coefficients and softmax record
     struct RowIn {
       uint32_t mk2[HC / 32], mk1[HC / 32];
+      uint32_t mk1x;  // half 1: h1 mask word of the last chunk of half 0 (its extra dz1 chunk)
       uint32_t sw[kMaxSWFwd];
       int act;
       float ga, gs, gf;
@@ -1902,6 +1903,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         x.mk2[0] = m2.x; x.mk2[1] = m2.y;
         x.mk1[0] = m1.x; x.mk1[1] = m1.y;
       }
+      x.mk1x = (v && half == 1) ? a.mask1[(size_t)r * (H / 32) + HC / 32 - 1] : 0u;
 #pragma unroll
       for (int i = 0; i < kMaxSWFwd; ++i) x.sw[i] = (v0 && i < P.SW) ? a.slot_st[(size_t)r * P.SW + i] : 0u;
       x.act = v0 ? a.slot_act[r] : 0;
@@ -1971,6 +1973,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
         mk2[q] = cx.mk2[q];
         mk1[q] = cx.mk1[q];
       }
+      const uint32_t mk1x = cx.mk1x;
       if (half == 0) {
         // dlogits (masked log-softmax backward, tape.cpp:413-434): g_c - p_c * sum(g)
         typename Env::State s;
@@ -2107,18 +2110,26 @@ __global__ void __launch_bounds__(kThreads, 1) k_fast_bwd(TrainArgs a) {
       if (tid == 0) bulk_wait_read0();
       __syncthreads();
       pmark(3);
-#pragma unroll
-      for (int q = 0; q < HC / 32; ++q) {
-        const int col = c0 + q * 32;
+      // dz1 = dh1 masked by ReLU(h1) -> atile: half 0 takes one 32-column chunk fewer than
+      // half 1 (it also builds the obs rows)
+      auto dz1_chunk = [&](int col, uint32_t mw) {
         uint32_t r32[32];
         tmem_ld32(lane_base + col, r32);
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i)
-          pk[i] = pack_bf16x2(((mk1[q] >> i) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
-                              ((mk1[q] >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
+          pk[i] = pack_bf16x2(((mw >> i) & 1u) ? __uint_as_float(r32[2 * i]) : 0.f,
+                              ((mw >> (16 + i)) & 1u) ? __uint_as_float(r32[2 * i + 1]) : 0.f);
         st_row32(atile, row, col, pk);
+      };
+      if (half == 0) {
+#pragma unroll
+        for (int q = 0; q < HC / 32 - 1; ++q) dz1_chunk(q * 32, mk1[q]);
+      } else {
+        dz1_chunk(HC - 32, mk1x);
+#pragma unroll
+        for (int q = 0; q < HC / 32; ++q) dz1_chunk(HC + q * 32, mk1[q]);
       }
       // obs units: rows 0..63 in htile, rows 64..127 in the W2 image's first 16 KB (its W2
       // MMA has completed)
